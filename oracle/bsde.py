@@ -1,0 +1,271 @@
+"""Per-step-network deep-BSDE iteration in float64 (TEST INFRASTRUCTURE ONLY).
+
+What one training iteration computes (the hot path that BASELINE.json's
+north_star names; formulation = the Han et al. scheme the paper describes at
+P:78, "there are N different neural networks. Y0 and Z0 are treated as
+parameters and all the Y_n are computed using an Euler discretization"):
+
+  ΔW_n ~ N(0, Δt)                                  Eq. 5, P:64   (philox.py, R8)
+  X_{n+1} = X_n + σ ΔW_n,  σ = √2 I, μ = 0         Eq. 5; Eq. 12
+  Z_n = net_n(X_n)  (lift, one residual block, head) Eq. 7; R4
+  Y_{n+1} = Y_n + φ Δt + Z_n·ΔW_n,  φ = -f         Eq. 5; R2
+  L = (1/B) Σ_m (Y_N - g(X_N))²                    Eq. 6, P:75 (terminal term); R5
+  gradient by the hand-derived adjoint (no autograd)   R19/DESIGN.md §Adjoint
+  Adam                                             P:319; R6
+  multilevel prolongation N -> 2N                  §3.2; R14
+
+Flat parameter layout (R-layout, same as the C-ABI, include/bsde.h):
+  [Y0 | step 0: W1 (w×d) b1 (w) W2 (w×w) b2 (w) W3 (d×w) b3 (d) | step 1 ...]
+all row-major.
+"""
+import numpy as np
+
+from . import philox
+
+HEAT, HJB, ALLEN_CAHN = 0, 1, 2
+PROBLEM_NAMES = {"heat": HEAT, "hjb": HJB, "allen_cahn": ALLEN_CAHN}
+SIGMA = np.sqrt(2.0)          # dX = √2 dW in every config (BASELINE.json configs 1-5)
+
+
+# ----------------------------------------------------------------------------
+# Problem data (R2, R10-R13).  Driver in the Han convention:
+#   Y_{n+1} = Y_n - f(Y_n, Z_n) Δt + Z_n·ΔW_n
+# ----------------------------------------------------------------------------
+def driver_f(problem, y, z, lam=1.0):
+    """f(y, z): heat 0 (R13); HJB -λ|z|²/2 (P:302 read as ‖Du‖², R10);
+    Allen-Cahn y - y³ (R12)."""
+    if problem == HEAT:
+        return np.zeros_like(y)
+    if problem == HJB:
+        return -0.5 * lam * np.sum(z * z, axis=-1)
+    if problem == ALLEN_CAHN:
+        return y - y ** 3
+    raise ValueError(problem)
+
+
+def driver_df_dy(problem, y, z, lam=1.0):
+    if problem == ALLEN_CAHN:
+        return 1.0 - 3.0 * y * y
+    return np.zeros_like(y)
+
+
+def driver_df_dz(problem, y, z, lam=1.0):
+    if problem == HJB:
+        return -lam * z
+    return np.zeros_like(z)
+
+
+def terminal_g(problem, x):
+    """g: heat |x|² (R13); HJB ln(0.5(1+|x|²)); Allen-Cahn 1/(2+0.4|x|²) (R12)."""
+    s = np.sum(x * x, axis=-1)
+    if problem == HEAT:
+        return s
+    if problem == HJB:
+        return np.log(0.5 * (1.0 + s))
+    if problem == ALLEN_CAHN:
+        return 1.0 / (2.0 + 0.4 * s)
+    raise ValueError(problem)
+
+
+# ----------------------------------------------------------------------------
+# Parameters
+# ----------------------------------------------------------------------------
+def step_size(d, w):
+    """P_step = 2dw + w² + 2w + d."""
+    return 2 * d * w + w * w + 2 * w + d
+
+
+def num_params(d, w, N):
+    return 1 + N * step_size(d, w)
+
+
+def unpack(params, d, w, N):
+    """Views (Y0, [dict(W1,b1,W2,b2,W3,b3) for n < N]) into the flat vector."""
+    params = np.asarray(params)
+    assert params.shape == (num_params(d, w, N),), (params.shape, num_params(d, w, N))
+    nets = []
+    off = 1
+    for _ in range(N):
+        net = {}
+        for name, shape in (("W1", (w, d)), ("b1", (w,)), ("W2", (w, w)),
+                            ("b2", (w,)), ("W3", (d, w)), ("b3", (d,))):
+            size = int(np.prod(shape))
+            net[name] = params[off:off + size].reshape(shape)
+            off += size
+        nets.append(net)
+    return params[0:1], nets
+
+
+def init_params(seed, d, w, N):
+    """R7: Xavier-uniform W ~ U(-a, a), a = sqrt(6/(fan_in+fan_out)); biases 0;
+    Y0 ~ U(0, 1).  Uniforms from the Philox init stream, tensor_id = 1 + 3n + k
+    (k = 0, 1, 2 for W1, W2, W3) and 0 for Y0."""
+    p = np.zeros(num_params(d, w, N))
+    y0, nets = unpack(p, d, w, N)
+    y0[0] = philox.init_uniforms(seed, 0, 1)[0]
+    for n, net in enumerate(nets):
+        for k, name in enumerate(("W1", "W2", "W3")):
+            fan_out, fan_in = net[name].shape
+            a = np.sqrt(6.0 / (fan_in + fan_out))
+            u = philox.init_uniforms(seed, 1 + 3 * n + k, net[name].size)
+            net[name][...] = (a * (2.0 * u - 1.0)).reshape(net[name].shape)
+    return p
+
+
+def round_bf16(x):
+    """Round-to-nearest-even to bfloat16, returned as float64 (R17 diagnosis mode)."""
+    f = np.asarray(x, dtype=np.float32)
+    b = f.view(np.uint32).astype(np.uint64)
+    b = (b + np.uint64(0x7FFF) + ((b >> np.uint64(16)) & np.uint64(1))) & np.uint64(0xFFFF0000)
+    return b.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+# ----------------------------------------------------------------------------
+# One iteration: rollout + terminal loss + hand adjoint
+# ----------------------------------------------------------------------------
+def net_forward(net, x, bf16=False):
+    """Per-step Z-net (R4; Eq. 7 with h = 1):
+    A1 = W1 x + b1, H1 = ReLU(A1), A2 = W2 H1 + b2, H2 = H1 + ReLU(A2), Z = W3 H2 + b3."""
+    op = round_bf16 if bf16 else (lambda a: a)
+    A1 = op(x) @ op(net["W1"]).T + net["b1"]
+    H1 = np.maximum(A1, 0.0)
+    A2 = op(H1) @ op(net["W2"]).T + net["b2"]
+    H2 = H1 + np.maximum(A2, 0.0)
+    Z = op(H2) @ op(net["W3"]).T + net["b3"]
+    return A1, H1, A2, H2, Z
+
+
+def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
+              x0=0.0, lam=1.0, want_grad=True, bf16=False, keep=False):
+    """One training iteration on the shard ``paths`` (global path indices).
+
+    Returns dict(loss_sum=Σ_m R², loss=Σ R²/B_global, grad=∂L/∂params of this
+    shard's contribution (sums over shards to the full gradient, R5, §8(e)),
+    R, Y_N, X_N, and per-step traces if keep).
+    """
+    paths = np.asarray(paths, dtype=np.int64)
+    B = float(batch_global)
+    dt = T / N
+    y0, nets = unpack(params, d, w, N)
+    M = paths.shape[0]
+    X = np.full((M, d), float(x0))
+    Y = np.full(M, y0[0])
+    trace = []
+    for n in range(N):
+        dW = philox.brownian_increments(seed, it, n, paths, d, dt)
+        A1, H1, A2, H2, Z = net_forward(nets[n], X, bf16)                # P:78, Eq. 7
+        trace.append((X, dW, A1, H1, A2, H2, Z, Y))
+        Y = Y - driver_f(problem, Y, Z, lam) * dt + np.sum(Z * dW, axis=-1)   # P:66 (φ=-f)
+        X = X + SIGMA * dW
+    R = Y - terminal_g(problem, X)
+    out = dict(loss_sum=float(np.sum(R * R)), loss=float(np.sum(R * R) / B),
+               R=R, Y_N=Y, X_N=X)
+    if keep:
+        out["trace"] = trace
+    if not want_grad:
+        return out
+    # Adjoint: ā_N = ∂L/∂Y_N = 2R/B.
+    grad = np.zeros_like(np.asarray(params, dtype=np.float64))
+    gy0, gnets = unpack(grad, d, w, N)
+    abar = 2.0 * R / B
+    op = round_bf16 if bf16 else (lambda a: a)
+    for n in range(N - 1, -1, -1):
+        X, dW, A1, H1, A2, H2, Z, Yn = trace[n]
+        net, g = nets[n], gnets[n]
+        # ∂Y_{n+1}/∂Z_n = ΔW_n - Δt ∂_z f ;  ∂Y_{n+1}/∂Y_n = 1 - Δt ∂_y f
+        dZ = abar[:, None] * (dW - dt * driver_df_dz(problem, Yn, Z, lam))
+        g["W3"][...] = op(dZ).T @ op(H2)
+        g["b3"][...] = dZ.sum(0)
+        dH2 = op(dZ) @ op(net["W3"])
+        dA2 = dH2 * (A2 > 0.0)                       # ReLU'(0) = 0 (R15)
+        g["W2"][...] = op(dA2).T @ op(H1)
+        g["b2"][...] = dA2.sum(0)
+        dH1 = dH2 + op(dA2) @ op(net["W2"])
+        dA1 = dH1 * (A1 > 0.0)
+        g["W1"][...] = op(dA1).T @ op(X)
+        g["b1"][...] = dA1.sum(0)
+        abar = abar * (1.0 - dt * driver_df_dy(problem, Yn, Z, lam))
+    gy0[0] = abar.sum()
+    out["grad"] = grad
+    return out
+
+
+def loss_and_grad(problem, d, w, N, T, params, seed, it, batch, **kw):
+    """Full-batch iteration over global paths 0..batch-1."""
+    return iteration(problem, d, w, N, T, params, seed, it, np.arange(batch), batch, **kw)
+
+
+# ----------------------------------------------------------------------------
+# Adam ("Adam optimizer"; hyper-parameters R6) with the divergence guard
+# (SPEC S:425 reading: loss > 1e12 or non-finite -> skip the update).
+# ----------------------------------------------------------------------------
+class AdamState:
+    def __init__(self, n):
+        self.m = np.zeros(n)
+        self.v = np.zeros(n)
+        self.t = 0
+
+
+def adam_step(params, grad, state, lr, beta1=0.9, beta2=0.999, eps=1e-8, loss=0.0):
+    """θ ← θ - lr m̂/(√v̂ + ε), m̂ = m/(1-β1^t), v̂ = v/(1-β2^t), t counted from 1.
+    Returns False (and leaves everything untouched) on divergence."""
+    if not (np.isfinite(loss) and loss <= 1e12 and np.all(np.isfinite(grad))):
+        return False
+    state.t += 1
+    state.m = beta1 * state.m + (1.0 - beta1) * grad
+    state.v = beta2 * state.v + (1.0 - beta2) * grad * grad
+    mhat = state.m / (1.0 - beta1 ** state.t)
+    vhat = state.v / (1.0 - beta2 ** state.t)
+    params -= lr * mhat / (np.sqrt(vhat) + eps)
+    return True
+
+
+# ----------------------------------------------------------------------------
+# Multilevel prolongation (§3.2: h_l = h0 M^-l with M = 2; R14)
+# ----------------------------------------------------------------------------
+COPY, INTERP = 0, 1
+
+
+def prolongate(params, d, w, N, mode=COPY):
+    """θ^{2N}_k = θ^N_{k//2} (copy), or θ_{2n} = θ_n, θ_{2n+1} = (θ_n+θ_{n+1})/2
+    for n < N-1 and θ_{2N-1} = θ_{N-1} (interp).  Y0 is carried (R14)."""
+    P = step_size(d, w)
+    src = np.asarray(params)[1:].reshape(N, P)
+    dst = np.empty((2 * N, P))
+    if mode == COPY:
+        dst[0::2] = src
+        dst[1::2] = src
+    else:
+        dst[0::2] = src
+        dst[1:-1:2] = 0.5 * (src[:-1] + src[1:])
+        dst[-1] = src[-1]
+    return np.concatenate([np.asarray(params)[:1], dst.reshape(-1)])
+
+
+# ----------------------------------------------------------------------------
+# Training loops (host schedule; §3.2 multilevel; R9 fresh paths every iteration)
+# ----------------------------------------------------------------------------
+def train(problem, d, w, N, T, params, seed, batch, iters, lr, it0=0, state=None, lam=1.0):
+    state = state or AdamState(params.size)
+    losses = []
+    for k in range(iters):
+        r = loss_and_grad(problem, d, w, N, T, params, seed, it0 + k, batch, lam=lam)
+        adam_step(params, r["grad"], state, lr, loss=r["loss"])
+        losses.append(r["loss"])
+    return params, state, losses
+
+
+def train_multilevel(problem, d, w, levels, T, params, seed, batch, iters_per_level, lr,
+                     mode=COPY, lam=1.0):
+    """Levels N_0 < N_1 = 2N_0 < ...; Adam state reset at each change (R14);
+    the Philox iteration counter continues across levels (R9)."""
+    it = 0
+    history = []
+    for li, N in enumerate(levels):
+        if li:
+            params = prolongate(params, d, w, levels[li - 1], mode)
+        params, _, losses = train(problem, d, w, N, T, params, seed, batch,
+                                  iters_per_level[li], lr, it0=it, lam=lam)
+        history += [(li, N, l) for l in losses]
+        it += iters_per_level[li]
+    return params, history

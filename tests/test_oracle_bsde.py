@@ -1,0 +1,268 @@
+"""Pins of the oracle's rollout, loss, adjoint, Adam and prolongation.
+
+Each test pins a part of oracle/bsde.py to something other than itself
+(DESIGN.md §Pins): algebraic identities of the method, exact martingale
+identities, closed forms, brute-force finite differences, and invariants.
+"""
+import numpy as np
+import pytest
+from scipy import integrate
+
+from oracle import bsde, closed_forms as cf, philox
+
+
+# ---------------------------------------------------------------- H1: heat optimum
+@pytest.mark.parametrize("N", [5, 10])
+def test_heat_optimum_pathwise_identity(N):
+    """Pin H1: at the hand-built optimum, R = 2dT - 2 Σ_n |ΔW_n|² path-wise.
+    Exercises Euler X, the Z-net (Eq. 7), the Y update and g."""
+    d, T, B = 10, 1.0, 512
+    p, w = cf.heat_optimum_params(d, T, N)
+    r = bsde.iteration(bsde.HEAT, d, w, N, T, p, 0, 3, np.arange(B), B, want_grad=False)
+    S = sum(np.sum(philox.brownian_increments(0, 3, n, np.arange(B), d, T / N) ** 2, axis=1)
+            for n in range(N))
+    assert np.max(np.abs(r["R"] - (2 * d * T - 2 * S))) < 1e-11
+
+
+def test_heat_optimum_loss_floor():
+    """E[L*] = 8dT²/N = 16 for config 1 (golden heat_floor_d10_T1_N5); sd of the
+    batch mean is sqrt(573.44/B)."""
+    d, T, N, B = 10, 1.0, 5, 16384
+    p, w = cf.heat_optimum_params(d, T, N)
+    r = bsde.iteration(bsde.HEAT, d, w, N, T, p, 0, 0, np.arange(B), B, want_grad=False)
+    assert abs(r["loss"] - 16.0) < 4.0 * np.sqrt(573.44 / B)
+    assert cf.heat_optimum_expected_loss(d, T, N) == 16.0
+
+
+def test_heat_optimum_is_stationary():
+    """Pin H2: E[∇L] = 0 at the exact optimum.  Two independent batches: for a
+    mean-zero estimator |g1+g2|² ≈ |g1-g2|²; a biased adjoint breaks the ratio."""
+    d, T, N, B = 4, 1.0, 3, 4096
+    p, w = cf.heat_optimum_params(d, T, N)
+    p = p + 0.0
+    g1 = bsde.iteration(bsde.HEAT, d, w, N, T, p, 0, 0, np.arange(B), B)["grad"]
+    g2 = bsde.iteration(bsde.HEAT, d, w, N, T, p, 0, 1, np.arange(B), B)["grad"]
+    ratio = np.sum((g1 + g2) ** 2) / np.sum((g1 - g2) ** 2)
+    assert 0.6 < ratio < 1.6, ratio
+    # ... while a perturbed (non-optimal) point has a gradient far above noise
+    q = p.copy()
+    q[0] += 1.0
+    h1 = bsde.iteration(bsde.HEAT, d, w, N, T, q, 0, 0, np.arange(B), B)["grad"]
+    h2 = bsde.iteration(bsde.HEAT, d, w, N, T, q, 0, 1, np.arange(B), B)["grad"]
+    assert np.sum((h1 + h2) ** 2) / np.sum((h1 - h2) ** 2) > 3.0
+    assert abs(h1[0] - 2.0) < 0.2          # ∂L/∂Y0 = 2 E[R] = 2·1
+
+
+# ---------------------------------------------------------------- HJB driver
+def test_hjb_exponential_martingale():
+    """With f = -|z|²/2 (λ = 1) and any adapted Z, exp(-(Y_N - Y0)) =
+    Π_n exp(-Z_n·ΔW_n - |Z_n|²Δt/2) is a discrete exponential martingale, so
+    E[exp(-(Y_N - Y0))] = 1 exactly (Gaussian ΔW).  A wrong sign or factor in
+    f (R2, R10) moves the mean by a factor e^{±Σ|Z|²Δt/2}."""
+    d, w, N, T, B = 4, 8, 4, 1.0, 200000
+    p = bsde.init_params(11, d, w, N)
+    _, nets = bsde.unpack(p, d, w, N)
+    for net in nets:
+        net["b3"][...] = 0.25
+        net["W3"][...] *= 0.3
+    r = bsde.iteration(bsde.HJB, d, w, N, T, p, 5, 0, np.arange(B), B, want_grad=False,
+                       keep=True)
+    qv = sum(np.sum(t[6] ** 2, axis=1) for t in r["trace"]) * (T / N)
+    assert 0.3 < qv.mean() < 2.0                      # the test has power
+    e = np.exp(-(r["Y_N"] - p[0]))
+    assert abs(e.mean() - 1.0) < 5.0 * e.std() / np.sqrt(B)
+    # the flipped driver would give a mean far from 1
+    e_flip = np.exp(-(r["Y_N"] - p[0]) + qv)
+    assert abs(e_flip.mean() - 1.0) > 20.0 * e_flip.std() / np.sqrt(B)
+
+
+def test_hjb_zero_z_keeps_y0():
+    """Pin H11: Z ≡ 0 ⇒ f(y, 0) = 0 ⇒ Y_N = Y0 and R = Y0 - g(√2 Σ ΔW)."""
+    d, w, N, T, B = 6, 7, 5, 1.0, 300
+    p = bsde.init_params(2, d, w, N)
+    _, nets = bsde.unpack(p, d, w, N)
+    for net in nets:
+        net["W3"][...] = 0.0
+    r = bsde.iteration(bsde.HJB, d, w, N, T, p, 0, 9, np.arange(B), B, want_grad=False)
+    XN = np.sqrt(2.0) * sum(philox.brownian_increments(0, 9, n, np.arange(B), d, T / N)
+                            for n in range(N))
+    g = np.log(0.5 * (1.0 + np.sum(XN * XN, 1)))
+    assert np.allclose(r["Y_N"], p[0], rtol=0, atol=1e-14)
+    assert np.allclose(r["R"], p[0] - g, rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------- Allen-Cahn driver
+def test_allen_cahn_zero_z_converges_to_ode():
+    """With Z ≡ 0 the Y recursion is forward Euler for y' = -(y - y³)
+    (f = y - y³, R12).  Its limit is the exact ODE solution
+    (closed form, cross-checked with scipy's solve_ivp); the error is O(1/N)."""
+    d, w, T, y0 = 3, 4, 0.3, 0.5
+    exact = cf.allen_cahn_zero_z_ode(y0, T)
+    sol = integrate.solve_ivp(lambda t, y: -(y - y ** 3), (0, T), [y0], rtol=1e-12, atol=1e-14)
+    assert abs(sol.y[0, -1] - exact) < 1e-10
+    ys = []
+    for N in (20, 40, 80, 160):
+        p = bsde.init_params(0, d, w, N)
+        p[0] = y0
+        _, nets = bsde.unpack(p, d, w, N)
+        for net in nets:
+            net["W3"][...] = 0.0
+        r = bsde.iteration(bsde.ALLEN_CAHN, d, w, N, T, p, 0, 0, np.arange(8), 8,
+                           want_grad=False)
+        assert np.ptp(r["Y_N"]) == 0.0
+        ys.append(r["Y_N"][0])
+    errs = [y - exact for y in ys]
+    for a, b in zip(errs, errs[1:]):
+        assert 1.8 < a / b < 2.2                       # first order
+    assert abs(2 * ys[-1] - ys[-2] - exact) < 2e-6     # Richardson
+    # survey's stated value for N = 20 (Appendix A)
+    assert abs(ys[0] - 0.392951276) < 1e-9
+
+
+# ---------------------------------------------------------------- H6: FD gradients
+@pytest.mark.parametrize("problem", [bsde.HEAT, bsde.HJB, bsde.ALLEN_CAHN])
+@pytest.mark.parametrize("d,w,N,B", [(2, 4, 2, 4), (3, 8, 3, 8)])
+def test_gradient_matches_central_differences(problem, d, w, N, B):
+    T, seed, it, x0 = 0.5, 3, 1, 0.3
+    p = bsde.init_params(seed, d, w, N)
+    rng = np.random.default_rng(7 + d)
+    p[1:] += 0.1 * rng.standard_normal(p.size - 1)     # non-zero biases
+    p[0] = 0.4
+    r = bsde.iteration(problem, d, w, N, T, p, seed, it, np.arange(B), B, x0=x0, keep=True)
+    # no ReLU kink within reach of the FD step
+    amin = min(min(np.abs(t[2]).min(), np.abs(t[4]).min()) for t in r["trace"])
+    assert amin > 1e-4
+    h = 1e-6
+    fd = np.empty_like(p)
+    for i in range(p.size):
+        e = np.zeros_like(p)
+        e[i] = h
+        lp = bsde.iteration(problem, d, w, N, T, p + e, seed, it, np.arange(B), B, x0=x0,
+                            want_grad=False)["loss"]
+        lm = bsde.iteration(problem, d, w, N, T, p - e, seed, it, np.arange(B), B, x0=x0,
+                            want_grad=False)["loss"]
+        fd[i] = (lp - lm) / (2 * h)
+    g = r["grad"]
+    scale = np.abs(g).max()
+    assert np.max(np.abs(g - fd)) < 1e-6 * scale + 1e-9, np.max(np.abs(g - fd)) / scale
+
+
+def test_net0_is_a_trainable_z0():
+    """Pin H7 / R3: with X0 = 0 and zero biases, net_0 sees A1 = A2 = 0, so only
+    its b3 (= Z0, P:78 'Z0 treated as parameter') receives gradient."""
+    d, w, N, T, B = 5, 6, 3, 1.0, 64
+    p = bsde.init_params(0, d, w, N)
+    state = bsde.AdamState(p.size)
+    P = bsde.step_size(d, w)
+    p_start = p.copy()
+    for it in range(3):
+        r = bsde.iteration(bsde.HJB, d, w, N, T, p, 0, it, np.arange(B), B)
+        g = r["grad"][1:1 + P]
+        assert np.all(g[:P - d] == 0.0)
+        assert np.any(g[P - d:] != 0.0)
+        bsde.adam_step(p, r["grad"], state, 1e-2, loss=r["loss"])
+    assert np.array_equal(p[1:1 + P - d], p_start[1:1 + P - d])
+
+
+def test_shard_sum_equals_full_batch():
+    """§8(e): any partition of the global paths gives the same loss and gradient
+    up to summation order."""
+    d, w, N, T, B = 4, 6, 3, 0.3, 48
+    p = bsde.init_params(1, d, w, N)
+    full = bsde.iteration(bsde.ALLEN_CAHN, d, w, N, T, p, 0, 2, np.arange(B), B)
+    parts = [bsde.iteration(bsde.ALLEN_CAHN, d, w, N, T, p, 0, 2, idx, B)
+             for idx in np.array_split(np.arange(B), 3)]
+    assert np.isclose(sum(q["loss"] for q in parts), full["loss"], rtol=1e-13)
+    assert np.allclose(sum(q["grad"] for q in parts), full["grad"], rtol=1e-12, atol=1e-15)
+    # permutation invariance of the loss
+    perm = bsde.iteration(bsde.ALLEN_CAHN, d, w, N, T, p, 0, 2, np.arange(B)[::-1], B)
+    assert np.isclose(perm["loss"], full["loss"], rtol=1e-13)
+
+
+# ---------------------------------------------------------------- Adam (H8)
+def test_adam_constant_gradient_moves_lr_per_step():
+    """With a constant gradient g, m̂ = g and v̂ = g² exactly at every t, so every
+    step moves θ by exactly lr·g/(|g|+ε); step 1 ≈ -lr·sign(g)."""
+    rng = np.random.default_rng(0)
+    g = rng.standard_normal(50)
+    g[0] = 0.0
+    th = rng.standard_normal(50)
+    st = bsde.AdamState(50)
+    lr = 1e-2
+    for k in range(1, 6):
+        before = th.copy()
+        assert bsde.adam_step(th, g, st, lr)
+        assert np.allclose(before - th, lr * g / (np.abs(g) + 1e-8), rtol=1e-9, atol=1e-15)
+        assert st.t == k
+    assert th[0] == before[0]                          # zero gradient: unchanged
+
+
+def test_adam_divergence_guard_skips_update():
+    th = np.ones(4)
+    st = bsde.AdamState(4)
+    assert not bsde.adam_step(th, np.array([1, np.nan, 0, 0.]), st, 0.1)
+    assert not bsde.adam_step(th, np.ones(4), st, 0.1, loss=2e12)
+    assert np.all(th == 1.0) and st.t == 0 and np.all(st.m == 0)
+
+
+# ---------------------------------------------------------------- prolongation (H9)
+def test_prolongate_copy_and_interp():
+    d, w, N = 3, 4, 4
+    p = bsde.init_params(0, d, w, N)
+    P = bsde.step_size(d, w)
+    c = bsde.prolongate(p, d, w, N, bsde.COPY)
+    assert c.size == bsde.num_params(d, w, 2 * N) and c[0] == p[0]
+    src = p[1:].reshape(N, P)
+    fine = c[1:].reshape(2 * N, P)
+    for k in range(2 * N):
+        assert np.array_equal(fine[k], src[k // 2])
+    i = bsde.prolongate(p, d, w, N, bsde.INTERP)[1:].reshape(2 * N, P)
+    for n in range(N):
+        assert np.array_equal(i[2 * n], src[n])
+    for n in range(N - 1):
+        assert np.allclose(i[2 * n + 1], 0.5 * (src[n] + src[n + 1]))
+    assert np.array_equal(i[-1], src[-1])
+
+
+def test_prolongated_heat_optimum_stays_optimal():
+    """The heat optimum is time-independent, so its prolongation is the optimum
+    on the 2N grid: the path-wise identity holds there too (floor 8dT²/(2N))."""
+    d, T, N, B = 10, 1.0, 5, 256
+    p, w = cf.heat_optimum_params(d, T, N)
+    q = bsde.prolongate(p, d, w, N, bsde.COPY)
+    r = bsde.iteration(bsde.HEAT, d, w, 2 * N, T, q, 0, 0, np.arange(B), B, want_grad=False)
+    S = sum(np.sum(philox.brownian_increments(0, 0, n, np.arange(B), d, T / (2 * N)) ** 2, 1)
+            for n in range(2 * N))
+    assert np.max(np.abs(r["R"] - (2 * d * T - 2 * S))) < 1e-11
+
+
+def test_single_level_schedule_equals_single_level_training():
+    """a one-level schedule is single-level training."""
+    d, w, N, T, B = 3, 4, 2, 1.0, 16
+    p0 = bsde.init_params(0, d, w, N)
+    a, _, la = bsde.train(bsde.HJB, d, w, N, T, p0.copy(), 0, B, 4, 1e-2)
+    b, hist = bsde.train_multilevel(bsde.HJB, d, w, [N], T, p0.copy(), 0, B, [4], 1e-2)
+    assert np.array_equal(a, b) and [h[2] for h in hist] == la
+
+
+# ---------------------------------------------------------------- init (R7) and bf16 (R17)
+def test_init_ranges():
+    d, w, N = 100, 110, 2
+    p = bsde.init_params(0, d, w, N)
+    y0, nets = bsde.unpack(p, d, w, N)
+    assert 0 < y0[0] < 1
+    for net in nets:
+        for name, (fo, fi) in (("W1", (w, d)), ("W2", (w, w)), ("W3", (d, w))):
+            a = np.sqrt(6.0 / (fi + fo))
+            assert np.abs(net[name]).max() <= a
+            assert abs(net[name].std() - a / np.sqrt(3)) < 0.05 * a
+        for b in ("b1", "b2", "b3"):
+            assert np.all(net[b] == 0)
+    assert not np.array_equal(nets[0]["W1"], nets[1]["W1"])
+
+
+def test_round_bf16_matches_torch():
+    torch = pytest.importorskip("torch")
+    x = np.random.default_rng(0).standard_normal(10000) * 10.0 ** np.random.default_rng(1).integers(-5, 5, 10000)
+    ref = torch.tensor(x, dtype=torch.float32).to(torch.bfloat16).to(torch.float64).numpy()
+    assert np.array_equal(bsde.round_bf16(x), ref)

@@ -1,0 +1,68 @@
+"""Pins of oracle/closed_forms.py against golden values and independent MC."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import bsde, closed_forms as cf
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def golden():
+    out = {}
+    with open(os.path.join(HERE, "golden", "closed_forms.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            name, val, tol = line.split()[:3]
+            out[name] = (float(val), float(tol))
+    return out
+
+
+def test_cole_hopf_quadrature_matches_golden():
+    g = golden()
+    for name, d in (("hjb_u0_d100_T1", 100), ("hjb_u0_d10_T1", 10)):
+        val, tol = g[name]
+        assert abs(cf.hjb_u0_quadrature(d, 1.0) - val) < tol
+
+
+def test_cole_hopf_quadrature_matches_monte_carlo():
+    """P:306 Cole-Hopf expectation by plain MC with an independent generator."""
+    rng = np.random.default_rng(2024)
+    u_mc, se = cf.hjb_u0_mc(100, 1.0, 400000, rng)
+    assert abs(u_mc - cf.hjb_u0_quadrature(100, 1.0)) < 4 * se
+
+
+def test_zero_z_optima_match_golden():
+    g = golden()
+    eg = cf.expected_g_chi2(lambda s: np.log(0.5 * (1 + s)), 100, 1.0)
+    assert abs(eg - g["hjb_Eg_d100_T1"][0]) < g["hjb_Eg_d100_T1"][1]
+    ea = cf.expected_g_chi2(lambda s: 1.0 / (2 + 0.4 * s), 100, 0.3)
+    assert abs(ea - g["ac_Eg_d100_T03"][0]) < g["ac_Eg_d100_T03"][1]
+    assert abs(cf.allen_cahn_linearised_u0(100, 0.3) - g["ac_linearised_u0_d100_T03"][0]) \
+        < g["ac_linearised_u0_d100_T03"][1]
+    assert cf.heat_optimum_expected_loss(10, 1.0, 5) == g["heat_floor_d10_T1_N5"][0]
+
+
+def test_expected_g_matches_oracle_terminal_sample():
+    """E[g(X_T)] by quadrature vs the oracle's own X_N and g on 20000 paths
+    (X_N = √2 Σ ΔW, independent of θ)."""
+    d, w, N, T, B = 100, 4, 4, 1.0, 20000
+    p = bsde.init_params(0, d, w, N)
+    r = bsde.iteration(bsde.HJB, d, w, N, T, p, 0, 0, np.arange(B), B, want_grad=False)
+    g = bsde.terminal_g(bsde.HJB, r["X_N"])
+    eg = cf.expected_g_chi2(lambda s: np.log(0.5 * (1 + s)), d, T)
+    assert abs(g.mean() - eg) < 4 * g.std() / np.sqrt(B)
+
+
+@pytest.mark.slow
+def test_heat_training_reaches_closed_form():
+    """Pin H3: trained Y0 → u(0,0) = 2dT = 20 for the config-1 problem.
+    Y0 moves ≈ lr per Adam step, so a longer run than config 1's 200 iterations
+    is needed: 4000 iterations, lr 1e-2, B = 256."""
+    d, w, N, T, B = 10, 20, 5, 1.0, 256
+    p = bsde.init_params(0, d, w, N)
+    p, _, losses = bsde.train(bsde.HEAT, d, w, N, T, p, 0, B, 4000, 1e-2)
+    assert abs(p[0] - cf.heat_u0(d, T)) < 0.5, p[0]
+    assert np.mean(losses[-100:]) < 40.0
