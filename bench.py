@@ -1,0 +1,309 @@
+"""Benchmark of the deep-BSDE training step (BASELINE.json metric: path-steps/s
+and % of roofline).  Prints ONE JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl reference]
+
+N = 1 runs in-process; N > 1 is launched by torchrun (one rank per GPU over
+NCCL).  The default workload is config 5 (Allen-Cahn, d = 100, N = 80,
+524288 paths, bf16 operands), the configuration the metric is quoted on at
+1/2/4/8 GPUs (global batch fixed: strong scaling).  A "step" is one full
+training iteration: Philox ΔW, forward rollout, terminal loss, adjoint,
+gradient allreduce, Adam.
+
+--impl reference runs the float64 CPU oracle (the reference arm of this tier)
+on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import CONFIGS  # noqa: E402
+
+METRIC = "BSDE train path-steps/sec & % roofline at d=100 (1/2/4/8 B200); multilevel time-to-loss"
+UNIT = "path-steps/s"
+# algorithmic flop per path-step: forward 2(dw + w² + wd),
+# adjoint without dX 6dw + 4w² (replay and padding are implementation work)
+def fwd_flops(d, w):
+    return 2 * (d * w + w * w + w * d)
+
+
+def bwd_flops(d, w):
+    return 6 * d * w + 4 * w * w
+
+
+def peaks():
+    p = {"hbm_gbs": 6558.4, "bf16_tflops": 1675.8, "bf16_tflops_sustained": 1400.3,
+         "sm_max_mhz": 1965.0, "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: m[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained",
+                                     "sm_max_mhz") if k in m})
+        p["source"] = "measured"
+    except Exception:
+        pass
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [x.strip() for x in l.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                model = l.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return model
+
+
+def oracle_rate(wl, paths, iters):
+    """The float64 oracle as it stands on a bounded path sample; path-steps/s."""
+    from threadpoolctl import threadpool_info
+    from oracle import bsde as ob
+    prob = {"heat": ob.HEAT, "hjb": ob.HJB, "allen_cahn": ob.ALLEN_CAHN}[wl.problem]
+    p = ob.init_params(wl.seed, wl.d, wl.w, wl.N)
+    st = ob.AdamState(p.size)
+    times = []
+    for k in range(iters):
+        t0 = time.perf_counter()
+        r = ob.iteration(prob, wl.d, wl.w, wl.N, wl.T, p, wl.seed, k, np.arange(paths), wl.batch)
+        ob.adam_step(p, r["grad"], st, wl.lr, loss=r["loss"])
+        times.append(time.perf_counter() - t0)
+    threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    return paths * wl.N / float(np.median(times)), threads, times
+
+
+def run_reference(args, wl, rank):
+    if rank != 0:
+        return
+    paths = args.ref_paths or max(256, min(wl.batch, int(2.4e5 // wl.N)))
+    rate, threads, times = oracle_rate(wl, paths, args.warmup + args.steps)
+    timed = times[args.warmup:] or times
+    sample = "%d of %d paths x N=%d, full network, fp64 numpy; median of %d iterations" % (
+        paths, wl.batch, wl.N, len(timed))
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.median(timed)) * wl.batch / paths,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Philox Brownian increments, R8)",
+            "config": config_dict(wl, args.gpus, "oracle"),
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": sample, "cpu": cpu_info()},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(wl, gpus, family):
+    return {"workload": wl.name, "problem": wl.problem, "d": wl.d, "w": wl.w, "N": wl.N,
+            "T": wl.T, "batch_global": wl.batch, "precision": wl.precision, "kernel": family,
+            "parallelism": "dp%d" % gpus,
+            "l2": "inputs larger than L2: per-step X_n store (N*B*d*4 bytes) >> 126 MB; "
+                  "no explicit flush"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg5_allen_cahn_scaleout", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", default="auto")
+    ap.add_argument("--precision", default=None)
+    ap.add_argument("--ref-paths", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = CONFIGS[args.workload]
+    if args.precision:
+        wl = wl.with_(precision=args.precision)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, wl, rank)
+        return
+
+    import torch
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_1910_11623_b200 import BSDE
+
+    kw = dict(lr=wl.lr, precision=wl.precision, kernel=args.kernel, seed=wl.seed,
+              device=local_rank)
+    if world > 1:
+        s = BSDE.distributed(wl.problem, wl.d, wl.N, wl.T, wl.w, wl.batch, **kw)
+    else:
+        s = BSDE(wl.problem, wl.d, wl.N, wl.T, wl.w, wl.batch, **kw)
+    family = s.family
+    stream = s.stream          # the stream libbsde enqueues on
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        s.train_step(sync=False)
+    barrier()
+    clocks = ClockSampler(local_rank if "CUDA_VISIBLE_DEVICES" not in os.environ else
+                          os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local_rank])
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        s.train_step(sync=False)
+    e1.record(stream)
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    launches = s.launches_per_step()
+    path_steps = wl.batch * wl.N
+    value = path_steps / (ms * 1e-3)
+
+    # per-phase CUDA-event timing of the same step (eager replay of the step)
+    ph = np.zeros(6, np.float32)
+    import ctypes
+    s._ck(s._L.bsde_profile_steps(s._h, max(2, min(args.steps, 5)),
+                                  ph.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), 6))
+    phase = dict(zip(["begin", "fwd", "bwd", "allreduce", "check", "adam"], ph.tolist()))
+
+    # e2e: the public API call per step with the loss read back to the host
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s.train_step(sync=True)
+    barrier()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank == 0:
+        pk = peaks()
+        B_local = wl.batch // world
+        if family == "tc" and wl.precision == "bf16":
+            bound, peak, pk_name = "tensor", pk["bf16_tflops_sustained"], "bf16 sustained (measured)"
+        elif family == "tc":
+            bound, peak = "tensor", pk["bf16_tflops_sustained"] / 3.0
+            pk_name = "bf16 sustained / 3 (bf16x3 fp32-accurate split)"
+        else:
+            bound, peak = "alu", 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+            pk_name = "fp32 FFMA: 148 SM x 128 lanes x 2 flop x sm_max_mhz (derived)"
+        dom = "bwd" if phase["bwd"] >= phase["fwd"] else "fwd"
+        flops = B_local * wl.N * (bwd_flops(wl.d, wl.w) if dom == "bwd" else fwd_flops(wl.d, wl.w))
+        achieved = flops / (phase[dom] * 1e-3) / 1e12
+        step_flops = wl.batch * wl.N * (fwd_flops(wl.d, wl.w) + bwd_flops(wl.d, wl.w)) / world
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16" if (family == "tc" and wl.precision == "bf16") else "f32",
+            "data": "synthetic (Philox4x32-10 Brownian increments generated on device, R8)",
+            "config": config_dict(wl, world, family),
+            "roofline": {"bound": bound, "kernel": "bsde_" + dom, "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": None, "peak_source": pk_name + "; " + pk["source"],
+                         "algorithmic_flop_per_path_step": bwd_flops(wl.d, wl.w) if dom == "bwd"
+                         else fwd_flops(wl.d, wl.w)},
+            "step_roofline": {"achieved_tflops": step_flops / (ms * 1e-3) / 1e12,
+                              "frac": step_flops / (ms * 1e-3) / 1e12 / peak,
+                              "flop_per_path_step": fwd_flops(wl.d, wl.w) + bwd_flops(wl.d, wl.w)},
+            "phase_ms": phase,
+            "gpu_launches": launches * args.steps,
+            "clocks": clk,
+            "e2e": {"value": path_steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 8,
+                    "note": "bsde_train_step(ctx, &loss) per step, loss read back and stream "
+                            "synchronised every step; the step's inputs are Philox counters "
+                            "held on the device (no host input data exists, R8)"},
+        }
+        if not args.no_cpu_baseline and world == 1:
+            paths = max(256, min(wl.batch, int(2.4e5 // wl.N)))
+            rate, threads, _ = oracle_rate(wl, paths, 2)
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+                                    "sample": "%d of %d paths x N=%d, fp64 numpy oracle, median "
+                                              "of 2 iterations" % (paths, wl.batch, wl.N),
+                                    "cpu": cpu_info()}
+        print(json.dumps(line), flush=True)
+    s.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

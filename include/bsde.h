@@ -1,0 +1,199 @@
+/*
+ * bsde.h — C-ABI of the B200-native deep-BSDE training hot path
+ * (arXiv:1910.11623; BASELINE.json north_star).
+ *
+ * One call of bsde_train_step() is one training iteration of the per-step
+ * Z-network scheme the paper describes at PAPER.md:78 (Han et al.: "there are N
+ * different neural networks. Y0 and Z0 are treated as parameters and all the
+ * Y_n are computed using an Euler discretization"), on the Euler-Maruyama
+ * discretisation of Eq. 5:
+ *
+ *   ΔW_n ~ N(0, Δt)                       Eq. 5, PAPER.md:64   (Philox4x32-10, R8)
+ *   X_{n+1} = X_n + √2 ΔW_n                Eq. 5; Eq. 12
+ *   Z_n = W3 H2 + b3, H2 = H1 + ReLU(W2 H1 + b2), H1 = ReLU(W1 X_n + b1)
+ *                                         Eq. 7, PAPER.md:217-219 (residual block, h = 1)
+ *   Y_{n+1} = Y_n - f(Y_n, Z_n) Δt + Z_n·ΔW_n      Eq. 5, PAPER.md:66 with φ = -f (R2)
+ *   L = (1/B) Σ_m (Y_N - g(X_N))²         Eq. 6, PAPER.md:75 (terminal term; R5)
+ *   ∇L by a hand-written adjoint, summed over all ranks (NCCL), then Adam
+ *                                         PAPER.md:319 (Adam), R6
+ * and bsde_prolongate() is one level change of the multilevel schedule
+ * (§3.2: h_l = h_0 M^-l, M = 2).
+ * "R<k>" are the readings listed in DESIGN.md §Readings.
+ *
+ * Conventions for every call:
+ *  - Return value: BSDE_OK (0) or a negative BSDE_E* code; never throws.
+ *    bsde_last_error(ctx) returns a message naming the offending argument.
+ *  - Host pointers are owned by the caller and only read/written during the call.
+ *  - The library owns all device state of a context (parameters, gradients,
+ *    Adam moments, scratch, the NCCL communicator) until bsde_destroy().
+ *  - All device work is enqueued on cfg.stream.  Calls that return a host
+ *    value computed on the device synchronise that stream.
+ *  - A context is bound to one device and one rank and is not thread-safe.
+ */
+#ifndef BSDE_H_
+#define BSDE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Problems (BASELINE.json configs; R10-R13). */
+enum {
+  BSDE_HEAT = 0,       /* f = 0,            g = |x|²            (config 1; R13)      */
+  BSDE_HJB = 1,        /* f = -λ|z|²/2,     g = ln(0.5(1+|x|²))   */
+  BSDE_ALLEN_CAHN = 2  /* f = y - y³,       g = 1/(2+0.4|x|²)   */
+};
+
+/* GEMM operand precision; accumulation is always fp32 (R17, R18). */
+enum {
+  BSDE_FP32 = 0,       /* fp32-accurate: bf16x3 split operands on tcgen05, or SIMT FFMA */
+  BSDE_BF16 = 1        /* bf16 operands, fp32 accumulate                              */
+};
+
+/* Kernel family selection. */
+enum {
+  BSDE_KERNEL_AUTO = 0,  /* tcgen05 when d+1 <= 128 and w+1 <= 128, else SIMT          */
+  BSDE_KERNEL_SIMT = 1,  /* fp32 CUDA-core kernels (ignores precision: always fp32)    */
+  BSDE_KERNEL_TC = 2     /* tcgen05 tensor-core kernels (sm_100a)                       */
+};
+
+enum { BSDE_PROLONG_COPY = 0, BSDE_PROLONG_INTERP = 1 };   /* a9, R14 */
+
+enum {
+  BSDE_OK = 0,
+  BSDE_EINVAL = -1,     /* bad argument; message names it                         */
+  BSDE_ECUDA = -2,      /* CUDA runtime error (message has cudaGetErrorString)     */
+  BSDE_ENCCL = -3,      /* NCCL error                                             */
+  BSDE_EDIVERGED = -4,  /* loss non-finite or > 1e12, or non-finite gradient: the
+                           Adam update of that step was skipped (SPEC S:425 reading) */
+  BSDE_ESTATE = -5,     /* call not valid in the current state                    */
+  BSDE_ENOMEM = -6      /* device allocation failed                               */
+};
+
+typedef struct bsde_ctx bsde_ctx;   /* opaque; one per GPU / rank */
+
+typedef struct {
+  int64_t batch_global;   /* B: paths per iteration summed over ranks; B % world == 0      */
+  double x0;              /* X_0 = x0 * ones(d) (0 in all configs)                          */
+  double lambda;          /* HJB λ (1.0)                                                    */
+  double lr, beta1, beta2, eps;  /* Adam (R6): per-config lr, 0.9, 0.999, 1e-8              */
+  uint64_t seed;          /* Philox key = (seed mod 2^32, seed >> 32) (R8)                  */
+  int precision;          /* BSDE_FP32 | BSDE_BF16                                          */
+  int kernel;             /* BSDE_KERNEL_*                                                  */
+  int prolong_mode;       /* BSDE_PROLONG_COPY | BSDE_PROLONG_INTERP                        */
+  int max_levels;         /* buffers sized for N * 2^max_levels time steps                  */
+  int device;             /* CUDA ordinal                                                   */
+  void* stream;           /* cudaStream_t to enqueue on (NULL = legacy default stream)      */
+  int rank, world;        /* this rank's index and the number of ranks (0, 1 for one GPU)  */
+  const void* nccl_id;    /* 128-byte ncclUniqueId shared by all ranks (bsde_nccl_unique_id
+                             on rank 0, broadcast by the caller); NULL => no collective:
+                             "fake-world" mode, the context computes its shard's local
+                             gradient only (tests)                      */
+  int use_graph;          /* 1: capture the step in a CUDA graph and replay it              */
+  int init_zero_head;     /* 1: W3 = 0 at init, so Z ≡ 0 (R7b; default for Allen-Cahn,
+                             whose cubic driver diverges from a Xavier-initialised Z)      */
+} bsde_config;
+
+/* Fill *cfg with defaults: B = 256, x0 = 0, λ = 1, Adam (1e-2, 0.9, 0.999, 1e-8),
+ * seed 0, FP32, KERNEL_AUTO, COPY, max_levels 0, device 0, default stream,
+ * rank 0 of 1, no NCCL, graphs on, Xavier head (init_zero_head 0). */
+void bsde_config_default(bsde_config* cfg);
+
+/* Create a context for `problem` in dimension d with N time steps on [0, T]
+ * (Δt = T/N, R16) and per-step Z-nets of hidden widths widths[0..n_widths)
+ * (n_widths must be 2 with widths[0] == widths[1] = w: "d→w→w→d ReLU residual",
+ * R4).  Parameters are initialised by R7 (Xavier-uniform weights, zero biases,
+ * Y0 ~ U(0,1), from the Philox init stream keyed by cfg.seed), Adam state is zero
+ * and the iteration counter is 0.  This rank owns global paths
+ * [rank·B/world, (rank+1)·B/world).  Errors: EINVAL (shapes, B % world,
+ * precision/kernel combination), ENOMEM, ECUDA, ENCCL. */
+int bsde_create(int problem, int d, int N, double T, const int* widths, int n_widths,
+                const bsde_config* cfg, bsde_ctx** out);
+
+/* One training iteration: Philox ΔW for global
+ * iteration `it`, forward rollout, terminal loss, adjoint, gradient allreduce
+ * over the ranks, Adam.  Afterwards it += 1.  *loss_out (if non-NULL) receives the
+ * loss of the parameters BEFORE the update (R20), mean over the global batch, and
+ * the call synchronises; with loss_out == NULL the call is fully asynchronous.
+ * Returns EDIVERGED (update skipped) if the loss is non-finite or > 1e12 or a
+ * gradient is non-finite; with loss_out == NULL a divergence is reported by the
+ * next synchronising call. */
+int bsde_train_step(bsde_ctx* ctx, double* loss_out);
+
+/* Multilevel level change (§3.2):
+ * N <- 2N, Δt <- T/(2N); step k of the fine grid takes the coarse net k/2 (COPY)
+ * or the midpoint rule (INTERP); Y0 is kept; Adam m, v, t are reset; the
+ * iteration counter continues.  `level` must equal the current level + 1 and be
+ * <= cfg.max_levels.  Errors: ESTATE. */
+int bsde_prolongate(bsde_ctx* ctx, int level);
+
+/* The trainable Y0 ≈ u(0, X0) (BASELINE.json north_star). Synchronises. */
+int bsde_y0(const bsde_ctx* ctx, double* y0_out);
+
+/* Introspection, checkpoint and resume.  The flat layout is
+ * [Y0 | step 0: W1 (w×d) b1 (w) W2 (w×w) b2 (w) W3 (d×w) b3 (d) | step 1 | ...],
+ * row-major fp32, 1 + N·(2dw + w² + 2w + d) values at the current N. */
+int bsde_num_params(const bsde_ctx* ctx, int64_t* n);
+int bsde_get_params(const bsde_ctx* ctx, float* host, int64_t n);
+int bsde_set_params(bsde_ctx* ctx, const float* host, int64_t n);
+/* Gradient of the last bsde_train_step / bsde_compute_grad (after the
+ * allreduce), same layout. */
+int bsde_get_grads(const bsde_ctx* ctx, float* host, int64_t n);
+int bsde_get_adam_state(const bsde_ctx* ctx, float* m, float* v, int64_t n, int64_t* t);
+int bsde_set_adam_state(bsde_ctx* ctx, const float* m, const float* v, int64_t n, int64_t t);
+int bsde_get_iteration(const bsde_ctx* ctx, int64_t* it);
+int bsde_set_iteration(bsde_ctx* ctx, int64_t it);     /* Philox counter position (R9) */
+int bsde_current_steps(const bsde_ctx* ctx, int* N);
+
+/* Forward + adjoint + allreduce of one iteration WITHOUT the Adam update and
+ * without advancing the iteration counter (teacher-forced parity, R19).
+ * *loss_out as in bsde_train_step.  Synchronises. */
+int bsde_compute_grad(bsde_ctx* ctx, double* loss_out);
+
+/* Forward-only loss on an evaluation stream: Philox counter word 3 is
+ * 0x80000000 | eval_id, global paths [0, batch) of which this rank takes its
+ * share; summed over ranks.  Synchronises. */
+int bsde_eval_loss(bsde_ctx* ctx, uint32_t eval_id, int64_t batch, double* loss_out);
+
+/* Test hooks for bit-parity of the generator (SURVEY.md pin H0): the raw
+ * Philox4x32-10 outputs for `count` counters ctr[4*i..4*i+3] under key
+ * (key[0], key[1]), and the increments ΔW_n for global paths
+ * [m0, m0+count) at iteration it (host out[count×d], fp32).  Both run on the
+ * device with the same code the training kernels use.  Synchronise. */
+int bsde_debug_philox(const bsde_ctx* ctx, const uint32_t* ctr, const uint32_t key[2],
+                      int64_t count, uint32_t* out);
+int bsde_debug_dw(const bsde_ctx* ctx, int64_t it, int n, int64_t m0, int64_t count,
+                  float* host_out);
+/* Terminal residuals R^m = Y_N^m - g(X_N^m) of the last training forward pass
+ * for this rank's local paths [m0, m0+count) (global path rank·B/world + m):
+ * sampled full-size parity (R19).  host_out[count] fp32.  Synchronises. */
+int bsde_debug_residuals(const bsde_ctx* ctx, int64_t m0, int64_t count, float* host_out);
+
+/* Profiling hook for the bench's roofline figures: runs `steps` training
+ * iterations (eagerly, no graph) with CUDA events recorded on cfg.stream
+ * between the phases of the step and returns the mean duration of each phase
+ * in milliseconds: ms_out[0] begin (zero grad), [1] forward kernel, [2] adjoint
+ * kernel, [3] allreduce, [4] check, [5] Adam (+ bf16 weight pack).
+ * n_out must be >= 6.  Synchronises. */
+int bsde_profile_steps(bsde_ctx* ctx, int steps, float* ms_out, int n_out);
+
+/* Number of kernels the last bsde_train_step enqueued (for the bench's
+ * gpu_launches), and the name of the kernel family in use ("simt" | "tc"). */
+int bsde_launches_per_step(const bsde_ctx* ctx, int* n);
+const char* bsde_kernel_family(const bsde_ctx* ctx);
+
+/* NCCL unique id for bsde_config.nccl_id (call on rank 0; 128 bytes). */
+int bsde_nccl_unique_id(void* out128);
+
+/* Message of the last error on ctx (ctx may be NULL: last create error on this thread). */
+const char* bsde_last_error(const bsde_ctx* ctx);
+
+void bsde_destroy(bsde_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSDE_H_ */

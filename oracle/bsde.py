@@ -96,15 +96,16 @@ def unpack(params, d, w, N):
     return params[0:1], nets
 
 
-def init_params(seed, d, w, N):
+def init_params(seed, d, w, N, zero_head=False):
     """R7: Xavier-uniform W ~ U(-a, a), a = sqrt(6/(fan_in+fan_out)); biases 0;
     Y0 ~ U(0, 1).  Uniforms from the Philox init stream, tensor_id = 1 + 3n + k
-    (k = 0, 1, 2 for W1, W2, W3) and 0 for Y0."""
+    (k = 0, 1, 2 for W1, W2, W3) and 0 for Y0.  zero_head (R7b, Allen-Cahn):
+    W3 = 0, so Z ≡ 0 at initialisation."""
     p = np.zeros(num_params(d, w, N))
     y0, nets = unpack(p, d, w, N)
     y0[0] = philox.init_uniforms(seed, 0, 1)[0]
     for n, net in enumerate(nets):
-        for k, name in enumerate(("W1", "W2", "W3")):
+        for k, name in enumerate(("W1", "W2") if zero_head else ("W1", "W2", "W3")):
             fan_out, fan_in = net[name].shape
             a = np.sqrt(6.0 / (fan_in + fan_out))
             u = philox.init_uniforms(seed, 1 + 3 * n + k, net[name].size)
@@ -136,12 +137,20 @@ def net_forward(net, x, bf16=False):
 
 
 def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
-              x0=0.0, lam=1.0, want_grad=True, bf16=False, keep=False):
+              x0=0.0, lam=1.0, want_grad=True, bf16=False, keep=False, kink_band=0.0,
+              mask_shift=0.0):
     """One training iteration on the shard ``paths`` (global path indices).
 
     Returns dict(loss_sum=Σ_m R², loss=Σ R²/B_global, grad=∂L/∂params of this
     shard's contribution (sums over shards to the full gradient, R5, §8(e)),
     R, Y_N, X_N, and per-step traces if keep).
+
+    kink_band > 0 also returns ``slack`` (shape of grad): for every hidden unit
+    whose pre-activation lies within kink_band·(Σ|W x| + |b|) of the ReLU kink,
+    both masks are valid answers of a finite-precision evaluation (R15, R19),
+    and slack bounds (to first order) how much the gradient moves when that
+    mask flips.  mask_shift (tests only) evaluates the backward masks as
+    1[A > mask_shift] to emulate such flips.
     """
     paths = np.asarray(paths, dtype=np.int64)
     B = float(batch_global)
@@ -167,6 +176,9 @@ def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
     # Adjoint: ā_N = ∂L/∂Y_N = 2R/B.
     grad = np.zeros_like(np.asarray(params, dtype=np.float64))
     gy0, gnets = unpack(grad, d, w, N)
+    if kink_band > 0.0:
+        slack = np.zeros_like(grad)
+        _, snets = unpack(slack, d, w, N)
     abar = 2.0 * R / B
     op = round_bf16 if bf16 else (lambda a: a)
     for n in range(N - 1, -1, -1):
@@ -177,16 +189,31 @@ def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
         g["W3"][...] = op(dZ).T @ op(H2)
         g["b3"][...] = dZ.sum(0)
         dH2 = op(dZ) @ op(net["W3"])
-        dA2 = dH2 * (A2 > 0.0)                       # ReLU'(0) = 0 (R15)
+        m2 = A2 > mask_shift                         # ReLU'(0) = 0 (R15)
+        dA2 = dH2 * m2
         g["W2"][...] = op(dA2).T @ op(H1)
         g["b2"][...] = dA2.sum(0)
         dH1 = dH2 + op(dA2) @ op(net["W2"])
-        dA1 = dH1 * (A1 > 0.0)
+        m1 = A1 > mask_shift
+        dA1 = dH1 * m1
         g["W1"][...] = op(dA1).T @ op(X)
         g["b1"][...] = dA1.sum(0)
+        if kink_band > 0.0:
+            s = snets[n]
+            amb1 = np.abs(A1) <= kink_band * (np.abs(X) @ np.abs(net["W1"]).T + np.abs(net["b1"]))
+            amb2 = np.abs(A2) <= kink_band * (np.abs(H1) @ np.abs(net["W2"]).T + np.abs(net["b2"]))
+            e2 = np.abs(dH2) * amb2                  # |ΔdA2| if an A2 mask flips
+            e1 = (np.abs(dH1) * amb1                 # |ΔdA1| from an A1 flip ...
+                  + (e2 @ np.abs(net["W2"])) * (m1 | amb1))   # ... or propagated from A2
+            s["W2"][...] = e2.T @ np.abs(H1)
+            s["b2"][...] = e2.sum(0)
+            s["W1"][...] = e1.T @ np.abs(X)
+            s["b1"][...] = e1.sum(0)
         abar = abar * (1.0 - dt * driver_df_dy(problem, Yn, Z, lam))
     gy0[0] = abar.sum()
     out["grad"] = grad
+    if kink_band > 0.0:
+        out["slack"] = slack
     return out
 
 

@@ -1,0 +1,689 @@
+// api.cu — the C-ABI of include/bsde.h: context lifetime, validation, the
+// per-iteration launch sequence (optionally captured in a CUDA graph), the NCCL
+// gradient allreduce (a7, loaded with dlopen so the library has no link-time
+// NCCL dependency), multilevel prolongation and the introspection calls.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bsde.h"
+#include "kernels.cuh"
+
+namespace bsde {
+size_t simt_max_smem(int d, int w);
+bool tc_supported(int d, int w);
+cudaError_t launch_fwd_tc(const PassArgs& a, cudaStream_t s);
+cudaError_t launch_bwd_tc(const PassArgs& a, cudaStream_t s);
+cudaError_t launch_pack_weights(const PassArgs& a, cudaStream_t s);
+size_t tc_pack_bytes(int d, int w, int N, int precision);
+size_t tc_partial_bytes(int d, int w, int precision);
+}  // namespace bsde
+
+using namespace bsde;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+// ---- NCCL, resolved at run time --------------------------------------------
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+    a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
+    a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
+    a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.GroupStart &&
+           a.GroupEnd && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+
+}  // namespace
+
+struct bsde_ctx {
+  int problem = 0, d = 0, w = 0, N = 0, N0 = 0, level = 0, N_max = 0;
+  double T = 1.0;
+  bsde_config cfg{};
+  int64_t B_local = 0, m0 = 0;
+  int family = BSDE_KERNEL_SIMT;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  float *params = nullptr, *grad = nullptr, *adam_m = nullptr, *adam_v = nullptr;
+  float *scratch = nullptr, *Xstore = nullptr, *Ystore = nullptr, *abar = nullptr;
+  float* Rstore = nullptr;
+  void* wpack = nullptr;
+  void* xpack = nullptr;
+  float* gpart = nullptr;
+  DeviceState* state = nullptr;
+  double* eval_loss = nullptr;
+  ncclComm_t comm = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int graph_N = -1;
+  int launches = 0;
+  int64_t host_it = 0;   // mirror of state->it
+  std::string err;
+};
+
+namespace {
+
+int fail(bsde_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf; else g_create_error = buf;
+  return code;
+}
+
+#define CK(expr)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(ctx, BSDE_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),     \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+#define NK(expr)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (expr);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      return fail(ctx, BSDE_ENCCL, "%s: %s", #expr, nccl().GetErrorString(r_));         \
+  } while (0)
+
+int64_t num_params_at(const bsde_ctx* c, int N) { return 1 + (int64_t)N * NetDims{c->d, c->w}.step_size(); }
+
+PassArgs pass_args(bsde_ctx* c) {
+  PassArgs a{};
+  a.problem = c->problem;
+  a.d = c->d;
+  a.w = c->w;
+  a.N = c->N;
+  a.dt = (float)(c->T / c->N);
+  a.sqrt_dt = (float)std::sqrt(c->T / c->N);
+  a.lam = (float)c->cfg.lambda;
+  a.x0 = (float)c->cfg.x0;
+  a.inv_B = (float)(1.0 / (double)c->cfg.batch_global);
+  a.B_local = c->B_local;
+  a.m0 = c->m0;
+  a.k0 = (uint32_t)(c->cfg.seed & 0xffffffffu);
+  a.k1 = (uint32_t)(c->cfg.seed >> 32);
+  a.params = c->params;
+  a.grad = c->grad;
+  a.Xstore = c->Xstore;
+  a.Ystore = c->Ystore;
+  a.abar = c->abar;
+  a.Rstore = c->Rstore;
+  a.state = c->state;
+  a.loss_acc = &c->state->loss_sum;
+  a.wpack = c->wpack;
+  a.xpack = c->xpack;
+  a.gpart = c->gpart;
+  a.precision = c->cfg.precision;
+  return a;
+}
+
+// Enqueue one iteration; with_update = 0 stops after the gradient + check.
+// ev (optional, 7 events) brackets the phases for bsde_profile_steps.
+int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
+  const int64_t np = num_params_at(ctx, ctx->N);
+  const PassArgs a = pass_args(ctx);
+  auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], ctx->stream); };
+  int launches = 0;
+  mark(0);
+  CK(launch_begin_step(ctx->state, ctx->grad, np, ctx->stream));
+  launches += 1;   // k_begin_step (the memset is not a kernel)
+  mark(1);
+  if (ctx->family == BSDE_KERNEL_TC) {
+    CK(launch_fwd_tc(a, ctx->stream));
+    mark(2);
+    CK(launch_bwd_tc(a, ctx->stream));
+  } else {
+    CK(launch_fwd_simt(a, ctx->stream));
+    mark(2);
+    CK(launch_bwd_simt(a, ctx->stream));
+  }
+  launches += 2;
+  mark(3);
+  if (ctx->comm) {
+    NK(nccl().GroupStart());
+    NK(nccl().AllReduce(ctx->grad, ctx->grad, (size_t)np, ncclFloat32, ncclSum, ctx->comm,
+                        ctx->stream));
+    NK(nccl().AllReduce(&ctx->state->loss_sum, &ctx->state->loss_sum, 1, ncclFloat64, ncclSum,
+                        ctx->comm, ctx->stream));
+    NK(nccl().GroupEnd());
+  }
+  mark(4);
+  CK(launch_check(ctx->grad, np, ctx->state, 1.0 / (double)ctx->cfg.batch_global,
+                  (float)ctx->cfg.beta1, (float)ctx->cfg.beta2, ctx->stream));
+  launches += 1;
+  mark(5);
+  if (with_update) {
+    CK(launch_adam(ctx->params, ctx->grad, ctx->adam_m, ctx->adam_v, np, ctx->state,
+                   (float)ctx->cfg.lr, (float)ctx->cfg.beta1, (float)ctx->cfg.beta2,
+                   (float)ctx->cfg.eps, 1, ctx->stream));
+    launches += 2;
+    if (ctx->family == BSDE_KERNEL_TC) {   // bf16 weight images for the next step
+      CK(launch_pack_weights(a, ctx->stream));
+      launches += 1;
+    }
+  }
+  mark(6);
+  ctx->launches = launches;
+  return BSDE_OK;
+}
+
+int read_state(bsde_ctx* ctx, DeviceState* hs) {
+  CK(cudaMemcpyAsync(hs, ctx->state, sizeof(DeviceState), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return BSDE_OK;
+}
+
+int repack(bsde_ctx* ctx) {
+  if (ctx->family != BSDE_KERNEL_TC) return BSDE_OK;
+  CK(launch_pack_weights(pass_args(ctx), ctx->stream));
+  return BSDE_OK;
+}
+
+void free_all(bsde_ctx* c) {
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  void* bufs[] = {c->params, c->grad, c->adam_m, c->adam_v, c->scratch, c->Xstore, c->Ystore,
+                  c->abar, c->Rstore, c->wpack, c->xpack, c->gpart, c->state, c->eval_loss};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+void bsde_config_default(bsde_config* cfg) {
+  std::memset(cfg, 0, sizeof *cfg);
+  cfg->batch_global = 256;
+  cfg->x0 = 0.0;
+  cfg->lambda = 1.0;
+  cfg->lr = 1e-2;
+  cfg->beta1 = 0.9;
+  cfg->beta2 = 0.999;
+  cfg->eps = 1e-8;
+  cfg->seed = 0;
+  cfg->precision = BSDE_FP32;
+  cfg->kernel = BSDE_KERNEL_AUTO;
+  cfg->prolong_mode = BSDE_PROLONG_COPY;
+  cfg->max_levels = 0;
+  cfg->device = 0;
+  cfg->stream = nullptr;
+  cfg->rank = 0;
+  cfg->world = 1;
+  cfg->nccl_id = nullptr;
+  cfg->use_graph = 1;
+  cfg->init_zero_head = 0;
+}
+
+int bsde_nccl_unique_id(void* out128) {
+  bsde_ctx* ctx = nullptr;
+  if (!out128) return fail(ctx, BSDE_EINVAL, "out128 is NULL");
+  if (!nccl().ok) return fail(ctx, BSDE_ENCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  NK(nccl().GetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof id);
+  return BSDE_OK;
+}
+
+int bsde_create(int problem, int d, int N, double T, const int* widths, int n_widths,
+                const bsde_config* cfg_in, bsde_ctx** out) {
+  bsde_ctx* none = nullptr;
+  if (!out) return fail(none, BSDE_EINVAL, "out is NULL");
+  *out = nullptr;
+  bsde_config cfg;
+  if (cfg_in) cfg = *cfg_in; else bsde_config_default(&cfg);
+  if (problem < BSDE_HEAT || problem > BSDE_ALLEN_CAHN)
+    return fail(none, BSDE_EINVAL, "problem=%d not in {0 heat, 1 hjb, 2 allen_cahn}", problem);
+  if (d < 1 || N < 1 || !(T > 0.0))
+    return fail(none, BSDE_EINVAL, "need d >= 1, N >= 1, T > 0 (got d=%d N=%d T=%g)", d, N, T);
+  if (!widths || n_widths != 2 || widths[0] != widths[1] || widths[0] < 1)
+    return fail(none, BSDE_EINVAL,
+                "widths must be {w, w} with w >= 1 (d->w->w->d residual net, R4); got n_widths=%d",
+                n_widths);
+  const int w = widths[0];
+  if (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world)
+    return fail(none, BSDE_EINVAL, "rank=%d world=%d", cfg.rank, cfg.world);
+  if (cfg.batch_global < 1 || cfg.batch_global % cfg.world != 0)
+    return fail(none, BSDE_EINVAL, "batch_global=%lld must be >= 1 and divisible by world=%d",
+                (long long)cfg.batch_global, cfg.world);
+  if (cfg.batch_global > (int64_t)1 << 32)
+    return fail(none, BSDE_EINVAL, "batch_global=%lld exceeds 2^32 (Philox path word)",
+                (long long)cfg.batch_global);
+  if (cfg.precision != BSDE_FP32 && cfg.precision != BSDE_BF16)
+    return fail(none, BSDE_EINVAL, "precision=%d", cfg.precision);
+  if (cfg.max_levels < 0 || cfg.max_levels > 12)
+    return fail(none, BSDE_EINVAL, "max_levels=%d", cfg.max_levels);
+  if (cfg.prolong_mode != BSDE_PROLONG_COPY && cfg.prolong_mode != BSDE_PROLONG_INTERP)
+    return fail(none, BSDE_EINVAL, "prolong_mode=%d", cfg.prolong_mode);
+  if (!(cfg.lr > 0) || !(cfg.beta1 >= 0 && cfg.beta1 < 1) || !(cfg.beta2 >= 0 && cfg.beta2 < 1) ||
+      !(cfg.eps > 0))
+    return fail(none, BSDE_EINVAL, "Adam hyper-parameters out of range");
+  int family = cfg.kernel;
+  if (family == BSDE_KERNEL_AUTO) family = tc_supported(d, w) ? BSDE_KERNEL_TC : BSDE_KERNEL_SIMT;
+  if (family == BSDE_KERNEL_TC && !tc_supported(d, w))
+    return fail(none, BSDE_EINVAL, "tcgen05 kernels need d+1 <= 128 and w+1 <= 128 (d=%d w=%d)",
+                d, w);
+  if (family == BSDE_KERNEL_SIMT && cfg.precision == BSDE_BF16)
+    return fail(none, BSDE_EINVAL, "bf16 operands need the tcgen05 kernels (kernel=SIMT given)");
+  if (family == BSDE_KERNEL_SIMT && simt_max_smem(d, w) > 227 * 1024)
+    return fail(none, BSDE_EINVAL, "d=%d w=%d too large for the SIMT kernels' shared memory", d, w);
+  if (family != BSDE_KERNEL_SIMT && family != BSDE_KERNEL_TC)
+    return fail(none, BSDE_EINVAL, "kernel=%d", cfg.kernel);
+  if (cfg.world > 1 && cfg.nccl_id && !nccl().ok)
+    return fail(none, BSDE_ENCCL, "world=%d but libnccl.so.2 could not be loaded", cfg.world);
+
+  bsde_ctx* ctx = new bsde_ctx;
+  ctx->problem = problem;
+  ctx->d = d;
+  ctx->w = w;
+  ctx->N = ctx->N0 = N;
+  ctx->N_max = N << cfg.max_levels;
+  ctx->T = T;
+  ctx->cfg = cfg;
+  ctx->family = family;
+  ctx->B_local = cfg.batch_global / cfg.world;
+  ctx->m0 = (int64_t)cfg.rank * ctx->B_local;
+
+  auto bail = [&](int code) {
+    g_create_error = ctx->err;
+    free_all(ctx);
+    delete ctx;
+    return code;
+  };
+  {
+    cudaError_t e = cudaSetDevice(cfg.device);
+    if (e != cudaSuccess) { ctx->err = std::string("cudaSetDevice: ") + cudaGetErrorString(e); return bail(BSDE_ECUDA); }
+  }
+  if (cfg.stream) {
+    ctx->stream = (cudaStream_t)cfg.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      ctx->err = "cudaStreamCreate failed";
+      return bail(BSDE_ECUDA);
+    }
+    ctx->own_stream = true;
+  }
+  const int64_t npmax = num_params_at(ctx, ctx->N_max);
+  struct Alloc { void** p; size_t bytes; };
+  const size_t xs = (size_t)ctx->N_max * ctx->B_local * d * sizeof(float);
+  std::vector<Alloc> allocs = {
+      {(void**)&ctx->params, npmax * sizeof(float)},
+      {(void**)&ctx->grad, npmax * sizeof(float)},
+      {(void**)&ctx->adam_m, npmax * sizeof(float)},
+      {(void**)&ctx->adam_v, npmax * sizeof(float)},
+      {(void**)&ctx->scratch, npmax * sizeof(float)},
+      {(void**)&ctx->Xstore, xs},
+      {(void**)&ctx->abar, (size_t)ctx->N_max * ctx->B_local * sizeof(float)},
+      {(void**)&ctx->Rstore, (size_t)ctx->B_local * sizeof(float)},
+      {(void**)&ctx->state, sizeof(DeviceState)},
+      {(void**)&ctx->eval_loss, sizeof(double) * 2},
+  };
+  if (problem == BSDE_ALLEN_CAHN)
+    allocs.push_back({(void**)&ctx->Ystore, (size_t)ctx->N_max * ctx->B_local * sizeof(float)});
+  if (family == BSDE_KERNEL_TC) {
+    allocs.push_back({&ctx->wpack, tc_pack_bytes(d, w, ctx->N_max, cfg.precision)});
+    allocs.push_back({(void**)&ctx->gpart, tc_partial_bytes(d, w, cfg.precision)});
+  }
+  for (auto& al : allocs) {
+    cudaError_t e = cudaMalloc(al.p, al.bytes);
+    if (e != cudaSuccess) {
+      char b[256];
+      snprintf(b, sizeof b, "cudaMalloc(%zu bytes): %s", al.bytes, cudaGetErrorString(e));
+      ctx->err = b;
+      return bail(BSDE_ENOMEM);
+    }
+  }
+  cudaMemsetAsync(ctx->adam_m, 0, npmax * sizeof(float), ctx->stream);
+  cudaMemsetAsync(ctx->adam_v, 0, npmax * sizeof(float), ctx->stream);
+  cudaMemsetAsync(ctx->state, 0, sizeof(DeviceState), ctx->stream);
+  if (launch_init_params(ctx->params, d, w, N, (uint32_t)(cfg.seed & 0xffffffffu),
+                         (uint32_t)(cfg.seed >> 32), cfg.init_zero_head, ctx->stream) !=
+      cudaSuccess) {
+    ctx->err = "init kernel launch failed";
+    return bail(BSDE_ECUDA);
+  }
+  if (repack(ctx) != BSDE_OK) return bail(BSDE_ECUDA);
+  if (cfg.world > 1 && cfg.nccl_id) {
+    ncclUniqueId id;
+    std::memcpy(&id, cfg.nccl_id, sizeof id);
+    ncclResult_t r = nccl().CommInitRank(&ctx->comm, cfg.world, id, cfg.rank);
+    if (r != ncclSuccess) {
+      ctx->err = std::string("ncclCommInitRank: ") + nccl().GetErrorString(r);
+      ctx->comm = nullptr;
+      return bail(BSDE_ENCCL);
+    }
+  }
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    ctx->err = std::string("create: ") + cudaGetErrorString(cudaGetLastError());
+    return bail(BSDE_ECUDA);
+  }
+  *out = ctx;
+  return BSDE_OK;
+}
+
+int bsde_train_step(bsde_ctx* ctx, double* loss_out) {
+  if (!ctx) return fail(ctx, BSDE_EINVAL, "ctx is NULL");
+  if (ctx->cfg.use_graph) {
+    if (!ctx->graph || ctx->graph_N != ctx->N) {
+      if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      int rc = enqueue_step(ctx, true);
+      cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+      if (rc != BSDE_OK) { if (e == cudaSuccess) cudaGraphDestroy(g); return rc; }
+      CK(e);
+      cudaError_t ie = cudaGraphInstantiate(&ctx->graph, g, 0);
+      cudaGraphDestroy(g);
+      CK(ie);
+      ctx->graph_N = ctx->N;
+    }
+    CK(cudaGraphLaunch(ctx->graph, ctx->stream));
+  } else {
+    int rc = enqueue_step(ctx, true);
+    if (rc != BSDE_OK) return rc;
+  }
+  ctx->host_it += 1;
+  if (loss_out) {
+    DeviceState hs;
+    int rc = read_state(ctx, &hs);
+    if (rc != BSDE_OK) return rc;
+    *loss_out = hs.loss_last;
+    if (hs.diverged_any) return fail(ctx, BSDE_EDIVERGED,
+                                     "diverged: loss=%g (non-finite or > 1e12, or non-finite gradient); update skipped",
+                                     hs.loss_last);
+  }
+  return BSDE_OK;
+}
+
+int bsde_compute_grad(bsde_ctx* ctx, double* loss_out) {
+  if (!ctx) return fail(ctx, BSDE_EINVAL, "ctx is NULL");
+  int rc = enqueue_step(ctx, false);
+  if (rc != BSDE_OK) return rc;
+  DeviceState hs;
+  rc = read_state(ctx, &hs);
+  if (rc != BSDE_OK) return rc;
+  if (loss_out) *loss_out = hs.loss_last;
+  return BSDE_OK;
+}
+
+int bsde_prolongate(bsde_ctx* ctx, int level) {
+  if (!ctx) return fail(ctx, BSDE_EINVAL, "ctx is NULL");
+  if (level != ctx->level + 1 || level > ctx->cfg.max_levels)
+    return fail(ctx, BSDE_ESTATE, "prolongate(level=%d): current level %d, max_levels %d", level,
+                ctx->level, ctx->cfg.max_levels);
+  const int64_t P = NetDims{ctx->d, ctx->w}.step_size();
+  const int64_t np = num_params_at(ctx, ctx->N);
+  CK(cudaMemcpyAsync(ctx->scratch, ctx->params, np * sizeof(float), cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  CK(launch_prolong(ctx->scratch, ctx->params, P, ctx->N, ctx->cfg.prolong_mode, ctx->stream));
+  ctx->N *= 2;
+  ctx->level = level;
+  const int64_t np2 = num_params_at(ctx, ctx->N);
+  CK(cudaMemsetAsync(ctx->adam_m, 0, np2 * sizeof(float), ctx->stream));
+  CK(cudaMemsetAsync(ctx->adam_v, 0, np2 * sizeof(float), ctx->stream));
+  DeviceState hs;
+  int rc = read_state(ctx, &hs);
+  if (rc != BSDE_OK) return rc;
+  hs.t = 0;
+  CK(cudaMemcpyAsync(ctx->state, &hs, sizeof hs, cudaMemcpyHostToDevice, ctx->stream));
+  rc = repack(ctx);
+  if (rc != BSDE_OK) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return BSDE_OK;
+}
+
+int bsde_y0(const bsde_ctx* cctx, double* y0_out) {
+  bsde_ctx* ctx = const_cast<bsde_ctx*>(cctx);
+  if (!ctx || !y0_out) return fail(ctx, BSDE_EINVAL, "NULL argument");
+  float y;
+  CK(cudaMemcpyAsync(&y, ctx->params, sizeof y, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *y0_out = y;
+  return BSDE_OK;
+}
+
+int bsde_num_params(const bsde_ctx* ctx, int64_t* n) {
+  if (!ctx || !n) return fail(const_cast<bsde_ctx*>(ctx), BSDE_EINVAL, "NULL argument");
+  *n = num_params_at(ctx, ctx->N);
+  return BSDE_OK;
+}
+
+static int copy_out(bsde_ctx* ctx, const float* dev, float* host, int64_t n) {
+  if (!host || n != num_params_at(ctx, ctx->N))
+    return fail(ctx, BSDE_EINVAL, "buffer of %lld floats given, %lld expected", (long long)n,
+                (long long)num_params_at(ctx, ctx->N));
+  CK(cudaMemcpyAsync(host, dev, n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return BSDE_OK;
+}
+
+static int copy_in(bsde_ctx* ctx, float* dev, const float* host, int64_t n) {
+  if (!host || n != num_params_at(ctx, ctx->N))
+    return fail(ctx, BSDE_EINVAL, "buffer of %lld floats given, %lld expected", (long long)n,
+                (long long)num_params_at(ctx, ctx->N));
+  CK(cudaMemcpyAsync(dev, host, n * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return BSDE_OK;
+}
+
+int bsde_get_params(const bsde_ctx* c, float* host, int64_t n) {
+  bsde_ctx* ctx = const_cast<bsde_ctx*>(c);
+  if (!ctx) return BSDE_EINVAL;
+  return copy_out(ctx, ctx->params, host, n);
+}
+int bsde_set_params(bsde_ctx* ctx, const float* host, int64_t n) {
+  if (!ctx) return BSDE_EINVAL;
+  int rc = copy_in(ctx, ctx->params, host, n);
+  if (rc != BSDE_OK) return rc;
+  rc = repack(ctx);
+  if (rc != BSDE_OK) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return BSDE_OK;
+}
+int bsde_get_grads(const bsde_ctx* c, float* host, int64_t n) {
+  bsde_ctx* ctx = const_cast<bsde_ctx*>(c);
+  if (!ctx) return BSDE_EINVAL;
+  return copy_out(ctx, ctx->grad, host, n);
+}
+int bsde_get_adam_state(const bsde_ctx* c, float* m, float* v, int64_t n, int64_t* t) {
+  bsde_ctx* ctx = const_cast<bsde_ctx*>(c);
+  if (!ctx || !t) return BSDE_EINVAL;
+  int rc = copy_out(ctx, ctx->adam_m, m, n);
+  if (rc == BSDE_OK) rc = copy_out(ctx, ctx->adam_v, v, n);
+  if (rc != BSDE_OK) return rc;
+  DeviceState hs;
+  rc = read_state(ctx, &hs);
+  *t = hs.t;
+  return rc;
+}
+int bsde_set_adam_state(bsde_ctx* ctx, const float* m, const float* v, int64_t n, int64_t t) {
+  if (!ctx || t < 0) return BSDE_EINVAL;
+  int rc = copy_in(ctx, ctx->adam_m, m, n);
+  if (rc == BSDE_OK) rc = copy_in(ctx, ctx->adam_v, v, n);
+  if (rc != BSDE_OK) return rc;
+  DeviceState hs;
+  rc = read_state(ctx, &hs);
+  if (rc != BSDE_OK) return rc;
+  hs.t = (int32_t)t;
+  CK(cudaMemcpyAsync(ctx->state, &hs, sizeof hs, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return BSDE_OK;
+}
+int bsde_get_iteration(const bsde_ctx* c, int64_t* it) {
+  bsde_ctx* ctx = const_cast<bsde_ctx*>(c);
+  if (!ctx || !it) return BSDE_EINVAL;
+  DeviceState hs;
+  int rc = read_state(ctx, &hs);
+  *it = hs.it;
+  return rc;
+}
+int bsde_set_iteration(bsde_ctx* ctx, int64_t it) {
+  if (!ctx || it < 0 || it >= (int64_t)kEvalBit)
+    return fail(ctx, BSDE_EINVAL, "iteration must be in [0, 2^31)");
+  DeviceState hs;
+  int rc = read_state(ctx, &hs);
+  if (rc != BSDE_OK) return rc;
+  hs.it = (uint32_t)it;
+  hs.diverged_any = 0;
+  CK(cudaMemcpyAsync(ctx->state, &hs, sizeof hs, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->host_it = it;
+  return BSDE_OK;
+}
+int bsde_current_steps(const bsde_ctx* ctx, int* N) {
+  if (!ctx || !N) return BSDE_EINVAL;
+  *N = ctx->N;
+  return BSDE_OK;
+}
+
+int bsde_eval_loss(bsde_ctx* ctx, uint32_t eval_id, int64_t batch, double* loss_out) {
+  if (!ctx || !loss_out) return fail(ctx, BSDE_EINVAL, "NULL argument");
+  if (batch < 1 || batch % ctx->cfg.world || batch > ((int64_t)1 << 32))
+    return fail(ctx, BSDE_EINVAL, "eval batch=%lld must be divisible by world=%d",
+                (long long)batch, ctx->cfg.world);
+  PassArgs a = pass_args(ctx);
+  a.eval = 1;
+  a.eval_it = kEvalBit | (eval_id & 0x7fffffffu);
+  a.B_local = batch / ctx->cfg.world;
+  a.m0 = (int64_t)ctx->cfg.rank * a.B_local;
+  a.inv_B = (float)(1.0 / (double)batch);
+  a.loss_acc = ctx->eval_loss;
+  CK(cudaMemsetAsync(ctx->eval_loss, 0, sizeof(double), ctx->stream));
+  if (ctx->family == BSDE_KERNEL_TC) {
+    CK(launch_fwd_tc(a, ctx->stream));
+  } else {
+    CK(launch_fwd_simt(a, ctx->stream));
+  }
+  if (ctx->comm)
+    NK(nccl().AllReduce(ctx->eval_loss, ctx->eval_loss, 1, ncclFloat64, ncclSum, ctx->comm,
+                        ctx->stream));
+  double s;
+  CK(cudaMemcpyAsync(&s, ctx->eval_loss, sizeof s, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *loss_out = s / (double)batch;
+  return BSDE_OK;
+}
+
+int bsde_debug_philox(const bsde_ctx* c, const uint32_t* ctr, const uint32_t key[2],
+                      int64_t count, uint32_t* out) {
+  bsde_ctx* ctx = const_cast<bsde_ctx*>(c);
+  if (!ctx || !ctr || !key || !out || count < 1) return fail(ctx, BSDE_EINVAL, "bad argument");
+  uint32_t *dc = nullptr, *dout = nullptr;
+  CK(cudaMallocAsync((void**)&dc, count * 16, ctx->stream));
+  CK(cudaMallocAsync((void**)&dout, count * 16, ctx->stream));
+  CK(cudaMemcpyAsync(dc, ctr, count * 16, cudaMemcpyHostToDevice, ctx->stream));
+  CK(launch_debug_philox(dc, key[0], key[1], count, dout, ctx->stream));
+  CK(cudaMemcpyAsync(out, dout, count * 16, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaFreeAsync(dc, ctx->stream));
+  CK(cudaFreeAsync(dout, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return BSDE_OK;
+}
+
+int bsde_debug_dw(const bsde_ctx* c, int64_t it, int n, int64_t m0, int64_t count,
+                  float* host_out) {
+  bsde_ctx* ctx = const_cast<bsde_ctx*>(c);
+  if (!ctx || !host_out || count < 1 || n < 0) return fail(ctx, BSDE_EINVAL, "bad argument");
+  float* d_out = nullptr;
+  const size_t bytes = (size_t)count * ctx->d * sizeof(float);
+  CK(cudaMallocAsync((void**)&d_out, bytes, ctx->stream));
+  CK(launch_debug_dw((uint32_t)it, n, m0, count, ctx->d, (float)std::sqrt(ctx->T / ctx->N),
+                     (uint32_t)(ctx->cfg.seed & 0xffffffffu), (uint32_t)(ctx->cfg.seed >> 32),
+                     d_out, ctx->stream));
+  CK(cudaMemcpyAsync(host_out, d_out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaFreeAsync(d_out, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return BSDE_OK;
+}
+
+int bsde_debug_residuals(const bsde_ctx* c, int64_t m0, int64_t count, float* host_out) {
+  bsde_ctx* ctx = const_cast<bsde_ctx*>(c);
+  if (!ctx || !host_out || m0 < 0 || count < 1 || m0 + count > ctx->B_local)
+    return fail(ctx, BSDE_EINVAL, "residual range [%lld, %lld) outside [0, %lld)", (long long)m0,
+                (long long)(m0 + count), (long long)(ctx ? ctx->B_local : 0));
+  CK(cudaMemcpyAsync(host_out, ctx->Rstore + m0, count * sizeof(float), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return BSDE_OK;
+}
+
+int bsde_profile_steps(bsde_ctx* ctx, int steps, float* ms_out, int n_out) {
+  if (!ctx || steps < 1 || !ms_out || n_out < 6)
+    return fail(ctx, BSDE_EINVAL, "profile_steps: need steps >= 1 and n_out >= 6");
+  std::vector<cudaEvent_t> ev(7 * (size_t)steps);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  int rc = BSDE_OK;
+  for (int s = 0; s < steps && rc == BSDE_OK; ++s) {
+    rc = enqueue_step(ctx, true, &ev[7 * (size_t)s]);
+    ctx->host_it += 1;
+  }
+  if (rc == BSDE_OK) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 6; ++i) ms_out[i] = 0.0f;
+    for (int s = 0; s < steps; ++s)
+      for (int i = 0; i < 6; ++i) {
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, ev[7 * (size_t)s + i], ev[7 * (size_t)s + i + 1]));
+        ms_out[i] += ms / steps;
+      }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+int bsde_launches_per_step(const bsde_ctx* ctx, int* n) {
+  if (!ctx || !n) return BSDE_EINVAL;
+  *n = ctx->launches;
+  return BSDE_OK;
+}
+
+const char* bsde_kernel_family(const bsde_ctx* ctx) {
+  if (!ctx) return "none";
+  return ctx->family == BSDE_KERNEL_TC ? "tc" : "simt";
+}
+
+const char* bsde_last_error(const bsde_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+void bsde_destroy(bsde_ctx* ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  free_all(ctx);
+  delete ctx;
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+// kernels.cuh — argument blocks and launchers of every device kernel.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace bsde {
+
+// Arguments of one forward/adjoint pass.  Everything a graph replay needs to
+// change from step to step lives in DeviceState (it, t), not here.
+struct PassArgs {
+  int problem, d, w, N;
+  float dt, sqrt_dt, lam, x0, inv_B;   // Δt, √Δt, λ, X0 component, 1/B_global
+  int64_t B_local, m0;                 // this rank's paths: global [m0, m0 + B_local)
+  uint32_t k0, k1;                     // Philox key (R8)
+  int eval;                            // 1: forward only, counter word 3 = eval_it
+  uint32_t eval_it;
+  const float* params;                 // fp32 master (flat layout)
+  float* grad;                         // flat gradient (+ nothing else); zeroed per step
+  float* Xstore;                       // [N][B_local][d] fp32: X_n for the adjoint pass
+  float* Ystore;                       // [N][B_local]: Y_n (Allen-Cahn only)
+  float* abar;                         // [N][B_local] ā_{n+1} (AC) or [B_local] ā_N
+  float* Rstore;                       // [B_local] terminal residual R (debug / parity)
+  DeviceState* state;
+  double* loss_acc;                    // Σ_m R² accumulator (state->loss_sum or eval slot)
+  // tcgen05 path only
+  const void* wpack;                   // packed bf16 weight images (see tc.cu)
+  void* xpack;                         // bf16 X store (BF16 precision)
+  float* gpart;                        // per-CTA gradient partial scratch
+  int precision;
+};
+
+// SIMT fp32 kernels (simt.cu)
+cudaError_t launch_fwd_simt(const PassArgs& a, cudaStream_t s);
+cudaError_t launch_bwd_simt(const PassArgs& a, cudaStream_t s);
+
+// auxiliary kernels (aux.cu)
+cudaError_t launch_init_params(float* params, int d, int w, int N, uint32_t k0, uint32_t k1,
+                               int zero_head, cudaStream_t s);
+cudaError_t launch_begin_step(DeviceState* st, float* grad, int64_t n_grad, cudaStream_t s);
+cudaError_t launch_check(const float* grad, int64_t n, DeviceState* st, double inv_B,
+                         float beta1, float beta2, cudaStream_t s);
+cudaError_t launch_adam(float* params, const float* grad, float* m, float* v, int64_t n,
+                        DeviceState* st, float lr, float beta1, float beta2, float eps,
+                        int advance_it, cudaStream_t s);
+cudaError_t launch_prolong(const float* src, float* dst, int64_t P, int N, int mode,
+                           cudaStream_t s);
+cudaError_t launch_debug_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, int64_t count,
+                                uint32_t* out, cudaStream_t s);
+cudaError_t launch_debug_dw(uint32_t it, int n, int64_t m0, int64_t count, int d,
+                            float sqrt_dt, uint32_t k0, uint32_t k1, float* out,
+                            cudaStream_t s);
+
+}  // namespace bsde

@@ -1,0 +1,218 @@
+"""Python face of libbsde.so: one object per GPU/rank wrapping a bsde_ctx.
+
+Marshalling only — every step of the training iteration runs in the CUDA
+kernels behind include/bsde.h.  PyTorch is used for the device's current
+stream and for torch.distributed (broadcast of the NCCL unique id).
+"""
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import BSDEError
+
+PROBLEMS = {"heat": _lib.HEAT, "hjb": _lib.HJB, "allen_cahn": _lib.ALLEN_CAHN}
+PRECISIONS = {"fp32": _lib.FP32, "bf16": _lib.BF16}
+KERNELS = {"auto": _lib.KERNEL_AUTO, "simt": _lib.KERNEL_SIMT, "tc": _lib.KERNEL_TC}
+PROLONG = {"copy": _lib.PROLONG_COPY, "interp": _lib.PROLONG_INTERP}
+
+
+def _fptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    rc = _lib.lib().bsde_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p))
+    if rc:
+        raise BSDEError(rc, _lib.lib().bsde_last_error(None).decode())
+    return buf.raw
+
+
+def step_size(d, w):
+    return 2 * d * w + w * w + 2 * w + d
+
+
+class BSDE:
+    """bsde_create(problem, d, N, T, widths) + the step / level / introspection calls."""
+
+    def __init__(self, problem, d, N, T, width, batch, *, lr=1e-2, seed=0, precision="fp32",
+                 kernel="auto", x0=0.0, lam=1.0, prolong="copy", max_levels=0, device=0,
+                 stream=None, rank=0, world=1, nccl_id=None, use_graph=True, beta1=0.9,
+                 beta2=0.999, eps=1e-8, zero_head=None):
+        """stream: a torch.cuda.Stream, a raw cudaStream_t (int), or None (a new
+        torch stream on `device`, kept in self.stream).  zero_head: R7b, defaults
+        to True for Allen-Cahn."""
+        L = _lib.lib()
+        cfg = _lib.Config()
+        L.bsde_config_default(ctypes.byref(cfg))
+        cfg.batch_global = int(batch)
+        cfg.x0, cfg.lam = float(x0), float(lam)
+        cfg.lr, cfg.beta1, cfg.beta2, cfg.eps = float(lr), float(beta1), float(beta2), float(eps)
+        cfg.seed = int(seed)
+        cfg.precision = PRECISIONS[precision] if isinstance(precision, str) else int(precision)
+        cfg.kernel = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
+        cfg.prolong_mode = PROLONG[prolong] if isinstance(prolong, str) else int(prolong)
+        cfg.max_levels = int(max_levels)
+        cfg.device = int(device)
+        self.stream = None
+        if stream is None:
+            import torch
+            if torch.cuda.is_available():
+                self.stream = torch.cuda.Stream(device=device)
+                stream = self.stream.cuda_stream
+        elif not isinstance(stream, int):
+            self.stream = stream
+            stream = stream.cuda_stream
+        cfg.stream = stream or None
+        if zero_head is None:
+            zero_head = (problem == "allen_cahn" or problem == _lib.ALLEN_CAHN)
+        cfg.init_zero_head = int(bool(zero_head))
+        self.zero_head = bool(zero_head)
+        cfg.rank, cfg.world = int(rank), int(world)
+        self._nccl_id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+        cfg.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p) if nccl_id else None
+        cfg.use_graph = int(bool(use_graph))
+        self.problem = PROBLEMS[problem] if isinstance(problem, str) else int(problem)
+        self.d, self.w, self.T, self.batch = int(d), int(width), float(T), int(batch)
+        self.rank, self.world = int(rank), int(world)
+        widths = (ctypes.c_int * 2)(int(width), int(width))
+        h = ctypes.c_void_p()
+        rc = L.bsde_create(self.problem, self.d, int(N), self.T, widths, 2, ctypes.byref(cfg),
+                           ctypes.byref(h))
+        if rc:
+            raise BSDEError(rc, L.bsde_last_error(None).decode())
+        self._h = h
+        self._L = L
+
+    @classmethod
+    def distributed(cls, problem, d, N, T, width, batch, **kw):
+        """One context per rank of the default torch.distributed group; rank 0
+        creates the NCCL unique id and broadcasts it."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        return cls(problem, d, N, T, width, batch, rank=rank, world=world,
+                   nccl_id=obj[0] if world > 1 else None, **kw)
+
+    # ------------------------------------------------------------------ core
+    def _ck(self, rc):
+        if rc:
+            raise BSDEError(rc, self._L.bsde_last_error(self._h).decode())
+
+    def train_step(self, sync=True):
+        """One iteration (a1-a8).  sync=True returns the pre-update loss."""
+        if not sync:
+            self._ck(self._L.bsde_train_step(self._h, None))
+            return None
+        loss = ctypes.c_double()
+        self._ck(self._L.bsde_train_step(self._h, ctypes.byref(loss)))
+        return loss.value
+
+    def compute_grad(self):
+        loss = ctypes.c_double()
+        self._ck(self._L.bsde_compute_grad(self._h, ctypes.byref(loss)))
+        return loss.value
+
+    def prolongate(self, level):
+        self._ck(self._L.bsde_prolongate(self._h, int(level)))
+
+    def y0(self):
+        v = ctypes.c_double()
+        self._ck(self._L.bsde_y0(self._h, ctypes.byref(v)))
+        return v.value
+
+    def eval_loss(self, eval_id=0, batch=None):
+        v = ctypes.c_double()
+        self._ck(self._L.bsde_eval_loss(self._h, int(eval_id), int(batch or self.batch),
+                                        ctypes.byref(v)))
+        return v.value
+
+    # ------------------------------------------------------------------ state
+    @property
+    def N(self):
+        n = ctypes.c_int()
+        self._ck(self._L.bsde_current_steps(self._h, ctypes.byref(n)))
+        return n.value
+
+    def num_params(self):
+        n = ctypes.c_int64()
+        self._ck(self._L.bsde_num_params(self._h, ctypes.byref(n)))
+        return n.value
+
+    def get_params(self):
+        a = np.empty(self.num_params(), np.float32)
+        self._ck(self._L.bsde_get_params(self._h, _fptr(a), a.size))
+        return a
+
+    def set_params(self, p):
+        a = np.ascontiguousarray(p, dtype=np.float32)
+        self._ck(self._L.bsde_set_params(self._h, _fptr(a), a.size))
+
+    def get_grads(self):
+        a = np.empty(self.num_params(), np.float32)
+        self._ck(self._L.bsde_get_grads(self._h, _fptr(a), a.size))
+        return a
+
+    def get_adam_state(self):
+        n = self.num_params()
+        m, v, t = np.empty(n, np.float32), np.empty(n, np.float32), ctypes.c_int64()
+        self._ck(self._L.bsde_get_adam_state(self._h, _fptr(m), _fptr(v), n, ctypes.byref(t)))
+        return m, v, t.value
+
+    def set_adam_state(self, m, v, t):
+        m = np.ascontiguousarray(m, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        self._ck(self._L.bsde_set_adam_state(self._h, _fptr(m), _fptr(v), m.size, int(t)))
+
+    @property
+    def iteration(self):
+        v = ctypes.c_int64()
+        self._ck(self._L.bsde_get_iteration(self._h, ctypes.byref(v)))
+        return v.value
+
+    @iteration.setter
+    def iteration(self, it):
+        self._ck(self._L.bsde_set_iteration(self._h, int(it)))
+
+    def launches_per_step(self):
+        n = ctypes.c_int()
+        self._ck(self._L.bsde_launches_per_step(self._h, ctypes.byref(n)))
+        return n.value
+
+    @property
+    def family(self):
+        return self._L.bsde_kernel_family(self._h).decode()
+
+    # ------------------------------------------------------------------ test hooks
+    def debug_philox(self, ctr, key):
+        ctr = np.ascontiguousarray(ctr, np.uint32).reshape(-1, 4)
+        key = np.ascontiguousarray(key, np.uint32).reshape(2)
+        out = np.empty_like(ctr)
+        P = ctypes.POINTER(ctypes.c_uint32)
+        self._ck(self._L.bsde_debug_philox(self._h, ctr.ctypes.data_as(P), key.ctypes.data_as(P),
+                                           ctr.shape[0], out.ctypes.data_as(P)))
+        return out
+
+    def debug_dw(self, it, n, m0, count):
+        out = np.empty((count, self.d), np.float32)
+        self._ck(self._L.bsde_debug_dw(self._h, int(it), int(n), int(m0), int(count), _fptr(out)))
+        return out
+
+    def debug_residuals(self, m0, count):
+        out = np.empty(count, np.float32)
+        self._ck(self._L.bsde_debug_residuals(self._h, int(m0), int(count), _fptr(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.bsde_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

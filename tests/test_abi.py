@@ -1,0 +1,65 @@
+"""CPU checks of the boundary: libbsde.so builds for sm_100a, loads, and exports
+every symbol include/bsde.h declares; argument validation without a GPU."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_1910_11623_b200 import build
+    return build.build()
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "bsde.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bsde_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(libpath):
+    syms = header_symbols()
+    assert len(syms) >= 20
+    L = ctypes.CDLL(libpath)
+    for s in syms:
+        assert hasattr(L, s), s
+    from paper_1910_11623_b200 import _lib
+    assert sorted(_lib.SYMBOLS) == syms
+
+
+def test_library_is_sm100a_and_uses_tensor_memory(libpath):
+    out = subprocess.run(["cuobjdump", "--list-elf", libpath], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_config_struct_layout_matches_header(libpath):
+    """The ctypes mirror of bsde_config has the C layout: defaults round-trip."""
+    from paper_1910_11623_b200 import _lib
+    cfg = _lib.Config()
+    _lib.lib().bsde_config_default(ctypes.byref(cfg))
+    assert cfg.batch_global == 256 and cfg.lam == 1.0 and cfg.lr == 1e-2
+    assert cfg.beta1 == 0.9 and cfg.beta2 == 0.999 and cfg.eps == 1e-8
+    assert cfg.world == 1 and cfg.rank == 0 and cfg.use_graph == 1 and cfg.kernel == 0
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(problem="heat", d=0), "d >= 1"),
+    (dict(problem="heat", width=0), "widths"),
+    (dict(problem="hjb", batch=10, world=3), "divisible"),
+    (dict(problem="allen_cahn", kernel="simt", precision="bf16"), "bf16"),
+])
+def test_create_rejects_bad_arguments(libpath, kw, msg):
+    """Validation happens before any device call, so it runs on the CPU box."""
+    from paper_1910_11623_b200 import BSDE, BSDEError
+    args = dict(problem="heat", d=4, N=2, T=1.0, width=8, batch=16)
+    args.update(kw)
+    world = args.pop("world", 1)
+    with pytest.raises(BSDEError) as e:
+        BSDE(args.pop("problem"), args.pop("d"), args.pop("N"), args.pop("T"), args.pop("width"),
+             args.pop("batch"), world=world, stream=0, **args)
+    assert msg in str(e.value) and e.value.code == -1

@@ -1,0 +1,227 @@
+"""GPU ↔ oracle parity through the C-ABI (libbsde.so), DESIGN.md §Parity.
+
+All inputs are seeded and synthetic (Philox counters); sizes span several tiles
+and a ragged tail.  Tolerances: north_star (1e-4 fp32, 2e-2 bf16).
+"""
+import numpy as np
+import pytest
+
+from oracle import bsde as ob, closed_forms as cf, philox
+from parity_util import KINK_BAND, TOL, compare_grads, oracle_iteration
+from workloads import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1910_11623_b200 import build
+    build.build()
+
+
+def make(problem, d, w, N, T, batch, **kw):
+    from paper_1910_11623_b200 import BSDE
+    return BSDE(problem, d, N, T, w, batch, **kw)
+
+
+# ------------------------------------------------------------------ a1: Philox
+def test_philox_bit_exact_on_device():
+    s = make("heat", 4, 8, 2, 1.0, 64, kernel="simt")
+    rng = np.random.default_rng(0)
+    ctr = rng.integers(0, 2 ** 32, size=(4096, 4), dtype=np.uint64).astype(np.uint32)
+    for key in ([0, 0], [0xDEADBEEF, 0x12345678]):
+        out = s.debug_philox(ctr, np.array(key, np.uint32))
+        ref = np.stack(philox.philox4x32_10(ctr[:, 0], ctr[:, 1], ctr[:, 2], ctr[:, 3], *key), 1)
+        assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("d,N,T", [(100, 20, 1.0), (10, 5, 1.0), (7, 3, 0.3)])
+def test_dw_matches_oracle(d, N, T):
+    s = make("hjb", d, 8, N, T, 64, kernel="simt", seed=0x1234567890ABCDEF)
+    for it, n, m0 in ((0, 0, 0), (17, N - 1, 1000), (2 ** 31 - 1, 1, 2 ** 32 - 300)):
+        gpu = s.debug_dw(it, n, m0, 257)
+        ref = philox.brownian_increments(0x1234567890ABCDEF, it, n, np.arange(m0, m0 + 257), d,
+                                         T / N)
+        assert np.max(np.abs(gpu - ref)) <= 2e-6 * np.sqrt(T / N) * 6
+
+
+@pytest.mark.parametrize("problem", ["hjb", "allen_cahn"])
+def test_init_matches_oracle(problem):
+    d, w, N = 100, 110, 3
+    s = make(problem, d, w, N, 1.0, 64, kernel="simt", seed=5)
+    p = s.get_params()
+    ref = ob.init_params(5, d, w, N, zero_head=(problem == "allen_cahn"))
+    assert np.max(np.abs(p - ref)) <= 1e-6 * np.max(np.abs(ref))
+
+
+# ------------------------------------------------------------------ a2-a6 teacher-forced
+CASES = [
+    # (config, overrides)
+    ("cfg1_heat", dict()),
+    ("cfg2_hjb", dict(batch=1000)),
+    ("cfg3_allen_cahn", dict(batch=1000, precision="fp32")),
+    ("cfg4_hjb_multilevel", dict(batch=1000)),
+    ("cfg2_hjb", dict(batch=300, N=3, d=37, w=45)),       # odd sizes, ragged tiles
+]
+
+
+@pytest.mark.parametrize("cfg,over", CASES, ids=[c + str(sorted(o.items())) for c, o in CASES])
+@pytest.mark.parametrize("kernel", ["simt"])
+def test_teacher_forced_iteration(cfg, over, kernel):
+    wl = CONFIGS[cfg].with_(**over)
+    tol = TOL[wl.precision]
+    s = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr, precision=wl.precision,
+             kernel=kernel, seed=wl.seed)
+    # move away from the zero-bias init so every tensor has a gradient (smaller
+    # for Allen-Cahn, whose cubic driver explodes for a large Z, R7b)
+    p = s.get_params()
+    rng = np.random.default_rng(1)
+    scale = 0.003 if wl.problem == "allen_cahn" else 0.02
+    p[1:] += (scale * rng.standard_normal(p.size - 1)).astype(np.float32)
+    s.set_params(p)
+    for it in (0, 7):
+        s.iteration = it
+        loss = s.compute_grad()
+        g = s.get_grads()
+        ref = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, p, wl.seed, it,
+                               np.arange(wl.batch), wl.batch, kink_band=KINK_BAND[wl.precision])
+        assert np.isfinite(ref["loss"])
+        assert abs(loss - ref["loss"]) <= tol * ref["loss"], (loss, ref["loss"])
+        compare_grads(g, ref["grad"], wl.d, wl.w, wl.N, tol, ref["slack"])
+    # Adam (a8): the step recomputes the same gradient (same it) and applies Adam
+    loss2 = s.train_step()
+    assert loss2 == pytest.approx(loss, rel=1e-6)
+    st = ob.AdamState(p.size)
+    q = p.astype(np.float64)
+    ob.adam_step(q, g.astype(np.float64), st, wl.lr)
+    got = s.get_params()
+    assert np.max(np.abs(got - q)) <= 1e-5 * wl.lr + 1e-6 * np.max(np.abs(q))
+    m, v, t = s.get_adam_state()
+    assert t == 1 and np.allclose(m, st.m, rtol=1e-5, atol=1e-6 * np.abs(st.m).max())
+    assert s.iteration == 8
+
+
+def test_full_size_cfg2_gradient_and_sampled_residuals():
+    """Config 2 at its full batch (16384 paths, N = 20), launch as bench.py times it."""
+    wl = CONFIGS["cfg2_hjb"]
+    s = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr)
+    p = s.get_params()
+    loss = s.compute_grad()
+    ref = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, p, 0, 0, np.arange(wl.batch),
+                           wl.batch, kink_band=KINK_BAND["fp32"])
+    assert abs(loss - ref["loss"]) <= 1e-4 * ref["loss"]
+    compare_grads(s.get_grads(), ref["grad"], wl.d, wl.w, wl.N, 1e-4, ref["slack"])
+    idx = np.random.default_rng(3).choice(wl.batch, 64, replace=False)
+    R = np.array([s.debug_residuals(int(i), 1)[0] for i in idx])
+    assert np.allclose(R, ref["R"][idx], rtol=1e-4, atol=1e-4 * np.abs(ref["R"]).max())
+
+
+def test_heat_optimum_identity_on_gpu():
+    """Pin H1 on the device: at the exact optimum R = 2dT - 2Σ|ΔW|² per path."""
+    d, T, N, B = 10, 1.0, 5, 256
+    p, w = cf.heat_optimum_params(d, T, N)
+    s = make("heat", d, w, N, T, B, kernel="simt")
+    s.set_params(p.astype(np.float32))
+    loss = s.compute_grad()
+    R = s.debug_residuals(0, B)
+    S = sum(np.sum(s.debug_dw(0, n, 0, B).astype(np.float64) ** 2, 1) for n in range(N))
+    assert np.max(np.abs(R - (2 * d * T - 2 * S))) < 2e-4
+    assert abs(loss - np.mean(R.astype(np.float64) ** 2)) < 1e-4 * loss
+
+
+def test_cfg1_trajectory():
+    """Config 1 end to end: 200 Adam iterations through the C-ABI (CUDA graph
+    replay), teacher-forced parity at it = 50 and 199 and the free-running
+    trajectory against the oracle's own 200 iterations (R19)."""
+    wl = CONFIGS["cfg1_heat"]
+    s = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr)
+    p0 = s.get_params().astype(np.float64)
+    losses = []
+    for k in range(wl.iterations):
+        if k in (50, 199):
+            pk = s.get_params()
+            lk = s.compute_grad()
+            ref = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, pk, 0, k,
+                                   np.arange(wl.batch), wl.batch, kink_band=KINK_BAND["fp32"])
+            assert abs(lk - ref["loss"]) <= 1e-4 * ref["loss"]
+            compare_grads(s.get_grads(), ref["grad"], wl.d, wl.w, wl.N, 1e-4, ref["slack"])
+        losses.append(s.train_step())
+    po, _, lo = ob.train(ob.HEAT, wl.d, wl.w, wl.N, wl.T, p0.copy(), 0, wl.batch, wl.iterations,
+                         wl.lr)
+    assert abs(s.y0() - po[0]) <= 1e-3 * abs(po[0])
+    assert np.allclose(losses[:20], lo[:20], rtol=1e-4)
+    assert abs(np.mean(losses[-10:]) - np.mean(lo[-10:])) <= 1e-2 * np.mean(lo[-10:])
+
+
+# ------------------------------------------------------------------ a9, eval, guards
+@pytest.mark.parametrize("mode", ["copy", "interp"])
+def test_prolongate_matches_oracle(mode):
+    d, w, N = 6, 9, 5
+    s = make("hjb", d, w, N, 1.0, 64, kernel="simt", max_levels=2, prolong=mode)
+    s.train_step()
+    p = s.get_params()
+    s.prolongate(1)
+    q = s.get_params()
+    ref = ob.prolongate(p.astype(np.float64), d, w, N, ob.COPY if mode == "copy" else ob.INTERP)
+    assert s.N == 2 * N and q.size == ref.size
+    if mode == "copy":
+        assert np.array_equal(q, ref.astype(np.float32))
+    else:
+        assert np.allclose(q, ref, rtol=1e-6, atol=1e-7)
+    m, v, t = s.get_adam_state()
+    assert t == 0 and not m.any() and not v.any()
+    it = s.iteration
+    loss = s.compute_grad()
+    r = oracle_iteration("hjb", d, w, 2 * N, 1.0, q, 0, it, np.arange(64), 64)
+    assert abs(loss - r["loss"]) <= 1e-4 * r["loss"]
+    with pytest.raises(Exception):
+        s.prolongate(3)
+
+
+def test_eval_loss_matches_oracle():
+    d, w, N, T = 20, 24, 4, 0.3
+    s = make("allen_cahn", d, w, N, T, 128, kernel="simt")
+    p = s.get_params()
+    for eid, batch in ((0, 500), (3, 128)):
+        got = s.eval_loss(eid, batch)
+        ref = oracle_iteration("allen_cahn", d, w, N, T, p, 0, philox.EVAL_BIT | eid,
+                               np.arange(batch), batch, want_grad=False)
+        assert abs(got - ref["loss"]) <= 1e-5 * ref["loss"]
+
+
+def test_divergence_guard_skips_update():
+    from paper_1910_11623_b200 import BSDEError
+    s = make("heat", 4, 8, 2, 1.0, 64, kernel="simt")
+    p = s.get_params()
+    p[0] = 3e6          # loss ≈ 9e12 > 1e12
+    s.set_params(p)
+    with pytest.raises(BSDEError) as e:
+        s.train_step()
+    assert e.value.code == -4
+    assert np.array_equal(s.get_params(), p)
+
+
+def test_fake_world_shards_sum_to_full_batch():
+    """§8(e)/H10: rank r of G owns global paths [rB/G, (r+1)B/G); the shard
+    gradients (no collective) sum to the single-rank gradient."""
+    d, w, N, T, B = 12, 16, 4, 1.0, 512
+    full = make("hjb", d, w, N, T, B, kernel="simt")
+    lf = full.compute_grad()
+    gf = full.get_grads().astype(np.float64)
+    parts = [make("hjb", d, w, N, T, B, kernel="simt", rank=r, world=4) for r in range(4)]
+    ls = sum(pt.compute_grad() for pt in parts)
+    gs = sum(pt.get_grads().astype(np.float64) for pt in parts)
+    assert abs(ls - lf) <= 1e-6 * lf
+    assert np.linalg.norm(gs - gf) <= 1e-5 * np.linalg.norm(gf)
+
+
+def test_graph_replay_equals_eager():
+    a = make("allen_cahn", 16, 20, 4, 0.3, 300, kernel="simt", use_graph=True)
+    b = make("allen_cahn", 16, 20, 4, 0.3, 300, kernel="simt", use_graph=False)
+    la = [a.train_step() for _ in range(5)]
+    lb = [b.train_step() for _ in range(5)]
+    assert np.allclose(la, lb, rtol=1e-6)
+    assert np.allclose(a.get_params(), b.get_params(), rtol=1e-5, atol=1e-7)

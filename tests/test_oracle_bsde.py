@@ -266,3 +266,38 @@ def test_round_bf16_matches_torch():
     x = np.random.default_rng(0).standard_normal(10000) * 10.0 ** np.random.default_rng(1).integers(-5, 5, 10000)
     ref = torch.tensor(x, dtype=torch.float32).to(torch.bfloat16).to(torch.float64).numpy()
     assert np.array_equal(bsde.round_bf16(x), ref)
+
+
+def test_zero_head_init_keeps_allen_cahn_bounded():
+    """R7b: with a Xavier head the Allen-Cahn rollout explodes at config-3 sizes
+    (Y leaves [-1, 1] and the cubic driver diverges); with W3 = 0 (Z ≡ 0) Y_n
+    follows the bounded scalar ODE map."""
+    d, w, N, T, B = 100, 110, 20, 0.3, 256
+    with np.errstate(all="ignore"):
+        bad = bsde.iteration(bsde.ALLEN_CAHN, d, w, N, T, bsde.init_params(0, d, w, N), 0, 0,
+                             np.arange(B), B, want_grad=False)
+    assert not np.isfinite(bad["loss"]) or bad["loss"] > 1e6
+    p = bsde.init_params(0, d, w, N, zero_head=True)
+    _, nets = bsde.unpack(p, d, w, N)
+    assert all(not net["W3"].any() for net in nets) and nets[1]["W1"].any()
+    r = bsde.iteration(bsde.ALLEN_CAHN, d, w, N, T, p, 0, 0, np.arange(B), B)
+    assert np.isfinite(r["loss"]) and r["loss"] < 1.0 and np.all(np.isfinite(r["grad"]))
+
+
+def test_kink_slack_bounds_mask_flips():
+    """The slack returned with kink_band bounds the gradient change when every
+    pre-activation inside the band flips its ReLU mask (emulated by evaluating
+    the backward masks as 1[A > shift])."""
+    d, w, N, T, B = 6, 10, 3, 1.0, 64
+    p = bsde.init_params(4, d, w, N)
+    p[1:] += 0.05 * np.random.default_rng(0).standard_normal(p.size - 1)
+    for problem in (bsde.HJB, bsde.ALLEN_CAHN):
+        base = bsde.iteration(problem, d, w, N, T, p, 0, 0, np.arange(B), B, kink_band=0.05,
+                              keep=True)
+        shifted = bsde.iteration(problem, d, w, N, T, p, 0, 0, np.arange(B), B, mask_shift=0.002)
+        flipped = sum(int(np.sum((A > 0) & (A <= 0.002))) for t in base["trace"]
+                      for A in (t[2], t[4]))
+        assert flipped > 0
+        diff = np.abs(shifted["grad"] - base["grad"])
+        assert diff.max() > 0                           # the flips did change the gradient
+        assert np.all(diff <= base["slack"] * 1.05 + 1e-12)

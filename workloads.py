@@ -1,0 +1,44 @@
+"""The five BASELINE.json configurations as plain data (no arithmetic of the method).
+
+Shared by tests/ and bench.py; neither the oracle nor the product imports it.
+"""
+from dataclasses import dataclass, replace
+from typing import Optional, Tuple
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    problem: str          # "heat" | "hjb" | "allen_cahn"
+    d: int
+    w: int
+    N: int
+    T: float
+    batch: int            # global paths per iteration
+    precision: str        # "fp32" | "bf16"
+    lr: float
+    iterations: int
+    seed: int = 0
+    levels: Optional[Tuple[int, ...]] = None     # multilevel grids (config 4)
+    iters_per_level: int = 0
+
+    def with_(self, **kw):
+        return replace(self, **kw)
+
+
+CONFIGS = {
+    # BASELINE.json configs[0]: heat BSDE, closed form u(0,0) = 2dT = 20
+    "cfg1_heat": Workload("cfg1_heat", "heat", 10, 20, 5, 1.0, 256, "fp32", 1e-2, 200),
+    # configs[1]: HJB / LQ control, Cole-Hopf check
+    "cfg2_hjb": Workload("cfg2_hjb", "hjb", 100, 110, 20, 1.0, 16384, "fp32", 1e-2, 2000),
+    # configs[2]: Allen-Cahn, bf16 operands / fp32 accumulate
+    "cfg3_allen_cahn": Workload("cfg3_allen_cahn", "allen_cahn", 100, 110, 20, 0.3, 65536,
+                                "bf16", 5e-4, 4000),
+    # configs[3]: multilevel HJB, N = 5 -> 80, fixed budget per level (400)
+    "cfg4_hjb_multilevel": Workload("cfg4_hjb_multilevel", "hjb", 100, 110, 5, 1.0, 65536,
+                                    "fp32", 1e-2, 2000, levels=(5, 10, 20, 40, 80),
+                                    iters_per_level=400),
+    # configs[4]: scale-out Allen-Cahn, 524288 paths sharded over 1/2/4/8 GPUs
+    "cfg5_allen_cahn_scaleout": Workload("cfg5_allen_cahn_scaleout", "allen_cahn", 100, 110, 80,
+                                         0.3, 524288, "bf16", 5e-4, 1000),
+}
