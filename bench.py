@@ -234,11 +234,7 @@ def main():
     value = path_steps / (ms * 1e-3)
 
     # per-phase CUDA-event timing of the same step (eager replay of the step)
-    ph = np.zeros(6, np.float32)
-    import ctypes
-    s._ck(s._L.bsde_profile_steps(s._h, max(2, min(args.steps, 5)),
-                                  ph.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), 6))
-    phase = dict(zip(["begin", "fwd", "bwd", "allreduce", "check", "adam"], ph.tolist()))
+    phase = s.profile_steps(max(2, min(args.steps, 5)))
 
     # e2e: the public API call per step with the loss read back to the host
     barrier()

@@ -172,6 +172,13 @@ int bsde_debug_dw(const bsde_ctx* ctx, int64_t it, int n, int64_t m0, int64_t co
  * sampled full-size parity (R19).  host_out[count] fp32.  Synchronises. */
 int bsde_debug_residuals(const bsde_ctx* ctx, int64_t m0, int64_t count, float* host_out);
 
+/* Test hook for the tcgen05 operand layouts: one
+ * M=128, N=112 bf16 UMMA on the current device with fp32 host inputs rounded to
+ * bf16.  mode 0: D[128×112] = A[128×112]·B[112×112]ᵀ (both K-major);
+ * mode 1: D = A[128×112]·B[112×112] (B MN-major); mode 2: D = A[128×112]ᵀ·B[128×112]
+ * (both MN-major, rows >= 112 of D undefined).  Row-major host arrays.  Synchronises. */
+int bsde_debug_umma(int mode, const float* a, const float* b, float* d_out);
+
 /* Profiling hook for the bench's roofline figures: runs `steps` training
  * iterations (eagerly, no graph) with CUDA events recorded on cfg.stream
  * between the phases of the step and returns the mean duration of each phase

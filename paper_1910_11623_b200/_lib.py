@@ -23,8 +23,9 @@ SYMBOLS = [
     "bsde_num_params", "bsde_get_params", "bsde_set_params", "bsde_get_grads",
     "bsde_get_adam_state", "bsde_set_adam_state", "bsde_get_iteration", "bsde_set_iteration",
     "bsde_current_steps", "bsde_compute_grad", "bsde_eval_loss", "bsde_debug_philox",
-    "bsde_debug_dw", "bsde_debug_residuals", "bsde_launches_per_step", "bsde_kernel_family", "bsde_nccl_unique_id",
-    "bsde_last_error", "bsde_destroy",
+    "bsde_debug_dw", "bsde_debug_residuals", "bsde_debug_umma", "bsde_profile_steps",
+    "bsde_launches_per_step", "bsde_kernel_family", "bsde_nccl_unique_id", "bsde_last_error",
+    "bsde_destroy",
 ]
 
 
@@ -87,6 +88,8 @@ def lib():
             "bsde_debug_philox": (I32, [P, pU32, pU32, I64, pU32]),
             "bsde_debug_dw": (I32, [P, I64, I32, I64, I64, pF]),
             "bsde_debug_residuals": (I32, [P, I64, I64, pF]),
+            "bsde_debug_umma": (I32, [I32, pF, pF, pF]),
+            "bsde_profile_steps": (I32, [P, I32, pF, I32]),
             "bsde_launches_per_step": (I32, [P, ctypes.POINTER(I32)]),
             "bsde_kernel_family": (ctypes.c_char_p, [P]),
             "bsde_nccl_unique_id": (I32, [P]),

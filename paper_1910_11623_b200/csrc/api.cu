@@ -23,6 +23,8 @@ cudaError_t launch_bwd_tc(const PassArgs& a, cudaStream_t s);
 cudaError_t launch_pack_weights(const PassArgs& a, cudaStream_t s);
 size_t tc_pack_bytes(int d, int w, int N, int precision);
 size_t tc_partial_bytes(int d, int w, int precision);
+size_t tc_xstore_bytes(int d, int w, int N, int64_t B_local);
+cudaError_t launch_umma_test(int mode, const float* A, const float* B, float* D, cudaStream_t s);
 }  // namespace bsde
 
 using namespace bsde;
@@ -143,7 +145,7 @@ PassArgs pass_args(bsde_ctx* c) {
   a.state = c->state;
   a.loss_acc = &c->state->loss_sum;
   a.wpack = c->wpack;
-  a.xpack = c->xpack;
+  a.xpack = c->Xstore;   // the tcgen05 path stores X_n as bf16 operand images
   a.gpart = c->gpart;
   a.precision = c->cfg.precision;
   return a;
@@ -292,10 +294,16 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
       !(cfg.eps > 0))
     return fail(none, BSDE_EINVAL, "Adam hyper-parameters out of range");
   int family = cfg.kernel;
-  if (family == BSDE_KERNEL_AUTO) family = tc_supported(d, w) ? BSDE_KERNEL_TC : BSDE_KERNEL_SIMT;
+  if (family == BSDE_KERNEL_AUTO)
+    family = (cfg.precision == BSDE_BF16 && tc_supported(d, w)) ? BSDE_KERNEL_TC : BSDE_KERNEL_SIMT;
   if (family == BSDE_KERNEL_TC && !tc_supported(d, w))
-    return fail(none, BSDE_EINVAL, "tcgen05 kernels need d+1 <= 128 and w+1 <= 128 (d=%d w=%d)",
+    return fail(none, BSDE_EINVAL,
+                "no tcgen05 instantiation for d=%d w=%d (built: 100/110, 10/20, 37/45; d+1, w+1 <= 128)",
                 d, w);
+  if (family == BSDE_KERNEL_TC && cfg.precision != BSDE_BF16)
+    return fail(none, BSDE_EINVAL,
+                "the tcgen05 kernels compute with bf16 operands; fp32-accurate precision runs on "
+                "kernel=SIMT");
   if (family == BSDE_KERNEL_SIMT && cfg.precision == BSDE_BF16)
     return fail(none, BSDE_EINVAL, "bf16 operands need the tcgen05 kernels (kernel=SIMT given)");
   if (family == BSDE_KERNEL_SIMT && simt_max_smem(d, w) > 227 * 1024)
@@ -338,7 +346,10 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
   }
   const int64_t npmax = num_params_at(ctx, ctx->N_max);
   struct Alloc { void** p; size_t bytes; };
-  const size_t xs = (size_t)ctx->N_max * ctx->B_local * d * sizeof(float);
+  // X_n store for the adjoint: fp32 rows (SIMT) or bf16 operand images (tcgen05)
+  const size_t xs = family == BSDE_KERNEL_TC
+                        ? tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)
+                        : (size_t)ctx->N_max * ctx->B_local * d * sizeof(float);
   std::vector<Alloc> allocs = {
       {(void**)&ctx->params, npmax * sizeof(float)},
       {(void**)&ctx->grad, npmax * sizeof(float)},
@@ -687,3 +698,22 @@ void bsde_destroy(bsde_ctx* ctx) {
 }
 
 }  // extern "C"
+
+extern "C" int bsde_debug_umma(int mode, const float* a, const float* b, float* d_out) {
+  bsde_ctx* ctx = nullptr;
+  if (mode < 0 || mode > 2 || !a || !b || !d_out) return fail(ctx, BSDE_EINVAL, "debug_umma: bad argument");
+  const size_t na = 128 * 112, nb = (mode == 2 ? 128 : 112) * 112, nd = 128 * 112;
+  float *da = nullptr, *db = nullptr, *dd = nullptr;
+  CK(cudaMalloc(&da, na * 4));
+  CK(cudaMalloc(&db, nb * 4));
+  CK(cudaMalloc(&dd, nd * 4));
+  CK(cudaMemcpy(da, a, na * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(db, b, nb * 4, cudaMemcpyHostToDevice));
+  CK(launch_umma_test(mode, da, db, dd, 0));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(d_out, dd, nd * 4, cudaMemcpyDeviceToHost));
+  cudaFree(da);
+  cudaFree(db);
+  cudaFree(dd);
+  return BSDE_OK;
+}

@@ -29,6 +29,17 @@ def nccl_unique_id():
     return buf.raw
 
 
+def debug_umma(mode, a, b):
+    """One bf16 tcgen05 MMA (M=128, N=112) in the given operand-major mode."""
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    out = np.empty((128, 112), np.float32)
+    rc = _lib.lib().bsde_debug_umma(int(mode), _fptr(a), _fptr(b), _fptr(out))
+    if rc:
+        raise BSDEError(rc, _lib.lib().bsde_last_error(None).decode())
+    return out
+
+
 def step_size(d, w):
     return 2 * d * w + w * w + 2 * w + d
 
@@ -200,6 +211,14 @@ class BSDE:
         out = np.empty((count, self.d), np.float32)
         self._ck(self._L.bsde_debug_dw(self._h, int(it), int(n), int(m0), int(count), _fptr(out)))
         return out
+
+    PHASES = ("begin", "fwd", "bwd", "allreduce", "check", "adam")
+
+    def profile_steps(self, steps):
+        """Mean per-phase milliseconds over `steps` eager iterations (CUDA events)."""
+        out = np.zeros(6, np.float32)
+        self._ck(self._L.bsde_profile_steps(self._h, int(steps), _fptr(out), 6))
+        return dict(zip(self.PHASES, out.tolist()))
 
     def debug_residuals(self, m0, count):
         out = np.empty(count, np.float32)

@@ -94,9 +94,11 @@ def test_teacher_forced_iteration(cfg, over, kernel):
     # Adam (a8): the step recomputes the same gradient (same it) and applies Adam
     loss2 = s.train_step()
     assert loss2 == pytest.approx(loss, rel=1e-6)
+    g2 = s.get_grads()          # the gradient this step used (atomic order may differ)
+    assert np.linalg.norm(g2 - g) <= 1e-5 * np.linalg.norm(g)
     st = ob.AdamState(p.size)
     q = p.astype(np.float64)
-    ob.adam_step(q, g.astype(np.float64), st, wl.lr)
+    ob.adam_step(q, g2.astype(np.float64), st, wl.lr)
     got = s.get_params()
     assert np.max(np.abs(got - q)) <= 1e-5 * wl.lr + 1e-6 * np.max(np.abs(q))
     m, v, t = s.get_adam_state()

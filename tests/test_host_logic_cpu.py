@@ -1,0 +1,132 @@
+"""CPU tests of the host-side logic around the kernels (no GPU):
+
+* data parallelism (§8(e)): world_size-2 `gloo` processes, each owning the
+  global paths [rB/G, (r+1)B/G) exactly as bsde_create assigns them, summing
+  gradient and Σ R² with an allreduce and running replicated Adam — parameters
+  stay bitwise identical across ranks and equal single-process training;
+* the multilevel schedule driver (paper_1910_11623_b200.multilevel) driving an
+  oracle-backed stand-in of the BSDE object reproduces the oracle's own
+  multilevel training, and detects time-to-target only on the final grid.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import bsde as ob
+
+D, W, N, T, B = 4, 6, 3, 1.0, 32
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _dp_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % port, rank=rank,
+                            world_size=world)
+    B_local = B // world
+    shard = np.arange(rank * B_local, (rank + 1) * B_local)     # bsde_create's m0 = rank·B/world
+    p = ob.init_params(0, D, W, N)
+    st = ob.AdamState(p.size)
+    losses = []
+    for it in range(4):
+        r = ob.iteration(ob.HJB, D, W, N, T, p, 0, it, shard, B)
+        g = torch.from_numpy(r["grad"].copy())
+        L = torch.tensor([r["loss_sum"]], dtype=torch.float64)
+        dist.all_reduce(g)
+        dist.all_reduce(L)
+        loss = L.item() / B
+        ob.adam_step(p, g.numpy(), st, 1e-2, loss=loss)
+        losses.append(loss)
+    q.put((rank, p, losses))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_data_parallel_gloo_world2():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = dict((r, (p, l)) for r, p, l in (q.get(timeout=120) for _ in procs))
+    for pr in procs:
+        pr.join(60)
+        assert pr.exitcode == 0
+    p0, l0 = out[0]
+    p1, l1 = out[1]
+    assert np.array_equal(p0, p1) and l0 == l1                  # replicated state
+    ref, _, lref = ob.train(ob.HJB, D, W, N, T, ob.init_params(0, D, W, N), 0, B, 4, 1e-2)
+    assert np.allclose(l0, lref, rtol=1e-12)
+    assert np.allclose(p0, ref, rtol=1e-10, atol=1e-13)
+
+
+class OracleSolver:
+    """Stand-in with the BSDE object's interface, backed by the oracle (test only)."""
+
+    def __init__(self, problem, d, w, N, T, batch, lr, seed=0, mode=ob.COPY):
+        self.problem, self.d, self.w, self.N, self.T = problem, d, w, N, T
+        self.batch, self.lr, self.seed, self.mode = batch, lr, seed, mode
+        self.p = ob.init_params(seed, d, w, N)
+        self.st = ob.AdamState(self.p.size)
+        self.iteration = 0
+        self.stream = None
+        self.level = 0
+
+    def train_step(self, sync=True):
+        r = ob.loss_and_grad(self.problem, self.d, self.w, self.N, self.T, self.p, self.seed,
+                             self.iteration, self.batch)
+        ob.adam_step(self.p, r["grad"], self.st, self.lr, loss=r["loss"])
+        self.iteration += 1
+        return r["loss"]
+
+    def eval_loss(self, eval_id=0, batch=None):
+        from oracle import philox
+        b = batch or self.batch
+        return ob.iteration(self.problem, self.d, self.w, self.N, self.T, self.p, self.seed,
+                            philox.EVAL_BIT | eval_id, np.arange(b), b, want_grad=False)["loss"]
+
+    def prolongate(self, level):
+        assert level == self.level + 1
+        self.p = ob.prolongate(self.p, self.d, self.w, self.N, self.mode)
+        self.N *= 2
+        self.level = level
+        self.st = ob.AdamState(self.p.size)      # R14: Adam state reset
+
+    def y0(self):
+        return float(self.p[0])
+
+
+def test_multilevel_driver_reproduces_oracle_schedule():
+    from paper_1910_11623_b200.multilevel import run_schedule
+    s = OracleSolver(ob.HJB, D, W, 2, T, 16, 1e-2)
+    res = run_schedule(s, [3, 3, 2], eval_every=0)
+    assert [r.N for r in res.records] == [2] * 3 + [4] * 3 + [8] * 2
+    assert [r.iteration for r in res.records] == list(range(1, 9))
+    p_ref, hist = ob.train_multilevel(ob.HJB, D, W, [2, 4, 8], T, ob.init_params(0, D, W, 2),
+                                      0, 16, [3, 3, 2], 1e-2)
+    assert np.allclose([r.train_loss for r in res.records], [h[2] for h in hist], rtol=1e-13)
+    assert np.allclose(s.p, p_ref, rtol=1e-13)
+    assert len(res.y0_per_level) == 3
+
+
+def test_multilevel_time_to_target_only_on_final_grid():
+    from paper_1910_11623_b200.multilevel import run_schedule
+    ticks = iter(np.arange(0.0, 1000.0, 0.5))
+    s = OracleSolver(ob.HEAT, D, W, 2, T, 16, 1e-2)
+    res = run_schedule(s, [2, 2], eval_every=1, target_loss=1e9, final_N=4, extend_last=5,
+                       clock=lambda: next(ticks))
+    # the target (trivially met) is first recorded on the N = 4 grid, after 3 timed steps
+    assert res.iteration_at_target == 3
+    assert res.time_to_target == pytest.approx(1.5)
+    assert res.records[-1].N == 4 and len(res.records) == 4
