@@ -167,6 +167,10 @@ int bsde_debug_philox(const bsde_ctx* ctx, const uint32_t* ctr, const uint32_t k
                       int64_t count, uint32_t* out);
 int bsde_debug_dw(const bsde_ctx* ctx, int64_t it, int n, int64_t m0, int64_t count,
                   float* host_out);
+/* As bsde_debug_dw, with the MUFU-based Box-Muller the tcgen05 kernels use
+ * (same counter and map, R8; |error| ~ 1e-6 relative to the exact map). */
+int bsde_debug_dw_fast(const bsde_ctx* ctx, int64_t it, int n, int64_t m0, int64_t count,
+                       float* host_out);
 /* Terminal residuals R^m = Y_N^m - g(X_N^m) of the last training forward pass
  * for this rank's local paths [m0, m0+count) (global path rank·B/world + m):
  * sampled full-size parity (R19).  host_out[count] fp32.  Synchronises. */

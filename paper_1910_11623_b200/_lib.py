@@ -23,7 +23,7 @@ SYMBOLS = [
     "bsde_num_params", "bsde_get_params", "bsde_set_params", "bsde_get_grads",
     "bsde_get_adam_state", "bsde_set_adam_state", "bsde_get_iteration", "bsde_set_iteration",
     "bsde_current_steps", "bsde_compute_grad", "bsde_eval_loss", "bsde_debug_philox",
-    "bsde_debug_dw", "bsde_debug_residuals", "bsde_debug_umma", "bsde_profile_steps",
+    "bsde_debug_dw", "bsde_debug_dw_fast", "bsde_debug_residuals", "bsde_debug_umma", "bsde_profile_steps",
     "bsde_launches_per_step", "bsde_kernel_family", "bsde_nccl_unique_id", "bsde_last_error",
     "bsde_destroy",
 ]
@@ -87,6 +87,7 @@ def lib():
             "bsde_eval_loss": (I32, [P, ctypes.c_uint32, I64, pD]),
             "bsde_debug_philox": (I32, [P, pU32, pU32, I64, pU32]),
             "bsde_debug_dw": (I32, [P, I64, I32, I64, I64, pF]),
+            "bsde_debug_dw_fast": (I32, [P, I64, I32, I64, I64, pF]),
             "bsde_debug_residuals": (I32, [P, I64, I64, pF]),
             "bsde_debug_umma": (I32, [I32, pF, pF, pF]),
             "bsde_profile_steps": (I32, [P, I32, pF, I32]),

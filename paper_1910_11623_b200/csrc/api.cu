@@ -25,6 +25,9 @@ size_t tc_pack_bytes(int d, int w, int N, int precision);
 size_t tc_partial_bytes(int d, int w, int precision);
 size_t tc_xstore_bytes(int d, int w, int N, int64_t B_local);
 cudaError_t launch_umma_test(int mode, const float* A, const float* B, float* D, cudaStream_t s);
+cudaError_t launch_debug_dw_fast(uint32_t it, int n, int64_t m0, int64_t count, int d,
+                                 float sqrt_dt, uint32_t k0, uint32_t k1, float* out,
+                                 cudaStream_t s);
 }  // namespace bsde
 
 using namespace bsde;
@@ -624,20 +627,32 @@ int bsde_debug_philox(const bsde_ctx* c, const uint32_t* ctr, const uint32_t key
   return BSDE_OK;
 }
 
-int bsde_debug_dw(const bsde_ctx* c, int64_t it, int n, int64_t m0, int64_t count,
-                  float* host_out) {
-  bsde_ctx* ctx = const_cast<bsde_ctx*>(c);
+static int debug_dw_impl(bsde_ctx* ctx, int64_t it, int n, int64_t m0, int64_t count,
+                         float* host_out, bool fast) {
   if (!ctx || !host_out || count < 1 || n < 0) return fail(ctx, BSDE_EINVAL, "bad argument");
   float* d_out = nullptr;
   const size_t bytes = (size_t)count * ctx->d * sizeof(float);
   CK(cudaMallocAsync((void**)&d_out, bytes, ctx->stream));
-  CK(launch_debug_dw((uint32_t)it, n, m0, count, ctx->d, (float)std::sqrt(ctx->T / ctx->N),
-                     (uint32_t)(ctx->cfg.seed & 0xffffffffu), (uint32_t)(ctx->cfg.seed >> 32),
-                     d_out, ctx->stream));
+  const float sdt = (float)std::sqrt(ctx->T / ctx->N);
+  const uint32_t k0 = (uint32_t)(ctx->cfg.seed & 0xffffffffu), k1 = (uint32_t)(ctx->cfg.seed >> 32);
+  if (fast)
+    CK(launch_debug_dw_fast((uint32_t)it, n, m0, count, ctx->d, sdt, k0, k1, d_out, ctx->stream));
+  else
+    CK(launch_debug_dw((uint32_t)it, n, m0, count, ctx->d, sdt, k0, k1, d_out, ctx->stream));
   CK(cudaMemcpyAsync(host_out, d_out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaFreeAsync(d_out, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return BSDE_OK;
+}
+
+int bsde_debug_dw(const bsde_ctx* c, int64_t it, int n, int64_t m0, int64_t count,
+                  float* host_out) {
+  return debug_dw_impl(const_cast<bsde_ctx*>(c), it, n, m0, count, host_out, false);
+}
+
+int bsde_debug_dw_fast(const bsde_ctx* c, int64_t it, int n, int64_t m0, int64_t count,
+                       float* host_out) {
+  return debug_dw_impl(const_cast<bsde_ctx*>(c), it, n, m0, count, host_out, true);
 }
 
 int bsde_debug_residuals(const bsde_ctx* c, int64_t m0, int64_t count, float* host_out) {

@@ -58,6 +58,52 @@ __device__ __forceinline__ float4 normals4(uint32_t q, uint32_t m, uint32_t n, u
   return z;
 }
 
+// ---- fast Box-Muller for the tensor-core kernels (same map as R8) ----------
+// u = ((x >> 9) + 1/2) 2^-23 via the exponent trick (exact): 1.m - (1 - 2^-24).
+__device__ __forceinline__ float unit_fast(uint32_t x) {
+  return __int_as_float((int)((x >> 9) | 0x3F800000u)) - 0.99999994039535522f;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// √Δt·(r cos 2πu2, r sin 2πu2), r = sqrt(-2 ln u1), with MUFU lg2 / sqrt / sin / cos.
+// ln u1 for u1 > 1 - 2^-6 uses the series of log1p(-v), v = 1 - u1 (exact), so
+// the relative accuracy of r holds near u1 = 1 where lg2.approx's absolute
+// error would dominate.  The angle is reduced to (-π, π): 2πu2 - π, so
+// cos(2πu2) = -cos(a), sin(2πu2) = -sin(a).  Typical |error| ~ 1e-6 (pinned by
+// tests/test_gpu_tc.py::test_fast_normals_match_oracle).
+__device__ __forceinline__ void box_muller_fast(uint32_t xa, uint32_t xb, float sdt, float& z0,
+                                                float& z1) {
+  const uint32_t k = xa >> 9;
+  float r2;   // -2 ln(u1)
+  if (k >= 0x7E0000u) {   // u1 > 1 - 2^-6
+    const float v = (float)(0x7FFFFFu - k) * 1.1920928955078125e-07f + 5.9604644775390625e-08f;
+    r2 = 2.0f * v * fmaf(v, fmaf(v, fmaf(v, 0.25f, 0.33333333f), 0.5f), 1.0f);
+  } else {
+    float l2;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(unit_fast(xa)));
+    r2 = -1.38629436111989061f * l2;   // -2 ln 2 · log2(u1)
+  }
+  const float r = sqrt_approx(r2) * sdt;
+  const float a = fmaf(unit_fast(xb), 6.28318530717958648f, -3.14159265358979324f);
+  float s, c;
+  __sincosf(a, &s, &c);
+  z0 = -r * c;
+  z1 = -r * s;
+}
+
+// √Δt · normals 4q..4q+3 of (m, n, it): the increments ΔW of R8, fast map.
+__device__ __forceinline__ float4 dw4_fast(uint32_t q, uint32_t m, uint32_t n, uint32_t it,
+                                           uint32_t k0, uint32_t k1, float sdt) {
+  const uint4 x = philox4x32_10(make_uint4(q, m, n, it), k0, k1);
+  float4 z;
+  box_muller_fast(x.x, x.y, sdt, z.x, z.y);
+  box_muller_fast(x.z, x.w, sdt, z.z, z.w);
+  return z;
+}
+
 // ---- problems (R2, R10-R13) ------------------------------------------------
 // f(y, z) given |z|²; ∂f/∂y; the scalar c with ∂f/∂z = c·z; g(s = |x|²).
 __device__ __forceinline__ float driver_f(int problem, float y, float zz, float lam) {

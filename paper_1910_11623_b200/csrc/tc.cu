@@ -1,212 +1,37 @@
 // tc.cu — tcgen05 (sm_100a) forward and adjoint kernels: bf16 operands in shared
-// memory, fp32 accumulators in tensor memory (TMEM), one CTA per SM.
+// memory, fp32 accumulators in tensor memory (TMEM), one CTA of 512 threads per SM.
 //
-// Data flow (DESIGN.md §Kernels):
-//  k_pack_tc  fp32 master θ -> per-step bf16 operand images  W̃1 [Wp×Dp], W̃2 [Wp×Wp],
+// Thread layout: warp w accesses TMEM lanes 32·(w%4)..+31, so a 128-path tile is
+// one path per lane and four threads per path; thread group g = w/4 owns the
+// 8-column chunks g, g+4, g+8, g+12 of every 112-column accumulator / operand
+// image (loads: 4 × tcgen05.ld.32x32b.x8 and one wait).
+//
+// Data flow (DESIGN.md §6):
+//  k_pack_tc  fp32 master θ -> per-step bf16 operand images W̃1 [Wp×Dp], W̃2 [Wp×Wp],
 //             W̃3 [Dp×Wp] with the biases folded into a constant-1 column
-//             (W̃1 row w = e_d makes H1[w] = 1, W̃2/W̃3 take b2/b3 in column w).
-//  k_fwd_tc   tile-major: one 128-path tile (one path per thread = per TMEM lane)
-//             walks all N steps: a1 Philox ΔW, a2 Euler X (fp32, in registers),
-//             a3 the three GEMMs on tcgen05 (weights double-buffered by bulk
-//             copy), a4 Y update, a5 terminal loss; stores each X_n operand image
-//             (bf16, bulk copy smem->global) for the adjoint pass.
+//             (W̃1 row w = e_d makes H1[w] = 1; W̃2/W̃3 take b2/b3 in column w).
+//  k_fwd_tc   tile-major: one 128-path tile walks all N steps: a1 Philox ΔW (computed
+//             while the step's GEMMs run), a2 Euler X (fp32 registers), a3 three
+//             tcgen05 GEMMs (weights double-buffered by bulk copy), a4 Y update, a5
+//             terminal loss; each X_n operand image is bulk-copied to HBM for the
+//             adjoint pass.
 //  k_bwd_tc   step-major: each CTA owns a contiguous range of (n, tile) items,
 //             recomputes the step-n net, forms dZ_n = ā_{n+1}(ΔW_n - Δt ∂_z f),
-//             back-propagates with 2 input-gradient GEMMs, and accumulates the 3
-//             weight-gradient GEMMs (contracting over paths, MN-major operands)
-//             in TMEM across the range; one flush of fp32 atomics per step change.
-//
-// Operand images: a [R×C] bf16 matrix in the canonical no-swizzle UMMA layout,
-// 8x8 core matrices: byte offset(r, c) = (r/8)·(C·16) + (c/8)·128 + (r%8)·16 + (c%8)·2.
-// As a K-major operand (rows = M|N, cols = K): LBO = 128, SBO = C·16.
-// As an MN-major operand (cols = M|N, rows = K): LBO = C·16, SBO = 128.
+//             back-propagates with 2 input-gradient GEMMs and accumulates the 3
+//             weight-gradient GEMMs (contracting over paths, MN-major operands) in
+//             TMEM across its range; one flush of fp32 atomics per step change.
 //
 // Citations: Eq. 5, Eq. 7, Eq. 6.
-#include <cuda_bf16.h>
-
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace bsde {
 namespace tc {
 
-// ------------------------------------------------------------------ PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\t"
-      "bra LAB_WAIT;\n"
-      "DONE:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-               "r"(smem_u32(src)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                   smem_u32(slot)),
-               "r"(ncols)
-               : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
-               : "memory");
-}
-__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-// 16 consecutive fp32 columns of the calling thread's TMEM lane (32x32b shape).
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
-      "tcgen05.wait::ld.sync.aligned;"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr)
-      : "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// ------------------------------------------------------------------ descriptors
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);   // version 1, no swizzle
-}
-// kind::f16 instruction descriptor: D fp32, A/B bf16, majors, N>>3, M>>4.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-// An operand view of an image in shared memory.
-struct Opnd {
-  uint32_t base, lbo, sbo, kstep;
-};
-// image [R×C] used K-major (rows = M|N, K = C)
-__device__ __forceinline__ Opnd kmaj(const void* img, int C) {
-  return Opnd{smem_u32(img), 128u, (uint32_t)C * 16u, 256u};
-}
-// image [R×C] used MN-major (M|N = C, K = R)
-__device__ __forceinline__ Opnd mnmaj(const void* img, int C) {
-  return Opnd{smem_u32(img), (uint32_t)C * 16u, 128u, (uint32_t)C * 32u};
-}
-// D (+)= A·B over ksteps×16 of K; single thread.
-__device__ __forceinline__ void gemm(uint32_t d_tmem, Opnd A, Opnd B, int ksteps, uint32_t idesc,
-                                     bool accumulate) {
-  for (int k = 0; k < ksteps; ++k)
-    mma_bf16(d_tmem, sdesc(A.base + k * A.kstep, A.lbo, A.sbo),
-             sdesc(B.base + k * B.kstep, B.lbo, B.sbo), idesc, (k > 0 || accumulate) ? 1u : 0u);
-}
-
-__host__ __device__ constexpr int pad16(int x) { return (x + 15) / 16 * 16; }
-
-template <int D, int W>
-struct Dims {
-  static constexpr int Dp = pad16(D + 1);    // + constant-1 column (folded bias)
-  static constexpr int Wp = pad16(W + 1);
-  static constexpr int KM = Dp > Wp ? Dp : Wp;
-  static constexpr uint32_t W1B = Wp * Dp * 2, W2B = Wp * Wp * 2, W3B = Dp * Wp * 2;
-  static constexpr uint32_t WB = W1B + W2B + W3B;          // one step's weight images
-  static constexpr uint32_t XB = 128u * Dp * 2;            // X operand image of one tile
-  // activation buffer; an M=128 MN-major operand over a C-column image reads
-  // (128 - C)/8 core-matrix columns past each row group (garbage rows of D that
-  // are never read), so pad by that much plus slack.
-  static constexpr int CMIN = Dp < Wp ? Dp : Wp;
-  static constexpr uint32_t ACT = 128u * KM * 2 + (128 - CMIN) / 8 * 128 + 256;
-  static_assert(Dp <= 128 && Wp <= 128, "tcgen05 tiles need d+1 <= 128 and w+1 <= 128");
-};
-
-// byte offset of element (r, c) in an image with C columns
-__device__ __forceinline__ uint32_t img_off(int r, int c, int C) {
-  return (uint32_t)((r >> 3) * (C * 16) + (c >> 3) * 128 + (r & 7) * 16 + (c & 7) * 2);
-}
-__device__ __forceinline__ uint32_t pack2(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-// 8 consecutive columns [8c, 8c+8) of row `row`
-__device__ __forceinline__ void st_chunk(uint8_t* img, int row, int chunk, int C, const float* v) {
-  uint4 u;
-  u.x = pack2(v[0], v[1]);
-  u.y = pack2(v[2], v[3]);
-  u.z = pack2(v[4], v[5]);
-  u.w = pack2(v[6], v[7]);
-  *reinterpret_cast<uint4*>(img + (row >> 3) * (C * 16) + chunk * 128 + (row & 7) * 16) = u;
-}
-__device__ __forceinline__ void ld_chunk(const uint8_t* img, int row, int chunk, int C, float* v) {
-  const uint4 u =
-      *reinterpret_cast<const uint4*>(img + (row >> 3) * (C * 16) + chunk * 128 + (row & 7) * 16);
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    v[2 * i] = __uint_as_float(w[i] << 16);
-    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
-  }
-}
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+constexpr int NTH = 512;   // threads per CTA (4 per path)
+constexpr float kSqrt2 = 1.41421356237309515f;
 
 // ------------------------------------------------------------------ weight packing
-// One thread per (step n, matrix, row, 8-column chunk): 16 bytes of the image.
 template <int D, int W>
 __global__ void k_pack_tc(const float* __restrict__ params, uint8_t* __restrict__ out, int N) {
   using Dm = Dims<D, W>;
@@ -257,9 +82,28 @@ __global__ void k_pack_tc(const float* __restrict__ params, uint8_t* __restrict_
   }
 }
 
+// ΔW_n at this thread's columns: dw[8i + e] = ΔW[8(g + 4i) + e] for columns < D.
+template <int D>
+__device__ __forceinline__ void gen_dw(float (&dw)[32], int g, uint32_t m, uint32_t n, uint32_t it,
+                                       uint32_t k0, uint32_t k1, float sdt) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = 2 * (g + 4 * i) + h;     // 4-block index
+      float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (4 * q < D) z = dw4_fast((uint32_t)q, m, n, it, k0, k1, sdt);
+      dw[8 * i + 4 * h + 0] = z.x;
+      dw[8 * i + 4 * h + 1] = z.y;
+      dw[8 * i + 4 * h + 2] = z.z;
+      dw[8 * i + 4 * h + 3] = z.w;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ forward
 template <int D, int W>
-__global__ void __launch_bounds__(128, 1) k_fwd_tc(PassArgs a, int ntiles) {
+__global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
   using Dm = Dims<D, W>;
   constexpr int Dp = Dm::Dp, Wp = Dm::Wp;
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -267,11 +111,15 @@ __global__ void __launch_bounds__(128, 1) k_fwd_tc(PassArgs a, int ntiles) {
   uint8_t* wimg1 = sm + Dm::WB;
   uint8_t* xop = sm + 2 * Dm::WB;
   uint8_t* hop = xop + Dm::ACT;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(hop + Dm::ACT);   // [0],[1] weights, [2] mma
+  float2* red = reinterpret_cast<float2*>(hop + Dm::ACT);            // [4][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 4 * 128);       // [0],[1] weights, [2] mma
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
-  __shared__ float red[8];
+  __shared__ double lred[4];
+  __shared__ float gred[4];
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int q = warp & 3, g = warp >> 2;
+  const int row = 32 * q + lane;
   if (t == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -283,18 +131,17 @@ __global__ void __launch_bounds__(128, 1) k_fwd_tc(PassArgs a, int ntiles) {
   __syncthreads();
   tc_after();
   const uint32_t tm = *tslot;
-  const uint32_t lq = (uint32_t)(warp * 32) << 16;   // this warp's TMEM lane quadrant
-  const uint32_t acc0 = tm, acc1 = tm + 128;
+  const uint32_t lq = ((uint32_t)(32 * q) << 16) + 8u * g;   // lane quadrant + first chunk column
+  const uint32_t acc0 = tm + lq, acc1 = tm + 128 + lq;
 
   const int N = a.N;
   const uint8_t* wsrc = static_cast<const uint8_t*>(a.wpack);
   uint8_t* xst = static_cast<uint8_t*>(a.xpack);
   const uint32_t it = a.eval ? a.eval_it : a.state->it;
-  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int my_tiles = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int64_t total_seq = (int64_t)my_tiles * N;
   constexpr uint32_t I1 = idesc_bf16(128, Wp, false, false);
   constexpr uint32_t I3 = idesc_bf16(128, Dp, false, false);
-  constexpr float kSqrt2 = 1.41421356237309515f;
 
   auto load_weights = [&](int64_t s) {   // thread 0
     const int n = (int)(s % N);
@@ -312,26 +159,29 @@ __global__ void __launch_bounds__(128, 1) k_fwd_tc(PassArgs a, int ntiles) {
   double lsum = 0.0;
   float dy0 = 0.0f;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t mloc = (int64_t)tile * 128 + t;
+    const int64_t mloc = (int64_t)tile * 128 + row;
     const bool valid = mloc < a.B_local;
     const uint32_t mg = (uint32_t)(a.m0 + mloc);
-    float X[D];
+    float X[32];                       // X at this thread's columns
 #pragma unroll
-    for (int j = 0; j < D; ++j) X[j] = a.x0;
+    for (int i = 0; i < 32; ++i) X[i] = a.x0;
     float Y = a.params[0];
     for (int n = 0; n < N; ++n, ++s) {
       uint8_t* wimg = (s & 1) ? wimg1 : wimg0;
       if (t == 0 && s + 1 < total_seq) load_weights(s + 1);
-      // X_n operand (bf16; column D is the constant 1 of the folded bias)
+      // X_n operand chunks (bf16; column D is the constant 1 of the folded bias)
 #pragma unroll
-      for (int c = 0; c < Dp / 8; ++c) {
-        float v[8];
+      for (int i = 0; i < 4; ++i) {
+        const int c = g + 4 * i;
+        if (c < Dp / 8) {
+          float v[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int j = c * 8 + e;
-          v[e] = j < D ? X[j] : (j == D ? 1.0f : 0.0f);
+          for (int e = 0; e < 8; ++e) {
+            const int j = 8 * c + e;
+            v[e] = j < D ? X[8 * i + e] : (j == D ? 1.0f : 0.0f);
+          }
+          st_chunk(xop, row, c, Dp, v);
         }
-        st_chunk(xop, t, c, Dp, v);
       }
       fence_async_smem();
       __syncthreads();
@@ -342,93 +192,106 @@ __global__ void __launch_bounds__(128, 1) k_fwd_tc(PassArgs a, int ntiles) {
         }
         mbar_wait(&bars[s & 1], (uint32_t)((s >> 1) & 1));
         tc_after();
-        gemm(acc0, kmaj(xop, Dp), kmaj(wimg, Dp), Dp / 16, I1, false);          // A1
+        gemm(tm, kmaj(xop, Dp), kmaj(wimg, Dp), Dp / 16, I1, false);                  // A1
         mma_commit(&bars[2]);
       }
+      float dw[32];                                                                   // a1
+      gen_dw<D>(dw, g, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt);
       mbar_wait(&bars[2], mph);
       mph ^= 1;
       tc_after();
-      // H1 = ReLU(A1)
+      {  // H1 = ReLU(A1)
+        float v[32];
+        tmem_ld4x8(acc0, v);
 #pragma unroll
-      for (int c = 0; c < Wp / 16; ++c) {
-        float v[16];
-        tmem_ld16(acc0 + lq + c * 16, v);
+        for (int i = 0; i < 4; ++i) {
+          const int c = g + 4 * i;
+          if (c < Wp / 8) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e], 0.0f);
-        st_chunk(hop, t, 2 * c, Wp, v);
-        st_chunk(hop, t, 2 * c + 1, Wp, v + 8);
+            for (int e = 0; e < 8; ++e) v[8 * i + e] = fmaxf(v[8 * i + e], 0.0f);
+            st_chunk(hop, row, c, Wp, v + 8 * i);
+          }
+        }
       }
       fence_async_smem();
       tc_before();
       __syncthreads();
       if (t == 0) {
         tc_after();
-        gemm(acc1, kmaj(hop, Wp), kmaj(wimg + Dm::W1B, Wp), Wp / 16, I1, false);  // A2
+        gemm(tm + 128, kmaj(hop, Wp), kmaj(wimg + Dm::W1B, Wp), Wp / 16, I1, false);   // A2
         mma_commit(&bars[2]);
-        if (!a.eval) bulk_wait_read0();   // X_n image stored: xop may be reused
+        if (!a.eval) bulk_wait_read0();   // the X_n image left xop: it may be reused
       }
       __syncthreads();
       mbar_wait(&bars[2], mph);
       mph ^= 1;
       tc_after();
-      // H2 = ReLU(A1) + ReLU(A2)  (residual block, Eq. 7 with h = 1)
+      {  // H2 = ReLU(A1) + ReLU(A2)  (residual block, Eq. 7 with h = 1)
+        float v1[32], v2[32];
+        tmem_ld4x8(acc0, v1);
+        tmem_ld4x8(acc1, v2);
 #pragma unroll
-      for (int c = 0; c < Wp / 16; ++c) {
-        float v1[16], v2[16];
-        tmem_ld16(acc0 + lq + c * 16, v1);
-        tmem_ld16(acc1 + lq + c * 16, v2);
+        for (int i = 0; i < 4; ++i) {
+          const int c = g + 4 * i;
+          if (c < Wp / 8) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) v1[e] = fmaxf(v1[e], 0.0f) + fmaxf(v2[e], 0.0f);
-        st_chunk(xop, t, 2 * c, Wp, v1);
-        st_chunk(xop, t, 2 * c + 1, Wp, v1 + 8);
+            for (int e = 0; e < 8; ++e)
+              v1[8 * i + e] = fmaxf(v1[8 * i + e], 0.0f) + fmaxf(v2[8 * i + e], 0.0f);
+            st_chunk(xop, row, c, Wp, v1 + 8 * i);
+          }
+        }
       }
       fence_async_smem();
       tc_before();
       __syncthreads();
       if (t == 0) {
         tc_after();
-        gemm(acc0, kmaj(xop, Wp), kmaj(wimg + Dm::W1B + Dm::W2B, Wp), Wp / 16, I3, false);  // Z
+        gemm(tm, kmaj(xop, Wp), kmaj(wimg + Dm::W1B + Dm::W2B, Wp), Wp / 16, I3, false);  // Z
         mma_commit(&bars[2]);
       }
       mbar_wait(&bars[2], mph);
       mph ^= 1;
       tc_after();
-      // a1 + a2 + a4: ΔW_n (Philox), c = Z·ΔW, |Z|², X += √2 ΔW
       float cz = 0.0f, zz = 0.0f;
+      {  // a4 partials c = Z·ΔW, |Z|²; a2: X += √2 ΔW
+        float z[32];
+        tmem_ld4x8(acc0, z);
 #pragma unroll
-      for (int c = 0; c < (D + 15) / 16; ++c) {
-        float z[16];
-        tmem_ld16(acc0 + lq + c * 16, z);
+        for (int i = 0; i < 4; ++i) {
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int q = c * 4 + q4;
-          if (4 * q < D) {
-            const float4 g = normals4((uint32_t)q, mg, (uint32_t)n, it, a.k0, a.k1);
-            const float gg[4] = {g.x, g.y, g.z, g.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int j = 4 * q + i;
-              if (j < D) {
-                const float dw = a.sqrt_dt * gg[i];
-                const float zj = z[4 * q4 + i];
-                cz = fmaf(zj, dw, cz);
-                zz = fmaf(zj, zj, zz);
-                X[j] = fmaf(kSqrt2, dw, X[j]);
-              }
+          for (int e = 0; e < 8; ++e) {
+            const int j = 8 * (g + 4 * i) + e;
+            if (j < D) {
+              cz = fmaf(z[8 * i + e], dw[8 * i + e], cz);
+              zz = fmaf(z[8 * i + e], z[8 * i + e], zz);
+              X[8 * i + e] = fmaf(kSqrt2, dw[8 * i + e], X[8 * i + e]);
             }
           }
         }
       }
-      if (!a.eval && a.problem == kAllenCahn && valid) a.Ystore[(int64_t)n * a.B_local + mloc] = Y;
-      Y = Y - driver_f(a.problem, Y, zz, a.lam) * a.dt + cz;
+      red[g * 128 + row] = make_float2(cz, zz);
       tc_before();
+      __syncthreads();
+      {
+        const float2 r0 = red[row], r1 = red[128 + row], r2 = red[256 + row], r3 = red[384 + row];
+        cz = (r0.x + r1.x) + (r2.x + r3.x);
+        zz = (r0.y + r1.y) + (r2.y + r3.y);
+      }
+      if (!a.eval && a.problem == kAllenCahn && valid && g == 0)
+        a.Ystore[(int64_t)n * a.B_local + mloc] = Y;
+      Y = Y - driver_f(a.problem, Y, zz, a.lam) * a.dt + cz;                         // a4
     }
     // a5: R = Y_N - g(X_N); loss; ā recursion and dY0
     float sx = 0.0f;
 #pragma unroll
-    for (int j = 0; j < D; ++j) sx = fmaf(X[j], X[j], sx);
-    const float R = Y - terminal_g(a.problem, sx);
-    if (valid) {
+    for (int i = 0; i < 32; ++i)
+      if (8 * (g + 4 * (i / 8)) + (i % 8) < D) sx = fmaf(X[i], X[i], sx);
+    __syncthreads();
+    red[g * 128 + row] = make_float2(sx, 0.0f);
+    __syncthreads();
+    sx = (red[row].x + red[128 + row].x) + (red[256 + row].x + red[384 + row].x);
+    if (g == 0 && valid) {
+      const float R = Y - terminal_g(a.problem, sx);
       lsum += (double)R * R;
       if (!a.eval) {
         a.Rstore[mloc] = R;
@@ -436,35 +299,30 @@ __global__ void __launch_bounds__(128, 1) k_fwd_tc(PassArgs a, int ntiles) {
         if (a.problem == kAllenCahn) {
           for (int n = N - 1; n >= 0; --n) {
             const float y = a.Ystore[(int64_t)n * a.B_local + mloc];
-            a.abar[(int64_t)n * a.B_local + mloc] = ab;
+            a.abar[(int64_t)n * a.B_local + mloc] = ab;               // ā_{n+1}
             ab *= 1.0f - a.dt * driver_dfdy(a.problem, y);
           }
         } else {
-          a.abar[mloc] = ab;
+          a.abar[mloc] = ab;                                          // ā_N
         }
         dy0 += ab;
       }
     }
   }
-  // block reductions of Σ R² (double) and dY0
-  float l32 = (float)lsum;   // per-thread sums are small; reduce in fp32 then add in double
-  double lwarp = 0.0;
-  {
-    double v = lsum;
+  double lw = lsum;
+  float gw = dy0;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    lwarp = v;
+  for (int o = 16; o; o >>= 1) {
+    lw += __shfl_xor_sync(0xffffffffu, lw, o);
+    gw += __shfl_xor_sync(0xffffffffu, gw, o);
   }
-  (void)l32;
-  const float gw = warp_sum(dy0);
-  __shared__ double lred[4];
-  if (lane == 0) { lred[warp] = lwarp; red[warp] = gw; }
+  if (g == 0 && lane == 0) { lred[q] = lw; gred[q] = gw; }
   tc_before();
   __syncthreads();
   if (t == 0) {
     const double L = lred[0] + lred[1] + lred[2] + lred[3];
     if (L != 0.0) atomicAdd(a.loss_acc, L);
-    const float g0 = red[0] + red[1] + red[2] + red[3];
+    const float g0 = gred[0] + gred[1] + gred[2] + gred[3];
     if (!a.eval && g0 != 0.0f) atomicAdd(a.grad, g0);
     if (!a.eval) bulk_wait0();
   }
@@ -476,7 +334,7 @@ __global__ void __launch_bounds__(128, 1) k_fwd_tc(PassArgs a, int ntiles) {
 
 // ------------------------------------------------------------------ adjoint
 template <int D, int W>
-__global__ void __launch_bounds__(128, 1) k_bwd_tc(PassArgs a, int ntiles, int64_t items) {
+__global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64_t items) {
   using Dm = Dims<D, W>;
   constexpr int Dp = Dm::Dp, Wp = Dm::Wp;
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -489,7 +347,9 @@ __global__ void __launch_bounds__(128, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   uint64_t* bars = reinterpret_cast<uint64_t*>(b3 + Dm::ACT);  // 0 w, 1-2 x, 3 mma, 4 G8
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
 
-  const int t = threadIdx.x, warp = t >> 5;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int q = warp & 3, g = warp >> 2;
+  const int row = 32 * q + lane;
   if (t == 0) {
     for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
@@ -499,7 +359,7 @@ __global__ void __launch_bounds__(128, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   __syncthreads();
   tc_after();
   const uint32_t tm = *tslot;
-  const uint32_t lq = (uint32_t)(warp * 32) << 16;
+  const uint32_t lq = ((uint32_t)(32 * q) << 16) + 8u * g;
   const uint32_t acc = tm, G1 = tm + 128, G2 = tm + 256, G3 = tm + 384;
 
   const int64_t i0 = blockIdx.x * items / gridDim.x, i1 = (blockIdx.x + 1) * items / gridDim.x;
@@ -529,46 +389,44 @@ __global__ void __launch_bounds__(128, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   uint32_t mph = 0, wph = 0, gph = 0;
   int cur_n = -1;
   bool first = true;
-  int64_t g8_pending = 0;
+  bool g8_pending = false;
 
-  // gradient flush of step cur_n: TMEM -> fp32 atomics (lane = gradient row)
+  // gradient flush of step cur_n: TMEM -> fp32 atomics (lane = gradient row,
+  // this thread's column chunks)
   auto flush = [&]() {
     if (g8_pending) {
       mbar_wait(&bars[4], gph);
       gph ^= 1;
-      g8_pending = 0;
+      g8_pending = false;
     }
     tc_after();
     float* G = a.grad + nd.step_base(cur_n);
-#pragma unroll 1
-    for (int c = 0; c < Dp / 16; ++c) {              // dW1 | db1 (rows i < W)
-      float v[16];
-      tmem_ld16(G1 + lq + c * 16, v);
-      if (t < W) {
+    float v[32];
+    tmem_ld4x8(G1 + lq, v);                          // dW̃1 row = w-unit, cols = d-inputs
+    if (row < W) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int k = c * 16 + e;
-          if (k < D) atomicAdd(G + nd.off_W1() + t * D + k, v[e]);
-          else if (k == D) atomicAdd(G + nd.off_b1() + t, v[e]);
-        }
+      for (int i = 0; i < 32; ++i) {
+        const int k = 8 * (g + 4 * (i / 8)) + (i % 8);
+        if (k < D) atomicAdd(G + nd.off_W1() + row * D + k, v[i]);
+        else if (k == D) atomicAdd(G + nd.off_b1() + row, v[i]);
       }
     }
-#pragma unroll 1
-    for (int c = 0; c < Wp / 16; ++c) {              // dW2 | db2 (rows i < W), dW3 | db3 (rows j < D)
-      float v[16], u[16];
-      tmem_ld16(G2 + lq + c * 16, v);
-      tmem_ld16(G3 + lq + c * 16, u);
+    tmem_ld4x8(G2 + lq, v);                          // dW̃2
+    if (row < W) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int k = c * 16 + e;
-        if (t < W) {
-          if (k < W) atomicAdd(G + nd.off_W2() + t * W + k, v[e]);
-          else if (k == W) atomicAdd(G + nd.off_b2() + t, v[e]);
-        }
-        if (t < D) {
-          if (k < W) atomicAdd(G + nd.off_W3() + t * W + k, u[e]);
-          else if (k == W) atomicAdd(G + nd.off_b3() + t, u[e]);
-        }
+      for (int i = 0; i < 32; ++i) {
+        const int k = 8 * (g + 4 * (i / 8)) + (i % 8);
+        if (k < W) atomicAdd(G + nd.off_W2() + row * W + k, v[i]);
+        else if (k == W) atomicAdd(G + nd.off_b2() + row, v[i]);
+      }
+    }
+    tmem_ld4x8(G3 + lq, v);                          // dW̃3 row = d-output
+    if (row < D) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int k = 8 * (g + 4 * (i / 8)) + (i % 8);
+        if (k < W) atomicAdd(G + nd.off_W3() + row * W + k, v[i]);
+        else if (k == W) atomicAdd(G + nd.off_b3() + row, v[i]);
       }
     }
     tc_before();
@@ -592,41 +450,41 @@ __global__ void __launch_bounds__(128, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       cur_n = n;
       first = true;
     }
-    const int64_t mloc = (int64_t)tile * 128 + t;
+    const int64_t mloc = (int64_t)tile * 128 + row;
     const bool valid = mloc < a.B_local;
     const uint32_t mg = (uint32_t)(a.m0 + mloc);
     const float ab = valid ? (a.problem == kAllenCahn ? a.abar[(int64_t)n * a.B_local + mloc]
                                                       : a.abar[mloc])
                            : 0.0f;
-    // G1: A1 = X̃ W̃1ᵀ (recompute)
-    if (t == 0) {
+    if (t == 0) {   // G1: A1 = X̃ W̃1ᵀ (recompute)
       mbar_wait(&bars[1 + buf], (uint32_t)(((item - i0) >> 1) & 1));
       tc_after();
       gemm(acc, kmaj(xop, Dp), kmaj(wimg, Dp), Dp / 16, IW, false);
       mma_commit(&bars[3]);
     }
+    float dw[32];   // ΔW_n regenerated while G1..G3 run
+    gen_dw<D>(dw, g, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt);
     mbar_wait(&bars[3], mph);
     mph ^= 1;
-    if (g8_pending) {            // previous item's dW1 GEMM (issued before G1) is done too
+    if (g8_pending) {            // the previous item's dW̃1 GEMM was issued before G1
       mbar_wait(&bars[4], gph);
       gph ^= 1;
-      g8_pending = 0;
+      g8_pending = false;
     }
-    if (t == 0 && item + 1 < i1 && item > i0) load_x(item + 1);   // its buffer's last reader (G8) finished
+    if (t == 0 && item + 1 < i1 && item > i0) load_x(item + 1);   // its buffer's last reader (G8) is done
     tc_after();
-    uint32_t m1[4] = {0, 0, 0, 0}, m2[4] = {0, 0, 0, 0};
+    uint32_t m1 = 0, m2 = 0;   // ReLU masks of this thread's 32 columns
+    {
+      float v[32];
+      tmem_ld4x8(acc + lq, v);
 #pragma unroll
-    for (int c = 0; c < Wp / 16; ++c) {
-      float v[16];
-      tmem_ld16(acc + lq + c * 16, v);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int j = c * 16 + e;
-        if (v[e] > 0.0f) m1[j >> 5] |= 1u << (j & 31);
-        v[e] = fmaxf(v[e], 0.0f);
+      for (int i = 0; i < 32; ++i) {
+        if (v[i] > 0.0f) m1 |= 1u << i;
+        v[i] = fmaxf(v[i], 0.0f);
       }
-      st_chunk(hop, t, 2 * c, Wp, v);
-      st_chunk(hop, t, 2 * c + 1, Wp, v + 8);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (g + 4 * i < Wp / 8) st_chunk(hop, row, g + 4 * i, Wp, v + 8 * i);
     }
     fence_async_smem();
     tc_before();
@@ -639,20 +497,20 @@ __global__ void __launch_bounds__(128, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     tc_after();
+    {
+      float v[32], h[32];
+      tmem_ld4x8(acc + lq, v);
 #pragma unroll
-    for (int c = 0; c < Wp / 16; ++c) {
-      float v[16], h[16];
-      tmem_ld16(acc + lq + c * 16, v);
-      ld_chunk(hop, t, 2 * c, Wp, h);
-      ld_chunk(hop, t, 2 * c + 1, Wp, h + 8);
+      for (int i = 0; i < 4; ++i)
+        if (g + 4 * i < Wp / 8) ld_chunk(hop, row, g + 4 * i, Wp, h + 8 * i);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int j = c * 16 + e;
-        if (v[e] > 0.0f) m2[j >> 5] |= 1u << (j & 31);
-        v[e] = h[e] + fmaxf(v[e], 0.0f);
+      for (int i = 0; i < 32; ++i) {
+        if (v[i] > 0.0f) m2 |= 1u << i;
+        v[i] = h[i] + fmaxf(v[i], 0.0f);
       }
-      st_chunk(b2, t, 2 * c, Wp, v);
-      st_chunk(b2, t, 2 * c + 1, Wp, v + 8);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (g + 4 * i < Wp / 8) st_chunk(b2, row, g + 4 * i, Wp, v + 8 * i);
     }
     fence_async_smem();
     tc_before();
@@ -665,27 +523,17 @@ __global__ void __launch_bounds__(128, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     tc_after();
-    // dZ = ā_{n+1} (ΔW_n - Δt ∂_z f), columns >= D zero
+    {  // dZ = ā_{n+1}(ΔW_n - Δt ∂_z f), columns >= D zero
+      float z[32];
+      tmem_ld4x8(acc + lq, z);
 #pragma unroll
-    for (int c = 0; c < Dp / 16; ++c) {
-      float z[16];
-      tmem_ld16(acc + lq + c * 16, z);
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const int q = c * 4 + q4;
-        float gg[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-        if (4 * q < D) {
-          const float4 g = normals4((uint32_t)q, mg, (uint32_t)n, it, a.k0, a.k1);
-          gg[0] = g.x; gg[1] = g.y; gg[2] = g.z; gg[3] = g.w;
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int j = 4 * q + i;
-          z[4 * q4 + i] = j < D ? ab * fmaf(zc, z[4 * q4 + i], a.sqrt_dt * gg[i]) : 0.0f;
-        }
+      for (int i = 0; i < 32; ++i) {
+        const int j = 8 * (g + 4 * (i / 8)) + (i % 8);
+        z[i] = j < D ? ab * fmaf(zc, z[i], dw[i]) : 0.0f;
       }
-      st_chunk(b3, t, 2 * c, Dp, z);
-      st_chunk(b3, t, 2 * c + 1, Dp, z + 8);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (g + 4 * i < Dp / 8) st_chunk(b3, row, g + 4 * i, Dp, z + 8 * i);
     }
     fence_async_smem();
     tc_before();
@@ -700,25 +548,21 @@ __global__ void __launch_bounds__(128, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     tc_after();
-    // dA2 = dH2 ⊙ 1[A2 > 0]
+    {  // dA2 = dH2 ⊙ 1[A2 > 0]
+      float v[32];
+      tmem_ld4x8(acc + lq, v);
 #pragma unroll
-    for (int c = 0; c < Wp / 16; ++c) {
-      float v[16];
-      tmem_ld16(acc + lq + c * 16, v);
+      for (int i = 0; i < 32; ++i) v[i] = (m2 >> i) & 1u ? v[i] : 0.0f;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int j = c * 16 + e;
-        v[e] = (m2[j >> 5] >> (j & 31)) & 1u ? v[e] : 0.0f;
-      }
-      st_chunk(b2, t, 2 * c, Wp, v);
-      st_chunk(b2, t, 2 * c + 1, Wp, v + 8);
+      for (int i = 0; i < 4; ++i)
+        if (g + 4 * i < Wp / 8) st_chunk(b2, row, g + 4 * i, Wp, v + 8 * i);
     }
     fence_async_smem();
     tc_before();
     __syncthreads();
     if (t == 0) {
       tc_after();
-      // G6: dH1 = dH2 + dA2 W̃2 (accumulate onto dH2) ; G7: dW̃2 += dA2ᵀ H1
+      // G6: dH1 = dH2 + dA2 W̃2 (accumulated onto dH2) ; G7: dW̃2 += dA2ᵀ H1
       gemm(acc, kmaj(b2, Wp), mnmaj(wimg + Dm::W1B, Wp), Wp / 16, IWm, true);
       gemm(G2, mnmaj(b2, Wp), mnmaj(hop, Wp), 128 / 16, IGW, !first);
       mma_commit(&bars[3]);
@@ -726,18 +570,14 @@ __global__ void __launch_bounds__(128, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     tc_after();
-    // dA1 = dH1 ⊙ 1[A1 > 0]
+    {  // dA1 = dH1 ⊙ 1[A1 > 0]
+      float v[32];
+      tmem_ld4x8(acc + lq, v);
 #pragma unroll
-    for (int c = 0; c < Wp / 16; ++c) {
-      float v[16];
-      tmem_ld16(acc + lq + c * 16, v);
+      for (int i = 0; i < 32; ++i) v[i] = (m1 >> i) & 1u ? v[i] : 0.0f;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int j = c * 16 + e;
-        v[e] = (m1[j >> 5] >> (j & 31)) & 1u ? v[e] : 0.0f;
-      }
-      st_chunk(b3, t, 2 * c, Wp, v);
-      st_chunk(b3, t, 2 * c + 1, Wp, v + 8);
+      for (int i = 0; i < 4; ++i)
+        if (g + 4 * i < Wp / 8) st_chunk(b3, row, g + 4 * i, Wp, v + 8 * i);
     }
     fence_async_smem();
     tc_before();
@@ -747,7 +587,7 @@ __global__ void __launch_bounds__(128, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       gemm(G1, mnmaj(b3, Wp), mnmaj(xop, Dp), 128 / 16, IGD, !first);
       mma_commit(&bars[4]);
     }
-    g8_pending = 1;
+    g8_pending = true;
     first = false;
   }
   if (cur_n >= 0) flush();
@@ -812,34 +652,47 @@ __global__ void __launch_bounds__(128, 1) k_umma_test(int mode, const float* A, 
   }
 }
 
+__global__ void k_debug_dw_fast(uint32_t it, int n, int64_t m0, int64_t count, int d, float sdt,
+                                uint32_t k0, uint32_t k1, float* out) {
+  const int nq = (d + 3) >> 2;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count * nq) return;
+  const int64_t p = i / nq;
+  const int q = (int)(i - p * nq);
+  const float4 z = dw4_fast((uint32_t)q, (uint32_t)(m0 + p), (uint32_t)n, it, k0, k1, sdt);
+  const float zz[4] = {z.x, z.y, z.z, z.w};
+  for (int k = 0; k < 4; ++k)
+    if (4 * q + k < d) out[p * d + 4 * q + k] = zz[k];
+}
+
 // ------------------------------------------------------------------ dispatch
 template <int D, int W>
 struct Impl {
   using Dm = Dims<D, W>;
-  static size_t fwd_smem() { return 2 * Dm::WB + 2 * Dm::ACT + 64; }
+  static size_t fwd_smem() { return 2 * Dm::WB + 2 * Dm::ACT + 4 * 128 * 8 + 64; }
   static size_t bwd_smem() { return Dm::WB + 5 * Dm::ACT + 64; }
   static int ntiles(const PassArgs& a) { return (int)((a.B_local + 127) / 128); }
+  static int sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+  }
   static cudaError_t fwd(const PassArgs& a, cudaStream_t s) {
     const size_t smem = fwd_smem();
     cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int nt = ntiles(a);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int grid = nt < sms ? nt : sms;
-    k_fwd_tc<D, W><<<grid, 128, smem, s>>>(a, nt);
+    const int nt = ntiles(a), sms = sm_count();
+    k_fwd_tc<D, W><<<nt < sms ? nt : sms, NTH, smem, s>>>(a, nt);
     return cudaGetLastError();
   }
   static cudaError_t bwd(const PassArgs& a, cudaStream_t s) {
     const size_t smem = bwd_smem();
     cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int nt = ntiles(a);
+    const int nt = ntiles(a), sms = sm_count();
     const int64_t items = (int64_t)nt * a.N;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int grid = (int)(items < sms ? items : sms);
-    k_bwd_tc<D, W><<<grid, 128, smem, s>>>(a, nt, items);
+    k_bwd_tc<D, W><<<(int)(items < sms ? items : sms), NTH, smem, s>>>(a, nt, items);
     return cudaGetLastError();
   }
   static cudaError_t pack(const PassArgs& a, cudaStream_t s) {
@@ -904,6 +757,15 @@ cudaError_t launch_umma_test(int mode, const float* A, const float* B, float* D,
   cudaError_t e = cudaFuncSetAttribute(tc::k_umma_test, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   tc::k_umma_test<<<1, 128, smem, s>>>(mode, A, B, D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_debug_dw_fast(uint32_t it, int n, int64_t m0, int64_t count, int d,
+                                 float sqrt_dt, uint32_t k0, uint32_t k1, float* out,
+                                 cudaStream_t s) {
+  const int64_t th = count * ((d + 3) / 4);
+  tc::k_debug_dw_fast<<<(int)((th + 255) / 256), 256, 0, s>>>(it, n, m0, count, d, sqrt_dt, k0, k1,
+                                                             out);
   return cudaGetLastError();
 }
 

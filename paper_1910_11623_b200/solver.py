@@ -207,9 +207,10 @@ class BSDE:
                                            ctr.shape[0], out.ctypes.data_as(P)))
         return out
 
-    def debug_dw(self, it, n, m0, count):
+    def debug_dw(self, it, n, m0, count, fast=False):
         out = np.empty((count, self.d), np.float32)
-        self._ck(self._L.bsde_debug_dw(self._h, int(it), int(n), int(m0), int(count), _fptr(out)))
+        fn = self._L.bsde_debug_dw_fast if fast else self._L.bsde_debug_dw
+        self._ck(fn(self._h, int(it), int(n), int(m0), int(count), _fptr(out)))
         return out
 
     PHASES = ("begin", "fwd", "bwd", "allreduce", "check", "adam")

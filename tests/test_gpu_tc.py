@@ -53,6 +53,23 @@ def test_umma_operand_layouts(mode):
     assert np.max(np.abs(D - ref)) <= 1e-4 * np.max(np.abs(ref)), np.max(np.abs(D - ref))
 
 
+def test_fast_normals_match_oracle():
+    """The MUFU Box-Muller of the tensor-core kernels (same counters and map, R8)
+    against the float64 oracle: |Δ| ≤ 1e-5·√Δt·max(1,|z|) everywhere, including
+    u1 -> 1 (small radii) where the log1p series takes over."""
+    from oracle import philox
+    d, N, T = 100, 20, 1.0
+    s = make("hjb", d, 110, N, T, 64, kernel="simt")
+    sdt = np.sqrt(T / N)
+    worst = 0.0
+    for it, n, m0 in ((0, 0, 0), (3, 7, 5000), (2 ** 31 - 1, N - 1, 2 ** 32 - 4096)):
+        gpu = s.debug_dw(it, n, m0, 4096, fast=True).astype(np.float64)
+        ref = philox.brownian_increments(0, it, n, np.arange(m0, m0 + 4096), d, T / N)
+        err = np.abs(gpu - ref) / (sdt * np.maximum(1.0, np.abs(ref) / sdt))
+        worst = max(worst, err.max())
+    assert worst <= 1e-5, worst
+
+
 CASES = [
     ("cfg3_allen_cahn", dict(batch=1000)),
     ("cfg2_hjb", dict(batch=1000, precision="bf16")),
