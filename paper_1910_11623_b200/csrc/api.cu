@@ -22,7 +22,6 @@ cudaError_t launch_fwd_tc(const PassArgs& a, cudaStream_t s);
 cudaError_t launch_bwd_tc(const PassArgs& a, cudaStream_t s);
 cudaError_t launch_pack_weights(const PassArgs& a, cudaStream_t s);
 size_t tc_pack_bytes(int d, int w, int N, int precision);
-size_t tc_partial_bytes(int d, int w, int precision);
 size_t tc_xstore_bytes(int d, int w, int N, int64_t B_local);
 cudaError_t launch_umma_test(int mode, const float* A, const float* B, float* D, cudaStream_t s);
 cudaError_t launch_debug_dw_fast(uint32_t it, int n, int64_t m0, int64_t count, int d,
@@ -369,7 +368,6 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     allocs.push_back({(void**)&ctx->Ystore, (size_t)ctx->N_max * ctx->B_local * sizeof(float)});
   if (family == BSDE_KERNEL_TC) {
     allocs.push_back({&ctx->wpack, tc_pack_bytes(d, w, ctx->N_max, cfg.precision)});
-    allocs.push_back({(void**)&ctx->gpart, tc_partial_bytes(d, w, cfg.precision)});
   }
   for (auto& al : allocs) {
     cudaError_t e = cudaMalloc(al.p, al.bytes);

@@ -27,7 +27,7 @@ struct PassArgs {
   // tcgen05 path only
   const void* wpack;                   // packed bf16 weight images (see tc.cu)
   void* xpack;                         // bf16 X store (BF16 precision)
-  float* gpart;                        // per-CTA gradient partial scratch
+  float* gpart;                        // reserved (unused)
   int precision;
 };
 

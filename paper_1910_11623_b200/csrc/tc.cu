@@ -29,6 +29,8 @@ namespace bsde {
 namespace tc {
 
 constexpr int NTH = 512;   // threads per CTA (4 per path)
+template <int D>
+constexpr int kDwChunks = (D + 7) / 8;   // 8-column chunks of the stored ΔW image
 constexpr float kSqrt2 = 1.41421356237309515f;
 
 // ------------------------------------------------------------------ weight packing
@@ -82,24 +84,40 @@ __global__ void k_pack_tc(const float* __restrict__ params, uint8_t* __restrict_
   }
 }
 
-// ΔW_n at this thread's columns: dw[8i + e] = ΔW[8(g + 4i) + e] for columns < D.
-template <int D>
-__device__ __forceinline__ void gen_dw(float (&dw)[32], int g, uint32_t m, uint32_t n, uint32_t it,
-                                       uint32_t k0, uint32_t k1, float sdt) {
+// Column predicates of this thread's chunks c = g + 4i (g = 0..3) that fold at
+// compile time after unrolling: column 8(g+4i)+e is < LIM for every g when
+// 8(3+4i)+e < LIM, and for no g when 8(4i)+e >= LIM.
+__device__ __forceinline__ bool col_lt(int g, int i, int e, int LIM) {
+  return (8 * (3 + 4 * i) + e < LIM) || (8 * (4 * i) + e < LIM && 8 * (g + 4 * i) + e < LIM);
+}
+// chunk g + 4i exists in an image of NC chunks
+__device__ __forceinline__ bool chunk_lt(int g, int i, int NC) {
+  return (3 + 4 * i < NC) || (4 * i < NC && g + 4 * i < NC);
+}
+
+// ΔW_n at this thread's columns, dw[8i + e] = ΔW[8(g + 4i) + e] (columns < D),
+// produced one Philox block (4 normals) per call so that the generation can fill
+// the waits for the tensor core ("work while waiting").
+struct DwGen {
+  uint32_t m, n, it, k0, k1;
+  float sdt;
+  int g;   // slot s = (i, h) = (s/2, s%2) holds 4-block 2(g+4i)+h
+  // slots [S0, S1) — a compile-time share of the step's RNG, issued right after
+  // a GEMM so that the generation overlaps it
+  template <int D, int S0, int S1>
+  __device__ __forceinline__ void run(float (&dw)[32]) const {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int q = 2 * (g + 4 * i) + h;     // 4-block index
+    for (int s = S0; s < S1; ++s) {
+      const int i = s / 2, h = s % 2;
       float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (4 * q < D) z = dw4_fast((uint32_t)q, m, n, it, k0, k1, sdt);
+      if (col_lt(g, i, 4 * h, D)) z = dw4_fast((uint32_t)(2 * (g + 4 * i) + h), m, n, it, k0, k1, sdt);
       dw[8 * i + 4 * h + 0] = z.x;
       dw[8 * i + 4 * h + 1] = z.y;
       dw[8 * i + 4 * h + 2] = z.z;
       dw[8 * i + 4 * h + 3] = z.w;
     }
   }
-}
+};
 
 // ------------------------------------------------------------------ forward
 template <int D, int W>
@@ -111,8 +129,8 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
   uint8_t* wimg1 = sm + Dm::WB;
   uint8_t* xop = sm + 2 * Dm::WB;
   uint8_t* hop = xop + Dm::ACT;
-  float2* red = reinterpret_cast<float2*>(hop + Dm::ACT);            // [4][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 4 * 128);       // [0],[1] weights, [2] mma
+  float2* red = reinterpret_cast<float2*>(hop + Dm::ACT);            // [2][4][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * 128);       // [0],[1] weights, [2] mma
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
   __shared__ double lred[4];
   __shared__ float gred[4];
@@ -172,19 +190,25 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
       // X_n operand chunks (bf16; column D is the constant 1 of the folded bias)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int c = g + 4 * i;
-        if (c < Dp / 8) {
+        if (chunk_lt(g, i, Dp / 8)) {
           float v[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const int j = 8 * c + e;
-            v[e] = j < D ? X[8 * i + e] : (j == D ? 1.0f : 0.0f);
+            const int j = 8 * (g + 4 * i) + e;
+            v[e] = col_lt(g, i, e, D) ? X[8 * i + e] : (j == D ? 1.0f : 0.0f);
           }
-          st_chunk(xop, row, c, Dp, v);
+          st_chunk(xop, row, g + 4 * i, Dp, v);
         }
       }
       fence_async_smem();
       __syncthreads();
+      if (n > 0) {   // finish a4 of step n-1 from the partial sums of the four threads
+        const float2 r0 = red[row], r1 = red[128 + row], r2 = red[256 + row], r3 = red[384 + row];
+        const float cz = (r0.x + r1.x) + (r2.x + r3.x), zz = (r0.y + r1.y) + (r2.y + r3.y);
+        Y = Y - driver_f(a.problem, Y, zz, a.lam) * a.dt + cz;
+      }
+      if (!a.eval && a.problem == kAllenCahn && valid && g == 0)
+        a.Ystore[(int64_t)n * a.B_local + mloc] = Y;
       if (t == 0) {
         if (!a.eval) {
           bulk_s2g(xst + ((size_t)n * ntiles + tile) * Dm::XB, xop, Dm::XB);
@@ -195,8 +219,9 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
         gemm(tm, kmaj(xop, Dp), kmaj(wimg, Dp), Dp / 16, I1, false);                  // A1
         mma_commit(&bars[2]);
       }
-      float dw[32];                                                                   // a1
-      gen_dw<D>(dw, g, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt);
+      float dw[32];                                // a1: ΔW_n, generated while the GEMMs run
+      const DwGen gen{mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt, g};
+      gen.run<D, 0, 3>(dw);
       mbar_wait(&bars[2], mph);
       mph ^= 1;
       tc_after();
@@ -205,11 +230,10 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
         tmem_ld4x8(acc0, v);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int c = g + 4 * i;
-          if (c < Wp / 8) {
+          if (chunk_lt(g, i, Wp / 8)) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[8 * i + e] = fmaxf(v[8 * i + e], 0.0f);
-            st_chunk(hop, row, c, Wp, v + 8 * i);
+            st_chunk(hop, row, g + 4 * i, Wp, v + 8 * i);
           }
         }
       }
@@ -220,35 +244,35 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
         tc_after();
         gemm(tm + 128, kmaj(hop, Wp), kmaj(wimg + Dm::W1B, Wp), Wp / 16, I1, false);   // A2
         mma_commit(&bars[2]);
-        if (!a.eval) bulk_wait_read0();   // the X_n image left xop: it may be reused
       }
-      __syncthreads();
+      gen.run<D, 3, 6>(dw);
       mbar_wait(&bars[2], mph);
       mph ^= 1;
       tc_after();
-      {  // H2 = ReLU(A1) + ReLU(A2)  (residual block, Eq. 7 with h = 1)
+      {  // H2 = ReLU(A1) + ReLU(A2) (residual block, Eq. 7 with h = 1), over H1 in hop
         float v1[32], v2[32];
         tmem_ld4x8(acc0, v1);
         tmem_ld4x8(acc1, v2);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int c = g + 4 * i;
-          if (c < Wp / 8) {
+          if (chunk_lt(g, i, Wp / 8)) {
 #pragma unroll
             for (int e = 0; e < 8; ++e)
               v1[8 * i + e] = fmaxf(v1[8 * i + e], 0.0f) + fmaxf(v2[8 * i + e], 0.0f);
-            st_chunk(xop, row, c, Wp, v1 + 8 * i);
+            st_chunk(hop, row, g + 4 * i, Wp, v1 + 8 * i);
           }
         }
       }
       fence_async_smem();
       tc_before();
+      if (t == 0 && !a.eval) bulk_wait_read0();   // the X_n image has left xop
       __syncthreads();
       if (t == 0) {
         tc_after();
-        gemm(tm, kmaj(xop, Wp), kmaj(wimg + Dm::W1B + Dm::W2B, Wp), Wp / 16, I3, false);  // Z
+        gemm(tm, kmaj(hop, Wp), kmaj(wimg + Dm::W1B + Dm::W2B, Wp), Wp / 16, I3, false);  // Z
         mma_commit(&bars[2]);
       }
+      gen.run<D, 6, 8>(dw);
       mbar_wait(&bars[2], mph);
       mph ^= 1;
       tc_after();
@@ -260,8 +284,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
         for (int i = 0; i < 4; ++i) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const int j = 8 * (g + 4 * i) + e;
-            if (j < D) {
+            if (col_lt(g, i, e, D)) {
               cz = fmaf(z[8 * i + e], dw[8 * i + e], cz);
               zz = fmaf(z[8 * i + e], z[8 * i + e], zz);
               X[8 * i + e] = fmaf(kSqrt2, dw[8 * i + e], X[8 * i + e]);
@@ -269,27 +292,25 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
           }
         }
       }
-      red[g * 128 + row] = make_float2(cz, zz);
+      red[g * 128 + row] = make_float2(cz, zz);   // a4 is finished at the next step's barrier
       tc_before();
-      __syncthreads();
-      {
-        const float2 r0 = red[row], r1 = red[128 + row], r2 = red[256 + row], r3 = red[384 + row];
-        cz = (r0.x + r1.x) + (r2.x + r3.x);
-        zz = (r0.y + r1.y) + (r2.y + r3.y);
-      }
-      if (!a.eval && a.problem == kAllenCahn && valid && g == 0)
-        a.Ystore[(int64_t)n * a.B_local + mloc] = Y;
-      Y = Y - driver_f(a.problem, Y, zz, a.lam) * a.dt + cz;                         // a4
     }
     // a5: R = Y_N - g(X_N); loss; ā recursion and dY0
     float sx = 0.0f;
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (8 * (g + 4 * (i / 8)) + (i % 8) < D) sx = fmaf(X[i], X[i], sx);
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (col_lt(g, i, e, D)) sx = fmaf(X[8 * i + e], X[8 * i + e], sx);
+    red[512 + g * 128 + row] = make_float2(sx, 0.0f);
     __syncthreads();
-    red[g * 128 + row] = make_float2(sx, 0.0f);
-    __syncthreads();
-    sx = (red[row].x + red[128 + row].x) + (red[256 + row].x + red[384 + row].x);
+    {
+      const float2 r0 = red[row], r1 = red[128 + row], r2 = red[256 + row], r3 = red[384 + row];
+      const float cz = (r0.x + r1.x) + (r2.x + r3.x), zz = (r0.y + r1.y) + (r2.y + r3.y);
+      Y = Y - driver_f(a.problem, Y, zz, a.lam) * a.dt + cz;                         // a4, n = N-1
+    }
+    sx = (red[512 + row].x + red[640 + row].x) + (red[768 + row].x + red[896 + row].x);
+    __syncthreads();   // red is rewritten by the next tile's first step
     if (g == 0 && valid) {
       const float R = Y - terminal_g(a.problem, sx);
       lsum += (double)R * R;
@@ -462,8 +483,9 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       gemm(acc, kmaj(xop, Dp), kmaj(wimg, Dp), Dp / 16, IW, false);
       mma_commit(&bars[3]);
     }
-    float dw[32];   // ΔW_n regenerated while G1..G3 run
-    gen_dw<D>(dw, g, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt);
+    float dw[32];   // ΔW_n regenerated (Philox) while G1..G3 run
+    const DwGen gen{mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt, g};
+    gen.run<D, 0, 3>(dw);
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     if (g8_pending) {            // the previous item's dW̃1 GEMM was issued before G1
@@ -484,7 +506,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (g + 4 * i < Wp / 8) st_chunk(hop, row, g + 4 * i, Wp, v + 8 * i);
+        if (chunk_lt(g, i, Wp / 8))st_chunk(hop, row, g + 4 * i, Wp, v + 8 * i);
     }
     fence_async_smem();
     tc_before();
@@ -494,23 +516,25 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       gemm(acc, kmaj(hop, Wp), kmaj(wimg + Dm::W1B, Wp), Wp / 16, IW, false);
       mma_commit(&bars[3]);
     }
+    gen.run<D, 3, 6>(dw);
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     tc_after();
-    {
-      float v[32], h[32];
+    {  // H2 = H1 (bf16 copy, R17) + ReLU(A2), chunk by chunk
+      float v[32];
       tmem_ld4x8(acc + lq, v);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (g + 4 * i < Wp / 8) ld_chunk(hop, row, g + 4 * i, Wp, h + 8 * i);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < 32; ++i)
         if (v[i] > 0.0f) m2 |= 1u << i;
-        v[i] = h[i] + fmaxf(v[i], 0.0f);
-      }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (g + 4 * i < Wp / 8) st_chunk(b2, row, g + 4 * i, Wp, v + 8 * i);
+        if (chunk_lt(g, i, Wp / 8)) {
+          float h[8];
+          ld_chunk(hop, row, g + 4 * i, Wp, h);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) h[e] += fmaxf(v[8 * i + e], 0.0f);
+          st_chunk(b2, row, g + 4 * i, Wp, h);
+        }
     }
     fence_async_smem();
     tc_before();
@@ -520,6 +544,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       gemm(acc, kmaj(b2, Wp), kmaj(wimg + Dm::W1B + Dm::W2B, Wp), Wp / 16, ID, false);
       mma_commit(&bars[3]);
     }
+    gen.run<D, 6, 8>(dw);
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     tc_after();
@@ -527,13 +552,11 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       float z[32];
       tmem_ld4x8(acc + lq, z);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int j = 8 * (g + 4 * (i / 8)) + (i % 8);
-        z[i] = j < D ? ab * fmaf(zc, z[i], dw[i]) : 0.0f;
-      }
+      for (int i = 0; i < 32; ++i)
+        z[i] = col_lt(g, i / 8, i % 8, D) ? ab * fmaf(zc, z[i], dw[i]) : 0.0f;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (g + 4 * i < Dp / 8) st_chunk(b3, row, g + 4 * i, Dp, z + 8 * i);
+        if (chunk_lt(g, i, Dp / 8)) st_chunk(b3, row, g + 4 * i, Dp, z + 8 * i);
     }
     fence_async_smem();
     tc_before();
@@ -555,7 +578,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       for (int i = 0; i < 32; ++i) v[i] = (m2 >> i) & 1u ? v[i] : 0.0f;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (g + 4 * i < Wp / 8) st_chunk(b2, row, g + 4 * i, Wp, v + 8 * i);
+        if (chunk_lt(g, i, Wp / 8))st_chunk(b2, row, g + 4 * i, Wp, v + 8 * i);
     }
     fence_async_smem();
     tc_before();
@@ -577,7 +600,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       for (int i = 0; i < 32; ++i) v[i] = (m1 >> i) & 1u ? v[i] : 0.0f;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (g + 4 * i < Wp / 8) st_chunk(b3, row, g + 4 * i, Wp, v + 8 * i);
+        if (chunk_lt(g, i, Wp / 8))st_chunk(b3, row, g + 4 * i, Wp, v + 8 * i);
     }
     fence_async_smem();
     tc_before();
@@ -669,7 +692,7 @@ __global__ void k_debug_dw_fast(uint32_t it, int n, int64_t m0, int64_t count, i
 template <int D, int W>
 struct Impl {
   using Dm = Dims<D, W>;
-  static size_t fwd_smem() { return 2 * Dm::WB + 2 * Dm::ACT + 4 * 128 * 8 + 64; }
+  static size_t fwd_smem() { return 2 * Dm::WB + 2 * Dm::ACT + 8 * 128 * 8 + 64; }
   static size_t bwd_smem() { return Dm::WB + 5 * Dm::ACT + 64; }
   static int ntiles(const PassArgs& a) { return (int)((a.B_local + 127) / 128); }
   static int sm_count() {
@@ -731,7 +754,6 @@ size_t tc_xstore_bytes(int d, int w, int N, int64_t B_local) {
   return 16;
 }
 
-size_t tc_partial_bytes(int, int, int) { return 16; }
 
 cudaError_t launch_fwd_tc(const PassArgs& a, cudaStream_t s) {
 #define X(D_, W_) if (a.d == D_ && a.w == W_) return tc::Impl<D_, W_>::fwd(a, s);
