@@ -365,14 +365,15 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   uint8_t* hop = xbuf1 + Dm::ACT;     // H1
   uint8_t* b2 = hop + Dm::ACT;        // H2, then dA2
   uint8_t* b3 = b2 + Dm::ACT;         // dZ, then dA1
-  uint64_t* bars = reinterpret_cast<uint64_t*>(b3 + Dm::ACT);  // 0 w, 1-2 x, 3 mma, 4 G8
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
+  // barriers: 0 weights, 1-2 X images, 3 chain MMAs, 4 G8, 5 G5, 6 G7
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b3 + Dm::ACT);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int q = warp & 3, g = warp >> 2;
   const int row = 32 * q + lane;
   if (t == 0) {
-    for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 7; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tslot, 512);
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     if (i0 + 1 < i1) load_x(i0 + 1);
   }
 
-  uint32_t mph = 0, wph = 0, gph = 0;
+  uint32_t mph = 0, wph = 0, gph = 0, g5ph = 0, g7ph = 0;
   int cur_n = -1;
   bool first = true;
   bool g8_pending = false;
@@ -415,7 +416,9 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   // gradient flush of step cur_n: TMEM -> fp32 atomics (lane = gradient row,
   // this thread's column chunks)
   auto flush = [&]() {
-    if (g8_pending) {
+    if (g8_pending) {            // G7 and G8 of the last item
+      mbar_wait(&bars[6], g7ph);
+      g7ph ^= 1;
       mbar_wait(&bars[4], gph);
       gph ^= 1;
       g8_pending = false;
@@ -488,7 +491,9 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     gen.run<D, 0, 3>(dw);
     mbar_wait(&bars[3], mph);
     mph ^= 1;
-    if (g8_pending) {            // the previous item's dW̃1 GEMM was issued before G1
+    if (g8_pending) {            // the previous item's G7, G8 were issued before G1
+      mbar_wait(&bars[6], g7ph);
+      g7ph ^= 1;
       mbar_wait(&bars[4], gph);
       gph ^= 1;
       g8_pending = false;
@@ -565,17 +570,20 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       tc_after();
       // G4: dH2 = dZ W̃3 ; G5: dW̃3 += dZᵀ H2
       gemm(acc, kmaj(b3, Dp), mnmaj(wimg + Dm::W1B + Dm::W2B, Wp), Dp / 16, IWm, false);
-      gemm(G3, mnmaj(b3, Dp), mnmaj(b2, Wp), 128 / 16, IGW, !first);
       mma_commit(&bars[3]);
+      gemm(G3, mnmaj(b3, Dp), mnmaj(b2, Wp), 128 / 16, IGW, !first);
+      mma_commit(&bars[5]);
     }
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     tc_after();
-    {  // dA2 = dH2 ⊙ 1[A2 > 0]
+    {  // dA2 = dH2 ⊙ 1[A2 > 0]  (computed while G5 runs; stored over H2 once G5 is done)
       float v[32];
       tmem_ld4x8(acc + lq, v);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = (m2 >> i) & 1u ? v[i] : 0.0f;
+      mbar_wait(&bars[5], g5ph);
+      g5ph ^= 1;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         if (chunk_lt(g, i, Wp / 8))st_chunk(b2, row, g + 4 * i, Wp, v + 8 * i);
@@ -587,8 +595,9 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       tc_after();
       // G6: dH1 = dH2 + dA2 W̃2 (accumulated onto dH2) ; G7: dW̃2 += dA2ᵀ H1
       gemm(acc, kmaj(b2, Wp), mnmaj(wimg + Dm::W1B, Wp), Wp / 16, IWm, true);
-      gemm(G2, mnmaj(b2, Wp), mnmaj(hop, Wp), 128 / 16, IGW, !first);
       mma_commit(&bars[3]);
+      gemm(G2, mnmaj(b2, Wp), mnmaj(hop, Wp), 128 / 16, IGW, !first);
+      mma_commit(&bars[6]);
     }
     mbar_wait(&bars[3], mph);
     mph ^= 1;
@@ -693,7 +702,7 @@ template <int D, int W>
 struct Impl {
   using Dm = Dims<D, W>;
   static size_t fwd_smem() { return 2 * Dm::WB + 2 * Dm::ACT + 8 * 128 * 8 + 64; }
-  static size_t bwd_smem() { return Dm::WB + 5 * Dm::ACT + 64; }
+  static size_t bwd_smem() { return Dm::WB + 5 * Dm::ACT + 96; }
   static int ntiles(const PassArgs& a) { return (int)((a.B_local + 127) / 128); }
   static int sm_count() {
     int dev = 0, sms = 148;
