@@ -89,9 +89,10 @@ typedef struct {
   void* stream;           /* cudaStream_t to enqueue on (NULL = legacy default stream)      */
   int rank, world;        /* this rank's index and the number of ranks (0, 1 for one GPU)  */
   const void* nccl_id;    /* 128-byte ncclUniqueId shared by all ranks (bsde_nccl_unique_id
-                             on rank 0, broadcast by the caller); NULL => no collective:
-                             "fake-world" mode, the context computes its shard's local
-                             gradient only (tests)                      */
+                             on rank 0, broadcast by the caller): the context joins an NCCL
+                             communicator of `world` ranks (world = 1 allowed).  NULL => no
+                             collective: "fake-world" mode, the context computes its shard's
+                             local gradient only (tests)                */
   int use_graph;          /* 1: capture the step in a CUDA graph and replay it              */
   int init_zero_head;     /* 1: W3 = 0 at init, so Z ≡ 0 (R7b; default for Allen-Cahn,
                              whose cubic driver diverges from a Xavier-initialised Z)      */

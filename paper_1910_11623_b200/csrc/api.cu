@@ -312,8 +312,9 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     return fail(none, BSDE_EINVAL, "d=%d w=%d too large for the SIMT kernels' shared memory", d, w);
   if (family != BSDE_KERNEL_SIMT && family != BSDE_KERNEL_TC)
     return fail(none, BSDE_EINVAL, "kernel=%d", cfg.kernel);
-  if (cfg.world > 1 && cfg.nccl_id && !nccl().ok)
-    return fail(none, BSDE_ENCCL, "world=%d but libnccl.so.2 could not be loaded", cfg.world);
+  if (cfg.nccl_id && !nccl().ok)
+    return fail(none, BSDE_ENCCL, "nccl_id given (world=%d) but libnccl.so.2 could not be loaded",
+                cfg.world);
 
   bsde_ctx* ctx = new bsde_ctx;
   ctx->problem = problem;
@@ -388,7 +389,7 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     return bail(BSDE_ECUDA);
   }
   if (repack(ctx) != BSDE_OK) return bail(BSDE_ECUDA);
-  if (cfg.world > 1 && cfg.nccl_id) {
+  if (cfg.nccl_id) {   // any world size, including a 1-rank communicator
     ncclUniqueId id;
     std::memcpy(&id, cfg.nccl_id, sizeof id);
     ncclResult_t r = nccl().CommInitRank(&ctx->comm, cfg.world, id, cfg.rank);

@@ -105,8 +105,7 @@ class BSDE:
         obj = [nccl_unique_id() if rank == 0 else None]
         if world > 1:
             dist.broadcast_object_list(obj, src=0)
-        return cls(problem, d, N, T, width, batch, rank=rank, world=world,
-                   nccl_id=obj[0] if world > 1 else None, **kw)
+        return cls(problem, d, N, T, width, batch, rank=rank, world=world, nccl_id=obj[0], **kw)
 
     # ------------------------------------------------------------------ core
     def _ck(self, rc):
