@@ -17,6 +17,11 @@
 
 namespace bsde {
 size_t simt_max_smem(int d, int w);
+bool simt_supported(int d, int w);
+size_t simt_pack_bytes(int d, int w, int N);
+size_t simt_xstore_bytes(int d, int N, int64_t B_local);
+size_t simt_scratch_bytes(int d, int w);
+cudaError_t launch_pack_simt(const PassArgs& a, cudaStream_t s);
 bool tc_supported(int d, int w);
 cudaError_t launch_fwd_tc(const PassArgs& a, cudaStream_t s);
 cudaError_t launch_bwd_tc(const PassArgs& a, cudaStream_t s);
@@ -193,10 +198,10 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
                    (float)ctx->cfg.lr, (float)ctx->cfg.beta1, (float)ctx->cfg.beta2,
                    (float)ctx->cfg.eps, 1, ctx->stream));
     launches += 2;
-    if (ctx->family == BSDE_KERNEL_TC) {   // bf16 weight images for the next step
-      CK(launch_pack_weights(a, ctx->stream));
-      launches += 1;
-    }
+    // weight images for the next step (bf16 UMMA images / fp32 transposed images)
+    if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(a, ctx->stream));
+    else CK(launch_pack_simt(a, ctx->stream));
+    launches += 1;
   }
   mark(6);
   ctx->launches = launches;
@@ -210,8 +215,8 @@ int read_state(bsde_ctx* ctx, DeviceState* hs) {
 }
 
 int repack(bsde_ctx* ctx) {
-  if (ctx->family != BSDE_KERNEL_TC) return BSDE_OK;
-  CK(launch_pack_weights(pass_args(ctx), ctx->stream));
+  if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(pass_args(ctx), ctx->stream));
+  else CK(launch_pack_simt(pass_args(ctx), ctx->stream));
   return BSDE_OK;
 }
 
@@ -308,8 +313,9 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
                 "kernel=SIMT");
   if (family == BSDE_KERNEL_SIMT && cfg.precision == BSDE_BF16)
     return fail(none, BSDE_EINVAL, "bf16 operands need the tcgen05 kernels (kernel=SIMT given)");
-  if (family == BSDE_KERNEL_SIMT && simt_max_smem(d, w) > 227 * 1024)
-    return fail(none, BSDE_EINVAL, "d=%d w=%d too large for the SIMT kernels' shared memory", d, w);
+  if (family == BSDE_KERNEL_SIMT && !simt_supported(d, w))
+    return fail(none, BSDE_EINVAL, "d=%d w=%d too large for the SIMT kernels (d, w <= 127 and shared "
+                "memory)", d, w);
   if (family != BSDE_KERNEL_SIMT && family != BSDE_KERNEL_TC)
     return fail(none, BSDE_EINVAL, "kernel=%d", cfg.kernel);
   if (cfg.nccl_id && !nccl().ok)
@@ -350,9 +356,8 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
   const int64_t npmax = num_params_at(ctx, ctx->N_max);
   struct Alloc { void** p; size_t bytes; };
   // X_n store for the adjoint: fp32 rows (SIMT) or bf16 operand images (tcgen05)
-  const size_t xs = family == BSDE_KERNEL_TC
-                        ? tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)
-                        : (size_t)ctx->N_max * ctx->B_local * d * sizeof(float);
+  const size_t xs = family == BSDE_KERNEL_TC ? tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)
+                                             : simt_xstore_bytes(d, ctx->N_max, ctx->B_local);
   std::vector<Alloc> allocs = {
       {(void**)&ctx->params, npmax * sizeof(float)},
       {(void**)&ctx->grad, npmax * sizeof(float)},
@@ -369,6 +374,9 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     allocs.push_back({(void**)&ctx->Ystore, (size_t)ctx->N_max * ctx->B_local * sizeof(float)});
   if (family == BSDE_KERNEL_TC) {
     allocs.push_back({&ctx->wpack, tc_pack_bytes(d, w, ctx->N_max, cfg.precision)});
+  } else {
+    allocs.push_back({&ctx->wpack, simt_pack_bytes(d, w, ctx->N_max)});
+    allocs.push_back({(void**)&ctx->gpart, simt_scratch_bytes(d, w)});
   }
   for (auto& al : allocs) {
     cudaError_t e = cudaMalloc(al.p, al.bytes);

@@ -1,17 +1,20 @@
-// simt.cu — fp32 CUDA-core forward and adjoint kernels.
+// simt.cu — fp32 CUDA-core forward and adjoint kernels (the fp32-accurate path:
+// configs 1, 2, 4 and any d, w <= 127 outside the tcgen05 instantiations).
 //
-// The exact-fp32 path: configs with fp32 operands at small width (config 1),
-// any d, w too large for the tcgen05 tiles, and the on-device cross-check of
-// the tensor-core kernels.  Same data flow as the tcgen05 path:
-//
-//  k_fwd_simt  one CTA = TP paths, all N steps ("tile-major"): a1 Philox ΔW,
-//              a2 Euler X, a3 Z-net, a4 Y update, a5 terminal loss; stores X_n
-//              (for the adjoint) and, for Allen-Cahn, Y_n; ends with the ā
-//              recursion (a6 scalar part) and dY0.
-//  k_bwd_simt  one CTA = (step n, TP paths) ("step-major"): reloads X_n,
-//              regenerates ΔW_n, recomputes the net, and back-propagates
-//              dZ_n = ā_{n+1}(ΔW_n - Δt ∂_z f) through it (a6), accumulating
-//              the per-step weight gradients with fp32 atomics.
+// Same data flow as the tensor-core path, register-tiled FFMA GEMMs:
+//  k_pack_simt  fp32 master θ -> per-step transposed/padded weight images
+//               W1ᵀ [d][128], W2ᵀ [w][128], W3ᵀ [w][128], W3 [d][128], W2 [w][128]
+//               (row pitch 128 floats, zero padded) so staging is a straight copy.
+//  k_fwd_simt   tile-major: a 64-path tile walks all N steps; activations are kept
+//               feature-major in shared memory ([feature][64 paths]); every GEMM
+//               C[64×nout] = A[64×K]·B[K×nout] gives each thread a 4-path × 8-output
+//               block (32 FFMA per 3 LDS.128).  a1 Philox ΔW, a2 Euler X, a3 Z-net,
+//               a4 Y update, a5 terminal loss; X_n stored for the adjoint.
+//  k_bwd_simt   step-major persistent: each CTA owns a contiguous range of (n, tile)
+//               items, recomputes the step-n net, back-propagates dZ_n, and adds the
+//               weight-gradient blocks (8×8 per thread, contraction over the 64 paths)
+//               into a per-CTA scratch gradient that is flushed with fp32 atomics when
+//               the step changes.
 //
 // Citations: Eq. 5, Eq. 7, Eq. 6.
 #include "kernels.cuh"
@@ -19,173 +22,253 @@
 namespace bsde {
 namespace {
 
-constexpr int TP = 32;    // paths per CTA
-constexpr int NT = 256;   // threads per CTA
+constexpr int TP = 64;     // paths per tile
+constexpr int NT = 256;    // threads per CTA
+constexpr int LDW = 128;   // row pitch of the packed weight images (floats)
 constexpr float kSqrt2 = 1.41421356237309515f;
 
-__host__ __device__ inline int odd_ld(int K) { return (K & 1) ? K + 2 : K + 1; }
+struct Pack {
+  int d, w;
+  __host__ __device__ size_t w1t() const { return 0; }                        // [d][LDW]
+  __host__ __device__ size_t w2t() const { return (size_t)d * LDW; }          // [w][LDW]
+  __host__ __device__ size_t w3t() const { return (size_t)(d + w) * LDW; }    // [w][LDW]
+  __host__ __device__ size_t w3n() const { return (size_t)(d + 2 * w) * LDW; }  // [d][LDW]
+  __host__ __device__ size_t w2n() const { return (size_t)(2 * d + 2 * w) * LDW; }  // [w][LDW]
+  __host__ __device__ size_t per_step() const { return (size_t)(2 * d + 3 * w) * LDW; }
+};
 
-// Ws[j*ld + k] = W[j*K + k]  (rows of a [nout][K] row-major matrix, odd pitch)
-__device__ void stage_rows(float* Ws, int ld, const float* __restrict__ W, int nout, int K) {
-  for (int idx = threadIdx.x; idx < nout * K; idx += NT) {
-    const int j = idx / K, k = idx - j * K;
-    Ws[j * ld + k] = __ldg(W + idx);
+__global__ void k_pack_simt(const float* __restrict__ params, float* __restrict__ out, int d,
+                            int w, int N) {
+  const NetDims nd{d, w};
+  const Pack pk{d, w};
+  const int64_t per = (int64_t)pk.per_step();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)N * per;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(i / per);
+    const int64_t r = i - n * per;
+    const int row = (int)(r / LDW), col = (int)(r % LDW);
+    const float* P = params + nd.step_base(n);
+    float v = 0.0f;
+    if (row < d) {                                  // W1ᵀ[k][j] = W1[j][k]
+      if (col < w) v = P[nd.off_W1() + (int64_t)col * d + row];
+    } else if (row < d + w) {                       // W2ᵀ[k][j] = W2[j][k]
+      const int k = row - d;
+      if (col < w) v = P[nd.off_W2() + (int64_t)col * w + k];
+    } else if (row < d + 2 * w) {                   // W3ᵀ[k][j] = W3[j][k]
+      const int k = row - d - w;
+      if (col < d) v = P[nd.off_W3() + (int64_t)col * w + k];
+    } else if (row < 2 * d + 2 * w) {               // W3[i][j]
+      const int k = row - d - 2 * w;
+      if (col < w) v = P[nd.off_W3() + (int64_t)k * w + col];
+    } else {                                        // W2[i][j]
+      const int k = row - 2 * d - 2 * w;
+      if (col < w) v = P[nd.off_W2() + (int64_t)k * w + col];
+    }
+    out[i] = v;
   }
 }
-__device__ void stage_copy(float* Ws, const float* __restrict__ W, int count) {
-  for (int idx = threadIdx.x; idx < count; idx += NT) Ws[idx] = __ldg(W + idx);
+
+// copy `floats` (multiple of 4) from global to shared, 16 B per thread-iteration
+__device__ __forceinline__ void stage(float* dst, const float* __restrict__ src, int floats) {
+  const float4* s = reinterpret_cast<const float4*>(src);
+  float4* o = reinterpret_cast<float4*>(dst);
+  for (int i = threadIdx.x; i < floats / 4; i += NT) o[i] = __ldg(s + i);
 }
 
-// out[p][j] = Σ_k A[p][k] · (TRANS ? Ws[j][k] : Ws[k][j]) for p < TP, j < nout;
-// epi(p, j, acc).  A row reads are warp broadcasts; Ws reads are unit-stride in
-// j (odd pitch for TRANS), hence bank-conflict free.
-template <bool TRANS, typename Epi>
-__device__ __forceinline__ void gemm_tp(const float* A, int lda, int K, const float* Ws,
-                                        int ldw, int nout, Epi epi) {
-  const int jt = min(128, (nout + 31) & ~31);
-  const int groups = NT / jt;
-  const int g = threadIdx.x / jt;
-  const int jl = threadIdx.x - g * jt;
-  const int rows = TP / groups;
-  if (g >= groups) return;
-  for (int j0 = 0; j0 < nout; j0 += jt) {
-    const int j = j0 + jl;
-    if (j >= nout) continue;
-    float acc[16];
+// C[p][j] = Σ_k At[k][p] · Bs[k][j] for p < 64, j < nout (<= 128).  Thread
+// (ty, tx) = (t/16, t%16) owns paths 4ty..4ty+3 and outputs 4tx..4tx+3 and
+// 64+4tx..64+4tx+3.  epi(p0, j, float4 values-of-paths p0..p0+3).
+template <typename Epi>
+__device__ __forceinline__ void gemm_n(const float* At, const float* Bs, int K, int nout, Epi epi) {
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  const int p0 = 4 * ty, j0 = 4 * tx, j1 = 64 + 4 * tx;
+  float acc[4][8];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) acc[r] = 0.0f;
-    for (int k = 0; k < K; ++k) {
-      const float wv = TRANS ? Ws[j * ldw + k] : Ws[k * ldw + j];
+  for (int r = 0; r < 4; ++r)
 #pragma unroll
-      for (int r = 0; r < 16; ++r)
-        if (r < rows) acc[r] = fmaf(A[(g + r * groups) * lda + k], wv, acc[r]);
+    for (int c = 0; c < 8; ++c) acc[r][c] = 0.0f;
+  const bool hi = j1 < nout;
+#pragma unroll 2
+  for (int k = 0; k < K; ++k) {
+    const float4 a = *reinterpret_cast<const float4*>(At + k * TP + p0);
+    const float4 b0 = *reinterpret_cast<const float4*>(Bs + k * LDW + j0);
+    const float4 b1 = hi ? *reinterpret_cast<const float4*>(Bs + k * LDW + j1) : make_float4(0, 0, 0, 0);
+    const float av[4] = {a.x, a.y, a.z, a.w};
+    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int j = (c < 4 ? j0 : j1 - 4) + c;
+    if (j < nout) epi(p0, j, make_float4(acc[0][c], acc[1][c], acc[2][c], acc[3][c]));
+  }
+}
+
+// G[i][j] += Σ_p L[i][p] R[j][p] (feature-major operands, p < 64) into the per-CTA
+// scratch gradient, i < ni, j < nj, row pitch ldg; gb[i] += Σ_p L[i][p].
+__device__ void gemm_t(const float* L, int ni, const float* R, int nj, float* __restrict__ G,
+                       int ldg, float* __restrict__ gb) {
+  const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
+  int iv[8], jv[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    iv[r] = (r < 4 ? 4 * ti : 64 + 4 * ti - 4) + r;
+    jv[r] = (r < 4 ? 4 * tj : 64 + 4 * tj - 4) + r;
+  }
+  float acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = 0.0f;
+  for (int p = 0; p < TP; p += 4) {
+    float4 lv[8], rv[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      lv[r] = iv[r] < ni ? *reinterpret_cast<const float4*>(L + iv[r] * TP + p) : make_float4(0, 0, 0, 0);
+      rv[r] = jv[r] < nj ? *reinterpret_cast<const float4*>(R + jv[r] * TP + p) : make_float4(0, 0, 0, 0);
     }
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
-      if (r < rows) epi(g + r * groups, j, acc[r]);
-  }
-}
-
-// G[i][j] += Σ_p L[p][i] R[p][j];  gb[i] += Σ_p L[p][i]   (fp32 atomics)
-__device__ void wgrad_tp(const float* L, int ldl, int ni, const float* R, int ldr, int nj,
-                         float* G, float* gb) {
-  for (int idx = threadIdx.x; idx < ni * nj; idx += NT) {
-    const int i = idx / nj, j = idx - i * nj;
-    float s = 0.0f;
-#pragma unroll 8
-    for (int p = 0; p < TP; ++p) s = fmaf(L[p * ldl + i], R[p * ldr + j], s);
-    atomicAdd(G + idx, s);
-  }
-  for (int i = threadIdx.x; i < ni; i += NT) {
-    float s = 0.0f;
-    for (int p = 0; p < TP; ++p) s += L[p * ldl + i];
-    atomicAdd(gb + i, s);
-  }
-}
-
-__device__ __forceinline__ float warp_sum(float v) {
+    for (int r = 0; r < 8; ++r)
 #pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+      for (int c = 0; c < 8; ++c) {
+        acc[r][c] = fmaf(lv[r].x, rv[c].x, acc[r][c]);
+        acc[r][c] = fmaf(lv[r].y, rv[c].y, acc[r][c]);
+        acc[r][c] = fmaf(lv[r].z, rv[c].z, acc[r][c]);
+        acc[r][c] = fmaf(lv[r].w, rv[c].w, acc[r][c]);
+      }
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (iv[r] < ni && jv[c] < nj) G[iv[r] * ldg + jv[c]] += acc[r][c];
+  for (int i = threadIdx.x; i < ni; i += NT) {
+    const float4* l = reinterpret_cast<const float4*>(L + i * TP);
+    float s = 0.0f;
+#pragma unroll 4
+    for (int q = 0; q < TP / 4; ++q) {
+      const float4 v = l[q];
+      s += (v.x + v.y) + (v.z + v.w);
+    }
+    gb[i] += s;
+  }
 }
 
-// ΔW_n for the TP paths of this CTA (global index mg0 + p) into dW[p][j].
-__device__ void gen_dw(float* dW, int d, int64_t mg0, int64_t valid, int n, uint32_t it,
+// ΔW_n of the tile into dWs[k][p] (feature-major), zero for paths >= valid.
+__device__ void gen_dw(float* dWs, int d, int64_t mg0, int64_t valid, int n, uint32_t it,
                        uint32_t k0, uint32_t k1, float sqrt_dt) {
   const int nq = (d + 3) >> 2;
   for (int idx = threadIdx.x; idx < TP * nq; idx += NT) {
-    const int p = idx / nq, q = idx - p * nq;
-    const float4 z = normals4((uint32_t)q, (uint32_t)(mg0 + p), (uint32_t)n, it, k0, k1);
+    const int q = idx / TP, p = idx - q * TP;   // consecutive threads: consecutive paths
+    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (p < valid) z = normals4((uint32_t)q, (uint32_t)(mg0 + p), (uint32_t)n, it, k0, k1);
     const float zz[4] = {z.x, z.y, z.z, z.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int j = 4 * q + i;
-      if (j < d) dW[p * d + j] = p < valid ? sqrt_dt * zz[i] : 0.0f;
-    }
+    for (int i = 0; i < 4; ++i)
+      if (4 * q + i < d) dWs[(4 * q + i) * TP + p] = sqrt_dt * zz[i];
   }
 }
 
-__global__ void __launch_bounds__(NT) k_fwd_simt(PassArgs a) {
-  extern __shared__ float sm[];
+__device__ __forceinline__ float sum16(float v) {   // over the 16 lanes sharing ty
+#pragma unroll
+  for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
+  extern __shared__ __align__(16) float sm[];
   const int d = a.d, w = a.w;
   const NetDims nd{d, w};
-  const int64_t mloc0 = (int64_t)blockIdx.x * TP;
-  const int64_t valid = min((int64_t)TP, a.B_local - mloc0);
+  const Pack pk{d, w};
+  float* Xs = sm;                         // [d][64] X_n (fp32 state)
+  float* dWs = Xs + d * TP;               // [d][64]
+  float* H1 = dWs + d * TP;               // [w][64]
+  float* H2 = H1 + w * TP;                // [w][64]
+  float* Ws = H2 + w * TP;                // [K <= max(d, w)][128]
+  float* Ys = Ws + (d > w ? d : w) * LDW; // [64]
+  const float* wp = static_cast<const float*>(a.wpack);
+  const int t = threadIdx.x, lane = t & 31, ty = t >> 4, tx = t & 15;
   const uint32_t it = a.eval ? a.eval_it : a.state->it;
-  float* X = sm;
-  float* dW = X + TP * d;
-  float* Z = dW + TP * d;
-  float* H1 = Z + TP * d;
-  float* H2 = H1 + TP * w;
-  float* Y = H2 + TP * w;
-  float* red = Y + TP;
-  float* Ws = red + 64;
-  const int lw = odd_ld(w), ld_ = odd_ld(d);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  for (int idx = threadIdx.x; idx < TP * d; idx += NT) X[idx] = a.x0;
-  if (threadIdx.x < TP) Y[threadIdx.x] = a.params[0];
-  __syncthreads();
-
-  for (int n = 0; n < a.N; ++n) {
-    const float* P = a.params + nd.step_base(n);
-    if (!a.eval) {   // X_n for the adjoint pass (coalesced: the tile is contiguous)
-      float* xs = a.Xstore + ((int64_t)n * a.B_local + mloc0) * d;
-      for (int idx = threadIdx.x; idx < valid * d; idx += NT) xs[idx] = X[idx];
-    }
-    gen_dw(dW, d, a.m0 + mloc0, valid, n, it, a.k0, a.k1, a.sqrt_dt);          // a1
-    stage_rows(Ws, ld_, P + nd.off_W1(), w, d);
+  double lsum = 0.0;
+  float dy0 = 0.0f;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t mloc0 = (int64_t)tile * TP;
+    const int64_t valid = min((int64_t)TP, a.B_local - mloc0);
+    for (int i = t; i < d * TP; i += NT) Xs[i] = a.x0;
+    if (t < TP) Ys[t] = a.params[0];
     __syncthreads();
-    const float* b1 = P + nd.off_b1();
-    gemm_tp<true>(X, d, d, Ws, ld_, w, [&](int p, int j, float v) {            // a3
-      H1[p * w + j] = fmaxf(v + __ldg(b1 + j), 0.0f);
-    });
-    __syncthreads();
-    stage_rows(Ws, lw, P + nd.off_W2(), w, w);
-    __syncthreads();
-    const float* b2 = P + nd.off_b2();
-    gemm_tp<true>(H1, w, w, Ws, lw, w, [&](int p, int j, float v) {
-      H2[p * w + j] = H1[p * w + j] + fmaxf(v + __ldg(b2 + j), 0.0f);
-    });
-    __syncthreads();
-    stage_rows(Ws, lw, P + nd.off_W3(), d, w);
-    __syncthreads();
-    const float* b3 = P + nd.off_b3();
-    gemm_tp<true>(H2, w, w, Ws, lw, d, [&](int p, int j, float v) {
-      Z[p * d + j] = v + __ldg(b3 + j);
-    });
-    __syncthreads();
-    for (int p = warp; p < TP; p += NT / 32) {                                  // a4
-      float c = 0.0f, zz = 0.0f;
-      for (int j = lane; j < d; j += 32) {
-        const float z = Z[p * d + j];
-        c = fmaf(z, dW[p * d + j], c);
-        zz = fmaf(z, z, zz);
+    for (int n = 0; n < a.N; ++n) {
+      const float* P = a.params + nd.step_base(n);
+      const float* W = wp + (size_t)n * pk.per_step();
+      if (!a.eval) {   // X_n for the adjoint pass: [n][tile][k][64], coalesced
+        float4* xs = reinterpret_cast<float4*>(a.Xstore + ((size_t)n * ntiles + tile) * d * TP);
+        for (int i = t; i < d * TP / 4; i += NT) xs[i] = reinterpret_cast<const float4*>(Xs)[i];
       }
-      c = warp_sum(c);
-      zz = warp_sum(zz);
-      if (lane == 0) {
-        const float y = Y[p];
-        if (!a.eval && a.problem == kAllenCahn && p < valid)
-          a.Ystore[(int64_t)n * a.B_local + mloc0 + p] = y;
-        Y[p] = y - driver_f(a.problem, y, zz, a.lam) * a.dt + c;
+      gen_dw(dWs, d, a.m0 + mloc0, valid, n, it, a.k0, a.k1, a.sqrt_dt);           // a1
+      stage(Ws, W + pk.w1t(), d * LDW);
+      __syncthreads();
+      const float* b1 = P + nd.off_b1();
+      gemm_n(Xs, Ws, d, w, [&](int p0, int j, float4 v) {                          // a3
+        const float b = __ldg(b1 + j);
+        *reinterpret_cast<float4*>(H1 + j * TP + p0) =
+            make_float4(fmaxf(v.x + b, 0.f), fmaxf(v.y + b, 0.f), fmaxf(v.z + b, 0.f), fmaxf(v.w + b, 0.f));
+      });
+      __syncthreads();
+      stage(Ws, W + pk.w2t(), w * LDW);
+      __syncthreads();
+      const float* b2 = P + nd.off_b2();
+      gemm_n(H1, Ws, w, w, [&](int p0, int j, float4 v) {
+        const float b = __ldg(b2 + j);
+        const float4 h = *reinterpret_cast<const float4*>(H1 + j * TP + p0);
+        *reinterpret_cast<float4*>(H2 + j * TP + p0) =
+            make_float4(h.x + fmaxf(v.x + b, 0.f), h.y + fmaxf(v.y + b, 0.f),
+                        h.z + fmaxf(v.z + b, 0.f), h.w + fmaxf(v.w + b, 0.f));
+      });
+      __syncthreads();
+      stage(Ws, W + pk.w3t(), w * LDW);
+      __syncthreads();
+      const float* b3 = P + nd.off_b3();
+      float c4[4] = {0, 0, 0, 0}, z4[4] = {0, 0, 0, 0};
+      gemm_n(H2, Ws, w, d, [&](int p0, int j, float4 v) {                          // a4 partials
+        const float b = __ldg(b3 + j);
+        const float4 dw = *reinterpret_cast<const float4*>(dWs + j * TP + p0);
+        const float zv[4] = {v.x + b, v.y + b, v.z + b, v.w + b};
+        const float wv[4] = {dw.x, dw.y, dw.z, dw.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          c4[r] = fmaf(zv[r], wv[r], c4[r]);
+          z4[r] = fmaf(zv[r], zv[r], z4[r]);
+        }
+      });
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        c4[r] = sum16(c4[r]);
+        z4[r] = sum16(z4[r]);
       }
+      if (tx == 0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int p = 4 * ty + r;
+          const float y = Ys[p];
+          if (!a.eval && a.problem == kAllenCahn && p < valid)
+            a.Ystore[(int64_t)n * a.B_local + mloc0 + p] = y;
+          Ys[p] = y - driver_f(a.problem, y, z4[r], a.lam) * a.dt + c4[r];
+        }
+      }
+      for (int i = t; i < d * TP; i += NT) Xs[i] = fmaf(kSqrt2, dWs[i], Xs[i]);     // a2
+      __syncthreads();
     }
-    for (int idx = threadIdx.x; idx < TP * d; idx += NT) X[idx] = fmaf(kSqrt2, dW[idx], X[idx]);  // a2
-    __syncthreads();
-  }
-
-  // a5: R = Y_N - g(X_N); loss; ā recursion and dY0 (a6, scalar part)
-  float l2 = 0.0f, dy0 = 0.0f;
-  for (int p = warp; p < TP; p += NT / 32) {
-    float s = 0.0f;
-    for (int j = lane; j < d; j += 32) s = fmaf(X[p * d + j], X[p * d + j], s);
-    s = warp_sum(s);
-    if (lane == 0 && p < valid) {
-      const float R = Y[p] - terminal_g(a.problem, s);
-      l2 += R * R;
+    // a5: R = Y_N - g(X_N); loss; ā recursion and dY0
+    if (t < TP && t < valid) {
+      float s = 0.0f;
+      for (int k = 0; k < d; ++k) s = fmaf(Xs[k * TP + t], Xs[k * TP + t], s);
+      const float R = Ys[t] - terminal_g(a.problem, s);
+      const int64_t m = mloc0 + t;
+      lsum += (double)R * R;
       if (!a.eval) {
-        const int64_t m = mloc0 + p;
         a.Rstore[m] = R;
         float ab = 2.0f * R * a.inv_B;
         if (a.problem == kAllenCahn) {
@@ -195,134 +278,205 @@ __global__ void __launch_bounds__(NT) k_fwd_simt(PassArgs a) {
             ab *= 1.0f - a.dt * driver_dfdy(a.problem, y);
           }
         } else {
-          a.abar[m] = ab;                                              // ā_N = ā_n
+          a.abar[m] = ab;                                              // ā_N
         }
         dy0 += ab;
       }
     }
+    __syncthreads();
   }
-  if (lane == 0) { red[warp] = l2; red[32 + warp] = dy0; }
+  // block reduction (threads t < 64 carry the sums)
+  double lw = lsum;
+  float gw = dy0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lw += __shfl_xor_sync(0xffffffffu, lw, o);
+    gw += __shfl_xor_sync(0xffffffffu, gw, o);
+  }
+  __shared__ double lred[2];
+  __shared__ float gred[2];
+  if (t < 64 && lane == 0) { lred[t >> 5] = lw; gred[t >> 5] = gw; }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double L = 0.0;
-    float g0 = 0.0f;
-    for (int i = 0; i < NT / 32; ++i) { L += (double)red[i]; g0 += red[32 + i]; }
-    atomicAdd(a.loss_acc, L);
-    if (!a.eval) atomicAdd(a.grad, g0);
+  if (t == 0) {
+    const double L = lred[0] + lred[1];
+    if (L != 0.0) atomicAdd(a.loss_acc, L);
+    const float g0 = gred[0] + gred[1];
+    if (!a.eval && g0 != 0.0f) atomicAdd(a.grad, g0);
   }
 }
 
-__global__ void __launch_bounds__(NT) k_bwd_simt(PassArgs a, int tiles) {
-  extern __shared__ float sm[];
+__global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int64_t items) {
+  extern __shared__ __align__(16) float sm[];
   const int d = a.d, w = a.w;
   const NetDims nd{d, w};
-  const int n = blockIdx.x / tiles;
-  const int tile = blockIdx.x - n * tiles;
-  const int64_t mloc0 = (int64_t)tile * TP;
-  const int64_t valid = min((int64_t)TP, a.B_local - mloc0);
+  const Pack pk{d, w};
+  float* Xs = sm;                         // [d][64]
+  float* dZ = Xs + d * TP;                // [d][64]  ΔW_n, then dZ_n in place
+  float* H1 = dZ + d * TP;                // [w][64]
+  float* H2 = H1 + w * TP;                // [w][64]
+  float* dH = H2 + w * TP;                // [w][64]  dH2, then dA1 in place
+  float* dA2 = dH + w * TP;               // [w][64]
+  float* Ws = dA2 + w * TP;               // [K <= max(d, w)][128]
+  float* ab = Ws + (d > w ? d : w) * LDW; // [64]
+  uint8_t* m2 = reinterpret_cast<uint8_t*>(ab + TP);   // [w][64] 1[A2 > 0]
+  const float* wp = static_cast<const float*>(a.wpack);
+  float* scratch = a.gpart + (size_t)blockIdx.x * nd.step_size();
+  const int t = threadIdx.x;
   const uint32_t it = a.state->it;
-  float* X = sm;
-  float* dW = X + TP * d;     // ΔW_n, then dZ_n in place
-  float* H1 = dW + TP * d;    // H1, then dA1 in place
-  float* A2 = H1 + TP * w;    // A2, then dA2 in place
-  float* H2 = A2 + TP * w;    // H2, then dH2
-  float* ab = H2 + TP * w;    // ā_{n+1} per path
-  float* Ws = ab + TP;
-  const int lw = odd_ld(w), ld_ = odd_ld(d);
-  const float* P = a.params + nd.step_base(n);
-  float* G = a.grad + nd.step_base(n);
+  const float zc = -a.dt * driver_dfdz_coef(a.problem, a.lam);
+  const int64_t i0 = blockIdx.x * items / gridDim.x, i1 = (blockIdx.x + 1) * items / gridDim.x;
+  const int64_t P = nd.step_size();
+  int cur_n = -1;
 
-  const float* xs = a.Xstore + ((int64_t)n * a.B_local + mloc0) * d;
-  for (int idx = threadIdx.x; idx < TP * d; idx += NT) X[idx] = idx < valid * d ? xs[idx] : 0.0f;
-  if (threadIdx.x < TP) {
-    const int p = threadIdx.x;
-    float v = 0.0f;
-    if (p < valid)
-      v = a.problem == kAllenCahn ? a.abar[(int64_t)n * a.B_local + mloc0 + p] : a.abar[mloc0 + p];
-    ab[p] = v;
+  auto flush = [&]() {   // scratch -> gradient of step cur_n (fp32 atomics), then zero
+    __syncthreads();
+    float* G = a.grad + nd.step_base(cur_n);
+    for (int64_t i = t; i < P; i += NT) {
+      const float v = scratch[i];
+      if (v != 0.0f) atomicAdd(G + i, v);
+      scratch[i] = 0.0f;
+    }
+    __syncthreads();
+  };
+  for (int64_t i = t; i < P; i += NT) scratch[i] = 0.0f;
+  __syncthreads();
+
+  for (int64_t item = i0; item < i1; ++item) {
+    const int n = (int)(item / ntiles), tile = (int)(item - (int64_t)n * ntiles);
+    if (n != cur_n) {
+      if (cur_n >= 0) flush();
+      cur_n = n;
+    }
+    const int64_t mloc0 = (int64_t)tile * TP;
+    const int64_t valid = min((int64_t)TP, a.B_local - mloc0);
+    const float* Pn = a.params + nd.step_base(n);
+    const float* W = wp + (size_t)n * pk.per_step();
+    {
+      const float4* xs = reinterpret_cast<const float4*>(a.Xstore + ((size_t)n * ntiles + tile) * d * TP);
+      for (int i = t; i < d * TP / 4; i += NT) reinterpret_cast<float4*>(Xs)[i] = __ldg(xs + i);
+    }
+    if (t < TP) {
+      const int64_t m = mloc0 + t;
+      ab[t] = t < valid ? (a.problem == kAllenCahn ? a.abar[(int64_t)n * a.B_local + m] : a.abar[m])
+                        : 0.0f;
+    }
+    gen_dw(dZ, d, a.m0 + mloc0, valid, n, it, a.k0, a.k1, a.sqrt_dt);
+    stage(Ws, W + pk.w1t(), d * LDW);
+    __syncthreads();
+    const float* b1 = Pn + nd.off_b1();
+    gemm_n(Xs, Ws, d, w, [&](int p0, int j, float4 v) {           // recompute H1
+      const float b = __ldg(b1 + j);
+      *reinterpret_cast<float4*>(H1 + j * TP + p0) =
+          make_float4(fmaxf(v.x + b, 0.f), fmaxf(v.y + b, 0.f), fmaxf(v.z + b, 0.f), fmaxf(v.w + b, 0.f));
+    });
+    __syncthreads();
+    stage(Ws, W + pk.w2t(), w * LDW);
+    __syncthreads();
+    const float* b2 = Pn + nd.off_b2();
+    gemm_n(H1, Ws, w, w, [&](int p0, int j, float4 v) {           // recompute H2, mask of A2
+      const float b = __ldg(b2 + j);
+      const float4 h = *reinterpret_cast<const float4*>(H1 + j * TP + p0);
+      const float av[4] = {v.x + b, v.y + b, v.z + b, v.w + b};
+      *reinterpret_cast<float4*>(H2 + j * TP + p0) =
+          make_float4(h.x + fmaxf(av[0], 0.f), h.y + fmaxf(av[1], 0.f), h.z + fmaxf(av[2], 0.f),
+                      h.w + fmaxf(av[3], 0.f));
+      uchar4 mk;
+      mk.x = av[0] > 0.f; mk.y = av[1] > 0.f; mk.z = av[2] > 0.f; mk.w = av[3] > 0.f;
+      *reinterpret_cast<uchar4*>(m2 + j * TP + p0) = mk;
+    });
+    __syncthreads();
+    stage(Ws, W + pk.w3t(), w * LDW);
+    __syncthreads();
+    const float* b3 = Pn + nd.off_b3();
+    gemm_n(H2, Ws, w, d, [&](int p0, int j, float4 v) {           // dZ = ā(ΔW - Δt ∂_z f)
+      const float b = __ldg(b3 + j);
+      float4 dw = *reinterpret_cast<const float4*>(dZ + j * TP + p0);
+      dw.x = ab[p0] * fmaf(zc, v.x + b, dw.x);
+      dw.y = ab[p0 + 1] * fmaf(zc, v.y + b, dw.y);
+      dw.z = ab[p0 + 2] * fmaf(zc, v.z + b, dw.z);
+      dw.w = ab[p0 + 3] * fmaf(zc, v.w + b, dw.w);
+      *reinterpret_cast<float4*>(dZ + j * TP + p0) = dw;
+    });
+    __syncthreads();
+    stage(Ws, W + pk.w3n(), d * LDW);
+    // dW3 += dZᵀ H2 ; db3 += Σ dZ   (while W3 is being staged)
+    gemm_t(dZ, d, H2, w, scratch + nd.off_W3(), w, scratch + nd.off_b3());
+    __syncthreads();
+    gemm_n(dZ, Ws, d, w, [&](int p0, int j, float4 v) {           // dH2 = dZ W3 ; dA2
+      *reinterpret_cast<float4*>(dH + j * TP + p0) = v;
+      const uchar4 mk = *reinterpret_cast<const uchar4*>(m2 + j * TP + p0);
+      *reinterpret_cast<float4*>(dA2 + j * TP + p0) =
+          make_float4(mk.x ? v.x : 0.f, mk.y ? v.y : 0.f, mk.z ? v.z : 0.f, mk.w ? v.w : 0.f);
+    });
+    __syncthreads();
+    stage(Ws, W + pk.w2n(), w * LDW);
+    // dW2 += dA2ᵀ H1 ; db2 += Σ dA2
+    gemm_t(dA2, w, H1, w, scratch + nd.off_W2(), w, scratch + nd.off_b2());
+    __syncthreads();
+    gemm_n(dA2, Ws, w, w, [&](int p0, int j, float4 v) {          // dA1 = (dH2 + dA2 W2) ⊙ 1[H1 > 0]
+      const float4 h = *reinterpret_cast<const float4*>(H1 + j * TP + p0);
+      const float4 g = *reinterpret_cast<const float4*>(dH + j * TP + p0);
+      *reinterpret_cast<float4*>(dH + j * TP + p0) =
+          make_float4(h.x > 0.f ? g.x + v.x : 0.f, h.y > 0.f ? g.y + v.y : 0.f,
+                      h.z > 0.f ? g.z + v.z : 0.f, h.w > 0.f ? g.w + v.w : 0.f);
+    });
+    __syncthreads();
+    // dW1 += dA1ᵀ X ; db1 += Σ dA1
+    gemm_t(dH, w, Xs, d, scratch + nd.off_W1(), d, scratch + nd.off_b1());
+    __syncthreads();
   }
-  gen_dw(dW, d, a.m0 + mloc0, valid, n, it, a.k0, a.k1, a.sqrt_dt);
-  stage_rows(Ws, ld_, P + nd.off_W1(), w, d);
-  __syncthreads();
-  // recompute the forward of step n (activation recompute)
-  const float* b1 = P + nd.off_b1();
-  gemm_tp<true>(X, d, d, Ws, ld_, w, [&](int p, int j, float v) {
-    H1[p * w + j] = fmaxf(v + __ldg(b1 + j), 0.0f);
-  });
-  __syncthreads();
-  stage_rows(Ws, lw, P + nd.off_W2(), w, w);
-  __syncthreads();
-  const float* b2 = P + nd.off_b2();
-  gemm_tp<true>(H1, w, w, Ws, lw, w, [&](int p, int j, float v) {
-    const float a2 = v + __ldg(b2 + j);
-    A2[p * w + j] = a2;
-    H2[p * w + j] = H1[p * w + j] + fmaxf(a2, 0.0f);
-  });
-  __syncthreads();
-  stage_rows(Ws, lw, P + nd.off_W3(), d, w);
-  __syncthreads();
-  const float* b3 = P + nd.off_b3();
-  const float zc = -a.dt * driver_dfdz_coef(a.problem, a.lam);   // dZ = ā(ΔW - Δt ∂_z f)
-  gemm_tp<true>(H2, w, w, Ws, lw, d, [&](int p, int j, float v) {
-    const float z = v + __ldg(b3 + j);
-    dW[p * d + j] = ab[p] * fmaf(zc, z, dW[p * d + j]);
-  });
-  __syncthreads();
-  // dW3 += dZᵀ H2 ; db3 += Σ dZ
-  wgrad_tp(dW, d, d, H2, w, w, G + nd.off_W3(), G + nd.off_b3());
-  stage_copy(Ws, P + nd.off_W3(), d * w);
-  __syncthreads();
-  // dH2 = dZ W3 ; dA2 = dH2 ⊙ 1[A2 > 0]  (ReLU'(0) = 0, R15)
-  gemm_tp<false>(dW, d, d, Ws, w, w, [&](int p, int j, float v) {
-    H2[p * w + j] = v;
-    A2[p * w + j] = A2[p * w + j] > 0.0f ? v : 0.0f;
-  });
-  __syncthreads();
-  // dW2 += dA2ᵀ H1 ; db2 += Σ dA2
-  wgrad_tp(A2, w, w, H1, w, w, G + nd.off_W2(), G + nd.off_b2());
-  stage_copy(Ws, P + nd.off_W2(), w * w);
-  __syncthreads();
-  // dH1 = dH2 + dA2 W2 ; dA1 = dH1 ⊙ 1[A1 > 0]  (A1 > 0 ⟺ H1 > 0)
-  gemm_tp<false>(A2, w, w, Ws, w, w, [&](int p, int j, float v) {
-    const float dh1 = H2[p * w + j] + v;
-    H1[p * w + j] = H1[p * w + j] > 0.0f ? dh1 : 0.0f;
-  });
-  __syncthreads();
-  // dW1 += dA1ᵀ X ; db1 += Σ dA1
-  wgrad_tp(H1, w, w, X, d, d, G + nd.off_W1(), G + nd.off_b1());
+  if (cur_n >= 0) flush();
 }
 
 size_t fwd_smem(int d, int w) {
-  const size_t ws = (size_t)max(w * odd_ld(d), max(w * odd_ld(w), d * odd_ld(w)));
-  return sizeof(float) * ((size_t)TP * (3 * d + 2 * w) + TP + 64 + ws);
+  return sizeof(float) * ((size_t)TP * (2 * d + 2 * w) + (size_t)(d > w ? d : w) * LDW + TP + 16);
 }
 size_t bwd_smem(int d, int w) {
-  const size_t ws = (size_t)max(w * odd_ld(d), max(w * odd_ld(w), d * odd_ld(w)));
-  return sizeof(float) * ((size_t)TP * (2 * d + 3 * w) + TP + ws);
+  return sizeof(float) * ((size_t)TP * (2 * d + 4 * w) + (size_t)(d > w ? d : w) * LDW + TP) +
+         (size_t)w * TP;
+}
+int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
 }
 
 }  // namespace
 
+bool simt_supported(int d, int w) { return d <= 128 && w <= 128 && bwd_smem(d, w) <= 227 * 1024; }
+size_t simt_max_smem(int d, int w) { return fwd_smem(d, w) > bwd_smem(d, w) ? fwd_smem(d, w) : bwd_smem(d, w); }
+size_t simt_pack_bytes(int d, int w, int N) { return (size_t)N * Pack{d, w}.per_step() * sizeof(float); }
+size_t simt_xstore_bytes(int d, int N, int64_t B_local) {
+  return (size_t)N * (size_t)((B_local + TP - 1) / TP) * d * TP * sizeof(float);
+}
+size_t simt_scratch_bytes(int d, int w) { return (size_t)sm_count() * NetDims{d, w}.step_size() * sizeof(float); }
+
+cudaError_t launch_pack_simt(const PassArgs& a, cudaStream_t s) {
+  const int64_t total = (int64_t)a.N * Pack{a.d, a.w}.per_step();
+  int grid = (int)((total + NT - 1) / NT);
+  if (grid > 148 * 16) grid = 148 * 16;
+  k_pack_simt<<<grid, NT, 0, s>>>(a.params, static_cast<float*>(const_cast<void*>(a.wpack)), a.d, a.w, a.N);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fwd_simt(const PassArgs& a, cudaStream_t s) {
   const size_t smem = fwd_smem(a.d, a.w);
-  cudaError_t e = cudaFuncSetAttribute(k_fwd_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_fwd_simt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int grid = (int)((a.B_local + TP - 1) / TP);
-  k_fwd_simt<<<grid, NT, smem, s>>>(a);
+  const int ntiles = (int)((a.B_local + TP - 1) / TP), sms = sm_count();
+  k_fwd_simt<<<ntiles < sms ? ntiles : sms, NT, smem, s>>>(a, ntiles);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bwd_simt(const PassArgs& a, cudaStream_t s) {
   const size_t smem = bwd_smem(a.d, a.w);
-  cudaError_t e = cudaFuncSetAttribute(k_bwd_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_bwd_simt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int tiles = (int)((a.B_local + TP - 1) / TP);
-  k_bwd_simt<<<a.N * tiles, NT, smem, s>>>(a, tiles);
+  const int ntiles = (int)((a.B_local + TP - 1) / TP), sms = sm_count();
+  const int64_t items = (int64_t)ntiles * a.N;
+  k_bwd_simt<<<(int)(items < sms ? items : sms), NT, smem, s>>>(a, ntiles, items);
   return cudaGetLastError();
 }
-
-size_t simt_max_smem(int d, int w) { return fwd_smem(d, w) > bwd_smem(d, w) ? fwd_smem(d, w) : bwd_smem(d, w); }
 
 }  // namespace bsde
