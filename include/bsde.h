@@ -184,6 +184,13 @@ int bsde_debug_residuals(const bsde_ctx* ctx, int64_t m0, int64_t count, float* 
  * (both MN-major, rows >= 112 of D undefined).  Row-major host arrays.  Synchronises. */
 int bsde_debug_umma(int mode, const float* a, const float* b, float* d_out);
 
+/* Profiling hook: runs one forward (which = 0) or forward + adjoint (which = 1)
+ * pass of the current iteration with a clock64() trace of CTA 0 enabled and
+ * copies up to n stamps to host out[] (16 slots per step/item, 0 = unused; see
+ * tc.cu CLK points).  Overwrites the gradient buffer.  tcgen05 path only.
+ * Synchronises. */
+int bsde_debug_phase_clocks(bsde_ctx* ctx, int which, uint64_t* out, int n);
+
 /* Profiling hook for the bench's roofline figures: runs `steps` training
  * iterations (eagerly, no graph) with CUDA events recorded on cfg.stream
  * between the phases of the step and returns the mean duration of each phase

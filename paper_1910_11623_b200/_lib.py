@@ -23,7 +23,8 @@ SYMBOLS = [
     "bsde_num_params", "bsde_get_params", "bsde_set_params", "bsde_get_grads",
     "bsde_get_adam_state", "bsde_set_adam_state", "bsde_get_iteration", "bsde_set_iteration",
     "bsde_current_steps", "bsde_compute_grad", "bsde_eval_loss", "bsde_debug_philox",
-    "bsde_debug_dw", "bsde_debug_dw_fast", "bsde_debug_residuals", "bsde_debug_umma", "bsde_profile_steps",
+    "bsde_debug_dw", "bsde_debug_dw_fast", "bsde_debug_residuals", "bsde_debug_umma",
+    "bsde_debug_phase_clocks", "bsde_profile_steps",
     "bsde_launches_per_step", "bsde_kernel_family", "bsde_nccl_unique_id", "bsde_last_error",
     "bsde_destroy",
 ]
@@ -91,6 +92,7 @@ def lib():
             "bsde_debug_residuals": (I32, [P, I64, I64, pF]),
             "bsde_debug_umma": (I32, [I32, pF, pF, pF]),
             "bsde_profile_steps": (I32, [P, I32, pF, I32]),
+            "bsde_debug_phase_clocks": (I32, [P, I32, ctypes.POINTER(ctypes.c_uint64), I32]),
             "bsde_launches_per_step": (I32, [P, ctypes.POINTER(I32)]),
             "bsde_kernel_family": (ctypes.c_char_p, [P]),
             "bsde_nccl_unique_id": (I32, [P]),

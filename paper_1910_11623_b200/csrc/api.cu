@@ -697,6 +697,27 @@ int bsde_profile_steps(bsde_ctx* ctx, int steps, float* ms_out, int n_out) {
   return rc;
 }
 
+int bsde_debug_phase_clocks(bsde_ctx* ctx, int which, uint64_t* out, int n) {
+  if (!ctx || !out || n < 1 || (which != 0 && which != 1) || ctx->family != BSDE_KERNEL_TC)
+    return fail(ctx, BSDE_EINVAL, "debug_phase_clocks: bad argument (tcgen05 path only)");
+  unsigned long long* buf = nullptr;
+  CK(cudaMalloc(&buf, (size_t)n * sizeof(uint64_t)));
+  CK(cudaMemsetAsync(buf, 0, (size_t)n * sizeof(uint64_t), ctx->stream));
+  const int64_t np = num_params_at(ctx, ctx->N);
+  PassArgs a = pass_args(ctx);
+  CK(launch_begin_step(ctx->state, ctx->grad, np, ctx->stream));
+  if (which == 0) a.clk = buf;
+  CK(launch_fwd_tc(a, ctx->stream));
+  if (which == 1) {
+    a.clk = buf;
+    CK(launch_bwd_tc(a, ctx->stream));
+  }
+  CK(cudaMemcpyAsync(out, buf, (size_t)n * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(buf);
+  return BSDE_OK;
+}
+
 int bsde_launches_per_step(const bsde_ctx* ctx, int* n) {
   if (!ctx || !n) return BSDE_EINVAL;
   *n = ctx->launches;

@@ -27,7 +27,8 @@ struct PassArgs {
   // tcgen05 path only
   const void* wpack;                   // packed bf16 weight images (see tc.cu)
   void* xpack;                         // bf16 X store (BF16 precision)
-  float* gpart;                        // reserved (unused)
+  float* gpart;                        // SIMT adjoint: per-CTA scratch gradients
+  unsigned long long* clk;             // debug: per-phase clock64() trace of CTA 0 (or null)
   int precision;
 };
 

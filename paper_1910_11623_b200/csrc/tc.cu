@@ -172,6 +172,9 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
   };
   if (t == 0 && total_seq > 0) load_weights(0);
 
+  // debug trace: thread 32 of CTA 0 stamps clock64() at the phase boundaries of its steps
+  unsigned long long* const clk = (a.clk && blockIdx.x == 0 && t == 32) ? a.clk : nullptr;
+#define CLK(i) do { if (clk && s < 64) clk[s * 16 + (i)] = clock64(); } while (0)
   uint32_t mph = 0;
   int64_t s = 0;
   double lsum = 0.0;
@@ -186,6 +189,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
     float Y = a.params[0];
     for (int n = 0; n < N; ++n, ++s) {
       uint8_t* wimg = (s & 1) ? wimg1 : wimg0;
+      CLK(0);
       if (t == 0 && s + 1 < total_seq) load_weights(s + 1);
       // X_n operand chunks (bf16; column D is the constant 1 of the folded bias)
 #pragma unroll
@@ -201,7 +205,9 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
         }
       }
       fence_async_smem();
+      CLK(1);
       __syncthreads();
+      CLK(2);
       if (n > 0) {   // finish a4 of step n-1 from the partial sums of the four threads
         const float2 r0 = red[row], r1 = red[128 + row], r2 = red[256 + row], r3 = red[384 + row];
         const float cz = (r0.x + r1.x) + (r2.x + r3.x), zz = (r0.y + r1.y) + (r2.y + r3.y);
@@ -222,8 +228,10 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
       float dw[32];                                // a1: ΔW_n, generated while the GEMMs run
       const DwGen gen{mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt, g};
       gen.run<D, 0, 3>(dw);
+      CLK(3);
       mbar_wait(&bars[2], mph);
       mph ^= 1;
+      CLK(4);
       tc_after();
       {  // H1 = ReLU(A1)
         float v[32];
@@ -239,15 +247,19 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
       }
       fence_async_smem();
       tc_before();
+      CLK(5);
       __syncthreads();
+      CLK(6);
       if (t == 0) {
         tc_after();
         gemm(tm + 128, kmaj(hop, Wp), kmaj(wimg + Dm::W1B, Wp), Wp / 16, I1, false);   // A2
         mma_commit(&bars[2]);
       }
       gen.run<D, 3, 6>(dw);
+      CLK(7);
       mbar_wait(&bars[2], mph);
       mph ^= 1;
+      CLK(8);
       tc_after();
       {  // H2 = ReLU(A1) + ReLU(A2) (residual block, Eq. 7 with h = 1), over H1 in hop
         float v1[32], v2[32];
@@ -266,15 +278,19 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
       fence_async_smem();
       tc_before();
       if (t == 0 && !a.eval) bulk_wait_read0();   // the X_n image has left xop
+      CLK(9);
       __syncthreads();
+      CLK(10);
       if (t == 0) {
         tc_after();
         gemm(tm, kmaj(hop, Wp), kmaj(wimg + Dm::W1B + Dm::W2B, Wp), Wp / 16, I3, false);  // Z
         mma_commit(&bars[2]);
       }
       gen.run<D, 6, 8>(dw);
+      CLK(11);
       mbar_wait(&bars[2], mph);
       mph ^= 1;
+      CLK(12);
       tc_after();
       float cz = 0.0f, zz = 0.0f;
       {  // a4 partials c = Z·ΔW, |Z|²; a2: X += √2 ΔW
@@ -293,6 +309,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
         }
       }
       red[g * 128 + row] = make_float2(cz, zz);   // a4 is finished at the next step's barrier
+      CLK(13);
       tc_before();
     }
     // a5: R = Y_N - g(X_N); loss; ā recursion and dY0
@@ -351,6 +368,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
     tc_after();
     tmem_dealloc(tm, 256);
   }
+#undef CLK
 }
 
 // ------------------------------------------------------------------ adjoint
@@ -409,6 +427,8 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   }
 
   uint32_t mph = 0, wph = 0, gph = 0, g5ph = 0, g7ph = 0;
+  unsigned long long* const clk = (a.clk && blockIdx.x == 0 && t == 32) ? a.clk : nullptr;
+#define CLK(i) do { if (clk && item - i0 < 64) clk[(item - i0) * 16 + (i)] = clock64(); } while (0)
   int cur_n = -1;
   bool first = true;
   bool g8_pending = false;
@@ -474,6 +494,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       cur_n = n;
       first = true;
     }
+    CLK(0);
     const int64_t mloc = (int64_t)tile * 128 + row;
     const bool valid = mloc < a.B_local;
     const uint32_t mg = (uint32_t)(a.m0 + mloc);
@@ -491,6 +512,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     gen.run<D, 0, 3>(dw);
     mbar_wait(&bars[3], mph);
     mph ^= 1;
+    CLK(1);
     if (g8_pending) {            // the previous item's G7, G8 were issued before G1
       mbar_wait(&bars[6], g7ph);
       g7ph ^= 1;
@@ -516,6 +538,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     fence_async_smem();
     tc_before();
     __syncthreads();
+    CLK(2);
     if (t == 0) {   // G2: A2 = H1 W̃2ᵀ
       tc_after();
       gemm(acc, kmaj(hop, Wp), kmaj(wimg + Dm::W1B, Wp), Wp / 16, IW, false);
@@ -524,6 +547,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     gen.run<D, 3, 6>(dw);
     mbar_wait(&bars[3], mph);
     mph ^= 1;
+    CLK(3);
     tc_after();
     {  // H2 = H1 (bf16 copy, R17) + ReLU(A2), chunk by chunk
       float v[32];
@@ -544,6 +568,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     fence_async_smem();
     tc_before();
     __syncthreads();
+    CLK(4);
     if (t == 0) {   // G3: Z = H2 W̃3ᵀ
       tc_after();
       gemm(acc, kmaj(b2, Wp), kmaj(wimg + Dm::W1B + Dm::W2B, Wp), Wp / 16, ID, false);
@@ -552,6 +577,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     gen.run<D, 6, 8>(dw);
     mbar_wait(&bars[3], mph);
     mph ^= 1;
+    CLK(5);
     tc_after();
     {  // dZ = ā_{n+1}(ΔW_n - Δt ∂_z f), columns >= D zero
       float z[32];
@@ -566,6 +592,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     fence_async_smem();
     tc_before();
     __syncthreads();
+    CLK(6);
     if (t == 0) {
       tc_after();
       // G4: dH2 = dZ W̃3 ; G5: dW̃3 += dZᵀ H2
@@ -576,6 +603,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     }
     mbar_wait(&bars[3], mph);
     mph ^= 1;
+    CLK(7);
     tc_after();
     {  // dA2 = dH2 ⊙ 1[A2 > 0]  (computed while G5 runs; stored over H2 once G5 is done)
       float v[32];
@@ -584,6 +612,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       for (int i = 0; i < 32; ++i) v[i] = (m2 >> i) & 1u ? v[i] : 0.0f;
       mbar_wait(&bars[5], g5ph);
       g5ph ^= 1;
+      CLK(8);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         if (chunk_lt(g, i, Wp / 8))st_chunk(b2, row, g + 4 * i, Wp, v + 8 * i);
@@ -591,6 +620,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     fence_async_smem();
     tc_before();
     __syncthreads();
+    CLK(9);
     if (t == 0) {
       tc_after();
       // G6: dH1 = dH2 + dA2 W̃2 (accumulated onto dH2) ; G7: dW̃2 += dA2ᵀ H1
@@ -601,6 +631,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     }
     mbar_wait(&bars[3], mph);
     mph ^= 1;
+    CLK(10);
     tc_after();
     {  // dA1 = dH1 ⊙ 1[A1 > 0]
       float v[32];
@@ -614,6 +645,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     fence_async_smem();
     tc_before();
     __syncthreads();
+    CLK(11);
     if (t == 0) {   // G8: dW̃1 += dA1ᵀ X̃
       tc_after();
       gemm(G1, mnmaj(b3, Wp), mnmaj(xop, Dp), 128 / 16, IGD, !first);
@@ -621,12 +653,14 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     }
     g8_pending = true;
     first = false;
+    CLK(12);
   }
   if (cur_n >= 0) flush();
   if (warp == 0) {
     tc_after();
     tmem_dealloc(tm, 512);
   }
+#undef CLK
 }
 
 // ------------------------------------------------------------------ UMMA self-test

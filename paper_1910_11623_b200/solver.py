@@ -220,6 +220,13 @@ class BSDE:
         self._ck(self._L.bsde_profile_steps(self._h, int(steps), _fptr(out), 6))
         return dict(zip(self.PHASES, out.tolist()))
 
+    def debug_phase_clocks(self, which, n=1024):
+        """clock64() stamps of CTA 0 (16 per step / item; 0 = unused), see tc.cu CLK."""
+        out = np.zeros(n, np.uint64)
+        self._ck(self._L.bsde_debug_phase_clocks(
+            self._h, int(which), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), n))
+        return out.reshape(-1, 16)
+
     def debug_residuals(self, m0, count):
         out = np.empty(count, np.float32)
         self._ck(self._L.bsde_debug_residuals(self._h, int(m0), int(count), _fptr(out)))
