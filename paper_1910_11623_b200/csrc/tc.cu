@@ -104,17 +104,44 @@ struct DwGen {
   int g;   // slot s = (i, h) = (s/2, s%2) holds 4-block 2(g+4i)+h
   // slots [S0, S1) — a compile-time share of the step's RNG, issued right after
   // a GEMM so that the generation overlaps it
+  // The Philox rounds of all slots are interleaved (independent dependency chains
+  // give the scheduler ILP), then the Box-Muller maps.  Slots whose columns are
+  // >= D for every column group are skipped at compile time.
   template <int D, int S0, int S1>
   __device__ __forceinline__ void run(float (&dw)[32]) const {
+    constexpr int K = S1 - S0;
+    uint4 c[K];
 #pragma unroll
-    for (int s = S0; s < S1; ++s) {
-      const int i = s / 2, h = s % 2;
-      float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (col_lt(g, i, 4 * h, D)) z = dw4_fast((uint32_t)(2 * (g + 4 * i) + h), m, n, it, k0, k1, sdt);
-      dw[8 * i + 4 * h + 0] = z.x;
-      dw[8 * i + 4 * h + 1] = z.y;
-      dw[8 * i + 4 * h + 2] = z.z;
-      dw[8 * i + 4 * h + 3] = z.w;
+    for (int j = 0; j < K; ++j) {
+      const int s = S0 + j;
+      c[j] = make_uint4((uint32_t)(2 * (g + 4 * (s / 2)) + s % 2), m, n, it);
+    }
+    uint32_t a0 = k0, a1 = k1;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      if (r) { a0 += kPhiloxW0; a1 += kPhiloxW1; }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const int s = S0 + j;
+        if (8 * (4 * (s / 2)) + 4 * (s % 2) >= D) continue;   // never valid
+        const uint32_t lo0 = kPhiloxM0 * c[j].x, hi0 = __umulhi(kPhiloxM0, c[j].x);
+        const uint32_t lo1 = kPhiloxM1 * c[j].z, hi1 = __umulhi(kPhiloxM1, c[j].z);
+        c[j] = make_uint4(hi1 ^ c[j].y ^ a0, lo1, hi0 ^ c[j].w ^ a1, lo0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int s = S0 + j, i = s / 2, h = s % 2;
+      float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+      if (8 * (4 * i) + 4 * h < D) {
+        box_muller_fast(c[j].x, c[j].y, sdt, z0, z1);
+        box_muller_fast(c[j].z, c[j].w, sdt, z2, z3);
+      }
+      const bool ok = col_lt(g, i, 4 * h, D);
+      dw[8 * i + 4 * h + 0] = ok ? z0 : 0.f;
+      dw[8 * i + 4 * h + 1] = ok ? z1 : 0.f;
+      dw[8 * i + 4 * h + 2] = ok ? z2 : 0.f;
+      dw[8 * i + 4 * h + 3] = ok ? z3 : 0.f;
     }
   }
 };
@@ -227,7 +254,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
       }
       float dw[32];                                // a1: ΔW_n, generated while the GEMMs run
       const DwGen gen{mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt, g};
-      gen.run<D, 0, 3>(dw);
+      gen.run<D, 0, 4>(dw);
       CLK(3);
       mbar_wait(&bars[2], mph);
       mph ^= 1;
@@ -255,7 +282,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
         gemm(tm + 128, kmaj(hop, Wp), kmaj(wimg + Dm::W1B, Wp), Wp / 16, I1, false);   // A2
         mma_commit(&bars[2]);
       }
-      gen.run<D, 3, 6>(dw);
+      gen.run<D, 4, 8>(dw);
       CLK(7);
       mbar_wait(&bars[2], mph);
       mph ^= 1;
@@ -286,7 +313,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
         gemm(tm, kmaj(hop, Wp), kmaj(wimg + Dm::W1B + Dm::W2B, Wp), Wp / 16, I3, false);  // Z
         mma_commit(&bars[2]);
       }
-      gen.run<D, 6, 8>(dw);
+      // (all ΔW slots generated during G1 and G2)
       CLK(11);
       mbar_wait(&bars[2], mph);
       mph ^= 1;
@@ -509,7 +536,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     }
     float dw[32];   // ΔW_n regenerated (Philox) while G1..G3 run
     const DwGen gen{mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt, g};
-    gen.run<D, 0, 3>(dw);
+    gen.run<D, 0, 4>(dw);
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     CLK(1);
@@ -544,7 +571,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       gemm(acc, kmaj(hop, Wp), kmaj(wimg + Dm::W1B, Wp), Wp / 16, IW, false);
       mma_commit(&bars[3]);
     }
-    gen.run<D, 3, 6>(dw);
+    gen.run<D, 4, 8>(dw);
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     CLK(3);
@@ -574,7 +601,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       gemm(acc, kmaj(b2, Wp), kmaj(wimg + Dm::W1B + Dm::W2B, Wp), Wp / 16, ID, false);
       mma_commit(&bars[3]);
     }
-    gen.run<D, 6, 8>(dw);
+    // (all ΔW slots generated during G1 and G2)
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     CLK(5);
