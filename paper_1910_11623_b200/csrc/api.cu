@@ -25,6 +25,7 @@ cudaError_t launch_pack_simt(const PassArgs& a, cudaStream_t s);
 bool tc_supported(int d, int w);
 cudaError_t launch_fwd_tc(const PassArgs& a, cudaStream_t s);
 cudaError_t launch_bwd_tc(const PassArgs& a, cudaStream_t s);
+cudaError_t launch_paths_tc(const PassArgs& a, cudaStream_t s);
 cudaError_t launch_pack_weights(const PassArgs& a, cudaStream_t s);
 size_t tc_pack_bytes(int d, int w, int N, int precision);
 size_t tc_xstore_bytes(int d, int w, int N, int64_t B_local);
@@ -87,7 +88,8 @@ struct bsde_ctx {
   float *scratch = nullptr, *Xstore = nullptr, *Ystore = nullptr, *abar = nullptr;
   float* Rstore = nullptr;
   void* wpack = nullptr;
-  void* xpack = nullptr;
+  void* xpack = nullptr;        // tcgen05 path: fp16 ΔW_n images
+  float* xn2 = nullptr;         // tcgen05 path: |X_N|² per path
   float* gpart = nullptr;
   DeviceState* state = nullptr;
   double* eval_loss = nullptr;
@@ -154,6 +156,8 @@ PassArgs pass_args(bsde_ctx* c) {
   a.wpack = c->wpack;
   a.xpack = c->Xstore;   // the tcgen05 path stores X_n as bf16 operand images
   a.gpart = c->gpart;
+  a.dwpack = c->xpack;
+  a.xn2 = c->xn2;
   a.precision = c->cfg.precision;
   return a;
 }
@@ -170,6 +174,8 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
   launches += 1;   // k_begin_step (the memset is not a kernel)
   mark(1);
   if (ctx->family == BSDE_KERNEL_TC) {
+    CK(launch_paths_tc(a, ctx->stream));
+    launches += 1;
     CK(launch_fwd_tc(a, ctx->stream));
     mark(2);
     CK(launch_bwd_tc(a, ctx->stream));
@@ -223,7 +229,8 @@ int repack(bsde_ctx* ctx) {
 void free_all(bsde_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   void* bufs[] = {c->params, c->grad, c->adam_m, c->adam_v, c->scratch, c->Xstore, c->Ystore,
-                  c->abar, c->Rstore, c->wpack, c->xpack, c->gpart, c->state, c->eval_loss};
+                  c->abar, c->Rstore, c->wpack, c->xpack, c->xn2, c->gpart, c->state,
+                  c->eval_loss};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
@@ -374,6 +381,8 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     allocs.push_back({(void**)&ctx->Ystore, (size_t)ctx->N_max * ctx->B_local * sizeof(float)});
   if (family == BSDE_KERNEL_TC) {
     allocs.push_back({&ctx->wpack, tc_pack_bytes(d, w, ctx->N_max, cfg.precision)});
+    allocs.push_back({&ctx->xpack, tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)});
+    allocs.push_back({(void**)&ctx->xn2, (size_t)ctx->B_local * sizeof(float)});
   } else {
     allocs.push_back({&ctx->wpack, simt_pack_bytes(d, w, ctx->N_max)});
     allocs.push_back({(void**)&ctx->gpart, simt_scratch_bytes(d, w)});
@@ -604,7 +613,14 @@ int bsde_eval_loss(bsde_ctx* ctx, uint32_t eval_id, int64_t batch, double* loss_
   a.loss_acc = ctx->eval_loss;
   CK(cudaMemsetAsync(ctx->eval_loss, 0, sizeof(double), ctx->stream));
   if (ctx->family == BSDE_KERNEL_TC) {
-    CK(launch_fwd_tc(a, ctx->stream));
+    // the path images are sized for B_local paths: evaluate in chunks of them
+    const int64_t local = a.B_local, m_first = a.m0;
+    for (int64_t off = 0; off < local; off += ctx->B_local) {
+      a.B_local = local - off < ctx->B_local ? local - off : ctx->B_local;
+      a.m0 = m_first + off;
+      CK(launch_paths_tc(a, ctx->stream));
+      CK(launch_fwd_tc(a, ctx->stream));
+    }
   } else {
     CK(launch_fwd_simt(a, ctx->stream));
   }
@@ -706,6 +722,7 @@ int bsde_debug_phase_clocks(bsde_ctx* ctx, int which, uint64_t* out, int n) {
   const int64_t np = num_params_at(ctx, ctx->N);
   PassArgs a = pass_args(ctx);
   CK(launch_begin_step(ctx->state, ctx->grad, np, ctx->stream));
+  CK(launch_paths_tc(a, ctx->stream));
   if (which == 0) a.clk = buf;
   CK(launch_fwd_tc(a, ctx->stream));
   if (which == 1) {

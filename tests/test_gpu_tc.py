@@ -191,7 +191,7 @@ def test_nccl_one_rank_communicator_matches_local():
                nccl_id=nccl_unique_id(), world=1, rank=0)
     la = [ref.train_step() for _ in range(3)]
     lb = [com.train_step() for _ in range(3)]
-    assert np.allclose(la, lb, rtol=1e-6)
+    assert abs(la[0] - lb[0]) <= 1e-6 * la[0] and np.allclose(la, lb, rtol=1e-4)
     # fp32 atomics make the two gradients differ in the last bits; Adam can flip
     # the step of a near-zero gradient component (at most 2·lr per step)
     diff = np.abs(ref.get_params() - com.get_params())
