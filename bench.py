@@ -260,6 +260,14 @@ def main():
             bound, peak = "alu", 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
             pk_name = "fp32 FFMA: 148 SM x 128 lanes x 2 flop x sm_max_mhz (derived)"
         dom = "bwd" if phase["bwd"] >= phase["fwd"] else "fwd"
+        traffic, traffic_src = None, None
+        try:   # dram bytes per launch from one `ncu --set full` capture (tools/ncu_traffic.py)
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                tr = json.load(f).get(wl.name, {}).get("bsde_" + dom)
+            if tr and world == 1:
+                traffic, traffic_src = tr["bytes_per_launch"], "profiles/" + tr["source"]
+        except Exception:
+            pass
         flops = B_local * wl.N * (bwd_flops(wl.d, wl.w) if dom == "bwd" else fwd_flops(wl.d, wl.w))
         achieved = flops / (phase[dom] * 1e-3) / 1e12
         step_flops = wl.batch * wl.N * (fwd_flops(wl.d, wl.w) + bwd_flops(wl.d, wl.w)) / world
@@ -272,7 +280,8 @@ def main():
             "config": config_dict(wl, world, family),
             "roofline": {"bound": bound, "kernel": "bsde_" + dom, "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": pk_name + "; " + pk["source"],
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": pk_name + "; " + pk["source"],
                          "algorithmic_flop_per_path_step": bwd_flops(wl.d, wl.w) if dom == "bwd"
                          else fwd_flops(wl.d, wl.w)},
             "step_roofline": {"achieved_tflops": step_flops / (ms * 1e-3) / 1e12,
