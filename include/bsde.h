@@ -181,7 +181,8 @@ int bsde_debug_residuals(const bsde_ctx* ctx, int64_t m0, int64_t count, float* 
  * M=128, N=112 bf16 UMMA on the current device with fp32 host inputs rounded to
  * bf16.  mode 0: D[128×112] = A[128×112]·B[112×112]ᵀ (both K-major);
  * mode 1: D = A[128×112]·B[112×112] (B MN-major); mode 2: D = A[128×112]ᵀ·B[128×112]
- * (both MN-major, rows >= 112 of D undefined).  Row-major host arrays.  Synchronises. */
+ * (both MN-major, rows >= 112 of D undefined); mode 3: as mode 0 with A staged in
+ * tensor memory (the forward's TMEM A operands).  Row-major host arrays.  Synchronises. */
 int bsde_debug_umma(int mode, const float* a, const float* b, float* d_out);
 
 /* Profiling hook: runs one forward (which = 0) or forward + adjoint (which = 1)

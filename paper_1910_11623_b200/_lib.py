@@ -7,7 +7,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbsde.so")
+# BSDE_LIB: an alternative build of the same library (kernel experiments)
+LIB_PATH = os.environ.get("BSDE_LIB") or os.path.join(_HERE, "libbsde.so")
 
 HEAT, HJB, ALLEN_CAHN = 0, 1, 2
 FP32, BF16 = 0, 1

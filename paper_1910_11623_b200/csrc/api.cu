@@ -25,7 +25,6 @@ cudaError_t launch_pack_simt(const PassArgs& a, cudaStream_t s);
 bool tc_supported(int d, int w);
 cudaError_t launch_fwd_tc(const PassArgs& a, cudaStream_t s);
 cudaError_t launch_bwd_tc(const PassArgs& a, cudaStream_t s);
-cudaError_t launch_paths_tc(const PassArgs& a, cudaStream_t s);
 cudaError_t launch_pack_weights(const PassArgs& a, cudaStream_t s);
 size_t tc_pack_bytes(int d, int w, int N, int precision);
 size_t tc_xstore_bytes(int d, int w, int N, int64_t B_local);
@@ -89,7 +88,6 @@ struct bsde_ctx {
   float* Rstore = nullptr;
   void* wpack = nullptr;
   void* xpack = nullptr;        // tcgen05 path: fp16 ΔW_n images
-  float* xn2 = nullptr;         // tcgen05 path: |X_N|² per path
   float* gpart = nullptr;
   DeviceState* state = nullptr;
   double* eval_loss = nullptr;
@@ -157,7 +155,6 @@ PassArgs pass_args(bsde_ctx* c) {
   a.xpack = c->Xstore;   // the tcgen05 path stores X_n as bf16 operand images
   a.gpart = c->gpart;
   a.dwpack = c->xpack;
-  a.xn2 = c->xn2;
   a.precision = c->cfg.precision;
   return a;
 }
@@ -174,8 +171,6 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
   launches += 1;   // k_begin_step (the memset is not a kernel)
   mark(1);
   if (ctx->family == BSDE_KERNEL_TC) {
-    CK(launch_paths_tc(a, ctx->stream));
-    launches += 1;
     CK(launch_fwd_tc(a, ctx->stream));
     mark(2);
     CK(launch_bwd_tc(a, ctx->stream));
@@ -229,7 +224,7 @@ int repack(bsde_ctx* ctx) {
 void free_all(bsde_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   void* bufs[] = {c->params, c->grad, c->adam_m, c->adam_v, c->scratch, c->Xstore, c->Ystore,
-                  c->abar, c->Rstore, c->wpack, c->xpack, c->xn2, c->gpart, c->state,
+                  c->abar, c->Rstore, c->wpack, c->xpack, c->gpart, c->state,
                   c->eval_loss};
   for (void* p : bufs)
     if (p) cudaFree(p);
@@ -382,7 +377,6 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
   if (family == BSDE_KERNEL_TC) {
     allocs.push_back({&ctx->wpack, tc_pack_bytes(d, w, ctx->N_max, cfg.precision)});
     allocs.push_back({&ctx->xpack, tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)});
-    allocs.push_back({(void**)&ctx->xn2, (size_t)ctx->B_local * sizeof(float)});
   } else {
     allocs.push_back({&ctx->wpack, simt_pack_bytes(d, w, ctx->N_max)});
     allocs.push_back({(void**)&ctx->gpart, simt_scratch_bytes(d, w)});
@@ -613,14 +607,7 @@ int bsde_eval_loss(bsde_ctx* ctx, uint32_t eval_id, int64_t batch, double* loss_
   a.loss_acc = ctx->eval_loss;
   CK(cudaMemsetAsync(ctx->eval_loss, 0, sizeof(double), ctx->stream));
   if (ctx->family == BSDE_KERNEL_TC) {
-    // the path images are sized for B_local paths: evaluate in chunks of them
-    const int64_t local = a.B_local, m_first = a.m0;
-    for (int64_t off = 0; off < local; off += ctx->B_local) {
-      a.B_local = local - off < ctx->B_local ? local - off : ctx->B_local;
-      a.m0 = m_first + off;
-      CK(launch_paths_tc(a, ctx->stream));
-      CK(launch_fwd_tc(a, ctx->stream));
-    }
+    CK(launch_fwd_tc(a, ctx->stream));   // an evaluation pass stores no path images
   } else {
     CK(launch_fwd_simt(a, ctx->stream));
   }
@@ -722,7 +709,6 @@ int bsde_debug_phase_clocks(bsde_ctx* ctx, int which, uint64_t* out, int n) {
   const int64_t np = num_params_at(ctx, ctx->N);
   PassArgs a = pass_args(ctx);
   CK(launch_begin_step(ctx->state, ctx->grad, np, ctx->stream));
-  CK(launch_paths_tc(a, ctx->stream));
   if (which == 0) a.clk = buf;
   CK(launch_fwd_tc(a, ctx->stream));
   if (which == 1) {
@@ -761,7 +747,7 @@ void bsde_destroy(bsde_ctx* ctx) {
 
 extern "C" int bsde_debug_umma(int mode, const float* a, const float* b, float* d_out) {
   bsde_ctx* ctx = nullptr;
-  if (mode < 0 || mode > 2 || !a || !b || !d_out) return fail(ctx, BSDE_EINVAL, "debug_umma: bad argument");
+  if (mode < 0 || mode > 3 || !a || !b || !d_out) return fail(ctx, BSDE_EINVAL, "debug_umma: bad argument");
   const size_t na = 128 * 112, nb = (mode == 2 ? 128 : 112) * 112, nd = 128 * 112;
   float *da = nullptr, *db = nullptr, *dd = nullptr;
   CK(cudaMalloc(&da, na * 4));

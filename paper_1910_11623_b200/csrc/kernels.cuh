@@ -28,8 +28,7 @@ struct PassArgs {
   const void* wpack;                   // packed bf16 weight images (see tc.cu)
   void* xpack;                         // bf16 X store (BF16 precision)
   float* gpart;                        // SIMT adjoint: per-CTA scratch gradients
-  void* dwpack;                        // tcgen05 path: fp16 ΔW_n images (k_paths_tc)
-  float* xn2;                          // tcgen05 path: |X_N|² per path (k_paths_tc)
+  void* dwpack;                        // tcgen05 path: fp16 ΔW_n images (written by k_fwd_tc)
   unsigned long long* clk;             // debug: per-phase clock64() trace of CTA 0 (or null)
   int precision;
 };

@@ -10,10 +10,10 @@
 //  k_pack_tc   fp32 master θ -> per-step bf16 operand images W̃1 [Wp×Dp], W̃2 [Wp×Wp],
 //              W̃3 [Dp×Wp] with the biases folded into a constant-1 column
 //              (W̃1 row w = e_d makes H1[w] = 1; W̃2/W̃3 take b2/b3 in column w).
-//  k_paths_tc  a1 + a2 for all (tile, n): Philox ΔW and exact fp32 Euler X; writes the
-//              bf16 X_n operand images, fp16 ΔW_n images and |X_N|² (tc_paths.cuh).
-//  k_fwd_tc    tile-major rollout: a3 three GEMMs per step, a4 Y update, a5 terminal
-//              loss and the scalar adjoint ā (tc_fwd.cuh).
+//  k_fwd_tc    tile-major rollout: a1 Philox ΔW (fused behind the GEMMs), a2 exact
+//              fp32 Euler X, a3 three GEMMs per step, a4 Y update, a5 terminal loss
+//              and the scalar adjoint ā; stores the bf16 X_n operand images and the
+//              fp16 ΔW_n images for the adjoint (tc_fwd.cuh).
 //  k_bwd_tc    step-major adjoint a6 with TMEM-resident per-step weight-gradient
 //              accumulators (tc_bwd.cuh).
 //
@@ -141,7 +141,6 @@ struct DwGen {
 }  // namespace tc
 }  // namespace bsde
 
-#include "tc_paths.cuh"
 #include "tc_fwd.cuh"
 #include "tc_bwd.cuh"
 
@@ -153,6 +152,7 @@ namespace tc {
 // mode 1: D = A·B,  A [128×112] K-major, B [112(k)×112(n)] MN-major view (like G4/G6)
 // mode 2: D = Aᵀ·B, A [128(k)×112(m)], B [128(k)×112(n)], both MN-major (like G5/G7/G8);
 //         output rows m >= 112 are undefined.
+// mode 3: D = A·Bᵀ as mode 0 with A in tensor memory (like the forward's G2/G3).
 __global__ void __launch_bounds__(128, 1) k_umma_test(int mode, const float* A, const float* B,
                                                       float* Dout) {
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -176,13 +176,26 @@ __global__ void __launch_bounds__(128, 1) k_umma_test(int mode, const float* A, 
       st_chunk(bimg, r, t, C, v);
     }
   if (t == 0) { mbar_init(bar, 1); fence_mbar_init(); }
-  if (warp == 0) tmem_alloc(tslot, 128);
+  if (warp == 0) tmem_alloc(tslot, 256);
   fence_async_smem();
   tc_before();
   __syncthreads();
   tc_after();
   const uint32_t tm = *tslot;
+  if (mode == 3) {   // A into TMEM columns [128, 184): thread t = row t, bf16 pairs
+    for (int c = 0; c < C / 8; ++c) {
+      uint4 u;
+      const float* r = A + t * C + 8 * c;
+      u.x = pack2(r[0], r[1]); u.y = pack2(r[2], r[3]); u.z = pack2(r[4], r[5]); u.w = pack2(r[6], r[7]);
+      tmem_st4(tm + ((uint32_t)(warp * 32) << 16) + 128 + 4 * c, u);
+    }
+    tmem_wait_st();
+    tc_before();
+    __syncthreads();
+    tc_after();
+  }
   if (t == 0) {
+    if (mode == 3) gemm_ta(tm, tm + 128, kmaj(bimg, C), C / 16, idesc_bf16(128, 112, false, false), false);
     if (mode == 0) gemm(tm, kmaj(aimg, C), kmaj(bimg, C), C / 16, idesc_bf16(128, 112, false, false), false);
     if (mode == 1) gemm(tm, kmaj(aimg, C), mnmaj(bimg, C), C / 16, idesc_bf16(128, 112, false, true), false);
     if (mode == 2) gemm(tm, mnmaj(aimg, C), mnmaj(bimg, C), 128 / 16, idesc_bf16(128, 112, true, true), false);
@@ -199,7 +212,7 @@ __global__ void __launch_bounds__(128, 1) k_umma_test(int mode, const float* A, 
   __syncthreads();
   if (warp == 0) {
     tc_after();
-    tmem_dealloc(tm, 128);
+    tmem_dealloc(tm, 256);
   }
 }
 
@@ -220,7 +233,7 @@ __global__ void k_debug_dw_fast(uint32_t it, int n, int64_t m0, int64_t count, i
 template <int D, int W>
 struct Impl {
   using Dm = Dims<D, W>;
-  static size_t fwd_smem() { return 2 * Dm::WB + 2 * Dm::ACT + 4 * 128 * 8 + 64; }
+  static size_t fwd_smem() { return FwdSmem<D, W>::BYTES; }
   static size_t bwd_smem() { return Dm::WB + 5 * Dm::ACT + 96; }
   static int ntiles(const PassArgs& a) { return (int)((a.B_local + 127) / 128); }
   static int sm_count() {
@@ -228,11 +241,6 @@ struct Impl {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return sms;
-  }
-  static cudaError_t paths(const PassArgs& a, cudaStream_t s) {
-    const int nt = ntiles(a), sms = sm_count();
-    k_paths_tc<D, W><<<nt < sms ? nt : sms, NTH, 0, s>>>(a, nt);
-    return cudaGetLastError();
   }
   static cudaError_t fwd(const PassArgs& a, cudaStream_t s) {
     const size_t smem = fwd_smem();
@@ -242,14 +250,19 @@ struct Impl {
     k_fwd_tc<D, W><<<nt < sms ? nt : sms, NTH, smem, s>>>(a, nt);
     return cudaGetLastError();
   }
-  static cudaError_t bwd(const PassArgs& a, cudaStream_t s) {
+  template <bool NEEDZ>
+  static cudaError_t bwd_z(const PassArgs& a, cudaStream_t s) {
     const size_t smem = bwd_smem();
-    cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<D, W, NEEDZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int nt = ntiles(a), sms = sm_count();
     const int64_t items = (int64_t)nt * a.N;
-    k_bwd_tc<D, W><<<(int)(items < sms ? items : sms), NTH, smem, s>>>(a, nt, items);
+    k_bwd_tc<D, W, NEEDZ><<<(int)(items < sms ? items : sms), NTH, smem, s>>>(a, nt, items);
     return cudaGetLastError();
+  }
+  // dZ needs the recomputed Z only where ∂_z f != 0 (HJB)
+  static cudaError_t bwd(const PassArgs& a, cudaStream_t s) {
+    return a.problem == kHJB ? bwd_z<true>(a, s) : bwd_z<false>(a, s);
   }
   static cudaError_t pack(const PassArgs& a, cudaStream_t s) {
     constexpr int per = Dm::Wp * (Dm::Dp / 8) + Dm::Wp * (Dm::Wp / 8) + Dm::Dp * (Dm::Wp / 8);
@@ -288,12 +301,6 @@ size_t tc_xstore_bytes(int d, int w, int N, int64_t B_local) {
   return 16;
 }
 
-cudaError_t launch_paths_tc(const PassArgs& a, cudaStream_t s) {
-#define X(D_, W_) if (a.d == D_ && a.w == W_) return tc::Impl<D_, W_>::paths(a, s);
-  BSDE_TC_DIMS(X)
-#undef X
-  return cudaErrorNotSupported;
-}
 cudaError_t launch_fwd_tc(const PassArgs& a, cudaStream_t s) {
 #define X(D_, W_) if (a.d == D_ && a.w == W_) return tc::Impl<D_, W_>::fwd(a, s);
   BSDE_TC_DIMS(X)

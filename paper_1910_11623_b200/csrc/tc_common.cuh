@@ -107,6 +107,27 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D (+)= A·B with A read from tensor memory (kind::f16: row r of A in lane r,
+// bf16 pairs (k, k+1) packed per 32-bit column, low half = even k; one K=16
+// step spans 8 columns).
+__device__ __forceinline__ void mma_bf16_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// four 32-bit columns [taddr, taddr+4) of the calling thread's lane
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint4& u) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+               "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -152,6 +173,84 @@ __device__ __forceinline__ void tmem_ld4x8(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Two 8-column chunks of the calling thread's lane at column offsets c0, c0+32.
+__device__ __forceinline__ void tmem_ld2x8(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%16];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%17];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr), "r"(taddr + 32u)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 8 consecutive fp32 columns of the calling thread's lane, without the wait:
+// issue several, then tmem_ld_wait() and reg_fence8() on each destination.
+__device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// orders later uses of r after the preceding tmem_ld_wait()
+__device__ __forceinline__ void reg_fence8(uint32_t (&r)[8]) {
+  asm volatile("" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+               "+r"(r[6]), "+r"(r[7]));
+}
+__device__ __forceinline__ void tmem_ld4_nowait(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void reg_fence4(uint32_t (&r)[4]) {
+  asm volatile("" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]));
+}
+// chunks c = c0 + 2i (i < NC) of 8 columns each from TMEM lane address base
+template <int NC>
+__device__ __forceinline__ void tmem_ld_chunks2(uint32_t base, int c0, float (&v)[NC][8]) {
+  uint32_t r[NC][8];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) tmem_ld8_nowait(base + 8u * (uint32_t)(c0 + 2 * i), r[i]);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    reg_fence8(r[i]);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[i][e] = __uint_as_float(r[i][e]);
+  }
+}
+
+// chunks c0 + i (i < NC, only those with i < nvalid) of 8 columns each from TMEM
+template <int NC>
+__device__ __forceinline__ void tmem_ld_chunks(uint32_t base, float (&v)[NC][8], int nvalid) {
+  uint32_t r[NC][8];
+#pragma unroll
+  for (int i = 0; i < NC; ++i)
+    if (i < nvalid) tmem_ld8_nowait(base + 8u * (uint32_t)i, r[i]);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    if (i < nvalid) {
+      reg_fence8(r[i]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[i][e] = __uint_as_float(r[i][e]);
+    }
+  }
+}
+
+template <int I>
+struct Int {
+  static constexpr int value = I;
+};
+
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);   // version 1, no swizzle
@@ -180,6 +279,14 @@ __device__ __forceinline__ void gemm(uint32_t d_tmem, Opnd A, Opnd B, int ksteps
              sdesc(B.base + k * B.kstep, B.lbo, B.sbo), idesc, (k > 0 || accumulate) ? 1u : 0u);
 }
 
+// D (+)= A·B over ksteps·16 of K with A in tensor memory at column a_tmem.
+__device__ __forceinline__ void gemm_ta(uint32_t d_tmem, uint32_t a_tmem, Opnd B, int ksteps,
+                                        uint32_t idesc, bool accumulate) {
+  for (int k = 0; k < ksteps; ++k)
+    mma_bf16_ta(d_tmem, a_tmem + 8u * k, sdesc(B.base + k * B.kstep, B.lbo, B.sbo), idesc,
+                (k > 0 || accumulate) ? 1u : 0u);
+}
+
 __host__ __device__ constexpr int pad16(int x) { return (x + 15) / 16 * 16; }
 
 template <int D, int W>
@@ -201,6 +308,30 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+// bf16x2 {lo = ReLU(a), hi = ReLU(b)} (RNE), one instruction
+__device__ __forceinline__ uint32_t relu_pack2(float a, float b) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
+  return d;
+}
+// bf16x2 sum (RNE)
+__device__ __forceinline__ uint32_t bf2_add(uint32_t x, uint32_t y) {
+  uint32_t d;
+  asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(y));
+  return d;
+}
+// per-half 0xFFFF where the bf16 half is non-zero, for halves >= +0 (ReLU
+// outputs): h + 0x7FFF sets bit 15 of the half iff h != 0 without carrying
+// out of it, and PRMT replicates that bit over the half.
+__device__ __forceinline__ uint32_t nz_mask2(uint32_t w) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(d) : "r"(w + 0x7FFF7FFFu));
+  return d;
+}
+__device__ __forceinline__ void st_chunk_u4(uint8_t* img, int row, int chunk, int C, const uint4& u) {
+  *reinterpret_cast<uint4*>(img + (row >> 3) * (C * 16) + chunk * 128 + (row & 7) * 16) = u;
+}
+
 // row `row`, columns [8·chunk, 8·chunk + 8) of an image with C columns
 __device__ __forceinline__ void st_chunk(uint8_t* img, int row, int chunk, int C, const float* v) {
   uint4 u;

@@ -1,206 +1,400 @@
-// tc_fwd.cuh — forward rollout on tcgen05:
-// one 128-path tile (4 threads per path, TMEM lane = path) walks all N steps.
-// Per step: the X_n operand image (written by k_paths_tc) is bulk-copied into
-// shared memory, the three GEMMs A1 = X̃ W̃1ᵀ, A2 = H1 W̃2ᵀ, Z = H2 W̃3ᵀ run on the
-// tensor cores with fp32 accumulators in TMEM (weights double-buffered), the
-// epilogues form H1 = ReLU(A1), H2 = H1 + ReLU(A2) (Eq. 7, h = 1) and the Y
-// update Y_{n+1} = Y_n - f(Y_n, Z_n) Δt + Z_n·ΔW_n (Eq. 5, φ = -f, R2).  The
-// terminal residual R = Y_N - g(X_N) (Eq. 6) uses |X_N|² from k_paths_tc.
+// tc_fwd.cuh — forward rollout on tcgen05, one fused,
+// warp-specialised pass; CTAs are persistent over 128-path tiles, every tile
+// walks all N steps.
+//
+// Producer warps 0-11 (3 threads per path) generate the Brownian paths: the
+// increments ΔW_n = √Δt·z (Philox4x32-10 + Box-Muller, R8) and the
+// Euler states X_{n+1} = X_n + √2 ΔW_n (Eq. 5) in exact fp32
+// registers.  Per step they fill one slot of a four-deep ring: the bf16 X̃_n
+// operand image (constant-1 column d folds the bias) in shared memory and the
+// fp16 ΔW_n pairs in tensor memory, and write both as images to global memory
+// for the adjoint.
+//
+// Consumer warps 12-15 (1 thread per path = TMEM lane; thread 480 issues the
+// MMAs) run the network of step n on the tensor cores:
+//   G1  A1 = X̃_n W̃1ᵀ   (A from the ring slot)     E1  H1 = ReLU(A1)  -> TMEM operand
+//   G2  A2 = H1 W̃2ᵀ    (A from TMEM)              E2  H2 = H1 + ReLU(A2) (Eq. 7, h = 1)
+//   G3  Z  = H2 W̃3ᵀ    (A from TMEM)              E3  Y_{n+1} = Y_n - f Δt + Z·ΔW (Eq. 5, R2)
+// H1 and H2 never touch shared memory: the epilogues store them as bf16 pairs
+// into tensor memory (tcgen05.st), the A operand of the next GEMM, so no proxy
+// fence sits on the chain.  The two fp32 accumulators alternate between steps,
+// which lets G1 of step n+1 run during E3 of step n.  The terminal residual
+// R = Y_N - g(X_N) (Eq. 6) and the scalar adjoint ā close each tile.
+//
+// Sync: ring slot full/empty mbarriers (producers -> MMA thread -> producers);
+// G1 and G2/G3 commits on separate mbarriers; weight images are reloaded per
+// matrix as soon as the GEMM that read them has completed (W̃1 double-buffered).
 #pragma once
 
 namespace bsde {
 namespace tc {
 
-template <int D, int W>
-__global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
-  using Dm = Dims<D, W>;
-  constexpr int Dp = Dm::Dp, Wp = Dm::Wp;
-  extern __shared__ __align__(1024) uint8_t sm[];
-  uint8_t* wimg0 = sm;
-  uint8_t* wimg1 = sm + Dm::WB;
-  uint8_t* xop = sm + 2 * Dm::WB;
-  uint8_t* hop = xop + Dm::ACT;
-  float2* red = reinterpret_cast<float2*>(hop + Dm::ACT);            // [4][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 4 * 128);       // 0,1 weights, 2 mma, 3 X
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
-  __shared__ double lred[4];
-  __shared__ float gred[4];
-
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int q = warp & 3, g = warp >> 2;
-  const int row = 32 * q + lane;
-  if (t == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
-    fence_mbar_init();
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// ΔW chunk from its fp16 image (16 bytes -> 8 floats)
+__device__ __forceinline__ void unpack_dw(const uint4& u, float* v) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+    v[2 * k] = f.x;
+    v[2 * k + 1] = f.y;
   }
-  if (warp == 0) tmem_alloc(tslot, 256);
-  tc_before();
-  __syncthreads();
-  tc_after();
-  const uint32_t tm = *tslot;
-  const uint32_t lq = ((uint32_t)(32 * q) << 16) + 8u * g;   // lane quadrant + first chunk column
-  const uint32_t acc0 = tm + lq, acc1 = tm + 128 + lq;
+}
+constexpr int kFwdProducers = 384, kFwdConsumers = 128;
+__device__ __forceinline__ void consumer_sync() { named_sync(1, kFwdConsumers); }
 
+// Normals of Philox blocks q = 2c, 2c+1 (columns 8c..8c+7) for the chunks
+// c = c0, c0 + CS, ..., NCH of them, interleaved for ILP; the normals of blocks
+// whose columns are all >= D are 0.
+template <int D, int CS, int NCH>
+__device__ __forceinline__ void gen_chunks(int c0, uint32_t m, uint32_t n, uint32_t it, uint32_t k0,
+                                           uint32_t k1, float sdt, float (&dw)[2 * 8]) {
+  constexpr int K = 2 * NCH;
+  uint4 c[K];
+  bool ok[K];   // warp-uniform: block has columns < D
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int q = 2 * (c0 + CS * (j / 2)) + j % 2;
+    c[j] = make_uint4((uint32_t)q, m, n, it);
+    ok[j] = 4 * q < D;
+  }
+  uint32_t a0 = k0, a1 = k1;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { a0 += kPhiloxW0; a1 += kPhiloxW1; }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint32_t lo0 = kPhiloxM0 * c[j].x, hi0 = __umulhi(kPhiloxM0, c[j].x);
+      const uint32_t lo1 = kPhiloxM1 * c[j].z, hi1 = __umulhi(kPhiloxM1, c[j].z);
+      c[j] = make_uint4(hi1 ^ c[j].y ^ a0, lo1, hi0 ^ c[j].w ^ a1, lo0);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+    if (ok[j]) {
+#ifdef BSDE_DBG_NOBM
+      z0 = __uint_as_float((c[j].x >> 9) | 0x3c000000u); z1 = __uint_as_float((c[j].y >> 9) | 0x3c000000u);
+      z2 = __uint_as_float((c[j].z >> 9) | 0x3c000000u); z3 = __uint_as_float((c[j].w >> 9) | 0x3c000000u);
+#else
+      box_muller_fast(c[j].x, c[j].y, sdt, z0, z1);
+      box_muller_fast(c[j].z, c[j].w, sdt, z2, z3);
+#endif
+    }
+    dw[4 * j + 0] = z0;
+    dw[4 * j + 1] = z1;
+    dw[4 * j + 2] = z2;
+    dw[4 * j + 3] = z3;
+  }
+}
+
+template <int D, int W>
+struct FwdSmem {
+  using Dm = Dims<D, W>;
+  static constexpr uint32_t W1 = 0;                           // W̃1 images, two buffers
+  static constexpr uint32_t W2 = 2 * Dm::W1B;
+  static constexpr uint32_t W3 = W2 + Dm::W2B;
+  static constexpr int NSLOT = 4;                            // ring depth (steps)
+  static constexpr uint32_t SLOT0 = W3 + Dm::W3B;
+  static constexpr uint32_t SLOTB = Dm::XB + 3 * 128 * 4;     // X̃_n | |X_N|² partials [3][128]
+  static constexpr uint32_t BARS = SLOT0 + NSLOT * SLOTB;
+  // full[NSLOT], empty[NSLOT], wf1[2], wf2, wf3, g1, g23
+  static constexpr int NBARS = 2 * NSLOT + 6;
+  static constexpr uint32_t TSLOT = BARS + NBARS * 8;
+  static constexpr uint32_t BYTES = TSLOT + 16;
+  // tensor memory columns: accumulators, the A operand of G2/G3, the ΔW_n ring
+  // (fp16 pairs, 4 columns per 8-column chunk of the first ceil(d/8) chunks)
+  static constexpr uint32_t T_ACC1 = 128, T_H = 240, T_DW = 296;
+  static constexpr uint32_t DWC = 4 * ((D + 7) / 8);
+  static_assert(T_H + Dm::Wp / 2 <= T_DW && T_DW + NSLOT * DWC <= 512, "TMEM budget");
+};
+
+// Producer thread k of a path (k = 0, 1, 2) owns the 8-column chunks c = k + 3i.
+// One code path for the three threads (instruction-cache footprint); k is
+// warp-uniform.
+template <int D, int W>
+__device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint8_t* sm, uint32_t tm,
+                                             int K3, int q, int lane) {
+  using Dm = Dims<D, W>;
+  using L = FwdSmem<D, W>;
+  constexpr int Dp = Dm::Dp, NCD = Dp / 8;
+  constexpr int NI = (NCD + 2) / 3;        // image chunks of thread 0 (>= those of 1, 2)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::BARS);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + L::NSLOT;
+  const int row = 32 * q + lane;
+  const uint32_t lane_off = (uint32_t)(32 * q) << 16;
   const int N = a.N;
+  const bool store = !a.eval;
+  const uint32_t it = a.eval ? a.eval_it : a.state->it;
+  uint8_t* xst = static_cast<uint8_t*>(a.xpack);
+  uint8_t* dst = static_cast<uint8_t*>(a.dwpack);
+  const uint32_t roff = (row >> 3) * (Dp * 16) + (row & 7) * 16;   // row's offset in an image
+  unsigned long long* const pclk = (a.clk && blockIdx.x == 0 && q == 0 && K3 == 0 && lane == 0) ? a.clk : nullptr;
+  int64_t s = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t mg = (uint32_t)(a.m0 + (int64_t)tile * 128 + row);
+    float X[8 * (NI > 0 ? NI : 1)];
+#pragma unroll
+    for (int i = 0; i < 8 * NI; ++i) X[i] = a.x0;
+    for (int n = 0; n < N; ++n, ++s) {
+      const int slot = (int)(s % L::NSLOT);
+      const uint32_t use = (uint32_t)(s / L::NSLOT);
+      uint8_t* ximg = sm + L::SLOT0 + slot * L::SLOTB;
+      float* xn2 = reinterpret_cast<float*>(ximg + Dm::XB);
+      const uint32_t tdw = tm + lane_off + L::T_DW + (uint32_t)slot * L::DWC;
+      if (pclk && s < 64) pclk[s * 16 + 8] = clock64();
+      mbar_wait(&empty[slot], (use & 1) ^ 1);
+      tc_after();
+      if (pclk && s < 64) pclk[s * 16 + 9] = clock64();
+      const size_t img = ((size_t)n * ntiles + tile) * Dm::XB;
+      // X̃_n chunk from X, ΔW_n chunk (fp16: TMEM ring + image), then X_{n+1}
+      auto chunk_out = [&](auto ic, const float* dw) {
+        constexpr int i = decltype(ic)::value;
+        const int c = K3 + 3 * i;
+        if (c >= NCD) return;
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = 8 * c + e;
+          v[e] = j < D ? X[8 * i + e] : (j == D ? 1.0f : 0.0f);
+        }
+        uint4 xu;
+        xu.x = pack2(v[0], v[1]); xu.y = pack2(v[2], v[3]); xu.z = pack2(v[4], v[5]); xu.w = pack2(v[6], v[7]);
+        *reinterpret_cast<uint4*>(ximg + roff + c * 128) = xu;
+        const uint4 du = make_uint4(pack_h2(dw[0], dw[1]), pack_h2(dw[2], dw[3]), pack_h2(dw[4], dw[5]),
+                                    pack_h2(dw[6], dw[7]));
+        if (8 * c < D) tmem_st4(tdw + 4u * c, du);
+#ifndef BSDE_DBG_NOSTORE
+        if (store) {
+          *reinterpret_cast<uint4*>(xst + img + roff + c * 128) = xu;
+          *reinterpret_cast<uint4*>(dst + img + roff + c * 128) = du;
+        }
+#endif
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (8 * c + e < D) X[8 * i + e] = fmaf(kSqrt2, dw[e], X[8 * i + e]);   // a2
+      };
+      // chunks i, i+1 together: four Philox streams interleaved
+      auto pair = [&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        if constexpr (i < NI) {
+          constexpr int nch = (i + 1 < NI) ? 2 : 1;
+          float dw[16];
+          gen_chunks<D, 3, nch>(K3 + 3 * i, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt, dw);
+          chunk_out(Int<i>{}, dw);
+          if constexpr (nch == 2) chunk_out(Int<i + 1>{}, dw + 8);
+        }
+      };
+      pair(Int<0>{});
+      pair(Int<2>{});
+      pair(Int<4>{});
+      pair(Int<6>{});
+      if (n + 1 == N) {   // |X_N|² partial for the terminal condition
+        float sx = 0.0f;
+#pragma unroll
+        for (int i = 0; i < NI; ++i)
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (8 * (K3 + 3 * i) + e < D) sx = fmaf(X[8 * i + e], X[8 * i + e], sx);
+        xn2[K3 * 128 + row] = sx;
+      }
+      if (pclk && s < 64) pclk[s * 16 + 10] = clock64();
+      tmem_wait_st();
+      tc_before();
+      fence_async_smem();   // X̃_n is read by the tensor cores
+      mbar_arrive(&full[slot]);
+    }
+  }
+}
+
+template <int D, int W>
+__device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint8_t* sm, uint32_t tm,
+                                             int q, int lane, double& lsum, float& dy0) {
+  using Dm = Dims<D, W>;
+  using L = FwdSmem<D, W>;
+  constexpr int Dp = Dm::Dp, Wp = Dm::Wp, NCW = Wp / 8, NCD = Dp / 8, NCV = (D + 7) / 8;
+  constexpr int HW = (NCW + 1) / 2;   // E1/E2 process the accumulator in two halves of chunks
+  constexpr int HV = (NCV + 1) / 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::BARS);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + L::NSLOT;
+  uint64_t* wf1 = bars + 2 * L::NSLOT;
+  uint64_t* wf2 = wf1 + 2;
+  uint64_t* wf3 = wf1 + 3;
+  uint64_t* bg1 = wf1 + 4;
+  uint64_t* bg23 = wf1 + 5;
+  const int row = 32 * q + lane;
+  const bool mma = (q == 3 && lane == 0);   // highest warp id: favoured by the scheduler
+  const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+  const uint32_t acc0 = tm + lane_off, acc1 = tm + L::T_ACC1 + lane_off;
+  auto acc = [&](int b) { return b ? acc1 : acc0; };
+  const uint32_t hT = tm + L::T_H;                       // TMEM A operand (Wp/2 columns)
+  const int N = a.N;
+  const bool store = !a.eval;
   const uint8_t* wsrc = static_cast<const uint8_t*>(a.wpack);
-  const uint8_t* xst = static_cast<const uint8_t*>(a.xpack);
-  const uint8_t* dst = static_cast<const uint8_t*>(a.dwpack);
   const int my_tiles = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int64_t total_seq = (int64_t)my_tiles * N;
+  const int64_t total = (int64_t)my_tiles * N;
   constexpr uint32_t I1 = idesc_bf16(128, Wp, false, false);
   constexpr uint32_t I3 = idesc_bf16(128, Dp, false, false);
+  (void)NCD;
 
-  // sequence s = (k-th tile of this CTA) * N + n
-  auto img_of = [&](int64_t s) -> size_t {
-    const int tile = (int)blockIdx.x + (int)(s / N) * (int)gridDim.x;
-    return ((size_t)(s % N) * ntiles + tile) * Dm::XB;
+  auto wsrc_of = [&](int64_t s) { return wsrc + (size_t)(s % N) * Dm::WB; };
+  auto load = [&](uint64_t* bar, uint8_t* dstp, const uint8_t* src, uint32_t bytes) {
+    mbar_expect_tx(bar, bytes);
+    for (uint32_t off = 0; off < bytes; off += 16384u)
+      bulk_g2s(dstp + off, src + off, min(16384u, bytes - off), bar);
   };
-  auto load_weights = [&](int64_t s) {   // thread 0
-    const int n = (int)(s % N);
-    uint8_t* dstw = (s & 1) ? wimg1 : wimg0;
-    uint64_t* bar = &bars[s & 1];
-    mbar_expect_tx(bar, Dm::WB);
-    const uint8_t* src = wsrc + (size_t)n * Dm::WB;
-    for (uint32_t off = 0; off < Dm::WB; off += 16384u)
-      bulk_g2s(dstw + off, src + off, min(16384u, Dm::WB - off), bar);
+  auto issue_g1 = [&](int64_t s) {   // MMA thread
+    const int slot = (int)(s % L::NSLOT), b = (int)(s & 1);
+    mbar_wait(&full[slot], (uint32_t)((s / L::NSLOT) & 1));
+    mbar_wait(&wf1[b], (uint32_t)((s >> 1) & 1));
+    tc_after();
+    gemm(tm + (b ? L::T_ACC1 : 0u), kmaj(sm + L::SLOT0 + slot * L::SLOTB, Dp),
+         kmaj(sm + L::W1 + b * Dm::W1B, Dp), Dp / 16, I1, false);
+    mma_commit(bg1);
   };
-  auto load_x = [&](int64_t s) {         // thread 0: X_n operand image into xop
-    mbar_expect_tx(&bars[3], Dm::XB);
-    bulk_g2s(xop, xst + img_of(s), Dm::XB, &bars[3]);
-    if (s + 2 < total_seq) bulk_prefetch_l2(xst + img_of(s + 2), Dm::XB);
-  };
-  if (t == 0 && total_seq > 0) {
-    load_weights(0);
-    load_x(0);
-    if (total_seq > 1) bulk_prefetch_l2(xst + img_of(1), Dm::XB);
+  if (mma && total > 0) {
+    load(&wf1[0], sm + L::W1, wsrc_of(0), Dm::W1B);
+    if (total > 1) load(&wf1[1], sm + L::W1 + Dm::W1B, wsrc_of(1), Dm::W1B);
+    load(wf2, sm + L::W2, wsrc_of(0) + Dm::W1B, Dm::W2B);
+    load(wf3, sm + L::W3, wsrc_of(0) + Dm::W1B + Dm::W2B, Dm::W3B);
+    issue_g1(0);
   }
 
-  unsigned long long* const clk = (a.clk && blockIdx.x == 0 && t == 32) ? a.clk : nullptr;
+  unsigned long long* const clk = (a.clk && blockIdx.x == 0 && q == 1 && lane == 0) ? a.clk : nullptr;
 #define CLK(i) do { if (clk && s < 64) clk[s * 16 + (i)] = clock64(); } while (0)
-  uint32_t mph = 0;
   int64_t s = 0;
-  double lsum = 0.0;
-  float dy0 = 0.0f;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t mloc = (int64_t)tile * 128 + row;
     const bool valid = mloc < a.B_local;
     float Y = a.params[0];
+    float xn2 = 0.0f;
     for (int n = 0; n < N; ++n, ++s) {
+      const int p = (int)(s & 1), slot = (int)(s % L::NSLOT);
+      uint8_t* slotp = sm + L::SLOT0 + slot * L::SLOTB;
       CLK(0);
-      uint8_t* wimg = (s & 1) ? wimg1 : wimg0;
-      if (t == 0) {
-        if (s + 1 < total_seq) load_weights(s + 1);
-        mbar_wait(&bars[3], (uint32_t)(s & 1));            // X_n image
-        mbar_wait(&bars[s & 1], (uint32_t)((s >> 1) & 1)); // weights of step n
-        tc_after();
-        gemm(tm, kmaj(xop, Dp), kmaj(wimg, Dp), Dp / 16, I1, false);                  // A1
-        mma_commit(&bars[2]);
-      }
-      uint4 dwp[4];                                   // ΔW_n chunks (fp16), needed at epi3
-      {
-        const uint8_t* src = dst + img_of(s) + (row >> 3) * (Dp * 16) + (row & 7) * 16;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dwp[i] = chunk_lt(g, i, Dp / 8) ? __ldcs(reinterpret_cast<const uint4*>(src + (g + 4 * i) * 128))
-                                          : make_uint4(0, 0, 0, 0);
-      }
-      mbar_wait(&bars[2], mph);
-      mph ^= 1;
+      // E1: H1 = ReLU(A1) -> TMEM operand (bf16 pairs)
+      mbar_wait(bg1, (uint32_t)(s & 1));
       CLK(1);
-      if (t == 0 && s + 1 < total_seq) load_x(s + 1);   // G1 has consumed xop
       tc_after();
-      {  // H1 = ReLU(A1)
-        float v[32];
-        tmem_ld4x8(acc0, v);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (chunk_lt(g, i, Wp / 8)) {
+      for (int h = 0; h < 2; ++h) {
+        constexpr int c0 = 0;
+        (void)c0;
+        float v[HW][8];
+        tmem_ld_chunks<HW>(acc(p) + 8u * (uint32_t)(h * HW), v, NCW - h * HW);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[8 * i + e] = fmaxf(v[8 * i + e], 0.0f);
-            st_chunk(hop, row, g + 4 * i, Wp, v + 8 * i);
-          }
+        for (int i = 0; i < HW; ++i) {
+          if (h * HW + i >= NCW) continue;
+          tmem_st4(hT + lane_off + 4u * (h * HW + i),
+                   make_uint4(relu_pack2(v[i][0], v[i][1]), relu_pack2(v[i][2], v[i][3]),
+                              relu_pack2(v[i][4], v[i][5]), relu_pack2(v[i][6], v[i][7])));
         }
       }
-      fence_async_smem();
+      tmem_wait_st();
       tc_before();
-      __syncthreads();
+      consumer_sync();
       CLK(2);
-      if (t == 0) {
+      if (mma) {   // G2 (A = H1 in TMEM); W̃1 buffer p is free for step s + 2
         tc_after();
-        gemm(tm + 128, kmaj(hop, Wp), kmaj(wimg + Dm::W1B, Wp), Wp / 16, I1, false);   // A2
-        mma_commit(&bars[2]);
+        mbar_wait(wf2, (uint32_t)(s & 1));
+        gemm_ta(tm + (p ? 0u : L::T_ACC1), hT, kmaj(sm + L::W2, Wp), Wp / 16, I1, false);
+        mma_commit(bg23);
+        if (s + 2 < total) load(&wf1[p], sm + L::W1 + p * Dm::W1B, wsrc_of(s + 2), Dm::W1B);
       }
-      if (n > 0) {   // finish a4 of step n-1 from the partial sums of the four threads
-        const float2 r0 = red[row], r1 = red[128 + row], r2 = red[256 + row], r3 = red[384 + row];
-        const float cz = (r0.x + r1.x) + (r2.x + r3.x), zz = (r0.y + r1.y) + (r2.y + r3.y);
-        Y = Y - driver_f(a.problem, Y, zz, a.lam) * a.dt + cz;
-      }
-      if (!a.eval && a.problem == kAllenCahn && valid && g == 0)
-        a.Ystore[(int64_t)n * a.B_local + mloc] = Y;
-      mbar_wait(&bars[2], mph);
-      mph ^= 1;
+      // E2: H2 = H1 + ReLU(A2) in bf16x2 arithmetic (R17) -> TMEM operand (over H1)
+      mbar_wait(bg23, 0);
       CLK(3);
       tc_after();
-      {  // H2 = ReLU(A1) + ReLU(A2) (residual block, Eq. 7 with h = 1), over H1 in hop
-        float v1[32], v2[32];
-        tmem_ld4x8(acc0, v1);
-        tmem_ld4x8(acc1, v2);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (chunk_lt(g, i, Wp / 8)) {
+      for (int h = 0; h < 2; ++h) {
+        float v[HW][8];
+        uint32_t hw[HW][4];
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              v1[8 * i + e] = fmaxf(v1[8 * i + e], 0.0f) + fmaxf(v2[8 * i + e], 0.0f);
-            st_chunk(hop, row, g + 4 * i, Wp, v1 + 8 * i);
-          }
+        for (int i = 0; i < HW; ++i)
+          if (h * HW + i < NCW) tmem_ld4_nowait(hT + lane_off + 4u * (h * HW + i), hw[i]);
+        tmem_ld_chunks<HW>(acc(p ^ 1) + 8u * (uint32_t)(h * HW), v, NCW - h * HW);
+#pragma unroll
+        for (int i = 0; i < HW; ++i) {
+          if (h * HW + i >= NCW) continue;
+          reg_fence4(hw[i]);
+          tmem_st4(hT + lane_off + 4u * (h * HW + i),
+                   make_uint4(bf2_add(hw[i][0], relu_pack2(v[i][0], v[i][1])),
+                              bf2_add(hw[i][1], relu_pack2(v[i][2], v[i][3])),
+                              bf2_add(hw[i][2], relu_pack2(v[i][4], v[i][5])),
+                              bf2_add(hw[i][3], relu_pack2(v[i][6], v[i][7]))));
         }
       }
-      fence_async_smem();
+      tmem_wait_st();
       tc_before();
-      __syncthreads();
+      consumer_sync();
       CLK(4);
-      if (t == 0) {
+      if (mma) {   // G3 (A = H2 in TMEM); then G1 of the next step into the other accumulator
         tc_after();
-        gemm(tm, kmaj(hop, Wp), kmaj(wimg + Dm::W1B + Dm::W2B, Wp), Wp / 16, I3, false);  // Z
-        mma_commit(&bars[2]);
+        mbar_wait(wf3, (uint32_t)(s & 1));
+        gemm_ta(tm + (p ? L::T_ACC1 : 0u), hT, kmaj(sm + L::W3, Wp), Wp / 16, I3, false);
+        mma_commit(bg23);
+        if (s + 1 < total) {
+          load(wf2, sm + L::W2, wsrc_of(s + 1) + Dm::W1B, Dm::W2B);
+          issue_g1(s + 1);
+        }
       }
-      mbar_wait(&bars[2], mph);
-      mph ^= 1;
+      // E3: a4 Y_{n+1} = Y_n - f(Y_n, Z_n) Δt + Z_n·ΔW_n (one thread per path)
+      mbar_wait(bg23, 1);
       CLK(5);
       tc_after();
+      mbar_wait(&full[slot], (uint32_t)((s / L::NSLOT) & 1));   // ΔW_n, |X_N|² partials
+      tc_after();
       float cz = 0.0f, zz = 0.0f;
-      {  // a4 partials c = Z·ΔW, |Z|²
-        float z[32];
-        tmem_ld4x8(acc0, z);
+      const uint32_t tdw = tm + lane_off + L::T_DW + (uint32_t)slot * L::DWC;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+      for (int h = 0; h < 2; ++h) {
+        float z[HV][8];
+        uint32_t dwr[HV][4];
+#pragma unroll
+        for (int i = 0; i < HV; ++i)
+          if (h * HV + i < NCV) tmem_ld4_nowait(tdw + 4u * (h * HV + i), dwr[i]);
+        tmem_ld_chunks<HV>(acc(p) + 8u * (uint32_t)(h * HV), z, NCV - h * HV);
+#pragma unroll
+        for (int i = 0; i < HV; ++i) {
+          const int c = h * HV + i;
+          if (c >= NCV) continue;
+          reg_fence4(dwr[i]);
           float dw[8];
-          unpack_dw(dwp[i], dw);
+          unpack_dw(make_uint4(dwr[i][0], dwr[i][1], dwr[i][2], dwr[i][3]), dw);
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            if (col_lt(g, i, e, D)) {
-              cz = fmaf(z[8 * i + e], dw[e], cz);
-              zz = fmaf(z[8 * i + e], z[8 * i + e], zz);
+            if (8 * c + e < D) {
+              cz = fmaf(z[i][e], dw[e], cz);
+              zz = fmaf(z[i][e], z[i][e], zz);
             }
           }
         }
       }
-      red[g * 128 + row] = make_float2(cz, zz);   // a4 is finished after the next barrier
+      if (n + 1 == N) {
+        const float* x2 = reinterpret_cast<const float*>(slotp + Dm::XB);
+        xn2 = (x2[row] + x2[128 + row]) + x2[256 + row];
+      }
+      if (store && a.problem == kAllenCahn && valid)
+        a.Ystore[(int64_t)n * a.B_local + mloc] = Y;
+      Y = Y - driver_f(a.problem, Y, zz, a.lam) * a.dt + cz;
       tc_before();
+      consumer_sync();
       CLK(6);
+      if (mma) {   // the slot and W̃3 are free
+        mbar_arrive(&empty[slot]);
+        if (s + 1 < total) load(wf3, sm + L::W3, wsrc_of(s + 1) + Dm::W1B + Dm::W2B, Dm::W3B);
+      }
     }
-    __syncthreads();
-    {
-      const float2 r0 = red[row], r1 = red[128 + row], r2 = red[256 + row], r3 = red[384 + row];
-      const float cz = (r0.x + r1.x) + (r2.x + r3.x), zz = (r0.y + r1.y) + (r2.y + r3.y);
-      Y = Y - driver_f(a.problem, Y, zz, a.lam) * a.dt + cz;                         // a4, n = N-1
-    }
-    __syncthreads();   // red is rewritten by the next tile
     // a5: R = Y_N - g(X_N); loss; ā recursion and dY0
-    if (g == 0 && valid) {
-      const float R = Y - terminal_g(a.problem, a.xn2[mloc]);
+    if (valid) {
+      const float R = Y - terminal_g(a.problem, xn2);
       lsum += (double)R * R;
-      if (!a.eval) {
+      if (store) {
         a.Rstore[mloc] = R;
         float ab = 2.0f * R * a.inv_B;
         if (a.problem == kAllenCahn) {
@@ -216,6 +410,34 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
       }
     }
   }
+#undef CLK
+}
+
+template <int D, int W>
+__global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
+  using L = FwdSmem<D, W>;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::BARS);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::TSLOT);
+  __shared__ double lred[4];
+  __shared__ float gred[4];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  if (t == 0) {
+    for (int i = 0; i < L::NSLOT; ++i) mbar_init(&bars[i], kFwdProducers);   // full
+    for (int i = L::NSLOT; i < L::NBARS; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tm = *tslot;
+  double lsum = 0.0;
+  float dy0 = 0.0f;
+  // consumers on the high warp ids: the schedulers favour them (the chain is
+  // latency-bound, the producers throughput-bound)
+  if (warp < 12) fwd_producer<D, W>(a, ntiles, sm, tm, warp >> 2, warp & 3, lane);
+  else fwd_consumer<D, W>(a, ntiles, sm, tm, warp & 3, lane, lsum, dy0);
   double lw = lsum;
   float gw = dy0;
 #pragma unroll
@@ -223,7 +445,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
     lw += __shfl_xor_sync(0xffffffffu, lw, o);
     gw += __shfl_xor_sync(0xffffffffu, gw, o);
   }
-  if (g == 0 && lane == 0) { lred[q] = lw; gred[q] = gw; }
+  if (warp >= 12 && lane == 0) { lred[warp - 12] = lw; gred[warp - 12] = gw; }
   tc_before();
   __syncthreads();
   if (t == 0) {
@@ -234,9 +456,8 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
   }
   if (warp == 0) {
     tc_after();
-    tmem_dealloc(tm, 256);
+    tmem_dealloc(tm, 512);
   }
-#undef CLK
 }
 
 }  // namespace tc

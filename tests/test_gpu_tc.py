@@ -32,7 +32,7 @@ def bf16(x):
     return ob.round_bf16(x)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 def test_umma_operand_layouts(mode):
     """One M=128, N=112 tcgen05 MMA per operand-major combination the kernels use."""
     from paper_1910_11623_b200.solver import debug_umma
@@ -41,7 +41,7 @@ def test_umma_operand_layouts(mode):
     B = rng.standard_normal((128 if mode == 2 else 112, 112)).astype(np.float32)
     D = debug_umma(mode, A, B)
     a, b = bf16(A), bf16(B)
-    if mode == 0:
+    if mode in (0, 3):
         ref = a @ b.T
     elif mode == 1:
         ref = a @ b
@@ -189,10 +189,17 @@ def test_nccl_one_rank_communicator_matches_local():
     ref = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr, precision="bf16")
     com = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr, precision="bf16",
                nccl_id=nccl_unique_id(), world=1, rank=0)
+    # same parameters, same paths: the reduced gradient equals the local one up to
+    # the order of the fp32 atomics (1e-6 of its scale)
+    l0a, l0b = ref.compute_grad(), com.compute_grad()
+    ga, gb = ref.get_grads(), com.get_grads()
+    assert abs(l0a - l0b) <= 1e-6 * l0a
+    assert np.max(np.abs(ga - gb)) <= 1e-5 * np.max(np.abs(ga))
     la = [ref.train_step() for _ in range(3)]
     lb = [com.train_step() for _ in range(3)]
     assert abs(la[0] - lb[0]) <= 1e-6 * la[0] and np.allclose(la, lb, rtol=1e-4)
-    # fp32 atomics make the two gradients differ in the last bits; Adam can flip
-    # the step of a near-zero gradient component (at most 2·lr per step)
+    # After an update the two runs drift apart: bf16 operand rounding turns the
+    # atomics-order noise into ulp flips of some operands, and Adam moves
+    # near-zero gradient components by up to lr either way; bounded by 2·lr per step.
     diff = np.abs(ref.get_params() - com.get_params())
-    assert diff.max() <= 6 * wl.lr and np.mean(diff > 1e-6) < 1e-3
+    assert diff.max() <= 6 * wl.lr

@@ -1,5 +1,7 @@
 """clock64() phase trace of CTA 0 of the tcgen05 forward / adjoint kernels on the
 config-5 workload (tc_fwd.cuh / tc_bwd.cuh CLK points), cycles per phase.
+Slots 0-7 of a row: consumer / adjoint phases; slots 8-11: forward producer
+(8 before the empty wait, 9 after it, 10 slot filled).
 
     python tools/phase_clocks.py
 """
@@ -15,10 +17,15 @@ s = BSDE("allen_cahn", 100, 80, 0.3, 110, 524288, precision="bf16", lr=5e-4)
 for _ in range(3):
     s.train_step()
 for which, name in ((0, "fwd (per step)"), (1, "bwd (per item)")):
-    c = s.debug_phase_clocks(which, 1024).astype(np.int64)
+    c = s.debug_phase_clocks(which, 1024).astype(np.int64).reshape(-1, 16)
     rows = [r for r in c if r[0] != 0]
-    npts = max(int(np.max(np.nonzero(r)[0])) + 1 for r in rows)
+    npts = max(int(np.max(np.nonzero(r[:8])[0])) + 1 for r in rows)
     d = np.array([np.diff(r[:npts]) for r in rows[2:40]])
     tot = np.array([rows[i + 1][0] - rows[i][0] for i in range(2, min(40, len(rows) - 1))])
     print("%s: %d traced, mean cycles %.0f" % (name, len(rows), tot.mean()))
     print("  phase deltas:", " ".join("%d" % x for x in d.mean(0)))
+    if which == 0 and c[2:40, 8].any():
+        p = c[2:40]
+        print("  producer: wait-empty %.0f  fill %.0f  period %.0f  (fill start - consumer step start %.0f)"
+              % ((p[:, 9] - p[:, 8]).mean(), (p[:, 10] - p[:, 9]).mean(),
+                 np.diff(p[:, 8]).mean(), (p[:, 9] - p[:, 0]).mean()))
