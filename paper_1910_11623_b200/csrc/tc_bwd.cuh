@@ -23,6 +23,10 @@
 // is issued before the gradient GEMM that can overlap the next epilogue; the
 // commit after a chain GEMM also covers every earlier GEMM, which is what frees
 // the operand buffers (H1 after G7, H2/dA2 after G5/G6/G7) without extra waits.
+// The chain GEMMs G2, G4, G6 read their A operand (H1, dZ, dA2) from tensor
+// memory, written by the epilogue next to the shared-memory copy the gradient
+// GEMMs need: shared-memory bandwidth, which the SS MMAs nearly saturate, is the
+// scarce resource of this kernel.
 #pragma once
 
 namespace bsde {
@@ -47,6 +51,9 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int q = warp & 3, g = warp >> 2;
   const int row = 32 * q + lane;
+  // MMA / bulk-copy issuer: lane 0 of the highest warp, which the warp
+  // schedulers favour (every GEMM of the chain waits on its issue)
+  const bool issuer = t == NTH - 32;
   if (t == 0) {
     for (int i = 0; i < 6; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
@@ -57,7 +64,9 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   tc_after();
   const uint32_t tm = *tslot;
   const uint32_t lq = ((uint32_t)(32 * q) << 16) + 8u * g;
-  const uint32_t acc = tm, GA1 = tm + 128, GA2 = tm + 256, GA3 = tm + 384;
+  // TMEM: chain accumulator | A operand of G2/G4/G6 (bf16 pairs) | dW̃1 | dW̃2 | dW̃3
+  const uint32_t acc = tm, hT = tm + 112, GA1 = tm + 176, GA2 = tm + 288, GA3 = tm + 400;
+  const uint32_t lrow = (uint32_t)(32 * q) << 16;
 
   const int64_t i0 = blockIdx.x * items / gridDim.x, i1 = (blockIdx.x + 1) * items / gridDim.x;
   const uint8_t* wsrc = static_cast<const uint8_t*>(a.wpack);
@@ -95,7 +104,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       dwp[i] = chunk_lt(g, i, Dp / 8) ? __ldcs(reinterpret_cast<const uint4*>(src + (g + 4 * i) * 128))
                                       : make_uint4(0, 0, 0, 0);
   };
-  if (t == 0) {
+  if (issuer) {
     if (i0 < i1) load_x(i0);
     if (i0 + 1 < i1) load_x(i0 + 1);
   }
@@ -117,7 +126,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   };
   // gradient flush of step cur_n: TMEM -> fp32 atomics (lane = gradient row)
   auto flush = [&](int pbuf) {
-    if (t == 0) {
+    if (issuer) {
       tc_after();
       if (g8_pending) issue_g8(pbuf);
       else mma_commit(&bars[4]);   // covers every GEMM issued so far
@@ -128,7 +137,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     tc_after();
     float* G = a.grad + nd.step_base(cur_n);
     float v[32];
-    tmem_ld4x8(GA1 + lq, v);                          // dW̃1 row = w-unit, cols = d-inputs
+    tmem_ld_g4(GA1 + lq, g, Dp / 8, v);               // dW̃1 row = w-unit, cols = d-inputs
     if (row < W) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -137,7 +146,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
         else if (k == D) atomicAdd(G + nd.off_b1() + row, v[i]);
       }
     }
-    tmem_ld4x8(GA2 + lq, v);                          // dW̃2
+    tmem_ld_g4(GA2 + lq, g, Wp / 8, v);               // dW̃2
     if (row < W) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -146,7 +155,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
         else if (k == W) atomicAdd(G + nd.off_b2() + row, v[i]);
       }
     }
-    tmem_ld4x8(GA3 + lq, v);                          // dW̃3 row = d-output
+    tmem_ld_g4(GA3 + lq, g, Wp / 8, v);               // dW̃3 row = d-output
     if (row < D) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -164,7 +173,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     const int k = (int)(item - i0), buf = k & 1;
     if (n != cur_n) {
       if (cur_n >= 0) flush(buf ^ 1);
-      if (t == 0) {   // the weight images' last readers completed in flush
+      if (issuer) {   // the weight images' last readers completed in flush
         mbar_expect_tx(&bars[0], Dm::WB);
         const uint8_t* src = wsrc + (size_t)n * Dm::WB;
         for (uint32_t off = 0; off < Dm::WB; off += 16384u)
@@ -177,7 +186,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     }
     CLK(0);
     const bool g8_now = g8_pending;
-    if (t == 0) {   // G1 (recompute), then the previous item's G8
+    if (issuer) {   // G1 (recompute), then the previous item's G8
       mbar_wait(&bars[1 + buf], (uint32_t)((k >> 1) & 1));
       tc_after();
       gemm(acc, kmaj(xb(buf), Dp), kmaj(wimg, Dp), Dp / 16, IW, false);
@@ -186,8 +195,9 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     }
     if (g8_now) f8 = true;
     g8_pending = false;
-    // dZ of this item (heat, Allen-Cahn: ∂_z f = 0), packed bf16, stored into hC
-    // once G8 of the previous item has read dA1 from it
+    // dZ of this item (heat, Allen-Cahn: ∂_z f = 0), bf16 pairs: stored into hC
+    // (G5) once G8 of the previous item has read dA1 from it, and into hT (G4)
+    // once G2 has read H1 from it
     uint4 dzp[4];
     const float ab_i = ab;
     uint4 dwc[4];
@@ -212,41 +222,44 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     // H1 = ReLU(A1) and R2 = ReLU(A2) as bf16 pairs: operands, and (non-zero) the
     // ReLU masks 1[A1 > 0], 1[A2 > 0] of E6 / E4
     uint4 h1p[4], r2p[4];
-    {  // E1: H1 -> hA (its last reader, G7 of the previous item, is done)
+    {  // E1: H1 -> hA (G7; its last reader, G7 of the previous item, is done) and hT (G2)
       float v[32];
       tmem_ld4x8(acc + lq, v);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         h1p[i] = make_uint4(relu_pack2(v[8 * i], v[8 * i + 1]), relu_pack2(v[8 * i + 2], v[8 * i + 3]),
                             relu_pack2(v[8 * i + 4], v[8 * i + 5]), relu_pack2(v[8 * i + 6], v[8 * i + 7]));
-        if (chunk_lt(g, i, Wp / 8)) st_chunk_u4(hA, row, g + 4 * i, Wp, h1p[i]);
+        if (chunk_lt(g, i, Wp / 8)) {
+          tmem_st4(hT + lrow + 4u * (g + 4 * i), h1p[i]);
+          st_chunk_u4(hA, row, g + 4 * i, Wp, h1p[i]);
+        }
       }
     }
+    tmem_wait_st();
     fence_async_smem();
     tc_before();
     __syncthreads();
     CLK(2);
-    if (t == 0) {   // G2: A2 = H1 W̃2ᵀ
+    if (issuer) {   // G2: A2 = H1 W̃2ᵀ (A in TMEM)
       tc_after();
-      gemm(acc, kmaj(hA, Wp), kmaj(wimg + Dm::W1B, Wp), Wp / 16, IW, false);
+      gemm_ta(acc, hT, kmaj(wimg + Dm::W1B, Wp), Wp / 16, IW, false);
       mma_commit(&bars[3]);
     }
     if (g8_now) {   // G8 (previous item) has read hC and its X̃ buffer
       mbar_wait(&bars[4], g8ph);
       g8ph ^= 1;
     }
-    if (t == 0 && k > 0 && item + 1 < i1) load_x(item + 1);
+    if (issuer && k > 0 && item + 1 < i1) load_x(item + 1);
     if (!NEEDZ) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (chunk_lt(g, i, Dp / 8))
-          *reinterpret_cast<uint4*>(hC + (row >> 3) * (Dp * 16) + (g + 4 * i) * 128 + (row & 7) * 16) = dzp[i];
+        if (chunk_lt(g, i, Dp / 8)) st_chunk_u4(hC, row, g + 4 * i, Dp, dzp[i]);
     }
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     CLK(3);
     tc_after();
-    {  // E2: H2 = H1 + ReLU(A2) in bf16x2 arithmetic (R17, as in the forward) -> hB
+    {  // E2: H2 = H1 + ReLU(A2) in bf16x2 arithmetic (R17, as in the forward) -> hB (G5)
       float v[32];
       tmem_ld4x8(acc + lq, v);
 #pragma unroll
@@ -258,13 +271,19 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
                       make_uint4(bf2_add(h1p[i].x, r2p[i].x), bf2_add(h1p[i].y, r2p[i].y),
                                  bf2_add(h1p[i].z, r2p[i].z), bf2_add(h1p[i].w, r2p[i].w)));
       }
+      if (!NEEDZ) {   // dZ -> hT (G2 has read H1)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (chunk_lt(g, i, Dp / 8)) tmem_st4(hT + lrow + 4u * (g + 4 * i), dzp[i]);
+      }
     }
+    tmem_wait_st();
     fence_async_smem();
     tc_before();
     __syncthreads();
     CLK(4);
-    if (NEEDZ) {   // G3: Z = H2 W̃3ᵀ; E3: dZ = ā(ΔW - Δt ∂_z f) -> hC
-      if (t == 0) {
+    if (NEEDZ) {   // G3: Z = H2 W̃3ᵀ; E3: dZ = ā(ΔW - Δt ∂_z f) -> hC, hT
+      if (issuer) {
         tc_after();
         gemm(acc, kmaj(hB, Wp), kmaj(wimg + Dm::W1B + Dm::W2B, Wp), Wp / 16, ID, false);
         mma_commit(&bars[3]);
@@ -284,16 +303,22 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (chunk_lt(g, i, Dp / 8)) st_chunk(hC, row, g + 4 * i, Dp, z + 8 * i);
+        if (chunk_lt(g, i, Dp / 8)) {
+          const uint4 u = make_uint4(pack2(z[8 * i], z[8 * i + 1]), pack2(z[8 * i + 2], z[8 * i + 3]),
+                                     pack2(z[8 * i + 4], z[8 * i + 5]), pack2(z[8 * i + 6], z[8 * i + 7]));
+          st_chunk_u4(hC, row, g + 4 * i, Dp, u);
+          tmem_st4(hT + lrow + 4u * (g + 4 * i), u);
+        }
+      tmem_wait_st();
       fence_async_smem();
       tc_before();
       __syncthreads();
     }
     CLK(5);
-    if (t == 0) {
+    if (issuer) {
       tc_after();
-      // G4: dH2 = dZ W̃3 ; G5: dW̃3 += dZᵀ H2
-      gemm(acc, kmaj(hC, Dp), mnmaj(wimg + Dm::W1B + Dm::W2B, Wp), Dp / 16, IWm, false);
+      // G4: dH2 = dZ W̃3 (A in TMEM) ; G5: dW̃3 += dZᵀ H2
+      gemm_ta(acc, hT, mnmaj(wimg + Dm::W1B + Dm::W2B, Wp), Dp / 16, IWm, false);
       mma_commit(&bars[3]);
       gemm(GA3, mnmaj(hC, Dp), mnmaj(hB, Wp), 128 / 16, IGW, f5);
       mma_commit(&bars[5]);
@@ -303,33 +328,39 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     mph ^= 1;
     CLK(6);
     tc_after();
-    {  // E4: dA2 = dH2 ⊙ 1[A2 > 0], stored over H2 once G5 has read it
+    uint4 pk[4];
+    {  // E4: dA2 = dH2 ⊙ 1[A2 > 0] -> hT (G6), later over H2 in hB (G7)
       float v[32];
       tmem_ld4x8(acc + lq, v);
-      uint4 pk[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i) {
         pk[i] = make_uint4(pack2(v[8 * i], v[8 * i + 1]) & nz_mask2(r2p[i].x),
                            pack2(v[8 * i + 2], v[8 * i + 3]) & nz_mask2(r2p[i].y),
                            pack2(v[8 * i + 4], v[8 * i + 5]) & nz_mask2(r2p[i].z),
                            pack2(v[8 * i + 6], v[8 * i + 7]) & nz_mask2(r2p[i].w));
-      mbar_wait(&bars[5], g5ph);
-      g5ph ^= 1;
-      CLK(7);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (chunk_lt(g, i, Wp / 8))
-          *reinterpret_cast<uint4*>(hB + (row >> 3) * (Wp * 16) + (g + 4 * i) * 128 + (row & 7) * 16) = pk[i];
+        if (chunk_lt(g, i, Wp / 8)) tmem_st4(hT + lrow + 4u * (g + 4 * i), pk[i]);
+      }
     }
-    fence_async_smem();
+    tmem_wait_st();
     tc_before();
     __syncthreads();
-    CLK(8);
-    if (t == 0) {
+    CLK(7);
+    if (issuer) {   // G6: dH1 = dH2 + dA2 W̃2 (accumulated onto dH2; A in TMEM)
       tc_after();
-      // G6: dH1 = dH2 + dA2 W̃2 (accumulated onto dH2) ; G7: dW̃2 += dA2ᵀ H1
-      gemm(acc, kmaj(hB, Wp), mnmaj(wimg + Dm::W1B, Wp), Wp / 16, IWm, true);
+      gemm_ta(acc, hT, mnmaj(wimg + Dm::W1B, Wp), Wp / 16, IWm, true);
       mma_commit(&bars[3]);
+    }
+    // dA2 over H2 once G5 has read it, then G7: dW̃2 += dA2ᵀ H1 (runs during E6)
+    mbar_wait(&bars[5], g5ph);
+    g5ph ^= 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (chunk_lt(g, i, Wp / 8)) st_chunk_u4(hB, row, g + 4 * i, Wp, pk[i]);
+    fence_async_smem();
+    __syncthreads();
+    CLK(8);
+    if (issuer) {
+      tc_after();
       gemm(GA2, mnmaj(hB, Wp), mnmaj(hA, Wp), 128 / 16, IGW, f7);
     }
     f7 = true;

@@ -246,6 +246,27 @@ __device__ __forceinline__ void tmem_ld_chunks(uint32_t base, float (&v)[NC][8],
   }
 }
 
+// The calling thread's chunks g + 4i (i < 4) that exist in an NC-chunk matrix
+// (columns 8(g + 4i) .. +7 from taddr = first chunk of the thread); chunks past
+// the matrix are not read (they may lie past the allocation) and read as 0.
+__device__ __forceinline__ void tmem_ld_g4(uint32_t taddr, int g, int NC, float (&v)[32]) {
+  uint32_t r[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (g + 4 * i < NC) tmem_ld8_nowait(taddr + 32u * i, r[i]);
+    else
+#pragma unroll
+      for (int e = 0; e < 8; ++e) r[i][e] = 0u;
+  }
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    reg_fence8(r[i]);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[8 * i + e] = __uint_as_float(r[i][e]);
+  }
+}
+
 template <int I>
 struct Int {
   static constexpr int value = I;
@@ -272,18 +293,27 @@ __device__ __forceinline__ Opnd mnmaj(const void* img, int C) {
   return Opnd{smem_u32(img), (uint32_t)C * 16u, 128u, (uint32_t)C * 32u};
 }
 // D (+)= A·B over ksteps·16 of K; issued by one thread.
+// The descriptors are built once; a K step only advances the 14-bit start
+// address field (bits 0-13, in 16-byte units), which cannot carry out for
+// operands inside the 227 KB of shared memory.
 __device__ __forceinline__ void gemm(uint32_t d_tmem, Opnd A, Opnd B, int ksteps, uint32_t idesc,
                                      bool accumulate) {
+  const uint64_t a0 = sdesc(A.base, A.lbo, A.sbo), b0 = sdesc(B.base, B.lbo, B.sbo);
+  const uint32_t ai = A.kstep >> 4, bi = B.kstep >> 4;
+#pragma unroll
   for (int k = 0; k < ksteps; ++k)
-    mma_bf16(d_tmem, sdesc(A.base + k * A.kstep, A.lbo, A.sbo),
-             sdesc(B.base + k * B.kstep, B.lbo, B.sbo), idesc, (k > 0 || accumulate) ? 1u : 0u);
+    mma_bf16(d_tmem, a0 + (uint64_t)(k * ai), b0 + (uint64_t)(k * bi), idesc,
+             (k > 0 || accumulate) ? 1u : 0u);
 }
 
 // D (+)= A·B over ksteps·16 of K with A in tensor memory at column a_tmem.
 __device__ __forceinline__ void gemm_ta(uint32_t d_tmem, uint32_t a_tmem, Opnd B, int ksteps,
                                         uint32_t idesc, bool accumulate) {
+  const uint64_t b0 = sdesc(B.base, B.lbo, B.sbo);
+  const uint32_t bi = B.kstep >> 4;
+#pragma unroll
   for (int k = 0; k < ksteps; ++k)
-    mma_bf16_ta(d_tmem, a_tmem + 8u * k, sdesc(B.base + k * B.kstep, B.lbo, B.sbo), idesc,
+    mma_bf16_ta(d_tmem, a_tmem + 8u * k, b0 + (uint64_t)(k * bi), idesc,
                 (k > 0 || accumulate) ? 1u : 0u);
 }
 

@@ -310,6 +310,9 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
       mbar_wait(bg23, 0);
       CLK(3);
       tc_after();
+      // G2 has read W̃2: reload it for the next step right away (its latency
+      // must hide behind E2, G3, E3, G1, E1)
+      if (mma && s + 1 < total) load(wf2, sm + L::W2, wsrc_of(s + 1) + Dm::W1B, Dm::W2B);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float v[HW][8];
@@ -338,15 +341,14 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
         mbar_wait(wf3, (uint32_t)(s & 1));
         gemm_ta(tm + (p ? L::T_ACC1 : 0u), hT, kmaj(sm + L::W3, Wp), Wp / 16, I3, false);
         mma_commit(bg23);
-        if (s + 1 < total) {
-          load(wf2, sm + L::W2, wsrc_of(s + 1) + Dm::W1B, Dm::W2B);
-          issue_g1(s + 1);
-        }
+        if (s + 1 < total) issue_g1(s + 1);
       }
       // E3: a4 Y_{n+1} = Y_n - f(Y_n, Z_n) Δt + Z_n·ΔW_n (one thread per path)
       mbar_wait(bg23, 1);
       CLK(5);
       tc_after();
+      if (mma && s + 1 < total)   // G3 has read W̃3
+        load(wf3, sm + L::W3, wsrc_of(s + 1) + Dm::W1B + Dm::W2B, Dm::W3B);
       mbar_wait(&full[slot], (uint32_t)((s / L::NSLOT) & 1));   // ΔW_n, |X_N|² partials
       tc_after();
       float cz = 0.0f, zz = 0.0f;
@@ -385,10 +387,7 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
       tc_before();
       consumer_sync();
       CLK(6);
-      if (mma) {   // the slot and W̃3 are free
-        mbar_arrive(&empty[slot]);
-        if (s + 1 < total) load(wf3, sm + L::W3, wsrc_of(s + 1) + Dm::W1B + Dm::W2B, Dm::W3B);
-      }
+      if (mma) mbar_arrive(&empty[slot]);   // the slot is free
     }
     // a5: R = Y_N - g(X_N); loss; ā recursion and dY0
     if (valid) {
