@@ -17,6 +17,7 @@ KEYS = [
     ("dram_write_GB", "dram__bytes_write.sum"),
     ("dram_pct_peak", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
     ("tensor_pipe_pct", "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
+    ("tensor_mem_pct", "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
     ("sm_throughput_pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
     ("issue_active_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
     ("warps_active_pct", "sm__warps_active.avg.pct_of_peak_sustained_active"),
@@ -41,8 +42,9 @@ def main(path):
     for d in data:
         print("kernel:", d[idx["Kernel Name"]])
         for name, key in KEYS:
-            if key in idx:
-                print("  %-18s %s %s" % (name, d[idx[key]], units[idx[key]]))
+            k = key if key in idx else next((h for h in idx if h.endswith("." + key)), None)
+            if k is not None:
+                print("  %-18s %s %s" % (name, d[idx[k]], units[idx[k]]))
         stalls = []
         for h, i in idx.items():
             if h.startswith(STALL_PREFIX2) and not h.endswith("not_issued") and d[i]:
