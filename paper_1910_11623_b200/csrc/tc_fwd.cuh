@@ -101,8 +101,8 @@ struct FwdSmem {
   static constexpr uint32_t SLOT0 = W3 + Dm::W3B;
   static constexpr uint32_t SLOTB = Dm::XB + 3 * 128 * 4;     // X̃_n | |X_N|² partials [3][128]
   static constexpr uint32_t BARS = SLOT0 + NSLOT * SLOTB;
-  // full[NSLOT], empty[NSLOT], wf1[2], wf2, wf3, g1, g23
-  static constexpr int NBARS = 2 * NSLOT + 6;
+  // full[NSLOT], empty[NSLOT], wf1[2], wf2, wf3, g1, g23, w1free[2], w2free, w3free
+  static constexpr int NBARS = 2 * NSLOT + 10;
   static constexpr uint32_t TSLOT = BARS + NBARS * 8;
   static constexpr uint32_t BYTES = TSLOT + 16;
   // tensor memory columns: accumulators, the A operand of G2/G3, the ΔW_n ring
@@ -133,6 +133,38 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
   uint8_t* xst = static_cast<uint8_t*>(a.xpack);
   uint8_t* dst = static_cast<uint8_t*>(a.dwpack);
   const uint32_t roff = (row >> 3) * (Dp * 16) + (row & 7) * 16;   // row's offset in an image
+  // Weight reloads: a bulk copy blocks its issuing thread for about the copy's
+  // duration (~700 cycles for one 25 KB matrix), so they are issued here, by
+  // lane 0 of producer warps 1, 2, 3 (W̃1, W̃2, W̃3), between chunks and while
+  // waiting for a free ring slot, as soon as the MMA thread signals that the
+  // GEMM reading the buffer has completed (w?free).  The producers have slack.
+  uint64_t* wfull = bars + 2 * L::NSLOT;            // wf1[2], wf2, wf3
+  uint64_t* wfree = bars + 2 * L::NSLOT + 6;        // w1free[2], w2free, w3free
+  const int loader = (K3 == 0 && lane == 0 && q >= 1) ? q : 0;   // matrix 1, 2, 3 or none
+  const int my_tiles = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int64_t total = (int64_t)my_tiles * N;
+  const uint8_t* wsrc = static_cast<const uint8_t*>(a.wpack);
+  int64_t wnext = loader == 1 ? 2 : 1;                 // next step whose matrix this thread loads
+  auto poll_weights = [&]() {
+    if (!loader || wnext >= total) return;
+    const int64_t t = wnext;
+    uint64_t* fb;
+    uint32_t par;
+    if (loader == 1) { fb = &wfree[t & 1]; par = (uint32_t)(((t >> 1) - 1) & 1); }
+    else { fb = &wfree[loader]; par = (uint32_t)((t - 1) & 1); }
+    if (!mbar_test(fb, par)) return;
+    const uint8_t* src = wsrc + (size_t)(t % N) * Dm::WB;
+    uint8_t* dstw;
+    uint64_t* wb;
+    uint32_t bytes;
+    if (loader == 1) { dstw = sm + L::W1 + (t & 1) * Dm::W1B; wb = &wfull[t & 1]; bytes = Dm::W1B; }
+    else if (loader == 2) { dstw = sm + L::W2; wb = &wfull[2]; bytes = Dm::W2B; src += Dm::W1B; }
+    else { dstw = sm + L::W3; wb = &wfull[3]; bytes = Dm::W3B; src += Dm::W1B + Dm::W2B; }
+    mbar_expect_tx(wb, bytes);
+    for (uint32_t off = 0; off < bytes; off += 16384u)
+      bulk_g2s(dstw + off, src + off, min(16384u, bytes - off), wb);
+    ++wnext;
+  };
   unsigned long long* const pclk = (a.clk && blockIdx.x == 0 && q == 0 && K3 == 0 && lane == 0) ? a.clk : nullptr;
   int64_t s = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -147,7 +179,7 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
       float* xn2 = reinterpret_cast<float*>(ximg + Dm::XB);
       const uint32_t tdw = tm + lane_off + L::T_DW + (uint32_t)slot * L::DWC;
       if (pclk && s < 64) pclk[s * 16 + 8] = clock64();
-      mbar_wait(&empty[slot], (use & 1) ^ 1);
+      while (!mbar_test(&empty[slot], (use & 1) ^ 1)) poll_weights();
       tc_after();
       if (pclk && s < 64) pclk[s * 16 + 9] = clock64();
       const size_t img = ((size_t)n * ntiles + tile) * Dm::XB;
@@ -167,7 +199,9 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
         *reinterpret_cast<uint4*>(ximg + roff + c * 128) = xu;
         const uint4 du = make_uint4(pack_h2(dw[0], dw[1]), pack_h2(dw[2], dw[3]), pack_h2(dw[4], dw[5]),
                                     pack_h2(dw[6], dw[7]));
+#ifndef BSDE_DBG_NOTMEMDW
         if (8 * c < D) tmem_st4(tdw + 4u * c, du);
+#endif
 #ifndef BSDE_DBG_NOSTORE
         if (store) {
           *reinterpret_cast<uint4*>(xst + img + roff + c * 128) = xu;
@@ -188,11 +222,14 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
           chunk_out(Int<i>{}, dw);
           if constexpr (nch == 2) chunk_out(Int<i + 1>{}, dw + 8);
         }
+        poll_weights();
       };
+#ifndef BSDE_DBG_PRODIDLE   // (timing experiments only: producers generate nothing)
       pair(Int<0>{});
       pair(Int<2>{});
       pair(Int<4>{});
       pair(Int<6>{});
+#endif
       if (n + 1 == N) {   // |X_N|² partial for the terminal condition
         float sx = 0.0f;
 #pragma unroll
@@ -209,6 +246,7 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
       mbar_arrive(&full[slot]);
     }
   }
+  while (loader && wnext < total) poll_weights();   // the consumers' last steps
 }
 
 template <int D, int W>
@@ -227,6 +265,7 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
   uint64_t* wf3 = wf1 + 3;
   uint64_t* bg1 = wf1 + 4;
   uint64_t* bg23 = wf1 + 5;
+  uint64_t* wfree = wf1 + 6;   // w1free[2], w2free, w3free (producer-side loaders)
   const int row = 32 * q + lane;
   const bool mma = (q == 3 && lane == 0);   // highest warp id: favoured by the scheduler
   const uint32_t lane_off = (uint32_t)(32 * q) << 16;
@@ -266,6 +305,7 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
   }
 
   unsigned long long* const clk = (a.clk && blockIdx.x == 0 && q == 1 && lane == 0) ? a.clk : nullptr;
+  unsigned long long* const mclk = (a.clk && blockIdx.x == 0 && mma) ? a.clk : nullptr;
 #define CLK(i) do { if (clk && s < 64) clk[s * 16 + (i)] = clock64(); } while (0)
   int64_t s = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -304,7 +344,7 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
         mbar_wait(wf2, (uint32_t)(s & 1));
         gemm_ta(tm + (p ? 0u : L::T_ACC1), hT, kmaj(sm + L::W2, Wp), Wp / 16, I1, false);
         mma_commit(bg23);
-        if (s + 2 < total) load(&wf1[p], sm + L::W1 + p * Dm::W1B, wsrc_of(s + 2), Dm::W1B);
+        if (s + 2 < total) mbar_arrive(&wfree[p]);   // G1(s) done: W̃1 buffer p -> step s + 2
       }
       // E2: H2 = H1 + ReLU(A2) in bf16x2 arithmetic (R17) -> TMEM operand (over H1)
       mbar_wait(bg23, 0);
@@ -312,7 +352,9 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
       tc_after();
       // G2 has read W̃2: reload it for the next step right away (its latency
       // must hide behind E2, G3, E3, G1, E1)
-      if (mma && s + 1 < total) load(wf2, sm + L::W2, wsrc_of(s + 1) + Dm::W1B, Dm::W2B);
+      if (mclk && s < 64) mclk[s * 16 + 12] = clock64();
+      if (mma && s + 1 < total) mbar_arrive(&wfree[2]);   // G2 done: W̃2 -> step s + 1
+      if (mclk && s < 64) mclk[s * 16 + 13] = clock64();
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float v[HW][8];
@@ -333,9 +375,11 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
         }
       }
       tmem_wait_st();
+      if (mclk && s < 64) mclk[s * 16 + 14] = clock64();
       tc_before();
       consumer_sync();
       CLK(4);
+      if (mclk && s < 64) mclk[s * 16 + 15] = clock64();
       if (mma) {   // G3 (A = H2 in TMEM); then G1 of the next step into the other accumulator
         tc_after();
         mbar_wait(wf3, (uint32_t)(s & 1));
@@ -348,10 +392,11 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
       CLK(5);
       tc_after();
       if (mma && s + 1 < total)   // G3 has read W̃3
-        load(wf3, sm + L::W3, wsrc_of(s + 1) + Dm::W1B + Dm::W2B, Dm::W3B);
+        mbar_arrive(&wfree[3]);   // G3 done: W̃3 -> step s + 1
       mbar_wait(&full[slot], (uint32_t)((s / L::NSLOT) & 1));   // ΔW_n, |X_N|² partials
       tc_after();
       float cz = 0.0f, zz = 0.0f;
+      const bool hjb = a.problem == kHJB;
       const uint32_t tdw = tm + lane_off + L::T_DW + (uint32_t)slot * L::DWC;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -369,11 +414,12 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
           float dw[8];
           unpack_dw(make_uint4(dwr[i][0], dwr[i][1], dwr[i][2], dwr[i][3]), dw);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            if (8 * c + e < D) {
-              cz = fmaf(z[i][e], dw[e], cz);
-              zz = fmaf(z[i][e], z[i][e], zz);
-            }
+          for (int e = 0; e < 8; ++e)
+            if (8 * c + e < D) cz = fmaf(z[i][e], dw[e], cz);
+          if (hjb) {   // |Z|² enters the driver only there
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (8 * c + e < D) zz = fmaf(z[i][e], z[i][e], zz);
           }
         }
       }

@@ -33,13 +33,13 @@ for which, name in ((0, "fwd (per step)"), (1, "bwd (per item)")):
         print("  producer: wait-empty %.0f  fill %.0f  period %.0f  (fill start - consumer step start %.0f)"
               % ((p[:, 9] - p[:, 8]).mean(), (p[:, 10] - p[:, 9]).mean(),
                  np.diff(p[:, 8]).mean(), (p[:, 9] - p[:, 0]).mean()))
-    if which == 1 and c[2:40, 8].any():
+    if which == 1 and c[2:40, 8].any() and (c[2:40, 9] >= c[2:40, 8]).all():
         p = c[2:40].astype(np.int64)
         base = p[:, 8]
         print("  issuer (from I0 start): " + " ".join("%d" % (p[:, j] - base).mean() for j in range(9, 16))
               + "  | epilogue CLK0 %d" % (p[:, 0] - base).mean())
     if which == 0 and c[2:40, 12].any():
         p = c[2:40]
-        print("  issuer (G3 block): from step start %.0f, wf3 wait %.0f, G3 issue %.0f, G1(next) issue %.0f; G3 done seen at %.0f"
-              % ((p[:, 12] - p[:, 0]).mean(), (p[:, 13] - p[:, 12]).mean(), (p[:, 14] - p[:, 13]).mean(),
-                 (p[:, 15] - p[:, 14]).mean(), (p[:, 5] - p[:, 0]).mean()))
+        print("  issuer: G2 seen %.0f, W2 reload issued %.0f, E2 done %.0f, barrier passed %.0f | others: G2 seen %.0f, E2 barrier issued %.0f"
+              % ((p[:, 12] - p[:, 0]).mean(), (p[:, 13] - p[:, 0]).mean(), (p[:, 14] - p[:, 0]).mean(),
+                 (p[:, 15] - p[:, 0]).mean(), (p[:, 3] - p[:, 0]).mean(), (p[:, 4] - p[:, 0]).mean()))
