@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   uint8_t* hA = sm + Dm::WB + 2 * Dm::ACT;   // H1
   uint8_t* hB = hA + Dm::ACT;                // H2, then dA2
   uint8_t* hC = hB + Dm::ACT;                // dZ, then dA1
-  // barriers: 0 weights, 1-2 X̃ images, 3 chain GEMMs, 4 G8, 5 G5
+  // barriers: 0 weights, (1-2 unused), 3 chain GEMMs, 4 G8, 5 G5
   uint64_t* bars = reinterpret_cast<uint64_t*>(hC + Dm::ACT);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
 
@@ -85,13 +85,20 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     const int n = (int)(item / ntiles), tile = (int)(item - (int64_t)n * ntiles);
     return ((size_t)n * ntiles + tile) * Dm::XB;
   };
-  auto load_x = [&](int64_t item) {   // thread 0
+  // X̃ image of an item into its buffer: 16-byte cp.async by every thread (a bulk
+  // copy would block its issuing thread for the copy's duration, ~800 cycles)
+  auto load_x = [&](int64_t item) {
     const int buf = (int)((item - i0) & 1);
-    uint64_t* bar = &bars[1 + buf];
-    mbar_expect_tx(bar, Dm::XB);
-    bulk_g2s(xb(buf), xst + img_of(item), Dm::XB, bar);
-    if (item + 2 < i1) bulk_prefetch_l2(xst + img_of(item + 2), Dm::XB);
+    const uint8_t* src = xst + img_of(item);
+    uint8_t* dstp = xb(buf);
+#pragma unroll
+    for (int j = 0; j < (int)((Dm::XB / 16 + NTH - 1) / NTH); ++j) {
+      const int c = t + j * NTH;
+      if (c < (int)(Dm::XB / 16)) cp_async16(dstp + 16 * c, src + 16 * c);
+    }
+    cp_async_commit();
   };
+
   // per-path inputs of an item: ā_{n+1} and this thread's ΔW_n chunks (fp16)
   auto load_inputs = [&](int64_t item, float& ab, uint4 (&dwp)[4]) {
     const int n = (int)(item / ntiles), tile = (int)(item - (int64_t)n * ntiles);
@@ -104,10 +111,11 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       dwp[i] = chunk_lt(g, i, Dp / 8) ? __ldcs(reinterpret_cast<const uint4*>(src + (g + 4 * i) * 128))
                                       : make_uint4(0, 0, 0, 0);
   };
-  if (issuer) {
-    if (i0 < i1) load_x(i0);
-    if (i0 + 1 < i1) load_x(i0 + 1);
-  }
+  if (i0 < i1) load_x(i0);
+  if (i0 + 1 < i1) load_x(i0 + 1);
+  cp_async_wait_all();
+  fence_async_smem();
+  __syncthreads();
   float ab = 0.0f;
   uint4 dwp[4];
   if (i0 < i1) load_inputs(i0, ab, dwp);
@@ -187,7 +195,6 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     CLK(0);
     const bool g8_now = g8_pending;
     if (issuer) {   // G1 (recompute), then the previous item's G8
-      mbar_wait(&bars[1 + buf], (uint32_t)((k >> 1) & 1));
       tc_after();
       gemm(acc, kmaj(xb(buf), Dp), kmaj(wimg, Dp), Dp / 16, IW, false);
       mma_commit(&bars[3]);
@@ -249,7 +256,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       mbar_wait(&bars[4], g8ph);
       g8ph ^= 1;
     }
-    if (issuer && k > 0 && item + 1 < i1) load_x(item + 1);
+    if (k > 0 && item + 1 < i1) load_x(item + 1);
     if (!NEEDZ) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -380,6 +387,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
                                  pack2(v[8 * i + 4], v[8 * i + 5]) & nz_mask2(h1p[i].z),
                                  pack2(v[8 * i + 6], v[8 * i + 7]) & nz_mask2(h1p[i].w)));
     }
+    cp_async_wait_all();   // the next item's X̃ (loaded during this item) is in place
     fence_async_smem();
     tc_before();
     __syncthreads();
