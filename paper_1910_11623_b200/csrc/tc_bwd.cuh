@@ -81,15 +81,14 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   constexpr uint32_t IGW = idesc_bf16(128, Wp, true, true);      // G5, G7 (over paths)
   constexpr uint32_t IGD = idesc_bf16(128, Dp, true, true);      // G8
 
-  auto img_of = [&](int64_t item) -> size_t {
-    const int n = (int)(item / ntiles), tile = (int)(item - (int64_t)n * ntiles);
-    return ((size_t)n * ntiles + tile) * Dm::XB;
-  };
+  // items are (step n, tile) in n-major order; (n, tile) is tracked incrementally
+  // (a 64-bit division per item and thread costs more than an epilogue)
+  auto img_of = [&](int n, int tile) -> size_t { return ((size_t)n * ntiles + tile) * Dm::XB; };
   // X̃ image of an item into its buffer: 16-byte cp.async by every thread (a bulk
   // copy would block its issuing thread for the copy's duration, ~800 cycles)
-  auto load_x = [&](int64_t item) {
+  auto load_x = [&](int64_t item, int n, int tile) {
     const int buf = (int)((item - i0) & 1);
-    const uint8_t* src = xst + img_of(item);
+    const uint8_t* src = xst + img_of(n, tile);
     uint8_t* dstp = xb(buf);
 #pragma unroll
     for (int j = 0; j < (int)((Dm::XB / 16 + NTH - 1) / NTH); ++j) {
@@ -100,25 +99,32 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   };
 
   // per-path inputs of an item: ā_{n+1} and this thread's ΔW_n chunks (fp16)
-  auto load_inputs = [&](int64_t item, float& ab, uint4 (&dwp)[4]) {
-    const int n = (int)(item / ntiles), tile = (int)(item - (int64_t)n * ntiles);
+  auto load_inputs = [&](int n, int tile, float& ab, uint4 (&dwp)[4]) {
     const int64_t mloc = (int64_t)tile * 128 + row;
     ab = mloc < a.B_local ? (ac ? __ldcs(a.abar + (int64_t)n * a.B_local + mloc) : __ldg(a.abar + mloc))
                           : 0.0f;
-    const uint8_t* src = dst + img_of(item) + (row >> 3) * (Dp * 16) + (row & 7) * 16;
+    const uint8_t* src = dst + img_of(n, tile) + (row >> 3) * (Dp * 16) + (row & 7) * 16;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       dwp[i] = chunk_lt(g, i, Dp / 8) ? __ldcs(reinterpret_cast<const uint4*>(src + (g + 4 * i) * 128))
                                       : make_uint4(0, 0, 0, 0);
   };
-  if (i0 < i1) load_x(i0);
-  if (i0 + 1 < i1) load_x(i0 + 1);
+  const int n_first = (int)(i0 / ntiles), t_first = (int)(i0 - (int64_t)n_first * ntiles);
+  auto next_of = [&](int n, int tile, int& n1, int& t1) {
+    t1 = tile + 1;
+    n1 = n;
+    if (t1 == ntiles) { t1 = 0; ++n1; }
+  };
+  int n_nx, t_nx;
+  next_of(n_first, t_first, n_nx, t_nx);
+  if (i0 < i1) load_x(i0, n_first, t_first);
+  if (i0 + 1 < i1) load_x(i0 + 1, n_nx, t_nx);
   cp_async_wait_all();
   fence_async_smem();
   __syncthreads();
   float ab = 0.0f;
   uint4 dwp[4];
-  if (i0 < i1) load_inputs(i0, ab, dwp);
+  if (i0 < i1) load_inputs(n_first, t_first, ab, dwp);
 
   uint32_t mph = 0, wph = 0, g8ph = 0, g5ph = 0;
   unsigned long long* const clk = (a.clk && blockIdx.x == 0 && t == 32) ? a.clk : nullptr;
@@ -176,8 +182,9 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     __syncthreads();
   };
 
-  for (int64_t item = i0; item < i1; ++item) {
-    const int n = (int)(item / ntiles);
+  int n = n_first, tile = t_first;
+  for (int64_t item = i0; item < i1; ++item, n = n_nx, tile = t_nx) {
+    next_of(n, tile, n_nx, t_nx);
     const int k = (int)(item - i0), buf = k & 1;
     if (n != cur_n) {
       if (cur_n >= 0) flush(buf ^ 1);
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
                             pack2(dw[6], dw[7]));
       }
     }
-    if (item + 1 < i1) load_inputs(item + 1, ab, dwp);   // consumed by the next item
+    if (item + 1 < i1) load_inputs(n_nx, t_nx, ab, dwp);   // consumed by the next item
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     CLK(1);
@@ -256,7 +263,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
       mbar_wait(&bars[4], g8ph);
       g8ph ^= 1;
     }
-    if (k > 0 && item + 1 < i1) load_x(item + 1);
+    if (k > 0 && item + 1 < i1) load_x(item + 1, n_nx, t_nx);
     if (!NEEDZ) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)

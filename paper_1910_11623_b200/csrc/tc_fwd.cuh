@@ -153,7 +153,7 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
     if (loader == 1) { fb = &wfree[t & 1]; par = (uint32_t)(((t >> 1) - 1) & 1); }
     else { fb = &wfree[loader]; par = (uint32_t)((t - 1) & 1); }
     if (!mbar_test(fb, par)) return;
-    const uint8_t* src = wsrc + (size_t)(t % N) * Dm::WB;
+    const uint8_t* src = wsrc + (size_t)((uint32_t)t % (uint32_t)N) * Dm::WB;
     uint8_t* dstw;
     uint64_t* wb;
     uint32_t bytes;
@@ -281,7 +281,7 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
   constexpr uint32_t I3 = idesc_bf16(128, Dp, false, false);
   (void)NCD;
 
-  auto wsrc_of = [&](int64_t s) { return wsrc + (size_t)(s % N) * Dm::WB; };
+  auto wsrc_of = [&](int64_t s) { return wsrc + (size_t)((uint32_t)s % (uint32_t)N) * Dm::WB; };
   auto load = [&](uint64_t* bar, uint8_t* dstp, const uint8_t* src, uint32_t bytes) {
     mbar_expect_tx(bar, bytes);
     for (uint32_t off = 0; off < bytes; off += 16384u)

@@ -179,6 +179,13 @@ __global__ void __launch_bounds__(512, 1) k_epi(int iters, unsigned long long* o
 #pragma unroll
       for (int c = 0; c < 32; ++c) acc += __float_as_uint(v[c]);
     }
+    if (PARTS & 8) {   // + 4 tcgen05.st.32x32b.x4 of the packed chunks and wait::st
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        tmem_st4(tm + 256 + 4 * c + 16 * g, make_uint4(__float_as_uint(v[8 * c]), __float_as_uint(v[8 * c + 1]),
+                                                       __float_as_uint(v[8 * c + 2]), __float_as_uint(v[8 * c + 3])));
+      tmem_wait_st();
+    }
     if (PARTS & 2) fence_async_smem();
     if (PARTS & 4) {
       tc_before();
@@ -213,6 +220,8 @@ void run_epi() {
   EPI(5, "ld + cvt + STS + bar")
   EPI(7, "ld + cvt + STS + fence + bar")
   EPI(4, "ld + bar")
+  EPI(9, "ld + cvt + STS + tmem st")
+  EPI(15, "ld + cvt + STS + tmem st + fence + bar")
 }
 
 
