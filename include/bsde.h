@@ -188,7 +188,8 @@ int bsde_debug_umma(int mode, const float* a, const float* b, float* d_out);
 /* Profiling hook: runs one forward (which = 0) or forward + adjoint (which = 1)
  * pass of the current iteration with a clock64() trace of CTA 0 enabled and
  * copies up to n stamps to host out[] (16 slots per step/item, 0 = unused; see
- * tc.cu CLK points).  Overwrites the gradient buffer.  tcgen05 path only.
+ * tc.cu CLK points; all zero unless the library was built with
+ * -DBSDE_PHASE_CLOCKS).  Overwrites the gradient buffer.  tcgen05 path only.
  * Synchronises. */
 int bsde_debug_phase_clocks(bsde_ctx* ctx, int which, uint64_t* out, int n);
 

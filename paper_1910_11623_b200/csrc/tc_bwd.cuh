@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
 
   uint32_t mph = 0, wph = 0, g8ph = 0, g5ph = 0;
   unsigned long long* const clk = (a.clk && blockIdx.x == 0 && t == 32) ? a.clk : nullptr;
-#define CLK(i) do { if (clk && item - i0 < 64) clk[(item - i0) * 16 + (i)] = clock64(); } while (0)
+#define CLK(i) do { if (item - i0 < 64) BSDE_STAMP(clk, (item - i0) * 16 + (i)); } while (0)
   int cur_n = -1;
   bool f5 = false, f7 = false, f8 = false;   // accumulator holds a partial of step cur_n
   bool g8_pending = false;                   // G8 of the previous item not issued yet

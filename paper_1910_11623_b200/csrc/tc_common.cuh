@@ -278,6 +278,28 @@ __device__ __forceinline__ void tmem_ld_g4(uint32_t taddr, int g, int NC, float 
   }
 }
 
+// clock64() phase tracing of CTA 0 (tools/phase_clocks.py): compiled in only
+// with -DBSDE_PHASE_CLOCKS, so the product kernels carry no clock reads.
+#ifdef BSDE_PHASE_CLOCKS
+#define BSDE_STAMP(ptr, idx) do { if (ptr) (ptr)[idx] = clock64(); } while (0)
+#else
+#define BSDE_STAMP(ptr, idx) do { (void)(ptr); } while (0)
+#endif
+
+// mbarrier phase wait that suspends the thread for at most `ns` nanoseconds;
+// returns whether the phase completed
+__device__ __forceinline__ bool mbar_try_wait_ns(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+
 template <int I>
 struct Int {
   static constexpr int value = I;

@@ -178,10 +178,14 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
       uint8_t* ximg = sm + L::SLOT0 + slot * L::SLOTB;
       float* xn2 = reinterpret_cast<float*>(ximg + Dm::XB);
       const uint32_t tdw = tm + lane_off + L::T_DW + (uint32_t)slot * L::DWC;
-      if (pclk && s < 64) pclk[s * 16 + 8] = clock64();
-      while (!mbar_test(&empty[slot], (use & 1) ^ 1)) poll_weights();
+      if (s < 64) BSDE_STAMP(pclk, s * 16 + 8);
+      if (loader) {
+        while (!mbar_try_wait_ns(&empty[slot], (use & 1) ^ 1, 200)) poll_weights();
+      } else {
+        mbar_wait(&empty[slot], (use & 1) ^ 1);
+      }
       tc_after();
-      if (pclk && s < 64) pclk[s * 16 + 9] = clock64();
+      if (s < 64) BSDE_STAMP(pclk, s * 16 + 9);
       const size_t img = ((size_t)n * ntiles + tile) * Dm::XB;
       // X̃_n chunk from X, ΔW_n chunk (fp16: TMEM ring + image), then X_{n+1}
       auto chunk_out = [&](auto ic, const float* dw) {
@@ -239,14 +243,17 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
             if (8 * (K3 + 3 * i) + e < D) sx = fmaf(X[8 * i + e], X[8 * i + e], sx);
         xn2[K3 * 128 + row] = sx;
       }
-      if (pclk && s < 64) pclk[s * 16 + 10] = clock64();
+      if (s < 64) BSDE_STAMP(pclk, s * 16 + 10);
       tmem_wait_st();
       tc_before();
       fence_async_smem();   // X̃_n is read by the tensor cores
       mbar_arrive(&full[slot]);
     }
   }
-  while (loader && wnext < total) poll_weights();   // the consumers' last steps
+  while (loader && wnext < total) {   // the consumers' last steps
+    poll_weights();
+    __nanosleep(128);
+  }
 }
 
 template <int D, int W>
@@ -306,7 +313,7 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
 
   unsigned long long* const clk = (a.clk && blockIdx.x == 0 && q == 1 && lane == 0) ? a.clk : nullptr;
   unsigned long long* const mclk = (a.clk && blockIdx.x == 0 && mma) ? a.clk : nullptr;
-#define CLK(i) do { if (clk && s < 64) clk[s * 16 + (i)] = clock64(); } while (0)
+#define CLK(i) do { if (s < 64) BSDE_STAMP(clk, s * 16 + (i)); } while (0)
   int64_t s = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t mloc = (int64_t)tile * 128 + row;
@@ -352,9 +359,9 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
       tc_after();
       // G2 has read W̃2: reload it for the next step right away (its latency
       // must hide behind E2, G3, E3, G1, E1)
-      if (mclk && s < 64) mclk[s * 16 + 12] = clock64();
+      if (s < 64) BSDE_STAMP(mclk, s * 16 + 12);
       if (mma && s + 1 < total) mbar_arrive(&wfree[2]);   // G2 done: W̃2 -> step s + 1
-      if (mclk && s < 64) mclk[s * 16 + 13] = clock64();
+      if (s < 64) BSDE_STAMP(mclk, s * 16 + 13);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float v[HW][8];
@@ -375,11 +382,11 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
         }
       }
       tmem_wait_st();
-      if (mclk && s < 64) mclk[s * 16 + 14] = clock64();
+      if (s < 64) BSDE_STAMP(mclk, s * 16 + 14);
       tc_before();
       consumer_sync();
       CLK(4);
-      if (mclk && s < 64) mclk[s * 16 + 15] = clock64();
+      if (s < 64) BSDE_STAMP(mclk, s * 16 + 15);
       if (mma) {   // G3 (A = H2 in TMEM); then G1 of the next step into the other accumulator
         tc_after();
         mbar_wait(wf3, (uint32_t)(s & 1));

@@ -1,5 +1,10 @@
 """clock64() phase trace of CTA 0 of the tcgen05 forward / adjoint kernels on the
 config-5 workload (tc_fwd.cuh / tc_bwd.cuh CLK points), cycles per phase.
+The stamps are compiled in only with -DBSDE_PHASE_CLOCKS:
+
+    tools/build_variant.sh clocks -DBSDE_PHASE_CLOCKS
+    BSDE_LIB=build_variants/clocks.so python tools/phase_clocks.py
+
 Slots 0-7 of a row: consumer / adjoint phases; slots 8-11: forward producer
 (8 before the empty wait, 9 after it, 10 slot filled).
 
