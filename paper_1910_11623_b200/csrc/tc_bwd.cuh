@@ -249,8 +249,10 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
         }
       }
     }
+    // No proxy fence here: G2 reads H1 from TMEM; the smem copy (G7's operand) is
+    // fenced with dA2 later.  fence.proxy.async is a MEMBAR.ALL.CTA, which would
+    // also wait for this item's prefetch loads from HBM.
     tmem_wait_st();
-    fence_async_smem();
     tc_before();
     __syncthreads();
     CLK(2);
