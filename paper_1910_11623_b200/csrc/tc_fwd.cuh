@@ -51,7 +51,7 @@ __device__ __forceinline__ void consumer_sync() { named_sync(1, kFwdConsumers); 
 // whose columns are all >= D are 0.
 template <int D, int CS, int NCH>
 __device__ __forceinline__ void gen_chunks(int c0, uint32_t m, uint32_t n, uint32_t it, uint32_t k0,
-                                           uint32_t k1, float sdt, float (&dw)[2 * 8]) {
+                                           uint32_t k1, float sdt, float (&dw)[NCH * 8]) {
   constexpr int K = 2 * NCH;
   uint4 c[K];
   bool ok[K];   // warp-uniform: block has columns < D
@@ -216,23 +216,28 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
         for (int e = 0; e < 8; ++e)
           if (8 * c + e < D) X[8 * i + e] = fmaf(kSqrt2, dw[e], X[8 * i + e]);   // a2
       };
-      // chunks i, i+1 together: four Philox streams interleaved
-      auto pair = [&](auto ic) {
+      // GRP chunks together: 2·GRP Philox streams interleaved
+#ifndef BSDE_EXP_GROUP
+#define BSDE_EXP_GROUP 2
+#endif
+      constexpr int GRP = BSDE_EXP_GROUP;
+      auto group = [&](auto ic) {
         constexpr int i = decltype(ic)::value;
         if constexpr (i < NI) {
-          constexpr int nch = (i + 1 < NI) ? 2 : 1;
-          float dw[16];
+          constexpr int nch = (i + GRP <= NI) ? GRP : NI - i;
+          float dw[nch * 8];
           gen_chunks<D, 3, nch>(K3 + 3 * i, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt, dw);
           chunk_out(Int<i>{}, dw);
-          if constexpr (nch == 2) chunk_out(Int<i + 1>{}, dw + 8);
+          if constexpr (nch >= 2) chunk_out(Int<i + 1>{}, dw + 8);
+          if constexpr (nch >= 3) chunk_out(Int<i + 2>{}, dw + 16);
         }
         poll_weights();
       };
 #ifndef BSDE_DBG_PRODIDLE   // (timing experiments only: producers generate nothing)
-      pair(Int<0>{});
-      pair(Int<2>{});
-      pair(Int<4>{});
-      pair(Int<6>{});
+      group(Int<0>{});
+      group(Int<GRP>{});
+      group(Int<2 * GRP>{});
+      group(Int<3 * GRP>{});
 #endif
       if (n + 1 == N) {   // |X_N|² partial for the terminal condition
         float sx = 0.0f;
