@@ -7,6 +7,7 @@ parameters and all the Y_n are computed using an Euler discretization"):
 
   ΔW_n ~ N(0, Δt)                                  Eq. 5, P:64   (philox.py, R8)
   X_{n+1} = X_n + σ ΔW_n,  σ = √2 I, μ = 0         Eq. 5; Eq. 12
+     (Black-Scholes: X_{n+1} = X_n + σ X_n ⊙ ΔW_n, σ(x) = 0.4 diag(x); R21)
   Z_n = net_n(X_n)  (lift, one residual block, head) Eq. 7; R4
   Y_{n+1} = Y_n + φ Δt + Z_n·ΔW_n,  φ = -f         Eq. 5; R2
   L = (1/B) Σ_m (Y_N - g(X_N))²                    Eq. 6, P:75 (terminal term); R5
@@ -22,9 +23,21 @@ import numpy as np
 
 from . import philox
 
-HEAT, HJB, ALLEN_CAHN = 0, 1, 2
-PROBLEM_NAMES = {"heat": HEAT, "hjb": HJB, "allen_cahn": ALLEN_CAHN}
+HEAT, HJB, ALLEN_CAHN, BLACK_SCHOLES = 0, 1, 2, 3
+PROBLEM_NAMES = {"heat": HEAT, "hjb": HJB, "allen_cahn": ALLEN_CAHN,
+                 "black_scholes": BLACK_SCHOLES}
 SIGMA = np.sqrt(2.0)          # dX = √2 dW in every config (BASELINE.json configs 1-5)
+# Black-Scholes: uncorrelated assets with the
+# same volatility, "d = 100, r = 0.05 and σ = 0.4", g(x) = ‖x‖².
+BS_RATE, BS_SIGMA = 0.05, 0.4
+
+
+def forward_step(problem, X, dW):
+    """Euler step of the forward SDE (Eq. 5; μ = 0): X + σ ΔW with σ = √2 I,
+    or for Black-Scholes X + σ X ⊙ ΔW (σ(x) = σ diag(x))."""
+    if problem == BLACK_SCHOLES:
+        return X + BS_SIGMA * X * dW
+    return X + SIGMA * dW
 
 
 # ----------------------------------------------------------------------------
@@ -33,32 +46,40 @@ SIGMA = np.sqrt(2.0)          # dX = √2 dW in every config (BASELINE.json conf
 # ----------------------------------------------------------------------------
 def driver_f(problem, y, z, lam=1.0):
     """f(y, z): heat 0 (R13); HJB -λ|z|²/2 (P:302 read as ‖Du‖², R10);
-    Allen-Cahn y - y³ (R12)."""
+    Allen-Cahn y - y³ (R12); Black-Scholes -r(y - Σ_i z_i / σ) (P:293 with
+    z = σᵀ∇u = σ x ⊙ ∇u, so (Du)ᵀx = Σ z_i / σ; R21)."""
     if problem == HEAT:
         return np.zeros_like(y)
     if problem == HJB:
         return -0.5 * lam * np.sum(z * z, axis=-1)
     if problem == ALLEN_CAHN:
         return y - y ** 3
+    if problem == BLACK_SCHOLES:
+        return -BS_RATE * (y - np.sum(z, axis=-1) / BS_SIGMA)
     raise ValueError(problem)
 
 
 def driver_df_dy(problem, y, z, lam=1.0):
     if problem == ALLEN_CAHN:
         return 1.0 - 3.0 * y * y
+    if problem == BLACK_SCHOLES:
+        return np.full_like(y, -BS_RATE)
     return np.zeros_like(y)
 
 
 def driver_df_dz(problem, y, z, lam=1.0):
     if problem == HJB:
         return -lam * z
+    if problem == BLACK_SCHOLES:
+        return np.full_like(z, BS_RATE / BS_SIGMA)
     return np.zeros_like(z)
 
 
 def terminal_g(problem, x):
-    """g: heat |x|² (R13); HJB ln(0.5(1+|x|²)); Allen-Cahn 1/(2+0.4|x|²) (R12)."""
+    """g: heat |x|² (R13); HJB ln(0.5(1+|x|²)) (P:307); Allen-Cahn 1/(2+0.4|x|²) (P:312, R12);
+    Black-Scholes |x|² (P:294)."""
     s = np.sum(x * x, axis=-1)
-    if problem == HEAT:
+    if problem in (HEAT, BLACK_SCHOLES):
         return s
     if problem == HJB:
         return np.log(0.5 * (1.0 + s))
@@ -165,7 +186,7 @@ def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
         A1, H1, A2, H2, Z = net_forward(nets[n], X, bf16)                # P:78, Eq. 7
         trace.append((X, dW, A1, H1, A2, H2, Z, Y))
         Y = Y - driver_f(problem, Y, Z, lam) * dt + np.sum(Z * dW, axis=-1)   # P:66 (φ=-f)
-        X = X + SIGMA * dW
+        X = forward_step(problem, X, dW)
     R = Y - terminal_g(problem, X)
     out = dict(loss_sum=float(np.sum(R * R)), loss=float(np.sum(R * R) / B),
                R=R, Y_N=Y, X_N=X)

@@ -70,3 +70,23 @@ def allen_cahn_linearised_u0(d, T):
 def allen_cahn_zero_z_ode(y0, T):
     """Exact solution of y' = -(y - y³), y(0) = y0, at time T (the Z ≡ 0 limit)."""
     return float((1.0 + (y0 ** -2 - 1.0) * np.exp(2.0 * T)) ** -0.5)
+
+
+# ----------------------------------------------------------------------------
+# Black-Scholes (P:291-299; SURVEY §8(f) NEXT-3): dX = σ diag(X) dW, g = ‖x‖²
+# ----------------------------------------------------------------------------
+def bs_u0(d, T, x0=1.0, r=0.05, sigma=0.4):
+    """u(x0, 0) = e^{(r+σ²)T} ‖x0‖² with x0 = x0·1 (P:297)."""
+    return float(np.exp((r + sigma * sigma) * T) * d * x0 * x0)
+
+
+def bs_discrete_second_moment(d, N, T, x0=1.0, sigma=0.4):
+    """E‖X_N‖² of the Euler scheme X_{n+1,i} = X_{n,i}(1 + σΔW_{n,i}): every step
+    multiplies E[X_i²] by E[(1 + σΔW)²] = 1 + σ²Δt, exactly."""
+    return float(d * x0 * x0 * (1.0 + sigma * sigma * T / N) ** N)
+
+
+def bs_zero_z_growth(N, T, r=0.05):
+    """With Z ≡ 0 the Y recursion Y_{n+1} = Y_n - f Δt, f = -r(y - Σz/σ), is
+    Y_{n+1} = (1 + rΔt) Y_n: Y_N = Y0 (1 + rΔt)^N exactly."""
+    return float((1.0 + r * T / N) ** N)

@@ -119,8 +119,65 @@ def test_allen_cahn_zero_z_converges_to_ode():
     assert abs(ys[0] - 0.392951276) < 1e-9
 
 
+# ---------------------------------------------------------------- Black-Scholes (NEXT-3)
+def test_black_scholes_zero_z_growth_and_terminal():
+    """Pin BS1: Z ≡ 0 ⇒ f = -r y ⇒ Y_N = Y0 (1 + rΔt)^N exactly (closed form of the
+    linear recursion), and X_N = x0 Π_n (1 + σ ΔW_n) component-wise (the Euler
+    step of dX = σ diag(X) dW), so R = Y_N - ‖X_N‖² (g) is known
+    from the increments alone."""
+    d, w, N, T, B, x0 = 5, 6, 7, 1.0, 200, 1.3
+    p = bsde.init_params(4, d, w, N)
+    _, nets = bsde.unpack(p, d, w, N)
+    for net in nets:
+        net["W3"][...] = 0.0
+    r = bsde.iteration(bsde.BLACK_SCHOLES, d, w, N, T, p, 0, 3, np.arange(B), B, x0=x0,
+                       want_grad=False)
+    assert np.allclose(r["Y_N"], p[0] * cf.bs_zero_z_growth(N, T), rtol=1e-13, atol=0)
+    XN = np.full((B, d), x0)
+    for n in range(N):
+        XN = XN * (1.0 + 0.4 * philox.brownian_increments(0, 3, n, np.arange(B), d, T / N))
+    assert np.allclose(r["R"], r["Y_N"] - np.sum(XN * XN, 1), rtol=1e-12, atol=1e-12)
+
+
+def test_black_scholes_second_moment():
+    """Pin BS2: E‖X_N‖² = d x0² (1 + σ²Δt)^N exactly for the Euler scheme (each
+    step multiplies E[X_i²] by 1 + σ²Δt); checked within 4 standard errors over
+    the oracle's Philox paths, and -- a wrong σ or an additive step would move
+    it by > 30 SE -- against the continuous closed form's growth e^{σ²T}."""
+    d, N, T, B, x0 = 8, 10, 1.0, 40000, 2.0
+    X = np.full((B, d), x0)
+    for n in range(N):
+        X = bsde.forward_step(bsde.BLACK_SCHOLES, X, philox.brownian_increments(0, 0, n, np.arange(B), d, T / N))
+    s = np.sum(X * X, 1)
+    se = s.std() / np.sqrt(B)
+    assert abs(s.mean() - cf.bs_discrete_second_moment(d, N, T, x0)) < 4 * se
+    assert abs(cf.bs_discrete_second_moment(d, N, T, x0) - d * x0 * x0 * np.exp(0.16 * T)) < 0.02 * d * x0 * x0
+    additive = d * x0 * x0 + d * 0.16 * T          # X + σΔW instead of X + σXΔW
+    assert abs(s.mean() - additive) > 30 * se
+
+
+def test_black_scholes_closed_form():
+    """u(x, t) = e^{(r+σ²)(T-t)} ‖x‖² solves u_t = -½Tr[σ² diag(x²) D²u] + r(u - (Du)ᵀx)
+    (P:293-297), checked by finite differences at random points; and the driver
+    f = -r(y - Σz/σ) with z = σ x ⊙ ∇u reproduces the PDE's right-hand side term."""
+    rng = np.random.default_rng(0)
+    d, r, sg, T = 4, 0.05, 0.4, 1.0
+    u = lambda x, t: np.exp((r + sg * sg) * (T - t)) * np.sum(x * x)
+    for _ in range(5):
+        x, t, h = rng.uniform(0.5, 1.5, d), rng.uniform(0, T), 1e-4
+        ut = (u(x, t + h) - u(x, t - h)) / (2 * h)
+        grad = np.array([(u(x + h * e, t) - u(x - h * e, t)) / (2 * h) for e in np.eye(d)])
+        lap = np.array([(u(x + h * e, t) - 2 * u(x, t) + u(x - h * e, t)) / h ** 2 for e in np.eye(d)])
+        rhs = -0.5 * sg * sg * np.sum(x * x * lap) + r * (u(x, t) - grad @ x)
+        assert abs(ut - rhs) < 1e-5 * abs(ut)
+        z = sg * x * grad
+        f = bsde.driver_f(bsde.BLACK_SCHOLES, np.array(u(x, t)), z[None, :])
+        assert abs(-f - r * (u(x, t) - grad @ x)) < 1e-6 * abs(f)
+    assert abs(cf.bs_u0(100, 1.0) - 100 * np.exp(0.21)) < 1e-12
+
+
 # ---------------------------------------------------------------- H6: FD gradients
-@pytest.mark.parametrize("problem", [bsde.HEAT, bsde.HJB, bsde.ALLEN_CAHN])
+@pytest.mark.parametrize("problem", [bsde.HEAT, bsde.HJB, bsde.ALLEN_CAHN, bsde.BLACK_SCHOLES])
 @pytest.mark.parametrize("d,w,N,B", [(2, 4, 2, 4), (3, 8, 3, 8)])
 def test_gradient_matches_central_differences(problem, d, w, N, B):
     T, seed, it, x0 = 0.5, 3, 1, 0.3
