@@ -123,13 +123,14 @@ def oracle_rate(wl, paths, iters):
     """The float64 oracle as it stands on a bounded path sample; path-steps/s."""
     from threadpoolctl import threadpool_info
     from oracle import bsde as ob
-    prob = {"heat": ob.HEAT, "hjb": ob.HJB, "allen_cahn": ob.ALLEN_CAHN}[wl.problem]
+    prob = ob.PROBLEM_NAMES[wl.problem]
     p = ob.init_params(wl.seed, wl.d, wl.w, wl.N)
     st = ob.AdamState(p.size)
     times = []
     for k in range(iters):
         t0 = time.perf_counter()
-        r = ob.iteration(prob, wl.d, wl.w, wl.N, wl.T, p, wl.seed, k, np.arange(paths), wl.batch)
+        r = ob.iteration(prob, wl.d, wl.w, wl.N, wl.T, p, wl.seed, k, np.arange(paths), wl.batch,
+                         x0=wl.x0)
         ob.adam_step(p, r["grad"], st, wl.lr, loss=r["loss"])
         times.append(time.perf_counter() - t0)
     threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
@@ -196,7 +197,7 @@ def main():
     from paper_1910_11623_b200 import BSDE
 
     kw = dict(lr=wl.lr, precision=wl.precision, kernel=args.kernel, seed=wl.seed,
-              device=local_rank)
+              device=local_rank, x0=wl.x0)
     if world > 1:
         s = BSDE.distributed(wl.problem, wl.d, wl.N, wl.T, wl.w, wl.batch, **kw)
     else:

@@ -44,7 +44,9 @@ extern "C" {
 enum {
   BSDE_HEAT = 0,       /* f = 0,            g = |x|²            (config 1; R13)      */
   BSDE_HJB = 1,        /* f = -λ|z|²/2,     g = ln(0.5(1+|x|²))   */
-  BSDE_ALLEN_CAHN = 2  /* f = y - y³,       g = 1/(2+0.4|x|²)   */
+  BSDE_ALLEN_CAHN = 2, /* f = y - y³,       g = 1/(2+0.4|x|²)   */
+  BSDE_BLACK_SCHOLES = 3 /* X_{n+1} = X_n + σ X_n ⊙ ΔW_n, f = -r(y - Σz/σ), g = |x|²,
+                            r = 0.05, σ = 0.4 (DESIGN R21)            */
 };
 
 /* GEMM operand precision; accumulation is always fp32 (R17, R18). */
@@ -77,7 +79,7 @@ typedef struct bsde_ctx bsde_ctx;   /* opaque; one per GPU / rank */
 
 typedef struct {
   int64_t batch_global;   /* B: paths per iteration summed over ranks; B % world == 0      */
-  double x0;              /* X_0 = x0 * ones(d) (0 in all configs)                          */
+  double x0;              /* X_0 = x0 * ones(d) (0 in configs 1-5; 0.1 for Black-Scholes) */
   double lambda;          /* HJB λ (1.0)                                                    */
   double lr, beta1, beta2, eps;  /* Adam (R6): per-config lr, 0.9, 0.999, 1e-8              */
   uint64_t seed;          /* Philox key = (seed mod 2^32, seed >> 32) (R8)                  */

@@ -10,7 +10,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # BSDE_LIB: an alternative build of the same library (kernel experiments)
 LIB_PATH = os.environ.get("BSDE_LIB") or os.path.join(_HERE, "libbsde.so")
 
-HEAT, HJB, ALLEN_CAHN = 0, 1, 2
+HEAT, HJB, ALLEN_CAHN, BLACK_SCHOLES = 0, 1, 2, 3
 FP32, BF16 = 0, 1
 KERNEL_AUTO, KERNEL_SIMT, KERNEL_TC = 0, 1, 2
 PROLONG_COPY, PROLONG_INTERP = 0, 1

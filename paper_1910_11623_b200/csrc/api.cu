@@ -276,8 +276,9 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
   *out = nullptr;
   bsde_config cfg;
   if (cfg_in) cfg = *cfg_in; else bsde_config_default(&cfg);
-  if (problem < BSDE_HEAT || problem > BSDE_ALLEN_CAHN)
-    return fail(none, BSDE_EINVAL, "problem=%d not in {0 heat, 1 hjb, 2 allen_cahn}", problem);
+  if (problem < BSDE_HEAT || problem > BSDE_BLACK_SCHOLES)
+    return fail(none, BSDE_EINVAL, "problem=%d not in {0 heat, 1 hjb, 2 allen_cahn, 3 black_scholes}",
+                problem);
   if (d < 1 || N < 1 || !(T > 0.0))
     return fail(none, BSDE_EINVAL, "need d >= 1, N >= 1, T > 0 (got d=%d N=%d T=%g)", d, N, T);
   if (!widths || n_widths != 2 || widths[0] != widths[1] || widths[0] < 1)

@@ -17,7 +17,9 @@ constexpr uint32_t kPhiloxW0 = 0x9E3779B9u, kPhiloxW1 = 0xBB67AE85u;
 constexpr uint32_t kEvalBit = 0x80000000u;     // counter word 3 of evaluation streams
 constexpr uint32_t kInitStream = 0xC0000000u;  // counter word 3 of the init stream (R7)
 
-enum { kHeat = 0, kHJB = 1, kAllenCahn = 2 };
+enum { kHeat = 0, kHJB = 1, kAllenCahn = 2, kBlackScholes = 3 };
+// Black-Scholes constants ("d = 100, r = 0.05 and σ = 0.4")
+constexpr float kBSRate = 0.05f, kBSSigma = 0.4f;
 
 // 10 rounds; the key is warp-uniform, so ptxas folds the key schedule into
 // immediates / uniform registers and each round is 2 IMAD.WIDE + 2 LOP3.
@@ -102,23 +104,38 @@ __device__ __forceinline__ float4 dw4_fast(uint32_t q, uint32_t m, uint32_t n, u
   return z;
 }
 
-// ---- problems (R2, R10-R13) ------------------------------------------------
-// f(y, z) given |z|²; ∂f/∂y; the scalar c with ∂f/∂z = c·z; g(s = |x|²).
-__device__ __forceinline__ float driver_f(int problem, float y, float zz, float lam) {
+// ---- problems (R2, R10-R13, R21) -------------------------------------------
+// f(y, z) given |z|² and Σ z_i; ∂f/∂y; ∂f/∂z = c·z + c0·1 (the scalars c, c0);
+// g(s = |x|²); the Euler step of X (μ = 0).
+__device__ __forceinline__ float driver_f(int problem, float y, float zz, float sz, float lam) {
   if (problem == kHJB) return -0.5f * lam * zz;
   if (problem == kAllenCahn) return y - y * y * y;
+  if (problem == kBlackScholes) return -kBSRate * (y - sz * (1.0f / kBSSigma));
   return 0.0f;
 }
 __device__ __forceinline__ float driver_dfdy(int problem, float y) {
-  return problem == kAllenCahn ? 1.0f - 3.0f * y * y : 0.0f;
+  if (problem == kAllenCahn) return 1.0f - 3.0f * y * y;
+  if (problem == kBlackScholes) return -kBSRate;
+  return 0.0f;
 }
 __device__ __forceinline__ float driver_dfdz_coef(int problem, float lam) {
   return problem == kHJB ? -lam : 0.0f;
 }
+__device__ __forceinline__ float driver_dfdz_const(int problem) {
+  return problem == kBlackScholes ? kBSRate / kBSSigma : 0.0f;
+}
+// ā_n = ā_{n+1}(1 - Δt ∂_y f) varies with n: the adjoint reads a per-step ā
+__host__ __device__ __forceinline__ bool per_step_abar(int problem) {
+  return problem == kAllenCahn || problem == kBlackScholes;
+}
 __device__ __forceinline__ float terminal_g(int problem, float s) {
   if (problem == kHJB) return logf(0.5f * (1.0f + s));
   if (problem == kAllenCahn) return 1.0f / (2.0f + 0.4f * s);
-  return s;
+  return s;   // heat, Black-Scholes: |x|²
+}
+// X_{n+1} = X_n + σ ΔW_n with σ = √2 I, or σ X_n ⊙ ΔW_n (Black-Scholes)
+__device__ __forceinline__ float x_step(int problem, float x, float dw) {
+  return problem == kBlackScholes ? fmaf(kBSSigma * dw, x, x) : fmaf(1.41421356237309515f, dw, x);
 }
 
 // ---- flat parameter layout (include/bsde.h) -------------------------------

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
       stage(Ws, W + pk.w3t(), w * LDW);
       __syncthreads();
       const float* b3 = P + nd.off_b3();
-      float c4[4] = {0, 0, 0, 0}, z4[4] = {0, 0, 0, 0};
+      float c4[4] = {0, 0, 0, 0}, z4[4] = {0, 0, 0, 0}, s4[4] = {0, 0, 0, 0};
       gemm_n(H2, Ws, w, d, [&](int p0, int j, float4 v) {                          // a4 partials
         const float b = __ldg(b3 + j);
         const float4 dw = *reinterpret_cast<const float4*>(dWs + j * TP + p0);
@@ -241,12 +241,14 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
         for (int r = 0; r < 4; ++r) {
           c4[r] = fmaf(zv[r], wv[r], c4[r]);
           z4[r] = fmaf(zv[r], zv[r], z4[r]);
+          s4[r] += zv[r];
         }
       });
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         c4[r] = sum16(c4[r]);
         z4[r] = sum16(z4[r]);
+        s4[r] = sum16(s4[r]);
       }
       if (tx == 0) {
 #pragma unroll
@@ -255,10 +257,10 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
           const float y = Ys[p];
           if (!a.eval && a.problem == kAllenCahn && p < valid)
             a.Ystore[(int64_t)n * a.B_local + mloc0 + p] = y;
-          Ys[p] = y - driver_f(a.problem, y, z4[r], a.lam) * a.dt + c4[r];
+          Ys[p] = y - driver_f(a.problem, y, z4[r], s4[r], a.lam) * a.dt + c4[r];
         }
       }
-      for (int i = t; i < d * TP; i += NT) Xs[i] = fmaf(kSqrt2, dWs[i], Xs[i]);     // a2
+      for (int i = t; i < d * TP; i += NT) Xs[i] = x_step(a.problem, Xs[i], dWs[i]);   // a2
       __syncthreads();
     }
     // a5: R = Y_N - g(X_N); loss; ā recursion and dY0
@@ -271,9 +273,9 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
       if (!a.eval) {
         a.Rstore[m] = R;
         float ab = 2.0f * R * a.inv_B;
-        if (a.problem == kAllenCahn) {
+        if (per_step_abar(a.problem)) {
           for (int n = a.N - 1; n >= 0; --n) {
-            const float y = a.Ystore[(int64_t)n * a.B_local + m];
+            const float y = a.problem == kAllenCahn ? a.Ystore[(int64_t)n * a.B_local + m] : 0.0f;
             a.abar[(int64_t)n * a.B_local + m] = ab;                 // ā_{n+1}
             ab *= 1.0f - a.dt * driver_dfdy(a.problem, y);
           }
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
   const int t = threadIdx.x;
   const uint32_t it = a.state->it;
   const float zc = -a.dt * driver_dfdz_coef(a.problem, a.lam);
+  const float zc0 = -a.dt * driver_dfdz_const(a.problem);
   const int64_t i0 = blockIdx.x * items / gridDim.x, i1 = (blockIdx.x + 1) * items / gridDim.x;
   const int64_t P = nd.step_size();
   int cur_n = -1;
@@ -357,7 +360,7 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
     }
     if (t < TP) {
       const int64_t m = mloc0 + t;
-      ab[t] = t < valid ? (a.problem == kAllenCahn ? a.abar[(int64_t)n * a.B_local + m] : a.abar[m])
+      ab[t] = t < valid ? (per_step_abar(a.problem) ? a.abar[(int64_t)n * a.B_local + m] : a.abar[m])
                         : 0.0f;
     }
     gen_dw(dZ, d, a.m0 + mloc0, valid, n, it, a.k0, a.k1, a.sqrt_dt);
@@ -391,10 +394,10 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
     gemm_n(H2, Ws, w, d, [&](int p0, int j, float4 v) {           // dZ = ā(ΔW - Δt ∂_z f)
       const float b = __ldg(b3 + j);
       float4 dw = *reinterpret_cast<const float4*>(dZ + j * TP + p0);
-      dw.x = ab[p0] * fmaf(zc, v.x + b, dw.x);
-      dw.y = ab[p0 + 1] * fmaf(zc, v.y + b, dw.y);
-      dw.z = ab[p0 + 2] * fmaf(zc, v.z + b, dw.z);
-      dw.w = ab[p0 + 3] * fmaf(zc, v.w + b, dw.w);
+      dw.x = ab[p0] * fmaf(zc, v.x + b, dw.x + zc0);
+      dw.y = ab[p0 + 1] * fmaf(zc, v.y + b, dw.y + zc0);
+      dw.z = ab[p0 + 2] * fmaf(zc, v.z + b, dw.z + zc0);
+      dw.w = ab[p0 + 3] * fmaf(zc, v.w + b, dw.w + zc0);
       *reinterpret_cast<float4*>(dZ + j * TP + p0) = dw;
     });
     __syncthreads();

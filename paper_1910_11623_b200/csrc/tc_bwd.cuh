@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   const uint8_t* dst = static_cast<const uint8_t*>(a.dwpack);
   const NetDims nd{D, W};
   const float zc = -a.dt * driver_dfdz_coef(a.problem, a.lam);
-  const bool ac = a.problem == kAllenCahn;
+  const float zc0 = -a.dt * driver_dfdz_const(a.problem);   // Black-Scholes: ∂_z f = r/σ
+  const bool ac = per_step_abar(a.problem);
   constexpr uint32_t IW = idesc_bf16(128, Wp, false, false);     // G1, G2
   constexpr uint32_t ID = idesc_bf16(128, Dp, false, false);     // G3
   constexpr uint32_t IWm = idesc_bf16(128, Wp, false, true);     // G4, G6 (B = W̃ᵀ view)
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     }
     if (g8_now) f8 = true;
     g8_pending = false;
-    // dZ of this item (heat, Allen-Cahn: ∂_z f = 0), bf16 pairs: stored into hC
+    // dZ of this item (heat, Allen-Cahn: ∂_z f = 0; Black-Scholes: the constant r/σ), bf16 pairs: stored into hC
     // (G5) once G8 of the previous item has read dA1 from it, and into hT (G4)
     // once G2 has read H1 from it
     uint4 dzp[4];
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
         float dw[8];
         unpack_dw(dwc[i], dw);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) dw[e] = col_lt(g, i, e, D) ? ab_i * dw[e] : 0.0f;
+        for (int e = 0; e < 8; ++e) dw[e] = col_lt(g, i, e, D) ? ab_i * (dw[e] + zc0) : 0.0f;
         dzp[i] = make_uint4(pack2(dw[0], dw[1]), pack2(dw[2], dw[3]), pack2(dw[4], dw[5]),
                             pack2(dw[6], dw[7]));
       }
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
         unpack_dw(dwc[i], dw);
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-          z[8 * i + e] = col_lt(g, i, e, D) ? ab_i * fmaf(zc, z[8 * i + e], dw[e]) : 0.0f;
+          z[8 * i + e] = col_lt(g, i, e, D) ? ab_i * fmaf(zc, z[8 * i + e], dw[e] + zc0) : 0.0f;
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)

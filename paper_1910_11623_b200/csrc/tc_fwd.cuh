@@ -214,7 +214,7 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
 #endif
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-          if (8 * c + e < D) X[8 * i + e] = fmaf(kSqrt2, dw[e], X[8 * i + e]);   // a2
+          if (8 * c + e < D) X[8 * i + e] = x_step(a.problem, X[8 * i + e], dw[e]);   // a2
       };
       // GRP chunks together: 2·GRP Philox streams interleaved
 #ifndef BSDE_EXP_GROUP
@@ -407,8 +407,8 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
         mbar_arrive(&wfree[3]);   // G3 done: W̃3 -> step s + 1
       mbar_wait(&full[slot], (uint32_t)((s / L::NSLOT) & 1));   // ΔW_n, |X_N|² partials
       tc_after();
-      float cz = 0.0f, zz = 0.0f;
-      const bool hjb = a.problem == kHJB;
+      float cz = 0.0f, zz = 0.0f, sz = 0.0f;
+      const bool hjb = a.problem == kHJB, bs = a.problem == kBlackScholes;
       const uint32_t tdw = tm + lane_off + L::T_DW + (uint32_t)slot * L::DWC;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -433,6 +433,11 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
             for (int e = 0; e < 8; ++e)
               if (8 * c + e < D) zz = fmaf(z[i][e], z[i][e], zz);
           }
+          if (bs) {    // Σ_i Z_i enters the Black-Scholes driver
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (8 * c + e < D) sz += z[i][e];
+          }
         }
       }
       if (n + 1 == N) {
@@ -441,7 +446,7 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
       }
       if (store && a.problem == kAllenCahn && valid)
         a.Ystore[(int64_t)n * a.B_local + mloc] = Y;
-      Y = Y - driver_f(a.problem, Y, zz, a.lam) * a.dt + cz;
+      Y = Y - driver_f(a.problem, Y, zz, sz, a.lam) * a.dt + cz;
       tc_before();
       consumer_sync();
       CLK(6);
@@ -454,9 +459,9 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
       if (store) {
         a.Rstore[mloc] = R;
         float ab = 2.0f * R * a.inv_B;
-        if (a.problem == kAllenCahn) {
+        if (per_step_abar(a.problem)) {
           for (int n = N - 1; n >= 0; --n) {
-            const float y = a.Ystore[(int64_t)n * a.B_local + mloc];
+            const float y = a.problem == kAllenCahn ? a.Ystore[(int64_t)n * a.B_local + mloc] : 0.0f;
             a.abar[(int64_t)n * a.B_local + mloc] = ab;               // ā_{n+1}
             ab *= 1.0f - a.dt * driver_dfdy(a.problem, y);
           }

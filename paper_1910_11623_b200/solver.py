@@ -11,7 +11,8 @@ import numpy as np
 from . import _lib
 from ._lib import BSDEError
 
-PROBLEMS = {"heat": _lib.HEAT, "hjb": _lib.HJB, "allen_cahn": _lib.ALLEN_CAHN}
+PROBLEMS = {"heat": _lib.HEAT, "hjb": _lib.HJB, "allen_cahn": _lib.ALLEN_CAHN,
+            "black_scholes": _lib.BLACK_SCHOLES}
 PRECISIONS = {"fp32": _lib.FP32, "bf16": _lib.BF16}
 KERNELS = {"auto": _lib.KERNEL_AUTO, "simt": _lib.KERNEL_SIMT, "tc": _lib.KERNEL_TC}
 PROLONG = {"copy": _lib.PROLONG_COPY, "interp": _lib.PROLONG_INTERP}

@@ -3,7 +3,7 @@ import numpy as np
 
 from oracle import bsde as ob
 
-PROBLEM = {"heat": ob.HEAT, "hjb": ob.HJB, "allen_cahn": ob.ALLEN_CAHN}
+PROBLEM = dict(ob.PROBLEM_NAMES)
 
 # north_star: "GPU losses, Y0 and gradients must match the oracle to relative 1e-4
 # (fp32) or 2e-2 (bf16 operands with fp32 accumulate)"

@@ -65,6 +65,8 @@ CASES = [
     ("cfg3_allen_cahn", dict(batch=1000, precision="fp32")),
     ("cfg4_hjb_multilevel", dict(batch=1000)),
     ("cfg2_hjb", dict(batch=300, N=3, d=37, w=45)),       # odd sizes, ragged tiles
+    ("nx3_black_scholes", dict(batch=1000, precision="fp32")),
+    ("nx3_black_scholes", dict(batch=300, N=3, d=37, w=45, x0=1.3, precision="fp32")),
 ]
 
 
@@ -74,7 +76,7 @@ def test_teacher_forced_iteration(cfg, over, kernel):
     wl = CONFIGS[cfg].with_(**over)
     tol = TOL[wl.precision]
     s = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr, precision=wl.precision,
-             kernel=kernel, seed=wl.seed)
+             kernel=kernel, seed=wl.seed, x0=wl.x0)
     # move away from the zero-bias init so every tensor has a gradient (smaller
     # for Allen-Cahn, whose cubic driver explodes for a large Z, R7b)
     p = s.get_params()
@@ -87,7 +89,8 @@ def test_teacher_forced_iteration(cfg, over, kernel):
         loss = s.compute_grad()
         g = s.get_grads()
         ref = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, p, wl.seed, it,
-                               np.arange(wl.batch), wl.batch, kink_band=KINK_BAND[wl.precision])
+                               np.arange(wl.batch), wl.batch, x0=wl.x0,
+                               kink_band=KINK_BAND[wl.precision])
         assert np.isfinite(ref["loss"])
         assert abs(loss - ref["loss"]) <= tol * ref["loss"], (loss, ref["loss"])
         compare_grads(g, ref["grad"], wl.d, wl.w, wl.N, tol, ref["slack"])

@@ -76,6 +76,8 @@ CASES = [
     ("cfg1_heat", dict(precision="bf16")),
     ("cfg2_hjb", dict(batch=300, N=3, d=37, w=45, precision="bf16")),
     ("cfg5_allen_cahn_scaleout", dict(batch=640, N=6)),
+    ("nx3_black_scholes", dict(batch=1000)),
+    ("nx3_black_scholes", dict(batch=300, N=3, d=37, w=45, x0=1.3)),
 ]
 
 
@@ -84,7 +86,7 @@ def test_tc_teacher_forced_iteration(cfg, over):
     wl = CONFIGS[cfg].with_(**over)
     tol = TOL["bf16"]
     s = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr, precision="bf16",
-             kernel="tc", seed=wl.seed)
+             kernel="tc", seed=wl.seed, x0=wl.x0)
     assert s.family == "tc"
     p = s.get_params()
     rng = np.random.default_rng(1)
@@ -96,7 +98,7 @@ def test_tc_teacher_forced_iteration(cfg, over):
         loss = s.compute_grad()
         g = s.get_grads()
         ref = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, p, wl.seed, it,
-                               np.arange(wl.batch), wl.batch, kink_band=KINK_BAND["bf16"])
+                               np.arange(wl.batch), wl.batch, x0=wl.x0, kink_band=KINK_BAND["bf16"])
         assert np.isfinite(ref["loss"])
         assert abs(loss - ref["loss"]) <= tol * ref["loss"], (loss, ref["loss"])
         compare_grads(g, ref["grad"], wl.d, wl.w, wl.N, tol, ref["slack"])
@@ -203,3 +205,19 @@ def test_nccl_one_rank_communicator_matches_local():
     # near-zero gradient components by up to lr either way; bounded by 2·lr per step.
     diff = np.abs(ref.get_params() - com.get_params())
     assert diff.max() <= 6 * wl.lr
+
+
+def test_tc_black_scholes_converges_to_closed_form():
+    """SURVEY NEXT-3 workload trained on the tcgen05 path: Y0 reaches
+    the closed form e^{(r+σ²)T}‖x0‖² within 1.5%.  The Euler scheme's own
+    Y0 is d x0²((1+rΔt)² + σ²Δt)^N / (1+rΔt)^N = 1.2318 (-0.15%, DESIGN R21); the
+    rest is the Z-network's approximation (measured -0.6% at 600+ iterations)."""
+    from oracle.closed_forms import bs_u0
+    wl = CONFIGS["nx3_black_scholes"].with_(batch=16384)
+    s = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr, precision="bf16",
+             x0=wl.x0)
+    assert s.family == "tc"
+    losses = [s.train_step() for _ in range(600)]
+    assert np.all(np.isfinite(losses)) and np.mean(losses[-20:]) < 0.01 * losses[0]
+    u0 = bs_u0(wl.d, wl.T, wl.x0)
+    assert abs(s.y0() / u0 - 1.0) <= 1.5e-2, (s.y0(), u0)

@@ -1,4 +1,5 @@
-"""The five BASELINE.json configurations as plain data (no arithmetic of the method).
+"""The five BASELINE.json configurations (+ the SURVEY NEXT-3 Black-Scholes workload) as plain
+data (no arithmetic of the method).
 
 Shared by tests/ and bench.py; neither the oracle nor the product imports it.
 """
@@ -9,7 +10,7 @@ from typing import Optional, Tuple
 @dataclass(frozen=True)
 class Workload:
     name: str
-    problem: str          # "heat" | "hjb" | "allen_cahn"
+    problem: str          # "heat" | "hjb" | "allen_cahn" | "black_scholes"
     d: int
     w: int
     N: int
@@ -21,6 +22,7 @@ class Workload:
     seed: int = 0
     levels: Optional[Tuple[int, ...]] = None     # multilevel grids (config 4)
     iters_per_level: int = 0
+    x0: float = 0.0       # X_0 = x0 * ones(d)
 
     def with_(self, **kw):
         return replace(self, **kw)
@@ -41,4 +43,9 @@ CONFIGS = {
     # configs[4]: scale-out Allen-Cahn, 524288 paths sharded over 1/2/4/8 GPUs
     "cfg5_allen_cahn_scaleout": Workload("cfg5_allen_cahn_scaleout", "allen_cahn", 100, 110, 80,
                                          0.3, 524288, "bf16", 5e-4, 1000),
+    # Black-Scholes d = 100, r = 0.05, σ = 0.4; T, N, x0
+    # and the batch are not given by the paper: T = 1, N = 20, B = 65536 as config 3, and
+    # x0 = 0.1 so that u(0, x0) = e^{0.21}·d·0.01 ≈ 1.234 (DESIGN R21)
+    "nx3_black_scholes": Workload("nx3_black_scholes", "black_scholes", 100, 110, 20, 1.0, 65536,
+                                  "bf16", 1e-2, 2000, x0=0.1),
 }
