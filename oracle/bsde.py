@@ -159,7 +159,7 @@ def net_forward(net, x, bf16=False):
 
 def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
               x0=0.0, lam=1.0, want_grad=True, bf16=False, keep=False, kink_band=0.0,
-              mask_shift=0.0):
+              mask_shift=0.0, coupled_factor=1):
     """One training iteration on the shard ``paths`` (global path indices).
 
     Returns dict(loss_sum=Σ_m R², loss=Σ R²/B_global, grad=∂L/∂params of this
@@ -171,7 +171,9 @@ def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
     both masks are valid answers of a finite-precision evaluation (R15, R19),
     and slack bounds (to first order) how much the gradient moves when that
     mask flips.  mask_shift (tests only) evaluates the backward masks as
-    1[A > mask_shift] to emulate such flips.
+    1[A > mask_shift] to emulate such flips.  coupled_factor = f > 1 draws every
+    increment as the sum of the f increments of the grid with N·f steps that it
+    spans (coupled multilevel paths, philox.coupled_increments).
     """
     paths = np.asarray(paths, dtype=np.int64)
     B = float(batch_global)
@@ -182,7 +184,8 @@ def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
     Y = np.full(M, y0[0])
     trace = []
     for n in range(N):
-        dW = philox.brownian_increments(seed, it, n, paths, d, dt)
+        dW = (philox.brownian_increments(seed, it, n, paths, d, dt) if coupled_factor == 1
+              else philox.coupled_increments(seed, it, n, paths, d, dt, coupled_factor))
         A1, H1, A2, H2, Z = net_forward(nets[n], X, bf16)                # P:78, Eq. 7
         trace.append((X, dW, A1, H1, A2, H2, Z, Y))
         Y = Y - driver_f(problem, Y, Z, lam) * dt + np.sum(Z * dW, axis=-1)   # P:66 (φ=-f)

@@ -88,6 +88,21 @@ def brownian_increments(seed, it, n, m, d, dt):
     return np.sqrt(dt) * standard_normals(seed, it, n, m, d)
 
 
+def coupled_increments(seed, it, n, m, d, dt, factor):
+    """Coupled multilevel paths ("coarsen_increments",
+    PAPER.md §3.2 fig:multilevel: the levels simulate the same underlying path): the
+    increment of coarse step n (Δt = T/N) is the sum of the `factor` increments of the
+    finest grid (Δt/factor) that it spans, fine steps n·factor .. n·factor + factor - 1,
+    each drawn with its own fine step index in the counter (R8).  factor = 1 is
+    brownian_increments."""
+    if factor < 1:
+        raise ValueError("factor must be >= 1")
+    acc = np.zeros((len(np.atleast_1d(m)), d))
+    for j in range(factor):
+        acc = acc + brownian_increments(seed, it, n * factor + j, m, d, dt / factor)
+    return acc
+
+
 def init_uniforms(seed, tensor_id, count):
     """Uniforms of the initialisation stream (R7): ctr = (idx//4, tensor_id, 0, INIT_STREAM)."""
     idx = np.arange(count, dtype=np.uint64)

@@ -358,3 +358,60 @@ def test_kink_slack_bounds_mask_flips():
         diff = np.abs(shifted["grad"] - base["grad"])
         assert diff.max() > 0                           # the flips did change the gradient
         assert np.all(diff <= base["slack"] * 1.05 + 1e-12)
+
+
+# ------------------------------------------------- coupled multilevel paths (NEXT-3)
+def test_coupled_increments_share_the_brownian_path():
+    """Pin C1 (SPEC S:314-322 coarsen_increments): the coupled increments of every
+    level sum to the same W_T as the finest grid's own increments (the levels
+    simulate one underlying path), factor 1 is the plain generator, and a coarse
+    increment has variance Δt_coarse with no correlation between steps."""
+    d, T, Nf, seed, it = 4, 1.0, 80, 7, 3
+    m = np.arange(2000)
+    WT = sum(philox.brownian_increments(seed, it, k, m, d, T / Nf) for k in range(Nf))
+    for N in (5, 10, 20, 40, 80):
+        f = Nf // N
+        inc = [philox.coupled_increments(seed, it, n, m, d, T / N, f) for n in range(N)]
+        assert np.max(np.abs(sum(inc) - WT)) < 1e-12
+    np.testing.assert_array_equal(philox.coupled_increments(seed, it, 3, m, d, 0.05, 1),
+                                  philox.brownian_increments(seed, it, 3, m, d, 0.05))
+    big = np.arange(50000)
+    a = philox.coupled_increments(seed, it, 0, big, 2, 0.2, 16).ravel()
+    b = philox.coupled_increments(seed, it, 1, big, 2, 0.2, 16).ravel()
+    assert abs(a.var() / 0.2 - 1.0) < 0.02
+    assert abs(np.mean(a * b)) / 0.2 < 0.02
+    with pytest.raises(ValueError):
+        philox.coupled_increments(seed, it, 0, m, d, 0.1, 0)
+
+
+def test_coupled_levels_share_terminal_state():
+    """Pin C2: heat with Z ≡ 0 (zero head, zero biases) has Y_N = Y0 and X_N = √2 W_T,
+    so with coupled paths every level's residuals equal the finest grid's exactly."""
+    d, w, T, B, Nf = 6, 8, 1.0, 64, 16
+    ref = None
+    for N in (2, 4, 8, 16):
+        p = bsde.init_params(1, d, w, N, zero_head=True)
+        r = bsde.iteration(bsde.HEAT, d, w, N, T, p, 5, 2, np.arange(B), B, want_grad=False,
+                           coupled_factor=Nf // N)
+        ref = r["R"] if ref is None else ref
+        assert np.max(np.abs(r["R"] - ref)) < 1e-12
+
+
+def test_coupled_gbm_strong_order_half():
+    """Pin C3 (SPEC invariant "strong convergence order ½", fig:multilevel): the
+    Black-Scholes Euler step on coupled levels against the exact geometric Brownian
+    motion x0·exp(-σ²T/2 + σW_T) of the shared path: the RMS terminal error shrinks by
+    ≈ √2 per halving of Δt (successive ratios in [1.2, 1.7])."""
+    d, T, x0, B, Nf = 1, 1.0, 1.0, 4096, 64
+    m = np.arange(B)
+    WT = sum(philox.brownian_increments(0, 0, k, m, d, T / Nf) for k in range(Nf))
+    exact = x0 * np.exp(-0.5 * bsde.BS_SIGMA ** 2 * T + bsde.BS_SIGMA * WT)
+    errs = []
+    for N in (8, 16, 32, 64):
+        X = np.full((B, d), x0)
+        for n in range(N):
+            X = bsde.forward_step(bsde.BLACK_SCHOLES, X,
+                                  philox.coupled_increments(0, 0, n, m, d, T / N, Nf // N))
+        errs.append(np.sqrt(np.mean((X - exact) ** 2)))
+    ratios = [errs[i] / errs[i + 1] for i in range(3)]
+    assert all(1.2 <= r <= 1.7 for r in ratios), ratios
