@@ -98,11 +98,17 @@ typedef struct {
   int use_graph;          /* 1: capture the step in a CUDA graph and replay it              */
   int init_zero_head;     /* 1: W3 = 0 at init, so Z ≡ 0 (R7b; default for Allen-Cahn,
                              whose cubic driver diverges from a Xavier-initialised Z)      */
+  int coupled_paths;      /* 1: coupled multilevel paths:
+                             every level simulates the Brownian path of the finest grid
+                             N_fine = N·2^max_levels; the increment of step n at the current
+                             N is the sum of the f = N_fine/N fine increments it spans, each
+                             drawn with Philox counter step n·f + j and √(T/N_fine) (R8).
+                             0: each grid draws its own increments (default)               */
 } bsde_config;
 
 /* Fill *cfg with defaults: B = 256, x0 = 0, λ = 1, Adam (1e-2, 0.9, 0.999, 1e-8),
  * seed 0, FP32, KERNEL_AUTO, COPY, max_levels 0, device 0, default stream,
- * rank 0 of 1, no NCCL, graphs on, Xavier head (init_zero_head 0). */
+ * rank 0 of 1, no NCCL, graphs on, Xavier head (init_zero_head 0), uncoupled paths. */
 void bsde_config_default(bsde_config* cfg);
 
 /* Create a context for `problem` in dimension d with N time steps on [0, T]

@@ -52,6 +52,7 @@ class Config(ctypes.Structure):
         ("nccl_id", ctypes.c_void_p),
         ("use_graph", ctypes.c_int),
         ("init_zero_head", ctypes.c_int),
+        ("coupled_paths", ctypes.c_int),
     ]
 
 

@@ -84,7 +84,7 @@ struct bsde_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   float *params = nullptr, *grad = nullptr, *adam_m = nullptr, *adam_v = nullptr;
-  float *scratch = nullptr, *Xstore = nullptr, *Ystore = nullptr, *abar = nullptr;
+  float *scratch = nullptr, *Xstore = nullptr, *Pstore = nullptr, *abar = nullptr;
   float* Rstore = nullptr;
   void* wpack = nullptr;
   void* xpack = nullptr;        // tcgen05 path: fp16 ΔW_n images
@@ -136,6 +136,8 @@ PassArgs pass_args(bsde_ctx* c) {
   a.N = c->N;
   a.dt = (float)(c->T / c->N);
   a.sqrt_dt = (float)std::sqrt(c->T / c->N);
+  a.cpl = c->cfg.coupled_paths ? c->N_max / c->N : 1;
+  a.sqrt_dt_f = (float)std::sqrt(c->T / ((double)c->N * a.cpl));
   a.lam = (float)c->cfg.lambda;
   a.x0 = (float)c->cfg.x0;
   a.inv_B = (float)(1.0 / (double)c->cfg.batch_global);
@@ -146,7 +148,7 @@ PassArgs pass_args(bsde_ctx* c) {
   a.params = c->params;
   a.grad = c->grad;
   a.Xstore = c->Xstore;
-  a.Ystore = c->Ystore;
+  a.Pstore = c->Pstore;
   a.abar = c->abar;
   a.Rstore = c->Rstore;
   a.state = c->state;
@@ -223,7 +225,7 @@ int repack(bsde_ctx* ctx) {
 
 void free_all(bsde_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
-  void* bufs[] = {c->params, c->grad, c->adam_m, c->adam_v, c->scratch, c->Xstore, c->Ystore,
+  void* bufs[] = {c->params, c->grad, c->adam_m, c->adam_v, c->scratch, c->Xstore, c->Pstore,
                   c->abar, c->Rstore, c->wpack, c->xpack, c->gpart, c->state,
                   c->eval_loss};
   for (void* p : bufs)
@@ -368,13 +370,13 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
       {(void**)&ctx->adam_v, npmax * sizeof(float)},
       {(void**)&ctx->scratch, npmax * sizeof(float)},
       {(void**)&ctx->Xstore, xs},
-      {(void**)&ctx->abar, (size_t)ctx->N_max * ctx->B_local * sizeof(float)},
+      {(void**)&ctx->abar, (size_t)ctx->B_local * sizeof(float)},
       {(void**)&ctx->Rstore, (size_t)ctx->B_local * sizeof(float)},
       {(void**)&ctx->state, sizeof(DeviceState)},
       {(void**)&ctx->eval_loss, sizeof(double) * 2},
   };
-  if (problem == BSDE_ALLEN_CAHN)
-    allocs.push_back({(void**)&ctx->Ystore, (size_t)ctx->N_max * ctx->B_local * sizeof(float)});
+  if (per_step_abar(problem))
+    allocs.push_back({(void**)&ctx->Pstore, (size_t)ctx->N_max * ctx->B_local * sizeof(float)});
   if (family == BSDE_KERNEL_TC) {
     allocs.push_back({&ctx->wpack, tc_pack_bytes(d, w, ctx->N_max, cfg.precision)});
     allocs.push_back({&ctx->xpack, tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)});

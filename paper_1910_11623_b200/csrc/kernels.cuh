@@ -19,8 +19,11 @@ struct PassArgs {
   const float* params;                 // fp32 master (flat layout)
   float* grad;                         // flat gradient (+ nothing else); zeroed per step
   float* Xstore;                       // [N][B_local][d] fp32: X_n for the adjoint pass
-  float* Ystore;                       // [N][B_local]: Y_n (Allen-Cahn only)
-  float* abar;                         // [N][B_local] ā_{n+1} (AC) or [B_local] ā_N
+  // ā recursion ā_n = ā_{n+1} f_n, f_n = 1 - Δt ∂_y f(Y_n), in product form: the
+  // forward stores the prefix products P_{n+1} = f_0 ⋯ f_n and ā_N P_N, so that
+  // ā_{n+1} = ā_N P_N / P_{n+1} needs no backward scan (per_step_abar problems)
+  float* Pstore;                       // [N][B_local]: P_{n+1} (per_step_abar problems only)
+  float* abar;                         // [B_local]: ā_N P_N (per_step_abar) or ā_N
   float* Rstore;                       // [B_local] terminal residual R (debug / parity)
   DeviceState* state;
   double* loss_acc;                    // Σ_m R² accumulator (state->loss_sum or eval slot)
@@ -31,6 +34,8 @@ struct PassArgs {
   void* dwpack;                        // tcgen05 path: fp16 ΔW_n images (written by k_fwd_tc)
   unsigned long long* clk;             // debug: per-phase clock64() trace of CTA 0 (or null)
   int precision;
+  int cpl;                             // coupled paths: fine steps per step (1 = uncoupled)
+  float sqrt_dt_f;                     // √(Δt/cpl)
 };
 
 // SIMT fp32 kernels (simt.cu)

@@ -158,17 +158,24 @@ __device__ void gemm_t(const float* L, int ni, const float* R, int nj, float* __
 }
 
 // ΔW_n of the tile into dWs[k][p] (feature-major), zero for paths >= valid.
+// ΔW_n of a 64-path tile; coupled paths (cpl > 1): the sum of the cpl increments
+// of fine steps n·cpl + j, each √(Δt/cpl)·z (NEXT-3)
 __device__ void gen_dw(float* dWs, int d, int64_t mg0, int64_t valid, int n, uint32_t it,
-                       uint32_t k0, uint32_t k1, float sqrt_dt) {
+                       uint32_t k0, uint32_t k1, float sqrt_dt_f, int cpl) {
   const int nq = (d + 3) >> 2;
   for (int idx = threadIdx.x; idx < TP * nq; idx += NT) {
     const int q = idx / TP, p = idx - q * TP;   // consecutive threads: consecutive paths
-    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (p < valid) z = normals4((uint32_t)q, (uint32_t)(mg0 + p), (uint32_t)n, it, k0, k1);
-    const float zz[4] = {z.x, z.y, z.z, z.w};
+    float zz[4] = {0.f, 0.f, 0.f, 0.f};
+    if (p < valid) {
+      for (int j = 0; j < cpl; ++j) {
+        const float4 z = normals4((uint32_t)q, (uint32_t)(mg0 + p), (uint32_t)(n * cpl + j), it, k0, k1);
+        zz[0] += sqrt_dt_f * z.x; zz[1] += sqrt_dt_f * z.y;
+        zz[2] += sqrt_dt_f * z.z; zz[3] += sqrt_dt_f * z.w;
+      }
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (4 * q + i < d) dWs[(4 * q + i) * TP + p] = sqrt_dt * zz[i];
+      if (4 * q + i < d) dWs[(4 * q + i) * TP + p] = zz[i];
   }
 }
 
@@ -189,6 +196,7 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
   float* H2 = H1 + w * TP;                // [w][64]
   float* Ws = H2 + w * TP;                // [K <= max(d, w)][128]
   float* Ys = Ws + (d > w ? d : w) * LDW; // [64]
+  float* Ps = Ys + TP;                    // [64] prefix products P_{n+1} of the ā factors
   const float* wp = static_cast<const float*>(a.wpack);
   const int t = threadIdx.x, lane = t & 31, ty = t >> 4, tx = t & 15;
   const uint32_t it = a.eval ? a.eval_it : a.state->it;
@@ -198,7 +206,7 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
     const int64_t mloc0 = (int64_t)tile * TP;
     const int64_t valid = min((int64_t)TP, a.B_local - mloc0);
     for (int i = t; i < d * TP; i += NT) Xs[i] = a.x0;
-    if (t < TP) Ys[t] = a.params[0];
+    if (t < TP) { Ys[t] = a.params[0]; Ps[t] = 1.0f; }
     __syncthreads();
     for (int n = 0; n < a.N; ++n) {
       const float* P = a.params + nd.step_base(n);
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
         float4* xs = reinterpret_cast<float4*>(a.Xstore + ((size_t)n * ntiles + tile) * d * TP);
         for (int i = t; i < d * TP / 4; i += NT) xs[i] = reinterpret_cast<const float4*>(Xs)[i];
       }
-      gen_dw(dWs, d, a.m0 + mloc0, valid, n, it, a.k0, a.k1, a.sqrt_dt);           // a1
+      gen_dw(dWs, d, a.m0 + mloc0, valid, n, it, a.k0, a.k1, a.sqrt_dt_f, a.cpl);  // a1
       stage(Ws, W + pk.w1t(), d * LDW);
       __syncthreads();
       const float* b1 = P + nd.off_b1();
@@ -255,15 +263,17 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
         for (int r = 0; r < 4; ++r) {
           const int p = 4 * ty + r;
           const float y = Ys[p];
-          if (!a.eval && a.problem == kAllenCahn && p < valid)
-            a.Ystore[(int64_t)n * a.B_local + mloc0 + p] = y;
+          if (!a.eval && per_step_abar(a.problem)) {
+            Ps[p] *= 1.0f - a.dt * driver_dfdy(a.problem, y);
+            if (p < valid) a.Pstore[(int64_t)n * a.B_local + mloc0 + p] = Ps[p];
+          }
           Ys[p] = y - driver_f(a.problem, y, z4[r], s4[r], a.lam) * a.dt + c4[r];
         }
       }
       for (int i = t; i < d * TP; i += NT) Xs[i] = x_step(a.problem, Xs[i], dWs[i]);   // a2
       __syncthreads();
     }
-    // a5: R = Y_N - g(X_N); loss; ā recursion and dY0
+    // a5: R = Y_N - g(X_N); loss; ā_N (times P_N) and dY0 = ā_0 = ā_N P_N
     if (t < TP && t < valid) {
       float s = 0.0f;
       for (int k = 0; k < d; ++k) s = fmaf(Xs[k * TP + t], Xs[k * TP + t], s);
@@ -273,15 +283,8 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
       if (!a.eval) {
         a.Rstore[m] = R;
         float ab = 2.0f * R * a.inv_B;
-        if (per_step_abar(a.problem)) {
-          for (int n = a.N - 1; n >= 0; --n) {
-            const float y = a.problem == kAllenCahn ? a.Ystore[(int64_t)n * a.B_local + m] : 0.0f;
-            a.abar[(int64_t)n * a.B_local + m] = ab;                 // ā_{n+1}
-            ab *= 1.0f - a.dt * driver_dfdy(a.problem, y);
-          }
-        } else {
-          a.abar[m] = ab;                                              // ā_N
-        }
+        if (per_step_abar(a.problem)) ab *= Ps[t];
+        a.abar[m] = ab;
         dy0 += ab;
       }
     }
@@ -360,10 +363,10 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
     }
     if (t < TP) {
       const int64_t m = mloc0 + t;
-      ab[t] = t < valid ? (per_step_abar(a.problem) ? a.abar[(int64_t)n * a.B_local + m] : a.abar[m])
+      ab[t] = t < valid ? (per_step_abar(a.problem) ? a.abar[m] / a.Pstore[(int64_t)n * a.B_local + m] : a.abar[m])
                         : 0.0f;
     }
-    gen_dw(dZ, d, a.m0 + mloc0, valid, n, it, a.k0, a.k1, a.sqrt_dt);
+    gen_dw(dZ, d, a.m0 + mloc0, valid, n, it, a.k0, a.k1, a.sqrt_dt_f, a.cpl);
     stage(Ws, W + pk.w1t(), d * LDW);
     __syncthreads();
     const float* b1 = Pn + nd.off_b1();
@@ -432,7 +435,7 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
 }
 
 size_t fwd_smem(int d, int w) {
-  return sizeof(float) * ((size_t)TP * (2 * d + 2 * w) + (size_t)(d > w ? d : w) * LDW + TP + 16);
+  return sizeof(float) * ((size_t)TP * (2 * d + 2 * w) + (size_t)(d > w ? d : w) * LDW + 2 * TP + 16);
 }
 size_t bwd_smem(int d, int w) {
   return sizeof(float) * ((size_t)TP * (2 * d + 4 * w) + (size_t)(d > w ? d : w) * LDW + TP) +

@@ -100,10 +100,11 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   };
 
   // per-path inputs of an item: ā_{n+1} and this thread's ΔW_n chunks (fp16)
-  auto load_inputs = [&](int n, int tile, float& ab, uint4 (&dwp)[4]) {
+  auto load_inputs = [&](int n, int tile, float& ab, float& pn, uint4 (&dwp)[4]) {
     const int64_t mloc = (int64_t)tile * 128 + row;
-    ab = mloc < a.B_local ? (ac ? __ldcs(a.abar + (int64_t)n * a.B_local + mloc) : __ldg(a.abar + mloc))
-                          : 0.0f;
+    // ā_{n+1} = ā_N P_N / P_{n+1}: both loaded here, divided where ā is used
+    ab = mloc < a.B_local ? __ldg(a.abar + mloc) : 0.0f;
+    pn = (ac && mloc < a.B_local) ? __ldcs(a.Pstore + (int64_t)n * a.B_local + mloc) : 1.0f;
     const uint8_t* src = dst + img_of(n, tile) + (row >> 3) * (Dp * 16) + (row & 7) * 16;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -123,9 +124,9 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
   cp_async_wait_all();
   fence_async_smem();
   __syncthreads();
-  float ab = 0.0f;
+  float ab = 0.0f, pn = 1.0f;
   uint4 dwp[4];
-  if (i0 < i1) load_inputs(n_first, t_first, ab, dwp);
+  if (i0 < i1) load_inputs(n_first, t_first, ab, pn, dwp);
 
   uint32_t mph = 0, wph = 0, g8ph = 0, g5ph = 0;
   unsigned long long* const clk = (a.clk && blockIdx.x == 0 && t == 32) ? a.clk : nullptr;
@@ -214,7 +215,8 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     // (G5) once G8 of the previous item has read dA1 from it, and into hT (G4)
     // once G2 has read H1 from it
     uint4 dzp[4];
-    const float ab_i = ab;
+    const float ab_i = ac ? __fdividef(ab, pn) : ab;
+    const float abz0 = ab_i * zc0;   // ā(ΔW - Δt ∂_z f) with the constant part of ∂_z f
     uint4 dwc[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) dwc[i] = dwp[i];
@@ -224,12 +226,12 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
         float dw[8];
         unpack_dw(dwc[i], dw);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) dw[e] = col_lt(g, i, e, D) ? ab_i * (dw[e] + zc0) : 0.0f;
+        for (int e = 0; e < 8; ++e) dw[e] = col_lt(g, i, e, D) ? fmaf(ab_i, dw[e], abz0) : 0.0f;
         dzp[i] = make_uint4(pack2(dw[0], dw[1]), pack2(dw[2], dw[3]), pack2(dw[4], dw[5]),
                             pack2(dw[6], dw[7]));
       }
     }
-    if (item + 1 < i1) load_inputs(n_nx, t_nx, ab, dwp);   // consumed by the next item
+    if (item + 1 < i1) load_inputs(n_nx, t_nx, ab, pn, dwp);   // consumed by the next item
     mbar_wait(&bars[3], mph);
     mph ^= 1;
     CLK(1);
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
         unpack_dw(dwc[i], dw);
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-          z[8 * i + e] = col_lt(g, i, e, D) ? ab_i * fmaf(zc, z[8 * i + e], dw[e] + zc0) : 0.0f;
+          z[8 * i + e] = col_lt(g, i, e, D) ? fmaf(ab_i, fmaf(zc, z[8 * i + e], dw[e]), abz0) : 0.0f;
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)

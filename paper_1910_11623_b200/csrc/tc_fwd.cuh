@@ -46,48 +46,57 @@ __device__ __forceinline__ void unpack_dw(const uint4& u, float* v) {
 constexpr int kFwdProducers = 384, kFwdConsumers = 128;
 __device__ __forceinline__ void consumer_sync() { named_sync(1, kFwdConsumers); }
 
-// Normals of Philox blocks q = 2c, 2c+1 (columns 8c..8c+7) for the chunks
-// c = c0, c0 + CS, ..., NCH of them, interleaved for ILP; the normals of blocks
-// whose columns are all >= D are 0.
-template <int D, int CS, int NCH>
+// Increments of Philox blocks q = 2c, 2c+1 (columns 8c..8c+7) for the chunks
+// c = c0, c0 + CS, ..., NCH of them, interleaved for ILP; those of blocks whose
+// columns are all >= D are 0.  Coupled paths (cpl > 1, NEXT-3): the sum over the
+// cpl fine steps n·cpl + j of √(Δt/cpl)·z (sdt = √(Δt/cpl)).  The uncoupled
+// instance (CPL false) keeps the loop out of the hot code.
+template <int D, int CS, int NCH, bool CPL>
 __device__ __forceinline__ void gen_chunks(int c0, uint32_t m, uint32_t n, uint32_t it, uint32_t k0,
-                                           uint32_t k1, float sdt, float (&dw)[NCH * 8]) {
+                                           uint32_t k1, float sdt, float (&dw)[NCH * 8], int cpl) {
   constexpr int K = 2 * NCH;
-  uint4 c[K];
-  bool ok[K];   // warp-uniform: block has columns < D
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const int q = 2 * (c0 + CS * (j / 2)) + j % 2;
-    c[j] = make_uint4((uint32_t)q, m, n, it);
-    ok[j] = 4 * q < D;
-  }
-  uint32_t a0 = k0, a1 = k1;
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    if (r) { a0 += kPhiloxW0; a1 += kPhiloxW1; }
+  auto one = [&](uint32_t nf, bool add) {   // the normals of (fine) step nf
+    uint4 c[K];
+    bool ok[K];   // warp-uniform: block has columns < D
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      const uint32_t lo0 = kPhiloxM0 * c[j].x, hi0 = __umulhi(kPhiloxM0, c[j].x);
-      const uint32_t lo1 = kPhiloxM1 * c[j].z, hi1 = __umulhi(kPhiloxM1, c[j].z);
-      c[j] = make_uint4(hi1 ^ c[j].y ^ a0, lo1, hi0 ^ c[j].w ^ a1, lo0);
+      const int q = 2 * (c0 + CS * (j / 2)) + j % 2;
+      c[j] = make_uint4((uint32_t)q, m, nf, it);
+      ok[j] = 4 * q < D;
     }
-  }
+    uint32_t a0 = k0, a1 = k1;
 #pragma unroll
-  for (int j = 0; j < K; ++j) {
-    float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-    if (ok[j]) {
-#ifdef BSDE_DBG_NOBM
-      z0 = __uint_as_float((c[j].x >> 9) | 0x3c000000u); z1 = __uint_as_float((c[j].y >> 9) | 0x3c000000u);
-      z2 = __uint_as_float((c[j].z >> 9) | 0x3c000000u); z3 = __uint_as_float((c[j].w >> 9) | 0x3c000000u);
-#else
-      box_muller_fast(c[j].x, c[j].y, sdt, z0, z1);
-      box_muller_fast(c[j].z, c[j].w, sdt, z2, z3);
-#endif
+    for (int r = 0; r < 10; ++r) {
+      if (r) { a0 += kPhiloxW0; a1 += kPhiloxW1; }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const uint32_t lo0 = kPhiloxM0 * c[j].x, hi0 = __umulhi(kPhiloxM0, c[j].x);
+        const uint32_t lo1 = kPhiloxM1 * c[j].z, hi1 = __umulhi(kPhiloxM1, c[j].z);
+        c[j] = make_uint4(hi1 ^ c[j].y ^ a0, lo1, hi0 ^ c[j].w ^ a1, lo0);
+      }
     }
-    dw[4 * j + 0] = z0;
-    dw[4 * j + 1] = z1;
-    dw[4 * j + 2] = z2;
-    dw[4 * j + 3] = z3;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      float z[4] = {0.f, 0.f, 0.f, 0.f};
+      if (ok[j]) {
+#ifdef BSDE_DBG_NOBM
+        z[0] = __uint_as_float((c[j].x >> 9) | 0x3c000000u); z[1] = __uint_as_float((c[j].y >> 9) | 0x3c000000u);
+        z[2] = __uint_as_float((c[j].z >> 9) | 0x3c000000u); z[3] = __uint_as_float((c[j].w >> 9) | 0x3c000000u);
+#else
+        box_muller_fast(c[j].x, c[j].y, sdt, z[0], z[1]);
+        box_muller_fast(c[j].z, c[j].w, sdt, z[2], z[3]);
+#endif
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dw[4 * j + e] = add ? dw[4 * j + e] + z[e] : z[e];
+    }
+  };
+  if constexpr (!CPL) {
+    one(n, false);
+  } else {
+    one(n * (uint32_t)cpl, false);
+#pragma unroll 1
+    for (int jf = 1; jf < cpl; ++jf) one(n * (uint32_t)cpl + (uint32_t)jf, true);
   }
 }
 
@@ -115,7 +124,7 @@ struct FwdSmem {
 // Producer thread k of a path (k = 0, 1, 2) owns the 8-column chunks c = k + 3i.
 // One code path for the three threads (instruction-cache footprint); k is
 // warp-uniform.
-template <int D, int W>
+template <int D, int W, bool MULT, bool CPL>
 __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint8_t* sm, uint32_t tm,
                                              int K3, int q, int lane) {
   using Dm = Dims<D, W>;
@@ -214,7 +223,9 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
 #endif
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-          if (8 * c + e < D) X[8 * i + e] = x_step(a.problem, X[8 * i + e], dw[e]);   // a2
+          if (8 * c + e < D)   // a2: X + √2 ΔW, or X + σ X ΔW (Black-Scholes, MULT)
+            X[8 * i + e] = MULT ? fmaf(kBSSigma * dw[e], X[8 * i + e], X[8 * i + e])
+                                : fmaf(kSqrt2, dw[e], X[8 * i + e]);
       };
       // GRP chunks together: 2·GRP Philox streams interleaved
 #ifndef BSDE_EXP_GROUP
@@ -226,7 +237,7 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
         if constexpr (i < NI) {
           constexpr int nch = (i + GRP <= NI) ? GRP : NI - i;
           float dw[nch * 8];
-          gen_chunks<D, 3, nch>(K3 + 3 * i, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt, dw);
+          gen_chunks<D, 3, nch, CPL>(K3 + 3 * i, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt_f, dw, a.cpl);
           chunk_out(Int<i>{}, dw);
           if constexpr (nch >= 2) chunk_out(Int<i + 1>{}, dw + 8);
           if constexpr (nch >= 3) chunk_out(Int<i + 2>{}, dw + 16);
@@ -324,6 +335,7 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
     const int64_t mloc = (int64_t)tile * 128 + row;
     const bool valid = mloc < a.B_local;
     float Y = a.params[0];
+    float P = 1.0f;   // prefix product P_{n+1} of the ā factors (per_step_abar problems)
     float xn2 = 0.0f;
     for (int n = 0; n < N; ++n, ++s) {
       const int p = (int)(s & 1), slot = (int)(s % L::NSLOT);
@@ -408,66 +420,65 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
       mbar_wait(&full[slot], (uint32_t)((s / L::NSLOT) & 1));   // ΔW_n, |X_N|² partials
       tc_after();
       float cz = 0.0f, zz = 0.0f, sz = 0.0f;
-      const bool hjb = a.problem == kHJB, bs = a.problem == kBlackScholes;
       const uint32_t tdw = tm + lane_off + L::T_DW + (uint32_t)slot * L::DWC;
+      // the driver's extra reduction (|Z|² for HJB, Σ Z for Black-Scholes) is a
+      // compile-time choice: one instance runs, the chain carries no predicated work
+      auto e3 = [&](auto mode_c) {
+        constexpr int MODE = decltype(mode_c)::value;   // 0 none, 1 |Z|², 2 Σ Z
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float z[HV][8];
-        uint32_t dwr[HV][4];
+        for (int h = 0; h < 2; ++h) {
+          float z[HV][8];
+          uint32_t dwr[HV][4];
 #pragma unroll
-        for (int i = 0; i < HV; ++i)
-          if (h * HV + i < NCV) tmem_ld4_nowait(tdw + 4u * (h * HV + i), dwr[i]);
-        tmem_ld_chunks<HV>(acc(p) + 8u * (uint32_t)(h * HV), z, NCV - h * HV);
+          for (int i = 0; i < HV; ++i)
+            if (h * HV + i < NCV) tmem_ld4_nowait(tdw + 4u * (h * HV + i), dwr[i]);
+          tmem_ld_chunks<HV>(acc(p) + 8u * (uint32_t)(h * HV), z, NCV - h * HV);
 #pragma unroll
-        for (int i = 0; i < HV; ++i) {
-          const int c = h * HV + i;
-          if (c >= NCV) continue;
-          reg_fence4(dwr[i]);
-          float dw[8];
-          unpack_dw(make_uint4(dwr[i][0], dwr[i][1], dwr[i][2], dwr[i][3]), dw);
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (8 * c + e < D) cz = fmaf(z[i][e], dw[e], cz);
-          if (hjb) {   // |Z|² enters the driver only there
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (8 * c + e < D) zz = fmaf(z[i][e], z[i][e], zz);
-          }
-          if (bs) {    // Σ_i Z_i enters the Black-Scholes driver
+          for (int i = 0; i < HV; ++i) {
+            const int c = h * HV + i;
+            if (c >= NCV) continue;
+            reg_fence4(dwr[i]);
+            float dw[8];
+            unpack_dw(make_uint4(dwr[i][0], dwr[i][1], dwr[i][2], dwr[i][3]), dw);
 #pragma unroll
             for (int e = 0; e < 8; ++e)
-              if (8 * c + e < D) sz += z[i][e];
+              if (8 * c + e < D) {
+                cz = fmaf(z[i][e], dw[e], cz);
+                if (MODE == 1) zz = fmaf(z[i][e], z[i][e], zz);
+                if (MODE == 2) sz += z[i][e];
+              }
           }
         }
-      }
+      };
+      if (a.problem == kHJB)
+        e3(Int<1>{});
+      else if (a.problem == kBlackScholes)
+        e3(Int<2>{});
+      else
+        e3(Int<0>{});
       if (n + 1 == N) {
         const float* x2 = reinterpret_cast<const float*>(slotp + Dm::XB);
         xn2 = (x2[row] + x2[128 + row]) + x2[256 + row];
       }
-      if (store && a.problem == kAllenCahn && valid)
-        a.Ystore[(int64_t)n * a.B_local + mloc] = Y;
+      if (store && per_step_abar(a.problem)) {
+        P *= 1.0f - a.dt * driver_dfdy(a.problem, Y);
+        if (valid) a.Pstore[(int64_t)n * a.B_local + mloc] = P;
+      }
       Y = Y - driver_f(a.problem, Y, zz, sz, a.lam) * a.dt + cz;
       tc_before();
       consumer_sync();
       CLK(6);
       if (mma) mbar_arrive(&empty[slot]);   // the slot is free
     }
-    // a5: R = Y_N - g(X_N); loss; ā recursion and dY0
+    // a5: R = Y_N - g(X_N); loss; ā_N (times P_N) and dY0 = ā_0 = ā_N P_N
     if (valid) {
       const float R = Y - terminal_g(a.problem, xn2);
       lsum += (double)R * R;
       if (store) {
         a.Rstore[mloc] = R;
         float ab = 2.0f * R * a.inv_B;
-        if (per_step_abar(a.problem)) {
-          for (int n = N - 1; n >= 0; --n) {
-            const float y = a.problem == kAllenCahn ? a.Ystore[(int64_t)n * a.B_local + mloc] : 0.0f;
-            a.abar[(int64_t)n * a.B_local + mloc] = ab;               // ā_{n+1}
-            ab *= 1.0f - a.dt * driver_dfdy(a.problem, y);
-          }
-        } else {
-          a.abar[mloc] = ab;                                          // ā_N
-        }
+        if (per_step_abar(a.problem)) ab *= P;
+        a.abar[mloc] = ab;
         dy0 += ab;
       }
     }
@@ -498,7 +509,17 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
   float dy0 = 0.0f;
   // consumers on the high warp ids: the schedulers favour them (the chain is
   // latency-bound, the producers throughput-bound)
-  if (warp < 12) fwd_producer<D, W>(a, ntiles, sm, tm, warp >> 2, warp & 3, lane);
+  if (warp < 12) {   // one instance runs: X step and path coupling are compile-time choices
+    const int q = warp & 3, k3 = warp >> 2;
+    const bool mult = a.problem == kBlackScholes;
+    if (a.cpl > 1) {
+      if (mult) fwd_producer<D, W, true, true>(a, ntiles, sm, tm, k3, q, lane);
+      else fwd_producer<D, W, false, true>(a, ntiles, sm, tm, k3, q, lane);
+    } else {
+      if (mult) fwd_producer<D, W, true, false>(a, ntiles, sm, tm, k3, q, lane);
+      else fwd_producer<D, W, false, false>(a, ntiles, sm, tm, k3, q, lane);
+    }
+  }
   else fwd_consumer<D, W>(a, ntiles, sm, tm, warp & 3, lane, lsum, dy0);
   double lw = lsum;
   float gw = dy0;

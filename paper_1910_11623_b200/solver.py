@@ -51,10 +51,11 @@ class BSDE:
     def __init__(self, problem, d, N, T, width, batch, *, lr=1e-2, seed=0, precision="fp32",
                  kernel="auto", x0=0.0, lam=1.0, prolong="copy", max_levels=0, device=0,
                  stream=None, rank=0, world=1, nccl_id=None, use_graph=True, beta1=0.9,
-                 beta2=0.999, eps=1e-8, zero_head=None):
+                 beta2=0.999, eps=1e-8, zero_head=None, coupled_paths=False):
         """stream: a torch.cuda.Stream, a raw cudaStream_t (int), or None (a new
         torch stream on `device`, kept in self.stream).  zero_head: R7b, defaults
-        to True for Allen-Cahn."""
+        to True for Allen-Cahn.  coupled_paths: every level draws the finest grid's
+        (N·2^max_levels) Brownian path, summed per coarse step (NEXT-3)."""
         L = _lib.lib()
         cfg = _lib.Config()
         L.bsde_config_default(ctypes.byref(cfg))
@@ -85,6 +86,7 @@ class BSDE:
         self._nccl_id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         cfg.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p) if nccl_id else None
         cfg.use_graph = int(bool(use_graph))
+        cfg.coupled_paths = int(bool(coupled_paths))
         self.problem = PROBLEMS[problem] if isinstance(problem, str) else int(problem)
         self.d, self.w, self.T, self.batch = int(d), int(width), float(T), int(batch)
         self.rank, self.world = int(rank), int(world)

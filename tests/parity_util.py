@@ -28,10 +28,10 @@ KINK_BAND = {"fp32": 2e-6, "bf16": 8e-3}
 
 
 def oracle_iteration(problem, d, w, N, T, params, seed, it, paths, batch, x0=0.0, lam=1.0,
-                     want_grad=True, kink_band=0.0):
+                     want_grad=True, kink_band=0.0, coupled_factor=1):
     return ob.iteration(PROBLEM[problem], d, w, N, T, np.asarray(params, np.float64), seed, it,
                         np.asarray(paths), batch, x0=x0, lam=lam, want_grad=want_grad,
-                        kink_band=kink_band)
+                        kink_band=kink_band, coupled_factor=coupled_factor)
 
 
 def compare_grads(g_gpu, g_orc, d, w, N, tol, slack=None):

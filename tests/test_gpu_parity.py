@@ -186,6 +186,41 @@ def test_prolongate_matches_oracle(mode):
         s.prolongate(3)
 
 
+@pytest.mark.parametrize("problem,x0", [("hjb", 0.0), ("black_scholes", 0.7)])
+def test_coupled_paths_match_oracle(problem, x0):
+    """Coupled multilevel paths (NEXT-3): at every level of N = 5 -> 10 -> 20 the
+    increments are sums of the N = 20 grid's (factor 4, 2, 1); teacher-forced
+    loss and gradient against the oracle with the same coupling."""
+    d, w, N, T, B = 12, 16, 5, 1.0, 200
+    s = make(problem, d, w, N, T, B, kernel="simt", max_levels=2, coupled_paths=True, x0=x0)
+    for level in range(3):
+        if level:
+            s.prolongate(level)
+        p = s.get_params()
+        p[1:] += (0.02 * np.random.default_rng(level).standard_normal(p.size - 1)).astype(np.float32)
+        s.set_params(p)
+        loss = s.compute_grad()
+        ref = oracle_iteration(problem, d, w, s.N, T, p, 0, s.iteration, np.arange(B), B, x0=x0,
+                               kink_band=KINK_BAND["fp32"], coupled_factor=20 // s.N)
+        assert abs(loss - ref["loss"]) <= 1e-4 * ref["loss"], (level, loss, ref["loss"])
+        compare_grads(s.get_grads(), ref["grad"], d, w, s.N, 1e-4, ref["slack"])
+        s.train_step()
+
+
+def test_coupled_paths_share_terminal_state_on_gpu():
+    """Heat with Z ≡ 0: Y_N = Y0 and X_N = √2 W_T, so coupled levels give the same
+    residuals (pin C2 of the oracle, on the device)."""
+    d, w, N, T, B = 10, 20, 4, 1.0, 256
+    s = make("heat", d, w, N, T, B, kernel="simt", max_levels=2, coupled_paths=True,
+             zero_head=True)
+    s.compute_grad()
+    R0 = s.debug_residuals(0, B)
+    for level in (1, 2):
+        s.prolongate(level)
+        s.compute_grad()
+        assert np.max(np.abs(s.debug_residuals(0, B) - R0)) <= 1e-5 * np.max(np.abs(R0))
+
+
 def test_eval_loss_matches_oracle():
     d, w, N, T = 20, 24, 4, 0.3
     s = make("allen_cahn", d, w, N, T, 128, kernel="simt")

@@ -125,6 +125,26 @@ def test_tc_fake_world_shards_sum():
     assert np.linalg.norm(gs - gf) <= 1e-4 * np.linalg.norm(gf)
 
 
+def test_tc_coupled_paths_match_oracle():
+    """Coupled multilevel paths on the tcgen05 path (NEXT-3): Allen-Cahn d = 100,
+    N = 4 -> 8 -> 16 with factors 4, 2, 1, teacher-forced against the oracle."""
+    d, w, N, T, B = 100, 110, 4, 0.3, 300
+    s = make("allen_cahn", d, w, N, T, B, kernel="tc", precision="bf16", max_levels=2,
+             coupled_paths=True, lr=5e-4)
+    for level in range(3):
+        if level:
+            s.prolongate(level)
+        p = s.get_params()
+        p[1:] += (0.003 * np.random.default_rng(level).standard_normal(p.size - 1)).astype(np.float32)
+        s.set_params(p)
+        loss = s.compute_grad()
+        ref = oracle_iteration("allen_cahn", d, w, s.N, T, p, 0, s.iteration, np.arange(B), B,
+                               kink_band=KINK_BAND["bf16"], coupled_factor=16 // s.N)
+        assert abs(loss - ref["loss"]) <= 2e-2 * ref["loss"], (level, loss, ref["loss"])
+        compare_grads(s.get_grads(), ref["grad"], d, w, s.N, 2e-2, ref["slack"])
+        s.train_step()
+
+
 def test_tc_eval_loss_matches_oracle():
     from oracle import philox
     d, w, N, T = 100, 110, 4, 0.3
