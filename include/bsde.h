@@ -104,11 +104,24 @@ typedef struct {
                              N is the sum of the f = N_fine/N fine increments it spans, each
                              drawn with Philox counter step n·f + j and √(T/N_fine) (R8).
                              0: each grid draws its own increments (default)               */
+  int formulation;        /* BSDE_FORM_PER_STEP (default): N per-step Z-nets + trainable Y0,
+                             terminal loss (BASELINE north_star).
+                             BSDE_FORM_SHARED: the paper's own formulation (PAPER.md:69-77,
+                             Eq. 6; DESIGN R23, R24): one network
+                             u(t, x) of n_widths tanh layers shared by all steps, Y_n =
+                             u(t_n, X_n), z_n = σ(X_n)ᵀ∇ₓu, residual-sum loss.  FP32 and the
+                             SIMT kernels only                                              */
+  int arch;               /* BSDE_FORM_SHARED: BSDE_ARCH_FC or BSDE_ARCH_RESNET (h_k = h_{k-1}
+                             + tanh(W_k h_{k-1} + b_k) for k >= 2)        */
 } bsde_config;
+
+enum { BSDE_FORM_PER_STEP = 0, BSDE_FORM_SHARED = 1 };
+enum { BSDE_ARCH_FC = 0, BSDE_ARCH_RESNET = 1 };
 
 /* Fill *cfg with defaults: B = 256, x0 = 0, λ = 1, Adam (1e-2, 0.9, 0.999, 1e-8),
  * seed 0, FP32, KERNEL_AUTO, COPY, max_levels 0, device 0, default stream,
- * rank 0 of 1, no NCCL, graphs on, Xavier head (init_zero_head 0), uncoupled paths. */
+ * rank 0 of 1, no NCCL, graphs on, Xavier head (init_zero_head 0), uncoupled paths,
+ * per-step formulation (FC arch for the shared one). */
 void bsde_config_default(bsde_config* cfg);
 
 /* Create a context for `problem` in dimension d with N time steps on [0, T]

@@ -53,6 +53,8 @@ class Config(ctypes.Structure):
         ("use_graph", ctypes.c_int),
         ("init_zero_head", ctypes.c_int),
         ("coupled_paths", ctypes.c_int),
+        ("formulation", ctypes.c_int),
+        ("arch", ctypes.c_int),
     ]
 
 

@@ -77,6 +77,9 @@ NcclApi& nccl() {
 
 struct bsde_ctx {
   int problem = 0, d = 0, w = 0, N = 0, N0 = 0, level = 0, N_max = 0;
+  bool shared = false;          // BSDE_FORM_SHARED (NEXT-1)
+  int L = 0;                    // shared: number of tanh layers
+  void* shbuf = nullptr;        // shared: row buffers (carved into ShArgs)
   double T = 1.0;
   bsde_config cfg{};
   int64_t B_local = 0, m0 = 0;
@@ -126,7 +129,39 @@ int fail(bsde_ctx* c, int code, const char* fmt, ...) {
       return fail(ctx, BSDE_ENCCL, "%s: %s", #expr, nccl().GetErrorString(r_));         \
   } while (0)
 
-int64_t num_params_at(const bsde_ctx* c, int N) { return 1 + (int64_t)N * NetDims{c->d, c->w}.step_size(); }
+int64_t num_params_at(const bsde_ctx* c, int N) {
+  if (c->shared) return (int64_t)shared_num_params(c->d, c->w, c->L);   // independent of N
+  return 1 + (int64_t)N * NetDims{c->d, c->w}.step_size();
+}
+
+ShArgs sh_args(bsde_ctx* c) {
+  ShArgs a{};
+  a.problem = c->problem;
+  a.arch = c->cfg.arch;
+  a.d = c->d;
+  a.w = c->w;
+  a.L = c->L;
+  a.N = c->N;
+  a.K0p = (c->d + 1 + 3) & ~3;
+  a.M = c->B_local;
+  a.m0 = c->m0;
+  a.dt = (float)(c->T / c->N);
+  a.cpl = c->cfg.coupled_paths ? c->N_max / c->N : 1;
+  a.sqrt_dt_f = (float)std::sqrt(c->T / ((double)c->N * a.cpl));
+  a.lam = (float)c->cfg.lambda;
+  a.x0 = (float)c->cfg.x0;
+  a.inv_B = (float)(1.0 / (double)c->cfg.batch_global);
+  a.k0 = (uint32_t)(c->cfg.seed & 0xffffffffu);
+  a.k1 = (uint32_t)(c->cfg.seed >> 32);
+  a.state = c->state;
+  a.loss_acc = &c->state->loss_sum;
+  a.params = c->params;
+  a.grad = c->grad;
+  a.Rstore = c->Rstore;
+  shared_offsets(a);
+  if (c->shbuf) shared_carve(a, c->shbuf, c->N_max);
+  return a;
+}
 
 PassArgs pass_args(bsde_ctx* c) {
   PassArgs a{};
@@ -172,16 +207,21 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
   CK(launch_begin_step(ctx->state, ctx->grad, np, ctx->stream));
   launches += 1;   // k_begin_step (the memset is not a kernel)
   mark(1);
-  if (ctx->family == BSDE_KERNEL_TC) {
+  if (ctx->shared) {
+    int nl = 0;
+    CK(launch_shared_step(sh_args(ctx), ctx->stream, ev ? ev[2] : nullptr, &nl));
+    launches += nl;
+  } else if (ctx->family == BSDE_KERNEL_TC) {
     CK(launch_fwd_tc(a, ctx->stream));
     mark(2);
     CK(launch_bwd_tc(a, ctx->stream));
+    launches += 2;
   } else {
     CK(launch_fwd_simt(a, ctx->stream));
     mark(2);
     CK(launch_bwd_simt(a, ctx->stream));
+    launches += 2;
   }
-  launches += 2;
   mark(3);
   if (ctx->comm) {
     NK(nccl().GroupStart());
@@ -202,9 +242,11 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
                    (float)ctx->cfg.eps, 1, ctx->stream));
     launches += 2;
     // weight images for the next step (bf16 UMMA images / fp32 transposed images)
-    if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(a, ctx->stream));
-    else CK(launch_pack_simt(a, ctx->stream));
-    launches += 1;
+    if (!ctx->shared) {
+      if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(a, ctx->stream));
+      else CK(launch_pack_simt(a, ctx->stream));
+      launches += 1;
+    }
   }
   mark(6);
   ctx->launches = launches;
@@ -218,6 +260,7 @@ int read_state(bsde_ctx* ctx, DeviceState* hs) {
 }
 
 int repack(bsde_ctx* ctx) {
+  if (ctx->shared) return BSDE_OK;   // the shared kernels read the fp32 master directly
   if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(pass_args(ctx), ctx->stream));
   else CK(launch_pack_simt(pass_args(ctx), ctx->stream));
   return BSDE_OK;
@@ -227,7 +270,7 @@ void free_all(bsde_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   void* bufs[] = {c->params, c->grad, c->adam_m, c->adam_v, c->scratch, c->Xstore, c->Pstore,
                   c->abar, c->Rstore, c->wpack, c->xpack, c->gpart, c->state,
-                  c->eval_loss};
+                  c->eval_loss, c->shbuf};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
@@ -283,10 +326,25 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
                 problem);
   if (d < 1 || N < 1 || !(T > 0.0))
     return fail(none, BSDE_EINVAL, "need d >= 1, N >= 1, T > 0 (got d=%d N=%d T=%g)", d, N, T);
-  if (!widths || n_widths != 2 || widths[0] != widths[1] || widths[0] < 1)
+  const bool shared = cfg.formulation == BSDE_FORM_SHARED;
+  if (cfg.formulation != BSDE_FORM_PER_STEP && !shared)
+    return fail(none, BSDE_EINVAL, "formulation=%d", cfg.formulation);
+  if (shared) {
+    if (!widths || n_widths < 1 || n_widths > kMaxSharedLayers || widths[0] < 1)
+      return fail(none, BSDE_EINVAL, "shared net: 1 <= n_widths <= %d layers of width w >= 1",
+                  kMaxSharedLayers);
+    for (int k = 1; k < n_widths; ++k)
+      if (widths[k] != widths[0])
+        return fail(none, BSDE_EINVAL, "shared net: all layer widths must be equal (R23)");
+    if (cfg.arch != BSDE_ARCH_FC && cfg.arch != BSDE_ARCH_RESNET)
+      return fail(none, BSDE_EINVAL, "arch=%d", cfg.arch);
+    if (cfg.precision != BSDE_FP32 || cfg.kernel == BSDE_KERNEL_TC)
+      return fail(none, BSDE_EINVAL, "the shared formulation runs fp32 SIMT kernels only");
+  } else if (!widths || n_widths != 2 || widths[0] != widths[1] || widths[0] < 1) {
     return fail(none, BSDE_EINVAL,
                 "widths must be {w, w} with w >= 1 (d->w->w->d residual net, R4); got n_widths=%d",
                 n_widths);
+  }
   const int w = widths[0];
   if (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world)
     return fail(none, BSDE_EINVAL, "rank=%d world=%d", cfg.rank, cfg.world);
@@ -306,6 +364,7 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
       !(cfg.eps > 0))
     return fail(none, BSDE_EINVAL, "Adam hyper-parameters out of range");
   int family = cfg.kernel;
+  if (shared) family = BSDE_KERNEL_SIMT;
   if (family == BSDE_KERNEL_AUTO)
     family = (cfg.precision == BSDE_BF16 && tc_supported(d, w)) ? BSDE_KERNEL_TC : BSDE_KERNEL_SIMT;
   if (family == BSDE_KERNEL_TC && !tc_supported(d, w))
@@ -318,7 +377,7 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
                 "kernel=SIMT");
   if (family == BSDE_KERNEL_SIMT && cfg.precision == BSDE_BF16)
     return fail(none, BSDE_EINVAL, "bf16 operands need the tcgen05 kernels (kernel=SIMT given)");
-  if (family == BSDE_KERNEL_SIMT && !simt_supported(d, w))
+  if (family == BSDE_KERNEL_SIMT && !shared && !simt_supported(d, w))
     return fail(none, BSDE_EINVAL, "d=%d w=%d too large for the SIMT kernels (d, w <= 127 and shared "
                 "memory)", d, w);
   if (family != BSDE_KERNEL_SIMT && family != BSDE_KERNEL_TC)
@@ -329,6 +388,8 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
 
   bsde_ctx* ctx = new bsde_ctx;
   ctx->problem = problem;
+  ctx->shared = shared;
+  ctx->L = shared ? n_widths : 0;
   ctx->d = d;
   ctx->w = w;
   ctx->N = ctx->N0 = N;
@@ -361,8 +422,9 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
   const int64_t npmax = num_params_at(ctx, ctx->N_max);
   struct Alloc { void** p; size_t bytes; };
   // X_n store for the adjoint: fp32 rows (SIMT) or bf16 operand images (tcgen05)
-  const size_t xs = family == BSDE_KERNEL_TC ? tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)
-                                             : simt_xstore_bytes(d, ctx->N_max, ctx->B_local);
+  const size_t xs = shared ? 16
+                   : family == BSDE_KERNEL_TC ? tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)
+                                              : simt_xstore_bytes(d, ctx->N_max, ctx->B_local);
   std::vector<Alloc> allocs = {
       {(void**)&ctx->params, npmax * sizeof(float)},
       {(void**)&ctx->grad, npmax * sizeof(float)},
@@ -375,9 +437,14 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
       {(void**)&ctx->state, sizeof(DeviceState)},
       {(void**)&ctx->eval_loss, sizeof(double) * 2},
   };
-  if (per_step_abar(problem))
+  if (shared) {
+    allocs.push_back({&ctx->shbuf, shared_buffer_bytes(d, w, ctx->L, cfg.arch, ctx->N_max,
+                                                       ctx->B_local)});
+  } else if (per_step_abar(problem)) {
     allocs.push_back({(void**)&ctx->Pstore, (size_t)ctx->N_max * ctx->B_local * sizeof(float)});
-  if (family == BSDE_KERNEL_TC) {
+  }
+  if (shared) {
+  } else if (family == BSDE_KERNEL_TC) {
     allocs.push_back({&ctx->wpack, tc_pack_bytes(d, w, ctx->N_max, cfg.precision)});
     allocs.push_back({&ctx->xpack, tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)});
   } else {
@@ -396,9 +463,12 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
   cudaMemsetAsync(ctx->adam_m, 0, npmax * sizeof(float), ctx->stream);
   cudaMemsetAsync(ctx->adam_v, 0, npmax * sizeof(float), ctx->stream);
   cudaMemsetAsync(ctx->state, 0, sizeof(DeviceState), ctx->stream);
-  if (launch_init_params(ctx->params, d, w, N, (uint32_t)(cfg.seed & 0xffffffffu),
-                         (uint32_t)(cfg.seed >> 32), cfg.init_zero_head, ctx->stream) !=
-      cudaSuccess) {
+  const cudaError_t ie =
+      shared ? launch_shared_init(ctx->params, sh_args(ctx), (uint32_t)(cfg.seed & 0xffffffffu),
+                                  (uint32_t)(cfg.seed >> 32), ctx->stream)
+             : launch_init_params(ctx->params, d, w, N, (uint32_t)(cfg.seed & 0xffffffffu),
+                                  (uint32_t)(cfg.seed >> 32), cfg.init_zero_head, ctx->stream);
+  if (ie != cudaSuccess) {
     ctx->err = "init kernel launch failed";
     return bail(BSDE_ECUDA);
   }
@@ -471,11 +541,13 @@ int bsde_prolongate(bsde_ctx* ctx, int level) {
   if (level != ctx->level + 1 || level > ctx->cfg.max_levels)
     return fail(ctx, BSDE_ESTATE, "prolongate(level=%d): current level %d, max_levels %d", level,
                 ctx->level, ctx->cfg.max_levels);
-  const int64_t P = NetDims{ctx->d, ctx->w}.step_size();
-  const int64_t np = num_params_at(ctx, ctx->N);
-  CK(cudaMemcpyAsync(ctx->scratch, ctx->params, np * sizeof(float), cudaMemcpyDeviceToDevice,
-                     ctx->stream));
-  CK(launch_prolong(ctx->scratch, ctx->params, P, ctx->N, ctx->cfg.prolong_mode, ctx->stream));
+  if (!ctx->shared) {   // the shared network is the same function on every grid
+    const int64_t P = NetDims{ctx->d, ctx->w}.step_size();
+    const int64_t np = num_params_at(ctx, ctx->N);
+    CK(cudaMemcpyAsync(ctx->scratch, ctx->params, np * sizeof(float), cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    CK(launch_prolong(ctx->scratch, ctx->params, P, ctx->N, ctx->cfg.prolong_mode, ctx->stream));
+  }
   ctx->N *= 2;
   ctx->level = level;
   const int64_t np2 = num_params_at(ctx, ctx->N);
@@ -496,7 +568,12 @@ int bsde_y0(const bsde_ctx* cctx, double* y0_out) {
   bsde_ctx* ctx = const_cast<bsde_ctx*>(cctx);
   if (!ctx || !y0_out) return fail(ctx, BSDE_EINVAL, "NULL argument");
   float y;
-  CK(cudaMemcpyAsync(&y, ctx->params, sizeof y, cudaMemcpyDeviceToHost, ctx->stream));
+  if (ctx->shared) {   // Y0 = u(0, X_0), evaluated by the network on the device
+    CK(launch_shared_point(sh_args(ctx), ctx->scratch, ctx->stream));
+    CK(cudaMemcpyAsync(&y, ctx->scratch, sizeof y, cudaMemcpyDeviceToHost, ctx->stream));
+  } else {
+    CK(cudaMemcpyAsync(&y, ctx->params, sizeof y, cudaMemcpyDeviceToHost, ctx->stream));
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   *y0_out = y;
   return BSDE_OK;
@@ -601,6 +678,21 @@ int bsde_eval_loss(bsde_ctx* ctx, uint32_t eval_id, int64_t batch, double* loss_
   if (batch < 1 || batch % ctx->cfg.world || batch > ((int64_t)1 << 32))
     return fail(ctx, BSDE_EINVAL, "eval batch=%lld must be divisible by world=%d",
                 (long long)batch, ctx->cfg.world);
+  if (ctx->shared) {
+    if (batch / ctx->cfg.world > ctx->B_local)
+      return fail(ctx, BSDE_EINVAL, "shared formulation: eval batch per rank must be <= %lld",
+                  (long long)ctx->B_local);
+    ShArgs sa = sh_args(ctx);
+    sa.eval = 1;
+    sa.eval_it = kEvalBit | (eval_id & 0x7fffffffu);
+    sa.M = batch / ctx->cfg.world;
+    sa.m0 = (int64_t)ctx->cfg.rank * sa.M;
+    sa.inv_B = (float)(1.0 / (double)batch);
+    sa.loss_acc = ctx->eval_loss;
+    shared_carve(sa, ctx->shbuf, ctx->N_max);
+    CK(cudaMemsetAsync(ctx->eval_loss, 0, sizeof(double), ctx->stream));
+    CK(launch_shared_step(sa, ctx->stream, nullptr, nullptr));
+  }
   PassArgs a = pass_args(ctx);
   a.eval = 1;
   a.eval_it = kEvalBit | (eval_id & 0x7fffffffu);
@@ -608,10 +700,12 @@ int bsde_eval_loss(bsde_ctx* ctx, uint32_t eval_id, int64_t batch, double* loss_
   a.m0 = (int64_t)ctx->cfg.rank * a.B_local;
   a.inv_B = (float)(1.0 / (double)batch);
   a.loss_acc = ctx->eval_loss;
-  CK(cudaMemsetAsync(ctx->eval_loss, 0, sizeof(double), ctx->stream));
-  if (ctx->family == BSDE_KERNEL_TC) {
+  if (ctx->shared) {
+  } else if (ctx->family == BSDE_KERNEL_TC) {
+    CK(cudaMemsetAsync(ctx->eval_loss, 0, sizeof(double), ctx->stream));
     CK(launch_fwd_tc(a, ctx->stream));   // an evaluation pass stores no path images
   } else {
+    CK(cudaMemsetAsync(ctx->eval_loss, 0, sizeof(double), ctx->stream));
     CK(launch_fwd_simt(a, ctx->stream));
   }
   if (ctx->comm)
@@ -704,7 +798,8 @@ int bsde_profile_steps(bsde_ctx* ctx, int steps, float* ms_out, int n_out) {
 }
 
 int bsde_debug_phase_clocks(bsde_ctx* ctx, int which, uint64_t* out, int n) {
-  if (!ctx || !out || n < 1 || (which != 0 && which != 1) || ctx->family != BSDE_KERNEL_TC)
+  if (!ctx || !out || n < 1 || (which != 0 && which != 1) || ctx->family != BSDE_KERNEL_TC ||
+      ctx->shared)
     return fail(ctx, BSDE_EINVAL, "debug_phase_clocks: bad argument (tcgen05 path only)");
   unsigned long long* buf = nullptr;
   CK(cudaMalloc(&buf, (size_t)n * sizeof(uint64_t)));
@@ -732,6 +827,7 @@ int bsde_launches_per_step(const bsde_ctx* ctx, int* n) {
 
 const char* bsde_kernel_family(const bsde_ctx* ctx) {
   if (!ctx) return "none";
+  if (ctx->shared) return "shared-simt";
   return ctx->family == BSDE_KERNEL_TC ? "tc" : "simt";
 }
 

@@ -38,6 +38,42 @@ struct PassArgs {
   float sqrt_dt_f;                     // √(Δt/cpl)
 };
 
+// Shared-network formulation (shared.cu): one
+// iteration's device state.  Rows r = n·M + m, n = 0..N, row-major buffers.
+constexpr int kMaxSharedLayers = 8;
+struct ShArgs {
+  int problem, arch, d, w, L, N, K0p;       // K0p = d+1 rounded up to 4 (row stride of U0, G0, Ḡ0)
+  int64_t M, m0;                            // local paths, first global path
+  float dt, sqrt_dt_f, lam, x0, inv_B;
+  int cpl;                                  // coupled paths: fine steps per step (R22)
+  uint32_t k0, k1;
+  int eval;
+  uint32_t eval_it;
+  DeviceState* state;
+  double* loss_acc;
+  const float* params;
+  float* grad;
+  float* Rstore;                            // [M] terminal residuals r_N
+  int64_t off_W[kMaxSharedLayers], off_v;   // flat offsets of W_k (b_k follows) and v (c follows)
+  float *U0, *G0, *G0b, *dW;                // [R×K0p] inputs, ∇u, ∂L/∂∇u;  [N·M×d] increments
+  float* S[kMaxSharedLayers];               // s_k = tanh(a_k)
+  float* H[kMaxSharedLayers];               // h_k (= S[k] unless residual)
+  float* D[kMaxSharedLayers];               // δ_k = g_k ⊙ (1 - s_k²)
+  float* G[kMaxSharedLayers];               // g_k = ∂u/∂h_k, k < L-1 (g_{L-1} = v)
+  float* Sb[kMaxSharedLayers];              // s̄_k from the input-gradient adjoint
+  float* HL;
+  float *Gb[2], *Ab[2], *Hb[2];             // ping-pong ḡ, ā, h̄
+  float *u, *ub, *q;                        // [R] u, ū; [R×4] z·ΔW | |z|² | Σz
+};
+size_t shared_num_params(int d, int w, int L);
+void shared_offsets(ShArgs& a);
+size_t shared_buffer_bytes(int d, int w, int L, int arch, int N_max, int64_t M);
+void shared_carve(ShArgs& a, void* base, int N_max);
+cudaError_t launch_shared_init(float* params, const ShArgs& a, uint32_t k0, uint32_t k1,
+                               cudaStream_t s);
+cudaError_t launch_shared_point(const ShArgs& a, float* out, cudaStream_t s);
+cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid, int* launches);
+
 // SIMT fp32 kernels (simt.cu)
 cudaError_t launch_fwd_simt(const PassArgs& a, cudaStream_t s);
 cudaError_t launch_bwd_simt(const PassArgs& a, cudaStream_t s);

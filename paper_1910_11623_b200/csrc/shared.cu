@@ -1,0 +1,663 @@
+// shared.cu — the paper's own formulation (PAPER.md:69-77,
+// fig:neural, Eq. 6): ONE network u(t, x; Θ) for every time step, Y_n =
+// u(t_n, X_n), z_n = σ(X_n)ᵀ∇ₓu(t_n, X_n), and the residual-sum loss
+//   L = (1/B) Σ_m [ Σ_{n<N} (Y_{n+1} - Y_n + f(Y_n, z_n)Δt - z_n·ΔW_n)² + (Y_N - g(X_N))² ]
+// (R23, R24).  Because the loss contains ∇ₓu, ∂L/∂Θ is a second derivative of
+// the network: the hand-written reverse-over-reverse pass below, checked
+// against oracle/shared.py (itself pinned by finite differences).
+//
+// Every (path, time) pair is an independent row once the paths are drawn (X
+// does not depend on Θ), so the iteration is a sequence of row-batched dense
+// GEMMs over R = (N+1)·B_local rows with fused elementwise epilogues:
+//
+//   paths     U0 = [t_n | X_n] rows, ΔW_n                    (Philox, Euler; R8)
+//   forward   a_k = h_{k-1} W_kᵀ + b_k, s_k = tanh a_k, h_k = s_k (+ h_{k-1}, ResNet)   NT GEMMs
+//             δ_L = v ⊙ (1 - s_L²)                              (last epilogue)
+//   ∇ₓu       g_{k-1} = δ_k W_k (+ g_k), δ_{k-1} = g_{k-1} ⊙ (1 - s_{k-1}²)            NN GEMMs
+//   rows      u = v·h_L + c; z = σ(X)ᵀ g_0[1:]; z·ΔW, |z|², Σz                  (warp per row)
+//   loss      r_n, Σ r²; ū = ∂L/∂u, ḡ_0 = σ(X) z̄ per row                          (warp per row)
+//   up        W̄_k += δ_kᵀ ḡ_{k-1};  δ̄_k = ḡ_{k-1} W_kᵀ;  ḡ_k = δ̄_k ⊙ s'_k (+ ḡ_{k-1});
+//             s̄_k = -2 s_k g_k δ̄_k                                      NT + TN GEMMs
+//   down      ā_k = (s̄_k + h̄_k) ⊙ s'_k;  W̄_k += ā_kᵀ h_{k-1}, b̄_k += Σ ā_k;
+//             h̄_{k-1} = ā_k W_k (+ h̄_k)                                   NN + TN GEMMs
+//   head      v̄ = Σ (ḡ_L + ū h_L), c̄ = Σ ū
+//
+// fp32 throughout (the paper's PyTorch precision); SIMT FFMA GEMM
+// tiles 64×64×16 with 4×4 register tiles per thread.
+#include "kernels.cuh"
+
+namespace bsde {
+namespace {
+
+constexpr int TB = 64, TK = 16, NTH = 256;
+
+// ---------------------------------------------------------------- GEMM cores
+// Row GEMM: C[i][j] = Σ_k A[i][k]·B'[k][j] for i < R, j < NC, then epi(i, j, c).
+// NT: B' = Bᵀ with B row-major [NC×K] (a weight W_k [out×in]);  NN: B' = B, [K×NC].
+template <bool NT, class Epi>
+__global__ void __launch_bounds__(NTH) k_gemm_rows(const float* __restrict__ A, int lda,
+                                                   const float* __restrict__ B, int ldb, int R,
+                                                   int NC, int K, Epi epi) {
+  __shared__ __align__(16) float As[TK][TB + 4];
+  __shared__ __align__(16) float Bs[TK][TB + 4];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int i0 = blockIdx.y * TB, j0 = blockIdx.x * TB;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += TK) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = t + NTH * e, ii = idx >> 4, kk = idx & 15;
+      const int i = i0 + ii, k = k0 + kk;
+      As[kk][ii] = (i < R && k < K) ? __ldg(A + (int64_t)i * lda + k) : 0.0f;
+      if (NT) {
+        const int j = j0 + ii;
+        Bs[kk][ii] = (j < NC && k < K) ? __ldg(B + (int64_t)j * ldb + k) : 0.0f;
+      } else {
+        const int kb = idx >> 6, jj = idx & 63, k2 = k0 + kb, j = j0 + jj;
+        Bs[kb][jj] = (k2 < K && j < NC) ? __ldg(B + (int64_t)k2 * ldb + j) : 0.0f;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[kk][4 * ty]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][4 * tx]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + 4 * ty + r, j = j0 + 4 * tx + c;
+      if (i < R && j < NC) epi(i, j, acc[r][c]);
+    }
+}
+
+// Weight-gradient GEMM over rows: C[p][q] += Σ_r A[r][p]·B[r][q] (+ A2[r][p]·B2[r][q]),
+// rows split over blockIdx.z, fp32 atomics into C (row-major, ldc).
+__global__ void __launch_bounds__(NTH) k_gemm_tn(const float* __restrict__ A, int lda,
+                                                 const float* __restrict__ B, int ldb,
+                                                 const float* __restrict__ A2, int lda2,
+                                                 const float* __restrict__ B2, int ldb2, int R,
+                                                 int P, int Q, float* __restrict__ C, int ldc,
+                                                 int rows_per_split) {
+  __shared__ __align__(16) float As[TK][TB + 4];
+  __shared__ __align__(16) float Bs[TK][TB + 4];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int p0 = blockIdx.y * TB, q0 = blockIdx.x * TB;
+  const int r_begin = blockIdx.z * rows_per_split;
+  const int r_end = min(R, r_begin + rows_per_split);
+  float acc[4][4] = {};
+  for (int pass = 0; pass < (A2 ? 2 : 1); ++pass) {
+    const float* a_ = pass ? A2 : A;
+    const float* b_ = pass ? B2 : B;
+    const int la = pass ? lda2 : lda, lb = pass ? ldb2 : ldb;
+    for (int r0 = r_begin; r0 < r_end; r0 += TK) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int idx = t + NTH * e, kk = idx >> 6, pp = idx & 63, r = r0 + kk;
+        As[kk][pp] = (r < r_end && p0 + pp < P) ? __ldg(a_ + (int64_t)r * la + p0 + pp) : 0.0f;
+        Bs[kk][pp] = (r < r_end && q0 + pp < Q) ? __ldg(b_ + (int64_t)r * lb + q0 + pp) : 0.0f;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < TK; ++kk) {
+        const float4 a = *reinterpret_cast<const float4*>(&As[kk][4 * ty]);
+        const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][4 * tx]);
+        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int p = p0 + 4 * ty + r, q = q0 + 4 * tx + c;
+      if (p < P && q < Q && acc[r][c] != 0.0f) atomicAdd(C + (int64_t)p * ldc + q, acc[r][c]);
+    }
+}
+
+// out[j] += Σ_r X[r][j] (+ s[r]·Y[r][j]);  blockDim 256 = 8 row lanes × 32 columns
+__global__ void __launch_bounds__(NTH) k_colsum(const float* __restrict__ X, int ldx,
+                                                const float* __restrict__ s,
+                                                const float* __restrict__ Y, int ldy, int R,
+                                                int NC, int rows_per_block, float* __restrict__ out) {
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31), lr = threadIdx.x >> 5;
+  const int r0 = blockIdx.y * rows_per_block, r1 = min(R, r0 + rows_per_block);
+  float acc = 0.0f;
+  if (j < NC)
+    for (int r = r0 + lr; r < r1; r += 8) {
+      float v = X ? X[(int64_t)r * ldx + j] : 0.0f;
+      if (Y) v = fmaf(s[r], Y[(int64_t)r * ldy + j], v);
+      acc += v;
+    }
+  __shared__ float red[8][33];
+  red[lr][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (lr == 0 && j < NC) {
+    float tot = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tot += red[k][threadIdx.x & 31];
+    if (tot != 0.0f) atomicAdd(out + j, tot);
+  }
+}
+
+// ---------------------------------------------------------------- epilogues
+struct EpiFwd {        // layer k: s = tanh(a + b); S_k, H_k (ResNet); δ_L on the last layer
+  const float* b;
+  float* S;
+  float* H;            // != S for ResNet layers k ≥ 2
+  const float* Hprev;  // h_{k-1} (ResNet)
+  const float* v;      // head (last layer only) for δ_L = v ⊙ (1 - s²)
+  float* D;
+  int ld;
+  __device__ void operator()(int i, int j, float a) const {
+    const float s = tanhf(a + __ldg(b + j));
+    const int64_t o = (int64_t)i * ld + j;
+    S[o] = s;
+    if (H != S) H[o] = Hprev[o] + s;
+    if (v) D[o] = __ldg(v + j) * (1.0f - s * s);
+  }
+};
+
+struct EpiIg {         // g_{k-1} = δ_k W_k (+ g_k); δ_{k-1} = g_{k-1} ⊙ (1 - s_{k-1}²)
+  const float* gk;     // g_k for the residual term (null: none); gk_is_v: g_L = v (row-broadcast)
+  int gk_is_v;
+  float* G;            // g_{k-1}
+  const float* S;      // s_{k-1} (null for k = 1: g_0 has no δ)
+  float* D;            // δ_{k-1}
+  int ld;              // of G, S, D (and gk unless gk_is_v)
+  __device__ void operator()(int i, int j, float c) const {
+    const int64_t o = (int64_t)i * ld + j;
+    if (gk) c += gk_is_v ? __ldg(gk + j) : gk[o];
+    G[o] = c;
+    if (S) {
+      const float s = S[o];
+      D[o] = c * (1.0f - s * s);
+    }
+  }
+};
+
+struct EpiUp {         // δ̄_k = ḡ_{k-1} W_kᵀ:  ḡ_k = δ̄ ⊙ s'_k (+ ḡ_{k-1});  s̄_k = -2 s_k g_k δ̄
+  const float* S;      // s_k
+  const float* Gk;     // g_k (null: g_L = v, row-broadcast from gv)
+  const float* gv;
+  const float* Gbprev; // ḡ_{k-1} for the residual term (same width w), or null
+  float* Gb;           // ḡ_k
+  float* Sb;           // s̄_k
+  int ld;
+  __device__ void operator()(int i, int j, float db) const {
+    const int64_t o = (int64_t)i * ld + j;
+    const float s = S[o];
+    const float g = Gk ? Gk[o] : __ldg(gv + j);
+    float gb = db * (1.0f - s * s);
+    if (Gbprev) gb += Gbprev[o];
+    Gb[o] = gb;
+    Sb[o] = -2.0f * s * g * db;
+  }
+};
+
+struct EpiDown {       // h̄_{k-1} = ā_k W_k (+ h̄_k);  ā_{k-1} = (s̄_{k-1} + h̄_{k-1}) ⊙ s'_{k-1}
+  const float* Hb;     // h̄_k (residual term) or null
+  float* Hbout;        // h̄_{k-1} when layer k-1 is itself residual (needed one level down), or null
+  const float* Sb;     // s̄_{k-1}
+  const float* S;      // s_{k-1}
+  float* Ab;           // ā_{k-1}
+  int ld;
+  __device__ void operator()(int i, int j, float c) const {
+    const int64_t o = (int64_t)i * ld + j;
+    if (Hb) c += Hb[o];
+    if (Hbout) Hbout[o] = c;
+    const float s = S[o];
+    Ab[o] = (Sb[o] + c) * (1.0f - s * s);
+  }
+};
+
+// ---------------------------------------------------------------- row kernels
+// Paths of this rank: U0 rows (n·M + m) = [t_n, X_n, 0 pad], ΔW rows (n·M + m) = ΔW_n.
+// One thread per (path, 4-component block); coupled paths sum fine increments (R22).
+__global__ void k_sh_paths(ShArgs a) {
+  const int nq = (a.d + 3) >> 2;
+  const int64_t tot = a.M * nq;
+  const uint32_t it = a.eval ? a.eval_it : a.state->it;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < tot;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = id / nq;
+    const int q = (int)(id - m * nq);
+    float x[4] = {a.x0, a.x0, a.x0, a.x0};
+    for (int n = 0; n <= a.N; ++n) {
+      float* u = a.U0 + ((int64_t)n * a.M + m) * a.K0p;
+      if (q == 0) u[0] = (float)n * a.dt;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (4 * q + e < a.d) u[1 + 4 * q + e] = x[e];
+      if (n == a.N) break;
+      float dw[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int j = 0; j < a.cpl; ++j) {
+        const float4 z = normals4((uint32_t)q, (uint32_t)(a.m0 + m), (uint32_t)(n * a.cpl + j), it,
+                                  a.k0, a.k1);
+        dw[0] += a.sqrt_dt_f * z.x; dw[1] += a.sqrt_dt_f * z.y;
+        dw[2] += a.sqrt_dt_f * z.z; dw[3] += a.sqrt_dt_f * z.w;
+      }
+      float* o = a.dW + ((int64_t)n * a.M + m) * a.d;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (4 * q + e < a.d) {
+          o[4 * q + e] = dw[e];
+          x[e] = x_step(a.problem, x[e], dw[e]);
+        }
+    }
+  }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// z_i = σ(X)ᵀ∇ₓu: √2 g_i, or σ x_i g_i (Black-Scholes)
+__device__ __forceinline__ float sig(int problem, float x, float g) {
+  return problem == kBlackScholes ? kBSSigma * x * g : 1.41421356237309515f * g;
+}
+
+// One warp per row: u = v·h_L + c; z·ΔW, |z|², Σz (n < N) or |X_N|² (n = N).
+__global__ void k_sh_rowscal(ShArgs a) {
+  const int64_t R = (int64_t)(a.N + 1) * a.M;
+  const int lane = threadIdx.x & 31;
+  const float* v = a.params + a.off_v;
+  const float c = a.params[a.off_v + a.w];
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < R;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int n = (int)(r / a.M);
+    const float* h = a.HL + r * a.w;
+    float u = 0.0f;
+    for (int j = lane; j < a.w; j += 32) u = fmaf(h[j], __ldg(v + j), u);
+    u = warp_sum(u) + c;
+    const float* xr = a.U0 + r * a.K0p + 1;
+    const float* gr = a.G0 + r * a.K0p + 1;
+    float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
+    if (n < a.N) {
+      const float* dw = a.dW + r * a.d;
+      for (int i = lane; i < a.d; i += 32) {
+        const float z = sig(a.problem, xr[i], gr[i]);
+        s0 = fmaf(z, dw[i], s0);
+        s1 = fmaf(z, z, s1);
+        s2 += z;
+      }
+    } else {
+      for (int i = lane; i < a.d; i += 32) s0 = fmaf(xr[i], xr[i], s0);
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      a.u[r] = u;
+      a.q[4 * r + 0] = s0;   // z·ΔW, or |X_N|²
+      a.q[4 * r + 1] = s1;   // |z|²
+      a.q[4 * r + 2] = s2;   // Σ z
+    }
+  }
+}
+
+__device__ __forceinline__ float residual(const ShArgs& a, int n, int64_t m) {
+  const int64_t r = (int64_t)n * a.M + m;
+  if (n == a.N) return a.u[r] - terminal_g(a.problem, a.q[4 * r]);
+  const float y = a.u[r];
+  return a.u[r + a.M] - y + driver_f(a.problem, y, a.q[4 * r + 1], a.q[4 * r + 2], a.lam) * a.dt -
+         a.q[4 * r];
+}
+
+// One warp per row (n, m): the residuals r_{n-1}, r_n; Σ r²; ū = ∂L/∂u and
+// ḡ_0 = [0, σ(X) z̄] with z̄ = (2/B) r_n (Δt ∂_z f - ΔW_n) (R24).
+__global__ void k_sh_loss(ShArgs a) {
+  const int64_t R = (int64_t)(a.N + 1) * a.M;
+  const int lane = threadIdx.x & 31;
+  const float sc = 2.0f * a.inv_B;
+  const float zc = a.dt * driver_dfdz_coef(a.problem, a.lam), zc0 = a.dt * driver_dfdz_const(a.problem);
+  double lsum = 0.0;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < R;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int n = (int)(r / a.M);
+    const int64_t m = r - (int64_t)n * a.M;
+    const float rn = residual(a, n, m);
+    if (lane == 0) lsum += (double)rn * rn;
+    if (a.eval) continue;
+    const float y = a.u[r];
+    float ub = 0.0f;
+    if (n >= 1) ub += residual(a, n - 1, m);
+    if (n < a.N) ub += rn * (-1.0f + a.dt * driver_dfdy(a.problem, y));
+    else ub += rn;
+    float* gb = a.G0b + r * a.K0p;
+    if (lane == 0) {
+      a.ub[r] = sc * ub;
+      gb[0] = 0.0f;
+    }
+    const float* xr = a.U0 + r * a.K0p + 1;
+    if (n < a.N) {
+      const float* gr = a.G0 + r * a.K0p + 1;
+      const float* dw = a.dW + r * a.d;
+      const float f = sc * rn;
+      for (int i = lane; i < a.d; i += 32) {
+        const float z = sig(a.problem, xr[i], gr[i]);
+        gb[1 + i] = sig(a.problem, xr[i], f * (fmaf(zc, z, zc0) - dw[i]));
+      }
+    } else {
+      for (int i = lane; i < a.d; i += 32) gb[1 + i] = 0.0f;
+      if (lane == 0) a.Rstore[m] = rn;
+    }
+  }
+  // block reduction of Σ r² (lane 0 of each warp holds a partial)
+  __shared__ double red[NTH / 32];
+  if (lane == 0) red[threadIdx.x >> 5] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+    if (s != 0.0) atomicAdd(a.loss_acc, s);
+  }
+}
+
+// ā_L = (s̄_L + ū v) ⊙ s'_L (and h̄_L = ū v for a residual last layer)
+__global__ void k_sh_abar_last(ShArgs a, const float* Sb, const float* S, float* Ab, float* Hb) {
+  const int64_t R = (int64_t)(a.N + 1) * a.M, tot = R * a.w;
+  const float* v = a.params + a.off_v;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < tot;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = id / a.w;
+    const int j = (int)(id - r * a.w);
+    const float hb = a.ub[r] * __ldg(v + j);
+    if (Hb) Hb[id] = hb;
+    const float s = S[id];
+    Ab[id] = (Sb[id] + hb) * (1.0f - s * s);
+  }
+}
+
+// Y0 = u(0, X_0): one CTA evaluates the network at one point.
+__global__ void k_sh_point(ShArgs a, float* out) {
+  extern __shared__ float hbuf[];                 // [2][max(K0p, w)]
+  const int W = a.w, ldh = a.K0p > W ? a.K0p : W;
+  float* h0 = hbuf;
+  float* h1 = hbuf + ldh;
+  for (int i = threadIdx.x; i < a.K0p; i += blockDim.x) h0[i] = (i == 0 || i > a.d) ? 0.0f : a.x0;
+  __syncthreads();
+  int K = a.d + 1;
+  for (int k = 0; k < a.L; ++k) {
+    const float* Wk = a.params + a.off_W[k];
+    const float* bk = Wk + (int64_t)W * K;
+    for (int j = threadIdx.x; j < W; j += blockDim.x) {
+      float acc = bk[j];
+      for (int i = 0; i < K; ++i) acc = fmaf(Wk[(int64_t)j * K + i], h0[i], acc);
+      const float s = tanhf(acc);
+      h1[j] = (a.arch == 1 && k > 0) ? h0[j] + s : s;
+    }
+    __syncthreads();
+    float* tmp = h0; h0 = h1; h1 = tmp;
+    K = W;
+    __syncthreads();
+  }
+  float p = 0.0f;
+  for (int j = threadIdx.x; j < W; j += blockDim.x) p = fmaf(h0[j], a.params[a.off_v + j], p);
+  p = warp_sum(p);
+  __shared__ float red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = a.params[a.off_v + W];
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+    *out = s;
+  }
+}
+
+__global__ void k_sh_init(float* params, ShArgs a, uint32_t k0, uint32_t k1) {
+  // R23: Xavier-uniform W_k (tensor 1 + k), v (tensor 1 + L), zero biases, c ~ U(0,1) (tensor 0)
+  const int64_t total = a.off_v + a.w + 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t tid = 0, idx = 0;
+    int fan_in = 0, fan_out = 0;
+    bool weight = false, bias = false;
+    if (i >= a.off_v) {
+      if (i == a.off_v + a.w) { tid = 0; idx = 0; }
+      else { tid = 1 + a.L; idx = (uint32_t)(i - a.off_v); fan_in = a.w; fan_out = 1; weight = true; }
+    } else {
+      int k = a.L - 1;
+      while (i < a.off_W[k]) --k;
+      const int K = k == 0 ? a.d + 1 : a.w;
+      const int64_t r = i - a.off_W[k];
+      if (r < (int64_t)a.w * K) { tid = 1 + k; idx = (uint32_t)r; fan_in = K; fan_out = a.w; weight = true; }
+      else bias = true;
+    }
+    if (bias) { params[i] = 0.0f; continue; }
+    const uint4 x = philox4x32_10(make_uint4(idx >> 2, tid, 0u, kInitStream), k0, k1);
+    const uint32_t sel = (idx & 3) == 0 ? x.x : (idx & 3) == 1 ? x.y : (idx & 3) == 2 ? x.z : x.w;
+    const float u = unit_from_u32(sel);
+    params[i] = weight ? sqrtf(6.0f / (float)(fan_in + fan_out)) * (2.0f * u - 1.0f) : u;
+  }
+}
+
+int grid_for(int64_t work, int per_block) {
+  int64_t g = (work + per_block - 1) / per_block;
+  return (int)(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
+}
+
+template <bool NT, class Epi>
+cudaError_t gemm_rows(const float* A, int lda, const float* B, int ldb, int R, int NC, int K,
+                      const Epi& epi, cudaStream_t s) {
+  dim3 grid((NC + TB - 1) / TB, (R + TB - 1) / TB);
+  k_gemm_rows<NT, Epi><<<grid, NTH, 0, s>>>(A, lda, B, ldb, R, NC, K, epi);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_tn(const float* A, int lda, const float* B, int ldb, const float* A2, int lda2,
+                    const float* B2, int ldb2, int R, int P, int Q, float* C, int ldc,
+                    cudaStream_t s) {
+  const int tiles = ((P + TB - 1) / TB) * ((Q + TB - 1) / TB);
+  int splits = (2 * 148 + tiles - 1) / tiles;
+  const int max_splits = (R + 4 * TK - 1) / (4 * TK);   // >= 64 rows per split
+  if (splits > max_splits) splits = max_splits;
+  if (splits < 1) splits = 1;
+  int rows = (R + splits - 1) / splits;
+  rows = (rows + TK - 1) / TK * TK;
+  splits = (R + rows - 1) / rows;
+  dim3 grid((Q + TB - 1) / TB, (P + TB - 1) / TB, splits);
+  k_gemm_tn<<<grid, NTH, 0, s>>>(A, lda, B, ldb, A2, lda2, B2, ldb2, R, P, Q, C, ldc, rows);
+  return cudaGetLastError();
+}
+
+cudaError_t colsum(const float* X, int ldx, const float* sv, const float* Y, int ldy, int R, int NC,
+                   float* out, cudaStream_t s) {
+  const int cb = (NC + 31) / 32;
+  int rb = (2 * 148 + cb - 1) / cb;
+  int rows = (R + rb - 1) / rb;
+  if (rows < 64) rows = 64;
+  rb = (R + rows - 1) / rows;
+  k_colsum<<<dim3(cb, rb), NTH, 0, s>>>(X, ldx, sv, Y, ldy, R, NC, rows, out);
+  return cudaGetLastError();
+}
+
+#define RET(x)                                \
+  do {                                        \
+    cudaError_t e_ = (x);                     \
+    if (e_ != cudaSuccess) return e_;         \
+  } while (0)
+
+}  // namespace
+
+size_t shared_num_params(int d, int w, int L) {
+  return (size_t)w * (d + 1) + w + (size_t)(L - 1) * ((size_t)w * w + w) + w + 1;
+}
+
+void shared_offsets(ShArgs& a) {
+  int64_t off = 0;
+  for (int k = 0; k < a.L; ++k) {
+    a.off_W[k] = off;
+    const int K = k == 0 ? a.d + 1 : a.w;
+    off += (int64_t)a.w * K + a.w;
+  }
+  a.off_v = off;
+}
+
+// Device buffers for R_max = (N_max + 1)·M rows.
+size_t shared_buffer_bytes(int d, int w, int L, int arch, int N_max, int64_t M) {
+  const int64_t R = (int64_t)(N_max + 1) * M;
+  const int K0p = (d + 1 + 3) & ~3;
+  size_t f = 0;
+  f += (size_t)R * K0p * 3;                 // U0, G0, G0b
+  f += (size_t)N_max * M * d;               // ΔW
+  f += (size_t)R * w * (size_t)L * 2;       // S_k, δ_k
+  f += (size_t)R * w * (size_t)(L - 1);     // g_1..g_{L-1}
+  if (arch == 1) f += (size_t)R * w * (size_t)(L - 1);   // H_k, k ≥ 2
+  f += (size_t)R * w * (size_t)L;           // s̄_k
+  f += (size_t)R * w * 4;                   // ḡ ping-pong, ā ping-pong
+  if (arch == 1) f += (size_t)R * w * 2;    // h̄ ping-pong
+  f += (size_t)R * 6;                       // u, ū, q[4]
+  return f * sizeof(float) + 256 * 64;
+}
+
+void shared_carve(ShArgs& a, void* base, int N_max) {
+  const int64_t R = (int64_t)(N_max + 1) * a.M;
+  float* p = static_cast<float*>(base);
+  auto take = [&](size_t n) { float* q = p; p += (n + 63) & ~(size_t)63; return q; };
+  a.U0 = take((size_t)R * a.K0p);
+  a.G0 = take((size_t)R * a.K0p);
+  a.G0b = take((size_t)R * a.K0p);
+  a.dW = take((size_t)N_max * a.M * a.d);
+  for (int k = 0; k < a.L; ++k) {
+    a.S[k] = take((size_t)R * a.w);
+    a.D[k] = take((size_t)R * a.w);
+    a.Sb[k] = take((size_t)R * a.w);
+    a.G[k] = k < a.L - 1 ? take((size_t)R * a.w) : nullptr;
+    a.H[k] = (a.arch == 1 && k > 0) ? take((size_t)R * a.w) : a.S[k];
+  }
+  a.HL = a.H[a.L - 1];
+  a.Gb[0] = take((size_t)R * a.w);
+  a.Gb[1] = take((size_t)R * a.w);
+  a.Ab[0] = take((size_t)R * a.w);
+  a.Ab[1] = take((size_t)R * a.w);
+  if (a.arch == 1) {
+    a.Hb[0] = take((size_t)R * a.w);
+    a.Hb[1] = take((size_t)R * a.w);
+  } else {
+    a.Hb[0] = a.Hb[1] = nullptr;
+  }
+  a.u = take((size_t)R);
+  a.ub = take((size_t)R);
+  a.q = take((size_t)R * 4);
+}
+
+cudaError_t launch_shared_init(float* params, const ShArgs& a, uint32_t k0, uint32_t k1,
+                               cudaStream_t s) {
+  k_sh_init<<<grid_for(a.off_v + a.w + 1, NTH), NTH, 0, s>>>(params, a, k0, k1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shared_point(const ShArgs& a, float* out, cudaStream_t s) {
+  const int ldh = a.K0p > a.w ? a.K0p : a.w;
+  k_sh_point<<<1, 256, 2 * ldh * sizeof(float), s>>>(a, out);
+  return cudaGetLastError();
+}
+
+// One iteration's forward, loss and (unless a.eval) gradient into a.grad.
+// mid (optional) is recorded between the loss and the double-backward pass.
+// Returns the number of kernels launched in *launches.
+cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid, int* launches) {
+  const int R = (a.N + 1) * (int)a.M;
+  const int W = a.w, K0 = a.d + 1, L = a.L;
+  const bool res = a.arch == 1;
+  const float* P = a.params;
+  int nl = 0;
+  auto Wk = [&](int k) { return P + a.off_W[k]; };                    // layer k+1 (0-based k)
+  auto bk = [&](int k) { return P + a.off_W[k] + (int64_t)W * (k == 0 ? K0 : W); };
+  const float* v = P + a.off_v;
+  // paths
+  k_sh_paths<<<grid_for(a.M * ((a.d + 3) / 4), NTH), NTH, 0, s>>>(a);
+  RET(cudaGetLastError());
+  ++nl;
+  // forward: layers 1..L (0-based k)
+  for (int k = 0; k < L; ++k) {
+    EpiFwd e{bk(k), a.S[k], a.H[k], k > 0 ? a.H[k - 1] : nullptr, k == L - 1 ? v : nullptr,
+             a.D[L - 1], W};
+    const float* A = k == 0 ? a.U0 : a.H[k - 1];
+    const int lda = k == 0 ? a.K0p : W, K = k == 0 ? K0 : W;
+    RET(gemm_rows<true>(A, lda, Wk(k), K, R, W, K, e, s));
+    ++nl;
+  }
+  // input gradient: g_{k-1} = δ_k W_k (+ g_k), k = L..2, then g_0 = δ_1 W_1
+  for (int k = L - 1; k >= 1; --k) {
+    const float* gk = res ? (k == L - 1 ? v : a.G[k]) : nullptr;
+    EpiIg e{gk, (res && k == L - 1) ? 1 : 0, a.G[k - 1], a.S[k - 1], a.D[k - 1], W};
+    RET(gemm_rows<false>(a.D[k], W, Wk(k), W, R, W, W, e, s));
+    ++nl;
+  }
+  {
+    EpiIg e{nullptr, 0, a.G0, nullptr, nullptr, a.K0p};
+    RET(gemm_rows<false>(a.D[0], W, Wk(0), K0, R, K0, W, e, s));
+    ++nl;
+  }
+  // per-row scalars and the loss
+  k_sh_rowscal<<<grid_for((int64_t)R * 32, NTH), NTH, 0, s>>>(a);
+  RET(cudaGetLastError());
+  k_sh_loss<<<grid_for((int64_t)R * 32, NTH), NTH, 0, s>>>(a);
+  RET(cudaGetLastError());
+  nl += 2;
+  if (mid) cudaEventRecord(mid, s);
+  if (a.eval) { if (launches) *launches = nl; return cudaSuccess; }
+  float* G = a.grad;
+  auto gW = [&](int k) { return G + a.off_W[k]; };
+  auto gb = [&](int k) { return G + a.off_W[k] + (int64_t)W * (k == 0 ? K0 : W); };
+  float* gv = G + a.off_v;
+  // up: k = 1..L (0-based 0..L-1): W̄_k += δ_kᵀ ḡ_{k-1}; δ̄_k = ḡ_{k-1} W_kᵀ -> ḡ_k, s̄_k
+  const float* gprev = a.G0b;
+  int ldprev = a.K0p;
+  for (int k = 0; k < L; ++k) {
+    const int K = k == 0 ? K0 : W;
+    RET(gemm_tn(a.D[k], W, gprev, ldprev, nullptr, 0, nullptr, 0, R, W, K, gW(k), K, s));
+    float* gout = a.Gb[k & 1];
+    EpiUp e{a.S[k], k < L - 1 ? a.G[k] : nullptr, v, (res && k > 0) ? gprev : nullptr, gout,
+            a.Sb[k], W};
+    RET(gemm_rows<true>(gprev, ldprev, Wk(k), K, R, W, K, e, s));
+    nl += 2;
+    gprev = gout;
+    ldprev = W;
+  }
+  // head: v̄ = Σ (ḡ_L + ū h_L), c̄ = Σ ū
+  RET(colsum(gprev, W, a.ub, a.HL, W, R, W, gv, s));
+  RET(colsum(a.ub, 1, nullptr, nullptr, 0, R, 1, gv + W, s));
+  nl += 2;
+  // down: ā_L, then k = L..1: W̄_k += ā_kᵀ h_{k-1}, b̄_k += Σ ā_k, ā_{k-1} = (s̄_{k-1} + ā_k W_k (+ h̄_k)) ⊙ s'
+  int cur = 0;
+  k_sh_abar_last<<<grid_for((int64_t)R * W, NTH), NTH, 0, s>>>(
+      a, a.Sb[L - 1], a.S[L - 1], a.Ab[cur], res ? a.Hb[cur] : nullptr);
+  RET(cudaGetLastError());
+  ++nl;
+  for (int k = L - 1; k >= 0; --k) {
+    const float* hin = k == 0 ? a.U0 : a.H[k - 1];
+    const int K = k == 0 ? K0 : W, ldh = k == 0 ? a.K0p : W;
+    RET(gemm_tn(a.Ab[cur], W, hin, ldh, nullptr, 0, nullptr, 0, R, W, K, gW(k), K, s));
+    RET(colsum(a.Ab[cur], W, nullptr, nullptr, 0, R, W, gb(k), s));
+    nl += 2;
+    if (k == 0) break;
+    const int nxt = cur ^ 1;
+    EpiDown e{(res && k > 0) ? a.Hb[cur] : nullptr, (res && k - 1 > 0) ? a.Hb[nxt] : nullptr,
+              a.Sb[k - 1], a.S[k - 1], a.Ab[nxt], W};
+    RET(gemm_rows<false>(a.Ab[cur], W, Wk(k), W, R, W, W, e, s));
+    ++nl;
+    cur = nxt;
+  }
+  if (launches) *launches = nl;
+  return cudaSuccess;
+}
+
+}  // namespace bsde

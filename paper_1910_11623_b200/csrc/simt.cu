@@ -25,7 +25,6 @@ namespace {
 constexpr int TP = 64;     // paths per tile
 constexpr int NT = 256;    // threads per CTA
 constexpr int LDW = 128;   // row pitch of the packed weight images (floats)
-constexpr float kSqrt2 = 1.41421356237309515f;
 
 struct Pack {
   int d, w;

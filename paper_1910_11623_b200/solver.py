@@ -11,6 +11,8 @@ import numpy as np
 from . import _lib
 from ._lib import BSDEError
 
+FORMULATIONS = {"per_step": 0, "shared": 1}
+ARCHS = {"fc": 0, "resnet": 1}
 PROBLEMS = {"heat": _lib.HEAT, "hjb": _lib.HJB, "allen_cahn": _lib.ALLEN_CAHN,
             "black_scholes": _lib.BLACK_SCHOLES}
 PRECISIONS = {"fp32": _lib.FP32, "bf16": _lib.BF16}
@@ -51,11 +53,14 @@ class BSDE:
     def __init__(self, problem, d, N, T, width, batch, *, lr=1e-2, seed=0, precision="fp32",
                  kernel="auto", x0=0.0, lam=1.0, prolong="copy", max_levels=0, device=0,
                  stream=None, rank=0, world=1, nccl_id=None, use_graph=True, beta1=0.9,
-                 beta2=0.999, eps=1e-8, zero_head=None, coupled_paths=False):
+                 beta2=0.999, eps=1e-8, zero_head=None, coupled_paths=False,
+                 formulation="per_step", arch="fc", layers=4):
         """stream: a torch.cuda.Stream, a raw cudaStream_t (int), or None (a new
         torch stream on `device`, kept in self.stream).  zero_head: R7b, defaults
         to True for Allen-Cahn.  coupled_paths: every level draws the finest grid's
-        (N·2^max_levels) Brownian path, summed per coarse step (NEXT-3)."""
+        (N·2^max_levels) Brownian path, summed per coarse step (NEXT-3).
+        formulation="shared": the paper's own method (one tanh network u(t, x) of
+        `layers` layers of `width`, arch "fc" | "resnet", Eq. 6 loss; NEXT-1)."""
         L = _lib.lib()
         cfg = _lib.Config()
         L.bsde_config_default(ctypes.byref(cfg))
@@ -87,12 +92,16 @@ class BSDE:
         cfg.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p) if nccl_id else None
         cfg.use_graph = int(bool(use_graph))
         cfg.coupled_paths = int(bool(coupled_paths))
+        cfg.formulation = FORMULATIONS[formulation]
+        cfg.arch = ARCHS[arch]
+        self.formulation, self.arch, self.layers = formulation, arch, int(layers)
         self.problem = PROBLEMS[problem] if isinstance(problem, str) else int(problem)
         self.d, self.w, self.T, self.batch = int(d), int(width), float(T), int(batch)
         self.rank, self.world = int(rank), int(world)
-        widths = (ctypes.c_int * 2)(int(width), int(width))
+        nw = self.layers if formulation == "shared" else 2
+        widths = (ctypes.c_int * nw)(*([int(width)] * nw))
         h = ctypes.c_void_p()
-        rc = L.bsde_create(self.problem, self.d, int(N), self.T, widths, 2, ctypes.byref(cfg),
+        rc = L.bsde_create(self.problem, self.d, int(N), self.T, widths, nw, ctypes.byref(cfg),
                            ctypes.byref(h))
         if rc:
             raise BSDEError(rc, L.bsde_last_error(None).decode())

@@ -1,0 +1,143 @@
+"""The paper's own formulation on the GPU (shared.cu) against
+oracle/shared.py: one tanh network u(t, x) for all steps, Eq. 6 residual loss,
+reverse-over-reverse gradient.  fp32 kernels: north-star tolerance 1e-4."""
+import numpy as np
+import pytest
+
+from oracle import bsde as ob, philox, shared as osh
+from parity_util import PROBLEM
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1910_11623_b200 import build
+    build.build()
+
+
+def make(problem, d, w, L, N, T, B, **kw):
+    from paper_1910_11623_b200 import BSDE
+    return BSDE(problem, d, N, T, w, B, formulation="shared", layers=L, **kw)
+
+
+def perturb(s, seed, scale=0.05):
+    p = s.get_params()
+    p += (scale * np.random.default_rng(seed).standard_normal(p.size)).astype(np.float32)
+    s.set_params(p)
+    return p
+
+
+def check_grad(g, ref, tol=TOL):
+    err = np.linalg.norm(g - ref) / np.linalg.norm(ref)
+    assert err <= tol, err
+    assert np.max(np.abs(g - ref)) <= 4 * tol * np.max(np.abs(ref))
+
+
+def test_init_matches_oracle():
+    d, w, L = 10, 32, 3
+    s = make("heat", d, w, L, 4, 1.0, 64, seed=5)
+    assert s.family == "shared-simt" and s.num_params() == osh.num_params(d, w, L)
+    ref = osh.init_params(5, d, w, L)
+    assert np.max(np.abs(s.get_params() - ref)) <= 1e-6 * np.max(np.abs(ref))
+
+
+CASES = [("heat", "fc", 0.0), ("hjb", "fc", 0.0), ("allen_cahn", "fc", 0.0),
+         ("black_scholes", "fc", 0.5), ("hjb", "resnet", 0.0), ("black_scholes", "resnet", 0.5)]
+
+
+@pytest.mark.parametrize("problem,arch,x0", CASES)
+def test_teacher_forced_gradient(problem, arch, x0):
+    """Loss and the full reverse-over-reverse gradient at a perturbed parameter
+    point, ragged sizes (d + 1 = 38 inputs, 101 paths, 6 steps)."""
+    d, w, L, N, T, B = 37, 48, 3, 6, 0.5, 101
+    s = make(problem, d, w, L, N, T, B, arch=arch, x0=x0, lr=1e-3)
+    p = perturb(s, 1)
+    for it in (0, 4):
+        s.iteration = it
+        loss = s.compute_grad()
+        ref = osh.iteration(PROBLEM[problem], d, w, L, osh.RESNET if arch == "resnet" else osh.FC,
+                            N, T, p.astype(np.float64), 0, it, np.arange(B), B, x0=x0)
+        assert abs(loss - ref["loss"]) <= TOL * ref["loss"], (loss, ref["loss"])
+        check_grad(s.get_grads(), ref["grad"])
+        R = s.debug_residuals(0, B)
+        assert np.max(np.abs(R - ref["r"][N])) <= TOL * np.max(np.abs(ref["r"][N]))
+
+
+def test_paper_workload_gradient_adam_and_y0():
+    """The paper's Table 1 workload: Black-Scholes d = 100, M = 100
+    paths, N = 50 steps, 4 tanh layers of 256, Adam lr 1e-3; X_0 = 0.1·1 (R21)."""
+    d, w, L, N, T, B, x0 = 100, 256, 4, 50, 1.0, 100, 0.1
+    s = make("black_scholes", d, w, L, N, T, B, x0=x0, lr=1e-3)
+    p = s.get_params().astype(np.float64)
+    loss = s.compute_grad()
+    ref = osh.iteration(ob.BLACK_SCHOLES, d, w, L, osh.FC, N, T, p, 0, 0, np.arange(B), B, x0=x0)
+    assert abs(loss - ref["loss"]) <= TOL * ref["loss"]
+    g = s.get_grads()
+    check_grad(g, ref["grad"])
+    assert abs(s.y0() - osh.u0(p, d, w, L, osh.FC, x0)) <= 1e-5
+    # one Adam step from these gradients
+    s.train_step()
+    st = ob.AdamState(p.size)
+    q = p.copy()
+    ob.adam_step(q, s.get_grads().astype(np.float64), st, 1e-3)
+    assert np.max(np.abs(s.get_params() - q)) <= 1e-8 + 1e-6 * np.max(np.abs(q))
+
+
+def test_prolongate_keeps_network_and_doubles_steps():
+    d, w, L, N, T, B = 8, 32, 2, 3, 1.0, 64
+    s = make("hjb", d, w, L, N, T, B, max_levels=2)
+    p = perturb(s, 3)
+    s.train_step()
+    q = s.get_params()
+    s.prolongate(1)
+    assert s.N == 2 * N and np.array_equal(s.get_params(), q)
+    m, v, t = s.get_adam_state()
+    assert t == 0 and not m.any() and not v.any()
+    loss = s.compute_grad()
+    ref = osh.iteration(ob.HJB, d, w, L, osh.FC, 2 * N, T, q.astype(np.float64), 0, s.iteration,
+                        np.arange(B), B)
+    assert abs(loss - ref["loss"]) <= TOL * ref["loss"]
+    check_grad(s.get_grads(), ref["grad"])
+
+
+def test_coupled_paths_shared():
+    """Coupled multilevel paths (R22) with the shared network: level N = 2 of a
+    N_fine = 8 grid uses sums of 4 fine increments."""
+    d, w, L, N, T, B = 6, 16, 2, 2, 1.0, 50
+    s = make("black_scholes", d, w, L, N, T, B, max_levels=2, coupled_paths=True, x0=0.8)
+    p = perturb(s, 4)
+    loss = s.compute_grad()
+    # the oracle's shared iteration with coupled increments: rebuild its paths
+    m = np.arange(B)
+    X = [np.full((B, d), 0.8)]
+    for n in range(N):
+        X.append(ob.forward_step(ob.BLACK_SCHOLES, X[-1],
+                                 philox.coupled_increments(0, 0, n, m, d, T / N, 4)))
+    R = s.debug_residuals(0, B)
+    u_N = osh.forward(p.astype(np.float64), d, w, L, osh.FC, np.full(B, T), X[N])[0]
+    assert np.max(np.abs(R - (u_N - np.sum(X[N] ** 2, axis=1)))) <= 1e-4 * np.max(np.abs(R))
+    assert np.isfinite(loss)
+
+
+def test_eval_loss_matches_oracle():
+    d, w, L, N, T = 12, 32, 3, 4, 0.3
+    s = make("allen_cahn", d, w, L, N, T, 256)
+    p = perturb(s, 2).astype(np.float64)
+    got = s.eval_loss(3, 200)
+    ref = osh.iteration(ob.ALLEN_CAHN, d, w, L, osh.FC, N, T, p, 0, philox.EVAL_BIT | 3,
+                        np.arange(200), 200, want_grad=False)
+    assert abs(got - ref["loss"]) <= TOL * ref["loss"]
+
+
+def test_training_descends():
+    """Black-Scholes d = 100 with the paper's network: 300 Adam steps (lr 1e-3) on
+    the shared formulation reduce the loss several-fold."""
+    s = make("black_scholes", 100, 256, 4, 20, 1.0, 256, x0=0.1, lr=1e-3)
+    losses = [s.train_step() for _ in range(300)]
+    assert np.all(np.isfinite(losses))
+    assert np.mean(losses[-20:]) < 0.2 * np.mean(losses[:5])
