@@ -40,6 +40,33 @@ def bwd_flops(d, w):
     return 6 * d * w + 4 * w * w
 
 
+# Shared-network formulation (NEXT-1, R23): per row (path, time point) the forward
+# (K0 = d+1 inputs, L tanh layers of w) and the input gradient each cost
+# 2(K0 w + (L-1) w²); the reverse-over-reverse gradient costs three such passes
+# (δᵀḡ, ḡWᵀ, āᵀh) plus the hidden-state back-propagation 2(L-1)w².  N+1 rows per
+# N path-steps.
+def shared_flops(wl):
+    K0, w, L = wl.d + 1, wl.w, wl.layers
+    one = 2 * (K0 * w + (L - 1) * w * w)
+    rows = (wl.N + 1) / wl.N
+    return rows * 2 * one, rows * (3 * one + 2 * (L - 1) * w * w)   # (fwd + ∇ₓu, gradient)
+
+
+def flops_per_path_step(wl):
+    if wl.formulation == "shared":
+        return shared_flops(wl)
+    return fwd_flops(wl.d, wl.w), bwd_flops(wl.d, wl.w)
+
+
+def shared_row_bytes(wl):
+    K0p = (wl.d + 1 + 3) // 4 * 4
+    L, w = wl.layers, wl.w
+    floats = 3 * K0p + wl.d + w * (2 * L + (L - 1) + L + 4) + 6
+    if wl.arch == "resnet":
+        floats += w * (L - 1 + 2)
+    return 4 * floats
+
+
 def peaks():
     p = {"hbm_gbs": 6558.4, "bf16_tflops": 1675.8, "bf16_tflops_sustained": 1400.3,
          "sm_max_mhz": 1965.0, "source": "fallback"}
@@ -123,14 +150,26 @@ def oracle_rate(wl, paths, iters):
     """The float64 oracle as it stands on a bounded path sample; path-steps/s."""
     from threadpoolctl import threadpool_info
     from oracle import bsde as ob
+    from oracle import shared as osh
     prob = ob.PROBLEM_NAMES[wl.problem]
-    p = ob.init_params(wl.seed, wl.d, wl.w, wl.N)
+    if wl.formulation == "shared":
+        arch = osh.RESNET if wl.arch == "resnet" else osh.FC
+        p = osh.init_params(wl.seed, wl.d, wl.w, wl.layers)
+
+        def one(k):
+            return osh.iteration(prob, wl.d, wl.w, wl.layers, arch, wl.N, wl.T, p, wl.seed, k,
+                                 np.arange(paths), wl.batch, x0=wl.x0)
+    else:
+        p = ob.init_params(wl.seed, wl.d, wl.w, wl.N)
+
+        def one(k):
+            return ob.iteration(prob, wl.d, wl.w, wl.N, wl.T, p, wl.seed, k, np.arange(paths),
+                                wl.batch, x0=wl.x0)
     st = ob.AdamState(p.size)
     times = []
     for k in range(iters):
         t0 = time.perf_counter()
-        r = ob.iteration(prob, wl.d, wl.w, wl.N, wl.T, p, wl.seed, k, np.arange(paths), wl.batch,
-                         x0=wl.x0)
+        r = one(k)
         ob.adam_step(p, r["grad"], st, wl.lr, loss=r["loss"])
         times.append(time.perf_counter() - t0)
     threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
@@ -158,11 +197,19 @@ def run_reference(args, wl, rank):
 
 
 def config_dict(wl, gpus, family):
-    return {"workload": wl.name, "problem": wl.problem, "d": wl.d, "w": wl.w, "N": wl.N,
-            "T": wl.T, "batch_global": wl.batch, "precision": wl.precision, "kernel": family,
-            "parallelism": "dp%d" % gpus,
-            "l2": "inputs larger than L2: per-step X_n store (N*B*d*4 bytes) >> 126 MB; "
-                  "no explicit flush"}
+    c = {"workload": wl.name, "problem": wl.problem, "d": wl.d, "w": wl.w, "N": wl.N,
+         "T": wl.T, "batch_global": wl.batch, "precision": wl.precision, "kernel": family,
+         "parallelism": "dp%d" % gpus, "formulation": wl.formulation}
+    if wl.formulation == "shared":
+        c.update({"arch": wl.arch, "layers": wl.layers, "x0": wl.x0})
+        ws = (wl.N + 1) * wl.batch // gpus * shared_row_bytes(wl) / 2 ** 20
+        c["l2"] = ("working set %.0f MiB per GPU; %s" % (ws, "L2 flushed between timed steps "
+                   "(256 MiB memset outside the per-step events)" if ws < 256 else
+                   "larger than L2, no explicit flush"))
+    else:
+        c["l2"] = ("inputs larger than L2: per-step X_n store (N*B*d*4 bytes) >> 126 MB; "
+                   "no explicit flush")
+    return c
 
 
 def main():
@@ -198,6 +245,8 @@ def main():
 
     kw = dict(lr=wl.lr, precision=wl.precision, kernel=args.kernel, seed=wl.seed,
               device=local_rank, x0=wl.x0)
+    if wl.formulation == "shared":
+        kw.update(formulation="shared", arch=wl.arch, layers=wl.layers)
     if world > 1:
         s = BSDE.distributed(wl.problem, wl.d, wl.N, wl.T, wl.w, wl.batch, **kw)
     else:
@@ -217,14 +266,29 @@ def main():
                           os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local_rank])
     clocks.start()
     time.sleep(0.3)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush = None
+    if wl.formulation == "shared" and (wl.N + 1) * wl.batch // world * shared_row_bytes(wl) < 2 ** 28:
+        flush = torch.empty(2 ** 26, dtype=torch.float32, device="cuda")   # 256 MiB > L2
     barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        s.train_step(sync=False)
-    e1.record(stream)
-    barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            s.train_step(sync=False)
+        e1.record(stream)
+        barrier()
+        ms = e0.elapsed_time(e1) / args.steps
+    else:   # working set < L2: flush between steps, time each step with its own events
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        with torch.cuda.stream(stream):
+            for a0, a1 in evs:
+                flush.fill_(1.0)
+                a0.record(stream)
+                s.train_step(sync=False)
+                a1.record(stream)
+        barrier()
+        ms = sum(a0.elapsed_time(a1) for a0, a1 in evs) / args.steps
     clk = clocks.stop()
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
@@ -269,9 +333,10 @@ def main():
                 traffic, traffic_src = tr["bytes_per_launch"], "profiles/" + tr["source"]
         except Exception:
             pass
-        flops = B_local * wl.N * (bwd_flops(wl.d, wl.w) if dom == "bwd" else fwd_flops(wl.d, wl.w))
+        ffw, fbw = flops_per_path_step(wl)
+        flops = B_local * wl.N * (fbw if dom == "bwd" else ffw)
         achieved = flops / (phase[dom] * 1e-3) / 1e12
-        step_flops = wl.batch * wl.N * (fwd_flops(wl.d, wl.w) + bwd_flops(wl.d, wl.w)) / world
+        step_flops = wl.batch * wl.N * (ffw + fbw) / world
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
@@ -283,11 +348,10 @@ def main():
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": pk_name + "; " + pk["source"],
-                         "algorithmic_flop_per_path_step": bwd_flops(wl.d, wl.w) if dom == "bwd"
-                         else fwd_flops(wl.d, wl.w)},
+                         "algorithmic_flop_per_path_step": fbw if dom == "bwd" else ffw},
             "step_roofline": {"achieved_tflops": step_flops / (ms * 1e-3) / 1e12,
                               "frac": step_flops / (ms * 1e-3) / 1e12 / peak,
-                              "flop_per_path_step": fwd_flops(wl.d, wl.w) + bwd_flops(wl.d, wl.w)},
+                              "flop_per_path_step": ffw + fbw},
             "phase_ms": phase,
             "gpu_launches": launches * args.steps,
             "clocks": clk,
@@ -297,6 +361,13 @@ def main():
                             "synchronised every step; the step's inputs are Philox counters "
                             "held on the device (no host input data exists, R8)"},
         }
+        if wl.name == "nx1_shared_bs_paper":
+            # the paper's own timing of this workload: context only
+            line["paper_context"] = {
+                "solution_time_min": 59.0, "hardware": "Tesla T4 (PyTorch)",
+                "iterations": wl.iterations, "derived_path_steps_per_s": 2.8e4,
+                "ours_solution_time_min": ms * wl.iterations / 6e4,
+                "source": "BASELINE.md section 1; PAPER.md:488 (single-level, fully connected)"}
         if not args.no_cpu_baseline and world == 1:
             paths = max(256, min(wl.batch, int(2.4e5 // wl.N)))
             rate, threads, _ = oracle_rate(wl, paths, 2)

@@ -22,8 +22,10 @@
 //             hÃÑ_{k-1} = ƒÅ_k W_k (+ hÃÑ_k)                                   NN + TN GEMMs
 //   head      vÃÑ = Œ£ (·∏°_L + ≈´ h_L), cÃÑ = Œ£ ≈´
 //
-// fp32 throughout (the paper's PyTorch precision); SIMT FFMA GEMM
-// tiles 64√ó64√ó16 with 4√ó4 register tiles per thread.
+// fp32 throughout (the paper's PyTorch precision); SIMT FFMA GEMMs:
+// 128√ó128√ó8 tiles with 8√ó8 register tiles per thread (double-buffered smem) when
+// the grid fills ‚â• 2 waves, else 64√ó64√ó16 with 4√ó4; weight gradients split the
+// row reduction over CTAs (fp32 atomics) and fold the bias sums in.
 #include "kernels.cuh"
 
 namespace bsde {
@@ -38,94 +40,69 @@ template <bool NT, class Epi>
 __global__ void __launch_bounds__(NTH) k_gemm_rows(const float* __restrict__ A, int lda,
                                                    const float* __restrict__ B, int ldb, int R,
                                                    int NC, int K, Epi epi) {
-  __shared__ __align__(16) float As[TK][TB + 4];
-  __shared__ __align__(16) float Bs[TK][TB + 4];
+  __shared__ __align__(16) float As[2][TK][TB + 4];
+  __shared__ __align__(16) float Bs[2][TK][TB + 4];
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
   const int i0 = blockIdx.y * TB, j0 = blockIdx.x * TB;
-  float acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += TK) {
+  float ra[4], rb[4];   // the next k-tile, in registers while the current one is used
+  auto load = [&](int k0) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int idx = t + NTH * e, ii = idx >> 4, kk = idx & 15;
       const int i = i0 + ii, k = k0 + kk;
-      As[kk][ii] = (i < R && k < K) ? __ldg(A + (int64_t)i * lda + k) : 0.0f;
+      ra[e] = (i < R && k < K) ? __ldg(A + (int64_t)i * lda + k) : 0.0f;
       if (NT) {
         const int j = j0 + ii;
-        Bs[kk][ii] = (j < NC && k < K) ? __ldg(B + (int64_t)j * ldb + k) : 0.0f;
+        rb[e] = (j < NC && k < K) ? __ldg(B + (int64_t)j * ldb + k) : 0.0f;
       } else {
         const int kb = idx >> 6, jj = idx & 63, k2 = k0 + kb, j = j0 + jj;
-        Bs[kb][jj] = (k2 < K && j < NC) ? __ldg(B + (int64_t)k2 * ldb + j) : 0.0f;
+        rb[e] = (k2 < K && j < NC) ? __ldg(B + (int64_t)k2 * ldb + j) : 0.0f;
       }
     }
-    __syncthreads();
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = t + NTH * e, ii = idx >> 4, kk = idx & 15;
+      As[buf][kk][ii] = ra[e];
+      if (NT) Bs[buf][kk][ii] = rb[e];
+      else Bs[buf][idx >> 6][idx & 63] = rb[e];
+    }
+  };
+  float acc[4][4] = {};
+  load(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += TK) {
+    const bool more = k0 + TK < K;
+    if (more) load(k0 + TK);
 #pragma unroll
     for (int kk = 0; kk < TK; ++kk) {
-      const float4 a = *reinterpret_cast<const float4*>(&As[kk][4 * ty]);
-      const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][4 * tx]);
+      const float4 a = *reinterpret_cast<const float4*>(&As[buf][kk][4 * ty]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][kk][4 * tx]);
       const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
     }
+    if (more) store(buf ^ 1);
     __syncthreads();
+    buf ^= 1;
   }
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int r = 0; r < 4; ++r) {
+    const int i = i0 + 4 * ty + r, j = j0 + 4 * tx;
+    if (i >= R) continue;
+    if (epi.ld % 4 == 0 && j + 3 < NC) {
+      epi.v4(i, j, make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
+    } else {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = i0 + 4 * ty + r, j = j0 + 4 * tx + c;
-      if (i < R && j < NC) epi(i, j, acc[r][c]);
-    }
-}
-
-// Weight-gradient GEMM over rows: C[p][q] += Œ£_r A[r][p]¬∑B[r][q] (+ A2[r][p]¬∑B2[r][q]),
-// rows split over blockIdx.z, fp32 atomics into C (row-major, ldc).
-__global__ void __launch_bounds__(NTH) k_gemm_tn(const float* __restrict__ A, int lda,
-                                                 const float* __restrict__ B, int ldb,
-                                                 const float* __restrict__ A2, int lda2,
-                                                 const float* __restrict__ B2, int ldb2, int R,
-                                                 int P, int Q, float* __restrict__ C, int ldc,
-                                                 int rows_per_split) {
-  __shared__ __align__(16) float As[TK][TB + 4];
-  __shared__ __align__(16) float Bs[TK][TB + 4];
-  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-  const int p0 = blockIdx.y * TB, q0 = blockIdx.x * TB;
-  const int r_begin = blockIdx.z * rows_per_split;
-  const int r_end = min(R, r_begin + rows_per_split);
-  float acc[4][4] = {};
-  for (int pass = 0; pass < (A2 ? 2 : 1); ++pass) {
-    const float* a_ = pass ? A2 : A;
-    const float* b_ = pass ? B2 : B;
-    const int la = pass ? lda2 : lda, lb = pass ? ldb2 : ldb;
-    for (int r0 = r_begin; r0 < r_end; r0 += TK) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int idx = t + NTH * e, kk = idx >> 6, pp = idx & 63, r = r0 + kk;
-        As[kk][pp] = (r < r_end && p0 + pp < P) ? __ldg(a_ + (int64_t)r * la + p0 + pp) : 0.0f;
-        Bs[kk][pp] = (r < r_end && q0 + pp < Q) ? __ldg(b_ + (int64_t)r * lb + q0 + pp) : 0.0f;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < TK; ++kk) {
-        const float4 a = *reinterpret_cast<const float4*>(&As[kk][4 * ty]);
-        const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][4 * tx]);
-        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
-      }
-      __syncthreads();
+      for (int c = 0; c < 4; ++c)
+        if (j + c < NC) epi(i, j + c, acc[r][c]);
     }
   }
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int p = p0 + 4 * ty + r, q = q0 + 4 * tx + c;
-      if (p < P && q < Q && acc[r][c] != 0.0f) atomicAdd(C + (int64_t)p * ldc + q, acc[r][c]);
-    }
 }
 
 // out[j] += Œ£_r X[r][j] (+ s[r]¬∑Y[r][j]);  blockDim 256 = 8 row lanes √ó 32 columns
@@ -153,7 +130,249 @@ __global__ void __launch_bounds__(NTH) k_colsum(const float* __restrict__ X, int
   }
 }
 
+// 128√ó128 tiles, BK = 8, 8√ó8 outputs per thread as 2√ó2 blocks of 4√ó4 (rows
+// 4ty + {0..3} and 64 + 4ty + {0..3}, the same for columns), smem double
+// buffer filled from registers one k-step ahead.  Used when the grid has at
+// least ~2 waves of such tiles; the 64√ó64 kernel above covers small problems.
+constexpr int BB = 128, BKK = 8;
+
+__device__ __forceinline__ float4 ld4_guard(const float* p, int valid) {
+  // 4 consecutive floats, zero beyond `valid` (0..4); p is 16-byte aligned when valid == 4
+  if (valid >= 4) return __ldg(reinterpret_cast<const float4*>(p));
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid > 0) v.x = __ldg(p);
+  if (valid > 1) v.y = __ldg(p + 1);
+  if (valid > 2) v.z = __ldg(p + 2);
+  return v;
+}
+
+template <class Epi>
+__device__ __forceinline__ void mma8x8_epilogue(const float (&acc)[8][8], int i0, int j0, int tx,
+                                                int ty, int R, int NC, const Epi& epi) {
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
+      const int j = j0 + (c < 4 ? 4 * tx + c : 64 + 4 * tx + c - 4);
+      if (i < R && j < NC) epi(i, j, acc[r][c]);
+    }
+}
+
+// the same with one 4-column call per (row, column group) where the group is whole
+template <class Epi>
+__device__ __forceinline__ void mma8x8_epilogue_v4(const float (&acc)[8][8], int i0, int j0, int tx,
+                                                   int ty, int R, int NC, const Epi& epi) {
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
+    if (i >= R) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = j0 + 64 * h + 4 * tx;
+      if (j + 3 < NC) {
+        epi.v4(i, j, make_float4(acc[r][4 * h], acc[r][4 * h + 1], acc[r][4 * h + 2], acc[r][4 * h + 3]));
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (j + c < NC) epi(i, j + c, acc[r][4 * h + c]);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void mma8x8_step(const float (*As)[BB], const float (*Bs)[BB], int tx,
+                                            int ty, float (&acc)[8][8]) {
+#pragma unroll
+  for (int kk = 0; kk < BKK; ++kk) {
+    const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][4 * ty]);
+    const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][64 + 4 * ty]);
+    const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][4 * tx]);
+    const float4 b1 = *reinterpret_cast<const float4*>(&Bs[kk][64 + 4 * tx]);
+    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
+  }
+}
+
+// Row GEMM, big tiles.  A [R√óK] row-major with lda % 4 == 0 (all activation
+// buffers); B as in k_gemm_rows (any ldb: loaded element-wise, it is a weight
+// matrix that stays in L1/L2).
+template <bool NT, class Epi>
+__global__ void __launch_bounds__(NTH, 2) k_gemm_rows128(const float* __restrict__ A, int lda,
+                                                         const float* __restrict__ B, int ldb,
+                                                         int R, int NC, int K, Epi epi) {
+  __shared__ __align__(16) float As[2][BKK][BB];
+  __shared__ __align__(16) float Bs[2][BKK][BB];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int i0 = blockIdx.y * BB, j0 = blockIdx.x * BB;
+  // A loads: row t/2, k offset 4(t&1);  B loads: NT row (col j) t/2, k 4(t&1);
+  //          NN k = t/32, cols 4(t&31)
+  const int ar = t >> 1, ak = 4 * (t & 1);
+  float4 ra, rb;
+  auto load = [&](int k0) {
+    const int i = i0 + ar, k = k0 + ak;
+    ra = (i < R) ? ld4_guard(A + (int64_t)i * lda + k, K - k) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (NT) {
+      const int j = j0 + ar;
+      if (j >= NC) {
+        rb = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else if (ldb % 4 == 0) {
+        rb = ld4_guard(B + (int64_t)j * ldb + k, K - k);
+      } else {
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (k + e < K) ? __ldg(B + (int64_t)j * ldb + k + e) : 0.f;
+        rb = make_float4(v[0], v[1], v[2], v[3]);
+      }
+    } else {
+      const int kb = k0 + (t >> 5), jb = j0 + 4 * (t & 31);
+      if (kb >= K) {
+        rb = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else if (ldb % 4 == 0) {
+        rb = ld4_guard(B + (int64_t)kb * ldb + jb, NC - jb);
+      } else {
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (jb + e < NC) ? __ldg(B + (int64_t)kb * ldb + jb + e) : 0.f;
+        rb = make_float4(v[0], v[1], v[2], v[3]);
+      }
+    }
+  };
+  auto store = [&](int buf) {
+    As[buf][ak + 0][ar] = ra.x; As[buf][ak + 1][ar] = ra.y;
+    As[buf][ak + 2][ar] = ra.z; As[buf][ak + 3][ar] = ra.w;
+    if (NT) {
+      Bs[buf][ak + 0][ar] = rb.x; Bs[buf][ak + 1][ar] = rb.y;
+      Bs[buf][ak + 2][ar] = rb.z; Bs[buf][ak + 3][ar] = rb.w;
+    } else {
+      *reinterpret_cast<float4*>(&Bs[buf][t >> 5][4 * (t & 31)]) = rb;
+    }
+  };
+  float acc[8][8] = {};
+  load(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += BKK) {
+    const bool more = k0 + BKK < K;
+    if (more) load(k0 + BKK);
+    mma8x8_step(As[buf], Bs[buf], tx, ty, acc);
+    if (more) store(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  if (epi.ld % 4 == 0) mma8x8_epilogue_v4(acc, i0, j0, tx, ty, R, NC, epi);
+  else mma8x8_epilogue(acc, i0, j0, tx, ty, R, NC, epi);
+}
+
+// Weight-gradient GEMM, big tiles: C[p][q] += Œ£_r A[r][p]¬∑B[r][q] over this CTA's
+// row range, fp32 atomics; bias (optional, blockIdx.x == 0 CTAs): += Œ£_r A[r][p].
+// lda, ldb % 4 == 0.
+__global__ void __launch_bounds__(NTH, 2) k_gemm_tn128(const float* __restrict__ A, int lda,
+                                                       const float* __restrict__ B, int ldb, int R,
+                                                       int P, int Q, float* __restrict__ C, int ldc,
+                                                       float* __restrict__ bias, int rows_per_split) {
+  __shared__ __align__(16) float As[2][BKK][BB];
+  __shared__ __align__(16) float Bs[2][BKK][BB];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int p0 = blockIdx.y * BB, q0 = blockIdx.x * BB;
+  const int r_begin = blockIdx.z * rows_per_split, r_end = min(R, r_begin + rows_per_split);
+  const int lk = t >> 5, lc = 4 * (t & 31);
+  float4 ra, rb;
+  auto load = [&](int r0) {
+    const int r = r0 + lk;
+    const bool ok = r < r_end;
+    ra = ok ? ld4_guard(A + (int64_t)r * lda + p0 + lc, P - p0 - lc) : make_float4(0.f, 0.f, 0.f, 0.f);
+    rb = ok ? ld4_guard(B + (int64_t)r * ldb + q0 + lc, Q - q0 - lc) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  auto store = [&](int buf) {
+    *reinterpret_cast<float4*>(&As[buf][lk][lc]) = ra;
+    *reinterpret_cast<float4*>(&Bs[buf][lk][lc]) = rb;
+  };
+  const bool do_bias = bias && blockIdx.x == 0 && t < BB;   // thread t sums column p0 + t
+  float acc[8][8] = {};
+  float bsum = 0.0f;
+  if (r_begin < r_end) {
+    load(r_begin);
+    store(0);
+  }
+  __syncthreads();
+  int buf = 0;
+  for (int r0 = r_begin; r0 < r_end; r0 += BKK) {
+    const bool more = r0 + BKK < r_end;
+    if (more) load(r0 + BKK);
+    mma8x8_step(As[buf], Bs[buf], tx, ty, acc);
+    if (do_bias) {
+#pragma unroll
+      for (int kk = 0; kk < BKK; ++kk) bsum += As[buf][kk][t];
+    }
+    if (more) store(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  struct AtomicEpi {
+    float* C;
+    int ldc;
+    __device__ void operator()(int p, int q, float v) const {
+      if (v != 0.0f) atomicAdd(C + (int64_t)p * ldc + q, v);
+    }
+  };
+  mma8x8_epilogue(acc, p0, q0, tx, ty, P, Q, AtomicEpi{C, ldc});
+  if (do_bias && p0 + t < P && bsum != 0.0f) atomicAdd(bias + p0 + t, bsum);
+}
+
+// out[j] += Œ£_r X[r][j] (+ s[r]¬∑Y[r][j]), 4 columns per thread (ldx, ldy % 4 == 0, NC % 4 == 0):
+// block = 16 column groups (64 columns) √ó 16 row lanes
+__global__ void __launch_bounds__(NTH) k_colsum4(const float* __restrict__ X, int ldx,
+                                                 const float* __restrict__ s,
+                                                 const float* __restrict__ Y, int ldy, int R, int NC,
+                                                 int rows_per_block, float* __restrict__ out) {
+  const int cg = threadIdx.x & 15, lr = threadIdx.x >> 4;
+  const int j = blockIdx.x * 64 + 4 * cg;
+  const int r0 = blockIdx.y * rows_per_block, r1 = min(R, r0 + rows_per_block);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j < NC)
+    for (int r = r0 + lr; r < r1; r += 16) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(X + (int64_t)r * ldx + j));
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+      if (Y) {
+        const float sv = __ldg(s + r);
+        const float4 y = __ldg(reinterpret_cast<const float4*>(Y + (int64_t)r * ldy + j));
+        acc.x = fmaf(sv, y.x, acc.x); acc.y = fmaf(sv, y.y, acc.y);
+        acc.z = fmaf(sv, y.z, acc.z); acc.w = fmaf(sv, y.w, acc.w);
+      }
+    }
+  __shared__ float4 red[16][17];
+  red[lr][cg] = acc;
+  __syncthreads();
+  if (lr == 0 && j < NC) {
+    float4 tot = red[0][cg];
+    for (int k = 1; k < 16; ++k) {
+      tot.x += red[k][cg].x; tot.y += red[k][cg].y; tot.z += red[k][cg].z; tot.w += red[k][cg].w;
+    }
+    atomicAdd(out + j, tot.x);
+    atomicAdd(out + j + 1, tot.y);
+    atomicAdd(out + j + 2, tot.z);
+    atomicAdd(out + j + 3, tot.w);
+  }
+}
+
 // ---------------------------------------------------------------- epilogues
+// Each functor has a scalar form and a 4-column form (j % 4 == 0, ld % 4 == 0,
+// j + 3 < NC) used by the 128-tile kernels: one 16-byte access per array.
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+#define F4MAP(expr)                                                                  \
+  make_float4([&](int e_) { return expr; }(0), [&](int e_) { return expr; }(1),       \
+              [&](int e_) { return expr; }(2), [&](int e_) { return expr; }(3))
+__device__ __forceinline__ float comp(const float4& v, int e) {
+  return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+
 struct EpiFwd {        // layer k: s = tanh(a + b); S_k, H_k (ResNet); Œ¥_L on the last layer
   const float* b;
   float* S;
@@ -168,6 +387,16 @@ struct EpiFwd {        // layer k: s = tanh(a + b); S_k, H_k (ResNet); Œ¥_L on t
     S[o] = s;
     if (H != S) H[o] = Hprev[o] + s;
     if (v) D[o] = __ldg(v + j) * (1.0f - s * s);
+  }
+  __device__ void v4(int i, int j, float4 a) const {
+    const int64_t o = (int64_t)i * ld + j;
+    const float4 s = F4MAP(tanhf(comp(a, e_) + __ldg(b + j + e_)));
+    st4(S + o, s);
+    if (H != S) {
+      const float4 hp = ld4(Hprev + o);
+      st4(H + o, F4MAP(comp(hp, e_) + comp(s, e_)));
+    }
+    if (v) st4(D + o, F4MAP(__ldg(v + j + e_) * (1.0f - comp(s, e_) * comp(s, e_))));
   }
 };
 
@@ -185,6 +414,18 @@ struct EpiIg {         // g_{k-1} = Œ¥_k W_k (+ g_k); Œ¥_{k-1} = g_{k-1} ‚äô (1 
     if (S) {
       const float s = S[o];
       D[o] = c * (1.0f - s * s);
+    }
+  }
+  __device__ void v4(int i, int j, float4 c) const {
+    const int64_t o = (int64_t)i * ld + j;
+    if (gk) {
+      const float4 g = gk_is_v ? F4MAP(__ldg(gk + j + e_)) : ld4(gk + o);
+      c = F4MAP(comp(c, e_) + comp(g, e_));
+    }
+    st4(G + o, c);
+    if (S) {
+      const float4 s = ld4(S + o);
+      st4(D + o, F4MAP(comp(c, e_) * (1.0f - comp(s, e_) * comp(s, e_))));
     }
   }
 };
@@ -206,6 +447,18 @@ struct EpiUp {         // Œ¥ÃÑ_k = ·∏°_{k-1} W_k·µÄ:  ·∏°_k = Œ¥ÃÑ ‚äô s'_k (+ ·
     Gb[o] = gb;
     Sb[o] = -2.0f * s * g * db;
   }
+  __device__ void v4(int i, int j, float4 db) const {
+    const int64_t o = (int64_t)i * ld + j;
+    const float4 s = ld4(S + o);
+    const float4 g = Gk ? ld4(Gk + o) : F4MAP(__ldg(gv + j + e_));
+    float4 gb = F4MAP(comp(db, e_) * (1.0f - comp(s, e_) * comp(s, e_)));
+    if (Gbprev) {
+      const float4 gp = ld4(Gbprev + o);
+      gb = F4MAP(comp(gb, e_) + comp(gp, e_));
+    }
+    st4(Gb + o, gb);
+    st4(Sb + o, F4MAP(-2.0f * comp(s, e_) * comp(g, e_) * comp(db, e_)));
+  }
 };
 
 struct EpiDown {       // hÃÑ_{k-1} = ƒÅ_k W_k (+ hÃÑ_k);  ƒÅ_{k-1} = (sÃÑ_{k-1} + hÃÑ_{k-1}) ‚äô s'_{k-1}
@@ -222,15 +475,50 @@ struct EpiDown {       // hÃÑ_{k-1} = ƒÅ_k W_k (+ hÃÑ_k);  ƒÅ_{k-1} = (sÃÑ_{k-1}
     const float s = S[o];
     Ab[o] = (Sb[o] + c) * (1.0f - s * s);
   }
+  __device__ void v4(int i, int j, float4 c) const {
+    const int64_t o = (int64_t)i * ld + j;
+    if (Hb) {
+      const float4 h = ld4(Hb + o);
+      c = F4MAP(comp(c, e_) + comp(h, e_));
+    }
+    if (Hbout) st4(Hbout + o, c);
+    const float4 s = ld4(S + o), sb = ld4(Sb + o);
+    st4(Ab + o, F4MAP((comp(sb, e_) + comp(c, e_)) * (1.0f - comp(s, e_) * comp(s, e_))));
+  }
 };
 
 // ---------------------------------------------------------------- row kernels
-// Paths of this rank: U0 rows (n¬∑M + m) = [t_n, X_n, 0 pad], ŒîW rows (n¬∑M + m) = ŒîW_n.
-// One thread per (path, 4-component block); coupled paths sum fine increments (R22).
-__global__ void k_sh_paths(ShArgs a) {
+// Paths of this rank, in two passes.  k_sh_dw: ŒîW rows (n¬∑M + m) = ŒîW_n, one
+// thread per (step, path, 4-component block), all independent (R8 counters);
+// coupled paths sum the fine increments (R22).  k_sh_x: one thread per (path,
+// block) runs the Euler recursion and writes U0 rows (n¬∑M + m) = [t_n, X_n].
+__global__ void k_sh_dw(ShArgs a) {
+  const int nq = (a.d + 3) >> 2;
+  const int64_t tot = (int64_t)a.N * a.M * nq;
+  const uint32_t it = a.eval ? a.eval_it : a.state->it;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < tot;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nm = id / nq;
+    const int q = (int)(id - nm * nq);
+    const int n = (int)(nm / a.M);
+    const int64_t m = nm - (int64_t)n * a.M;
+    float dw[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < a.cpl; ++j) {
+      const float4 z = normals4((uint32_t)q, (uint32_t)(a.m0 + m), (uint32_t)(n * a.cpl + j), it,
+                                a.k0, a.k1);
+      dw[0] += a.sqrt_dt_f * z.x; dw[1] += a.sqrt_dt_f * z.y;
+      dw[2] += a.sqrt_dt_f * z.z; dw[3] += a.sqrt_dt_f * z.w;
+    }
+    float* o = a.dW + nm * a.d + 4 * q;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (4 * q + e < a.d) o[e] = dw[e];
+  }
+}
+
+__global__ void k_sh_x(ShArgs a) {
   const int nq = (a.d + 3) >> 2;
   const int64_t tot = a.M * nq;
-  const uint32_t it = a.eval ? a.eval_it : a.state->it;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < tot;
        id += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = id / nq;
@@ -243,20 +531,10 @@ __global__ void k_sh_paths(ShArgs a) {
       for (int e = 0; e < 4; ++e)
         if (4 * q + e < a.d) u[1 + 4 * q + e] = x[e];
       if (n == a.N) break;
-      float dw[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int j = 0; j < a.cpl; ++j) {
-        const float4 z = normals4((uint32_t)q, (uint32_t)(a.m0 + m), (uint32_t)(n * a.cpl + j), it,
-                                  a.k0, a.k1);
-        dw[0] += a.sqrt_dt_f * z.x; dw[1] += a.sqrt_dt_f * z.y;
-        dw[2] += a.sqrt_dt_f * z.z; dw[3] += a.sqrt_dt_f * z.w;
-      }
-      float* o = a.dW + ((int64_t)n * a.M + m) * a.d;
+      const float* dw = a.dW + ((int64_t)n * a.M + m) * a.d + 4 * q;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (4 * q + e < a.d) {
-          o[4 * q + e] = dw[e];
-          x[e] = x_step(a.problem, x[e], dw[e]);
-        }
+        if (4 * q + e < a.d) x[e] = x_step(a.problem, x[e], dw[e]);
     }
   }
 }
@@ -369,18 +647,19 @@ __global__ void k_sh_loss(ShArgs a) {
   }
 }
 
-// ƒÅ_L = (sÃÑ_L + ≈´ v) ‚äô s'_L (and hÃÑ_L = ≈´ v for a residual last layer)
+// ƒÅ_L = (sÃÑ_L + ≈´ v) ‚äô s'_L (and hÃÑ_L = ≈´ v for a residual last layer); a CTA per row batch
 __global__ void k_sh_abar_last(ShArgs a, const float* Sb, const float* S, float* Ab, float* Hb) {
-  const int64_t R = (int64_t)(a.N + 1) * a.M, tot = R * a.w;
+  const int64_t R = (int64_t)(a.N + 1) * a.M;
   const float* v = a.params + a.off_v;
-  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < tot;
-       id += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = id / a.w;
-    const int j = (int)(id - r * a.w);
-    const float hb = a.ub[r] * __ldg(v + j);
-    if (Hb) Hb[id] = hb;
-    const float s = S[id];
-    Ab[id] = (Sb[id] + hb) * (1.0f - s * s);
+  for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
+    const float u = a.ub[r];
+    for (int j = threadIdx.x; j < a.w; j += blockDim.x) {
+      const int64_t id = r * a.w + j;
+      const float hb = u * __ldg(v + j);
+      if (Hb) Hb[id] = hb;
+      const float s = S[id];
+      Ab[id] = (Sb[id] + hb) * (1.0f - s * s);
+    }
   }
 }
 
@@ -455,29 +734,44 @@ int grid_for(int64_t work, int per_block) {
 template <bool NT, class Epi>
 cudaError_t gemm_rows(const float* A, int lda, const float* B, int ldb, int R, int NC, int K,
                       const Epi& epi, cudaStream_t s) {
-  dim3 grid((NC + TB - 1) / TB, (R + TB - 1) / TB);
-  k_gemm_rows<NT, Epi><<<grid, NTH, 0, s>>>(A, lda, B, ldb, R, NC, K, epi);
+  const int64_t big_tiles = (int64_t)((NC + BB - 1) / BB) * ((R + BB - 1) / BB);
+  if (lda % 4 == 0 && big_tiles >= 2 * 148) {
+    dim3 grid((NC + BB - 1) / BB, (R + BB - 1) / BB);
+    k_gemm_rows128<NT, Epi><<<grid, NTH, 0, s>>>(A, lda, B, ldb, R, NC, K, epi);
+  } else {
+    dim3 grid((NC + TB - 1) / TB, (R + TB - 1) / TB);
+    k_gemm_rows<NT, Epi><<<grid, NTH, 0, s>>>(A, lda, B, ldb, R, NC, K, epi);
+  }
   return cudaGetLastError();
 }
 
-cudaError_t gemm_tn(const float* A, int lda, const float* B, int ldb, const float* A2, int lda2,
-                    const float* B2, int ldb2, int R, int P, int Q, float* C, int ldc,
-                    cudaStream_t s) {
-  const int tiles = ((P + TB - 1) / TB) * ((Q + TB - 1) / TB);
+// C[P√óQ] += A·µÄ B over R rows (+ bias[p] += Œ£_r A[r][p] when bias != null)
+cudaError_t gemm_tn(const float* A, int lda, const float* B, int ldb, int R, int P, int Q, float* C,
+                    int ldc, float* bias, cudaStream_t s) {
+  const int tiles = ((P + BB - 1) / BB) * ((Q + BB - 1) / BB);
   int splits = (2 * 148 + tiles - 1) / tiles;
-  const int max_splits = (R + 4 * TK - 1) / (4 * TK);   // >= 64 rows per split
+  const int max_splits = (R + 8 * BKK - 1) / (8 * BKK);   // >= 64 rows per split
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
   int rows = (R + splits - 1) / splits;
-  rows = (rows + TK - 1) / TK * TK;
+  rows = (rows + BKK - 1) / BKK * BKK;
   splits = (R + rows - 1) / rows;
-  dim3 grid((Q + TB - 1) / TB, (P + TB - 1) / TB, splits);
-  k_gemm_tn<<<grid, NTH, 0, s>>>(A, lda, B, ldb, A2, lda2, B2, ldb2, R, P, Q, C, ldc, rows);
+  dim3 grid((Q + BB - 1) / BB, (P + BB - 1) / BB, splits);
+  k_gemm_tn128<<<grid, NTH, 0, s>>>(A, lda, B, ldb, R, P, Q, C, ldc, bias, rows);
   return cudaGetLastError();
 }
 
 cudaError_t colsum(const float* X, int ldx, const float* sv, const float* Y, int ldy, int R, int NC,
                    float* out, cudaStream_t s) {
+  if (NC % 4 == 0 && ldx % 4 == 0 && (!Y || ldy % 4 == 0)) {
+    const int cb = (NC + 63) / 64;
+    int rb = (4 * 148 + cb - 1) / cb;
+    int rows = (R + rb - 1) / rb;
+    if (rows < 64) rows = 64;
+    rb = (R + rows - 1) / rows;
+    k_colsum4<<<dim3(cb, rb), NTH, 0, s>>>(X, ldx, sv, Y, ldy, R, NC, rows, out);
+    return cudaGetLastError();
+  }
   const int cb = (NC + 31) / 32;
   int rb = (2 * 148 + cb - 1) / cb;
   int rows = (R + rb - 1) / rb;
@@ -582,9 +876,11 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   auto bk = [&](int k) { return P + a.off_W[k] + (int64_t)W * (k == 0 ? K0 : W); };
   const float* v = P + a.off_v;
   // paths
-  k_sh_paths<<<grid_for(a.M * ((a.d + 3) / 4), NTH), NTH, 0, s>>>(a);
+  k_sh_dw<<<grid_for((int64_t)a.N * a.M * ((a.d + 3) / 4), NTH), NTH, 0, s>>>(a);
   RET(cudaGetLastError());
-  ++nl;
+  k_sh_x<<<grid_for(a.M * ((a.d + 3) / 4), 64), 64, 0, s>>>(a);
+  RET(cudaGetLastError());
+  nl += 2;
   // forward: layers 1..L (0-based k)
   for (int k = 0; k < L; ++k) {
     EpiFwd e{bk(k), a.S[k], a.H[k], k > 0 ? a.H[k - 1] : nullptr, k == L - 1 ? v : nullptr,
@@ -623,7 +919,7 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   int ldprev = a.K0p;
   for (int k = 0; k < L; ++k) {
     const int K = k == 0 ? K0 : W;
-    RET(gemm_tn(a.D[k], W, gprev, ldprev, nullptr, 0, nullptr, 0, R, W, K, gW(k), K, s));
+    RET(gemm_tn(a.D[k], W, gprev, ldprev, R, W, K, gW(k), K, nullptr, s));
     float* gout = a.Gb[k & 1];
     EpiUp e{a.S[k], k < L - 1 ? a.G[k] : nullptr, v, (res && k > 0) ? gprev : nullptr, gout,
             a.Sb[k], W};
@@ -638,16 +934,15 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   nl += 2;
   // down: ƒÅ_L, then k = L..1: WÃÑ_k += ƒÅ_k·µÄ h_{k-1}, bÃÑ_k += Œ£ ƒÅ_k, ƒÅ_{k-1} = (sÃÑ_{k-1} + ƒÅ_k W_k (+ hÃÑ_k)) ‚äô s'
   int cur = 0;
-  k_sh_abar_last<<<grid_for((int64_t)R * W, NTH), NTH, 0, s>>>(
+  k_sh_abar_last<<<148 * 8, NTH, 0, s>>>(
       a, a.Sb[L - 1], a.S[L - 1], a.Ab[cur], res ? a.Hb[cur] : nullptr);
   RET(cudaGetLastError());
   ++nl;
   for (int k = L - 1; k >= 0; --k) {
     const float* hin = k == 0 ? a.U0 : a.H[k - 1];
     const int K = k == 0 ? K0 : W, ldh = k == 0 ? a.K0p : W;
-    RET(gemm_tn(a.Ab[cur], W, hin, ldh, nullptr, 0, nullptr, 0, R, W, K, gW(k), K, s));
-    RET(colsum(a.Ab[cur], W, nullptr, nullptr, 0, R, W, gb(k), s));
-    nl += 2;
+    RET(gemm_tn(a.Ab[cur], W, hin, ldh, R, W, K, gW(k), K, gb(k), s));   // + bÃÑ_k = Œ£ ƒÅ_k
+    ++nl;
     if (k == 0) break;
     const int nxt = cur ^ 1;
     EpiDown e{(res && k > 0) ? a.Hb[cur] : nullptr, (res && k - 1 > 0) ? a.Hb[nxt] : nullptr,

@@ -23,6 +23,9 @@ class Workload:
     levels: Optional[Tuple[int, ...]] = None     # multilevel grids (config 4)
     iters_per_level: int = 0
     x0: float = 0.0       # X_0 = x0 * ones(d)
+    formulation: str = "per_step"   # "per_step" (north_star) | "shared" (the paper's own, NEXT-1)
+    arch: str = "fc"      # shared: "fc" | "resnet"
+    layers: int = 2       # shared: tanh layers of width w
 
     def with_(self, **kw):
         return replace(self, **kw)
@@ -48,4 +51,12 @@ CONFIGS = {
     # x0 = 0.1 so that u(0, x0) = e^{0.21}·d·0.01 ≈ 1.234 (DESIGN R21)
     "nx3_black_scholes": Workload("nx3_black_scholes", "black_scholes", 100, 110, 20, 1.0, 65536,
                                   "bf16", 1e-2, 2000, x0=0.1),
+    # the paper's own formulation on its Table 1 workload (P:299, P:319,
+    # P:488): Black-Scholes d = 100, M = 100 paths, N = 50 steps, one network of 4 tanh
+    # layers x 256 shared by all steps, Adam lr 1e-3, 20 000 iterations, fp32
+    "nx1_shared_bs_paper": Workload("nx1_shared_bs_paper", "black_scholes", 100, 256, 50, 1.0, 100,
+                                    "fp32", 1e-3, 20000, x0=0.1, formulation="shared", layers=4),
+    # the same network and problem at a throughput batch (M = 4096)
+    "nx1_shared_bs_m4096": Workload("nx1_shared_bs_m4096", "black_scholes", 100, 256, 50, 1.0, 4096,
+                                    "fp32", 1e-3, 20000, x0=0.1, formulation="shared", layers=4),
 }
