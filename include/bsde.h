@@ -112,11 +112,17 @@ typedef struct {
                              u(t_n, X_n), z_n = σ(X_n)ᵀ∇ₓu, residual-sum loss.  FP32 and the
                              SIMT kernels only                                              */
   int arch;               /* BSDE_FORM_SHARED: BSDE_ARCH_FC or BSDE_ARCH_RESNET (h_k = h_{k-1}
-                             + tanh(W_k h_{k-1} + b_k) for k >= 2)        */
+                             + tanh(W_k h_{k-1} + b_k) for k >= 2).
+                             BSDE_FORM_PER_STEP: BSDE_ARCH_NAIS replaces the residual block
+                             by the NAIS-Net block H2 = H1 + ReLU(A H1 + B X_n + C), A =
+                             -RᵀR - 0.01 I, with R projected onto ‖RᵀR‖_F <= 0.99 after every
+                             Adam step (DESIGN R25); the
+                             per-step layout becomes [W1 b1 R C W3 b3 B (w×d)]; fp32 SIMT
+                             only.  Any other value: the R4 residual block              */
 } bsde_config;
 
 enum { BSDE_FORM_PER_STEP = 0, BSDE_FORM_SHARED = 1 };
-enum { BSDE_ARCH_FC = 0, BSDE_ARCH_RESNET = 1 };
+enum { BSDE_ARCH_FC = 0, BSDE_ARCH_RESNET = 1, BSDE_ARCH_NAIS = 2 };
 
 /* Fill *cfg with defaults: B = 256, x0 = 0, λ = 1, Adam (1e-2, 0.9, 0.999, 1e-8),
  * seed 0, FP32, KERNEL_AUTO, COPY, max_levels 0, device 0, default stream,

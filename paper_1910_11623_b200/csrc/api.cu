@@ -18,9 +18,9 @@
 namespace bsde {
 size_t simt_max_smem(int d, int w);
 bool simt_supported(int d, int w);
-size_t simt_pack_bytes(int d, int w, int N);
+size_t simt_pack_bytes(int d, int w, int N, int nais);
 size_t simt_xstore_bytes(int d, int N, int64_t B_local);
-size_t simt_scratch_bytes(int d, int w);
+size_t simt_scratch_bytes(int d, int w, int nais);
 cudaError_t launch_pack_simt(const PassArgs& a, cudaStream_t s);
 bool tc_supported(int d, int w);
 cudaError_t launch_fwd_tc(const PassArgs& a, cudaStream_t s);
@@ -78,6 +78,7 @@ NcclApi& nccl() {
 struct bsde_ctx {
   int problem = 0, d = 0, w = 0, N = 0, N0 = 0, level = 0, N_max = 0;
   bool shared = false;          // BSDE_FORM_SHARED (NEXT-1)
+  int nais = 0;                 // per-step nets with the NAIS-Net block (NEXT-2, R25)
   int L = 0;                    // shared: number of tanh layers
   void* shbuf = nullptr;        // shared: row buffers (carved into ShArgs)
   double T = 1.0;
@@ -131,7 +132,7 @@ int fail(bsde_ctx* c, int code, const char* fmt, ...) {
 
 int64_t num_params_at(const bsde_ctx* c, int N) {
   if (c->shared) return (int64_t)shared_num_params(c->d, c->w, c->L);   // independent of N
-  return 1 + (int64_t)N * NetDims{c->d, c->w}.step_size();
+  return 1 + (int64_t)N * NetDims{c->d, c->w, c->nais}.step_size();
 }
 
 ShArgs sh_args(bsde_ctx* c) {
@@ -193,6 +194,7 @@ PassArgs pass_args(bsde_ctx* c) {
   a.gpart = c->gpart;
   a.dwpack = c->xpack;
   a.precision = c->cfg.precision;
+  a.nais = c->nais;
   return a;
 }
 
@@ -221,6 +223,10 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
     mark(2);
     CK(launch_bwd_simt(a, ctx->stream));
     launches += 2;
+    if (ctx->nais) {   // Ā (W2 slot) -> R̄ = -R(Ā + Āᵀ), R25
+      CK(launch_nais_grad(ctx->params, ctx->grad, ctx->d, ctx->w, ctx->N, ctx->stream));
+      launches += 1;
+    }
   }
   mark(3);
   if (ctx->comm) {
@@ -241,6 +247,10 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
                    (float)ctx->cfg.lr, (float)ctx->cfg.beta1, (float)ctx->cfg.beta2,
                    (float)ctx->cfg.eps, 1, ctx->stream));
     launches += 2;
+    if (ctx->nais) {   // projection of every R_n after the optimizer step (R25)
+      CK(launch_nais_project(ctx->params, ctx->d, ctx->w, ctx->N, ctx->stream));
+      launches += 1;
+    }
     // weight images for the next step (bf16 UMMA images / fp32 transposed images)
     if (!ctx->shared) {
       if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(a, ctx->stream));
@@ -336,10 +346,12 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     for (int k = 1; k < n_widths; ++k)
       if (widths[k] != widths[0])
         return fail(none, BSDE_EINVAL, "shared net: all layer widths must be equal (R23)");
-    if (cfg.arch != BSDE_ARCH_FC && cfg.arch != BSDE_ARCH_RESNET)
+    if (cfg.arch != BSDE_ARCH_FC && cfg.arch != BSDE_ARCH_RESNET && cfg.arch != BSDE_ARCH_NAIS)
       return fail(none, BSDE_EINVAL, "arch=%d", cfg.arch);
     if (cfg.precision != BSDE_FP32 || cfg.kernel == BSDE_KERNEL_TC)
       return fail(none, BSDE_EINVAL, "the shared formulation runs fp32 SIMT kernels only");
+    if (cfg.arch == BSDE_ARCH_NAIS)
+      return fail(none, BSDE_EINVAL, "arch=NAIS is implemented for the per-step formulation only");
   } else if (!widths || n_widths != 2 || widths[0] != widths[1] || widths[0] < 1) {
     return fail(none, BSDE_EINVAL,
                 "widths must be {w, w} with w >= 1 (d->w->w->d residual net, R4); got n_widths=%d",
@@ -363,8 +375,11 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
   if (!(cfg.lr > 0) || !(cfg.beta1 >= 0 && cfg.beta1 < 1) || !(cfg.beta2 >= 0 && cfg.beta2 < 1) ||
       !(cfg.eps > 0))
     return fail(none, BSDE_EINVAL, "Adam hyper-parameters out of range");
+  const int nais = (!shared && cfg.arch == BSDE_ARCH_NAIS) ? 1 : 0;
+  if (nais && (cfg.precision != BSDE_FP32 || cfg.kernel == BSDE_KERNEL_TC))
+    return fail(none, BSDE_EINVAL, "the NAIS-Net block runs on the fp32 SIMT kernels only (R25)");
   int family = cfg.kernel;
-  if (shared) family = BSDE_KERNEL_SIMT;
+  if (shared || nais) family = BSDE_KERNEL_SIMT;
   if (family == BSDE_KERNEL_AUTO)
     family = (cfg.precision == BSDE_BF16 && tc_supported(d, w)) ? BSDE_KERNEL_TC : BSDE_KERNEL_SIMT;
   if (family == BSDE_KERNEL_TC && !tc_supported(d, w))
@@ -389,6 +404,7 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
   bsde_ctx* ctx = new bsde_ctx;
   ctx->problem = problem;
   ctx->shared = shared;
+  ctx->nais = nais;
   ctx->L = shared ? n_widths : 0;
   ctx->d = d;
   ctx->w = w;
@@ -448,8 +464,8 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     allocs.push_back({&ctx->wpack, tc_pack_bytes(d, w, ctx->N_max, cfg.precision)});
     allocs.push_back({&ctx->xpack, tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)});
   } else {
-    allocs.push_back({&ctx->wpack, simt_pack_bytes(d, w, ctx->N_max)});
-    allocs.push_back({(void**)&ctx->gpart, simt_scratch_bytes(d, w)});
+    allocs.push_back({&ctx->wpack, simt_pack_bytes(d, w, ctx->N_max, nais)});
+    allocs.push_back({(void**)&ctx->gpart, simt_scratch_bytes(d, w, nais)});
   }
   for (auto& al : allocs) {
     cudaError_t e = cudaMalloc(al.p, al.bytes);
@@ -467,7 +483,7 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
       shared ? launch_shared_init(ctx->params, sh_args(ctx), (uint32_t)(cfg.seed & 0xffffffffu),
                                   (uint32_t)(cfg.seed >> 32), ctx->stream)
              : launch_init_params(ctx->params, d, w, N, (uint32_t)(cfg.seed & 0xffffffffu),
-                                  (uint32_t)(cfg.seed >> 32), cfg.init_zero_head, ctx->stream);
+                                  (uint32_t)(cfg.seed >> 32), cfg.init_zero_head, nais, ctx->stream);
   if (ie != cudaSuccess) {
     ctx->err = "init kernel launch failed";
     return bail(BSDE_ECUDA);
@@ -542,7 +558,7 @@ int bsde_prolongate(bsde_ctx* ctx, int level) {
     return fail(ctx, BSDE_ESTATE, "prolongate(level=%d): current level %d, max_levels %d", level,
                 ctx->level, ctx->cfg.max_levels);
   if (!ctx->shared) {   // the shared network is the same function on every grid
-    const int64_t P = NetDims{ctx->d, ctx->w}.step_size();
+    const int64_t P = NetDims{ctx->d, ctx->w, ctx->nais}.step_size();
     const int64_t np = num_params_at(ctx, ctx->N);
     CK(cudaMemcpyAsync(ctx->scratch, ctx->params, np * sizeof(float), cudaMemcpyDeviceToDevice,
                        ctx->stream));

@@ -9,8 +9,8 @@ namespace {
 constexpr int NT = 256;
 
 __global__ void k_init_params(float* __restrict__ params, int d, int w, int N, uint32_t k0,
-                              uint32_t k1, int zero_head) {
-  const NetDims nd{d, w};
+                              uint32_t k1, int zero_head, int nais) {
+  const NetDims nd{d, w, nais};
   const int64_t P = nd.step_size();
   const int64_t total = 1 + (int64_t)N * P;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -28,6 +28,9 @@ __global__ void k_init_params(float* __restrict__ params, int d, int w, int N, u
         tid = base + 1; idx = (uint32_t)(r - nd.off_W2()); fan_in = w; fan_out = w; weight = true;
       } else if (r >= nd.off_W3() && r < nd.off_b3() && !zero_head) {
         tid = base + 2; idx = (uint32_t)(r - nd.off_W3()); fan_in = w; fan_out = d; weight = true;
+      } else if (nais && r >= nd.off_B()) {          // B_n of the NAIS block (R25)
+        tid = 0x100000u + (uint32_t)n; idx = (uint32_t)(r - nd.off_B()); fan_in = d; fan_out = w;
+        weight = true;
       } else {
         params[i] = 0.0f;      // biases (and W3 with a zero head, R7b)
         continue;
@@ -42,6 +45,55 @@ __global__ void k_init_params(float* __restrict__ params, int d, int w, int N, u
       const float a = sqrtf(6.0f / (float)(fan_in + fan_out));
       params[i] = a * (2.0f * u - 1.0f);                // Xavier-uniform
     }
+  }
+}
+
+// NAIS-Net projection (R25, SPEC nets.project_R), one CTA per step n:
+// f = ‖RᵀR‖_F = (Σ_{i,j} (Σ_r R[r][i] R[r][j])²)^½; if f > 1-ε, R *= ((1-ε)/f)^½.
+__global__ void k_nais_project(float* __restrict__ params, int d, int w) {
+  const NetDims nd{d, w, 1};
+  float* R = params + nd.step_base(blockIdx.x) + nd.off_W2();
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int i = e / w, j = e - i * w;
+    float g = 0.0f;
+    for (int r = 0; r < w; ++r) g = fmaf(R[r * w + i], R[r * w + j], g);
+    acc += (double)g * g;
+  }
+  __shared__ double red[NT / 32];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  __shared__ float scale;
+  if (threadIdx.x == 0) {
+    double f2 = 0.0;
+    for (int k = 0; k < NT / 32; ++k) f2 += red[k];
+    const double f = sqrt(f2);
+    scale = f > 1.0 - kNaisEps ? (float)sqrt((1.0 - kNaisEps) / f) : 1.0f;
+  }
+  __syncthreads();
+  if (scale != 1.0f)
+    for (int e = threadIdx.x; e < w * w; e += blockDim.x) R[e] *= scale;
+}
+
+// The adjoint accumulates Ā = Σ dA2ᵀ H1 in the W2 slot (the gradient with respect
+// to A); A = -RᵀR - εI gives R̄ = -R(Ā + Āᵀ) (R25).  One CTA per step.
+__global__ void k_nais_grad(const float* __restrict__ params, float* __restrict__ grad, int d,
+                            int w) {
+  extern __shared__ float S[];   // [w][w] Ā + Āᵀ
+  const NetDims nd{d, w, 1};
+  const float* R = params + nd.step_base(blockIdx.x) + nd.off_W2();
+  float* G = grad + nd.step_base(blockIdx.x) + nd.off_W2();
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int i = e / w, j = e - i * w;
+    S[e] = G[i * w + j] + G[j * w + i];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int i = e / w, j = e - i * w;
+    float g = 0.0f;
+    for (int k = 0; k < w; ++k) g = fmaf(R[i * w + k], S[k * w + j], g);
+    G[e] = -g;
   }
 }
 
@@ -151,9 +203,25 @@ int grid_for(int64_t n) {
 }  // namespace
 
 cudaError_t launch_init_params(float* params, int d, int w, int N, uint32_t k0, uint32_t k1,
-                               int zero_head, cudaStream_t s) {
-  const int64_t total = 1 + (int64_t)N * NetDims{d, w}.step_size();
-  k_init_params<<<grid_for(total), NT, 0, s>>>(params, d, w, N, k0, k1, zero_head);
+                               int zero_head, int nais, cudaStream_t s) {
+  const int64_t total = 1 + (int64_t)N * NetDims{d, w, nais}.step_size();
+  k_init_params<<<grid_for(total), NT, 0, s>>>(params, d, w, N, k0, k1, zero_head, nais);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && nais) e = launch_nais_project(params, d, w, N, s);   // R25: init projected
+  return e;
+}
+
+cudaError_t launch_nais_project(float* params, int d, int w, int N, cudaStream_t s) {
+  k_nais_project<<<N, NT, 0, s>>>(params, d, w);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nais_grad(const float* params, float* grad, int d, int w, int N, cudaStream_t s) {
+  const size_t smem = (size_t)w * w * sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(k_nais_grad, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  k_nais_grad<<<N, NT, smem, s>>>(params, grad, d, w);
   return cudaGetLastError();
 }
 

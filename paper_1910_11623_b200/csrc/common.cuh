@@ -18,6 +18,7 @@ constexpr uint32_t kEvalBit = 0x80000000u;     // counter word 3 of evaluation s
 constexpr uint32_t kInitStream = 0xC0000000u;  // counter word 3 of the init stream (R7)
 
 enum { kHeat = 0, kHJB = 1, kAllenCahn = 2, kBlackScholes = 3 };
+constexpr float kNaisEps = 0.01f;   // A = -RᵀR - εI ("ε = 0.01 in our case"); h = 1
 // Black-Scholes constants ("d = 100, r = 0.05 and σ = 0.4")
 constexpr float kBSRate = 0.05f, kBSSigma = 0.4f;
 
@@ -141,13 +142,17 @@ __device__ __forceinline__ float x_step(int problem, float x, float dw) {
 // ---- flat parameter layout (include/bsde.h) -------------------------------
 struct NetDims {
   int d, w;
-  __host__ __device__ int64_t step_size() const { return 2LL * d * w + 1LL * w * w + 2LL * w + d; }
+  int nais = 0;   // NAIS-Net block (R25): W2/b2 slots hold R/C and B (w×d) follows b3
+  __host__ __device__ int64_t step_size() const {
+    return 2LL * d * w + 1LL * w * w + 2LL * w + d + (nais ? 1LL * w * d : 0LL);
+  }
   __host__ __device__ int64_t off_W1() const { return 0; }
   __host__ __device__ int64_t off_b1() const { return 1LL * w * d; }
   __host__ __device__ int64_t off_W2() const { return off_b1() + w; }
   __host__ __device__ int64_t off_b2() const { return off_W2() + 1LL * w * w; }
   __host__ __device__ int64_t off_W3() const { return off_b2() + w; }
   __host__ __device__ int64_t off_b3() const { return off_W3() + 1LL * d * w; }
+  __host__ __device__ int64_t off_B() const { return off_b3() + d; }
   // parameters of step n start at 1 + n * step_size() (index 0 is Y0)
   __host__ __device__ int64_t step_base(int n) const { return 1 + (int64_t)n * step_size(); }
 };

@@ -34,6 +34,7 @@ struct PassArgs {
   void* dwpack;                        // tcgen05 path: fp16 ΔW_n images (written by k_fwd_tc)
   unsigned long long* clk;             // debug: per-phase clock64() trace of CTA 0 (or null)
   int precision;
+  int nais;                            // NAIS-Net block in the per-step nets (R25)
   int cpl;                             // coupled paths: fine steps per step (1 = uncoupled)
   float sqrt_dt_f;                     // √(Δt/cpl)
 };
@@ -80,7 +81,11 @@ cudaError_t launch_bwd_simt(const PassArgs& a, cudaStream_t s);
 
 // auxiliary kernels (aux.cu)
 cudaError_t launch_init_params(float* params, int d, int w, int N, uint32_t k0, uint32_t k1,
-                               int zero_head, cudaStream_t s);
+                               int zero_head, int nais, cudaStream_t s);
+// NAIS-Net (R25): R_n ← R_n((1-ε)/‖RᵀR‖_F)^½ where ‖RᵀR‖_F > 1-ε, every step n;
+// and the gradient transform Ā -> R̄ = -R(Ā + Āᵀ) in the W2 slot of each step
+cudaError_t launch_nais_project(float* params, int d, int w, int N, cudaStream_t s);
+cudaError_t launch_nais_grad(const float* params, float* grad, int d, int w, int N, cudaStream_t s);
 cudaError_t launch_begin_step(DeviceState* st, float* grad, int64_t n_grad, cudaStream_t s);
 cudaError_t launch_check(const float* grad, int64_t n, DeviceState* st, double inv_B,
                          float beta1, float beta2, cudaStream_t s);

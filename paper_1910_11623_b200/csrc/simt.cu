@@ -28,18 +28,28 @@ constexpr int LDW = 128;   // row pitch of the packed weight images (floats)
 
 struct Pack {
   int d, w;
+  int nais = 0;   // + Bᵀ image; the W2 images hold A = -RᵀR - εI (R25)
   __host__ __device__ size_t w1t() const { return 0; }                        // [d][LDW]
   __host__ __device__ size_t w2t() const { return (size_t)d * LDW; }          // [w][LDW]
   __host__ __device__ size_t w3t() const { return (size_t)(d + w) * LDW; }    // [w][LDW]
   __host__ __device__ size_t w3n() const { return (size_t)(d + 2 * w) * LDW; }  // [d][LDW]
   __host__ __device__ size_t w2n() const { return (size_t)(2 * d + 2 * w) * LDW; }  // [w][LDW]
-  __host__ __device__ size_t per_step() const { return (size_t)(2 * d + 3 * w) * LDW; }
+  __host__ __device__ size_t bt() const { return (size_t)(2 * d + 3 * w) * LDW; }    // [d][LDW]
+  __host__ __device__ size_t per_step() const { return (size_t)(2 * d + 3 * w + (nais ? d : 0)) * LDW; }
 };
 
+// A[i][j] = -Σ_r R[r][i] R[r][j] - ε δ_ij (NAIS-Net, R25; symmetric, so the
+// transposed and the plain W2 images are the same matrix)
+__device__ __forceinline__ float nais_A(const float* R, int w, int i, int j) {
+  float g = 0.0f;
+  for (int r = 0; r < w; ++r) g = fmaf(R[r * w + i], R[r * w + j], g);
+  return -g - (i == j ? kNaisEps : 0.0f);
+}
+
 __global__ void k_pack_simt(const float* __restrict__ params, float* __restrict__ out, int d,
-                            int w, int N) {
-  const NetDims nd{d, w};
-  const Pack pk{d, w};
+                            int w, int N, int nais) {
+  const NetDims nd{d, w, nais};
+  const Pack pk{d, w, nais};
   const int64_t per = (int64_t)pk.per_step();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)N * per;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -52,16 +62,19 @@ __global__ void k_pack_simt(const float* __restrict__ params, float* __restrict_
       if (col < w) v = P[nd.off_W1() + (int64_t)col * d + row];
     } else if (row < d + w) {                       // W2ᵀ[k][j] = W2[j][k]
       const int k = row - d;
-      if (col < w) v = P[nd.off_W2() + (int64_t)col * w + k];
+      if (col < w) v = nais ? nais_A(P + nd.off_W2(), w, k, col) : P[nd.off_W2() + (int64_t)col * w + k];
     } else if (row < d + 2 * w) {                   // W3ᵀ[k][j] = W3[j][k]
       const int k = row - d - w;
       if (col < d) v = P[nd.off_W3() + (int64_t)col * w + k];
     } else if (row < 2 * d + 2 * w) {               // W3[i][j]
       const int k = row - d - 2 * w;
       if (col < w) v = P[nd.off_W3() + (int64_t)k * w + col];
-    } else {                                        // W2[i][j]
+    } else if (row < 2 * d + 3 * w) {               // W2[i][j]
       const int k = row - 2 * d - 2 * w;
-      if (col < w) v = P[nd.off_W2() + (int64_t)k * w + col];
+      if (col < w) v = nais ? nais_A(P + nd.off_W2(), w, k, col) : P[nd.off_W2() + (int64_t)k * w + col];
+    } else {                                        // Bᵀ[k][j] = B[j][k] (NAIS)
+      const int k = row - 2 * d - 3 * w;
+      if (col < w) v = P[nd.off_B() + (int64_t)col * d + k];
     }
     out[i] = v;
   }
@@ -152,7 +165,7 @@ __device__ void gemm_t(const float* L, int ni, const float* R, int nj, float* __
       const float4 v = l[q];
       s += (v.x + v.y) + (v.z + v.w);
     }
-    gb[i] += s;
+    if (gb) gb[i] += s;
   }
 }
 
@@ -187,8 +200,8 @@ __device__ __forceinline__ float sum16(float v) {   // over the 16 lanes sharing
 __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
   extern __shared__ __align__(16) float sm[];
   const int d = a.d, w = a.w;
-  const NetDims nd{d, w};
-  const Pack pk{d, w};
+  const NetDims nd{d, w, a.nais};
+  const Pack pk{d, w, a.nais};
   float* Xs = sm;                         // [d][64] X_n (fp32 state)
   float* dWs = Xs + d * TP;               // [d][64]
   float* H1 = dWs + d * TP;               // [w][64]
@@ -224,15 +237,26 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
             make_float4(fmaxf(v.x + b, 0.f), fmaxf(v.y + b, 0.f), fmaxf(v.z + b, 0.f), fmaxf(v.w + b, 0.f));
       });
       __syncthreads();
+      const float* b2 = P + nd.off_b2();
+      if (a.nais) {   // NAIS block (R25): first B X + C into H2, then A H1 is added below
+        stage(Ws, W + pk.bt(), d * LDW);
+        __syncthreads();
+        gemm_n(Xs, Ws, d, w, [&](int p0, int j, float4 v) {
+          const float b = __ldg(b2 + j);
+          *reinterpret_cast<float4*>(H2 + j * TP + p0) = make_float4(v.x + b, v.y + b, v.z + b, v.w + b);
+        });
+        __syncthreads();
+      }
       stage(Ws, W + pk.w2t(), w * LDW);
       __syncthreads();
-      const float* b2 = P + nd.off_b2();
       gemm_n(H1, Ws, w, w, [&](int p0, int j, float4 v) {
-        const float b = __ldg(b2 + j);
+        // A2 = W2 H1 + b2, or A H1 + (B X + C) for NAIS; H2 = H1 + ReLU(A2)
+        const float4 c = a.nais ? *reinterpret_cast<const float4*>(H2 + j * TP + p0)
+                                : make_float4(__ldg(b2 + j), __ldg(b2 + j), __ldg(b2 + j), __ldg(b2 + j));
         const float4 h = *reinterpret_cast<const float4*>(H1 + j * TP + p0);
         *reinterpret_cast<float4*>(H2 + j * TP + p0) =
-            make_float4(h.x + fmaxf(v.x + b, 0.f), h.y + fmaxf(v.y + b, 0.f),
-                        h.z + fmaxf(v.z + b, 0.f), h.w + fmaxf(v.w + b, 0.f));
+            make_float4(h.x + fmaxf(v.x + c.x, 0.f), h.y + fmaxf(v.y + c.y, 0.f),
+                        h.z + fmaxf(v.z + c.z, 0.f), h.w + fmaxf(v.w + c.w, 0.f));
       });
       __syncthreads();
       stage(Ws, W + pk.w3t(), w * LDW);
@@ -312,8 +336,8 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
 __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int64_t items) {
   extern __shared__ __align__(16) float sm[];
   const int d = a.d, w = a.w;
-  const NetDims nd{d, w};
-  const Pack pk{d, w};
+  const NetDims nd{d, w, a.nais};
+  const Pack pk{d, w, a.nais};
   float* Xs = sm;                         // [d][64]
   float* dZ = Xs + d * TP;                // [d][64]  ΔW_n, then dZ_n in place
   float* H1 = dZ + d * TP;                // [w][64]
@@ -375,13 +399,23 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
           make_float4(fmaxf(v.x + b, 0.f), fmaxf(v.y + b, 0.f), fmaxf(v.z + b, 0.f), fmaxf(v.w + b, 0.f));
     });
     __syncthreads();
+    const float* b2 = Pn + nd.off_b2();
+    if (a.nais) {   // NAIS: B X + C into H2 first (R25)
+      stage(Ws, W + pk.bt(), d * LDW);
+      __syncthreads();
+      gemm_n(Xs, Ws, d, w, [&](int p0, int j, float4 v) {
+        const float b = __ldg(b2 + j);
+        *reinterpret_cast<float4*>(H2 + j * TP + p0) = make_float4(v.x + b, v.y + b, v.z + b, v.w + b);
+      });
+      __syncthreads();
+    }
     stage(Ws, W + pk.w2t(), w * LDW);
     __syncthreads();
-    const float* b2 = Pn + nd.off_b2();
     gemm_n(H1, Ws, w, w, [&](int p0, int j, float4 v) {           // recompute H2, mask of A2
-      const float b = __ldg(b2 + j);
+      const float4 c = a.nais ? *reinterpret_cast<const float4*>(H2 + j * TP + p0)
+                              : make_float4(__ldg(b2 + j), __ldg(b2 + j), __ldg(b2 + j), __ldg(b2 + j));
       const float4 h = *reinterpret_cast<const float4*>(H1 + j * TP + p0);
-      const float av[4] = {v.x + b, v.y + b, v.z + b, v.w + b};
+      const float av[4] = {v.x + c.x, v.y + c.y, v.z + c.z, v.w + c.w};
       *reinterpret_cast<float4*>(H2 + j * TP + p0) =
           make_float4(h.x + fmaxf(av[0], 0.f), h.y + fmaxf(av[1], 0.f), h.z + fmaxf(av[2], 0.f),
                       h.w + fmaxf(av[3], 0.f));
@@ -417,6 +451,7 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
     stage(Ws, W + pk.w2n(), w * LDW);
     // dW2 += dA2ᵀ H1 ; db2 += Σ dA2
     gemm_t(dA2, w, H1, w, scratch + nd.off_W2(), w, scratch + nd.off_b2());
+    if (a.nais) gemm_t(dA2, w, Xs, d, scratch + nd.off_B(), d, nullptr);   // B̄ += dA2ᵀ X (R25)
     __syncthreads();
     gemm_n(dA2, Ws, w, w, [&](int p0, int j, float4 v) {          // dA1 = (dH2 + dA2 W2) ⊙ 1[H1 > 0]
       const float4 h = *reinterpret_cast<const float4*>(H1 + j * TP + p0);
@@ -451,17 +486,22 @@ int sm_count() {
 
 bool simt_supported(int d, int w) { return d <= 128 && w <= 128 && bwd_smem(d, w) <= 227 * 1024; }
 size_t simt_max_smem(int d, int w) { return fwd_smem(d, w) > bwd_smem(d, w) ? fwd_smem(d, w) : bwd_smem(d, w); }
-size_t simt_pack_bytes(int d, int w, int N) { return (size_t)N * Pack{d, w}.per_step() * sizeof(float); }
+size_t simt_pack_bytes(int d, int w, int N, int nais) {
+  return (size_t)N * Pack{d, w, nais}.per_step() * sizeof(float);
+}
 size_t simt_xstore_bytes(int d, int N, int64_t B_local) {
   return (size_t)N * (size_t)((B_local + TP - 1) / TP) * d * TP * sizeof(float);
 }
-size_t simt_scratch_bytes(int d, int w) { return (size_t)sm_count() * NetDims{d, w}.step_size() * sizeof(float); }
+size_t simt_scratch_bytes(int d, int w, int nais) {
+  return (size_t)sm_count() * NetDims{d, w, nais}.step_size() * sizeof(float);
+}
 
 cudaError_t launch_pack_simt(const PassArgs& a, cudaStream_t s) {
-  const int64_t total = (int64_t)a.N * Pack{a.d, a.w}.per_step();
+  const int64_t total = (int64_t)a.N * Pack{a.d, a.w, a.nais}.per_step();
   int grid = (int)((total + NT - 1) / NT);
   if (grid > 148 * 16) grid = 148 * 16;
-  k_pack_simt<<<grid, NT, 0, s>>>(a.params, static_cast<float*>(const_cast<void*>(a.wpack)), a.d, a.w, a.N);
+  k_pack_simt<<<grid, NT, 0, s>>>(a.params, static_cast<float*>(const_cast<void*>(a.wpack)), a.d, a.w,
+                                  a.N, a.nais);
   return cudaGetLastError();
 }
 

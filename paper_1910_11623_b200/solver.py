@@ -12,7 +12,7 @@ from . import _lib
 from ._lib import BSDEError
 
 FORMULATIONS = {"per_step": 0, "shared": 1}
-ARCHS = {"fc": 0, "resnet": 1}
+ARCHS = {"fc": 0, "resnet": 1, "nais": 2}
 PROBLEMS = {"heat": _lib.HEAT, "hjb": _lib.HJB, "allen_cahn": _lib.ALLEN_CAHN,
             "black_scholes": _lib.BLACK_SCHOLES}
 PRECISIONS = {"fp32": _lib.FP32, "bf16": _lib.BF16}

@@ -10,13 +10,16 @@ PROBLEM = dict(ob.PROBLEM_NAMES)
 TOL = {"fp32": 1e-4, "bf16": 2e-2}
 
 
-def tensor_slices(d, w, N):
-    """(name, slice) of every parameter tensor in the flat layout."""
+def tensor_slices(d, w, N, nais=False):
+    """(name, slice) of every parameter tensor in the flat layout (NAIS-Net: the
+    W2/b2 slots hold R/C and B (w×d) follows b3, R25)."""
     out = [("Y0", slice(0, 1))]
     off = 1
     for n in range(N):
-        for name, size in (("W1", w * d), ("b1", w), ("W2", w * w), ("b2", w), ("W3", d * w),
-                           ("b3", d)):
+        tensors = [("W1", w * d), ("b1", w), ("W2", w * w), ("b2", w), ("W3", d * w), ("b3", d)]
+        if nais:
+            tensors.append(("B", w * d))
+        for name, size in tensors:
             out.append(("%s_%d" % (name, n), slice(off, off + size)))
             off += size
     return out
@@ -34,13 +37,13 @@ def oracle_iteration(problem, d, w, N, T, params, seed, it, paths, batch, x0=0.0
                         kink_band=kink_band, coupled_factor=coupled_factor)
 
 
-def compare_grads(g_gpu, g_orc, d, w, N, tol, slack=None):
+def compare_grads(g_gpu, g_orc, d, w, N, tol, slack=None, nais=False):
     """R19: per tensor ‖Δ‖₂/‖g‖₂ ≤ tol and max|Δ| ≤ 4·tol·max|g|, where Δ is the
     GPU-oracle difference beyond the kink slack (both ReLU masks are valid for a
     pre-activation inside the rounding band).  Returns the worst relative L2
     error; raises AssertionError naming the tensor."""
     worst = 0.0
-    for name, sl in tensor_slices(d, w, N):
+    for name, sl in tensor_slices(d, w, N, nais):
         a = np.asarray(g_gpu[sl], np.float64)
         b = np.asarray(g_orc[sl], np.float64)
         s = 0.0 if slack is None else np.asarray(slack[sl], np.float64)
