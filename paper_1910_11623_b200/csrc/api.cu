@@ -694,20 +694,20 @@ int bsde_eval_loss(bsde_ctx* ctx, uint32_t eval_id, int64_t batch, double* loss_
   if (batch < 1 || batch % ctx->cfg.world || batch > ((int64_t)1 << 32))
     return fail(ctx, BSDE_EINVAL, "eval batch=%lld must be divisible by world=%d",
                 (long long)batch, ctx->cfg.world);
-  if (ctx->shared) {
-    if (batch / ctx->cfg.world > ctx->B_local)
-      return fail(ctx, BSDE_EINVAL, "shared formulation: eval batch per rank must be <= %lld",
-                  (long long)ctx->B_local);
-    ShArgs sa = sh_args(ctx);
-    sa.eval = 1;
-    sa.eval_it = kEvalBit | (eval_id & 0x7fffffffu);
-    sa.M = batch / ctx->cfg.world;
-    sa.m0 = (int64_t)ctx->cfg.rank * sa.M;
-    sa.inv_B = (float)(1.0 / (double)batch);
-    sa.loss_acc = ctx->eval_loss;
-    shared_carve(sa, ctx->shbuf, ctx->N_max);
+  if (ctx->shared) {   // the rank's eval paths in chunks of at most B_local rows per step
+    const int64_t per_rank = batch / ctx->cfg.world, first = (int64_t)ctx->cfg.rank * per_rank;
     CK(cudaMemsetAsync(ctx->eval_loss, 0, sizeof(double), ctx->stream));
-    CK(launch_shared_step(sa, ctx->stream, nullptr, nullptr));
+    for (int64_t c0 = 0; c0 < per_rank; c0 += ctx->B_local) {
+      ShArgs sa = sh_args(ctx);
+      sa.eval = 1;
+      sa.eval_it = kEvalBit | (eval_id & 0x7fffffffu);
+      sa.M = per_rank - c0 < ctx->B_local ? per_rank - c0 : ctx->B_local;
+      sa.m0 = first + c0;
+      sa.inv_B = (float)(1.0 / (double)batch);
+      sa.loss_acc = ctx->eval_loss;
+      shared_carve(sa, ctx->shbuf, ctx->N_max);
+      CK(launch_shared_step(sa, ctx->stream, nullptr, nullptr));
+    }
   }
   PassArgs a = pass_args(ctx);
   a.eval = 1;

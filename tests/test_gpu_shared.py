@@ -126,7 +126,7 @@ def test_coupled_paths_shared():
 
 def test_eval_loss_matches_oracle():
     d, w, L, N, T = 12, 32, 3, 4, 0.3
-    s = make("allen_cahn", d, w, L, N, T, 256)
+    s = make("allen_cahn", d, w, L, N, T, 64)   # eval batch 200 runs in chunks of 64 paths
     p = perturb(s, 2).astype(np.float64)
     got = s.eval_loss(3, 200)
     ref = osh.iteration(ob.ALLEN_CAHN, d, w, L, osh.FC, N, T, p, 0, philox.EVAL_BIT | 3,
