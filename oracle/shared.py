@@ -16,8 +16,11 @@ Network (R23; P:319 "4 fully connected layers and 256 neurons", P:217-220 for
 the residual form): input h_0 = (t, x) ∈ R^{d+1}; for k = 1..L
   a_k = W_k h_{k-1} + b_k,   s_k = tanh(a_k),
   h_k = s_k  (FC)   or   h_k = h_{k-1} + s_k for k ≥ 2  (ResNet, h = 1)
-and u = v·h_L + c.  Flat parameter layout (same as the C-ABI):
+and u = v·h_L + c.  NAIS-Net (R26): layer 1 as FC, blocks k ≥ 2
+  h_k = h_{k-1} + h tanh(A_k h_{k-1} + B_k u + C_k),  A_k = -R_kᵀR_k - εI, u = h_0.
+Flat parameter layout (same as the C-ABI):
   [W_1 (w×(d+1)) b_1 (w) | W_2 (w×w) b_2 | ... | W_L b_L | v (w) | c]
+  NAIS-Net blocks: [R_k (w×w) C_k (w) B_k (w×(d+1))] in place of [W_k b_k]
 
 The gradient ∂L/∂Θ goes through ∇ₓu (the loss contains Z_n(Θ)), so it is the
 hand-written reverse-over-reverse derivative of the network (shared_grad
@@ -29,17 +32,20 @@ from . import philox
 from .bsde import (BLACK_SCHOLES, BS_SIGMA, SIGMA, driver_df_dy, driver_df_dz, driver_f,
                    forward_step, terminal_g)
 
-FC, RESNET = 0, 1
+FC, RESNET, NAIS = 0, 1, 2
+NAIS_EPS, NAIS_H = 0.01, 1.0    # A = -RᵀR - εI, block step h (R26)
 
 
-def num_params(d, w, L):
-    return w * (d + 1) + w + (L - 1) * (w * w + w) + w + 1
+def num_params(d, w, L, arch=FC):
+    blk = w * w + w + (w * (d + 1) if arch == NAIS else 0)
+    return w * (d + 1) + w + (L - 1) * blk + w + 1
 
 
-def unpack(params, d, w, L):
-    """Views ([(W_k, b_k) for k = 1..L], v, c) into the flat vector."""
+def unpack(params, d, w, L, arch=FC):
+    """Views ([(W_k, b_k) or (R_k, C_k, B_k) for k = 1..L], v, c) into the flat
+    vector; layer 1 is always (W_1, b_1), NAIS-Net blocks are (R, C, B)."""
     params = np.asarray(params)
-    assert params.shape == (num_params(d, w, L),), (params.shape, num_params(d, w, L))
+    assert params.shape == (num_params(d, w, L, arch),), (params.shape, num_params(d, w, L, arch))
     layers, off = [], 0
     for k in range(L):
         kin = d + 1 if k == 0 else w
@@ -47,33 +53,71 @@ def unpack(params, d, w, L):
         off += w * kin
         b = params[off:off + w]
         off += w
-        layers.append((W, b))
+        if arch == NAIS and k > 0:
+            Bk = params[off:off + w * (d + 1)].reshape(w, d + 1)
+            off += w * (d + 1)
+            layers.append((W, b, Bk))
+        else:
+            layers.append((W, b))
     v = params[off:off + w]
     c = params[off + w:off + w + 1]
     return layers, v, c
 
 
-def init_params(seed, d, w, L):
-    """R23 initialisation, as R7: Xavier-uniform W_k and v (tensor_id 1 + k, and
-    1 + L for v) from the Philox init stream, zero biases, c ~ U(0, 1) (tensor 0)."""
-    p = np.zeros(num_params(d, w, L))
-    layers, v, c = unpack(p, d, w, L)
-    for k, (W, _) in enumerate(layers):
+def nais_A(R):
+    return -R.T @ R - NAIS_EPS * np.eye(R.shape[0])
+
+
+def project(params, d, w, L, arch=NAIS):
+    """R_k ← R_k((1-ε)/‖R_kᵀR_k‖_F)^½ where ‖RᵀR‖_F > 1-ε (SPEC nets.project_R)."""
+    if arch != NAIS:
+        return params
+    layers, _, _ = unpack(params, d, w, L, arch)
+    for lay in layers[1:]:
+        R = lay[0]
+        f = np.linalg.norm(R.T @ R)
+        if f > 1.0 - NAIS_EPS:
+            R *= np.sqrt((1.0 - NAIS_EPS) / f)
+    return params
+
+
+def init_params(seed, d, w, L, arch=FC):
+    """R23 initialisation, as R7: Xavier-uniform W_k (R_k for NAIS-Net) and v
+    (tensor_id 1 + k, and 1 + L for v) from the Philox init stream, NAIS-Net B_k
+    Xavier-uniform with tensor 0x100000 + k, zero biases, c ~ U(0, 1) (tensor 0);
+    NAIS-Net R_k then projected (R26)."""
+    p = np.zeros(num_params(d, w, L, arch))
+    layers, v, c = unpack(p, d, w, L, arch)
+    for k, lay in enumerate(layers):
+        W = lay[0]
         fan_out, fan_in = W.shape
         a = np.sqrt(6.0 / (fan_in + fan_out))
         W[...] = (a * (2.0 * philox.init_uniforms(seed, 1 + k, W.size) - 1.0)).reshape(W.shape)
+        if len(lay) == 3:
+            Bk = lay[2]
+            a = np.sqrt(6.0 / (Bk.shape[0] + Bk.shape[1]))
+            Bk[...] = (a * (2.0 * philox.init_uniforms(seed, 0x100000 + k, Bk.size) - 1.0)
+                       ).reshape(Bk.shape)
     a = np.sqrt(6.0 / (w + 1))
     v[...] = a * (2.0 * philox.init_uniforms(seed, 1 + L, w) - 1.0)
     c[0] = philox.init_uniforms(seed, 0, 1)[0]
-    return p
+    return project(p, d, w, L, arch)
 
 
 def forward(params, d, w, L, arch, t, X):
-    """u(t, x) for rows (t, X) [R], [R×d]; returns (u [R], cache of h_0..h_L, s_1..s_L)."""
-    layers, v, c = unpack(params, d, w, L)
+    """u(t, x) for rows (t, X) [R], [R×d]; returns (u [R], cache of h_0..h_L, s_1..s_L).
+    NAIS-Net blocks (k ≥ 2): h_k = h_{k-1} + h tanh(A_k h_{k-1} + B_k u + C_k), u = h_0."""
+    layers, v, c = unpack(params, d, w, L, arch)
     h = [np.concatenate([np.asarray(t, float).reshape(-1, 1), X], axis=1)]
     s = []
-    for k, (W, b) in enumerate(layers):
+    for k, lay in enumerate(layers):
+        if arch == NAIS and k > 0:
+            R, C, Bk = lay
+            sk = np.tanh(h[-1] @ nais_A(R) + h[0] @ Bk.T + C)
+            s.append(sk)
+            h.append(h[-1] + NAIS_H * sk)
+            continue
+        W, b = lay
         sk = np.tanh(h[-1] @ W.T + b)
         s.append(sk)
         h.append(h[-1] + sk if (arch == RESNET and k > 0) else sk)
@@ -84,16 +128,24 @@ def input_gradient(params, d, w, L, arch, cache):
     """∇_{(t,x)} u by the chain rule backwards through the layers (the reverse
     pass of autodiff): g_L = v; δ_k = g_k ⊙ (1 - s_k²); g_{k-1} = ρ_k g_k + W_kᵀ δ_k
     with ρ_k = 1 for residual layers.  Returns (g_0 [R×(d+1)], g_1..g_L, δ_1..δ_L)."""
-    layers, v, _ = unpack(params, d, w, L)
+    layers, v, _ = unpack(params, d, w, L, arch)
     h, s = cache
     R = h[0].shape[0]
     g = [None] * (L + 1)
     delta = [None] * (L + 1)
     g[L] = np.broadcast_to(v, (R, w)).copy()
+    gu = np.zeros_like(h[0])             # NAIS-Net: the input-injection terms B_kᵀ δ_k
     for k in range(L, 0, -1):
-        W, _ = layers[k - 1]
+        if arch == NAIS and k > 1:
+            Rm, _, Bk = layers[k - 1]
+            delta[k] = NAIS_H * g[k] * (1.0 - s[k - 1] ** 2)
+            g[k - 1] = g[k] + delta[k] @ nais_A(Rm)
+            gu = gu + delta[k] @ Bk
+            continue
+        W = layers[k - 1][0]
         delta[k] = g[k] * (1.0 - s[k - 1] ** 2)
         g[k - 1] = delta[k] @ W + (g[k] if (arch == RESNET and k > 1) else 0.0)
+    g[0] = g[0] + gu
     return g, delta
 
 
@@ -166,6 +218,8 @@ def shared_grad(params, d, w, L, arch, cache, g, delta, ubar, g0bar):
       h_k = ρ_k h_{k-1} + s_k       :  s̄_k += h̄_k;  ā_k = s̄_k ⊙ (1 - s_k²)
       a_k = W_k h_{k-1} + b_k       :  W̄_k += ā_kᵀ h_{k-1};  b̄_k += Σ ā_k;  h̄_{k-1} = ρ_k h̄_k + ā_k W_k
     """
+    if arch == NAIS:
+        return _nais_grad(params, d, w, L, cache, g, delta, ubar, g0bar)
     layers, v, _ = unpack(params, d, w, L)
     h, s = cache
     grad = np.zeros_like(np.asarray(params, dtype=np.float64))
@@ -192,6 +246,62 @@ def shared_grad(params, d, w, L, arch, cache, g, delta, ubar, g0bar):
         glayers[k - 1][1][...] += abar.sum(axis=0)
         if k > 1:
             hbar = abar @ W + (hbar if res[k] else 0.0)
+    return grad
+
+
+def _nais_grad(params, d, w, L, cache, g, delta, ubar, g0bar):
+    """Reverse-over-reverse for the NAIS-Net network (R26): layer 1 as FC; block k
+    (A_k = -R_kᵀR_k - εI symmetric, u = h_0):
+      input-gradient adjoint, k = 1..L, seed ḡ_u = g0bar:
+        layer 1: W̄_1 += δ_1ᵀ ḡ_u;  δ̄_1 = ḡ_u W_1ᵀ;  ḡ_1 = δ̄_1 ⊙ s'_1;  s̄_1 = -2 s_1 g_1 δ̄_1
+        block k: Ā_k += δ_kᵀ ḡ_{k-1};  B̄_k += δ_kᵀ ḡ_u;  δ̄_k = ḡ_{k-1} A_k + ḡ_u B_kᵀ;
+                 ḡ_k = ḡ_{k-1} + h δ̄_k ⊙ s'_k;  s̄_k = -2 h s_k g_k δ̄_k
+      forward adjoint, k = L..1: ā_k = (s̄_k + h h̄_k) ⊙ s'_k (h = 1 for layer 1);
+        block: Ā_k += ā_kᵀ h_{k-1}, B̄_k += ā_kᵀ u, C̄_k += Σ ā_k, h̄_{k-1} = h̄_k + ā_k A_k;
+        layer 1: W̄_1 += ā_1ᵀ u, b̄_1 += Σ ā_1
+      then R̄_k = -R_k(Ā_k + Ā_kᵀ)."""
+    layers, v, _ = unpack(params, d, w, L, NAIS)
+    h, s = cache
+    grad = np.zeros_like(np.asarray(params, dtype=np.float64))
+    glayers, gv, gc = unpack(grad, d, w, L, NAIS)
+    Abar = [None] + [np.zeros((w, w)) for _ in range(1, L)]
+    gu_bar = g0bar
+    sbar = [None] * (L + 1)
+    W1 = layers[0][0]
+    glayers[0][0][...] += delta[1].T @ gu_bar
+    db = gu_bar @ W1.T
+    sp = 1.0 - s[0] ** 2
+    gbar = db * sp
+    sbar[1] = -2.0 * s[0] * g[1] * db
+    for k in range(2, L + 1):
+        Rm, C, Bk = layers[k - 1]
+        A = nais_A(Rm)
+        Abar[k - 1] += delta[k].T @ gbar
+        glayers[k - 1][2][...] += delta[k].T @ gu_bar
+        db = gbar @ A + gu_bar @ Bk.T
+        sp = 1.0 - s[k - 1] ** 2
+        sbar[k] = -2.0 * NAIS_H * s[k - 1] * g[k] * db
+        gbar = gbar + NAIS_H * db * sp
+    gv[...] += gbar.sum(axis=0)
+    gv[...] += ubar @ h[L]
+    gc[0] += ubar.sum()
+    hbar = np.outer(ubar, v)
+    for k in range(L, 0, -1):
+        sp = 1.0 - s[k - 1] ** 2
+        if k > 1:
+            Rm, C, Bk = layers[k - 1]
+            abar = (sbar[k] + NAIS_H * hbar) * sp
+            Abar[k - 1] += abar.T @ h[k - 1]
+            glayers[k - 1][2][...] += abar.T @ h[0]
+            glayers[k - 1][1][...] += abar.sum(axis=0)
+            hbar = hbar + abar @ nais_A(Rm)
+        else:
+            abar = (sbar[1] + hbar) * sp
+            glayers[0][0][...] += abar.T @ h[0]
+            glayers[0][1][...] += abar.sum(axis=0)
+    for k in range(1, L):
+        Rm = layers[k][0]
+        glayers[k][0][...] = -Rm @ (Abar[k] + Abar[k].T)
     return grad
 
 

@@ -13,19 +13,20 @@ from oracle import bsde, philox, shared
 PROBLEMS = [bsde.HEAT, bsde.HJB, bsde.ALLEN_CAHN, bsde.BLACK_SCHOLES]
 
 
-def _params(seed, d, w, L, scale=0.3):
-    p = shared.init_params(seed, d, w, L)
+def _params(seed, d, w, L, scale=0.3, arch=shared.FC):
+    p = shared.init_params(seed, d, w, L, arch)
     rng = np.random.default_rng(seed)
     return p + scale * rng.standard_normal(p.size)      # non-zero biases, generic weights
 
 
-@pytest.mark.parametrize("arch", [shared.FC, shared.RESNET])
+@pytest.mark.parametrize("arch", [shared.FC, shared.RESNET, shared.NAIS])
 @pytest.mark.parametrize("problem", PROBLEMS)
 def test_gradient_matches_central_differences(problem, arch):
     """Pin S1: ∂L/∂Θ through ∇ₓu (reverse-over-reverse) = central differences,
-    h = 1e-6, to 1e-6 of the largest component, every parameter."""
+    h = 1e-6, to 1e-6 of the largest component, every parameter (NAIS-Net: incl.
+    R̄ = -R(Ā + Āᵀ) and the input-injection B_k, R26)."""
     d, w, L, N, T, M, x0 = 3, 5, 3, 3, 0.5, 4, 0.6
-    p = _params(problem + 10 * arch, d, w, L)
+    p = _params(problem + 10 * arch, d, w, L, arch=arch)
     r = shared.iteration(problem, d, w, L, arch, N, T, p, 1, 2, np.arange(M), M, x0=x0)
     g = r["grad"]
     fd = np.zeros_like(p)
@@ -41,11 +42,12 @@ def test_gradient_matches_central_differences(problem, arch):
     assert np.max(np.abs(g - fd)) <= 1e-6 * np.max(np.abs(fd)), np.max(np.abs(g - fd))
 
 
-@pytest.mark.parametrize("arch", [shared.FC, shared.RESNET])
+@pytest.mark.parametrize("arch", [shared.FC, shared.RESNET, shared.NAIS])
 def test_input_gradient_matches_central_differences(arch):
-    """Pin S2: g_0 = ∇_{(t,x)} u from the reverse pass = central differences."""
+    """Pin S2: g_0 = ∇_{(t,x)} u from the reverse pass = central differences
+    (NAIS-Net: through every block's input injection B_k u)."""
     d, w, L = 4, 6, 4
-    p = _params(7, d, w, L)
+    p = _params(7, d, w, L, arch=arch)
     rng = np.random.default_rng(3)
     t = rng.random(5)
     X = rng.standard_normal((5, d))
@@ -139,3 +141,23 @@ def test_init_ranges():
         a = np.sqrt(6.0 / (W.shape[0] + W.shape[1]))
         assert np.all(np.abs(W) <= a) and np.abs(W).max() > 0.8 * a and not b.any()
     assert np.all(np.abs(v) <= np.sqrt(6.0 / (w + 1))) and 0.0 < c[0] < 1.0
+
+
+def test_nais_init_projected_and_zero_block_map():
+    """NAIS-Net (R26): initial R_k satisfy ‖RᵀR‖_F ≤ 1 - ε; with R = B = C = 0 a
+    block maps y to y + tanh(-εy) (SPEC nets example), so a point with h_1 = 0
+    (zero lift) stays 0 through every block and u = c."""
+    d, w, L = 5, 8, 3
+    p = shared.init_params(1, d, w, L, shared.NAIS)
+    layers, v, c = shared.unpack(p, d, w, L, shared.NAIS)
+    for R, C, Bk in layers[1:]:
+        assert np.linalg.norm(R.T @ R) <= 0.99 + 1e-12
+        assert not C.any() and np.abs(Bk).max() > 0
+    q = p.copy()
+    layers, v, c = shared.unpack(q, d, w, L, shared.NAIS)
+    layers[0][0][...] = 0.0
+    for R, C, Bk in layers[1:]:
+        R[...] = 0.0
+        Bk[...] = 0.0
+    u, _ = shared.forward(q, d, w, L, shared.NAIS, np.zeros(3), np.ones((3, d)))
+    np.testing.assert_array_equal(u, np.full(3, c[0]))
