@@ -28,6 +28,9 @@ sys.path.insert(0, ROOT)
 
 from workloads import CONFIGS  # noqa: E402
 
+# the paper's single-level solution times of its Table 1 workloads
+PAPER_MINUTES = {"nx1_shared_bs_paper": 59.0, "nx1_shared_bs_resnet_paper": 73.0,
+                 "nx2_shared_bs_nais_paper": 123.0}
 METRIC = "BSDE train path-steps/sec & % roofline at d=100 (1/2/4/8 B200); multilevel time-to-loss"
 UNIT = "path-steps/s"
 # algorithmic flop per path-step: forward 2(dw + w² + wd),
@@ -48,6 +51,8 @@ def bwd_flops(d, w):
 def shared_flops(wl):
     K0, w, L = wl.d + 1, wl.w, wl.layers
     one = 2 * (K0 * w + (L - 1) * w * w)
+    if wl.arch == "nais":   # + the input injection B_k u of every block (R26)
+        one += 2 * (L - 1) * w * K0
     rows = (wl.N + 1) / wl.N
     return rows * 2 * one, rows * (3 * one + 2 * (L - 1) * w * w)   # (fwd + ∇ₓu, gradient)
 
@@ -62,7 +67,7 @@ def shared_row_bytes(wl):
     K0p = (wl.d + 1 + 3) // 4 * 4
     L, w = wl.layers, wl.w
     floats = 3 * K0p + wl.d + w * (2 * L + (L - 1) + L + 4) + 6
-    if wl.arch == "resnet":
+    if wl.arch in ("resnet", "nais"):
         floats += w * (L - 1 + 2)
     return 4 * floats
 
@@ -153,8 +158,8 @@ def oracle_rate(wl, paths, iters):
     from oracle import shared as osh
     prob = ob.PROBLEM_NAMES[wl.problem]
     if wl.formulation == "shared":
-        arch = osh.RESNET if wl.arch == "resnet" else osh.FC
-        p = osh.init_params(wl.seed, wl.d, wl.w, wl.layers)
+        arch = {"fc": osh.FC, "resnet": osh.RESNET, "nais": osh.NAIS}[wl.arch]
+        p = osh.init_params(wl.seed, wl.d, wl.w, wl.layers, arch)
 
         def one(k):
             return osh.iteration(prob, wl.d, wl.w, wl.layers, arch, wl.N, wl.T, p, wl.seed, k,
@@ -361,13 +366,13 @@ def main():
                             "synchronised every step; the step's inputs are Philox counters "
                             "held on the device (no host input data exists, R8)"},
         }
-        if wl.name == "nx1_shared_bs_paper":
+        if wl.name in PAPER_MINUTES:
             # the paper's own timing of this workload: context only
             line["paper_context"] = {
-                "solution_time_min": 59.0, "hardware": "Tesla T4 (PyTorch)",
+                "solution_time_min": PAPER_MINUTES[wl.name], "hardware": "Tesla T4 (PyTorch)",
                 "iterations": wl.iterations, "derived_path_steps_per_s": 2.8e4,
                 "ours_solution_time_min": ms * wl.iterations / 6e4,
-                "source": "BASELINE.md section 1; PAPER.md:488 (single-level, fully connected)"}
+                "source": "BASELINE.md section 1; PAPER.md:488 (single-level, %s)" % wl.arch}
         if not args.no_cpu_baseline and world == 1:
             paths = max(256, min(wl.batch, int(2.4e5 // wl.N)))
             rate, threads, _ = oracle_rate(wl, paths, 2)

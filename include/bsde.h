@@ -111,8 +111,11 @@ typedef struct {
                              u(t, x) of n_widths tanh layers shared by all steps, Y_n =
                              u(t_n, X_n), z_n = σ(X_n)ᵀ∇ₓu, residual-sum loss.  FP32 and the
                              SIMT kernels only                                              */
-  int arch;               /* BSDE_FORM_SHARED: BSDE_ARCH_FC or BSDE_ARCH_RESNET (h_k = h_{k-1}
-                             + tanh(W_k h_{k-1} + b_k) for k >= 2).
+  int arch;               /* BSDE_FORM_SHARED: BSDE_ARCH_FC, BSDE_ARCH_RESNET (h_k = h_{k-1}
+                             + tanh(W_k h_{k-1} + b_k) for k >= 2) or
+                             BSDE_ARCH_NAIS (h_k = h_{k-1} + tanh(A_k h_{k-1} + B_k u + C_k),
+                             A_k = -R_kᵀR_k - 0.01 I, u = (t, x); block layout [R_k C_k B_k
+                             (w×(d+1))]; R_k projected after every Adam step; DESIGN R26).
                              BSDE_FORM_PER_STEP: BSDE_ARCH_NAIS replaces the residual block
                              by the NAIS-Net block H2 = H1 + ReLU(A H1 + B X_n + C), A =
                              -RᵀR - 0.01 I, with R projected onto ‖RᵀR‖_F <= 0.99 after every

@@ -131,7 +131,7 @@ int fail(bsde_ctx* c, int code, const char* fmt, ...) {
   } while (0)
 
 int64_t num_params_at(const bsde_ctx* c, int N) {
-  if (c->shared) return (int64_t)shared_num_params(c->d, c->w, c->L);   // independent of N
+  if (c->shared) return (int64_t)shared_num_params(c->d, c->w, c->L, c->cfg.arch);   // independent of N
   return 1 + (int64_t)N * NetDims{c->d, c->w, c->nais}.step_size();
 }
 
@@ -251,6 +251,10 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
       CK(launch_nais_project(ctx->params, ctx->d, ctx->w, ctx->N, ctx->stream));
       launches += 1;
     }
+    if (ctx->shared && ctx->cfg.arch == BSDE_ARCH_NAIS) {   // every block's R_k (R26)
+      CK(launch_shared_nais_project(sh_args(ctx), ctx->params, ctx->stream));
+      launches += 1;
+    }
     // weight images for the next step (bf16 UMMA images / fp32 transposed images)
     if (!ctx->shared) {
       if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(a, ctx->stream));
@@ -350,8 +354,6 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
       return fail(none, BSDE_EINVAL, "arch=%d", cfg.arch);
     if (cfg.precision != BSDE_FP32 || cfg.kernel == BSDE_KERNEL_TC)
       return fail(none, BSDE_EINVAL, "the shared formulation runs fp32 SIMT kernels only");
-    if (cfg.arch == BSDE_ARCH_NAIS)
-      return fail(none, BSDE_EINVAL, "arch=NAIS is implemented for the per-step formulation only");
   } else if (!widths || n_widths != 2 || widths[0] != widths[1] || widths[0] < 1) {
     return fail(none, BSDE_EINVAL,
                 "widths must be {w, w} with w >= 1 (d->w->w->d residual net, R4); got n_widths=%d",

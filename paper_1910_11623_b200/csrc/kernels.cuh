@@ -56,6 +56,8 @@ struct ShArgs {
   float* grad;
   float* Rstore;                            // [M] terminal residuals r_N
   int64_t off_W[kMaxSharedLayers], off_v;   // flat offsets of W_k (b_k follows) and v (c follows)
+  int64_t off_Bk[kMaxSharedLayers];         // NAIS-Net (arch 2): B_k of block k ≥ 1 (R26)
+  float* Am;                                // NAIS-Net: A_k = -R_kᵀR_k - εI, [L][w×w]
   float *U0, *G0, *G0b, *dW;                // [R×K0p] inputs, ∇u, ∂L/∂∇u;  [N·M×d] increments
   float* S[kMaxSharedLayers];               // s_k = tanh(a_k)
   float* H[kMaxSharedLayers];               // h_k (= S[k] unless residual)
@@ -66,13 +68,14 @@ struct ShArgs {
   float *Gb[2], *Ab[2], *Hb[2];             // ping-pong ḡ, ā, h̄
   float *u, *ub, *q;                        // [R] u, ū; [R×4] z·ΔW | |z|² | Σz
 };
-size_t shared_num_params(int d, int w, int L);
+size_t shared_num_params(int d, int w, int L, int arch);
 void shared_offsets(ShArgs& a);
 size_t shared_buffer_bytes(int d, int w, int L, int arch, int N_max, int64_t M);
 void shared_carve(ShArgs& a, void* base, int N_max);
 cudaError_t launch_shared_init(float* params, const ShArgs& a, uint32_t k0, uint32_t k1,
                                cudaStream_t s);
 cudaError_t launch_shared_point(const ShArgs& a, float* out, cudaStream_t s);
+cudaError_t launch_shared_nais_project(const ShArgs& a, float* params, cudaStream_t s);
 cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid, int* launches);
 
 // SIMT fp32 kernels (simt.cu)

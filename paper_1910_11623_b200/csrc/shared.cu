@@ -34,12 +34,23 @@ namespace {
 constexpr int TB = 64, TK = 16, NTH = 256;
 
 // ---------------------------------------------------------------- GEMM cores
+// An optional second operand pair accumulated into the same outputs (same NT/NN
+// mode): C = A·B' + A2·B2' (NAIS-Net: h A_kᵀ + u B_kᵀ, ḡ A_k + ḡ_u B_kᵀ).
+struct Op2 {
+  const float* A = nullptr;
+  int lda = 0;
+  const float* B = nullptr;
+  int ldb = 0, K = 0;
+};
 // Row GEMM: C[i][j] = Σ_k A[i][k]·B'[k][j] for i < R, j < NC, then epi(i, j, c).
 // NT: B' = Bᵀ with B row-major [NC×K] (a weight W_k [out×in]);  NN: B' = B, [K×NC].
 template <bool NT, class Epi>
 __global__ void __launch_bounds__(NTH) k_gemm_rows(const float* __restrict__ A, int lda,
                                                    const float* __restrict__ B, int ldb, int R,
-                                                   int NC, int K, Epi epi) {
+                                                   int NC, int K, Epi epi, Op2 op2) {
+  const float* Ap = A;
+  const float* Bp = B;
+  int ldap = lda, ldbp = ldb, Kp = K;
   __shared__ __align__(16) float As[2][TK][TB + 4];
   __shared__ __align__(16) float Bs[2][TK][TB + 4];
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
@@ -50,13 +61,13 @@ __global__ void __launch_bounds__(NTH) k_gemm_rows(const float* __restrict__ A, 
     for (int e = 0; e < 4; ++e) {
       const int idx = t + NTH * e, ii = idx >> 4, kk = idx & 15;
       const int i = i0 + ii, k = k0 + kk;
-      ra[e] = (i < R && k < K) ? __ldg(A + (int64_t)i * lda + k) : 0.0f;
+      ra[e] = (i < R && k < Kp) ? __ldg(Ap + (int64_t)i * ldap + k) : 0.0f;
       if (NT) {
         const int j = j0 + ii;
-        rb[e] = (j < NC && k < K) ? __ldg(B + (int64_t)j * ldb + k) : 0.0f;
+        rb[e] = (j < NC && k < Kp) ? __ldg(Bp + (int64_t)j * ldbp + k) : 0.0f;
       } else {
         const int kb = idx >> 6, jj = idx & 63, k2 = k0 + kb, j = j0 + jj;
-        rb[e] = (k2 < K && j < NC) ? __ldg(B + (int64_t)k2 * ldb + j) : 0.0f;
+        rb[e] = (k2 < Kp && j < NC) ? __ldg(Bp + (int64_t)k2 * ldbp + j) : 0.0f;
       }
     }
   };
@@ -70,12 +81,14 @@ __global__ void __launch_bounds__(NTH) k_gemm_rows(const float* __restrict__ A, 
     }
   };
   float acc[4][4] = {};
+  for (int pass = 0; pass < (op2.A ? 2 : 1); ++pass) {
+  if (pass) { Ap = op2.A; Bp = op2.B; ldap = op2.lda; ldbp = op2.ldb; Kp = op2.K; }
   load(0);
   store(0);
   __syncthreads();
   int buf = 0;
-  for (int k0 = 0; k0 < K; k0 += TK) {
-    const bool more = k0 + TK < K;
+  for (int k0 = 0; k0 < Kp; k0 += TK) {
+    const bool more = k0 + TK < Kp;
     if (more) load(k0 + TK);
 #pragma unroll
     for (int kk = 0; kk < TK; ++kk) {
@@ -91,6 +104,7 @@ __global__ void __launch_bounds__(NTH) k_gemm_rows(const float* __restrict__ A, 
     __syncthreads();
     buf ^= 1;
   }
+  }   // pass
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int i = i0 + 4 * ty + r, j = j0 + 4 * tx;
@@ -204,7 +218,10 @@ __device__ __forceinline__ void mma8x8_step(const float (*As)[BB], const float (
 template <bool NT, class Epi>
 __global__ void __launch_bounds__(NTH, 2) k_gemm_rows128(const float* __restrict__ A, int lda,
                                                          const float* __restrict__ B, int ldb,
-                                                         int R, int NC, int K, Epi epi) {
+                                                         int R, int NC, int K, Epi epi, Op2 op2) {
+  const float* Ap = A;
+  const float* Bp = B;
+  int ldap = lda, ldbp = ldb, Kp = K;
   __shared__ __align__(16) float As[2][BKK][BB];
   __shared__ __align__(16) float Bs[2][BKK][BB];
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
@@ -215,29 +232,29 @@ __global__ void __launch_bounds__(NTH, 2) k_gemm_rows128(const float* __restrict
   float4 ra, rb;
   auto load = [&](int k0) {
     const int i = i0 + ar, k = k0 + ak;
-    ra = (i < R) ? ld4_guard(A + (int64_t)i * lda + k, K - k) : make_float4(0.f, 0.f, 0.f, 0.f);
+    ra = (i < R) ? ld4_guard(Ap + (int64_t)i * ldap + k, Kp - k) : make_float4(0.f, 0.f, 0.f, 0.f);
     if (NT) {
       const int j = j0 + ar;
       if (j >= NC) {
         rb = make_float4(0.f, 0.f, 0.f, 0.f);
-      } else if (ldb % 4 == 0) {
-        rb = ld4_guard(B + (int64_t)j * ldb + k, K - k);
+      } else if (ldbp % 4 == 0) {
+        rb = ld4_guard(Bp + (int64_t)j * ldbp + k, Kp - k);
       } else {
         float v[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) v[e] = (k + e < K) ? __ldg(B + (int64_t)j * ldb + k + e) : 0.f;
+        for (int e = 0; e < 4; ++e) v[e] = (k + e < Kp) ? __ldg(Bp + (int64_t)j * ldbp + k + e) : 0.f;
         rb = make_float4(v[0], v[1], v[2], v[3]);
       }
     } else {
       const int kb = k0 + (t >> 5), jb = j0 + 4 * (t & 31);
-      if (kb >= K) {
+      if (kb >= Kp) {
         rb = make_float4(0.f, 0.f, 0.f, 0.f);
-      } else if (ldb % 4 == 0) {
-        rb = ld4_guard(B + (int64_t)kb * ldb + jb, NC - jb);
+      } else if (ldbp % 4 == 0) {
+        rb = ld4_guard(Bp + (int64_t)kb * ldbp + jb, NC - jb);
       } else {
         float v[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) v[e] = (jb + e < NC) ? __ldg(B + (int64_t)kb * ldb + jb + e) : 0.f;
+        for (int e = 0; e < 4; ++e) v[e] = (jb + e < NC) ? __ldg(Bp + (int64_t)kb * ldbp + jb + e) : 0.f;
         rb = make_float4(v[0], v[1], v[2], v[3]);
       }
     }
@@ -253,17 +270,20 @@ __global__ void __launch_bounds__(NTH, 2) k_gemm_rows128(const float* __restrict
     }
   };
   float acc[8][8] = {};
-  load(0);
-  store(0);
-  __syncthreads();
-  int buf = 0;
-  for (int k0 = 0; k0 < K; k0 += BKK) {
-    const bool more = k0 + BKK < K;
-    if (more) load(k0 + BKK);
-    mma8x8_step(As[buf], Bs[buf], tx, ty, acc);
-    if (more) store(buf ^ 1);
+  for (int pass = 0; pass < (op2.A ? 2 : 1); ++pass) {
+    if (pass) { Ap = op2.A; Bp = op2.B; ldap = op2.lda; ldbp = op2.ldb; Kp = op2.K; }
+    load(0);
+    store(0);
     __syncthreads();
-    buf ^= 1;
+    int buf = 0;
+    for (int k0 = 0; k0 < Kp; k0 += BKK) {
+      const bool more = k0 + BKK < Kp;
+      if (more) load(k0 + BKK);
+      mma8x8_step(As[buf], Bs[buf], tx, ty, acc);
+      if (more) store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
   }
   if (epi.ld % 4 == 0) mma8x8_epilogue_v4(acc, i0, j0, tx, ty, R, NC, epi);
   else mma8x8_epilogue(acc, i0, j0, tx, ty, R, NC, epi);
@@ -665,11 +685,13 @@ __global__ void k_sh_abar_last(ShArgs a, const float* Sb, const float* S, float*
 
 // Y0 = u(0, X_0): one CTA evaluates the network at one point.
 __global__ void k_sh_point(ShArgs a, float* out) {
-  extern __shared__ float hbuf[];                 // [2][max(K0p, w)]
+  extern __shared__ float hbuf[];                 // [3][max(K0p, w)]: h, h', u
   const int W = a.w, ldh = a.K0p > W ? a.K0p : W;
   float* h0 = hbuf;
   float* h1 = hbuf + ldh;
-  for (int i = threadIdx.x; i < a.K0p; i += blockDim.x) h0[i] = (i == 0 || i > a.d) ? 0.0f : a.x0;
+  float* u = hbuf + 2 * ldh;
+  for (int i = threadIdx.x; i < a.K0p; i += blockDim.x)
+    h0[i] = u[i] = (i == 0 || i > a.d) ? 0.0f : a.x0;
   __syncthreads();
   int K = a.d + 1;
   for (int k = 0; k < a.L; ++k) {
@@ -677,9 +699,16 @@ __global__ void k_sh_point(ShArgs a, float* out) {
     const float* bk = Wk + (int64_t)W * K;
     for (int j = threadIdx.x; j < W; j += blockDim.x) {
       float acc = bk[j];
-      for (int i = 0; i < K; ++i) acc = fmaf(Wk[(int64_t)j * K + i], h0[i], acc);
+      if (a.arch == 2 && k > 0) {   // NAIS-Net block: A_k h + B_k u + C_k (A_k from k_sh_nais_A)
+        const float* A = a.Am + (int64_t)k * W * W;
+        const float* Bk = a.params + a.off_Bk[k];
+        for (int i = 0; i < W; ++i) acc = fmaf(A[(int64_t)j * W + i], h0[i], acc);
+        for (int i = 0; i <= a.d; ++i) acc = fmaf(Bk[(int64_t)j * (a.d + 1) + i], u[i], acc);
+      } else {
+        for (int i = 0; i < K; ++i) acc = fmaf(Wk[(int64_t)j * K + i], h0[i], acc);
+      }
       const float s = tanhf(acc);
-      h1[j] = (a.arch == 1 && k > 0) ? h0[j] + s : s;
+      h1[j] = (a.arch != 0 && k > 0) ? h0[j] + s : s;
     }
     __syncthreads();
     float* tmp = h0; h0 = h1; h1 = tmp;
@@ -699,6 +728,56 @@ __global__ void k_sh_point(ShArgs a, float* out) {
   }
 }
 
+// NAIS-Net (R26) helpers around the w×w×w products, which run on the GEMM kernels:
+// G_k = R_kᵀR_k (weight-gradient GEMM over the w rows of R_k) into the A buffer,
+// then A_k = -G_k - εI (k_sh_nais_fix); S_k = Ā_k + Ā_kᵀ (k_sh_nais_sym) and
+// R̄_k = -R_k S_k (row GEMM, EpiNeg); ‖G_k‖_F and the projection (k_sh_nais_scale).
+__global__ void k_sh_nais_fix(ShArgs a) {
+  const int W = a.w;
+  const int64_t tot = (int64_t)(a.L - 1) * W * W;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < tot;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(id % ((int64_t)W * W)), i = e / W, j = e - i * W;
+    float* A = a.Am + (int64_t)W * W + id;      // blocks k = 1..L-1 start at Am + W·W
+    *A = -*A - (i == j ? kNaisEps : 0.0f);
+  }
+}
+
+__global__ void k_sh_nais_sym(ShArgs a) {      // S_k = Ā_k + Ā_kᵀ from the R_k gradient slot
+  const int W = a.w;
+  const int64_t tot = (int64_t)(a.L - 1) * W * W;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < tot;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int k = 1 + (int)(id / ((int64_t)W * W));
+    const int e = (int)(id - (int64_t)(k - 1) * W * W), i = e / W, j = e - i * W;
+    const float* G = a.grad + a.off_W[k];
+    a.Am[(int64_t)k * W * W + e] = G[i * W + j] + G[j * W + i];
+  }
+}
+
+// one CTA per block: f = ‖G_k‖_F (G_k = R_kᵀR_k in the A buffer); R_k *= ((1-ε)/f)^½ if f > 1-ε
+__global__ void k_sh_nais_scale(ShArgs a, float* __restrict__ params) {
+  const int W = a.w, k = 1 + blockIdx.x;
+  const float* Gk = a.Am + (int64_t)k * W * W;
+  float* R = params + a.off_W[k];
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < W * W; e += blockDim.x) acc += (double)Gk[e] * Gk[e];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double red[32];
+  __shared__ float scale;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double f2 = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) f2 += red[q];
+    const double f = sqrt(f2);
+    scale = f > 1.0 - kNaisEps ? (float)sqrt((1.0 - kNaisEps) / f) : 1.0f;
+  }
+  __syncthreads();
+  if (scale != 1.0f)
+    for (int e = threadIdx.x; e < W * W; e += blockDim.x) R[e] *= scale;
+}
+
 __global__ void k_sh_init(float* params, ShArgs a, uint32_t k0, uint32_t k1) {
   // R23: Xavier-uniform W_k (tensor 1 + k), v (tensor 1 + L), zero biases, c ~ U(0,1) (tensor 0)
   const int64_t total = a.off_v + a.w + 1;
@@ -716,7 +795,10 @@ __global__ void k_sh_init(float* params, ShArgs a, uint32_t k0, uint32_t k1) {
       const int K = k == 0 ? a.d + 1 : a.w;
       const int64_t r = i - a.off_W[k];
       if (r < (int64_t)a.w * K) { tid = 1 + k; idx = (uint32_t)r; fan_in = K; fan_out = a.w; weight = true; }
-      else bias = true;
+      else if (i >= a.off_Bk[k] && a.arch == 2 && k > 0) {   // NAIS-Net B_k (R26)
+        tid = 0x100000u + (uint32_t)k; idx = (uint32_t)(i - a.off_Bk[k]);
+        fan_in = a.d + 1; fan_out = a.w; weight = true;
+      } else bias = true;
     }
     if (bias) { params[i] = 0.0f; continue; }
     const uint4 x = philox4x32_10(make_uint4(idx >> 2, tid, 0u, kInitStream), k0, k1);
@@ -733,14 +815,14 @@ int grid_for(int64_t work, int per_block) {
 
 template <bool NT, class Epi>
 cudaError_t gemm_rows(const float* A, int lda, const float* B, int ldb, int R, int NC, int K,
-                      const Epi& epi, cudaStream_t s) {
+                      const Epi& epi, cudaStream_t s, Op2 op2 = Op2{}) {
   const int64_t big_tiles = (int64_t)((NC + BB - 1) / BB) * ((R + BB - 1) / BB);
-  if (lda % 4 == 0 && big_tiles >= 2 * 148) {
+  if (lda % 4 == 0 && (!op2.A || op2.lda % 4 == 0) && big_tiles >= 2 * 148) {
     dim3 grid((NC + BB - 1) / BB, (R + BB - 1) / BB);
-    k_gemm_rows128<NT, Epi><<<grid, NTH, 0, s>>>(A, lda, B, ldb, R, NC, K, epi);
+    k_gemm_rows128<NT, Epi><<<grid, NTH, 0, s>>>(A, lda, B, ldb, R, NC, K, epi, op2);
   } else {
     dim3 grid((NC + TB - 1) / TB, (R + TB - 1) / TB);
-    k_gemm_rows<NT, Epi><<<grid, NTH, 0, s>>>(A, lda, B, ldb, R, NC, K, epi);
+    k_gemm_rows<NT, Epi><<<grid, NTH, 0, s>>>(A, lda, B, ldb, R, NC, K, epi, op2);
   }
   return cudaGetLastError();
 }
@@ -781,16 +863,37 @@ cudaError_t colsum(const float* X, int ldx, const float* sv, const float* Y, int
   return cudaGetLastError();
 }
 
+struct EpiNeg {        // out = -c (R̄_k = -R_k S_k)
+  float* out;
+  int ld;
+  __device__ void operator()(int i, int j, float c) const { out[(int64_t)i * ld + j] = -c; }
+  __device__ void v4(int i, int j, float4 c) const {
+    *reinterpret_cast<float4*>(out + (int64_t)i * ld + j) = make_float4(-c.x, -c.y, -c.z, -c.w);
+  }
+};
+
 #define RET(x)                                \
   do {                                        \
     cudaError_t e_ = (x);                     \
     if (e_ != cudaSuccess) return e_;         \
   } while (0)
 
+// G_k = R_kᵀR_k for the NAIS-Net blocks into the A buffer (TN GEMM over R's rows)
+cudaError_t nais_gram(const ShArgs& a, const float* params, cudaStream_t s) {
+  const int W = a.w;
+  RET(cudaMemsetAsync(a.Am + (int64_t)W * W, 0, sizeof(float) * (size_t)(a.L - 1) * W * W, s));
+  for (int k = 1; k < a.L; ++k) {
+    const float* R = params + a.off_W[k];
+    RET(gemm_tn(R, W, R, W, W, W, W, a.Am + (int64_t)k * W * W, W, nullptr, s));
+  }
+  return cudaSuccess;
+}
+
 }  // namespace
 
-size_t shared_num_params(int d, int w, int L) {
-  return (size_t)w * (d + 1) + w + (size_t)(L - 1) * ((size_t)w * w + w) + w + 1;
+size_t shared_num_params(int d, int w, int L, int arch) {
+  const size_t blk = (size_t)w * w + w + (arch == 2 ? (size_t)w * (d + 1) : 0);
+  return (size_t)w * (d + 1) + w + (size_t)(L - 1) * blk + w + 1;
 }
 
 void shared_offsets(ShArgs& a) {
@@ -799,6 +902,8 @@ void shared_offsets(ShArgs& a) {
     a.off_W[k] = off;
     const int K = k == 0 ? a.d + 1 : a.w;
     off += (int64_t)a.w * K + a.w;
+    a.off_Bk[k] = off;
+    if (a.arch == 2 && k > 0) off += (int64_t)a.w * (a.d + 1);   // B_k after R_k, C_k
   }
   a.off_v = off;
 }
@@ -812,12 +917,13 @@ size_t shared_buffer_bytes(int d, int w, int L, int arch, int N_max, int64_t M) 
   f += (size_t)N_max * M * d;               // ΔW
   f += (size_t)R * w * (size_t)L * 2;       // S_k, δ_k
   f += (size_t)R * w * (size_t)(L - 1);     // g_1..g_{L-1}
-  if (arch == 1) f += (size_t)R * w * (size_t)(L - 1);   // H_k, k ≥ 2
+  if (arch != 0) f += (size_t)R * w * (size_t)(L - 1);   // H_k, k ≥ 2
   f += (size_t)R * w * (size_t)L;           // s̄_k
   f += (size_t)R * w * 4;                   // ḡ ping-pong, ā ping-pong
-  if (arch == 1) f += (size_t)R * w * 2;    // h̄ ping-pong
+  if (arch != 0) f += (size_t)R * w * 2;    // h̄ ping-pong
   f += (size_t)R * 6;                       // u, ū, q[4]
-  return f * sizeof(float) + 256 * 64;
+  if (arch == 2) f += (size_t)L * w * w;    // A_k
+  return f * sizeof(float) + 256 * 80;
 }
 
 void shared_carve(ShArgs& a, void* base, int N_max) {
@@ -833,14 +939,14 @@ void shared_carve(ShArgs& a, void* base, int N_max) {
     a.D[k] = take((size_t)R * a.w);
     a.Sb[k] = take((size_t)R * a.w);
     a.G[k] = k < a.L - 1 ? take((size_t)R * a.w) : nullptr;
-    a.H[k] = (a.arch == 1 && k > 0) ? take((size_t)R * a.w) : a.S[k];
+    a.H[k] = (a.arch != 0 && k > 0) ? take((size_t)R * a.w) : a.S[k];
   }
   a.HL = a.H[a.L - 1];
   a.Gb[0] = take((size_t)R * a.w);
   a.Gb[1] = take((size_t)R * a.w);
   a.Ab[0] = take((size_t)R * a.w);
   a.Ab[1] = take((size_t)R * a.w);
-  if (a.arch == 1) {
+  if (a.arch != 0) {
     a.Hb[0] = take((size_t)R * a.w);
     a.Hb[1] = take((size_t)R * a.w);
   } else {
@@ -849,17 +955,31 @@ void shared_carve(ShArgs& a, void* base, int N_max) {
   a.u = take((size_t)R);
   a.ub = take((size_t)R);
   a.q = take((size_t)R * 4);
+  a.Am = a.arch == 2 ? take((size_t)a.L * a.w * a.w) : nullptr;
 }
 
 cudaError_t launch_shared_init(float* params, const ShArgs& a, uint32_t k0, uint32_t k1,
                                cudaStream_t s) {
   k_sh_init<<<grid_for(a.off_v + a.w + 1, NTH), NTH, 0, s>>>(params, a, k0, k1);
+  RET(cudaGetLastError());
+  return a.arch == 2 ? launch_shared_nais_project(a, params, s) : cudaSuccess;   // R26
+}
+
+cudaError_t launch_shared_nais_project(const ShArgs& a, float* params, cudaStream_t s) {
+  if (a.arch != 2 || a.L < 2) return cudaSuccess;
+  RET(nais_gram(a, params, s));
+  k_sh_nais_scale<<<a.L - 1, NTH, 0, s>>>(a, params);
   return cudaGetLastError();
 }
 
 cudaError_t launch_shared_point(const ShArgs& a, float* out, cudaStream_t s) {
   const int ldh = a.K0p > a.w ? a.K0p : a.w;
-  k_sh_point<<<1, 256, 2 * ldh * sizeof(float), s>>>(a, out);
+  if (a.arch == 2) {
+    RET(nais_gram(a, a.params, s));
+    k_sh_nais_fix<<<grid_for((int64_t)(a.L - 1) * a.w * a.w, NTH), NTH, 0, s>>>(a);
+    RET(cudaGetLastError());
+  }
+  k_sh_point<<<1, 256, 3 * ldh * sizeof(float), s>>>(a, out);
   return cudaGetLastError();
 }
 
@@ -869,10 +989,13 @@ cudaError_t launch_shared_point(const ShArgs& a, float* out, cudaStream_t s) {
 cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid, int* launches) {
   const int R = (a.N + 1) * (int)a.M;
   const int W = a.w, K0 = a.d + 1, L = a.L;
-  const bool res = a.arch == 1;
+  const bool nais = a.arch == 2;
+  const bool res = a.arch == 1 || nais;      // NAIS-Net blocks are residual with h = 1 (R26)
   const float* P = a.params;
   int nl = 0;
-  auto Wk = [&](int k) { return P + a.off_W[k]; };                    // layer k+1 (0-based k)
+  // the layer matrix of the forward/back-propagation GEMMs: W_k, or A_k for a NAIS block
+  auto Wk = [&](int k) { return (nais && k > 0) ? a.Am + (int64_t)k * W * W : P + a.off_W[k]; };
+  auto Bk = [&](int k) { return P + a.off_Bk[k]; };
   auto bk = [&](int k) { return P + a.off_W[k] + (int64_t)W * (k == 0 ? K0 : W); };
   const float* v = P + a.off_v;
   // paths
@@ -881,24 +1004,40 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   k_sh_x<<<grid_for(a.M * ((a.d + 3) / 4), 64), 64, 0, s>>>(a);
   RET(cudaGetLastError());
   nl += 2;
-  // forward: layers 1..L (0-based k)
+  if (nais) {   // A_k = -R_kᵀR_k - εI from this iteration's parameters
+    RET(nais_gram(a, a.params, s));
+    k_sh_nais_fix<<<grid_for((int64_t)(L - 1) * W * W, NTH), NTH, 0, s>>>(a);
+    RET(cudaGetLastError());
+    nl += L;
+  }
+  // forward: layers 1..L (0-based k); NAIS-Net blocks add the input injection u B_kᵀ
   for (int k = 0; k < L; ++k) {
     EpiFwd e{bk(k), a.S[k], a.H[k], k > 0 ? a.H[k - 1] : nullptr, k == L - 1 ? v : nullptr,
              a.D[L - 1], W};
     const float* A = k == 0 ? a.U0 : a.H[k - 1];
     const int lda = k == 0 ? a.K0p : W, K = k == 0 ? K0 : W;
-    RET(gemm_rows<true>(A, lda, Wk(k), K, R, W, K, e, s));
+    Op2 inj;
+    if (nais && k > 0) inj = Op2{a.U0, a.K0p, Bk(k), K0, K0};
+    RET(gemm_rows<true>(A, lda, Wk(k), K, R, W, K, e, s, inj));
     ++nl;
   }
-  // input gradient: g_{k-1} = δ_k W_k (+ g_k), k = L..2, then g_0 = δ_1 W_1
+  // input gradient: g_{k-1} = δ_k W_k (+ g_k), k = L..2, then g_0 = δ_1 W_1; NAIS-Net
+  // blocks also add δ_k B_k to g_0 (the first such term initialises g_0)
+  bool g0_init = false;
   for (int k = L - 1; k >= 1; --k) {
     const float* gk = res ? (k == L - 1 ? v : a.G[k]) : nullptr;
     EpiIg e{gk, (res && k == L - 1) ? 1 : 0, a.G[k - 1], a.S[k - 1], a.D[k - 1], W};
     RET(gemm_rows<false>(a.D[k], W, Wk(k), W, R, W, W, e, s));
     ++nl;
+    if (nais) {
+      EpiIg eu{g0_init ? a.G0 : nullptr, 0, a.G0, nullptr, nullptr, a.K0p};
+      RET(gemm_rows<false>(a.D[k], W, Bk(k), K0, R, K0, W, eu, s));
+      ++nl;
+      g0_init = true;
+    }
   }
   {
-    EpiIg e{nullptr, 0, a.G0, nullptr, nullptr, a.K0p};
+    EpiIg e{g0_init ? a.G0 : nullptr, 0, a.G0, nullptr, nullptr, a.K0p};
     RET(gemm_rows<false>(a.D[0], W, Wk(0), K0, R, K0, W, e, s));
     ++nl;
   }
@@ -919,11 +1058,18 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   int ldprev = a.K0p;
   for (int k = 0; k < L; ++k) {
     const int K = k == 0 ? K0 : W;
+    // W̄_k (NAIS-Net: Ā_k, transformed to R̄_k at the end) += δ_kᵀ ḡ_{k-1}
     RET(gemm_tn(a.D[k], W, gprev, ldprev, R, W, K, gW(k), K, nullptr, s));
+    Op2 inj;
+    if (nais && k > 0) {   // B̄_k += δ_kᵀ ḡ_u;  δ̄_k += ḡ_u B_kᵀ
+      RET(gemm_tn(a.D[k], W, a.G0b, a.K0p, R, W, K0, G + a.off_Bk[k], K0, nullptr, s));
+      ++nl;
+      inj = Op2{a.G0b, a.K0p, Bk(k), K0, K0};
+    }
     float* gout = a.Gb[k & 1];
     EpiUp e{a.S[k], k < L - 1 ? a.G[k] : nullptr, v, (res && k > 0) ? gprev : nullptr, gout,
             a.Sb[k], W};
-    RET(gemm_rows<true>(gprev, ldprev, Wk(k), K, R, W, K, e, s));
+    RET(gemm_rows<true>(gprev, ldprev, Wk(k), K, R, W, K, e, s, inj));
     nl += 2;
     gprev = gout;
     ldprev = W;
@@ -941,8 +1087,14 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   for (int k = L - 1; k >= 0; --k) {
     const float* hin = k == 0 ? a.U0 : a.H[k - 1];
     const int K = k == 0 ? K0 : W, ldh = k == 0 ? a.K0p : W;
-    RET(gemm_tn(a.Ab[cur], W, hin, ldh, R, W, K, gW(k), K, gb(k), s));   // + b̄_k = Σ ā_k
-    ++nl;
+    if (nais && k > 0) {   // Ā_k += ā_kᵀ h_{k-1};  B̄_k += ā_kᵀ u, C̄_k += Σ ā_k
+      RET(gemm_tn(a.Ab[cur], W, hin, ldh, R, W, K, gW(k), K, nullptr, s));
+      RET(gemm_tn(a.Ab[cur], W, a.U0, a.K0p, R, W, K0, G + a.off_Bk[k], K0, gb(k), s));
+      nl += 2;
+    } else {
+      RET(gemm_tn(a.Ab[cur], W, hin, ldh, R, W, K, gW(k), K, gb(k), s));   // + b̄_k = Σ ā_k
+      ++nl;
+    }
     if (k == 0) break;
     const int nxt = cur ^ 1;
     EpiDown e{(res && k > 0) ? a.Hb[cur] : nullptr, (res && k - 1 > 0) ? a.Hb[nxt] : nullptr,
@@ -950,6 +1102,14 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
     RET(gemm_rows<false>(a.Ab[cur], W, Wk(k), W, R, W, W, e, s));
     ++nl;
     cur = nxt;
+  }
+  if (nais) {   // R̄_k = -R_k(Ā_k + Ā_kᵀ) (A_k is no longer needed: its buffer holds S_k)
+    k_sh_nais_sym<<<grid_for((int64_t)(L - 1) * W * W, NTH), NTH, 0, s>>>(a);
+    RET(cudaGetLastError());
+    for (int k = 1; k < L; ++k)
+      RET(gemm_rows<false>(P + a.off_W[k], W, a.Am + (int64_t)k * W * W, W, W, W, W,
+                           EpiNeg{G + a.off_W[k], W}, s));
+    nl += L;
   }
   if (launches) *launches = nl;
   return cudaSuccess;

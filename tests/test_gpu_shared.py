@@ -47,7 +47,9 @@ def test_init_matches_oracle():
 
 
 CASES = [("heat", "fc", 0.0), ("hjb", "fc", 0.0), ("allen_cahn", "fc", 0.0),
-         ("black_scholes", "fc", 0.5), ("hjb", "resnet", 0.0), ("black_scholes", "resnet", 0.5)]
+         ("black_scholes", "fc", 0.5), ("hjb", "resnet", 0.0), ("black_scholes", "resnet", 0.5),
+         ("hjb", "nais", 0.0), ("black_scholes", "nais", 0.5), ("allen_cahn", "nais", 0.0)]
+ARCH = {"fc": osh.FC, "resnet": osh.RESNET, "nais": osh.NAIS}
 
 
 @pytest.mark.parametrize("problem,arch,x0", CASES)
@@ -60,7 +62,7 @@ def test_teacher_forced_gradient(problem, arch, x0):
     for it in (0, 4):
         s.iteration = it
         loss = s.compute_grad()
-        ref = osh.iteration(PROBLEM[problem], d, w, L, osh.RESNET if arch == "resnet" else osh.FC,
+        ref = osh.iteration(PROBLEM[problem], d, w, L, ARCH[arch],
                             N, T, p.astype(np.float64), 0, it, np.arange(B), B, x0=x0)
         assert abs(loss - ref["loss"]) <= TOL * ref["loss"], (loss, ref["loss"])
         check_grad(s.get_grads(), ref["grad"])
@@ -141,3 +143,22 @@ def test_training_descends():
     losses = [s.train_step() for _ in range(300)]
     assert np.all(np.isfinite(losses))
     assert np.mean(losses[-20:]) < 0.2 * np.mean(losses[:5])
+
+
+def test_nais_init_adam_projection_and_y0():
+    """NAIS-Net shared network (R26): init = oracle init (projected R_k), one Adam
+    step = oracle Adam + projection, Y0 = u(0, X_0) with the A_k of the
+    current parameters."""
+    d, w, L, N, T, B = 10, 32, 3, 4, 1.0, 64
+    s = make("hjb", d, w, L, N, T, B, arch="nais", lr=0.05, seed=2)
+    assert s.num_params() == osh.num_params(d, w, L, osh.NAIS)
+    p = s.get_params().astype(np.float64)
+    ref = osh.init_params(2, d, w, L, osh.NAIS)
+    assert np.max(np.abs(p - ref)) <= 2e-6 * np.max(np.abs(ref))
+    s.train_step()
+    q = p.copy()
+    ob.adam_step(q, s.get_grads().astype(np.float64), ob.AdamState(p.size), 0.05)
+    osh.project(q, d, w, L, osh.NAIS)
+    got = s.get_params()
+    assert np.max(np.abs(got - q)) <= 1e-5 * np.max(np.abs(q))
+    assert abs(s.y0() - osh.u0(got.astype(np.float64), d, w, L, osh.NAIS, 0.0)) <= 1e-5

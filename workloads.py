@@ -56,6 +56,13 @@ CONFIGS = {
     # layers x 256 shared by all steps, Adam lr 1e-3, 20 000 iterations, fp32
     "nx1_shared_bs_paper": Workload("nx1_shared_bs_paper", "black_scholes", 100, 256, 50, 1.0, 100,
                                     "fp32", 1e-3, 20000, x0=0.1, formulation="shared", layers=4),
+    # the paper's ResNet and NAIS-Net rows of the same table (R23, R26)
+    "nx1_shared_bs_resnet_paper": Workload("nx1_shared_bs_resnet_paper", "black_scholes", 100, 256,
+                                           50, 1.0, 100, "fp32", 1e-3, 20000, x0=0.1,
+                                           formulation="shared", arch="resnet", layers=4),
+    "nx2_shared_bs_nais_paper": Workload("nx2_shared_bs_nais_paper", "black_scholes", 100, 256, 50,
+                                         1.0, 100, "fp32", 1e-3, 20000, x0=0.1,
+                                         formulation="shared", arch="nais", layers=4),
     # the same network and problem at a throughput batch (M = 4096)
     "nx1_shared_bs_m4096": Workload("nx1_shared_bs_m4096", "black_scholes", 100, 256, 50, 1.0, 4096,
                                     "fp32", 1e-3, 20000, x0=0.1, formulation="shared", layers=4),
