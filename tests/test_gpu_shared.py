@@ -162,3 +162,19 @@ def test_nais_init_adam_projection_and_y0():
     got = s.get_params()
     assert np.max(np.abs(got - q)) <= 1e-5 * np.max(np.abs(q))
     assert abs(s.y0() - osh.u0(got.astype(np.float64), d, w, L, osh.NAIS, 0.0)) <= 1e-5
+
+
+@pytest.mark.parametrize("arch", ["fc", "nais"])
+def test_fake_world_shards_sum(arch):
+    """Data-parallel sharding (§8(e)): two rank contexts without a communicator
+    ("fake world") own global paths [0, B/2) and [B/2, B); their local losses and
+    gradients sum to the single-context ones."""
+    d, w, L, N, T, B = 12, 32, 3, 4, 1.0, 128
+    full = make("hjb", d, w, L, N, T, B, arch=arch)
+    lf = full.compute_grad()
+    gf = full.get_grads().astype(np.float64)
+    parts = [make("hjb", d, w, L, N, T, B, arch=arch, rank=r, world=2) for r in range(2)]
+    ls = sum(pt.compute_grad() for pt in parts)
+    gs = sum(pt.get_grads().astype(np.float64) for pt in parts)
+    assert abs(ls - lf) <= 1e-5 * lf
+    assert np.linalg.norm(gs - gf) <= 1e-5 * np.linalg.norm(gf)
