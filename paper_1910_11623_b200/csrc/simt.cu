@@ -3,8 +3,8 @@
 //
 // Same data flow as the tensor-core path, register-tiled FFMA GEMMs:
 //  k_pack_simt  fp32 master θ -> per-step transposed/padded weight images
-//               W1ᵀ [d][128], W2ᵀ [w][128], W3ᵀ [w][128], W3 [d][128], W2 [w][128]
-//               (row pitch 128 floats, zero padded) so staging is a straight copy.
+//               W1ᵀ [d][112], W2ᵀ [w][112], W3ᵀ [w][112], W3 [d][112], W2 [w][112]
+//               (row pitch LDW = 112 floats, zero padded) so staging is a straight copy.
 //  k_fwd_simt   tile-major: a 64-path tile walks all N steps; activations are kept
 //               feature-major in shared memory ([feature][64 paths]); every GEMM
 //               C[64×nout] = A[64×K]·B[K×nout] gives each thread a 4-path × 8-output
@@ -23,8 +23,11 @@ namespace bsde {
 namespace {
 
 constexpr int TP = 64;     // paths per tile
+constexpr int TPP = 68;    // row pitch (floats) of the feature-major [k][path] smem buffers:
+                           // rows 16 B apart in bank space, so the weight-gradient GEMM's
+                           // 16-row float4 loads are conflict-free
 constexpr int NT = 256;    // threads per CTA
-constexpr int LDW = 128;   // row pitch of the packed weight images (floats)
+constexpr int LDW = 112;   // row pitch of the packed weight images (floats); d, w <= 112
 
 struct Pack {
   int d, w;
@@ -87,7 +90,7 @@ __device__ __forceinline__ void stage(float* dst, const float* __restrict__ src,
   for (int i = threadIdx.x; i < floats / 4; i += NT) o[i] = __ldg(s + i);
 }
 
-// C[p][j] = Σ_k At[k][p] · Bs[k][j] for p < 64, j < nout (<= 128).  Thread
+// C[p][j] = Σ_k At[k][p] · Bs[k][j] for p < 64, j < nout (<= LDW).  Thread
 // (ty, tx) = (t/16, t%16) owns paths 4ty..4ty+3 and outputs 4tx..4tx+3 and
 // 64+4tx..64+4tx+3.  epi(p0, j, float4 values-of-paths p0..p0+3).
 template <typename Epi>
@@ -102,7 +105,7 @@ __device__ __forceinline__ void gemm_n(const float* At, const float* Bs, int K, 
   const bool hi = j1 < nout;
 #pragma unroll 2
   for (int k = 0; k < K; ++k) {
-    const float4 a = *reinterpret_cast<const float4*>(At + k * TP + p0);
+    const float4 a = *reinterpret_cast<const float4*>(At + k * TPP + p0);
     const float4 b0 = *reinterpret_cast<const float4*>(Bs + k * LDW + j0);
     const float4 b1 = hi ? *reinterpret_cast<const float4*>(Bs + k * LDW + j1) : make_float4(0, 0, 0, 0);
     const float av[4] = {a.x, a.y, a.z, a.w};
@@ -139,8 +142,8 @@ __device__ void gemm_t(const float* L, int ni, const float* R, int nj, float* __
     float4 lv[8], rv[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      lv[r] = iv[r] < ni ? *reinterpret_cast<const float4*>(L + iv[r] * TP + p) : make_float4(0, 0, 0, 0);
-      rv[r] = jv[r] < nj ? *reinterpret_cast<const float4*>(R + jv[r] * TP + p) : make_float4(0, 0, 0, 0);
+      lv[r] = iv[r] < ni ? *reinterpret_cast<const float4*>(L + iv[r] * TPP + p) : make_float4(0, 0, 0, 0);
+      rv[r] = jv[r] < nj ? *reinterpret_cast<const float4*>(R + jv[r] * TPP + p) : make_float4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int r = 0; r < 8; ++r)
@@ -158,7 +161,7 @@ __device__ void gemm_t(const float* L, int ni, const float* R, int nj, float* __
     for (int c = 0; c < 8; ++c)
       if (iv[r] < ni && jv[c] < nj) G[iv[r] * ldg + jv[c]] += acc[r][c];
   for (int i = threadIdx.x; i < ni; i += NT) {
-    const float4* l = reinterpret_cast<const float4*>(L + i * TP);
+    const float4* l = reinterpret_cast<const float4*>(L + i * TPP);
     float s = 0.0f;
 #pragma unroll 4
     for (int q = 0; q < TP / 4; ++q) {
@@ -187,7 +190,7 @@ __device__ void gen_dw(float* dWs, int d, int64_t mg0, int64_t valid, int n, uin
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (4 * q + i < d) dWs[(4 * q + i) * TP + p] = zz[i];
+      if (4 * q + i < d) dWs[(4 * q + i) * TPP + p] = zz[i];
   }
 }
 
@@ -203,10 +206,10 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
   const NetDims nd{d, w, a.nais};
   const Pack pk{d, w, a.nais};
   float* Xs = sm;                         // [d][64] X_n (fp32 state)
-  float* dWs = Xs + d * TP;               // [d][64]
-  float* H1 = dWs + d * TP;               // [w][64]
-  float* H2 = H1 + w * TP;                // [w][64]
-  float* Ws = H2 + w * TP;                // [K <= max(d, w)][128]
+  float* dWs = Xs + d * TPP;              // [d][64]
+  float* H1 = dWs + d * TPP;              // [w][64]
+  float* H2 = H1 + w * TPP;               // [w][64]
+  float* Ws = H2 + w * TPP;               // [K <= max(d, w)][LDW]
   float* Ys = Ws + (d > w ? d : w) * LDW; // [64]
   float* Ps = Ys + TP;                    // [64] prefix products P_{n+1} of the ā factors
   const float* wp = static_cast<const float*>(a.wpack);
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t mloc0 = (int64_t)tile * TP;
     const int64_t valid = min((int64_t)TP, a.B_local - mloc0);
-    for (int i = t; i < d * TP; i += NT) Xs[i] = a.x0;
+    for (int i = t; i < d * TPP; i += NT) Xs[i] = a.x0;
     if (t < TP) { Ys[t] = a.params[0]; Ps[t] = 1.0f; }
     __syncthreads();
     for (int n = 0; n < a.N; ++n) {
@@ -225,7 +228,8 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
       const float* W = wp + (size_t)n * pk.per_step();
       if (!a.eval) {   // X_n for the adjoint pass: [n][tile][k][64], coalesced
         float4* xs = reinterpret_cast<float4*>(a.Xstore + ((size_t)n * ntiles + tile) * d * TP);
-        for (int i = t; i < d * TP / 4; i += NT) xs[i] = reinterpret_cast<const float4*>(Xs)[i];
+        for (int i = t; i < d * TP / 4; i += NT)
+          xs[i] = *reinterpret_cast<const float4*>(Xs + (i >> 4) * TPP + 4 * (i & 15));
       }
       gen_dw(dWs, d, a.m0 + mloc0, valid, n, it, a.k0, a.k1, a.sqrt_dt_f, a.cpl);  // a1
       stage(Ws, W + pk.w1t(), d * LDW);
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
       const float* b1 = P + nd.off_b1();
       gemm_n(Xs, Ws, d, w, [&](int p0, int j, float4 v) {                          // a3
         const float b = __ldg(b1 + j);
-        *reinterpret_cast<float4*>(H1 + j * TP + p0) =
+        *reinterpret_cast<float4*>(H1 + j * TPP + p0) =
             make_float4(fmaxf(v.x + b, 0.f), fmaxf(v.y + b, 0.f), fmaxf(v.z + b, 0.f), fmaxf(v.w + b, 0.f));
       });
       __syncthreads();
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
         __syncthreads();
         gemm_n(Xs, Ws, d, w, [&](int p0, int j, float4 v) {
           const float b = __ldg(b2 + j);
-          *reinterpret_cast<float4*>(H2 + j * TP + p0) = make_float4(v.x + b, v.y + b, v.z + b, v.w + b);
+          *reinterpret_cast<float4*>(H2 + j * TPP + p0) = make_float4(v.x + b, v.y + b, v.z + b, v.w + b);
         });
         __syncthreads();
       }
@@ -251,10 +255,10 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
       __syncthreads();
       gemm_n(H1, Ws, w, w, [&](int p0, int j, float4 v) {
         // A2 = W2 H1 + b2, or A H1 + (B X + C) for NAIS; H2 = H1 + ReLU(A2)
-        const float4 c = a.nais ? *reinterpret_cast<const float4*>(H2 + j * TP + p0)
+        const float4 c = a.nais ? *reinterpret_cast<const float4*>(H2 + j * TPP + p0)
                                 : make_float4(__ldg(b2 + j), __ldg(b2 + j), __ldg(b2 + j), __ldg(b2 + j));
-        const float4 h = *reinterpret_cast<const float4*>(H1 + j * TP + p0);
-        *reinterpret_cast<float4*>(H2 + j * TP + p0) =
+        const float4 h = *reinterpret_cast<const float4*>(H1 + j * TPP + p0);
+        *reinterpret_cast<float4*>(H2 + j * TPP + p0) =
             make_float4(h.x + fmaxf(v.x + c.x, 0.f), h.y + fmaxf(v.y + c.y, 0.f),
                         h.z + fmaxf(v.z + c.z, 0.f), h.w + fmaxf(v.w + c.w, 0.f));
       });
@@ -265,7 +269,7 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
       float c4[4] = {0, 0, 0, 0}, z4[4] = {0, 0, 0, 0}, s4[4] = {0, 0, 0, 0};
       gemm_n(H2, Ws, w, d, [&](int p0, int j, float4 v) {                          // a4 partials
         const float b = __ldg(b3 + j);
-        const float4 dw = *reinterpret_cast<const float4*>(dWs + j * TP + p0);
+        const float4 dw = *reinterpret_cast<const float4*>(dWs + j * TPP + p0);
         const float zv[4] = {v.x + b, v.y + b, v.z + b, v.w + b};
         const float wv[4] = {dw.x, dw.y, dw.z, dw.w};
 #pragma unroll
@@ -293,13 +297,13 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
           Ys[p] = y - driver_f(a.problem, y, z4[r], s4[r], a.lam) * a.dt + c4[r];
         }
       }
-      for (int i = t; i < d * TP; i += NT) Xs[i] = x_step(a.problem, Xs[i], dWs[i]);   // a2
+      for (int i = t; i < d * TPP; i += NT) Xs[i] = x_step(a.problem, Xs[i], dWs[i]);   // a2
       __syncthreads();
     }
     // a5: R = Y_N - g(X_N); loss; ā_N (times P_N) and dY0 = ā_0 = ā_N P_N
     if (t < TP && t < valid) {
       float s = 0.0f;
-      for (int k = 0; k < d; ++k) s = fmaf(Xs[k * TP + t], Xs[k * TP + t], s);
+      for (int k = 0; k < d; ++k) s = fmaf(Xs[k * TPP + t], Xs[k * TPP + t], s);
       const float R = Ys[t] - terminal_g(a.problem, s);
       const int64_t m = mloc0 + t;
       lsum += (double)R * R;
@@ -339,12 +343,12 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
   const NetDims nd{d, w, a.nais};
   const Pack pk{d, w, a.nais};
   float* Xs = sm;                         // [d][64]
-  float* dZ = Xs + d * TP;                // [d][64]  ΔW_n, then dZ_n in place
-  float* H1 = dZ + d * TP;                // [w][64]
-  float* H2 = H1 + w * TP;                // [w][64]
-  float* dH = H2 + w * TP;                // [w][64]  dH2, then dA1 in place
-  float* dA2 = dH + w * TP;               // [w][64]
-  float* Ws = dA2 + w * TP;               // [K <= max(d, w)][128]
+  float* dZ = Xs + d * TPP;               // [d][64]  ΔW_n, then dZ_n in place
+  float* H1 = dZ + d * TPP;               // [w][64]
+  float* H2 = H1 + w * TPP;               // [w][64]
+  float* dH = H2 + w * TPP;               // [w][64]  dH2, then dA1 in place
+  float* dA2 = dH + w * TPP;              // [w][64]
+  float* Ws = dA2 + w * TPP;              // [K <= max(d, w)][LDW]
   float* ab = Ws + (d > w ? d : w) * LDW; // [64]
   uint8_t* m2 = reinterpret_cast<uint8_t*>(ab + TP);   // [w][64] 1[A2 > 0]
   const float* wp = static_cast<const float*>(a.wpack);
@@ -382,7 +386,8 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
     const float* W = wp + (size_t)n * pk.per_step();
     {
       const float4* xs = reinterpret_cast<const float4*>(a.Xstore + ((size_t)n * ntiles + tile) * d * TP);
-      for (int i = t; i < d * TP / 4; i += NT) reinterpret_cast<float4*>(Xs)[i] = __ldg(xs + i);
+      for (int i = t; i < d * TP / 4; i += NT)
+        *reinterpret_cast<float4*>(Xs + (i >> 4) * TPP + 4 * (i & 15)) = __ldg(xs + i);
     }
     if (t < TP) {
       const int64_t m = mloc0 + t;
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
     const float* b1 = Pn + nd.off_b1();
     gemm_n(Xs, Ws, d, w, [&](int p0, int j, float4 v) {           // recompute H1
       const float b = __ldg(b1 + j);
-      *reinterpret_cast<float4*>(H1 + j * TP + p0) =
+      *reinterpret_cast<float4*>(H1 + j * TPP + p0) =
           make_float4(fmaxf(v.x + b, 0.f), fmaxf(v.y + b, 0.f), fmaxf(v.z + b, 0.f), fmaxf(v.w + b, 0.f));
     });
     __syncthreads();
@@ -405,18 +410,18 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
       __syncthreads();
       gemm_n(Xs, Ws, d, w, [&](int p0, int j, float4 v) {
         const float b = __ldg(b2 + j);
-        *reinterpret_cast<float4*>(H2 + j * TP + p0) = make_float4(v.x + b, v.y + b, v.z + b, v.w + b);
+        *reinterpret_cast<float4*>(H2 + j * TPP + p0) = make_float4(v.x + b, v.y + b, v.z + b, v.w + b);
       });
       __syncthreads();
     }
     stage(Ws, W + pk.w2t(), w * LDW);
     __syncthreads();
     gemm_n(H1, Ws, w, w, [&](int p0, int j, float4 v) {           // recompute H2, mask of A2
-      const float4 c = a.nais ? *reinterpret_cast<const float4*>(H2 + j * TP + p0)
+      const float4 c = a.nais ? *reinterpret_cast<const float4*>(H2 + j * TPP + p0)
                               : make_float4(__ldg(b2 + j), __ldg(b2 + j), __ldg(b2 + j), __ldg(b2 + j));
-      const float4 h = *reinterpret_cast<const float4*>(H1 + j * TP + p0);
+      const float4 h = *reinterpret_cast<const float4*>(H1 + j * TPP + p0);
       const float av[4] = {v.x + c.x, v.y + c.y, v.z + c.z, v.w + c.w};
-      *reinterpret_cast<float4*>(H2 + j * TP + p0) =
+      *reinterpret_cast<float4*>(H2 + j * TPP + p0) =
           make_float4(h.x + fmaxf(av[0], 0.f), h.y + fmaxf(av[1], 0.f), h.z + fmaxf(av[2], 0.f),
                       h.w + fmaxf(av[3], 0.f));
       uchar4 mk;
@@ -429,12 +434,12 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
     const float* b3 = Pn + nd.off_b3();
     gemm_n(H2, Ws, w, d, [&](int p0, int j, float4 v) {           // dZ = ā(ΔW - Δt ∂_z f)
       const float b = __ldg(b3 + j);
-      float4 dw = *reinterpret_cast<const float4*>(dZ + j * TP + p0);
+      float4 dw = *reinterpret_cast<const float4*>(dZ + j * TPP + p0);
       dw.x = ab[p0] * fmaf(zc, v.x + b, dw.x + zc0);
       dw.y = ab[p0 + 1] * fmaf(zc, v.y + b, dw.y + zc0);
       dw.z = ab[p0 + 2] * fmaf(zc, v.z + b, dw.z + zc0);
       dw.w = ab[p0 + 3] * fmaf(zc, v.w + b, dw.w + zc0);
-      *reinterpret_cast<float4*>(dZ + j * TP + p0) = dw;
+      *reinterpret_cast<float4*>(dZ + j * TPP + p0) = dw;
     });
     __syncthreads();
     stage(Ws, W + pk.w3n(), d * LDW);
@@ -442,9 +447,9 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
     gemm_t(dZ, d, H2, w, scratch + nd.off_W3(), w, scratch + nd.off_b3());
     __syncthreads();
     gemm_n(dZ, Ws, d, w, [&](int p0, int j, float4 v) {           // dH2 = dZ W3 ; dA2
-      *reinterpret_cast<float4*>(dH + j * TP + p0) = v;
+      *reinterpret_cast<float4*>(dH + j * TPP + p0) = v;
       const uchar4 mk = *reinterpret_cast<const uchar4*>(m2 + j * TP + p0);
-      *reinterpret_cast<float4*>(dA2 + j * TP + p0) =
+      *reinterpret_cast<float4*>(dA2 + j * TPP + p0) =
           make_float4(mk.x ? v.x : 0.f, mk.y ? v.y : 0.f, mk.z ? v.z : 0.f, mk.w ? v.w : 0.f);
     });
     __syncthreads();
@@ -454,9 +459,9 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
     if (a.nais) gemm_t(dA2, w, Xs, d, scratch + nd.off_B(), d, nullptr);   // B̄ += dA2ᵀ X (R25)
     __syncthreads();
     gemm_n(dA2, Ws, w, w, [&](int p0, int j, float4 v) {          // dA1 = (dH2 + dA2 W2) ⊙ 1[H1 > 0]
-      const float4 h = *reinterpret_cast<const float4*>(H1 + j * TP + p0);
-      const float4 g = *reinterpret_cast<const float4*>(dH + j * TP + p0);
-      *reinterpret_cast<float4*>(dH + j * TP + p0) =
+      const float4 h = *reinterpret_cast<const float4*>(H1 + j * TPP + p0);
+      const float4 g = *reinterpret_cast<const float4*>(dH + j * TPP + p0);
+      *reinterpret_cast<float4*>(dH + j * TPP + p0) =
           make_float4(h.x > 0.f ? g.x + v.x : 0.f, h.y > 0.f ? g.y + v.y : 0.f,
                       h.z > 0.f ? g.z + v.z : 0.f, h.w > 0.f ? g.w + v.w : 0.f);
     });
@@ -469,10 +474,10 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
 }
 
 size_t fwd_smem(int d, int w) {
-  return sizeof(float) * ((size_t)TP * (2 * d + 2 * w) + (size_t)(d > w ? d : w) * LDW + 2 * TP + 16);
+  return sizeof(float) * ((size_t)TPP * (2 * d + 2 * w) + (size_t)(d > w ? d : w) * LDW + 2 * TP + 16);
 }
 size_t bwd_smem(int d, int w) {
-  return sizeof(float) * ((size_t)TP * (2 * d + 4 * w) + (size_t)(d > w ? d : w) * LDW + TP) +
+  return sizeof(float) * ((size_t)TPP * (2 * d + 4 * w) + (size_t)(d > w ? d : w) * LDW + TP) +
          (size_t)w * TP;
 }
 int sm_count() {
@@ -484,7 +489,7 @@ int sm_count() {
 
 }  // namespace
 
-bool simt_supported(int d, int w) { return d <= 128 && w <= 128 && bwd_smem(d, w) <= 227 * 1024; }
+bool simt_supported(int d, int w) { return d <= LDW && w <= LDW && bwd_smem(d, w) <= 227 * 1024; }
 size_t simt_max_smem(int d, int w) { return fwd_smem(d, w) > bwd_smem(d, w) ? fwd_smem(d, w) : bwd_smem(d, w); }
 size_t simt_pack_bytes(int d, int w, int N, int nais) {
   return (size_t)N * Pack{d, w, nais}.per_step() * sizeof(float);
