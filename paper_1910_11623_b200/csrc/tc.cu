@@ -247,7 +247,7 @@ struct Impl {
     cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int nt = ntiles(a), sms = sm_count();
-    k_fwd_tc<D, W><<<nt < sms ? nt : sms, NTH, smem, s>>>(a, nt);
+    k_fwd_tc<D, W><<<nt < sms ? nt : sms, kFwdThreads, smem, s>>>(a, nt);
     return cudaGetLastError();
   }
   template <bool NEEDZ>

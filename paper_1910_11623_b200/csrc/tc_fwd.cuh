@@ -43,7 +43,12 @@ __device__ __forceinline__ void unpack_dw(const uint4& u, float* v) {
     v[2 * k + 1] = f.y;
   }
 }
-constexpr int kFwdProducers = 384, kFwdConsumers = 128;
+#ifndef BSDE_EXP_TPATH
+#define BSDE_EXP_TPATH 3
+#endif
+constexpr int kTPath = BSDE_EXP_TPATH;   // producer threads per path
+constexpr int kFwdProducers = 128 * kTPath, kFwdConsumers = 128;
+constexpr int kFwdThreads = kFwdProducers + kFwdConsumers, kFwdProdWarps = kFwdProducers / 32;
 __device__ __forceinline__ void consumer_sync() { named_sync(1, kFwdConsumers); }
 
 // Increments of Philox blocks q = 2c, 2c+1 (columns 8c..8c+7) for the chunks
@@ -108,7 +113,7 @@ struct FwdSmem {
   static constexpr uint32_t W3 = W2 + Dm::W2B;
   static constexpr int NSLOT = 4;                            // ring depth (steps)
   static constexpr uint32_t SLOT0 = W3 + Dm::W3B;
-  static constexpr uint32_t SLOTB = Dm::XB + 3 * 128 * 4;     // X̃_n | |X_N|² partials [3][128]
+  static constexpr uint32_t SLOTB = Dm::XB + 3 * 128 * 4;     // X̃_n | |X_N|² partials [kTPath][128]
   static constexpr uint32_t BARS = SLOT0 + NSLOT * SLOTB;
   // full[NSLOT], empty[NSLOT], wf1[2], wf2, wf3, g1, g23, w1free[2], w2free, w3free
   static constexpr int NBARS = 2 * NSLOT + 10;
@@ -130,7 +135,7 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
   using Dm = Dims<D, W>;
   using L = FwdSmem<D, W>;
   constexpr int Dp = Dm::Dp, NCD = Dp / 8;
-  constexpr int NI = (NCD + 2) / 3;        // image chunks of thread 0 (>= those of 1, 2)
+  constexpr int NI = (NCD + kTPath - 1) / kTPath;   // image chunks of thread 0 (>= the others')
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::BARS);
   uint64_t* full = bars;
   uint64_t* empty = bars + L::NSLOT;
@@ -199,7 +204,7 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
       // X̃_n chunk from X, ΔW_n chunk (fp16: TMEM ring + image), then X_{n+1}
       auto chunk_out = [&](auto ic, const float* dw) {
         constexpr int i = decltype(ic)::value;
-        const int c = K3 + 3 * i;
+        const int c = K3 + kTPath * i;
         if (c >= NCD) return;
         float v[8];
 #pragma unroll
@@ -237,7 +242,8 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
         if constexpr (i < NI) {
           constexpr int nch = (i + GRP <= NI) ? GRP : NI - i;
           float dw[nch * 8];
-          gen_chunks<D, 3, nch, CPL>(K3 + 3 * i, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt_f, dw, a.cpl);
+          gen_chunks<D, kTPath, nch, CPL>(K3 + kTPath * i, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt_f,
+                                          dw, a.cpl);
           chunk_out(Int<i>{}, dw);
           if constexpr (nch >= 2) chunk_out(Int<i + 1>{}, dw + 8);
           if constexpr (nch >= 3) chunk_out(Int<i + 2>{}, dw + 16);
@@ -256,7 +262,7 @@ __device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint
         for (int i = 0; i < NI; ++i)
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            if (8 * (K3 + 3 * i) + e < D) sx = fmaf(X[8 * i + e], X[8 * i + e], sx);
+            if (8 * (K3 + kTPath * i) + e < D) sx = fmaf(X[8 * i + e], X[8 * i + e], sx);
         xn2[K3 * 128 + row] = sx;
       }
       if (s < 64) BSDE_STAMP(pclk, s * 16 + 10);
@@ -458,7 +464,7 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
         e3(Int<0>{});
       if (n + 1 == N) {
         const float* x2 = reinterpret_cast<const float*>(slotp + Dm::XB);
-        xn2 = (x2[row] + x2[128 + row]) + x2[256 + row];
+        xn2 = kTPath == 3 ? (x2[row] + x2[128 + row]) + x2[256 + row] : x2[row] + x2[128 + row];
       }
       if (store && per_step_abar(a.problem)) {
         P *= 1.0f - a.dt * driver_dfdy(a.problem, Y);
@@ -487,7 +493,7 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
 }
 
 template <int D, int W>
-__global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
+__global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntiles) {
   using L = FwdSmem<D, W>;
   extern __shared__ __align__(1024) uint8_t sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::BARS);
@@ -509,7 +515,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
   float dy0 = 0.0f;
   // consumers on the high warp ids: the schedulers favour them (the chain is
   // latency-bound, the producers throughput-bound)
-  if (warp < 12) {   // one instance runs: X step and path coupling are compile-time choices
+  if (warp < kFwdProdWarps) {   // one instance runs: X step and path coupling are compile-time choices
     const int q = warp & 3, k3 = warp >> 2;
     const bool mult = a.problem == kBlackScholes;
     if (a.cpl > 1) {
@@ -528,7 +534,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fwd_tc(PassArgs a, int ntiles) {
     lw += __shfl_xor_sync(0xffffffffu, lw, o);
     gw += __shfl_xor_sync(0xffffffffu, gw, o);
   }
-  if (warp >= 12 && lane == 0) { lred[warp - 12] = lw; gred[warp - 12] = gw; }
+  if (warp >= kFwdProdWarps && lane == 0) { lred[warp - kFwdProdWarps] = lw; gred[warp - kFwdProdWarps] = gw; }
   tc_before();
   __syncthreads();
   if (t == 0) {
