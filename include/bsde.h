@@ -111,6 +111,12 @@ typedef struct {
                              u(t, x) of n_widths tanh layers shared by all steps, Y_n =
                              u(t_n, X_n), z_n = σ(X_n)ᵀ∇ₓu, residual-sum loss.  FP32 and the
                              SIMT kernels only                                              */
+  int sharded_adam;       /* 1 (with an NCCL communicator): reduce-scatter of the gradient,
+                             Adam on this rank's 1/world shard of the parameters, all-gather
+                             of the updated parameters (the optimizer half) in
+                             place of the allreduce + replicated Adam.  Same arithmetic; after
+                             bsde_train_step the gradient buffer holds the reduced values in
+                             this rank's shard only (bsde_compute_grad still allreduces)    */
   int arch;               /* BSDE_FORM_SHARED: BSDE_ARCH_FC, BSDE_ARCH_RESNET (h_k = h_{k-1}
                              + tanh(W_k h_{k-1} + b_k) for k >= 2) or
                              BSDE_ARCH_NAIS (h_k = h_{k-1} + tanh(A_k h_{k-1} + B_k u + C_k),

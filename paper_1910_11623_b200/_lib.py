@@ -54,6 +54,7 @@ class Config(ctypes.Structure):
         ("init_zero_head", ctypes.c_int),
         ("coupled_paths", ctypes.c_int),
         ("formulation", ctypes.c_int),
+        ("sharded_adam", ctypes.c_int),
         ("arch", ctypes.c_int),
     ]
 

@@ -5,6 +5,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -48,6 +49,10 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -64,9 +69,12 @@ NcclApi& nccl() {
     a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
     a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
     a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
+    a.ReduceScatter = (decltype(a.ReduceScatter))dlsym(h, "ncclReduceScatter");
+    a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
     a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
     a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
     a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.GroupStart &&
+           a.ReduceScatter && a.AllGather &&
            a.GroupEnd && a.GetErrorString;
     return a;
   }();
@@ -129,6 +137,12 @@ int fail(bsde_ctx* c, int code, const char* fmt, ...) {
     if (r_ != ncclSuccess)                                                              \
       return fail(ctx, BSDE_ENCCL, "%s: %s", #expr, nccl().GetErrorString(r_));         \
   } while (0)
+
+// sharded Adam (NEXT-4): parameters and gradient padded to world × shard floats, shard % 4 == 0
+int64_t shard_of(const bsde_ctx* c, int64_t np) {
+  const int64_t per = (np + c->cfg.world - 1) / c->cfg.world;
+  return (per + 3) / 4 * 4;
+}
 
 int64_t num_params_at(const bsde_ctx* c, int N) {
   if (c->shared) return (int64_t)shared_num_params(c->d, c->w, c->L, c->cfg.arch);   // independent of N
@@ -206,7 +220,9 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
   auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], ctx->stream); };
   int launches = 0;
   mark(0);
-  CK(launch_begin_step(ctx->state, ctx->grad, np, ctx->stream));
+  const bool sharded = ctx->comm && ctx->cfg.sharded_adam && with_update;
+  const int64_t shard = shard_of(ctx, np), npad = shard * ctx->cfg.world;
+  CK(launch_begin_step(ctx->state, ctx->grad, sharded ? npad : np, ctx->stream));
   launches += 1;   // k_begin_step (the memset is not a kernel)
   mark(1);
   if (ctx->shared) {
@@ -229,7 +245,16 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
     }
   }
   mark(3);
-  if (ctx->comm) {
+  const int64_t off = sharded ? shard * ctx->cfg.rank : 0;
+  const int64_t nloc = sharded ? std::max<int64_t>(0, std::min(shard, np - off)) : np;
+  if (sharded) {   // reduce-scatter: this rank's shard of the summed gradient, in place
+    NK(nccl().GroupStart());
+    NK(nccl().ReduceScatter(ctx->grad, ctx->grad + off, (size_t)shard, ncclFloat32, ncclSum,
+                            ctx->comm, ctx->stream));
+    NK(nccl().AllReduce(&ctx->state->loss_sum, &ctx->state->loss_sum, 1, ncclFloat64, ncclSum,
+                        ctx->comm, ctx->stream));
+    NK(nccl().GroupEnd());
+  } else if (ctx->comm) {
     NK(nccl().GroupStart());
     NK(nccl().AllReduce(ctx->grad, ctx->grad, (size_t)np, ncclFloat32, ncclSum, ctx->comm,
                         ctx->stream));
@@ -238,15 +263,21 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
     NK(nccl().GroupEnd());
   }
   mark(4);
-  CK(launch_check(ctx->grad, np, ctx->state, 1.0 / (double)ctx->cfg.batch_global,
+  CK(launch_check(ctx->grad + off, nloc, ctx->state, 1.0 / (double)ctx->cfg.batch_global,
                   (float)ctx->cfg.beta1, (float)ctx->cfg.beta2, ctx->stream));
   launches += 1;
+  if (sharded)   // a non-finite gradient in any shard skips the update on every rank
+    NK(nccl().AllReduce(&ctx->state->diverged, &ctx->state->diverged, 1, ncclInt32, ncclMax,
+                        ctx->comm, ctx->stream));
   mark(5);
   if (with_update) {
-    CK(launch_adam(ctx->params, ctx->grad, ctx->adam_m, ctx->adam_v, np, ctx->state,
-                   (float)ctx->cfg.lr, (float)ctx->cfg.beta1, (float)ctx->cfg.beta2,
+    CK(launch_adam(ctx->params + off, ctx->grad + off, ctx->adam_m + off, ctx->adam_v + off, nloc,
+                   ctx->state, (float)ctx->cfg.lr, (float)ctx->cfg.beta1, (float)ctx->cfg.beta2,
                    (float)ctx->cfg.eps, 1, ctx->stream));
     launches += 2;
+    if (sharded)   // every rank gets the updated parameters of every shard
+      NK(nccl().AllGather(ctx->params + off, ctx->params, (size_t)shard, ncclFloat32, ctx->comm,
+                          ctx->stream));
     if (ctx->nais) {   // projection of every R_n after the optimizer step (R25)
       CK(launch_nais_project(ctx->params, ctx->d, ctx->w, ctx->N, ctx->stream));
       launches += 1;
@@ -438,16 +469,17 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     ctx->own_stream = true;
   }
   const int64_t npmax = num_params_at(ctx, ctx->N_max);
+  const int64_t npalloc = std::max<int64_t>(npmax, shard_of(ctx, npmax) * cfg.world);   // NEXT-4 padding
   struct Alloc { void** p; size_t bytes; };
   // X_n store for the adjoint: fp32 rows (SIMT) or bf16 operand images (tcgen05)
   const size_t xs = shared ? 16
                    : family == BSDE_KERNEL_TC ? tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)
                                               : simt_xstore_bytes(d, ctx->N_max, ctx->B_local);
   std::vector<Alloc> allocs = {
-      {(void**)&ctx->params, npmax * sizeof(float)},
-      {(void**)&ctx->grad, npmax * sizeof(float)},
-      {(void**)&ctx->adam_m, npmax * sizeof(float)},
-      {(void**)&ctx->adam_v, npmax * sizeof(float)},
+      {(void**)&ctx->params, npalloc * sizeof(float)},
+      {(void**)&ctx->grad, npalloc * sizeof(float)},
+      {(void**)&ctx->adam_m, npalloc * sizeof(float)},
+      {(void**)&ctx->adam_v, npalloc * sizeof(float)},
       {(void**)&ctx->scratch, npmax * sizeof(float)},
       {(void**)&ctx->Xstore, xs},
       {(void**)&ctx->abar, (size_t)ctx->B_local * sizeof(float)},
@@ -478,8 +510,9 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
       return bail(BSDE_ENOMEM);
     }
   }
-  cudaMemsetAsync(ctx->adam_m, 0, npmax * sizeof(float), ctx->stream);
-  cudaMemsetAsync(ctx->adam_v, 0, npmax * sizeof(float), ctx->stream);
+  cudaMemsetAsync(ctx->adam_m, 0, npalloc * sizeof(float), ctx->stream);
+  cudaMemsetAsync(ctx->adam_v, 0, npalloc * sizeof(float), ctx->stream);
+  cudaMemsetAsync(ctx->params, 0, npalloc * sizeof(float), ctx->stream);
   cudaMemsetAsync(ctx->state, 0, sizeof(DeviceState), ctx->stream);
   const cudaError_t ie =
       shared ? launch_shared_init(ctx->params, sh_args(ctx), (uint32_t)(cfg.seed & 0xffffffffu),

@@ -54,7 +54,7 @@ class BSDE:
                  kernel="auto", x0=0.0, lam=1.0, prolong="copy", max_levels=0, device=0,
                  stream=None, rank=0, world=1, nccl_id=None, use_graph=True, beta1=0.9,
                  beta2=0.999, eps=1e-8, zero_head=None, coupled_paths=False,
-                 formulation="per_step", arch="fc", layers=4):
+                 formulation="per_step", arch="fc", layers=4, sharded_adam=False):
         """stream: a torch.cuda.Stream, a raw cudaStream_t (int), or None (a new
         torch stream on `device`, kept in self.stream).  zero_head: R7b, defaults
         to True for Allen-Cahn.  coupled_paths: every level draws the finest grid's
@@ -93,6 +93,7 @@ class BSDE:
         cfg.use_graph = int(bool(use_graph))
         cfg.coupled_paths = int(bool(coupled_paths))
         cfg.formulation = FORMULATIONS[formulation]
+        cfg.sharded_adam = int(bool(sharded_adam))
         cfg.arch = ARCHS[arch]
         self.formulation, self.arch, self.layers = formulation, arch, int(layers)
         self.problem = PROBLEMS[problem] if isinstance(problem, str) else int(problem)
