@@ -117,6 +117,12 @@ typedef struct {
                              place of the allreduce + replicated Adam.  Same arithmetic; after
                              bsde_train_step the gradient buffer holds the reduced values in
                              this rank's shard only (bsde_compute_grad still allreduces)    */
+  void* workspace;        /* optional caller-owned device memory (e.g. a torch tensor) of
+                             workspace_bytes >= bsde_workspace_bytes(): every device buffer
+                             of the context is carved from it (256-byte aligned) and nothing
+                             is cudaMalloc'ed; it must outlive the context.  NULL: the
+                             library allocates and frees its own buffers                   */
+  size_t workspace_bytes;
   int arch;               /* BSDE_FORM_SHARED: BSDE_ARCH_FC, BSDE_ARCH_RESNET (h_k = h_{k-1}
                              + tanh(W_k h_{k-1} + b_k) for k >= 2) or
                              BSDE_ARCH_NAIS (h_k = h_{k-1} + tanh(A_k h_{k-1} + B_k u + C_k),
@@ -149,6 +155,13 @@ void bsde_config_default(bsde_config* cfg);
  * precision/kernel combination), ENOMEM, ECUDA, ENCCL. */
 int bsde_create(int problem, int d, int N, double T, const int* widths, int n_widths,
                 const bsde_config* cfg, bsde_ctx** out);
+
+/* Device bytes a context with these arguments needs (the size of cfg.workspace
+ * to pass to bsde_create); same validation and errors as bsde_create; nothing is
+ * allocated, no stream or communicator is created (works without a GPU).  (T
+ * does not change the size.) */
+int bsde_workspace_bytes(int problem, int d, int N, const int* widths, int n_widths,
+                         const bsde_config* cfg, size_t* bytes);
 
 /* One training iteration: Philox ΔW for global
  * iteration `it`, forward rollout, terminal loss, adjoint, gradient allreduce

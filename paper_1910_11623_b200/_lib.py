@@ -20,7 +20,7 @@ ERROR_NAMES = {EINVAL: "EINVAL", ECUDA: "ECUDA", ENCCL: "ENCCL", EDIVERGED: "EDI
 
 # every symbol include/bsde.h declares (checked by tests/test_abi.py)
 SYMBOLS = [
-    "bsde_config_default", "bsde_create", "bsde_train_step", "bsde_prolongate", "bsde_y0",
+    "bsde_config_default", "bsde_create", "bsde_workspace_bytes", "bsde_train_step", "bsde_prolongate", "bsde_y0",
     "bsde_num_params", "bsde_get_params", "bsde_set_params", "bsde_get_grads",
     "bsde_get_adam_state", "bsde_set_adam_state", "bsde_get_iteration", "bsde_set_iteration",
     "bsde_current_steps", "bsde_compute_grad", "bsde_eval_loss", "bsde_debug_philox",
@@ -55,6 +55,8 @@ class Config(ctypes.Structure):
         ("coupled_paths", ctypes.c_int),
         ("formulation", ctypes.c_int),
         ("sharded_adam", ctypes.c_int),
+        ("workspace", ctypes.c_void_p),
+        ("workspace_bytes", ctypes.c_size_t),
         ("arch", ctypes.c_int),
     ]
 
@@ -78,6 +80,8 @@ def lib():
             "bsde_create": (I32, [I32, I32, I32, D, ctypes.POINTER(I32), I32,
                                   ctypes.POINTER(Config), ctypes.POINTER(P)]),
             "bsde_train_step": (I32, [P, pD]),
+            "bsde_workspace_bytes": (I32, [I32, I32, I32, ctypes.POINTER(I32), I32,
+                                           ctypes.POINTER(Config), ctypes.POINTER(ctypes.c_size_t)]),
             "bsde_compute_grad": (I32, [P, pD]),
             "bsde_prolongate": (I32, [P, I32]),
             "bsde_y0": (I32, [P, pD]),

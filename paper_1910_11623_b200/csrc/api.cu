@@ -40,6 +40,7 @@ using namespace bsde;
 namespace {
 
 thread_local std::string g_create_error;
+thread_local size_t* g_dry_run = nullptr;   // set by bsde_workspace_bytes around bsde_create
 
 // ---- NCCL, resolved at run time --------------------------------------------
 struct NcclApi {
@@ -89,6 +90,7 @@ struct bsde_ctx {
   int nais = 0;                 // per-step nets with the NAIS-Net block (NEXT-2, R25)
   int L = 0;                    // shared: number of tanh layers
   void* shbuf = nullptr;        // shared: row buffers (carved into ShArgs)
+  bool external_ws = false;     // buffers carved from cfg.workspace (caller-owned)
   double T = 1.0;
   bsde_config cfg{};
   int64_t B_local = 0, m0 = 0;
@@ -313,6 +315,11 @@ int repack(bsde_ctx* ctx) {
 
 void free_all(bsde_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->external_ws) {   // nothing of ours to free but the communicator and the stream
+    if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    return;
+  }
   void* bufs[] = {c->params, c->grad, c->adam_m, c->adam_v, c->scratch, c->Xstore, c->Pstore,
                   c->abar, c->Rstore, c->wpack, c->xpack, c->gpart, c->state,
                   c->eval_loss, c->shbuf};
@@ -455,19 +462,6 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     delete ctx;
     return code;
   };
-  {
-    cudaError_t e = cudaSetDevice(cfg.device);
-    if (e != cudaSuccess) { ctx->err = std::string("cudaSetDevice: ") + cudaGetErrorString(e); return bail(BSDE_ECUDA); }
-  }
-  if (cfg.stream) {
-    ctx->stream = (cudaStream_t)cfg.stream;
-  } else {
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
-      ctx->err = "cudaStreamCreate failed";
-      return bail(BSDE_ECUDA);
-    }
-    ctx->own_stream = true;
-  }
   const int64_t npmax = num_params_at(ctx, ctx->N_max);
   const int64_t npalloc = std::max<int64_t>(npmax, shard_of(ctx, npmax) * cfg.world);   // NEXT-4 padding
   struct Alloc { void** p; size_t bytes; };
@@ -501,13 +495,47 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     allocs.push_back({&ctx->wpack, simt_pack_bytes(d, w, ctx->N_max, nais)});
     allocs.push_back({(void**)&ctx->gpart, simt_scratch_bytes(d, w, nais)});
   }
-  for (auto& al : allocs) {
-    cudaError_t e = cudaMalloc(al.p, al.bytes);
-    if (e != cudaSuccess) {
-      char b[256];
-      snprintf(b, sizeof b, "cudaMalloc(%zu bytes): %s", al.bytes, cudaGetErrorString(e));
-      ctx->err = b;
-      return bail(BSDE_ENOMEM);
+  size_t ws_total = 0;
+  for (auto& al : allocs) ws_total += (al.bytes + 255) / 256 * 256;
+  if (g_dry_run) {   // bsde_workspace_bytes
+    *g_dry_run = ws_total;
+    delete ctx;
+    return BSDE_OK;
+  }
+  {
+    cudaError_t e = cudaSetDevice(cfg.device);
+    if (e != cudaSuccess) { ctx->err = std::string("cudaSetDevice: ") + cudaGetErrorString(e); return bail(BSDE_ECUDA); }
+  }
+  if (cfg.stream) {
+    ctx->stream = (cudaStream_t)cfg.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      ctx->err = "cudaStreamCreate failed";
+      return bail(BSDE_ECUDA);
+    }
+    ctx->own_stream = true;
+  }
+  if (cfg.workspace) {   // carve every buffer from the caller's memory
+    if (cfg.workspace_bytes < ws_total || ((uintptr_t)cfg.workspace & 255u)) {
+      ctx->err = "workspace too small or not 256-byte aligned (need " + std::to_string(ws_total) +
+                 " bytes)";
+      return bail(BSDE_EINVAL);
+    }
+    uint8_t* base = static_cast<uint8_t*>(cfg.workspace);
+    for (auto& al : allocs) {
+      *al.p = base;
+      base += (al.bytes + 255) / 256 * 256;
+    }
+    ctx->external_ws = true;
+  } else {
+    for (auto& al : allocs) {
+      cudaError_t e = cudaMalloc(al.p, al.bytes);
+      if (e != cudaSuccess) {
+        char b[256];
+        snprintf(b, sizeof b, "cudaMalloc(%zu bytes): %s", al.bytes, cudaGetErrorString(e));
+        ctx->err = b;
+        return bail(BSDE_ENOMEM);
+      }
     }
   }
   cudaMemsetAsync(ctx->adam_m, 0, npalloc * sizeof(float), ctx->stream);
@@ -540,6 +568,16 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
   }
   *out = ctx;
   return BSDE_OK;
+}
+
+int bsde_workspace_bytes(int problem, int d, int N, const int* widths, int n_widths,
+                         const bsde_config* cfg, size_t* bytes) {
+  if (!bytes) return fail(nullptr, BSDE_EINVAL, "bytes is NULL");
+  bsde_ctx* none = nullptr;
+  g_dry_run = bytes;
+  const int rc = bsde_create(problem, d, N, 1.0, widths, n_widths, cfg, &none);
+  g_dry_run = nullptr;
+  return rc;
 }
 
 int bsde_train_step(bsde_ctx* ctx, double* loss_out) {

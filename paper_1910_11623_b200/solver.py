@@ -47,6 +47,28 @@ def step_size(d, w):
     return 2 * d * w + w * w + 2 * w + d
 
 
+def workspace_bytes(problem, d, N, width, batch, *, precision="fp32", kernel="auto", world=1,
+                    max_levels=0, formulation="per_step", arch="fc", layers=4, sharded_adam=False):
+    """bsde_workspace_bytes: device bytes of a context (no GPU needed)."""
+    L = _lib.lib()
+    cfg = _lib.Config()
+    L.bsde_config_default(ctypes.byref(cfg))
+    cfg.batch_global, cfg.world = int(batch), int(world)
+    cfg.precision = PRECISIONS[precision] if isinstance(precision, str) else int(precision)
+    cfg.kernel = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
+    cfg.max_levels = int(max_levels)
+    cfg.formulation, cfg.arch = FORMULATIONS[formulation], ARCHS[arch]
+    cfg.sharded_adam = int(bool(sharded_adam))
+    nw = int(layers) if formulation == "shared" else 2
+    widths = (ctypes.c_int * nw)(*([int(width)] * nw))
+    out = ctypes.c_size_t()
+    p = PROBLEMS[problem] if isinstance(problem, str) else int(problem)
+    rc = L.bsde_workspace_bytes(p, int(d), int(N), widths, nw, ctypes.byref(cfg), ctypes.byref(out))
+    if rc:
+        raise BSDEError(rc, L.bsde_last_error(None).decode())
+    return out.value
+
+
 class BSDE:
     """bsde_create(problem, d, N, T, widths) + the step / level / introspection calls."""
 
@@ -54,7 +76,8 @@ class BSDE:
                  kernel="auto", x0=0.0, lam=1.0, prolong="copy", max_levels=0, device=0,
                  stream=None, rank=0, world=1, nccl_id=None, use_graph=True, beta1=0.9,
                  beta2=0.999, eps=1e-8, zero_head=None, coupled_paths=False,
-                 formulation="per_step", arch="fc", layers=4, sharded_adam=False):
+                 formulation="per_step", arch="fc", layers=4, sharded_adam=False,
+                 workspace=None):
         """stream: a torch.cuda.Stream, a raw cudaStream_t (int), or None (a new
         torch stream on `device`, kept in self.stream).  zero_head: R7b, defaults
         to True for Allen-Cahn.  coupled_paths: every level draws the finest grid's
@@ -94,6 +117,10 @@ class BSDE:
         cfg.coupled_paths = int(bool(coupled_paths))
         cfg.formulation = FORMULATIONS[formulation]
         cfg.sharded_adam = int(bool(sharded_adam))
+        if workspace is not None:   # caller-owned device memory (a torch tensor), kept alive
+            self._workspace = workspace
+            cfg.workspace = workspace.data_ptr()
+            cfg.workspace_bytes = workspace.numel() * workspace.element_size()
         cfg.arch = ARCHS[arch]
         self.formulation, self.arch, self.layers = formulation, arch, int(layers)
         self.problem = PROBLEMS[problem] if isinstance(problem, str) else int(problem)

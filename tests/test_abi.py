@@ -63,3 +63,21 @@ def test_create_rejects_bad_arguments(libpath, kw, msg):
         BSDE(args.pop("problem"), args.pop("d"), args.pop("N"), args.pop("T"), args.pop("width"),
              args.pop("batch"), world=world, stream=0, **args)
     assert msg in str(e.value) and e.value.code == -1
+
+
+def test_workspace_bytes_without_gpu(libpath):
+    """bsde_workspace_bytes: sizes a context with the create-time
+    validation and no allocation, so it runs on the CPU box; it grows with the
+    batch and the time grid and rejects what bsde_create rejects."""
+    from paper_1910_11623_b200 import BSDEError
+    from paper_1910_11623_b200.solver import workspace_bytes
+    a = workspace_bytes("allen_cahn", 100, 80, 110, 524288, precision="bf16")
+    b = workspace_bytes("allen_cahn", 100, 80, 110, 262144, precision="bf16")
+    c = workspace_bytes("allen_cahn", 100, 40, 110, 524288, precision="bf16")
+    assert a > b > 0 and a > c > 0
+    # config 5 holds the X̃ and ΔW images: 2 × 224 B per path-step at least
+    assert a >= 2 * 224 * 524288 * 80
+    s = workspace_bytes("black_scholes", 100, 50, 256, 100, formulation="shared", layers=4)
+    assert s > 0
+    with pytest.raises(BSDEError):
+        workspace_bytes("heat", 0, 2, 8, 16)

@@ -265,3 +265,23 @@ def test_graph_replay_equals_eager():
     lb = [b.train_step() for _ in range(5)]
     assert np.allclose(la, lb, rtol=1e-6)
     assert np.allclose(a.get_params(), b.get_params(), rtol=1e-5, atol=1e-7)
+
+
+def test_torch_workspace_context_matches_own_allocations():
+    """cfg.workspace: a context carved from a torch tensor of
+    bsde_workspace_bytes() trains exactly like one with its own allocations."""
+    import torch
+    from paper_1910_11623_b200.solver import workspace_bytes
+    d, w, N, B = 12, 16, 3, 128
+    nbytes = workspace_bytes("hjb", d, N, w, B)
+    ws = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+    off = (-ws.data_ptr()) % 256
+    view = ws[off:off + nbytes]
+    a = make("hjb", d, w, N, 1.0, B, kernel="simt")
+    b = make("hjb", d, w, N, 1.0, B, kernel="simt", workspace=view)
+    for _ in range(3):
+        assert a.train_step() == b.train_step()
+    assert np.array_equal(a.get_params(), b.get_params())
+    small = ws[off:off + nbytes // 2]
+    with pytest.raises(Exception):
+        make("hjb", d, w, N, 1.0, B, kernel="simt", workspace=small)
