@@ -228,6 +228,8 @@ def main():
     ap.add_argument("--precision", default=None)
     ap.add_argument("--ref-paths", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="fixed-order reductions instead of atomics (cfg.deterministic)")
     ap.add_argument("--sharded-adam", action="store_true",
                     help="reduce-scatter + sharded Adam + all-gather (NEXT-4) for N > 1")
     args = ap.parse_args()
@@ -256,6 +258,8 @@ def main():
         kw.update(formulation="shared", arch=wl.arch, layers=wl.layers)
     if args.sharded_adam:
         kw.update(sharded_adam=True)
+    if args.deterministic:
+        kw.update(deterministic=True)
     if world > 1:
         s = BSDE.distributed(wl.problem, wl.d, wl.N, wl.T, wl.w, wl.batch, **kw)
     else:

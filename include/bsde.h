@@ -117,6 +117,11 @@ typedef struct {
                              place of the allreduce + replicated Adam.  Same arithmetic; after
                              bsde_train_step the gradient buffer holds the reduced values in
                              this rank's shard only (bsde_compute_grad still allreduces)    */
+  int deterministic;      /* 1: fixed-order cross-CTA reductions (per-CTA partials of the
+                             gradient, loss and dY0 summed in CTA order by one kernel) in
+                             place of fp32/fp64 atomics, so repeated runs of the per-step
+                             formulation are bitwise identical (SPEC determinism
+                             invariant); the shared formulation rejects it (EINVAL)        */
   void* workspace;        /* optional caller-owned device memory (e.g. a torch tensor) of
                              workspace_bytes >= bsde_workspace_bytes(): every device buffer
                              of the context is carved from it (256-byte aligned) and nothing

@@ -91,6 +91,10 @@ struct bsde_ctx {
   int L = 0;                    // shared: number of tanh layers
   void* shbuf = nullptr;        // shared: row buffers (carved into ShArgs)
   bool external_ws = false;     // buffers carved from cfg.workspace (caller-owned)
+  int sms = 148;                // SM count (grid sizes of the deterministic partials)
+  float* dpart = nullptr;       // deterministic mode: adjoint partials
+  double* lpart = nullptr;      // deterministic mode: forward loss partials [256]
+  float* y0part = nullptr;      // deterministic mode: forward dY0 partials [256]
   double T = 1.0;
   bsde_config cfg{};
   int64_t B_local = 0, m0 = 0;
@@ -144,6 +148,18 @@ int fail(bsde_ctx* c, int code, const char* fmt, ...) {
 int64_t shard_of(const bsde_ctx* c, int64_t np) {
   const int64_t per = (np + c->cfg.world - 1) / c->cfg.world;
   return (per + 3) / 4 * 4;
+}
+
+// launch geometry of the per-step kernels (tc.cu / simt.cu launchers): tiles of
+// 128 (tcgen05) or 64 (SIMT) paths, forward grid min(tiles, SMs), adjoint grid
+// min(N·tiles, SMs)
+void det_geometry(const bsde_ctx* c, int N, int* fwd_grid, int* bwd_grid, int* ntiles,
+                  int64_t* items) {
+  const int tile = c->family == BSDE_KERNEL_TC ? 128 : 64;
+  *ntiles = (int)((c->B_local + tile - 1) / tile);
+  *items = (int64_t)N * *ntiles;
+  *fwd_grid = *ntiles < c->sms ? *ntiles : c->sms;
+  *bwd_grid = (int)(*items < c->sms ? *items : c->sms);
 }
 
 int64_t num_params_at(const bsde_ctx* c, int N) {
@@ -211,6 +227,15 @@ PassArgs pass_args(bsde_ctx* c) {
   a.dwpack = c->xpack;
   a.precision = c->cfg.precision;
   a.nais = c->nais;
+  if (c->cfg.deterministic) {
+    a.dpart = c->dpart;
+    a.lpart = c->lpart;
+    a.y0part = c->y0part;
+    int fg, bg, nt;
+    int64_t items;
+    det_geometry(c, c->N, &fg, &bg, &nt, &items);
+    a.dseg = det_segments(items, bg, nt);
+  }
   return a;
 }
 
@@ -236,11 +261,25 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
     mark(2);
     CK(launch_bwd_tc(a, ctx->stream));
     launches += 2;
+    if (ctx->cfg.deterministic) {
+      int fg, bg, nt;
+      int64_t items;
+      det_geometry(ctx, ctx->N, &fg, &bg, &nt, &items);
+      CK(launch_det_reduce(a, fg, bg, items, nt, ctx->stream));
+      launches += 1;
+    }
   } else {
     CK(launch_fwd_simt(a, ctx->stream));
     mark(2);
     CK(launch_bwd_simt(a, ctx->stream));
     launches += 2;
+    if (ctx->cfg.deterministic) {
+      int fg, bg, nt;
+      int64_t items;
+      det_geometry(ctx, ctx->N, &fg, &bg, &nt, &items);
+      CK(launch_det_reduce(a, fg, bg, items, nt, ctx->stream));
+      launches += 1;
+    }
     if (ctx->nais) {   // Ā (W2 slot) -> R̄ = -R(Ā + Āᵀ), R25
       CK(launch_nais_grad(ctx->params, ctx->grad, ctx->d, ctx->w, ctx->N, ctx->stream));
       launches += 1;
@@ -322,7 +361,7 @@ void free_all(bsde_ctx* c) {
   }
   void* bufs[] = {c->params, c->grad, c->adam_m, c->adam_v, c->scratch, c->Xstore, c->Pstore,
                   c->abar, c->Rstore, c->wpack, c->xpack, c->gpart, c->state,
-                  c->eval_loss, c->shbuf};
+                  c->eval_loss, c->shbuf, c->dpart, c->lpart, c->y0part};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
@@ -392,6 +431,8 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
       return fail(none, BSDE_EINVAL, "arch=%d", cfg.arch);
     if (cfg.precision != BSDE_FP32 || cfg.kernel == BSDE_KERNEL_TC)
       return fail(none, BSDE_EINVAL, "the shared formulation runs fp32 SIMT kernels only");
+    if (cfg.deterministic)
+      return fail(none, BSDE_EINVAL, "deterministic mode covers the per-step formulation only");
   } else if (!widths || n_widths != 2 || widths[0] != widths[1] || widths[0] < 1) {
     return fail(none, BSDE_EINVAL,
                 "widths must be {w, w} with w >= 1 (d->w->w->d residual net, R4); got n_widths=%d",
@@ -462,6 +503,23 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     delete ctx;
     return code;
   };
+  {
+    int dev = cfg.device, nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
+      ctx->sms = nsm;
+    else
+      cudaGetLastError();   // no device (bsde_workspace_bytes on a CPU box): keep 148
+  }
+  size_t det_floats = 0;   // deterministic mode: max over the levels of grid × segments × P_step
+  if (cfg.deterministic && !shared) {
+    const int64_t P = NetDims{d, w, nais}.step_size();
+    for (int l = 0, Nl = N; l <= cfg.max_levels; ++l, Nl *= 2) {
+      int fg, bg, nt;
+      int64_t items;
+      det_geometry(ctx, Nl, &fg, &bg, &nt, &items);
+      det_floats = std::max(det_floats, (size_t)bg * det_segments(items, bg, nt) * P);
+    }
+  }
   const int64_t npmax = num_params_at(ctx, ctx->N_max);
   const int64_t npalloc = std::max<int64_t>(npmax, shard_of(ctx, npmax) * cfg.world);   // NEXT-4 padding
   struct Alloc { void** p; size_t bytes; };
@@ -481,6 +539,11 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
       {(void**)&ctx->state, sizeof(DeviceState)},
       {(void**)&ctx->eval_loss, sizeof(double) * 2},
   };
+  if (det_floats) {
+    allocs.push_back({(void**)&ctx->dpart, det_floats * sizeof(float)});
+    allocs.push_back({(void**)&ctx->lpart, 256 * sizeof(double)});
+    allocs.push_back({(void**)&ctx->y0part, 256 * sizeof(float)});
+  }
   if (shared) {
     allocs.push_back({&ctx->shbuf, shared_buffer_bytes(d, w, ctx->L, cfg.arch, ctx->N_max,
                                                        ctx->B_local)});
@@ -796,6 +859,11 @@ int bsde_eval_loss(bsde_ctx* ctx, uint32_t eval_id, int64_t batch, double* loss_
   } else {
     CK(cudaMemsetAsync(ctx->eval_loss, 0, sizeof(double), ctx->stream));
     CK(launch_fwd_simt(a, ctx->stream));
+  }
+  if (!ctx->shared && ctx->cfg.deterministic) {   // the eval batch's own forward grid
+    const int tile = ctx->family == BSDE_KERNEL_TC ? 128 : 64;
+    const int nt = (int)((a.B_local + tile - 1) / tile);
+    CK(launch_det_reduce(a, nt < ctx->sms ? nt : ctx->sms, 0, 1, nt, ctx->stream));
   }
   if (ctx->comm)
     NK(nccl().AllReduce(ctx->eval_loss, ctx->eval_loss, 1, ncclFloat64, ncclSum, ctx->comm,

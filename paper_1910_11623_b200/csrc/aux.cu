@@ -97,6 +97,40 @@ __global__ void k_nais_grad(const float* __restrict__ params, float* __restrict_
   }
 }
 
+// Deterministic reduction (cfg.deterministic): one thread per (step, parameter)
+// sums the adjoint CTAs' partials in CTA order; block 0 thread 0 also sums the
+// forward CTAs' loss and dY0 partials.  CTA c of the adjoint owns items
+// [c·items/G, (c+1)·items/G), item = n·ntiles + tile.
+__global__ void k_det_reduce(PassArgs a, int fwd_grid, int bwd_grid, int64_t items, int ntiles) {
+  const NetDims nd{a.d, a.w, a.nais};
+  const int64_t P = nd.step_size();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double L = 0.0;
+    float g0 = 0.0f;
+    for (int c = 0; c < fwd_grid; ++c) { L += a.lpart[c]; g0 += a.y0part[c]; }
+    *a.loss_acc += L;
+    if (!a.eval) a.grad[0] += g0;
+  }
+  if (bwd_grid == 0) return;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < (int64_t)a.N * P;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(id / P);
+    const int64_t i = id - (int64_t)n * P;
+    // CTAs covering step n: i1(c) > n·ntiles and i0(c) < (n+1)·ntiles
+    const int64_t lo_item = (int64_t)n * ntiles, hi_item = lo_item + ntiles;
+    int c = max(0, (int)((lo_item * bwd_grid) / items) - 1);
+    float v = 0.0f;
+    for (; c < bwd_grid; ++c) {
+      const int64_t i0 = (int64_t)c * items / bwd_grid, i1 = (int64_t)(c + 1) * items / bwd_grid;
+      if (i0 >= hi_item) break;
+      if (i1 <= lo_item || i0 >= i1) continue;
+      const int seg = n - (int)(i0 / ntiles);
+      v += a.dpart[((int64_t)c * a.dseg + seg) * P + i];
+    }
+    a.grad[nd.step_base(n) + i] = v;
+  }
+}
+
 __global__ void k_begin_step(DeviceState* st) {
   st->loss_sum = 0.0;
   st->diverged = 0;
@@ -209,6 +243,22 @@ cudaError_t launch_init_params(float* params, int d, int w, int N, uint32_t k0, 
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && nais) e = launch_nais_project(params, d, w, N, s);   // R25: init projected
   return e;
+}
+
+int det_segments(int64_t items, int grid, int ntiles) {
+  int best = 1;
+  for (int c = 0; c < grid; ++c) {
+    const int64_t i0 = (int64_t)c * items / grid, i1 = (int64_t)(c + 1) * items / grid;
+    if (i1 > i0) best = max(best, (int)((i1 - 1) / ntiles - i0 / ntiles + 1));
+  }
+  return best;
+}
+
+cudaError_t launch_det_reduce(const PassArgs& a, int fwd_grid, int bwd_grid, int64_t items,
+                              int ntiles, cudaStream_t s) {
+  const int64_t work = bwd_grid ? (int64_t)a.N * NetDims{a.d, a.w, a.nais}.step_size() : 1;
+  k_det_reduce<<<grid_for(work), NT, 0, s>>>(a, fwd_grid, bwd_grid, items, ntiles);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_nais_project(float* params, int d, int w, int N, cudaStream_t s) {

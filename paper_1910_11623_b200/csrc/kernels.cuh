@@ -35,6 +35,12 @@ struct PassArgs {
   unsigned long long* clk;             // debug: per-phase clock64() trace of CTA 0 (or null)
   int precision;
   int nais;                            // NAIS-Net block in the per-step nets (R25)
+  // deterministic mode (cfg.deterministic): the kernels write per-CTA partials in
+  // place of cross-CTA atomics and k_det_reduce sums them in a fixed order
+  float* dpart;                        // [grid][dseg][P_step] adjoint gradient partials
+  int dseg;                            // step segments per adjoint CTA
+  double* lpart;                       // [forward grid] Σ R² partials
+  float* y0part;                       // [forward grid] dY0 partials
   int cpl;                             // coupled paths: fine steps per step (1 = uncoupled)
   float sqrt_dt_f;                     // √(Δt/cpl)
 };
@@ -77,6 +83,13 @@ cudaError_t launch_shared_init(float* params, const ShArgs& a, uint32_t k0, uint
 cudaError_t launch_shared_point(const ShArgs& a, float* out, cudaStream_t s);
 cudaError_t launch_shared_nais_project(const ShArgs& a, float* params, cudaStream_t s);
 cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid, int* launches);
+
+// deterministic reduction of the partials (aux.cu): grad[step n] = Σ_c dpart[c][n - n_first(c)]
+// over the adjoint CTAs c covering step n in ascending order, grad[0] = Σ_c y0part[c],
+// *loss_acc = Σ_c lpart[c] (fixed order); bwd_grid = 0 for a forward-only (eval) pass
+cudaError_t launch_det_reduce(const PassArgs& a, int fwd_grid, int bwd_grid, int64_t items,
+                              int ntiles, cudaStream_t s);
+int det_segments(int64_t items, int grid, int ntiles);
 
 // SIMT fp32 kernels (simt.cu)
 cudaError_t launch_fwd_simt(const PassArgs& a, cudaStream_t s);

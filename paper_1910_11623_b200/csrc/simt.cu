@@ -331,9 +331,14 @@ __global__ void __launch_bounds__(NT, 1) k_fwd_simt(PassArgs a, int ntiles) {
   __syncthreads();
   if (t == 0) {
     const double L = lred[0] + lred[1];
-    if (L != 0.0) atomicAdd(a.loss_acc, L);
     const float g0 = gred[0] + gred[1];
-    if (!a.eval && g0 != 0.0f) atomicAdd(a.grad, g0);
+    if (a.lpart) {   // deterministic mode: per-CTA partials, summed in order by k_det_reduce
+      a.lpart[blockIdx.x] = L;
+      a.y0part[blockIdx.x] = a.eval ? 0.0f : g0;
+    } else {
+      if (L != 0.0) atomicAdd(a.loss_acc, L);
+      if (!a.eval && g0 != 0.0f) atomicAdd(a.grad, g0);
+    }
   }
 }
 
@@ -363,11 +368,19 @@ __global__ void __launch_bounds__(NT, 1) k_bwd_simt(PassArgs a, int ntiles, int6
 
   auto flush = [&]() {   // scratch -> gradient of step cur_n (fp32 atomics), then zero
     __syncthreads();
-    float* G = a.grad + nd.step_base(cur_n);
-    for (int64_t i = t; i < P; i += NT) {
-      const float v = scratch[i];
-      if (v != 0.0f) atomicAdd(G + i, v);
-      scratch[i] = 0.0f;
+    if (a.dpart) {   // deterministic mode: this CTA's partial of step cur_n (every entry)
+      float* G = a.dpart + ((int64_t)blockIdx.x * a.dseg + (cur_n - (int)(i0 / ntiles))) * P;
+      for (int64_t i = t; i < P; i += NT) {
+        G[i] = scratch[i];
+        scratch[i] = 0.0f;
+      }
+    } else {
+      float* G = a.grad + nd.step_base(cur_n);
+      for (int64_t i = t; i < P; i += NT) {
+        const float v = scratch[i];
+        if (v != 0.0f) atomicAdd(G + i, v);
+        scratch[i] = 0.0f;
+      }
     }
     __syncthreads();
   };

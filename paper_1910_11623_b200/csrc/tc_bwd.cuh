@@ -151,15 +151,20 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
     mbar_wait(&bars[4], g8ph);
     g8ph ^= 1;
     tc_after();
-    float* G = a.grad + nd.step_base(cur_n);
+    // deterministic mode: this CTA's partial of step cur_n, every entry stored once
+    float* G = a.dpart ? a.dpart + ((int64_t)blockIdx.x * a.dseg + (cur_n - (int)(i0 / ntiles))) *
+                                      nd.step_size()
+                       : a.grad + nd.step_base(cur_n);
+    const bool det = a.dpart != nullptr;
+    auto put = [&](float* p, float x) { if (det) *p = x; else atomicAdd(p, x); };
     float v[32];
     tmem_ld_g4(GA1 + lq, g, Dp / 8, v);               // dW̃1 row = w-unit, cols = d-inputs
     if (row < W) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const int k = 8 * (g + 4 * (i / 8)) + (i % 8);
-        if (k < D) atomicAdd(G + nd.off_W1() + row * D + k, v[i]);
-        else if (k == D) atomicAdd(G + nd.off_b1() + row, v[i]);
+        if (k < D) put(G + nd.off_W1() + row * D + k, v[i]);
+        else if (k == D) put(G + nd.off_b1() + row, v[i]);
       }
     }
     tmem_ld_g4(GA2 + lq, g, Wp / 8, v);               // dW̃2
@@ -167,8 +172,8 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const int k = 8 * (g + 4 * (i / 8)) + (i % 8);
-        if (k < W) atomicAdd(G + nd.off_W2() + row * W + k, v[i]);
-        else if (k == W) atomicAdd(G + nd.off_b2() + row, v[i]);
+        if (k < W) put(G + nd.off_W2() + row * W + k, v[i]);
+        else if (k == W) put(G + nd.off_b2() + row, v[i]);
       }
     }
     tmem_ld_g4(GA3 + lq, g, Wp / 8, v);               // dW̃3 row = d-output
@@ -176,8 +181,8 @@ __global__ void __launch_bounds__(NTH, 1) k_bwd_tc(PassArgs a, int ntiles, int64
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const int k = 8 * (g + 4 * (i / 8)) + (i % 8);
-        if (k < W) atomicAdd(G + nd.off_W3() + row * W + k, v[i]);
-        else if (k == W) atomicAdd(G + nd.off_b3() + row, v[i]);
+        if (k < W) put(G + nd.off_W3() + row * W + k, v[i]);
+        else if (k == W) put(G + nd.off_b3() + row, v[i]);
       }
     }
     tc_before();

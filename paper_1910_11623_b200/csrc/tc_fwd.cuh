@@ -539,9 +539,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
   __syncthreads();
   if (t == 0) {
     const double L = lred[0] + lred[1] + lred[2] + lred[3];
-    if (L != 0.0) atomicAdd(a.loss_acc, L);
     const float g0 = gred[0] + gred[1] + gred[2] + gred[3];
-    if (!a.eval && g0 != 0.0f) atomicAdd(a.grad, g0);
+    if (a.lpart) {   // deterministic mode: per-CTA partials, summed in order by k_det_reduce
+      a.lpart[blockIdx.x] = L;
+      a.y0part[blockIdx.x] = a.eval ? 0.0f : g0;
+    } else {
+      if (L != 0.0) atomicAdd(a.loss_acc, L);
+      if (!a.eval && g0 != 0.0f) atomicAdd(a.grad, g0);
+    }
   }
   if (warp == 0) {
     tc_after();

@@ -264,3 +264,31 @@ def test_sharded_adam_one_rank_matches_replicated(kernel, precision):
     # normalises tiny gradients: allow the atomics noise, bounded by lr per step
     tol = 1e-6 * np.max(np.abs(pa)) if kernel == "simt" else 6 * wl.lr
     assert np.max(np.abs(pa - pb)) <= tol
+
+
+@pytest.mark.parametrize("kernel,precision,problem", [("tc", "bf16", "allen_cahn"),
+                                                      ("simt", "fp32", "hjb")])
+def test_deterministic_mode_is_bitwise_reproducible(kernel, precision, problem):
+    """cfg.deterministic: per-CTA partials summed in a fixed order.
+    Two contexts give bitwise-identical losses, gradients and parameters over
+    several steps, agree with the atomics build to rounding, and match the oracle
+    (R19 tolerances)."""
+    wl = CONFIGS["cfg3_allen_cahn" if problem == "allen_cahn" else "cfg2_hjb"].with_(batch=3000, N=4)
+    kw = dict(lr=wl.lr, precision=precision, kernel=kernel, deterministic=True)
+    a = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, **kw)
+    b = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, **kw)
+    p = a.get_params()
+    p[1:] += (0.003 * np.random.default_rng(4).standard_normal(p.size - 1)).astype(np.float32)
+    a.set_params(p)
+    b.set_params(p)
+    la, lb = a.compute_grad(), b.compute_grad()
+    assert la == lb and np.array_equal(a.get_grads(), b.get_grads())
+    ref = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, p, 0, 0, np.arange(wl.batch),
+                           wl.batch, kink_band=KINK_BAND[precision])
+    tol = TOL[precision]
+    assert abs(la - ref["loss"]) <= tol * ref["loss"]
+    compare_grads(a.get_grads(), ref["grad"], wl.d, wl.w, wl.N, tol, ref["slack"])
+    for _ in range(3):
+        assert a.train_step() == b.train_step()
+    assert np.array_equal(a.get_params(), b.get_params())
+    assert a.eval_loss(2, 1000) == b.eval_loss(2, 1000)
