@@ -91,6 +91,7 @@ class BSDE:
         cfg.x0, cfg.lam = float(x0), float(lam)
         cfg.lr, cfg.beta1, cfg.beta2, cfg.eps = float(lr), float(beta1), float(beta2), float(eps)
         cfg.seed = int(seed)
+        self.seed = int(seed)
         cfg.precision = PRECISIONS[precision] if isinstance(precision, str) else int(precision)
         cfg.kernel = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
         cfg.prolong_mode = PROLONG[prolong] if isinstance(prolong, str) else int(prolong)
@@ -217,6 +218,31 @@ class BSDE:
         m = np.ascontiguousarray(m, np.float32)
         v = np.ascontiguousarray(v, np.float32)
         self._ck(self._L.bsde_set_adam_state(self._h, _fptr(m), _fptr(v), m.size, int(t)))
+
+    # ------------------------------------------------------------------ checkpoint
+    def save_checkpoint(self, path):
+        """Flat named arrays: parameters, Adam m, v, t and the
+        Philox iteration (the paths of every later iteration follow from it, R8/R9).
+        np.savez; bit-exact round trip through load_checkpoint."""
+        m, v, t = self.get_adam_state()
+        np.savez(path, params=self.get_params(), adam_m=m, adam_v=v, adam_t=np.int64(t),
+                 iteration=np.int64(self.iteration), N=np.int64(self.N),
+                 seed=np.uint64(self.seed),
+                 manifest=np.array(["params", "adam_m", "adam_v", "adam_t", "iteration", "N",
+                                    "seed"]))
+
+    def load_checkpoint(self, path):
+        """Restore a checkpoint written by save_checkpoint into a context of the same
+        shape (problem, d, widths and the current N)."""
+        z = np.load(path)
+        if int(z["seed"]) != self.seed:   # the paths of later iterations depend on it (R8)
+            raise ValueError("checkpoint seed %d != context seed %d" % (int(z["seed"]), self.seed))
+        if int(z["N"]) != self.N or z["params"].size != self.num_params():
+            raise ValueError("checkpoint has N=%d and %d parameters; this context N=%d, %d"
+                             % (int(z["N"]), z["params"].size, self.N, self.num_params()))
+        self.set_params(z["params"])
+        self.set_adam_state(z["adam_m"], z["adam_v"], int(z["adam_t"]))
+        self.iteration = int(z["iteration"])
 
     @property
     def iteration(self):

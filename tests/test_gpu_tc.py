@@ -292,3 +292,28 @@ def test_deterministic_mode_is_bitwise_reproducible(kernel, precision, problem):
         assert a.train_step() == b.train_step()
     assert np.array_equal(a.get_params(), b.get_params())
     assert a.eval_loss(2, 1000) == b.eval_loss(2, 1000)
+
+
+@pytest.mark.parametrize("kernel,precision", [("tc", "bf16"), ("simt", "fp32")])
+def test_checkpoint_resume_is_bit_exact(tmp_path, kernel, precision):
+    """Checkpoint / resume: parameters, Adam state and the
+    Philox iteration round-trip bit-exactly, and a resumed context continues the
+    run bitwise (deterministic reductions, counter-based paths)."""
+    wl = CONFIGS["cfg3_allen_cahn"].with_(batch=2048, N=4)
+    kw = dict(lr=wl.lr, precision=precision, kernel=kernel, deterministic=True)
+    a = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, **kw)
+    for _ in range(4):
+        a.train_step()
+    ck = str(tmp_path / "ck.npz")
+    a.save_checkpoint(ck)
+    la = [a.train_step() for _ in range(4)]
+    b = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, **kw)
+    b.set_params(b.get_params() + 0.01)   # state to be overwritten by the checkpoint
+    b.load_checkpoint(ck)
+    lb = [b.train_step() for _ in range(4)]
+    assert la == lb
+    assert np.array_equal(a.get_params(), b.get_params())
+    ma, va, ta = a.get_adam_state()
+    mb, vb, tb = b.get_adam_state()
+    assert ta == tb == 8 and np.array_equal(ma, mb) and np.array_equal(va, vb)
+    assert a.iteration == b.iteration == 8
