@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3 (SURVEY §5 tracing)
+
 #include "bsde.h"
 #include "kernels.cuh"
 
@@ -244,7 +246,17 @@ PassArgs pass_args(bsde_ctx* c) {
 int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
   const int64_t np = num_params_at(ctx, ctx->N);
   const PassArgs a = pass_args(ctx);
-  auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], ctx->stream); };
+  // phase events (bsde_profile_steps) and NVTX ranges named after the §8(a) rows;
+  // the ranges mark the enqueue (capture) of each phase for nsys timelines
+  static const char* const kPhase[6] = {"bsde.begin", "bsde.fwd (a1-a5)", "bsde.adjoint (a6)",
+                                        "bsde.allreduce (a7)", "bsde.check", "bsde.adam (a8)"};
+  int open_range = -1;
+  auto mark = [&](int i) {
+    if (ev) cudaEventRecord(ev[i], ctx->stream);
+    if (open_range >= 0) nvtxRangePop();
+    open_range = i < 6 ? i : -1;
+    if (open_range >= 0) nvtxRangePushA(kPhase[i]);
+  };
   int launches = 0;
   mark(0);
   const bool sharded = ctx->comm && ctx->cfg.sharded_adam && with_update;

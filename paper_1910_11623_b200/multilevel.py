@@ -78,3 +78,14 @@ def run_schedule(solver, iters_per_level, *, eval_every=25, eval_batch=None, eva
         if li + 1 < L:
             solver.prolongate(li + 1)
     return res
+
+
+def write_loss_csv(result, path):
+    """Loss curve as CSV (SURVEY §5 metrics; SPEC S:502 columns iteration, level,
+    loss, elapsed_seconds, plus N and the evaluation loss where one was taken)."""
+    with open(path, "w") as f:
+        f.write("iteration,level,N,loss,eval_loss,elapsed_seconds\n")
+        for r in result.records:
+            f.write("%d,%d,%d,%.9g,%s,%.6f\n" % (r.iteration, r.level, r.N, r.train_loss,
+                                                 "" if r.eval_loss is None else "%.9g" % r.eval_loss,
+                                                 r.train_seconds))

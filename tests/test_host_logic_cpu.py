@@ -130,3 +130,18 @@ def test_multilevel_time_to_target_only_on_final_grid():
     assert res.iteration_at_target == 3
     assert res.time_to_target == pytest.approx(1.5)
     assert res.records[-1].N == 4 and len(res.records) == 4
+
+
+def test_multilevel_loss_csv(tmp_path):
+    """The loss-curve CSV (SURVEY §5 metrics): one row per iteration, levels and N
+    as scheduled, losses as recorded."""
+    from paper_1910_11623_b200.multilevel import run_schedule, write_loss_csv
+    s = OracleSolver(ob.HJB, D, W, 2, T, 16, 1e-2)
+    res = run_schedule(s, [2, 2], eval_every=0)
+    path = tmp_path / "loss.csv"
+    write_loss_csv(res, str(path))
+    rows = path.read_text().strip().split("\n")
+    assert rows[0] == "iteration,level,N,loss,eval_loss,elapsed_seconds" and len(rows) == 5
+    cols = [r.split(",") for r in rows[1:]]
+    assert [int(c[1]) for c in cols] == [0, 0, 1, 1] and [int(c[2]) for c in cols] == [2, 2, 4, 4]
+    assert np.allclose([float(c[3]) for c in cols], [r.train_loss for r in res.records])
