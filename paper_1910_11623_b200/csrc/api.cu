@@ -193,6 +193,7 @@ ShArgs sh_args(bsde_ctx* c) {
   a.params = c->params;
   a.grad = c->grad;
   a.Rstore = c->Rstore;
+  a.tc = c->cfg.precision == BSDE_BF16 ? 1 : 0;
   shared_offsets(a);
   if (c->shbuf) shared_carve(a, c->shbuf, c->N_max);
   return a;
@@ -441,8 +442,8 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
         return fail(none, BSDE_EINVAL, "shared net: all layer widths must be equal (R23)");
     if (cfg.arch != BSDE_ARCH_FC && cfg.arch != BSDE_ARCH_RESNET && cfg.arch != BSDE_ARCH_NAIS)
       return fail(none, BSDE_EINVAL, "arch=%d", cfg.arch);
-    if (cfg.precision != BSDE_FP32 || cfg.kernel == BSDE_KERNEL_TC)
-      return fail(none, BSDE_EINVAL, "the shared formulation runs fp32 SIMT kernels only");
+    if (cfg.precision == BSDE_BF16 && cfg.arch == BSDE_ARCH_NAIS)
+      return fail(none, BSDE_EINVAL, "the shared NAIS-Net network runs on the fp32 kernels only");
     if (cfg.deterministic)
       return fail(none, BSDE_EINVAL, "deterministic mode covers the per-step formulation only");
   } else if (!widths || n_widths != 2 || widths[0] != widths[1] || widths[0] < 1) {
@@ -483,7 +484,7 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     return fail(none, BSDE_EINVAL,
                 "the tcgen05 kernels compute with bf16 operands; fp32-accurate precision runs on "
                 "kernel=SIMT");
-  if (family == BSDE_KERNEL_SIMT && cfg.precision == BSDE_BF16)
+  if (family == BSDE_KERNEL_SIMT && cfg.precision == BSDE_BF16 && !shared)
     return fail(none, BSDE_EINVAL, "bf16 operands need the tcgen05 kernels (kernel=SIMT given)");
   if (family == BSDE_KERNEL_SIMT && !shared && !simt_supported(d, w))
     return fail(none, BSDE_EINVAL, "d=%d w=%d too large for the SIMT kernels (d, w <= 127 and shared "
@@ -996,7 +997,7 @@ int bsde_launches_per_step(const bsde_ctx* ctx, int* n) {
 
 const char* bsde_kernel_family(const bsde_ctx* ctx) {
   if (!ctx) return "none";
-  if (ctx->shared) return "shared-simt";
+  if (ctx->shared) return ctx->cfg.precision == BSDE_BF16 ? "shared-tc" : "shared-simt";
   return ctx->family == BSDE_KERNEL_TC ? "tc" : "simt";
 }
 

@@ -64,6 +64,9 @@ struct ShArgs {
   int64_t off_W[kMaxSharedLayers], off_v;   // flat offsets of W_k (b_k follows) and v (c follows)
   int64_t off_Bk[kMaxSharedLayers];         // NAIS-Net (arch 2): B_k of block k ≥ 1 (R26)
   float* Am;                                // NAIS-Net: A_k = -R_kᵀR_k - εI, [L][w×w]
+  int tc;                                   // 1: bf16 tcgen05 row GEMMs (cfg.precision BF16)
+  uint16_t* wimg;                           // tc: bf16 UMMA images of W_k [w × pad16(K_in)]
+  int64_t off_img[kMaxSharedLayers];        // tc: element offset of layer k's image
   float *U0, *G0, *G0b, *dW;                // [R×K0p] inputs, ∇u, ∂L/∂∇u;  [N·M×d] increments
   float* S[kMaxSharedLayers];               // s_k = tanh(a_k)
   float* H[kMaxSharedLayers];               // h_k (= S[k] unless residual)

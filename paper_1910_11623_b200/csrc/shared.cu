@@ -27,9 +27,16 @@
 // the grid fills ≥ 2 waves, else 64×64×16 with 4×4; weight gradients split the
 // row reduction over CTAs (fp32 atomics) and fold the bias sums in.
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace bsde {
 namespace {
+
+#define RET(x)                                \
+  do {                                        \
+    cudaError_t e_ = (x);                     \
+    if (e_ != cudaSuccess) return e_;         \
+  } while (0)
 
 constexpr int TB = 64, TK = 16, NTH = 256;
 
@@ -115,6 +122,151 @@ __global__ void __launch_bounds__(NTH) k_gemm_rows(const float* __restrict__ A, 
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         if (j + c < NC) epi(i, j + c, acc[r][c]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- tcgen05 row GEMM
+// bf16 operands, fp32 TMEM accumulation (BSDE_BF16 precision of the shared
+// formulation).  One CTA = 128 rows of C[R×NC] = A[R×K]·W_kᵀ (NT) or A·W_k (NN);
+// W_k's bf16 image [w rows × Kp cols] (tc_common.cuh layout) sits in shared
+// memory whole (NT: K-major B, NN: MN-major B — the same image), A is converted
+// from fp32 to bf16 64 columns at a time into a double-buffered image; thread 0
+// issues the MMAs; the 4 warps read the accumulator (lane = row) for the epilogue.
+constexpr int TCK = 64;   // K chunk of the A image
+constexpr int TCN = 128;  // N tile (columns of C per CTA)
+template <bool NT, class Epi>
+__global__ void __launch_bounds__(128, 2) k_tc_rowgemm(const float* __restrict__ A, int lda, int R,
+                                                      int K, const uint16_t* __restrict__ wimg,
+                                                      int wrows, int Kp, int NC, int Npad,
+                                                      Epi epi) {
+  using namespace tc;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* abuf = sm;                                   // 2 × [128 × TCK] bf16
+  uint8_t* wsm = sm + 2 * 128 * TCK * 2;                // this CTA's slab of the weight image
+  __shared__ __align__(8) uint64_t bars[3];             // weights, MMA done (×2)
+  __shared__ uint32_t tslot;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int i0 = blockIdx.x * 128, n0 = blockIdx.y * TCN, nn = min(TCN, Npad - n0);
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tslot, TCN);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tm = tslot;
+  const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wimg);
+  if (t == 0) {   // NT: image rows [n0, n0+nn) are contiguous; NN: columns [n0, n0+nn) of every row group
+    if (NT) {
+      const uint32_t bytes = (uint32_t)nn * Kp * 2;
+      mbar_expect_tx(&bars[0], bytes);
+      const uint8_t* src = wsrc + (size_t)(n0 / 8) * (Kp * 16);
+      for (uint32_t off = 0; off < bytes; off += 16384u)
+        bulk_g2s(wsm + off, src + off, min(16384u, bytes - off), &bars[0]);
+    } else {
+      const uint32_t gbytes = (uint32_t)nn * 16;
+      mbar_expect_tx(&bars[0], gbytes * (uint32_t)(wrows / 8));
+      for (int g = 0; g < wrows / 8; ++g)
+        bulk_g2s(wsm + g * gbytes, wsrc + (size_t)g * (Kp * 16) + (n0 / 8) * 128, gbytes, &bars[0]);
+    }
+  }
+  const int Kg = (K + 15) / 16 * 16;                     // GEMM K, padded
+  const int nch = (Kg + TCK - 1) / TCK;
+  // chunk kc of A (fp32, row-major) -> bf16 image in buffer b: 16 threads per row,
+  // 4 consecutive columns each (coalesced 256-byte row segments), 8 rows per pass
+  auto convert = [&](int kc, int b) {
+    const int k0 = kc * TCK, cw = min(TCK, Kg - k0), c4 = 4 * (t & 15);
+    uint8_t* img = abuf + b * (128 * TCK * 2);
+    if (c4 >= cw) return;
+    for (int r = t >> 4; r < 128; r += 8) {
+      const int i = i0 + r, k = k0 + c4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < R) {
+        const float* src = A + (int64_t)i * lda + k;
+        if (k + 3 < K) {
+          v = __ldg(reinterpret_cast<const float4*>(src));
+        } else {
+          if (k < K) v.x = __ldg(src);
+          if (k + 1 < K) v.y = __ldg(src + 1);
+          if (k + 2 < K) v.z = __ldg(src + 2);
+        }
+      }
+      const uint2 u = make_uint2(pack2(v.x, v.y), pack2(v.z, v.w));
+      *reinterpret_cast<uint2*>(img + (r >> 3) * (cw * 16) + (c4 >> 3) * 128 + (r & 7) * 16 +
+                                (c4 & 7) * 2) = u;
+    }
+  };
+  const uint32_t idesc = idesc_bf16(128, nn, false, !NT);
+  convert(0, 0);
+  fence_async_smem();
+  tc_before();
+  __syncthreads();
+  for (int kc = 0; kc < nch; ++kc) {
+    const int b = kc & 1, cw = min(TCK, Kg - kc * TCK);
+    if (t == 0) {
+      tc_after();
+      if (kc == 0) mbar_wait(&bars[0], 0);
+      const Opnd a = kmaj(abuf + b * (128 * TCK * 2), cw);
+      Opnd w = NT ? kmaj(wsm, Kp) : mnmaj(wsm, nn);
+      w.base += NT ? (uint32_t)kc * (TCK / 8) * 128u : (uint32_t)kc * (TCK / 8) * (uint32_t)nn * 16u;
+      gemm(tm, a, w, cw / 16, idesc, kc > 0);
+      mma_commit(&bars[1 + b]);
+    }
+    if (kc + 1 < nch) {
+      if (kc >= 1) mbar_wait(&bars[1 + (b ^ 1)], (uint32_t)(((kc - 1) >> 1) & 1));   // chunk kc-1 read it
+      convert(kc + 1, b ^ 1);
+      fence_async_smem();
+    }
+    tc_before();
+    __syncthreads();
+  }
+  mbar_wait(&bars[1 + ((nch - 1) & 1)], (uint32_t)(((nch - 1) >> 1) & 1));
+  tc_after();
+  // epilogue: warp w reads TMEM lanes 32w..32w+31 (row = lane)
+  const int row = warp * 32 + lane, i = i0 + row;
+  const uint32_t lane_base = tm + ((uint32_t)(warp * 32) << 16);
+  for (int jl = 0; jl < nn; jl += 16) {
+    float v[16];
+    tmem_ld16(lane_base + (uint32_t)jl, v);
+    if (i < R) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = n0 + jl + 4 * q;
+        if (epi.ld % 4 == 0 && j + 3 < NC) {
+          epi.v4(i, j, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (j + e < NC) epi(i, j + e, v[4 * q + e]);
+        }
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_after();
+    tmem_dealloc(tm, TCN);
+  }
+}
+
+// fp32 W_k [w × K_in] -> bf16 image [w rows × Kp cols] (layer k at wimg + off_img[k])
+__global__ void k_tc_pack_w(ShArgs a) {
+  for (int k = 0; k < a.L; ++k) {
+    const int Kin = k == 0 ? a.d + 1 : a.w, Kp = (Kin + 15) / 16 * 16;
+    const float* W = a.params + a.off_W[k];
+    uint16_t* img = a.wimg + a.off_img[k];
+    for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < (int64_t)a.w * Kp;
+         id += (int64_t)gridDim.x * blockDim.x) {
+      const int r = (int)(id / Kp), c = (int)(id - (int64_t)r * Kp);
+      const float x = c < Kin ? W[(int64_t)r * Kin + c] : 0.0f;
+      const __nv_bfloat16 h = __float2bfloat16_rn(x);
+      const size_t off = (size_t)(r >> 3) * (Kp * 8) + (c >> 3) * 64 + (r & 7) * 8 + (c & 7);
+      img[off] = *reinterpret_cast<const uint16_t*>(&h);
     }
   }
 }
@@ -827,6 +979,22 @@ cudaError_t gemm_rows(const float* A, int lda, const float* B, int ldb, int R, i
   return cudaGetLastError();
 }
 
+// tcgen05 row GEMM with layer k's bf16 image (NT: N = w, K = K_in; NN: K = w, N = K_in)
+template <bool NT, class Epi>
+cudaError_t tc_rows(const ShArgs& a, int k, const float* A, int lda, int R, int K, int NC,
+                    const Epi& epi, cudaStream_t s) {
+  const int Kin = k == 0 ? a.d + 1 : a.w, Kp = (Kin + 15) / 16 * 16;
+  const int Npad = NT ? (a.w + 15) / 16 * 16 : Kp;
+  // weight slab: NT [TCN rows × Kp], NN [w rows × TCN]
+  const size_t smem = 2 * 128 * TCK * 2 + (size_t)TCN * (NT ? Kp : a.w) * 2;
+  RET(cudaFuncSetAttribute(k_tc_rowgemm<NT, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem));
+  dim3 grid((R + 127) / 128, (Npad + TCN - 1) / TCN);
+  k_tc_rowgemm<NT, Epi><<<grid, 128, smem, s>>>(A, lda, R, K, a.wimg + a.off_img[k], a.w, Kp, NC,
+                                                 Npad, epi);
+  return cudaGetLastError();
+}
+
 // C[P×Q] += Aᵀ B over R rows (+ bias[p] += Σ_r A[r][p] when bias != null)
 cudaError_t gemm_tn(const float* A, int lda, const float* B, int ldb, int R, int P, int Q, float* C,
                     int ldc, float* bias, cudaStream_t s) {
@@ -872,11 +1040,7 @@ struct EpiNeg {        // out = -c (R̄_k = -R_k S_k)
   }
 };
 
-#define RET(x)                                \
-  do {                                        \
-    cudaError_t e_ = (x);                     \
-    if (e_ != cudaSuccess) return e_;         \
-  } while (0)
+
 
 // G_k = R_kᵀR_k for the NAIS-Net blocks into the A buffer (TN GEMM over R's rows)
 cudaError_t nais_gram(const ShArgs& a, const float* params, cudaStream_t s) {
@@ -923,6 +1087,7 @@ size_t shared_buffer_bytes(int d, int w, int L, int arch, int N_max, int64_t M) 
   if (arch != 0) f += (size_t)R * w * 2;    // h̄ ping-pong
   f += (size_t)R * 6;                       // u, ū, q[4]
   if (arch == 2) f += (size_t)L * w * w;    // A_k
+  f += ((size_t)w * ((d + 1 + 15) / 16 * 16) + (size_t)(L - 1) * w * ((w + 15) / 16 * 16) + 1) / 2;
   return f * sizeof(float) + 256 * 80;
 }
 
@@ -956,6 +1121,12 @@ void shared_carve(ShArgs& a, void* base, int N_max) {
   a.ub = take((size_t)R);
   a.q = take((size_t)R * 4);
   a.Am = a.arch == 2 ? take((size_t)a.L * a.w * a.w) : nullptr;
+  int64_t img = 0;   // bf16 weight images (tcgen05 row GEMMs)
+  for (int k = 0; k < a.L; ++k) {
+    a.off_img[k] = img;
+    img += (int64_t)a.w * (((k == 0 ? a.d + 1 : a.w) + 15) / 16 * 16);
+  }
+  a.wimg = reinterpret_cast<uint16_t*>(take((size_t)(img + 1) / 2));
 }
 
 cudaError_t launch_shared_init(float* params, const ShArgs& a, uint32_t k0, uint32_t k1,
@@ -991,6 +1162,7 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   const int W = a.w, K0 = a.d + 1, L = a.L;
   const bool nais = a.arch == 2;
   const bool res = a.arch == 1 || nais;      // NAIS-Net blocks are residual with h = 1 (R26)
+  const bool tcg = a.tc && !nais;            // bf16 tcgen05 row GEMMs (weight gradients stay fp32)
   const float* P = a.params;
   int nl = 0;
   // the layer matrix of the forward/back-propagation GEMMs: W_k, or A_k for a NAIS block
@@ -1004,6 +1176,11 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   k_sh_x<<<grid_for(a.M * ((a.d + 3) / 4), 64), 64, 0, s>>>(a);
   RET(cudaGetLastError());
   nl += 2;
+  if (tcg) {    // bf16 images of this iteration's W_k
+    k_tc_pack_w<<<grid_for((int64_t)W * W, NTH), NTH, 0, s>>>(a);
+    RET(cudaGetLastError());
+    ++nl;
+  }
   if (nais) {   // A_k = -R_kᵀR_k - εI from this iteration's parameters
     RET(nais_gram(a, a.params, s));
     k_sh_nais_fix<<<grid_for((int64_t)(L - 1) * W * W, NTH), NTH, 0, s>>>(a);
@@ -1018,7 +1195,8 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
     const int lda = k == 0 ? a.K0p : W, K = k == 0 ? K0 : W;
     Op2 inj;
     if (nais && k > 0) inj = Op2{a.U0, a.K0p, Bk(k), K0, K0};
-    RET(gemm_rows<true>(A, lda, Wk(k), K, R, W, K, e, s, inj));
+    if (tcg) RET(tc_rows<true>(a, k, A, lda, R, K, W, e, s));
+    else RET(gemm_rows<true>(A, lda, Wk(k), K, R, W, K, e, s, inj));
     ++nl;
   }
   // input gradient: g_{k-1} = δ_k W_k (+ g_k), k = L..2, then g_0 = δ_1 W_1; NAIS-Net
@@ -1027,7 +1205,8 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   for (int k = L - 1; k >= 1; --k) {
     const float* gk = res ? (k == L - 1 ? v : a.G[k]) : nullptr;
     EpiIg e{gk, (res && k == L - 1) ? 1 : 0, a.G[k - 1], a.S[k - 1], a.D[k - 1], W};
-    RET(gemm_rows<false>(a.D[k], W, Wk(k), W, R, W, W, e, s));
+    if (tcg) RET(tc_rows<false>(a, k, a.D[k], W, R, W, W, e, s));
+    else RET(gemm_rows<false>(a.D[k], W, Wk(k), W, R, W, W, e, s));
     ++nl;
     if (nais) {
       EpiIg eu{g0_init ? a.G0 : nullptr, 0, a.G0, nullptr, nullptr, a.K0p};
@@ -1038,7 +1217,8 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   }
   {
     EpiIg e{g0_init ? a.G0 : nullptr, 0, a.G0, nullptr, nullptr, a.K0p};
-    RET(gemm_rows<false>(a.D[0], W, Wk(0), K0, R, K0, W, e, s));
+    if (tcg) RET(tc_rows<false>(a, 0, a.D[0], W, R, W, K0, e, s));
+    else RET(gemm_rows<false>(a.D[0], W, Wk(0), K0, R, K0, W, e, s));
     ++nl;
   }
   // per-row scalars and the loss
@@ -1069,7 +1249,8 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
     float* gout = a.Gb[k & 1];
     EpiUp e{a.S[k], k < L - 1 ? a.G[k] : nullptr, v, (res && k > 0) ? gprev : nullptr, gout,
             a.Sb[k], W};
-    RET(gemm_rows<true>(gprev, ldprev, Wk(k), K, R, W, K, e, s, inj));
+    if (tcg) RET(tc_rows<true>(a, k, gprev, ldprev, R, K, W, e, s));
+    else RET(gemm_rows<true>(gprev, ldprev, Wk(k), K, R, W, K, e, s, inj));
     nl += 2;
     gprev = gout;
     ldprev = W;
@@ -1099,7 +1280,8 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
     const int nxt = cur ^ 1;
     EpiDown e{(res && k > 0) ? a.Hb[cur] : nullptr, (res && k - 1 > 0) ? a.Hb[nxt] : nullptr,
               a.Sb[k - 1], a.S[k - 1], a.Ab[nxt], W};
-    RET(gemm_rows<false>(a.Ab[cur], W, Wk(k), W, R, W, W, e, s));
+    if (tcg) RET(tc_rows<false>(a, k, a.Ab[cur], W, R, W, W, e, s));
+    else RET(gemm_rows<false>(a.Ab[cur], W, Wk(k), W, R, W, W, e, s));
     ++nl;
     cur = nxt;
   }

@@ -178,3 +178,33 @@ def test_fake_world_shards_sum(arch):
     gs = sum(pt.get_grads().astype(np.float64) for pt in parts)
     assert abs(ls - lf) <= 1e-5 * lf
     assert np.linalg.norm(gs - gf) <= 1e-5 * np.linalg.norm(gf)
+
+
+@pytest.mark.parametrize("problem,arch,x0", [("black_scholes", "fc", 0.5), ("hjb", "resnet", 0.0),
+                                             ("allen_cahn", "fc", 0.0)])
+def test_bf16_tensor_core_gradient(problem, arch, x0):
+    """precision="bf16": the row GEMMs (forward, ∇ₓu, and the reverse-over-reverse
+    δ̄ / h̄ products) run on tcgen05 with bf16 operands and fp32 TMEM accumulation;
+    the weight-gradient GEMMs stay fp32.  North-star bf16 tolerance 2e-2 against
+    the float64 oracle; ragged rows (R = 7·101) and d + 1 = 38 inputs."""
+    d, w, L, N, T, B = 37, 64, 3, 6, 0.5, 101
+    s = make(problem, d, w, L, N, T, B, arch=arch, x0=x0, lr=1e-3, precision="bf16")
+    assert s.family == "shared-tc"
+    p = perturb(s, 1)
+    loss = s.compute_grad()
+    ref = osh.iteration(PROBLEM[problem], d, w, L, ARCH[arch], N, T, p.astype(np.float64), 0, 0,
+                        np.arange(B), B, x0=x0)
+    assert abs(loss - ref["loss"]) <= 2e-2 * ref["loss"], (loss, ref["loss"])
+    check_grad(s.get_grads(), ref["grad"], tol=2e-2)
+
+
+def test_bf16_tensor_core_paper_workload():
+    """The paper's Table 1 workload with bf16 tcgen05 row GEMMs (4×256, M = 100,
+    N = 50, BS d = 100): loss and gradient within 2e-2 of the oracle."""
+    d, w, L, N, T, B, x0 = 100, 256, 4, 50, 1.0, 100, 0.1
+    s = make("black_scholes", d, w, L, N, T, B, x0=x0, lr=1e-3, precision="bf16")
+    p = s.get_params().astype(np.float64)
+    loss = s.compute_grad()
+    ref = osh.iteration(ob.BLACK_SCHOLES, d, w, L, osh.FC, N, T, p, 0, 0, np.arange(B), B, x0=x0)
+    assert abs(loss - ref["loss"]) <= 2e-2 * ref["loss"]
+    check_grad(s.get_grads(), ref["grad"], tol=2e-2)

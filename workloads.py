@@ -63,6 +63,13 @@ CONFIGS = {
     "nx2_shared_bs_nais_paper": Workload("nx2_shared_bs_nais_paper", "black_scholes", 100, 256, 50,
                                          1.0, 100, "fp32", 1e-3, 20000, x0=0.1,
                                          formulation="shared", arch="nais", layers=4),
+    # the same with bf16 tcgen05 row GEMMs (weight gradients fp32)
+    "nx1_shared_bs_paper_bf16": Workload("nx1_shared_bs_paper_bf16", "black_scholes", 100, 256, 50,
+                                         1.0, 100, "bf16", 1e-3, 20000, x0=0.1,
+                                         formulation="shared", layers=4),
+    "nx1_shared_bs_m4096_bf16": Workload("nx1_shared_bs_m4096_bf16", "black_scholes", 100, 256, 50,
+                                         1.0, 4096, "bf16", 1e-3, 20000, x0=0.1,
+                                         formulation="shared", layers=4),
     # the same network and problem at a throughput batch (M = 4096)
     "nx1_shared_bs_m4096": Workload("nx1_shared_bs_m4096", "black_scholes", 100, 256, 50, 1.0, 4096,
                                     "fp32", 1e-3, 20000, x0=0.1, formulation="shared", layers=4),
