@@ -29,8 +29,8 @@ below), pinned by central finite differences in tests/test_oracle_shared.py.
 import numpy as np
 
 from . import philox
-from .bsde import (BLACK_SCHOLES, BS_SIGMA, SIGMA, driver_df_dy, driver_df_dz, driver_f,
-                   forward_step, terminal_g)
+from .bsde import (ALLEN_CAHN, BLACK_SCHOLES, BS_SIGMA, HJB, SIGMA, driver_df_dy, driver_df_dz,
+                   driver_f, forward_step, terminal_g)
 
 FC, RESNET, NAIS = 0, 1, 2
 NAIS_EPS, NAIS_H = 0.01, 1.0    # A = -RᵀR - εI, block step h (R26)
@@ -149,6 +149,17 @@ def input_gradient(params, d, w, L, arch, cache):
     return g, delta
 
 
+def grad_g(problem, X):
+    """∇g(x) of the terminal conditions (R12, R13): heat and
+    Black-Scholes 2x, HJB 2x/(1+|x|²), Allen-Cahn -0.8x/(2+0.4|x|²)²."""
+    s = np.sum(X * X, axis=-1, keepdims=True)
+    if problem == HJB:
+        return 2.0 * X / (1.0 + s)
+    if problem == ALLEN_CAHN:
+        return -0.8 * X / (2.0 + 0.4 * s) ** 2
+    return 2.0 * X
+
+
 def sigma_t(problem, X, G):
     """z = σ(x)ᵀ ∇ₓu: √2 ∇ₓu, or σ x ⊙ ∇ₓu for Black-Scholes."""
     return BS_SIGMA * X * G if problem == BLACK_SCHOLES else SIGMA * G
@@ -166,9 +177,11 @@ def paths(problem, d, N, T, seed, it, m, x0):
 
 
 def iteration(problem, d, w, L, arch, N, T, params, seed, it, m, batch_global, x0=0.0, lam=1.0,
-              want_grad=True):
+              want_grad=True, zN=False):
     """Loss (R24) and its gradient for the shard of global paths m.  Rows are
-    (n, m) with n = 0..N; returns dict(loss, loss_sum, grad, r [M×(N+1)], Y, Z)."""
+    (n, m) with n = 0..N; returns dict(loss, loss_sum, grad, r [M×(N+1)], Y, Z).
+    zN adds the optional terminal gradient term Σ_m |∇ₓu(t_N, X_N) - ∇g(X_N)|² of
+    P:79 (with the paper's Z_N = ∇u, R27)."""
     m = np.asarray(m, dtype=np.int64)
     M = len(m)
     dt = T / N
@@ -186,6 +199,9 @@ def iteration(problem, d, w, L, arch, N, T, params, seed, it, m, batch_global, x
                 - np.sum(Z[n] * dW[n], axis=-1))
     r[N] = Y[N] - terminal_g(problem, X[N])
     loss_sum = float(np.sum(r * r))
+    eN = Gx[N] - grad_g(problem, X[N]) if zN else None
+    if zN:
+        loss_sum += float(np.sum(eN * eN))
     out = dict(loss_sum=loss_sum, loss=loss_sum / float(batch_global), r=r, Y=Y, Z=Z)
     if not want_grad:
         return out
@@ -200,6 +216,8 @@ def iteration(problem, d, w, L, arch, N, T, params, seed, it, m, batch_global, x
     Ybar[N] += sc * r[N]
     # ∂L/∂(∇ₓu) = σ(X) z̄ (σ diagonal); no gradient to t
     Gbar = np.concatenate([sigma_t(problem, X[n], Zbar[n]) for n in range(N + 1)], axis=0)
+    if zN:   # ∂/∂(∇ₓu) of the Z_N term, rows n = N
+        Gbar[N * M:] += sc * eN
     g0bar = np.concatenate([np.zeros((Gbar.shape[0], 1)), Gbar], axis=1)
     out["grad"] = shared_grad(params, d, w, L, arch, cache, g, delta, Ybar.reshape(-1), g0bar)
     return out

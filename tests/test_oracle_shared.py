@@ -161,3 +161,31 @@ def test_nais_init_projected_and_zero_block_map():
         Bk[...] = 0.0
     u, _ = shared.forward(q, d, w, L, shared.NAIS, np.zeros(3), np.ones((3, d)))
     np.testing.assert_array_equal(u, np.full(3, c[0]))
+
+
+@pytest.mark.parametrize("problem", PROBLEMS)
+def test_zN_term_gradient_and_grad_g(problem):
+    """R27 (P:79 optional term |Z_N - g'(X_N)|²): ∇g = central differences of g,
+    and the loss gradient with the term = central differences."""
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((6, 3))
+    h = 1e-6
+    for i in range(3):
+        e = np.zeros(3)
+        e[i] = h
+        fd = (bsde.terminal_g(problem, X + e) - bsde.terminal_g(problem, X - e)) / (2 * h)
+        assert np.max(np.abs(shared.grad_g(problem, X)[:, i] - fd)) < 1e-8
+    d, w, L, N, T, M, x0 = 3, 5, 2, 3, 0.5, 4, 0.6
+    p = _params(problem + 40, d, w, L)
+    r = shared.iteration(problem, d, w, L, shared.FC, N, T, p, 1, 2, np.arange(M), M, x0=x0, zN=True)
+    r0 = shared.iteration(problem, d, w, L, shared.FC, N, T, p, 1, 2, np.arange(M), M, x0=x0)
+    assert r["loss"] > r0["loss"]
+    fd = np.zeros_like(p)
+    for k in range(p.size):
+        e = np.zeros_like(p)
+        e[k] = h
+        fd[k] = (shared.iteration(problem, d, w, L, shared.FC, N, T, p + e, 1, 2, np.arange(M), M,
+                                  x0=x0, want_grad=False, zN=True)["loss"]
+                 - shared.iteration(problem, d, w, L, shared.FC, N, T, p - e, 1, 2, np.arange(M), M,
+                                    x0=x0, want_grad=False, zN=True)["loss"]) / (2 * h)
+    assert np.max(np.abs(r["grad"] - fd)) <= 1e-6 * np.max(np.abs(fd))
