@@ -122,6 +122,8 @@ typedef struct {
                              place of fp32/fp64 atomics, so repeated runs of the per-step
                              formulation are bitwise identical (SPEC determinism
                              invariant); the shared formulation rejects it (EINVAL)        */
+  int shared_zN;          /* BSDE_FORM_SHARED: add the optional terminal term
+                             Σ_m |∇ₓu(t_N, X_N) - ∇g(X_N)|² of PAPER.md:79 (DESIGN R27)    */
   void* workspace;        /* optional caller-owned device memory (e.g. a torch tensor) of
                              workspace_bytes >= bsde_workspace_bytes(): every device buffer
                              of the context is carved from it (256-byte aligned) and nothing

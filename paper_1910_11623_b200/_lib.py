@@ -56,6 +56,7 @@ class Config(ctypes.Structure):
         ("formulation", ctypes.c_int),
         ("sharded_adam", ctypes.c_int),
         ("deterministic", ctypes.c_int),
+        ("shared_zN", ctypes.c_int),
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_size_t),
         ("arch", ctypes.c_int),

@@ -194,6 +194,7 @@ ShArgs sh_args(bsde_ctx* c) {
   a.grad = c->grad;
   a.Rstore = c->Rstore;
   a.tc = c->cfg.precision == BSDE_BF16 ? 1 : 0;
+  a.zN = c->cfg.shared_zN;
   shared_offsets(a);
   if (c->shbuf) shared_carve(a, c->shbuf, c->N_max);
   return a;

@@ -65,6 +65,7 @@ struct ShArgs {
   int64_t off_Bk[kMaxSharedLayers];         // NAIS-Net (arch 2): B_k of block k ≥ 1 (R26)
   float* Am;                                // NAIS-Net: A_k = -R_kᵀR_k - εI, [L][w×w]
   int tc;                                   // 1: bf16 tcgen05 row GEMMs (cfg.precision BF16)
+  int zN;                                   // the optional Σ|∇ₓu(t_N, X_N) - ∇g(X_N)|² term (R27)
   uint16_t* wimg;                           // tc: bf16 UMMA images of W_k [w × pad16(K_in)]
   int64_t off_img[kMaxSharedLayers];        // tc: element offset of layer k's image
   float *U0, *G0, *G0b, *dW;                // [R×K0p] inputs, ∇u, ∂L/∂∇u;  [N·M×d] increments

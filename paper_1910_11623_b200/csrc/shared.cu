@@ -717,6 +717,17 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// ∂g/∂x_i given x_i and s = |x|² (R27): heat, Black-Scholes 2x; HJB 2x/(1+s);
+// Allen-Cahn -0.8x/(2+0.4s)²
+__device__ __forceinline__ float grad_g(int problem, float x, float s) {
+  if (problem == kHJB) return 2.0f * x / (1.0f + s);
+  if (problem == kAllenCahn) {
+    const float q = 2.0f + 0.4f * s;
+    return -0.8f * x / (q * q);
+  }
+  return 2.0f * x;
+}
+
 // z_i = σ(X)ᵀ∇ₓu: √2 g_i, or σ x_i g_i (Black-Scholes)
 __device__ __forceinline__ float sig(int problem, float x, float g) {
   return problem == kBlackScholes ? kBSSigma * x * g : 1.41421356237309515f * g;
@@ -750,6 +761,12 @@ __global__ void k_sh_rowscal(ShArgs a) {
       for (int i = lane; i < a.d; i += 32) s0 = fmaf(xr[i], xr[i], s0);
     }
     s0 = warp_sum(s0);
+    if (n == a.N && a.zN) {   // Σ_i (∂_i u - ∂_i g)² of the Z_N term (needs |X_N|² = s0)
+      for (int i = lane; i < a.d; i += 32) {
+        const float e = gr[i] - grad_g(a.problem, xr[i], s0);
+        s1 = fmaf(e, e, s1);
+      }
+    }
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
     if (lane == 0) {
@@ -783,6 +800,7 @@ __global__ void k_sh_loss(ShArgs a) {
     const int64_t m = r - (int64_t)n * a.M;
     const float rn = residual(a, n, m);
     if (lane == 0) lsum += (double)rn * rn;
+    if (lane == 0 && n == a.N && a.zN) lsum += (double)a.q[4 * r + 1];   // Z_N term (R27)
     if (a.eval) continue;
     const float y = a.u[r];
     float ub = 0.0f;
@@ -804,7 +822,10 @@ __global__ void k_sh_loss(ShArgs a) {
         gb[1 + i] = sig(a.problem, xr[i], f * (fmaf(zc, z, zc0) - dw[i]));
       }
     } else {
-      for (int i = lane; i < a.d; i += 32) gb[1 + i] = 0.0f;
+      const float* gr = a.G0 + r * a.K0p + 1;
+      const float sN = a.q[4 * r];
+      for (int i = lane; i < a.d; i += 32)   // Z_N term: 2/B (∂_i u - ∂_i g), else 0
+        gb[1 + i] = a.zN ? sc * (gr[i] - grad_g(a.problem, xr[i], sN)) : 0.0f;
       if (lane == 0) a.Rstore[m] = rn;
     }
   }

@@ -77,7 +77,7 @@ class BSDE:
                  stream=None, rank=0, world=1, nccl_id=None, use_graph=True, beta1=0.9,
                  beta2=0.999, eps=1e-8, zero_head=None, coupled_paths=False,
                  formulation="per_step", arch="fc", layers=4, sharded_adam=False,
-                 workspace=None, deterministic=False):
+                 workspace=None, deterministic=False, zN=False):
         """stream: a torch.cuda.Stream, a raw cudaStream_t (int), or None (a new
         torch stream on `device`, kept in self.stream).  zero_head: R7b, defaults
         to True for Allen-Cahn.  coupled_paths: every level draws the finest grid's
@@ -119,6 +119,7 @@ class BSDE:
         cfg.formulation = FORMULATIONS[formulation]
         cfg.sharded_adam = int(bool(sharded_adam))
         cfg.deterministic = int(bool(deterministic))
+        cfg.shared_zN = int(bool(zN))
         if workspace is not None:   # caller-owned device memory (a torch tensor), kept alive
             self._workspace = workspace
             cfg.workspace = workspace.data_ptr()

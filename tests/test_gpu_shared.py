@@ -208,3 +208,16 @@ def test_bf16_tensor_core_paper_workload():
     ref = osh.iteration(ob.BLACK_SCHOLES, d, w, L, osh.FC, N, T, p, 0, 0, np.arange(B), B, x0=x0)
     assert abs(loss - ref["loss"]) <= 2e-2 * ref["loss"]
     check_grad(s.get_grads(), ref["grad"], tol=2e-2)
+
+
+@pytest.mark.parametrize("problem", ["black_scholes", "hjb", "allen_cahn"])
+def test_zN_term_matches_oracle(problem):
+    """The optional Σ|∇ₓu(t_N, X_N) - ∇g(X_N)|² term of P:79 (R27, cfg.shared_zN)."""
+    d, w, L, N, T, B, x0 = 12, 32, 3, 4, 0.5, 101, (0.5 if problem == "black_scholes" else 0.0)
+    s = make(problem, d, w, L, N, T, B, x0=x0, zN=True)
+    p = perturb(s, 6)
+    loss = s.compute_grad()
+    ref = osh.iteration(PROBLEM[problem], d, w, L, osh.FC, N, T, p.astype(np.float64), 0, 0,
+                        np.arange(B), B, x0=x0, zN=True)
+    assert abs(loss - ref["loss"]) <= TOL * ref["loss"], (loss, ref["loss"])
+    check_grad(s.get_grads(), ref["grad"])
