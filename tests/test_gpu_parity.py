@@ -285,3 +285,28 @@ def test_torch_workspace_context_matches_own_allocations():
     small = ws[off:off + nbytes // 2]
     with pytest.raises(Exception):
         make("hjb", d, w, N, 1.0, B, kernel="simt", workspace=small)
+
+
+@pytest.mark.parametrize("kernel,problem,d,w,N,B", [
+    ("simt", "heat", 1, 1, 1, 1),          # every dimension at its minimum
+    ("simt", "hjb", 3, 2, 1, 65),          # one step, a 1-path ragged tail after a full tile
+    ("tc", "allen_cahn", 100, 110, 1, 1),  # one path in a 128-row tcgen05 tile, one step
+    ("tc", "hjb", 37, 45, 2, 129),         # ragged tail of one path, odd d and w
+])
+def test_degenerate_shapes(kernel, problem, d, w, N, B):
+    """Edge cases: minimal sizes, single step, single path, one-path ragged tails."""
+    prec = "bf16" if kernel == "tc" else "fp32"
+    T = 0.3 if problem == "allen_cahn" else 1.0
+    s = make(problem, d, w, N, T, B, kernel=kernel, precision=prec)
+    p = s.get_params()
+    p[1:] += (0.01 * np.random.default_rng(9).standard_normal(p.size - 1)).astype(np.float32)
+    s.set_params(p)
+    loss = s.compute_grad()
+    ref = oracle_iteration(problem, d, w, N, T, p, 0, 0, np.arange(B), B,
+                           kink_band=KINK_BAND[prec])
+    tol = TOL[prec]
+    assert abs(loss - ref["loss"]) <= tol * ref["loss"], (loss, ref["loss"])
+    compare_grads(s.get_grads(), ref["grad"], d, w, N, tol, ref["slack"])
+    assert np.isfinite(s.train_step())
+    with pytest.raises(Exception):
+        make(problem, d, w, N, T, 0, kernel=kernel, precision=prec)   # empty batch: EINVAL
