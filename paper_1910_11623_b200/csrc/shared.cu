@@ -134,9 +134,12 @@ __global__ void __launch_bounds__(NTH) k_gemm_rows(const float* __restrict__ A, 
 // from fp32 to bf16 64 columns at a time into a double-buffered image; thread 0
 // issues the MMAs; the 4 warps read the accumulator (lane = row) for the epilogue.
 constexpr int TCK = 64;   // K chunk of the A image
-constexpr int TCN = 128;  // N tile (columns of C per CTA)
+#ifndef BSDE_EXP_TCN
+#define BSDE_EXP_TCN 128
+#endif
+constexpr int TCN = BSDE_EXP_TCN;  // N tile (columns of C per CTA)
 template <bool NT, class Epi>
-__global__ void __launch_bounds__(128, 2) k_tc_rowgemm(const float* __restrict__ A, int lda, int R,
+__global__ void __launch_bounds__(128, TCN <= 128 ? 2 : 1) k_tc_rowgemm(const float* __restrict__ A, int lda, int R,
                                                       int K, const uint16_t* __restrict__ wimg,
                                                       int wrows, int Kp, int NC, int Npad,
                                                       Epi epi) {
