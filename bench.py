@@ -165,7 +165,8 @@ def oracle_rate(wl, paths, iters):
             return osh.iteration(prob, wl.d, wl.w, wl.layers, arch, wl.N, wl.T, p, wl.seed, k,
                                  np.arange(paths), wl.batch, x0=wl.x0)
     else:
-        p = ob.init_params(wl.seed, wl.d, wl.w, wl.N)
+        p = ob.init_params(wl.seed, wl.d, wl.w, wl.N,
+                           zero_head=(wl.problem == "allen_cahn"))   # R7b, as the GPU init
 
         def one(k):
             return ob.iteration(prob, wl.d, wl.w, wl.N, wl.T, p, wl.seed, k, np.arange(paths),
