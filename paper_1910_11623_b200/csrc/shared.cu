@@ -22,10 +22,14 @@
 //             h̄_{k-1} = ā_k W_k (+ h̄_k)                                   NN + TN GEMMs
 //   head      v̄ = Σ (ḡ_L + ū h_L), c̄ = Σ ū
 //
-// fp32 throughout (the paper's PyTorch precision); SIMT FFMA GEMMs:
+// Precision FP32 (the paper's PyTorch precision): SIMT FFMA GEMMs,
 // 128×128×8 tiles with 8×8 register tiles per thread (double-buffered smem) when
 // the grid fills ≥ 2 waves, else 64×64×16 with 4×4; weight gradients split the
-// row reduction over CTAs (fp32 atomics) and fold the bias sums in.
+// row reduction over CTAs (fp32 atomics) and fold the bias sums in.  Precision
+// BF16 (FC / ResNet): the row GEMMs run on tcgen05 (k_tc_rowgemm, bf16 operands,
+// fp32 TMEM accumulation, same epilogues); the weight gradients stay fp32.
+// NAIS-Net blocks (arch 2): A_k = -R_kᵀR_k - εI per iteration, the input
+// injection as a second operand pair of the row GEMMs (R26).
 #include "kernels.cuh"
 #include "tc_common.cuh"
 
