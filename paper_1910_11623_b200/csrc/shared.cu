@@ -143,7 +143,7 @@ constexpr int TCK = 64;   // K chunk of the A image
 #endif
 constexpr int TCN = BSDE_EXP_TCN;  // N tile (columns of C per CTA)
 template <bool NT, class Epi>
-__global__ void __launch_bounds__(128, TCN <= 128 ? 2 : 1) k_tc_rowgemm(const float* __restrict__ A, int lda, int R,
+__global__ void __launch_bounds__(256, TCN <= 128 ? 2 : 1) k_tc_rowgemm(const float* __restrict__ A, int lda, int R,
                                                       int K, const uint16_t* __restrict__ wimg,
                                                       int wrows, int Kp, int NC, int Npad,
                                                       Epi epi) {
@@ -189,20 +189,27 @@ __global__ void __launch_bounds__(128, TCN <= 128 ? 2 : 1) k_tc_rowgemm(const fl
     const int k0 = kc * TCK, cw = min(TCK, Kg - k0), c4 = 4 * (t & 15);
     uint8_t* img = abuf + b * (128 * TCK * 2);
     if (c4 >= cw) return;
-    for (int r = t >> 4; r < 128; r += 8) {
-      const int i = i0 + r, k = k0 + c4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    // all 8 rows' loads first (independent, in flight together), then convert
+    float4 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int i = i0 + (t >> 4) + 16 * q, k = k0 + c4;
+      v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (i < R) {
         const float* src = A + (int64_t)i * lda + k;
         if (k + 3 < K) {
-          v = __ldg(reinterpret_cast<const float4*>(src));
+          v[q] = __ldg(reinterpret_cast<const float4*>(src));
         } else {
-          if (k < K) v.x = __ldg(src);
-          if (k + 1 < K) v.y = __ldg(src + 1);
-          if (k + 2 < K) v.z = __ldg(src + 2);
+          if (k < K) v[q].x = __ldg(src);
+          if (k + 1 < K) v[q].y = __ldg(src + 1);
+          if (k + 2 < K) v[q].z = __ldg(src + 2);
         }
       }
-      const uint2 u = make_uint2(pack2(v.x, v.y), pack2(v.z, v.w));
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = (t >> 4) + 16 * q;
+      const uint2 u = make_uint2(pack2(v[q].x, v[q].y), pack2(v[q].z, v[q].w));
       *reinterpret_cast<uint2*>(img + (r >> 3) * (cw * 16) + (c4 >> 3) * 128 + (r & 7) * 16 +
                                 (c4 & 7) * 2) = u;
     }
@@ -233,10 +240,13 @@ __global__ void __launch_bounds__(128, TCN <= 128 ? 2 : 1) k_tc_rowgemm(const fl
   }
   mbar_wait(&bars[1 + ((nch - 1) & 1)], (uint32_t)(((nch - 1) >> 1) & 1));
   tc_after();
-  // epilogue: warp w reads TMEM lanes 32w..32w+31 (row = lane)
-  const int row = warp * 32 + lane, i = i0 + row;
-  const uint32_t lane_base = tm + ((uint32_t)(warp * 32) << 16);
-  for (int jl = 0; jl < nn; jl += 16) {
+  // epilogue: warp w reads TMEM lanes 32(w%4)..+31 (row = lane); warps 0-3 take the
+  // first half of the 16-column groups, warps 4-7 the second
+  const int row = (warp & 3) * 32 + lane, i = i0 + row;
+  const uint32_t lane_base = tm + ((uint32_t)((warp & 3) * 32) << 16);
+  const int ngrp = nn / 16, gsplit = (ngrp + 1) / 2;
+  const int jl_begin = (warp < 4 ? 0 : gsplit) * 16, jl_end = (warp < 4 ? gsplit : ngrp) * 16;
+  for (int jl = jl_begin; jl < jl_end; jl += 16) {
     float v[16];
     tmem_ld16(lane_base + (uint32_t)jl, v);
     if (i < R) {
@@ -258,6 +268,147 @@ __global__ void __launch_bounds__(128, TCN <= 128 ? 2 : 1) k_tc_rowgemm(const fl
   if (warp == 0) {
     tc_after();
     tmem_dealloc(tm, TCN);
+  }
+}
+
+// tcgen05 weight-gradient GEMM: C[P×Q] += Σ_r A[r][p]·B[r][q] over this CTA's row
+// range (split-K over blockIdx.z, fp32 atomics), bf16 operands, fp32 TMEM
+// accumulation.  One CTA = 128 p (MMA M) × Qt ≤ 256 q (MMA N); both operands are
+// MN-major images of 32 path-rows (K) converted from fp32, double-buffered.
+// bias (blockIdx.y == 0... CTAs of q-tile 0): += Σ_r A[r][p] accumulated during conversion.
+constexpr int TNK = 32;   // rows (K) per chunk
+__global__ void __launch_bounds__(256, 2) k_tc_tngemm(const float* __restrict__ A, int lda,
+                                                     const float* __restrict__ B, int ldb, int R,
+                                                     int P, int Q, float* __restrict__ C, int ldc,
+                                                     float* __restrict__ bias, int rows_per_split,
+                                                     int Qt) {
+  using namespace tc;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const int Qtp = (Qt + 15) / 16 * 16;
+  uint8_t* aimg = sm;                                   // 2 × [TNK rows × 128 cols] bf16
+  uint8_t* bimg = sm + 2 * TNK * 128 * 2;               // 2 × [TNK rows × Qtp cols] bf16
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ uint32_t tslot;
+  __shared__ float bsum[128];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int p0 = blockIdx.x * 128, q0 = blockIdx.y * Qt;
+  const int r_begin = blockIdx.z * rows_per_split, r_end = min(R, r_begin + rows_per_split);
+  const bool do_bias = bias && blockIdx.y == 0;
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  if (t < 128) bsum[t] = 0.0f;
+  if (warp == 0) tmem_alloc(&tslot, 256);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tm = tslot;
+  const int nch = (r_end - r_begin + TNK - 1) / TNK;
+  // chunk c: rows r_begin + 32c .. +31; A cols p0..p0+127 (32 float4 per row), B cols
+  // q0..q0+Qtp-1; thread t: float4 column group t % 32 (A) of rows t/32 + 8j
+  auto convert = [&](int c, int b) {
+    const int r0 = r_begin + c * TNK;
+    uint8_t* ai = aimg + b * (TNK * 128 * 2);
+    uint8_t* bi = bimg + b * (TNK * Qtp * 2);
+    float bs[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+      const int c4 = 4 * (t & 31), p = p0 + c4;
+      float4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int rl = (t >> 5) + 8 * j, r = r0 + rl;
+        v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < r_end) {
+          const float* src = A + (int64_t)r * lda + p;
+          if (p + 3 < P) v[j] = __ldg(reinterpret_cast<const float4*>(src));
+          else {
+            if (p < P) v[j].x = __ldg(src);
+            if (p + 1 < P) v[j].y = __ldg(src + 1);
+            if (p + 2 < P) v[j].z = __ldg(src + 2);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int rl = (t >> 5) + 8 * j;
+        *reinterpret_cast<uint2*>(ai + (rl >> 3) * (128 * 16) + (c4 >> 3) * 128 + (rl & 7) * 16 +
+                                  (c4 & 7) * 2) = make_uint2(pack2(v[j].x, v[j].y), pack2(v[j].z, v[j].w));
+        if (do_bias) { bs[0] += v[j].x; bs[1] += v[j].y; bs[2] += v[j].z; bs[3] += v[j].w; }
+      }
+      if (do_bias) {
+        atomicAdd(&bsum[c4], bs[0]); atomicAdd(&bsum[c4 + 1], bs[1]);
+        atomicAdd(&bsum[c4 + 2], bs[2]); atomicAdd(&bsum[c4 + 3], bs[3]);
+      }
+    }
+    // B: Qtp/4 float4 groups per row, TNK rows
+    const int ng = Qtp / 4;
+    for (int e = t; e < ng * TNK; e += 256) {
+      const int rl = e / ng, c4 = 4 * (e - rl * ng), r = r0 + rl, q = q0 + c4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < r_end && c4 < Qt) {
+        const float* src = B + (int64_t)r * ldb + q;
+        if (q + 3 < Q && c4 + 3 < Qt) v = __ldg(reinterpret_cast<const float4*>(src));
+        else {
+          if (q < Q && c4 < Qt) v.x = __ldg(src);
+          if (q + 1 < Q && c4 + 1 < Qt) v.y = __ldg(src + 1);
+          if (q + 2 < Q && c4 + 2 < Qt) v.z = __ldg(src + 2);
+        }
+      }
+      *reinterpret_cast<uint2*>(bi + (rl >> 3) * (Qtp * 16) + (c4 >> 3) * 128 + (rl & 7) * 16 +
+                                (c4 & 7) * 2) = make_uint2(pack2(v.x, v.y), pack2(v.z, v.w));
+    }
+  };
+  const uint32_t idesc = idesc_bf16(128, Qtp, true, true);
+  if (nch > 0) {
+    convert(0, 0);
+    fence_async_smem();
+  }
+  tc_before();
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    const int b = c & 1;
+    if (t == 0) {
+      tc_after();
+      gemm(tm, mnmaj(aimg + b * (TNK * 128 * 2), 128), mnmaj(bimg + b * (TNK * Qtp * 2), Qtp), TNK / 16,
+           idesc, c > 0);
+      mma_commit(&bars[b]);
+    }
+    if (c + 1 < nch) {
+      if (c >= 1) mbar_wait(&bars[b ^ 1], (uint32_t)(((c - 1) >> 1) & 1));
+      convert(c + 1, b ^ 1);
+      fence_async_smem();
+    }
+    tc_before();
+    __syncthreads();
+  }
+  if (nch > 0) {
+    mbar_wait(&bars[(nch - 1) & 1], (uint32_t)(((nch - 1) >> 1) & 1));
+    tc_after();
+    // epilogue: lane = p row (warps w%4), warps 0-3 / 4-7 split the 16-column groups
+    const int row = (warp & 3) * 32 + lane, p = p0 + row;
+    const uint32_t lane_base = tm + ((uint32_t)((warp & 3) * 32) << 16);
+    const int ngrp = Qtp / 16, gsplit = (ngrp + 1) / 2;
+    const int jb = (warp < 4 ? 0 : gsplit) * 16, je = (warp < 4 ? gsplit : ngrp) * 16;
+    for (int jl = jb; jl < je; jl += 16) {
+      float v[16];
+      tmem_ld16(lane_base + (uint32_t)jl, v);
+      if (p < P) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int q = q0 + jl + e;
+          if (jl + e < Qt && q < Q && v[e] != 0.0f) atomicAdd(C + (int64_t)p * ldc + q, v[e]);
+        }
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  if (do_bias && t < 128 && p0 + t < P && bsum[t] != 0.0f) atomicAdd(bias + p0 + t, bsum[t]);
+  if (warp == 0) {
+    tc_after();
+    tmem_dealloc(tm, 256);
   }
 }
 
@@ -1018,7 +1169,7 @@ cudaError_t tc_rows(const ShArgs& a, int k, const float* A, int lda, int R, int 
   RET(cudaFuncSetAttribute(k_tc_rowgemm<NT, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem));
   dim3 grid((R + 127) / 128, (Npad + TCN - 1) / TCN);
-  k_tc_rowgemm<NT, Epi><<<grid, 128, smem, s>>>(A, lda, R, K, a.wimg + a.off_img[k], a.w, Kp, NC,
+  k_tc_rowgemm<NT, Epi><<<grid, 256, smem, s>>>(A, lda, R, K, a.wimg + a.off_img[k], a.w, Kp, NC,
                                                  Npad, epi);
   return cudaGetLastError();
 }
@@ -1036,6 +1187,29 @@ cudaError_t gemm_tn(const float* A, int lda, const float* B, int ldb, int R, int
   splits = (R + rows - 1) / rows;
   dim3 grid((Q + BB - 1) / BB, (P + BB - 1) / BB, splits);
   k_gemm_tn128<<<grid, NTH, 0, s>>>(A, lda, B, ldb, R, P, Q, C, ldc, bias, rows);
+  return cudaGetLastError();
+}
+
+// bf16 tcgen05 weight-gradient GEMM (precision BF16 of the shared formulation)
+cudaError_t gemm_tn_tc(const float* A, int lda, const float* B, int ldb, int R, int P, int Q,
+                       float* C, int ldc, float* bias, cudaStream_t s) {
+  const int Qt = Q <= 256 ? Q : 256;
+  const int Qtp = (Qt + 15) / 16 * 16;
+  const int tiles = ((P + 127) / 128) * ((Q + Qt - 1) / Qt);
+#ifndef BSDE_EXP_TN_CTAS
+#define BSDE_EXP_TN_CTAS 296
+#endif
+  int splits = (BSDE_EXP_TN_CTAS + tiles - 1) / tiles;
+  const int max_splits = (R + 4 * TNK - 1) / (4 * TNK);   // >= 128 rows per split
+  if (splits > max_splits) splits = max_splits;
+  if (splits < 1) splits = 1;
+  int rows = (R + splits - 1) / splits;
+  rows = (rows + TNK - 1) / TNK * TNK;
+  splits = (R + rows - 1) / rows;
+  const size_t smem = 2 * (size_t)TNK * 128 * 2 + 2 * (size_t)TNK * Qtp * 2;
+  RET(cudaFuncSetAttribute(k_tc_tngemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((P + 127) / 128, (Q + Qt - 1) / Qt, splits);
+  k_tc_tngemm<<<grid, 256, smem, s>>>(A, lda, B, ldb, R, P, Q, C, ldc, bias, rows, Qt);
   return cudaGetLastError();
 }
 
@@ -1190,7 +1364,10 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   const int W = a.w, K0 = a.d + 1, L = a.L;
   const bool nais = a.arch == 2;
   const bool res = a.arch == 1 || nais;      // NAIS-Net blocks are residual with h = 1 (R26)
-  const bool tcg = a.tc && !nais;            // bf16 tcgen05 row GEMMs (weight gradients stay fp32)
+  const bool tcg = a.tc && !nais;            // bf16 tcgen05 row GEMMs
+  // weight gradients on tcgen05 too once the row reduction is long enough to hide the
+  // fp32 -> bf16 staging (measured: slower than the SIMT kernel at R = 5 100, faster at 2e5)
+  const bool tctn = tcg && R >= 32768;
   const float* P = a.params;
   int nl = 0;
   // the layer matrix of the forward/back-propagation GEMMs: W_k, or A_k for a NAIS block
@@ -1267,7 +1444,8 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   for (int k = 0; k < L; ++k) {
     const int K = k == 0 ? K0 : W;
     // W̄_k (NAIS-Net: Ā_k, transformed to R̄_k at the end) += δ_kᵀ ḡ_{k-1}
-    RET(gemm_tn(a.D[k], W, gprev, ldprev, R, W, K, gW(k), K, nullptr, s));
+    if (tctn) RET(gemm_tn_tc(a.D[k], W, gprev, ldprev, R, W, K, gW(k), K, nullptr, s));
+    else RET(gemm_tn(a.D[k], W, gprev, ldprev, R, W, K, gW(k), K, nullptr, s));
     Op2 inj;
     if (nais && k > 0) {   // B̄_k += δ_kᵀ ḡ_u;  δ̄_k += ḡ_u B_kᵀ
       RET(gemm_tn(a.D[k], W, a.G0b, a.K0p, R, W, K0, G + a.off_Bk[k], K0, nullptr, s));
@@ -1301,7 +1479,8 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
       RET(gemm_tn(a.Ab[cur], W, a.U0, a.K0p, R, W, K0, G + a.off_Bk[k], K0, gb(k), s));
       nl += 2;
     } else {
-      RET(gemm_tn(a.Ab[cur], W, hin, ldh, R, W, K, gW(k), K, gb(k), s));   // + b̄_k = Σ ā_k
+      if (tctn) RET(gemm_tn_tc(a.Ab[cur], W, hin, ldh, R, W, K, gW(k), K, gb(k), s));
+      else RET(gemm_tn(a.Ab[cur], W, hin, ldh, R, W, K, gW(k), K, gb(k), s));   // + b̄_k = Σ ā_k
       ++nl;
     }
     if (k == 0) break;

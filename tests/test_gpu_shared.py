@@ -221,3 +221,16 @@ def test_zN_term_matches_oracle(problem):
                         np.arange(B), B, x0=x0, zN=True)
     assert abs(loss - ref["loss"]) <= TOL * ref["loss"], (loss, ref["loss"])
     check_grad(s.get_grads(), ref["grad"])
+
+
+def test_bf16_tensor_core_weight_gradients_large_rows():
+    """R ≥ 32 768 rows: the weight-gradient GEMMs also run on tcgen05 (split over
+    row ranges, MN-major bf16 images).  Loss and gradient vs the oracle at 2e-2 on
+    sampled sizes: d = 20, w = 64, L = 3, N = 8, M = 4 000 (36 000 rows)."""
+    d, w, L, N, T, B = 20, 64, 3, 8, 1.0, 4000
+    s = make("hjb", d, w, L, N, T, B, precision="bf16", lr=1e-3)
+    p = perturb(s, 8)
+    loss = s.compute_grad()
+    ref = osh.iteration(ob.HJB, d, w, L, osh.FC, N, T, p.astype(np.float64), 0, 0, np.arange(B), B)
+    assert abs(loss - ref["loss"]) <= 2e-2 * ref["loss"]
+    check_grad(s.get_grads(), ref["grad"], tol=2e-2)
