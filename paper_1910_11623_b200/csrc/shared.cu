@@ -240,27 +240,39 @@ __global__ void __launch_bounds__(256, TCN <= 128 ? 2 : 1) k_tc_rowgemm(const fl
   }
   mbar_wait(&bars[1 + ((nch - 1) & 1)], (uint32_t)(((nch - 1) >> 1) & 1));
   tc_after();
-  // epilogue: warp w reads TMEM lanes 32(w%4)..+31 (row = lane); warps 0-3 take the
-  // first half of the 16-column groups, warps 4-7 the second
-  const int row = (warp & 3) * 32 + lane, i = i0 + row;
-  const uint32_t lane_base = tm + ((uint32_t)((warp & 3) * 32) << 16);
-  const int ngrp = nn / 16, gsplit = (ngrp + 1) / 2;
-  const int jl_begin = (warp < 4 ? 0 : gsplit) * 16, jl_end = (warp < 4 ? gsplit : ngrp) * 16;
-  for (int jl = jl_begin; jl < jl_end; jl += 16) {
-    float v[16];
-    tmem_ld16(lane_base + (uint32_t)jl, v);
-    if (i < R) {
+  // epilogue, two phases through shared memory (the operand buffers are free now):
+  // TMEM -> smem tile [128 rows][nn] (lane = row, warps 0-3 / 4-7 split the column
+  // groups), then each warp walks whole rows with 4 columns per lane, so every
+  // epilogue array access is a coalesced row segment
+  float* stile = reinterpret_cast<float*>(sm);
+  const int ldt = nn + 4;
+  {
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t lane_base = tm + ((uint32_t)((warp & 3) * 32) << 16);
+    const int ngrp = nn / 16, gsplit = (ngrp + 1) / 2;
+    const int jb = (warp < 4 ? 0 : gsplit) * 16, je = (warp < 4 ? gsplit : ngrp) * 16;
+    for (int jl = jb; jl < je; jl += 16) {
+      float v[16];
+      tmem_ld16(lane_base + (uint32_t)jl, v);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = n0 + jl + 4 * q;
-        if (epi.ld % 4 == 0 && j + 3 < NC) {
-          epi.v4(i, j, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-        } else {
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(stile + row * ldt + jl + 4 * q) =
+            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  }
+  __syncthreads();
+  for (int r = warp; r < 128; r += 8) {
+    const int i = i0 + r, jl = 4 * lane;
+    if (i >= R || jl >= nn) continue;
+    const float4 val = *reinterpret_cast<const float4*>(stile + r * ldt + jl);
+    const int j = n0 + jl;
+    if (epi.ld % 4 == 0 && j + 3 < NC) {
+      epi.v4(i, j, val);
+    } else {
+      const float vv[4] = {val.x, val.y, val.z, val.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (j + e < NC) epi(i, j + e, v[4 * q + e]);
-        }
-      }
+      for (int e = 0; e < 4; ++e)
+        if (j + e < NC) epi(i, j + e, vv[e]);
     }
   }
   tc_before();
@@ -1165,7 +1177,9 @@ cudaError_t tc_rows(const ShArgs& a, int k, const float* A, int lda, int R, int 
   const int Kin = k == 0 ? a.d + 1 : a.w, Kp = (Kin + 15) / 16 * 16;
   const int Npad = NT ? (a.w + 15) / 16 * 16 : Kp;
   // weight slab: NT [TCN rows × Kp], NN [w rows × TCN]
-  const size_t smem = 2 * 128 * TCK * 2 + (size_t)TCN * (NT ? Kp : a.w) * 2;
+  size_t smem = 2 * 128 * TCK * 2 + (size_t)TCN * (NT ? Kp : a.w) * 2;
+  const size_t stage = (size_t)128 * (TCN + 4) * sizeof(float);   // the epilogue tile
+  if (smem < stage) smem = stage;
   RET(cudaFuncSetAttribute(k_tc_rowgemm<NT, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem));
   dim3 grid((R + 127) / 128, (Npad + TCN - 1) / TCN);
