@@ -398,21 +398,37 @@ __global__ void __launch_bounds__(256, 2) k_tc_tngemm(const float* __restrict__ 
   if (nch > 0) {
     mbar_wait(&bars[(nch - 1) & 1], (uint32_t)(((nch - 1) >> 1) & 1));
     tc_after();
-    // epilogue: lane = p row (warps w%4), warps 0-3 / 4-7 split the 16-column groups
-    const int row = (warp & 3) * 32 + lane, p = p0 + row;
+    // epilogue in column halves of ≤128 through shared memory: TMEM -> tile [128 p][128 q]
+    // (lane = p), then warps walk whole p rows, 4 q per lane: the fp32 atomics of a warp
+    // hit one contiguous 512-byte row segment
+    float* stile = reinterpret_cast<float*>(sm);
+    constexpr int LDT = 128 + 4;
+    const int row = (warp & 3) * 32 + lane;
     const uint32_t lane_base = tm + ((uint32_t)((warp & 3) * 32) << 16);
-    const int ngrp = Qtp / 16, gsplit = (ngrp + 1) / 2;
-    const int jb = (warp < 4 ? 0 : gsplit) * 16, je = (warp < 4 ? gsplit : ngrp) * 16;
-    for (int jl = jb; jl < je; jl += 16) {
-      float v[16];
-      tmem_ld16(lane_base + (uint32_t)jl, v);
-      if (p < P) {
+    for (int h0 = 0; h0 < Qtp; h0 += 128) {
+      const int hn = min(128, Qtp - h0), ngrp = hn / 16, gsplit = (ngrp + 1) / 2;
+      const int jb = (warp < 4 ? 0 : gsplit) * 16, je = (warp < 4 ? gsplit : ngrp) * 16;
+      for (int jl = jb; jl < je; jl += 16) {
+        float v[16];
+        tmem_ld16(lane_base + (uint32_t)(h0 + jl), v);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int q = q0 + jl + e;
-          if (jl + e < Qt && q < Q && v[e] != 0.0f) atomicAdd(C + (int64_t)p * ldc + q, v[e]);
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(stile + row * LDT + jl + 4 * q) =
+              make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+      __syncthreads();
+      for (int r = warp; r < 128; r += 8) {
+        const int p = p0 + r, jl = 4 * lane;
+        if (p >= P || jl >= hn) continue;
+        const float4 val = *reinterpret_cast<const float4*>(stile + r * LDT + jl);
+        const float vv[4] = {val.x, val.y, val.z, val.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int ql = h0 + jl + e, q = q0 + ql;
+          if (ql < Qt && q < Q && vv[e] != 0.0f) atomicAdd(C + (int64_t)p * ldc + q, vv[e]);
         }
       }
+      __syncthreads();
     }
   }
   tc_before();
@@ -1220,7 +1236,8 @@ cudaError_t gemm_tn_tc(const float* A, int lda, const float* B, int ldb, int R, 
   int rows = (R + splits - 1) / splits;
   rows = (rows + TNK - 1) / TNK * TNK;
   splits = (R + rows - 1) / rows;
-  const size_t smem = 2 * (size_t)TNK * 128 * 2 + 2 * (size_t)TNK * Qtp * 2;
+  size_t smem = 2 * (size_t)TNK * 128 * 2 + 2 * (size_t)TNK * Qtp * 2;
+  if (smem < (size_t)128 * 132 * sizeof(float)) smem = (size_t)128 * 132 * sizeof(float);   // epilogue tile
   RET(cudaFuncSetAttribute(k_tc_tngemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((P + 127) / 128, (Q + Qt - 1) / Qt, splits);
   k_tc_tngemm<<<grid, 256, smem, s>>>(A, lda, B, ldb, R, P, Q, C, ldc, bias, rows, Qt);
