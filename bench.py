@@ -330,7 +330,7 @@ def main():
     if rank == 0:
         pk = peaks()
         B_local = wl.batch // world
-        if family == "tc" and wl.precision == "bf16":
+        if family in ("tc", "shared-tc") and wl.precision == "bf16":
             bound, peak, pk_name = "tensor", pk["bf16_tflops_sustained"], "bf16 sustained (measured)"
         elif family == "tc":
             bound, peak = "tensor", pk["bf16_tflops_sustained"] / 3.0
@@ -355,7 +355,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16" if (family == "tc" and wl.precision == "bf16") else "f32",
+            "dtype": "bf16" if (family in ("tc", "shared-tc") and wl.precision == "bf16") else "f32",
             "data": "synthetic (Philox4x32-10 Brownian increments generated on device, R8)",
             "config": config_dict(wl, world, family),
             "roofline": {"bound": bound, "kernel": "bsde_" + dom, "achieved": achieved,
