@@ -796,6 +796,11 @@ struct EpiUp {         // Œ¥ÃÑ_k = ·∏°_{k-1} W_k·µÄ:  ·∏°_k = Œ¥ÃÑ ‚äô s'_k (+ ·
   float* Gb;           // ·∏°_k
   float* Sb;           // sÃÑ_k
   int ld;
+  // last layer only: ƒÅ_L = (sÃÑ_L + ≈´ v) ‚äô s'_L straight away (and hÃÑ_L = ≈´ v for a
+  // residual last layer), instead of storing sÃÑ_L for a separate pass
+  const float* ub = nullptr;
+  float* Ab = nullptr;
+  float* HbL = nullptr;
   __device__ void operator()(int i, int j, float db) const {
     const int64_t o = (int64_t)i * ld + j;
     const float s = S[o];
@@ -803,7 +808,14 @@ struct EpiUp {         // Œ¥ÃÑ_k = ·∏°_{k-1} W_k·µÄ:  ·∏°_k = Œ¥ÃÑ ‚äô s'_k (+ ·
     float gb = db * (1.0f - s * s);
     if (Gbprev) gb += Gbprev[o];
     Gb[o] = gb;
-    Sb[o] = -2.0f * s * g * db;
+    const float sb = -2.0f * s * g * db;
+    if (Ab) {
+      const float hb = __ldg(ub + i) * __ldg(gv + j);
+      if (HbL) HbL[o] = hb;
+      Ab[o] = (sb + hb) * (1.0f - s * s);
+    } else {
+      Sb[o] = sb;
+    }
   }
   __device__ void v4(int i, int j, float4 db) const {
     const int64_t o = (int64_t)i * ld + j;
@@ -815,7 +827,15 @@ struct EpiUp {         // Œ¥ÃÑ_k = ·∏°_{k-1} W_k·µÄ:  ·∏°_k = Œ¥ÃÑ ‚äô s'_k (+ ·
       gb = F4MAP(comp(gb, e_) + comp(gp, e_));
     }
     st4(Gb + o, gb);
-    st4(Sb + o, F4MAP(-2.0f * comp(s, e_) * comp(g, e_) * comp(db, e_)));
+    const float4 sb = F4MAP(-2.0f * comp(s, e_) * comp(g, e_) * comp(db, e_));
+    if (Ab) {
+      const float u = __ldg(ub + i);
+      const float4 hb = F4MAP(u * __ldg(gv + j + e_));
+      if (HbL) st4(HbL + o, hb);
+      st4(Ab + o, F4MAP((comp(sb, e_) + comp(hb, e_)) * (1.0f - comp(s, e_) * comp(s, e_))));
+    } else {
+      st4(Sb + o, sb);
+    }
   }
 };
 
@@ -1023,22 +1043,6 @@ __global__ void k_sh_loss(ShArgs a) {
     double s = 0.0;
     for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
     if (s != 0.0) atomicAdd(a.loss_acc, s);
-  }
-}
-
-// ƒÅ_L = (sÃÑ_L + ≈´ v) ‚äô s'_L (and hÃÑ_L = ≈´ v for a residual last layer); a CTA per row batch
-__global__ void k_sh_abar_last(ShArgs a, const float* Sb, const float* S, float* Ab, float* Hb) {
-  const int64_t R = (int64_t)(a.N + 1) * a.M;
-  const float* v = a.params + a.off_v;
-  for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
-    const float u = a.ub[r];
-    for (int j = threadIdx.x; j < a.w; j += blockDim.x) {
-      const int64_t id = r * a.w + j;
-      const float hb = u * __ldg(v + j);
-      if (Hb) Hb[id] = hb;
-      const float s = S[id];
-      Ab[id] = (Sb[id] + hb) * (1.0f - s * s);
-    }
   }
 }
 
@@ -1486,6 +1490,11 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
     float* gout = a.Gb[k & 1];
     EpiUp e{a.S[k], k < L - 1 ? a.G[k] : nullptr, v, (res && k > 0) ? gprev : nullptr, gout,
             a.Sb[k], W};
+    if (k == L - 1) {   // fuse ƒÅ_L (former k_sh_abar_last) into the last up-product
+      e.ub = a.ub;
+      e.Ab = a.Ab[0];
+      e.HbL = res ? a.Hb[0] : nullptr;
+    }
     if (tcg) RET(tc_rows<true>(a, k, gprev, ldprev, R, K, W, e, s));
     else RET(gemm_rows<true>(gprev, ldprev, Wk(k), K, R, W, K, e, s, inj));
     nl += 2;
@@ -1498,10 +1507,7 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   nl += 2;
   // down: ƒÅ_L, then k = L..1: WÃÑ_k += ƒÅ_k·µÄ h_{k-1}, bÃÑ_k += Œ£ ƒÅ_k, ƒÅ_{k-1} = (sÃÑ_{k-1} + ƒÅ_k W_k (+ hÃÑ_k)) ‚äô s'
   int cur = 0;
-  k_sh_abar_last<<<148 * 8, NTH, 0, s>>>(
-      a, a.Sb[L - 1], a.S[L - 1], a.Ab[cur], res ? a.Hb[cur] : nullptr);
-  RET(cudaGetLastError());
-  ++nl;
+  // ƒÅ_L (and hÃÑ_L) were written by the last up-product's epilogue into Ab[0] / Hb[0]
   for (int k = L - 1; k >= 0; --k) {
     const float* hin = k == 0 ? a.U0 : a.H[k - 1];
     const int K = k == 0 ? K0 : W, ldh = k == 0 ? a.K0p : W;
