@@ -154,7 +154,9 @@ __global__ void __launch_bounds__(256, TCN <= 128 ? 2 : 1) k_tc_rowgemm(const fl
   __shared__ __align__(8) uint64_t bars[3];             // weights, MMA done (×2)
   __shared__ uint32_t tslot;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int i0 = blockIdx.x * 128, n0 = blockIdx.y * TCN, nn = min(TCN, Npad - n0);
+  // blockIdx.x = N tile (fastest): the CTAs sharing a row tile run back to back, so the
+  // second one finds A in L2
+  const int i0 = blockIdx.y * 128, n0 = blockIdx.x * TCN, nn = min(TCN, Npad - n0);
   if (t == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -1202,7 +1204,7 @@ cudaError_t tc_rows(const ShArgs& a, int k, const float* A, int lda, int R, int 
   if (smem < stage) smem = stage;
   RET(cudaFuncSetAttribute(k_tc_rowgemm<NT, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem));
-  dim3 grid((R + 127) / 128, (Npad + TCN - 1) / TCN);
+  dim3 grid((Npad + TCN - 1) / TCN, (R + 127) / 128);
   k_tc_rowgemm<NT, Epi><<<grid, 256, smem, s>>>(A, lda, R, K, a.wimg + a.off_img[k], a.w, Kp, NC,
                                                  Npad, epi);
   return cudaGetLastError();
