@@ -221,7 +221,8 @@ def config_dict(wl, gpus, family):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 40: >= 0.5 s under load, several 100 ms clock samples; 10 for --impl reference)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="cfg5_allen_cahn_scaleout", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -234,6 +235,8 @@ def main():
     ap.add_argument("--sharded-adam", action="store_true",
                     help="reduce-scatter + sharded Adam + all-gather (NEXT-4) for N > 1")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 10 if args.impl == "reference" else 40
     wl = CONFIGS[args.workload]
     if args.precision:
         wl = wl.with_(precision=args.precision)

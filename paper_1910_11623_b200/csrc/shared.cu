@@ -30,6 +30,8 @@
 // fp32 TMEM accumulation, same epilogues); the weight gradients stay fp32.
 // NAIS-Net blocks (arch 2): A_k = -R_kᵀR_k - εI per iteration, the input
 // injection as a second operand pair of the row GEMMs (R26).
+#include <type_traits>
+
 #include "kernels.cuh"
 #include "tc_common.cuh"
 
@@ -142,8 +144,8 @@ constexpr int TCK = 64;   // K chunk of the A image
 #define BSDE_EXP_TCN 128
 #endif
 constexpr int TCN = BSDE_EXP_TCN;  // N tile (columns of C per CTA)
-template <bool NT, class Epi>
-__global__ void __launch_bounds__(256, TCN <= 128 ? 2 : 1) k_tc_rowgemm(const float* __restrict__ A, int lda, int R,
+template <bool NT, class Epi, int TN>
+__global__ void __launch_bounds__(256, TN <= 128 ? 2 : 1) k_tc_rowgemm(const float* __restrict__ A, int lda, int R,
                                                       int K, const uint16_t* __restrict__ wimg,
                                                       int wrows, int Kp, int NC, int Npad,
                                                       Epi epi) {
@@ -156,14 +158,14 @@ __global__ void __launch_bounds__(256, TCN <= 128 ? 2 : 1) k_tc_rowgemm(const fl
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   // blockIdx.x = N tile (fastest): the CTAs sharing a row tile run back to back, so the
   // second one finds A in L2
-  const int i0 = blockIdx.y * 128, n0 = blockIdx.x * TCN, nn = min(TCN, Npad - n0);
+  const int i0 = blockIdx.y * 128, n0 = blockIdx.x * TN, nn = min(TN, Npad - n0);
   if (t == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     mbar_init(&bars[2], 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(&tslot, TCN);
+  if (warp == 0) tmem_alloc(&tslot, TN);
   tc_before();
   __syncthreads();
   tc_after();
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(256, TCN <= 128 ? 2 : 1) k_tc_rowgemm(const fl
   __syncthreads();
   if (warp == 0) {
     tc_after();
-    tmem_dealloc(tm, TCN);
+    tmem_dealloc(tm, TN);
   }
 }
 
@@ -868,54 +870,48 @@ struct EpiDown {       // h̄_{k-1} = ā_k W_k (+ h̄_k);  ā_{k-1} = (s̄_{k-1}
 };
 
 // ---------------------------------------------------------------- row kernels
-// Paths of this rank, in two passes.  k_sh_dw: ΔW rows (n·M + m) = ΔW_n, one
-// thread per (step, path, 4-component block), all independent (R8 counters);
-// coupled paths sum the fine increments (R22).  k_sh_x: one thread per (path,
-// block) runs the Euler recursion and writes U0 rows (n·M + m) = [t_n, X_n].
-__global__ void k_sh_dw(ShArgs a) {
-  const int nq = (a.d + 3) >> 2;
-  const int64_t tot = (int64_t)a.N * a.M * nq;
-  const uint32_t it = a.eval ? a.eval_it : a.state->it;
-  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < tot;
-       id += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t nm = id / nq;
-    const int q = (int)(id - nm * nq);
-    const int n = (int)(nm / a.M);
-    const int64_t m = nm - (int64_t)n * a.M;
-    float dw[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int j = 0; j < a.cpl; ++j) {
-      const float4 z = normals4((uint32_t)q, (uint32_t)(a.m0 + m), (uint32_t)(n * a.cpl + j), it,
-                                a.k0, a.k1);
-      dw[0] += a.sqrt_dt_f * z.x; dw[1] += a.sqrt_dt_f * z.y;
-      dw[2] += a.sqrt_dt_f * z.z; dw[3] += a.sqrt_dt_f * z.w;
-    }
-    float* o = a.dW + nm * a.d + 4 * q;
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (4 * q + e < a.d) o[e] = dw[e];
-  }
-}
-
-__global__ void k_sh_x(ShArgs a) {
+// Paths of this rank: ΔW rows (n·M + m) = ΔW_n and U0 rows (n·M + m) = [t_n, X_n].
+// a1 + a2 for the shared formulation in one pass: one thread per (path m, block q
+// of 4 components) walks n = 0..N, writes the row (t_n, X_n) of U0, draws the
+// step's four normals (one Philox call per coupled sub-step, R8/R22), stores ΔW_n
+// (the loss and the double-backward read it) and takes the Euler step in
+// registers — no load sits on the N-step dependency chain.
+__global__ void k_sh_paths(ShArgs a) {
   const int nq = (a.d + 3) >> 2;
   const int64_t tot = a.M * nq;
+  const uint32_t it = a.eval ? a.eval_it : a.state->it;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < tot;
        id += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = id / nq;
     const int q = (int)(id - m * nq);
     float x[4] = {a.x0, a.x0, a.x0, a.x0};
-    for (int n = 0; n <= a.N; ++n) {
+    auto row = [&](int n) {
       float* u = a.U0 + ((int64_t)n * a.M + m) * a.K0p;
       if (q == 0) u[0] = (float)n * a.dt;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         if (4 * q + e < a.d) u[1 + 4 * q + e] = x[e];
-      if (n == a.N) break;
-      const float* dw = a.dW + ((int64_t)n * a.M + m) * a.d + 4 * q;
+    };
+    // the draws do not depend on X: unrolled, four steps' Philox calls overlap
+#pragma unroll 4
+    for (int n = 0; n < a.N; ++n) {
+      row(n);
+      float dw[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int j = 0; j < a.cpl; ++j) {
+        const float4 z = normals4((uint32_t)q, (uint32_t)(a.m0 + m), (uint32_t)(n * a.cpl + j), it,
+                                  a.k0, a.k1);
+        dw[0] += a.sqrt_dt_f * z.x; dw[1] += a.sqrt_dt_f * z.y;
+        dw[2] += a.sqrt_dt_f * z.z; dw[3] += a.sqrt_dt_f * z.w;
+      }
+      float* o = a.dW + ((int64_t)n * a.M + m) * a.d + 4 * q;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (4 * q + e < a.d) x[e] = x_step(a.problem, x[e], dw[e]);
+        if (4 * q + e < a.d) {
+          o[e] = dw[e];
+          x[e] = x_step(a.problem, x[e], dw[e]);
+        }
     }
+    row(a.N);
   }
 }
 
@@ -1198,15 +1194,16 @@ cudaError_t tc_rows(const ShArgs& a, int k, const float* A, int lda, int R, int 
                     const Epi& epi, cudaStream_t s) {
   const int Kin = k == 0 ? a.d + 1 : a.w, Kp = (Kin + 15) / 16 * 16;
   const int Npad = NT ? (a.w + 15) / 16 * 16 : Kp;
-  // weight slab: NT [TCN rows × Kp], NN [w rows × TCN]
-  size_t smem = 2 * 128 * TCK * 2 + (size_t)TCN * (NT ? Kp : a.w) * 2;
-  const size_t stage = (size_t)128 * (TCN + 4) * sizeof(float);   // the epilogue tile
+  constexpr int TN = TCN;   // (TCN/2 at the paper's R = 5 100, 160 CTAs instead of 80: measured slower)
+  // weight slab: NT [TN rows × Kp], NN [w rows × TN]
+  size_t smem = 2 * 128 * TCK * 2 + (size_t)TN * (NT ? Kp : a.w) * 2;
+  const size_t stage = (size_t)128 * (TN + 4) * sizeof(float);   // the epilogue tile
   if (smem < stage) smem = stage;
-  RET(cudaFuncSetAttribute(k_tc_rowgemm<NT, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  RET(cudaFuncSetAttribute(k_tc_rowgemm<NT, Epi, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem));
-  dim3 grid((Npad + TCN - 1) / TCN, (R + 127) / 128);
-  k_tc_rowgemm<NT, Epi><<<grid, 256, smem, s>>>(A, lda, R, K, a.wimg + a.off_img[k], a.w, Kp, NC,
-                                                 Npad, epi);
+  dim3 grid((Npad + TN - 1) / TN, (R + 127) / 128);
+  k_tc_rowgemm<NT, Epi, TN><<<grid, 256, smem, s>>>(A, lda, R, K, a.wimg + a.off_img[k], a.w, Kp,
+                                                     NC, Npad, epi);
   return cudaGetLastError();
 }
 
@@ -1214,8 +1211,16 @@ cudaError_t tc_rows(const ShArgs& a, int k, const float* A, int lda, int R, int 
 cudaError_t gemm_tn(const float* A, int lda, const float* B, int ldb, int R, int P, int Q, float* C,
                     int ldc, float* bias, cudaStream_t s) {
   const int tiles = ((P + BB - 1) / BB) * ((Q + BB - 1) / BB);
-  int splits = (2 * 148 + tiles - 1) / tiles;
-  const int max_splits = (R + 8 * BKK - 1) / (8 * BKK);   // >= 64 rows per split
+  // CTA target: one per SM for short reductions (the paper's R = 5 100: 296 and 592
+  // measured 4-8% slower), two per SM for long ones (R = 2e5: 3% faster)
+#ifndef BSDE_EXP_TNS_CTAS
+#define BSDE_EXP_TNS_CTAS (R < 32768 ? 148 : 296)
+#endif
+#ifndef BSDE_EXP_TNS_MINROWS
+#define BSDE_EXP_TNS_MINROWS (8 * BKK)
+#endif
+  int splits = (BSDE_EXP_TNS_CTAS + tiles - 1) / tiles;
+  const int max_splits = (R + BSDE_EXP_TNS_MINROWS - 1) / (BSDE_EXP_TNS_MINROWS);   // rows per split
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
   int rows = (R + splits - 1) / splits;
@@ -1413,11 +1418,9 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   auto bk = [&](int k) { return P + a.off_W[k] + (int64_t)W * (k == 0 ? K0 : W); };
   const float* v = P + a.off_v;
   // paths
-  k_sh_dw<<<grid_for((int64_t)a.N * a.M * ((a.d + 3) / 4), NTH), NTH, 0, s>>>(a);
+  k_sh_paths<<<grid_for(a.M * ((a.d + 3) / 4), 64), 64, 0, s>>>(a);
   RET(cudaGetLastError());
-  k_sh_x<<<grid_for(a.M * ((a.d + 3) / 4), 64), 64, 0, s>>>(a);
-  RET(cudaGetLastError());
-  nl += 2;
+  ++nl;
   if (tcg) {    // bf16 images of this iteration's W_k
     k_tc_pack_w<<<grid_for((int64_t)W * W, NTH), NTH, 0, s>>>(a);
     RET(cudaGetLastError());
