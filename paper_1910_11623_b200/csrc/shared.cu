@@ -1241,7 +1241,10 @@ cudaError_t gemm_tn_tc(const float* A, int lda, const float* B, int ldb, int R, 
 #define BSDE_EXP_TN_CTAS 296
 #endif
   int splits = (BSDE_EXP_TN_CTAS + tiles - 1) / tiles;
-  const int max_splits = (R + 4 * TNK - 1) / (4 * TNK);   // >= 128 rows per split
+#ifndef BSDE_EXP_TCTN_MINROWS
+#define BSDE_EXP_TCTN_MINROWS (4 * TNK)
+#endif
+  const int max_splits = (R + BSDE_EXP_TCTN_MINROWS - 1) / (BSDE_EXP_TCTN_MINROWS);   // rows per split
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
   int rows = (R + splits - 1) / splits;
@@ -1408,8 +1411,12 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   const bool res = a.arch == 1 || nais;      // NAIS-Net blocks are residual with h = 1 (R26)
   const bool tcg = a.tc && !nais;            // bf16 tcgen05 row GEMMs
   // weight gradients on tcgen05 too once the row reduction is long enough to hide the
-  // fp32 -> bf16 staging (measured: slower than the SIMT kernel at R = 5 100, faster at 2e5)
-  const bool tctn = tcg && R >= 32768;
+  // fp32 -> bf16 staging (measured at R = 5 100: 1.6% faster per iteration than the
+  // SIMT kernel with its one-CTA-per-SM split; faster at 2e5)
+#ifndef BSDE_EXP_TCTN_MINR
+#define BSDE_EXP_TCTN_MINR 4096
+#endif
+  const bool tctn = tcg && R >= BSDE_EXP_TCTN_MINR;
   const float* P = a.params;
   int nl = 0;
   // the layer matrix of the forward/back-propagation GEMMs: W_k, or A_k for a NAIS block
