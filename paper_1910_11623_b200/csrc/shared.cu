@@ -871,31 +871,20 @@ struct EpiDown {       // h̄_{k-1} = ā_k W_k (+ h̄_k);  ā_{k-1} = (s̄_{k-1}
 
 // ---------------------------------------------------------------- row kernels
 // Paths of this rank: ΔW rows (n·M + m) = ΔW_n and U0 rows (n·M + m) = [t_n, X_n].
-// a1 + a2 for the shared formulation in one pass: one thread per (path m, block q
-// of 4 components) walks n = 0..N, writes the row (t_n, X_n) of U0, draws the
-// step's four normals (one Philox call per coupled sub-step, R8/R22), stores ΔW_n
-// (the loss and the double-backward read it) and takes the Euler step in
-// registers — no load sits on the N-step dependency chain.
+// a1 + a2 for the shared formulation, one CTA per path m: (1) the CTA's threads
+// draw every (step n, 4-component block q) of the path independently (one Philox
+// call per coupled sub-step, R8/R22) and store ΔW_n — the loss and the
+// double-backward read it; (2) one thread per component runs the Euler recursion
+// over n, its ΔW loads batched 8 steps ahead (the path's rows are L1/L2-hot), and
+// writes the rows (t_n, X_n) of U0.  (A thread per (m, q) walking n serially, with
+// the draws on the recursion's critical path, took 31 µs at the paper's M = 100.)
 __global__ void k_sh_paths(ShArgs a) {
   const int nq = (a.d + 3) >> 2;
-  const int64_t tot = a.M * nq;
   const uint32_t it = a.eval ? a.eval_it : a.state->it;
-  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < tot;
-       id += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = id / nq;
-    const int q = (int)(id - m * nq);
-    float x[4] = {a.x0, a.x0, a.x0, a.x0};
-    auto row = [&](int n) {
-      float* u = a.U0 + ((int64_t)n * a.M + m) * a.K0p;
-      if (q == 0) u[0] = (float)n * a.dt;
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (4 * q + e < a.d) u[1 + 4 * q + e] = x[e];
-    };
-    // the draws do not depend on X: unrolled, four steps' Philox calls overlap
-#pragma unroll 4
-    for (int n = 0; n < a.N; ++n) {
-      row(n);
+  const int64_t sdw = a.M * a.d, su = a.M * a.K0p;   // row strides of step n
+  for (int64_t m = blockIdx.x; m < a.M; m += gridDim.x) {
+    for (int id = threadIdx.x; id < a.N * nq; id += blockDim.x) {
+      const int n = id / nq, q = id - n * nq;
       float dw[4] = {0.f, 0.f, 0.f, 0.f};
       for (int j = 0; j < a.cpl; ++j) {
         const float4 z = normals4((uint32_t)q, (uint32_t)(a.m0 + m), (uint32_t)(n * a.cpl + j), it,
@@ -903,15 +892,36 @@ __global__ void k_sh_paths(ShArgs a) {
         dw[0] += a.sqrt_dt_f * z.x; dw[1] += a.sqrt_dt_f * z.y;
         dw[2] += a.sqrt_dt_f * z.z; dw[3] += a.sqrt_dt_f * z.w;
       }
-      float* o = a.dW + ((int64_t)n * a.M + m) * a.d + 4 * q;
+      float* o = a.dW + n * sdw + m * a.d + 4 * q;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (4 * q + e < a.d) {
-          o[e] = dw[e];
-          x[e] = x_step(a.problem, x[e], dw[e]);
-        }
+        if (4 * q + e < a.d) o[e] = dw[e];
     }
-    row(a.N);
+    __syncthreads();   // this path's ΔW rows are visible to the whole CTA
+    for (int j = threadIdx.x; j < a.d; j += blockDim.x) {
+      const float* dw = a.dW + m * a.d + j;
+      float* u = a.U0 + m * a.K0p + 1 + j;
+      float x = a.x0;
+      int n = 0;
+      for (; n + 8 <= a.N; n += 8) {
+        float w[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) w[r] = dw[(n + r) * sdw];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          u[(n + r) * su] = x;
+          x = x_step(a.problem, x, w[r]);
+        }
+      }
+      for (; n < a.N; ++n) {
+        const float w = dw[n * sdw];
+        u[n * su] = x;
+        x = x_step(a.problem, x, w);
+      }
+      u[(int64_t)a.N * su] = x;
+    }
+    for (int n = threadIdx.x; n <= a.N; n += blockDim.x) a.U0[n * su + m * a.K0p] = (float)n * a.dt;
+    __syncthreads();
   }
 }
 
@@ -1425,7 +1435,7 @@ cudaError_t launch_shared_step(const ShArgs& a, cudaStream_t s, cudaEvent_t mid,
   auto bk = [&](int k) { return P + a.off_W[k] + (int64_t)W * (k == 0 ? K0 : W); };
   const float* v = P + a.off_v;
   // paths
-  k_sh_paths<<<grid_for(a.M * ((a.d + 3) / 4), 64), 64, 0, s>>>(a);
+  k_sh_paths<<<(unsigned)(a.M < 65536 ? a.M : 65536), 128, 0, s>>>(a);
   RET(cudaGetLastError());
   ++nl;
   if (tcg) {    // bf16 images of this iteration's W_k
