@@ -142,13 +142,37 @@ def round_bf16(x):
     return b.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
+def round_fp16(x):
+    """Round-to-nearest-even to IEEE binary16 (via fp32), returned as float64:
+    the storage precision of ΔW_n in the tensor-core reading of R17."""
+    return np.asarray(x, dtype=np.float32).astype(np.float16).astype(np.float64)
+
+
+def _ident(a):
+    return a
+
+
 # ----------------------------------------------------------------------------
 # One iteration: rollout + terminal loss + hand adjoint
 # ----------------------------------------------------------------------------
-def net_forward(net, x, bf16=False):
+def net_forward(net, x, bf16=False, tc=False, rb=round_bf16):
     """Per-step Z-net (R4; Eq. 7 with h = 1):
-    A1 = W1 x + b1, H1 = ReLU(A1), A2 = W2 H1 + b2, H2 = H1 + ReLU(A2), Z = W3 H2 + b3."""
-    op = round_bf16 if bf16 else (lambda a: a)
+    A1 = W1 x + b1, H1 = ReLU(A1), A2 = W2 H1 + b2, H2 = H1 + ReLU(A2), Z = W3 H2 + b3.
+
+    bf16 (R17 as SURVEY states it): GEMM operands rounded to bf16, everything
+    else exact.  tc (R17 as DESIGN.md records it for the tensor-core path): the
+    biases are GEMM operands too (folded into a constant-1 input column), H1 is
+    stored as bf16(ReLU(A1)) and the residual sum is formed in bf16,
+    H2 = bf16(H1 + bf16(ReLU(A2))) (one rounding of the exact sum of two bf16
+    values).  ``rb`` is the rounding (identity in the structural pin)."""
+    if tc:
+        A1 = rb(x) @ rb(net["W1"]).T + rb(net["b1"])
+        H1 = rb(np.maximum(A1, 0.0))
+        A2 = H1 @ rb(net["W2"]).T + rb(net["b2"])
+        H2 = rb(H1 + rb(np.maximum(A2, 0.0)))
+        Z = H2 @ rb(net["W3"]).T + rb(net["b3"])
+        return A1, H1, A2, H2, Z
+    op = round_bf16 if bf16 else _ident
     A1 = op(x) @ op(net["W1"]).T + net["b1"]
     H1 = np.maximum(A1, 0.0)
     A2 = op(H1) @ op(net["W2"]).T + net["b2"]
@@ -159,7 +183,8 @@ def net_forward(net, x, bf16=False):
 
 def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
               x0=0.0, lam=1.0, want_grad=True, bf16=False, keep=False, kink_band=0.0,
-              mask_shift=0.0, coupled_factor=1):
+              mask_shift=0.0, coupled_factor=1, tc=False, rb=round_bf16, rh=round_fp16,
+              kink_flip=0.0):
     """One training iteration on the shard ``paths`` (global path indices).
 
     Returns dict(loss_sum=Σ_m R², loss=Σ R²/B_global, grad=∂L/∂params of this
@@ -173,7 +198,11 @@ def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
     mask flips.  mask_shift (tests only) evaluates the backward masks as
     1[A > mask_shift] to emulate such flips.  coupled_factor = f > 1 draws every
     increment as the sum of the f increments of the grid with N·f steps that it
-    spans (coupled multilevel paths, philox.coupled_increments).
+    spans (coupled multilevel paths, philox.coupled_increments).  kink_flip > 0
+    widens that band by kink_flip·max_j |W_ij x_j| (the largest single term of the
+    pre-activation): the reach of one operand x_j landing on the other side of a
+    rounding boundary (one bf16 ulp, kink_flip = 2^-8), which finite-precision
+    accumulation can cause upstream of the kink (R19, tensor-core reading).
     """
     paths = np.asarray(paths, dtype=np.int64)
     B = float(batch_global)
@@ -186,9 +215,10 @@ def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
     for n in range(N):
         dW = (philox.brownian_increments(seed, it, n, paths, d, dt) if coupled_factor == 1
               else philox.coupled_increments(seed, it, n, paths, d, dt, coupled_factor))
-        A1, H1, A2, H2, Z = net_forward(nets[n], X, bf16)                # P:78, Eq. 7
+        A1, H1, A2, H2, Z = net_forward(nets[n], X, bf16, tc, rb)        # P:78, Eq. 7
         trace.append((X, dW, A1, H1, A2, H2, Z, Y))
-        Y = Y - driver_f(problem, Y, Z, lam) * dt + np.sum(Z * dW, axis=-1)   # P:66 (φ=-f)
+        dWz = rh(dW) if tc else dW
+        Y = Y - driver_f(problem, Y, Z, lam) * dt + np.sum(Z * dWz, axis=-1)  # P:66 (φ=-f)
         X = forward_step(problem, X, dW)
     R = Y - terminal_g(problem, X)
     out = dict(loss_sum=float(np.sum(R * R)), loss=float(np.sum(R * R) / B),
@@ -209,23 +239,38 @@ def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
         X, dW, A1, H1, A2, H2, Z, Yn = trace[n]
         net, g = nets[n], gnets[n]
         # ∂Y_{n+1}/∂Z_n = ΔW_n - Δt ∂_z f ;  ∂Y_{n+1}/∂Y_n = 1 - Δt ∂_y f
-        dZ = abar[:, None] * (dW - dt * driver_df_dz(problem, Yn, Z, lam))
-        g["W3"][...] = op(dZ).T @ op(H2)
-        g["b3"][...] = dZ.sum(0)
-        dH2 = op(dZ) @ op(net["W3"])
+        dZ = abar[:, None] * ((rh(dW) if tc else dW) - dt * driver_df_dz(problem, Yn, Z, lam))
         m2 = A2 > mask_shift                         # ReLU'(0) = 0 (R15)
-        dA2 = dH2 * m2
-        g["W2"][...] = op(dA2).T @ op(H1)
-        g["b2"][...] = dA2.sum(0)
-        dH1 = dH2 + op(dA2) @ op(net["W2"])
         m1 = A1 > mask_shift
-        dA1 = dH1 * m1
-        g["W1"][...] = op(dA1).T @ op(X)
-        g["b1"][...] = dA1.sum(0)
+        if tc:
+            dZ = rb(dZ)
+            g["W3"][...] = dZ.T @ H2
+            g["b3"][...] = dZ.sum(0)
+            dH2 = dZ @ rb(net["W3"])
+            dA2 = rb(dH2) * m2
+            g["W2"][...] = dA2.T @ H1
+            g["b2"][...] = dA2.sum(0)
+            dH1 = dH2 + dA2 @ rb(net["W2"])
+            dA1 = rb(dH1) * m1
+            g["W1"][...] = dA1.T @ rb(X)
+            g["b1"][...] = dA1.sum(0)
+        else:
+            g["W3"][...] = op(dZ).T @ op(H2)
+            g["b3"][...] = dZ.sum(0)
+            dH2 = op(dZ) @ op(net["W3"])
+            dA2 = dH2 * m2
+            g["W2"][...] = op(dA2).T @ op(H1)
+            g["b2"][...] = dA2.sum(0)
+            dH1 = dH2 + op(dA2) @ op(net["W2"])
+            dA1 = dH1 * m1
+            g["W1"][...] = op(dA1).T @ op(X)
+            g["b1"][...] = dA1.sum(0)
         if kink_band > 0.0:
             s = snets[n]
-            amb1 = np.abs(A1) <= kink_band * (np.abs(X) @ np.abs(net["W1"]).T + np.abs(net["b1"]))
-            amb2 = np.abs(A2) <= kink_band * (np.abs(H1) @ np.abs(net["W2"]).T + np.abs(net["b2"]))
+            amb1 = np.abs(A1) <= (kink_band * (np.abs(X) @ np.abs(net["W1"]).T + np.abs(net["b1"]))
+                                  + kink_flip * _max_term(X, net["W1"]))
+            amb2 = np.abs(A2) <= (kink_band * (np.abs(H1) @ np.abs(net["W2"]).T + np.abs(net["b2"]))
+                                  + kink_flip * _max_term(H1, net["W2"]))
             e2 = np.abs(dH2) * amb2                  # |ΔdA2| if an A2 mask flips
             e1 = (np.abs(dH1) * amb1                 # |ΔdA1| from an A1 flip ...
                   + (e2 @ np.abs(net["W2"])) * (m1 | amb1))   # ... or propagated from A2
@@ -238,6 +283,15 @@ def iteration(problem, d, w, N, T, params, seed, it, paths, batch_global,
     out["grad"] = grad
     if kink_band > 0.0:
         out["slack"] = slack
+    return out
+
+
+def _max_term(x, W):
+    """max_j |W_ij x_j| per (row of x, i), or 0 when the caller passes no flip width."""
+    out = np.empty((x.shape[0], W.shape[0]))
+    aW = np.abs(W)
+    for i in range(0, x.shape[0], 128):
+        out[i:i + 128] = np.max(np.abs(x[i:i + 128])[:, None, :] * aW[None], axis=2)
     return out
 
 

@@ -425,7 +425,9 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
         mbar_arrive(&wfree[3]);   // G3 done: W̃3 -> step s + 1
       mbar_wait(&full[slot], (uint32_t)((s / L::NSLOT) & 1));   // ΔW_n, |X_N|² partials
       tc_after();
-      float cz = 0.0f, zz = 0.0f, sz = 0.0f;
+      // four partial sums per reduction: the 100-term dot products are not one
+      // serial FMA chain (4-cycle latency each) on the critical path
+      float cz4[4] = {0.f, 0.f, 0.f, 0.f}, zz4[4] = {0.f, 0.f, 0.f, 0.f}, sz4[4] = {0.f, 0.f, 0.f, 0.f};
       const uint32_t tdw = tm + lane_off + L::T_DW + (uint32_t)slot * L::DWC;
       // the driver's extra reduction (|Z|² for HJB, Σ Z for Black-Scholes) is a
       // compile-time choice: one instance runs, the chain carries no predicated work
@@ -449,9 +451,9 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
 #pragma unroll
             for (int e = 0; e < 8; ++e)
               if (8 * c + e < D) {
-                cz = fmaf(z[i][e], dw[e], cz);
-                if (MODE == 1) zz = fmaf(z[i][e], z[i][e], zz);
-                if (MODE == 2) sz += z[i][e];
+                cz4[e & 3] = fmaf(z[i][e], dw[e], cz4[e & 3]);
+                if (MODE == 1) zz4[e & 3] = fmaf(z[i][e], z[i][e], zz4[e & 3]);
+                if (MODE == 2) sz4[e & 3] += z[i][e];
               }
           }
         }
@@ -462,6 +464,9 @@ __device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint
         e3(Int<2>{});
       else
         e3(Int<0>{});
+      const float cz = (cz4[0] + cz4[1]) + (cz4[2] + cz4[3]);
+      const float zz = (zz4[0] + zz4[1]) + (zz4[2] + zz4[3]);
+      const float sz = (sz4[0] + sz4[1]) + (sz4[2] + sz4[3]);
       if (n + 1 == N) {
         const float* x2 = reinterpret_cast<const float*>(slotp + Dm::XB);
         xn2 = kTPath == 3 ? (x2[row] + x2[128 + row]) + x2[256 + row] : x2[row] + x2[128 + row];

@@ -325,6 +325,58 @@ def test_round_bf16_matches_torch():
     assert np.array_equal(bsde.round_bf16(x), ref)
 
 
+def test_round_fp16_matches_torch():
+    """The binary16 rounding of ΔW_n in the tensor-core reading of R17: RNE as
+    torch's conversion, over normal and subnormal half-precision magnitudes."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(20000) * 10.0 ** rng.integers(-7, 4, 20000)
+    ref = torch.tensor(x, dtype=torch.float32).to(torch.float16).to(torch.float64).numpy()
+    assert np.array_equal(bsde.round_fp16(x), ref)
+
+
+@pytest.mark.parametrize("problem", [bsde.HEAT, bsde.HJB, bsde.ALLEN_CAHN, bsde.BLACK_SCHOLES])
+def test_tc_emulation_with_identity_roundings_is_the_exact_oracle(problem):
+    """Structural pin of the tensor-core rounding model (iteration(tc=True)): with
+    the roundings replaced by the identity, the folded biases, the bf16-formed
+    residual sum, the ΔW_n storage and the adjoint's operand sites collapse to
+    the exact algebra, bit for bit (so the model differs from the oracle only
+    where it rounds), and with the roundings in place it does round."""
+    d, w, N, T, B = 7, 9, 3, 1.0, 40
+    p = bsde.init_params(2, d, w, N)
+    p[1:] += 0.05 * np.random.default_rng(1).standard_normal(p.size - 1)
+    x0 = 0.7 if problem == bsde.BLACK_SCHOLES else 0.0
+    ex = bsde.iteration(problem, d, w, N, T, p, 0, 1, np.arange(B), B, x0=x0, kink_band=1e-3)
+    idn = bsde.iteration(problem, d, w, N, T, p, 0, 1, np.arange(B), B, x0=x0, kink_band=1e-3,
+                         tc=True, rb=bsde._ident, rh=bsde._ident)
+    assert idn["loss"] == ex["loss"]
+    assert np.array_equal(idn["grad"], ex["grad"]) and np.array_equal(idn["slack"], ex["slack"])
+    tc = bsde.iteration(problem, d, w, N, T, p, 0, 1, np.arange(B), B, x0=x0, tc=True)
+    assert tc["loss"] != ex["loss"] and not np.array_equal(tc["grad"], ex["grad"])
+    # within the bf16 error model: operands carry 2^-9 relative rounding
+    assert abs(tc["loss"] - ex["loss"]) <= 2e-2 * ex["loss"]
+    assert np.linalg.norm(tc["grad"] - ex["grad"]) <= 2e-2 * np.linalg.norm(ex["grad"])
+
+
+def test_tc_emulation_rounds_at_each_documented_site():
+    """Each rounding site of the model moves the result on its own (a site the
+    model forgot would leave the result unchanged when only it is switched):
+    only ΔW_n in binary16, and only the bf16 operand rounding."""
+    d, w, N, T, B = 10, 12, 3, 1.0, 64
+    p = bsde.init_params(3, d, w, N)
+    p[1:] += 0.05 * np.random.default_rng(2).standard_normal(p.size - 1)
+    ex = bsde.iteration(bsde.HJB, d, w, N, T, p, 0, 0, np.arange(B), B)
+    only_h = bsde.iteration(bsde.HJB, d, w, N, T, p, 0, 0, np.arange(B), B, tc=True,
+                            rb=bsde._ident)
+    only_b = bsde.iteration(bsde.HJB, d, w, N, T, p, 0, 0, np.arange(B), B, tc=True,
+                            rh=bsde._ident)
+    for r, lo, hi in ((only_h, 1e-7, 3e-3), (only_b, 1e-6, 2e-2)):
+        rel = np.linalg.norm(r["grad"] - ex["grad"]) / np.linalg.norm(ex["grad"])
+        assert lo < rel < hi, rel
+    # binary16 ΔW: the Y update sees Σ Z·fp16(ΔW); X advances with the exact ΔW
+    assert np.array_equal(only_h["X_N"], ex["X_N"])
+
+
 def test_zero_head_init_keeps_allen_cahn_bounded():
     """R7b: with a Xavier head the Allen-Cahn rollout explodes at config-3 sizes
     (Y leaves [-1, 1] and the cubic driver diverges); with W3 = 0 (Z ≡ 0) Y_n

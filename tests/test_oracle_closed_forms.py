@@ -56,6 +56,22 @@ def test_expected_g_matches_oracle_terminal_sample():
     assert abs(g.mean() - eg) < 4 * g.std() / np.sqrt(B)
 
 
+def test_allen_cahn_terminal_g_matches_golden_expectation():
+    """Pin of terminal_g(ALLEN_CAHN) (P:312 garbled "(2+0.4‖x‖)^-1", read as
+    1/(2 + 0.4|x|²) per BASELINE config 3, R12): the oracle's own g on its own
+    X_N (20000 paths, T = 0.3) averages to the golden E[g(X_T)] = 0.0391263556
+    (SURVEY Appendix A quadrature, tests/golden/closed_forms.txt).  The literal
+    reading 1/(2 + 0.4|x|) would average ≈ 0.19 and fail."""
+    d, w, N, T, B = 100, 4, 4, 0.3, 20000
+    p = bsde.init_params(0, d, w, N, zero_head=True)
+    r = bsde.iteration(bsde.ALLEN_CAHN, d, w, N, T, p, 0, 0, np.arange(B), B, want_grad=False)
+    g = bsde.terminal_g(bsde.ALLEN_CAHN, r["X_N"])
+    val, tol = golden()["ac_Eg_d100_T03"]
+    assert abs(g.mean() - val) < 4 * g.std() / np.sqrt(B) + tol
+    # and the residual the iteration reports uses that g: R = Y_N - g(X_N)
+    assert np.allclose(r["R"], r["Y_N"] - g, rtol=0, atol=1e-15)
+
+
 @pytest.mark.slow
 def test_heat_training_reaches_closed_form():
     """Pin H3: trained Y0 → u(0,0) = 2dT = 20 for the config-1 problem.
