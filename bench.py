@@ -252,6 +252,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--deterministic", action="store_true",
                     help="fixed-order reductions instead of atomics (cfg.deterministic)")
+    ap.add_argument("--no-multilevel", action="store_true",
+                    help="skip the config-4 multilevel time-to-target sub-object (rank 0, N = 1)")
+    ap.add_argument("--ml-iters", type=int, default=10000,
+                    help="single-level iterations of the multilevel experiment")
+    ap.add_argument("--ml-precision", default="bf16")
     ap.add_argument("--sharded-adam", action="store_true",
                     help="reduce-scatter + sharded Adam + all-gather (NEXT-4) for N > 1")
     args = ap.parse_args()
@@ -425,8 +430,20 @@ def main():
                                     "sample": "%d of %d paths x N=%d, fp64 numpy oracle, median "
                                               "of 2 iterations" % (paths, wl.batch, wl.N),
                                     "cpu": cpu_info()}
+        if not args.no_multilevel and world == 1 and args.workload == "cfg5_allen_cahn_scaleout":
+            # the metric's second half (BASELINE.json): config 4's multilevel schedule
+            # against single-level training, wall clock to the same target loss, this run
+            s.close()
+            s = None
+            from bench_multilevel import run_cfg4
+            ml = run_cfg4(args.ml_precision, args.ml_iters)
+            ml["note"] = ("config 4 (HJB d=100, N 5->80, B=65536) with %s operands on the %s "
+                          "kernels; time-to-target = training wall clock (evaluations excluded) "
+                          "until the eval loss <= target" % (args.ml_precision, ml["kernel"]))
+            line["multilevel"] = ml
         print(json.dumps(line), flush=True)
-    s.close()
+    if s is not None:
+        s.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

@@ -52,7 +52,11 @@ enum {
 /* GEMM operand precision; accumulation is always fp32 (R17, R18). */
 enum {
   BSDE_FP32 = 0,       /* fp32-accurate: bf16x3 split operands on tcgen05, or SIMT FFMA */
-  BSDE_BF16 = 1        /* bf16 operands, fp32 accumulate                              */
+  BSDE_BF16 = 1        /* bf16 operands, fp32 accumulate.  Per-step nets on tcgen05
+                          (DESIGN R17): the biases are folded into the bf16 weight images,
+                          H1 = bf16(ReLU(A1)), H2 = bf16(H1 + bf16(ReLU(A2))) (one bf16x2
+                          add), ΔW_n enters the Y update's Z·ΔW and the adjoint's dZ as its
+                          binary16 value; X, Y, the reductions and Adam are fp32         */
 };
 
 /* Kernel family selection. */
@@ -109,8 +113,9 @@ typedef struct {
                              BSDE_FORM_SHARED: the paper's own formulation (PAPER.md:69-77,
                              Eq. 6; DESIGN R23, R24): one network
                              u(t, x) of n_widths tanh layers shared by all steps, Y_n =
-                             u(t_n, X_n), z_n = σ(X_n)ᵀ∇ₓu, residual-sum loss.  FP32 and the
-                             SIMT kernels only                                              */
+                             u(t_n, X_n), z_n = σ(X_n)ᵀ∇ₓu, residual-sum loss.  fp32 SIMT
+                             GEMMs, or (precision BSDE_BF16, FC / ResNet) tcgen05 row and
+                             weight-gradient GEMMs with bf16 operands                        */
   int sharded_adam;       /* 1 (with an NCCL communicator): reduce-scatter of the gradient,
                              Adam on this rank's 1/world shard of the parameters, all-gather
                              of the updated parameters (the optimizer half) in

@@ -80,15 +80,18 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 __device__ __forceinline__ void box_muller_fast(uint32_t xa, uint32_t xb, float sdt, float& z0,
                                                 float& z1) {
   const uint32_t k = xa >> 9;
-  // -2 ln(u1): series of -2 log1p(-v) for u1 > 1 - 2^-6 (v = 1 - u1, exact), else
-  // -2 ln2 · lg2.approx(u1); both evaluated, selected without a branch.
-  const float v = __int_as_float((int)((0x7FFFFFu - k) | 0x3F800000u)) - 0.99999994039535522f;
-  const float r2s = 2.0f * v * fmaf(v, fmaf(v, fmaf(v, 0.25f, 0.33333333f), 0.5f), 1.0f);
+  const float u1 = unit_fast(xa);
+  // -2 ln(u1): series of -2 log1p(-v), v = 1 - u1 (exact: Sterbenz) for u1 > 1 - 2^-6,
+  // else -2 ln2 · lg2.approx(u1); both evaluated, selected without a branch.
+  const float v = 1.0f - u1;
+  const float r2s = v * fmaf(v, fmaf(v, fmaf(v, 0.5f, 0.66666667f), 1.0f), 2.0f);
   float l2;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(unit_fast(xa)));
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(u1));
   const float r2 = k >= 0x7E0000u ? r2s : -1.38629436111989061f * l2;
   const float r = sqrt_approx(r2) * sdt;
-  const float a = fmaf(unit_fast(xb), 6.28318530717958648f, -3.14159265358979324f);
+  // angle 2π(u2 - 1/2) ∈ (-π, π); u2 - 1/2 by the same exponent trick (exact)
+  const float a = (__int_as_float((int)((xb >> 9) | 0x3F800000u)) - 1.49999994039535522f) *
+                  6.28318530717958648f;
   float s, c;
   __sincosf(a, &s, &c);
   z0 = -r * c;

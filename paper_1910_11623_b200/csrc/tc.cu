@@ -91,53 +91,6 @@ __device__ __forceinline__ bool chunk_lt(int g, int i, int NC) {
   return (3 + 4 * i < NC) || (4 * i < NC && g + 4 * i < NC);
 }
 
-// ΔW_n at this thread's columns, dw[8i + e] = ΔW[8(g + 4i) + e] (columns < D).
-struct DwGen {
-  uint32_t m, n, it, k0, k1;
-  float sdt;
-  int g;   // slot s = (i, h) = (s/2, s%2) holds 4-block 2(g+4i)+h
-  // Slots [S0, S1): the Philox rounds of all slots are interleaved (independent
-  // dependency chains give the scheduler ILP), then the Box-Muller maps.  Slots
-  // whose columns are >= D for every column group are skipped at compile time.
-  template <int D, int S0, int S1>
-  __device__ __forceinline__ void run(float (&dw)[32]) const {
-    constexpr int K = S1 - S0;
-    uint4 c[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      const int s = S0 + j;
-      c[j] = make_uint4((uint32_t)(2 * (g + 4 * (s / 2)) + s % 2), m, n, it);
-    }
-    uint32_t a0 = k0, a1 = k1;
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-      if (r) { a0 += kPhiloxW0; a1 += kPhiloxW1; }
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        const int s = S0 + j;
-        if (8 * (4 * (s / 2)) + 4 * (s % 2) >= D) continue;   // never valid
-        const uint32_t lo0 = kPhiloxM0 * c[j].x, hi0 = __umulhi(kPhiloxM0, c[j].x);
-        const uint32_t lo1 = kPhiloxM1 * c[j].z, hi1 = __umulhi(kPhiloxM1, c[j].z);
-        c[j] = make_uint4(hi1 ^ c[j].y ^ a0, lo1, hi0 ^ c[j].w ^ a1, lo0);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      const int s = S0 + j, i = s / 2, h = s % 2;
-      float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-      if (8 * (4 * i) + 4 * h < D) {
-        box_muller_fast(c[j].x, c[j].y, sdt, z0, z1);
-        box_muller_fast(c[j].z, c[j].w, sdt, z2, z3);
-      }
-      const bool ok = col_lt(g, i, 4 * h, D);
-      dw[8 * i + 4 * h + 0] = ok ? z0 : 0.f;
-      dw[8 * i + 4 * h + 1] = ok ? z1 : 0.f;
-      dw[8 * i + 4 * h + 2] = ok ? z2 : 0.f;
-      dw[8 * i + 4 * h + 3] = ok ? z3 : 0.f;
-    }
-  }
-};
-
 }  // namespace tc
 }  // namespace bsde
 
@@ -242,13 +195,20 @@ struct Impl {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return sms;
   }
-  static cudaError_t fwd(const PassArgs& a, cudaStream_t s) {
+  template <bool CPL, bool MULT>
+  static cudaError_t fwd_v(const PassArgs& a, cudaStream_t s) {
     const size_t smem = fwd_smem();
-    cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<D, W, CPL, MULT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int nt = ntiles(a), sms = sm_count();
-    k_fwd_tc<D, W><<<nt < sms ? nt : sms, kFwdThreads, smem, s>>>(a, nt);
+    k_fwd_tc<D, W, CPL, MULT><<<nt < sms ? nt : sms, kFwdThreads, smem, s>>>(a, nt);
     return cudaGetLastError();
+  }
+  static cudaError_t fwd(const PassArgs& a, cudaStream_t s) {
+    const bool mult = a.problem == kBlackScholes;
+    if (a.cpl > 1) return mult ? fwd_v<true, true>(a, s) : fwd_v<true, false>(a, s);
+    return mult ? fwd_v<false, true>(a, s) : fwd_v<false, false>(a, s);
   }
   template <bool NEEDZ>
   static cudaError_t bwd_z(const PassArgs& a, cudaStream_t s) {

@@ -1,29 +1,41 @@
-// tc_fwd.cuh — forward rollout on tcgen05, one fused,
-// warp-specialised pass; CTAs are persistent over 128-path tiles, every tile
-// walks all N steps.
+// tc_fwd.cuh — forward rollout on tcgen05, one fused
+// pass; CTAs are persistent over 128-path tiles, every tile walks all N steps.
 //
-// Producer warps 0-11 (3 threads per path) generate the Brownian paths: the
-// increments ΔW_n = √Δt·z (Philox4x32-10 + Box-Muller, R8) and the
-// Euler states X_{n+1} = X_n + √2 ΔW_n (Eq. 5) in exact fp32
-// registers.  Per step they fill one slot of a four-deep ring: the bf16 X̃_n
-// operand image (constant-1 column d folds the bias) in shared memory and the
-// fp16 ΔW_n pairs in tensor memory, and write both as images to global memory
-// for the adjoint.
+// Work split (12 worker warps + 1 control warp, 416 threads; 13 warps keep the
+// 128-register budget that 17 would cut to 96):
+//  * worker warp w serves TMEM lane quadrant q = w % 4 (paths 32q..32q+31 of the
+//    tile, one path per lane) and column group g = w / 4: the 8-column chunks
+//    c = g, g+3, g+6, ... of every 112-column image.  Every worker both draws
+//    its share of the Brownian increments ΔW_n = √Δt·z (Philox4x32-10 +
+//    Box-Muller, R8) and runs its share of the network epilogues;
+//    the Euler state X_{n+1} = X_n + √2 ΔW_n (Eq. 5) of its columns
+//    stays in exact fp32 registers, ΔW_n in binary16 registers until the Y
+//    update reads it.
+//  * the control warp issues the tcgen05 MMAs (lane 0) once all workers have
+//    arrived at the named barrier of the stage, and streams the per-step weight
+//    images into shared memory with bulk copies.  Workers never wait at a
+//    barrier: they arrive and continue with the next slice of random numbers,
+//    and wait only for the completion of the MMA whose result they read.
 //
-// Consumer warps 12-15 (1 thread per path = TMEM lane; thread 480 issues the
-// MMAs) run the network of step n on the tensor cores:
-//   G1  A1 = X̃_n W̃1ᵀ   (A from the ring slot)     E1  H1 = ReLU(A1)  -> TMEM operand
-//   G2  A2 = H1 W̃2ᵀ    (A from TMEM)              E2  H2 = H1 + ReLU(A2) (Eq. 7, h = 1)
-//   G3  Z  = H2 W̃3ᵀ    (A from TMEM)              E3  Y_{n+1} = Y_n - f Δt + Z·ΔW (Eq. 5, R2)
-// H1 and H2 never touch shared memory: the epilogues store them as bf16 pairs
-// into tensor memory (tcgen05.st), the A operand of the next GEMM, so no proxy
-// fence sits on the chain.  The two fp32 accumulators alternate between steps,
-// which lets G1 of step n+1 run during E3 of step n.  The terminal residual
-// R = Y_N - g(X_N) (Eq. 6) and the scalar adjoint ā close each tile.
-//
-// Sync: ring slot full/empty mbarriers (producers -> MMA thread -> producers);
-// G1 and G2/G3 commits on separate mbarriers; weight images are reloaded per
-// matrix as soon as the GEMM that read them has completed (W̃1 double-buffered).
+// One step n of a tile (Eq. 7, h = 1; R4):
+//    workers: X̃_n (bf16 operand, constant-1 column folds b1) -> TMEM  | arrive B_X
+//    control: G1  A1 = X̃_n W̃1ᵀ                        (A from TMEM)
+//    workers: slice 1 of ΔW_n   | wait G1 | E1 H1 = ReLU(A1) -> TMEM    | arrive B_1
+//    control: G2  A2 = H1 W̃2ᵀ                         (A from TMEM)
+//    workers: slice 2 of ΔW_n   | wait G2 | E2 H2 = H1 + ReLU(A2)       | arrive B_2
+//    control: G3  Z = H2 W̃3ᵀ                          (A from TMEM)
+//    workers: slice 3           | wait G3 | E3 partial sums of Z·ΔW (|Z|², Σ Z)
+//             over the worker's columns | X̃_{n+1} -> TMEM             | arrive B_X
+// A slice is three of the worker's Philox blocks (12 increments), each folded
+// into X at once; ~500 cycles of the SM's issue, longer than the GEMM it hides
+// (~420), so the tensor pipe and the epilogues stay off the critical path.
+// The Y update Y_{n+1} = Y_n - f(Y_n, Z_n)Δt + Z_n·ΔW_n (Eq. 5, R2) of path m is
+// finished by its group-0 worker from the three partial sums during E1 of the
+// next step (the partials are complete once G1 of the next step has been
+// issued, which waits for every worker).  The terminal residual
+// R = Y_N - g(X_N) (Eq. 6) and the scalar adjoint ā close each tile.  The
+// X̃_n (bf16) and ΔW_n (fp16) images go to global memory for the adjoint
+// (DESIGN.md §5).
 #pragma once
 
 namespace bsde {
@@ -43,57 +55,80 @@ __device__ __forceinline__ void unpack_dw(const uint4& u, float* v) {
     v[2 * k + 1] = f.y;
   }
 }
-#ifndef BSDE_EXP_TPATH
-#define BSDE_EXP_TPATH 3
-#endif
-constexpr int kTPath = BSDE_EXP_TPATH;   // producer threads per path
-constexpr int kFwdProducers = 128 * kTPath, kFwdConsumers = 128;
-constexpr int kFwdThreads = kFwdProducers + kFwdConsumers, kFwdProdWarps = kFwdProducers / 32;
-__device__ __forceinline__ void consumer_sync() { named_sync(1, kFwdConsumers); }
 
-// Increments of Philox blocks q = 2c, 2c+1 (columns 8c..8c+7) for the chunks
-// c = c0, c0 + CS, ..., NCH of them, interleaved for ILP; those of blocks whose
-// columns are all >= D are 0.  Coupled paths (cpl > 1, NEXT-3): the sum over the
-// cpl fine steps n·cpl + j of √(Δt/cpl)·z (sdt = √(Δt/cpl)).  The uncoupled
-// instance (CPL false) keeps the loop out of the hot code.
-template <int D, int CS, int NCH, bool CPL>
-__device__ __forceinline__ void gen_chunks(int c0, uint32_t m, uint32_t n, uint32_t it, uint32_t k0,
-                                           uint32_t k1, float sdt, float (&dw)[NCH * 8], int cpl) {
-  constexpr int K = 2 * NCH;
+constexpr int kFwdGroups = 3;                                   // column groups per path
+constexpr int kFwdWorkers = 128 * kFwdGroups, kFwdWorkerWarps = kFwdWorkers / 32;
+constexpr int kFwdThreads = kFwdWorkers + 32;
+// named barriers: X̃_n written (before G1), E1 done (before G2), E2 done (before
+// G3), workers only (tile tail)
+constexpr int kBarX = 1, kBarE1 = 2, kBarE2 = 3, kBarTail = 4;
+
+// Predicates on a worker's column chunk c = g + 3i (g = 0, 1, 2 the column group,
+// warp-uniform) that fold at compile time once i and the offset are constants
+// (after unrolling): true for every g when the largest c satisfies them, false
+// for every g when the smallest does not; only the rest is a runtime test.
+__device__ __forceinline__ bool chunk_lt3(int g, int i, int LIM) {
+  return (kFwdGroups - 1 + kFwdGroups * i < LIM) || (kFwdGroups * i < LIM && g + kFwdGroups * i < LIM);
+}
+// column 8c + off < LIM
+__device__ __forceinline__ bool col_lt3(int g, int i, int off, int LIM) {
+  return (8 * (kFwdGroups - 1 + kFwdGroups * i) + off < LIM) ||
+         (8 * kFwdGroups * i + off < LIM && 8 * (g + kFwdGroups * i) + off < LIM);
+}
+
+// Block b of a worker (columns 8c + 4(b%2), c = g + 3(b/2)) lies below D for every
+// column group / for none: compile-time facts that split a slice into an
+// unconditional prefix and single blocks behind a warp-uniform branch.
+__host__ __device__ constexpr bool blk_all(int b, int D) {
+  return 8 * (kFwdGroups - 1 + kFwdGroups * (b / 2)) + 4 * (b % 2) < D;
+}
+__host__ __device__ constexpr bool blk_none(int b, int D) {
+  return 8 * kFwdGroups * (b / 2) + 4 * (b % 2) >= D;
+}
+__host__ __device__ constexpr int blk_prefix(int b0, int b1, int D) {   // first not-all-valid block
+  return b0 >= b1 ? b1 : (blk_all(b0, D) ? blk_prefix(b0 + 1, b1, D) : b0);
+}
+
+// Increments of the worker's Philox blocks b = B0 .. B0+NB-1 of step n: block b
+// holds columns 8c + 4(b%2) .. +3 of chunk c = g + 3(b/2), i.e. counter word 0
+// q = 2c + b%2 (R8).  Interleaved for ILP; blocks whose columns are all >= D
+// are skipped (the test is warp-uniform: g depends on the warp only) and read
+// as 0.  Coupled paths (cpl > 1, NEXT-3): the sum over the cpl fine steps
+// n·cpl + j of √(Δt/cpl)·z (sdt = √(Δt/cpl)); the uncoupled instance (CPL false)
+// keeps the loop out of the hot code.
+template <int D, int B0, int NB, bool CPL>
+__device__ __forceinline__ void gen_blocks(int g, uint32_t m, uint32_t n, uint32_t it, uint32_t k0,
+                                           uint32_t k1, float sdt, float (&z)[4 * NB], int cpl) {
   auto one = [&](uint32_t nf, bool add) {   // the normals of (fine) step nf
-    uint4 c[K];
-    bool ok[K];   // warp-uniform: block has columns < D
+    uint4 c[NB];
+    bool ok[NB];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      const int q = 2 * (c0 + CS * (j / 2)) + j % 2;
+    for (int j = 0; j < NB; ++j) {
+      const int b = B0 + j, q = 2 * (g + kFwdGroups * (b / 2)) + b % 2;
       c[j] = make_uint4((uint32_t)q, m, nf, it);
-      ok[j] = 4 * q < D;
+      ok[j] = col_lt3(g, b / 2, 4 * (b % 2), D);   // 4q < D
     }
     uint32_t a0 = k0, a1 = k1;
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
       if (r) { a0 += kPhiloxW0; a1 += kPhiloxW1; }
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
+      for (int j = 0; j < NB; ++j) {
+        if (!ok[j]) continue;
         const uint32_t lo0 = kPhiloxM0 * c[j].x, hi0 = __umulhi(kPhiloxM0, c[j].x);
         const uint32_t lo1 = kPhiloxM1 * c[j].z, hi1 = __umulhi(kPhiloxM1, c[j].z);
         c[j] = make_uint4(hi1 ^ c[j].y ^ a0, lo1, hi0 ^ c[j].w ^ a1, lo0);
       }
     }
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      float z[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < NB; ++j) {
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
       if (ok[j]) {
-#ifdef BSDE_DBG_NOBM
-        z[0] = __uint_as_float((c[j].x >> 9) | 0x3c000000u); z[1] = __uint_as_float((c[j].y >> 9) | 0x3c000000u);
-        z[2] = __uint_as_float((c[j].z >> 9) | 0x3c000000u); z[3] = __uint_as_float((c[j].w >> 9) | 0x3c000000u);
-#else
-        box_muller_fast(c[j].x, c[j].y, sdt, z[0], z[1]);
-        box_muller_fast(c[j].z, c[j].w, sdt, z[2], z[3]);
-#endif
+        box_muller_fast(c[j].x, c[j].y, sdt, v[0], v[1]);
+        box_muller_fast(c[j].z, c[j].w, sdt, v[2], v[3]);
       }
 #pragma unroll
-      for (int e = 0; e < 4; ++e) dw[4 * j + e] = add ? dw[4 * j + e] + z[e] : z[e];
+      for (int e = 0; e < 4; ++e) z[4 * j + e] = add ? z[4 * j + e] + v[e] : v[e];
     }
   };
   if constexpr (!CPL) {
@@ -108,430 +143,389 @@ __device__ __forceinline__ void gen_chunks(int c0, uint32_t m, uint32_t n, uint3
 template <int D, int W>
 struct FwdSmem {
   using Dm = Dims<D, W>;
-  static constexpr uint32_t W1 = 0;                           // W̃1 images, two buffers
-  static constexpr uint32_t W2 = 2 * Dm::W1B;
-  static constexpr uint32_t W3 = W2 + Dm::W2B;
-  static constexpr int NSLOT = 4;                            // ring depth (steps)
-  static constexpr uint32_t SLOT0 = W3 + Dm::W3B;
-  static constexpr uint32_t SLOTB = Dm::XB + 3 * 128 * 4;     // X̃_n | |X_N|² partials [kTPath][128]
-  static constexpr uint32_t BARS = SLOT0 + NSLOT * SLOTB;
-  // full[NSLOT], empty[NSLOT], wf1[2], wf2, wf3, g1, g23, w1free[2], w2free, w3free
-  static constexpr int NBARS = 2 * NSLOT + 10;
+  static constexpr uint32_t W1 = 0, W2 = Dm::W1B, W3 = Dm::W1B + Dm::W2B;   // weight images
+  // partial sums per (kind, column group, row): 0 Z·ΔW, 1 |Z|² or Σ Z, 2 |X_N|²
+  static constexpr uint32_t PART = Dm::WB;
+  // ΔW_n of each worker thread in binary16, chunk-slot-major (16 B per thread and slot)
+  static constexpr int NSLOT = ((Dm::Dp / 8 > Dm::Wp / 8 ? Dm::Dp / 8 : Dm::Wp / 8) + kFwdGroups - 1) /
+                               kFwdGroups;
+  static constexpr uint32_t DWS = PART + 3 * kFwdGroups * 128 * 4;
+  static constexpr uint32_t BARS = DWS + NSLOT * kFwdWorkers * 16;
+  // mbarriers: 0 chain GEMM commits, 1-3 weight images W̃1, W̃2, W̃3
+  static constexpr int NBARS = 4;
   static constexpr uint32_t TSLOT = BARS + NBARS * 8;
   static constexpr uint32_t BYTES = TSLOT + 16;
-  // tensor memory columns: accumulators, the A operand of G2/G3, the ΔW_n ring
-  // (fp16 pairs, 4 columns per 8-column chunk of the first ceil(d/8) chunks)
-  static constexpr uint32_t T_ACC1 = 128, T_H = 240, T_DW = 296;
-  static constexpr uint32_t DWC = 4 * ((D + 7) / 8);
-  static_assert(T_H + Dm::Wp / 2 <= T_DW && T_DW + NSLOT * DWC <= 512, "TMEM budget");
+  // tensor memory: the fp32 accumulator, the bf16 A operand of G2/G3 (H1, H2)
+  // and that of G1 (X̃_n; no shared-memory operand, so no proxy fence on the
+  // workers' path)
+  static constexpr uint32_t T_H = 128, T_X = 192, TCOLS = 256;
+  static_assert(T_H + Dm::Wp / 2 <= T_X && T_X + Dm::Dp / 2 <= TCOLS, "TMEM budget");
 };
 
-// Producer thread k of a path (k = 0, 1, 2) owns the 8-column chunks c = k + 3i.
-// One code path for the three threads (instruction-cache footprint); k is
-// warp-uniform.
-template <int D, int W, bool MULT, bool CPL>
-__device__ __forceinline__ void fwd_producer(const PassArgs& a, int ntiles, uint8_t* sm, uint32_t tm,
-                                             int K3, int q, int lane) {
-  using Dm = Dims<D, W>;
-  using L = FwdSmem<D, W>;
-  constexpr int Dp = Dm::Dp, NCD = Dp / 8;
-  constexpr int NI = (NCD + kTPath - 1) / kTPath;   // image chunks of thread 0 (>= the others')
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::BARS);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + L::NSLOT;
-  const int row = 32 * q + lane;
-  const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-  const int N = a.N;
-  const bool store = !a.eval;
-  const uint32_t it = a.eval ? a.eval_it : a.state->it;
-  uint8_t* xst = static_cast<uint8_t*>(a.xpack);
-  uint8_t* dst = static_cast<uint8_t*>(a.dwpack);
-  const uint32_t roff = (row >> 3) * (Dp * 16) + (row & 7) * 16;   // row's offset in an image
-  // Weight reloads: a bulk copy blocks its issuing thread for about the copy's
-  // duration (~700 cycles for one 25 KB matrix), so they are issued here, by
-  // lane 0 of producer warps 1, 2, 3 (W̃1, W̃2, W̃3), between chunks and while
-  // waiting for a free ring slot, as soon as the MMA thread signals that the
-  // GEMM reading the buffer has completed (w?free).  The producers have slack.
-  uint64_t* wfull = bars + 2 * L::NSLOT;            // wf1[2], wf2, wf3
-  uint64_t* wfree = bars + 2 * L::NSLOT + 6;        // w1free[2], w2free, w3free
-  const int loader = (K3 == 0 && lane == 0 && q >= 1) ? q : 0;   // matrix 1, 2, 3 or none
-  const int my_tiles = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int64_t total = (int64_t)my_tiles * N;
-  const uint8_t* wsrc = static_cast<const uint8_t*>(a.wpack);
-  int64_t wnext = loader == 1 ? 2 : 1;                 // next step whose matrix this thread loads
-  auto poll_weights = [&]() {
-    if (!loader || wnext >= total) return;
-    const int64_t t = wnext;
-    uint64_t* fb;
-    uint32_t par;
-    if (loader == 1) { fb = &wfree[t & 1]; par = (uint32_t)(((t >> 1) - 1) & 1); }
-    else { fb = &wfree[loader]; par = (uint32_t)((t - 1) & 1); }
-    if (!mbar_test(fb, par)) return;
-    const uint8_t* src = wsrc + (size_t)((uint32_t)t % (uint32_t)N) * Dm::WB;
-    uint8_t* dstw;
-    uint64_t* wb;
-    uint32_t bytes;
-    if (loader == 1) { dstw = sm + L::W1 + (t & 1) * Dm::W1B; wb = &wfull[t & 1]; bytes = Dm::W1B; }
-    else if (loader == 2) { dstw = sm + L::W2; wb = &wfull[2]; bytes = Dm::W2B; src += Dm::W1B; }
-    else { dstw = sm + L::W3; wb = &wfull[3]; bytes = Dm::W3B; src += Dm::W1B + Dm::W2B; }
-    mbar_expect_tx(wb, bytes);
-    for (uint32_t off = 0; off < bytes; off += 16384u)
-      bulk_g2s(dstw + off, src + off, min(16384u, bytes - off), wb);
-    ++wnext;
-  };
-  unsigned long long* const pclk = (a.clk && blockIdx.x == 0 && q == 0 && K3 == 0 && lane == 0) ? a.clk : nullptr;
-  int64_t s = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t mg = (uint32_t)(a.m0 + (int64_t)tile * 128 + row);
-    float X[8 * (NI > 0 ? NI : 1)];
-#pragma unroll
-    for (int i = 0; i < 8 * NI; ++i) X[i] = a.x0;
-    for (int n = 0; n < N; ++n, ++s) {
-      const int slot = (int)(s % L::NSLOT);
-      const uint32_t use = (uint32_t)(s / L::NSLOT);
-      uint8_t* ximg = sm + L::SLOT0 + slot * L::SLOTB;
-      float* xn2 = reinterpret_cast<float*>(ximg + Dm::XB);
-      const uint32_t tdw = tm + lane_off + L::T_DW + (uint32_t)slot * L::DWC;
-      if (s < 64) BSDE_STAMP(pclk, s * 16 + 8);
-      if (loader) {
-        while (!mbar_try_wait_ns(&empty[slot], (use & 1) ^ 1, 200)) poll_weights();
-      } else {
-        mbar_wait(&empty[slot], (use & 1) ^ 1);
-      }
-      tc_after();
-      if (s < 64) BSDE_STAMP(pclk, s * 16 + 9);
-      const size_t img = ((size_t)n * ntiles + tile) * Dm::XB;
-      // X̃_n chunk from X, ΔW_n chunk (fp16: TMEM ring + image), then X_{n+1}
-      auto chunk_out = [&](auto ic, const float* dw) {
-        constexpr int i = decltype(ic)::value;
-        const int c = K3 + kTPath * i;
-        if (c >= NCD) return;
-        float v[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int j = 8 * c + e;
-          v[e] = j < D ? X[8 * i + e] : (j == D ? 1.0f : 0.0f);
-        }
-        uint4 xu;
-        xu.x = pack2(v[0], v[1]); xu.y = pack2(v[2], v[3]); xu.z = pack2(v[4], v[5]); xu.w = pack2(v[6], v[7]);
-        *reinterpret_cast<uint4*>(ximg + roff + c * 128) = xu;
-        const uint4 du = make_uint4(pack_h2(dw[0], dw[1]), pack_h2(dw[2], dw[3]), pack_h2(dw[4], dw[5]),
-                                    pack_h2(dw[6], dw[7]));
-#ifndef BSDE_DBG_NOTMEMDW
-        if (8 * c < D) tmem_st4(tdw + 4u * c, du);
-#endif
-#ifndef BSDE_DBG_NOSTORE
-        if (store) {
-          *reinterpret_cast<uint4*>(xst + img + roff + c * 128) = xu;
-          *reinterpret_cast<uint4*>(dst + img + roff + c * 128) = du;
-        }
-#endif
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (8 * c + e < D)   // a2: X + √2 ΔW, or X + σ X ΔW (Black-Scholes, MULT)
-            X[8 * i + e] = MULT ? fmaf(kBSSigma * dw[e], X[8 * i + e], X[8 * i + e])
-                                : fmaf(kSqrt2, dw[e], X[8 * i + e]);
-      };
-      // GRP chunks together: 2·GRP Philox streams interleaved
-#ifndef BSDE_EXP_GROUP
-#define BSDE_EXP_GROUP 2
-#endif
-      constexpr int GRP = BSDE_EXP_GROUP;
-      auto group = [&](auto ic) {
-        constexpr int i = decltype(ic)::value;
-        if constexpr (i < NI) {
-          constexpr int nch = (i + GRP <= NI) ? GRP : NI - i;
-          float dw[nch * 8];
-          gen_chunks<D, kTPath, nch, CPL>(K3 + kTPath * i, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt_f,
-                                          dw, a.cpl);
-          chunk_out(Int<i>{}, dw);
-          if constexpr (nch >= 2) chunk_out(Int<i + 1>{}, dw + 8);
-          if constexpr (nch >= 3) chunk_out(Int<i + 2>{}, dw + 16);
-        }
-        poll_weights();
-      };
-#ifndef BSDE_DBG_PRODIDLE   // (timing experiments only: producers generate nothing)
-      group(Int<0>{});
-      group(Int<GRP>{});
-      group(Int<2 * GRP>{});
-      group(Int<3 * GRP>{});
-#endif
-      if (n + 1 == N) {   // |X_N|² partial for the terminal condition
-        float sx = 0.0f;
-#pragma unroll
-        for (int i = 0; i < NI; ++i)
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (8 * (K3 + kTPath * i) + e < D) sx = fmaf(X[8 * i + e], X[8 * i + e], sx);
-        xn2[K3 * 128 + row] = sx;
-      }
-      if (s < 64) BSDE_STAMP(pclk, s * 16 + 10);
-      tmem_wait_st();
-      tc_before();
-      fence_async_smem();   // X̃_n is read by the tensor cores
-      mbar_arrive(&full[slot]);
-    }
-  }
-  while (loader && wnext < total) {   // the consumers' last steps
-    poll_weights();
-    __nanosleep(128);
-  }
-}
-
+// ---------------------------------------------------------------- control warp
 template <int D, int W>
-__device__ __forceinline__ void fwd_consumer(const PassArgs& a, int ntiles, uint8_t* sm, uint32_t tm,
-                                             int q, int lane, double& lsum, float& dy0) {
+__device__ __forceinline__ void fwd_control(const PassArgs& a, int64_t total, uint8_t* sm,
+                                            uint32_t tm, int lane) {
   using Dm = Dims<D, W>;
   using L = FwdSmem<D, W>;
-  constexpr int Dp = Dm::Dp, Wp = Dm::Wp, NCW = Wp / 8, NCD = Dp / 8, NCV = (D + 7) / 8;
-  constexpr int HW = (NCW + 1) / 2;   // E1/E2 process the accumulator in two halves of chunks
-  constexpr int HV = (NCV + 1) / 2;
+  constexpr int Dp = Dm::Dp, Wp = Dm::Wp;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::BARS);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + L::NSLOT;
-  uint64_t* wf1 = bars + 2 * L::NSLOT;
-  uint64_t* wf2 = wf1 + 2;
-  uint64_t* wf3 = wf1 + 3;
-  uint64_t* bg1 = wf1 + 4;
-  uint64_t* bg23 = wf1 + 5;
-  uint64_t* wfree = wf1 + 6;   // w1free[2], w2free, w3free (producer-side loaders)
-  const int row = 32 * q + lane;
-  const bool mma = (q == 3 && lane == 0);   // highest warp id: favoured by the scheduler
-  const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-  const uint32_t acc0 = tm + lane_off, acc1 = tm + L::T_ACC1 + lane_off;
-  auto acc = [&](int b) { return b ? acc1 : acc0; };
-  const uint32_t hT = tm + L::T_H;                       // TMEM A operand (Wp/2 columns)
+  uint64_t* bg = bars;
+  uint64_t* wb = bars + 1;
   const int N = a.N;
-  const bool store = !a.eval;
+  const bool lead = lane == 0;
   const uint8_t* wsrc = static_cast<const uint8_t*>(a.wpack);
-  const int my_tiles = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int64_t total = (int64_t)my_tiles * N;
+  auto reload = [&](int k, int64_t s) {   // weight matrix k (W̃1, W̃2, W̃3) of step s mod N
+    if (!lead) return;
+    const uint32_t bytes = k == 0 ? Dm::W1B : k == 1 ? Dm::W2B : Dm::W3B;
+    const uint32_t off = k == 0 ? L::W1 : k == 1 ? L::W2 : L::W3;
+    const uint8_t* src = wsrc + (size_t)((uint32_t)s % (uint32_t)N) * Dm::WB + off;
+    mbar_expect_tx(&wb[k], bytes);
+    for (uint32_t o = 0; o < bytes; o += 16384u)
+      bulk_g2s(sm + off + o, src + o, min(16384u, bytes - o), &wb[k]);
+  };
+  if (total <= 0) return;
+  for (int k = 0; k < 3; ++k) reload(k, 0);
   constexpr uint32_t I1 = idesc_bf16(128, Wp, false, false);
   constexpr uint32_t I3 = idesc_bf16(128, Dp, false, false);
-  (void)NCD;
-
-  auto wsrc_of = [&](int64_t s) { return wsrc + (size_t)((uint32_t)s % (uint32_t)N) * Dm::WB; };
-  auto load = [&](uint64_t* bar, uint8_t* dstp, const uint8_t* src, uint32_t bytes) {
-    mbar_expect_tx(bar, bytes);
-    for (uint32_t off = 0; off < bytes; off += 16384u)
-      bulk_g2s(dstp + off, src + off, min(16384u, bytes - off), bar);
-  };
-  auto issue_g1 = [&](int64_t s) {   // MMA thread
-    const int slot = (int)(s % L::NSLOT), b = (int)(s & 1);
-    mbar_wait(&full[slot], (uint32_t)((s / L::NSLOT) & 1));
-    mbar_wait(&wf1[b], (uint32_t)((s >> 1) & 1));
-    tc_after();
-    gemm(tm + (b ? L::T_ACC1 : 0u), kmaj(sm + L::SLOT0 + slot * L::SLOTB, Dp),
-         kmaj(sm + L::W1 + b * Dm::W1B, Dp), Dp / 16, I1, false);
-    mma_commit(bg1);
-  };
-  if (mma && total > 0) {
-    load(&wf1[0], sm + L::W1, wsrc_of(0), Dm::W1B);
-    if (total > 1) load(&wf1[1], sm + L::W1 + Dm::W1B, wsrc_of(1), Dm::W1B);
-    load(wf2, sm + L::W2, wsrc_of(0) + Dm::W1B, Dm::W2B);
-    load(wf3, sm + L::W3, wsrc_of(0) + Dm::W1B + Dm::W2B, Dm::W3B);
-    issue_g1(0);
-  }
-
-  unsigned long long* const clk = (a.clk && blockIdx.x == 0 && q == 1 && lane == 0) ? a.clk : nullptr;
-  unsigned long long* const mclk = (a.clk && blockIdx.x == 0 && mma) ? a.clk : nullptr;
-#define CLK(i) do { if (s < 64) BSDE_STAMP(clk, s * 16 + (i)); } while (0)
-  int64_t s = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t mloc = (int64_t)tile * 128 + row;
-    const bool valid = mloc < a.B_local;
-    float Y = a.params[0];
-    float P = 1.0f;   // prefix product P_{n+1} of the ā factors (per_step_abar problems)
-    float xn2 = 0.0f;
-    for (int n = 0; n < N; ++n, ++s) {
-      const int p = (int)(s & 1), slot = (int)(s % L::NSLOT);
-      uint8_t* slotp = sm + L::SLOT0 + slot * L::SLOTB;
-      CLK(0);
-      // E1: H1 = ReLU(A1) -> TMEM operand (bf16 pairs)
-      mbar_wait(bg1, (uint32_t)(s & 1));
-      CLK(1);
+  unsigned long long* const clk = (a.clk && blockIdx.x == 0 && lead) ? a.clk : nullptr;
+  for (int64_t s = 0; s < total; ++s) {
+    const uint32_t wp = (uint32_t)(s & 1);   // phase of the weight barriers for step s
+    named_sync(kBarX, kFwdThreads);          // X̃_n written; E3 of the previous step done
+    if (s < 64) BSDE_STAMP(clk, s * 16 + 12);
+    if (lead) {
+      mbar_wait(&wb[0], wp);
       tc_after();
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        constexpr int c0 = 0;
-        (void)c0;
-        float v[HW][8];
-        tmem_ld_chunks<HW>(acc(p) + 8u * (uint32_t)(h * HW), v, NCW - h * HW);
-#pragma unroll
-        for (int i = 0; i < HW; ++i) {
-          if (h * HW + i >= NCW) continue;
-          tmem_st4(hT + lane_off + 4u * (h * HW + i),
-                   make_uint4(relu_pack2(v[i][0], v[i][1]), relu_pack2(v[i][2], v[i][3]),
-                              relu_pack2(v[i][4], v[i][5]), relu_pack2(v[i][6], v[i][7])));
-        }
-      }
-      tmem_wait_st();
-      tc_before();
-      consumer_sync();
-      CLK(2);
-      if (mma) {   // G2 (A = H1 in TMEM); W̃1 buffer p is free for step s + 2
-        tc_after();
-        mbar_wait(wf2, (uint32_t)(s & 1));
-        gemm_ta(tm + (p ? 0u : L::T_ACC1), hT, kmaj(sm + L::W2, Wp), Wp / 16, I1, false);
-        mma_commit(bg23);
-        if (s + 2 < total) mbar_arrive(&wfree[p]);   // G1(s) done: W̃1 buffer p -> step s + 2
-      }
-      // E2: H2 = H1 + ReLU(A2) in bf16x2 arithmetic (R17) -> TMEM operand (over H1)
-      mbar_wait(bg23, 0);
-      CLK(3);
-      tc_after();
-      // G2 has read W̃2: reload it for the next step right away (its latency
-      // must hide behind E2, G3, E3, G1, E1)
-      if (s < 64) BSDE_STAMP(mclk, s * 16 + 12);
-      if (mma && s + 1 < total) mbar_arrive(&wfree[2]);   // G2 done: W̃2 -> step s + 1
-      if (s < 64) BSDE_STAMP(mclk, s * 16 + 13);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float v[HW][8];
-        uint32_t hw[HW][4];
-#pragma unroll
-        for (int i = 0; i < HW; ++i)
-          if (h * HW + i < NCW) tmem_ld4_nowait(hT + lane_off + 4u * (h * HW + i), hw[i]);
-        tmem_ld_chunks<HW>(acc(p ^ 1) + 8u * (uint32_t)(h * HW), v, NCW - h * HW);
-#pragma unroll
-        for (int i = 0; i < HW; ++i) {
-          if (h * HW + i >= NCW) continue;
-          reg_fence4(hw[i]);
-          tmem_st4(hT + lane_off + 4u * (h * HW + i),
-                   make_uint4(bf2_add(hw[i][0], relu_pack2(v[i][0], v[i][1])),
-                              bf2_add(hw[i][1], relu_pack2(v[i][2], v[i][3])),
-                              bf2_add(hw[i][2], relu_pack2(v[i][4], v[i][5])),
-                              bf2_add(hw[i][3], relu_pack2(v[i][6], v[i][7]))));
-        }
-      }
-      tmem_wait_st();
-      if (s < 64) BSDE_STAMP(mclk, s * 16 + 14);
-      tc_before();
-      consumer_sync();
-      CLK(4);
-      if (s < 64) BSDE_STAMP(mclk, s * 16 + 15);
-      if (mma) {   // G3 (A = H2 in TMEM); then G1 of the next step into the other accumulator
-        tc_after();
-        mbar_wait(wf3, (uint32_t)(s & 1));
-        gemm_ta(tm + (p ? L::T_ACC1 : 0u), hT, kmaj(sm + L::W3, Wp), Wp / 16, I3, false);
-        mma_commit(bg23);
-        if (s + 1 < total) issue_g1(s + 1);
-      }
-      // E3: a4 Y_{n+1} = Y_n - f(Y_n, Z_n) Δt + Z_n·ΔW_n (one thread per path)
-      mbar_wait(bg23, 1);
-      CLK(5);
-      tc_after();
-      if (mma && s + 1 < total)   // G3 has read W̃3
-        mbar_arrive(&wfree[3]);   // G3 done: W̃3 -> step s + 1
-      mbar_wait(&full[slot], (uint32_t)((s / L::NSLOT) & 1));   // ΔW_n, |X_N|² partials
-      tc_after();
-      // four partial sums per reduction: the 100-term dot products are not one
-      // serial FMA chain (4-cycle latency each) on the critical path
-      float cz4[4] = {0.f, 0.f, 0.f, 0.f}, zz4[4] = {0.f, 0.f, 0.f, 0.f}, sz4[4] = {0.f, 0.f, 0.f, 0.f};
-      const uint32_t tdw = tm + lane_off + L::T_DW + (uint32_t)slot * L::DWC;
-      // the driver's extra reduction (|Z|² for HJB, Σ Z for Black-Scholes) is a
-      // compile-time choice: one instance runs, the chain carries no predicated work
-      auto e3 = [&](auto mode_c) {
-        constexpr int MODE = decltype(mode_c)::value;   // 0 none, 1 |Z|², 2 Σ Z
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float z[HV][8];
-          uint32_t dwr[HV][4];
-#pragma unroll
-          for (int i = 0; i < HV; ++i)
-            if (h * HV + i < NCV) tmem_ld4_nowait(tdw + 4u * (h * HV + i), dwr[i]);
-          tmem_ld_chunks<HV>(acc(p) + 8u * (uint32_t)(h * HV), z, NCV - h * HV);
-#pragma unroll
-          for (int i = 0; i < HV; ++i) {
-            const int c = h * HV + i;
-            if (c >= NCV) continue;
-            reg_fence4(dwr[i]);
-            float dw[8];
-            unpack_dw(make_uint4(dwr[i][0], dwr[i][1], dwr[i][2], dwr[i][3]), dw);
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (8 * c + e < D) {
-                cz4[e & 3] = fmaf(z[i][e], dw[e], cz4[e & 3]);
-                if (MODE == 1) zz4[e & 3] = fmaf(z[i][e], z[i][e], zz4[e & 3]);
-                if (MODE == 2) sz4[e & 3] += z[i][e];
-              }
-          }
-        }
-      };
-      if (a.problem == kHJB)
-        e3(Int<1>{});
-      else if (a.problem == kBlackScholes)
-        e3(Int<2>{});
-      else
-        e3(Int<0>{});
-      const float cz = (cz4[0] + cz4[1]) + (cz4[2] + cz4[3]);
-      const float zz = (zz4[0] + zz4[1]) + (zz4[2] + zz4[3]);
-      const float sz = (sz4[0] + sz4[1]) + (sz4[2] + sz4[3]);
-      if (n + 1 == N) {
-        const float* x2 = reinterpret_cast<const float*>(slotp + Dm::XB);
-        xn2 = kTPath == 3 ? (x2[row] + x2[128 + row]) + x2[256 + row] : x2[row] + x2[128 + row];
-      }
-      if (store && per_step_abar(a.problem)) {
-        P *= 1.0f - a.dt * driver_dfdy(a.problem, Y);
-        if (valid) a.Pstore[(int64_t)n * a.B_local + mloc] = P;
-      }
-      Y = Y - driver_f(a.problem, Y, zz, sz, a.lam) * a.dt + cz;
-      tc_before();
-      consumer_sync();
-      CLK(6);
-      if (mma) mbar_arrive(&empty[slot]);   // the slot is free
+      gemm_ta(tm, tm + L::T_X, kmaj(sm + L::W1, Dp), Dp / 16, I1, false);
+      mma_commit(bg);
     }
-    // a5: R = Y_N - g(X_N); loss; ā_N (times P_N) and dY0 = ā_0 = ā_N P_N
-    if (valid) {
-      const float R = Y - terminal_g(a.problem, xn2);
-      lsum += (double)R * R;
-      if (store) {
-        a.Rstore[mloc] = R;
-        float ab = 2.0f * R * a.inv_B;
-        if (per_step_abar(a.problem)) ab *= P;
-        a.abar[mloc] = ab;
-        dy0 += ab;
-      }
+    if (s > 0) reload(2, s);                 // G3 of step s-1 has completed: W̃3 -> step s
+    __syncwarp();
+    named_sync(kBarE1, kFwdThreads);         // H1 in TMEM (so G1 has completed)
+    if (s < 64) BSDE_STAMP(clk, s * 16 + 13);
+    if (lead) {
+      mbar_wait(&wb[1], wp);
+      tc_after();
+      gemm_ta(tm, tm + L::T_H, kmaj(sm + L::W2, Wp), Wp / 16, I1, false);
+      mma_commit(bg);
     }
+    if (s + 1 < total) reload(0, s + 1);     // G1 of step s has completed: W̃1 -> step s+1
+    __syncwarp();
+    named_sync(kBarE2, kFwdThreads);         // H2 in TMEM (G2 has completed)
+    if (s < 64) BSDE_STAMP(clk, s * 16 + 14);
+    if (lead) {
+      mbar_wait(&wb[2], wp);
+      tc_after();
+      gemm_ta(tm, tm + L::T_H, kmaj(sm + L::W3, Wp), Wp / 16, I3, false);
+      mma_commit(bg);
+    }
+    if (s + 1 < total) reload(1, s + 1);     // G2 of step s has completed: W̃2 -> step s+1
+    __syncwarp();
   }
-#undef CLK
 }
 
-template <int D, int W>
+// CPL: coupled multilevel paths (a.cpl > 1); MULT: Black-Scholes multiplicative
+// noise.  Both are compile-time so that the hot instance carries neither.
+template <int D, int W, bool CPL, bool MULT>
 __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntiles) {
+  using Dm = Dims<D, W>;
   using L = FwdSmem<D, W>;
+  constexpr int Dp = Dm::Dp, Wp = Dm::Wp, NCD = Dp / 8, NCW = Wp / 8;
+  constexpr int G = kFwdGroups;
+  constexpr int NS = ((NCD > NCW ? NCD : NCW) + G - 1) / G;   // chunk slots per worker
+  constexpr int NB = 2 * NS;                                   // Philox blocks per worker
+  constexpr int S1 = NB / 3, S2 = 2 * NB / 3;                  // slices [0,S1) [S1,S2) [S2,NB)
   extern __shared__ __align__(1024) uint8_t sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::BARS);
+  uint64_t* bg = bars;          // chain GEMM commits (3 per step, in order)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L::TSLOT);
-  __shared__ double lred[4];
-  __shared__ float gred[4];
+  float* part = reinterpret_cast<float*>(sm + L::PART);
+  __shared__ double lred[kFwdWorkerWarps];
+  __shared__ float gred[kFwdWorkerWarps];
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   if (t == 0) {
-    for (int i = 0; i < L::NSLOT; ++i) mbar_init(&bars[i], kFwdProducers);   // full
-    for (int i = L::NSLOT; i < L::NBARS; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < L::NBARS; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(tslot, 512);
+  if (warp == 0) tmem_alloc(tslot, L::TCOLS);
   tc_before();
   __syncthreads();
   tc_after();
   const uint32_t tm = *tslot;
+  const int N = a.N;
+  const bool store = !a.eval;
+  const int my_tiles = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   double lsum = 0.0;
   float dy0 = 0.0f;
-  // consumers on the high warp ids: the schedulers favour them (the chain is
-  // latency-bound, the producers throughput-bound)
-  if (warp < kFwdProdWarps) {   // one instance runs: X step and path coupling are compile-time choices
-    const int q = warp & 3, k3 = warp >> 2;
-    const bool mult = a.problem == kBlackScholes;
-    if (a.cpl > 1) {
-      if (mult) fwd_producer<D, W, true, true>(a, ntiles, sm, tm, k3, q, lane);
-      else fwd_producer<D, W, false, true>(a, ntiles, sm, tm, k3, q, lane);
-    } else {
-      if (mult) fwd_producer<D, W, true, false>(a, ntiles, sm, tm, k3, q, lane);
-      else fwd_producer<D, W, false, false>(a, ntiles, sm, tm, k3, q, lane);
+
+  if (warp == kFwdWorkerWarps) {
+    fwd_control<D, W>(a, (int64_t)my_tiles * N, sm, tm, lane);
+  } else {
+    const int q = warp & 3, g = warp >> 2;
+    const int row = 32 * q + lane;
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+    const uint32_t acc = tm + lane_off, hT = tm + L::T_H + lane_off, xT = tm + L::T_X + lane_off;
+    const uint32_t it = a.eval ? a.eval_it : a.state->it;
+    uint8_t* xst = static_cast<uint8_t*>(a.xpack);
+    uint8_t* dst = static_cast<uint8_t*>(a.dwpack);
+    const uint32_t roff = (row >> 3) * (Dp * 16) + (row & 7) * 16;   // row's offset in an image
+    constexpr bool mult = MULT;
+    const bool hjb = a.problem == kHJB;
+    uint4* const dws = reinterpret_cast<uint4*>(sm + L::DWS) + t;   // this thread's ΔW_n slots
+    // slot i of this worker is column chunk c = g + 3i (warp-uniform predicates)
+    auto chunk = [&](int i) { return g + G * i; };
+    unsigned long long* const clk = (a.clk && blockIdx.x == 0 && t == 0) ? a.clk : nullptr;
+    uint32_t gph = 0;   // parity of the next chain-GEMM completion
+    int64_t s = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t mloc = (int64_t)tile * 128 + row;
+      const bool valid = mloc < a.B_local;
+      const uint32_t mg = (uint32_t)(a.m0 + mloc);
+      float X[8 * NS];
+#pragma unroll
+      for (int i = 0; i < 8 * NS; ++i) X[i] = a.x0;
+      float Y = a.params[0];   // Y and P are carried by the group-0 worker of each path
+      float P = 1.0f;          // prefix product P_{n+1} of the ā factors (per_step_abar problems)
+      // X̃_n chunk i from X (bf16, constant 1 in column D)
+      auto xchunk = [&](int i) {
+        const int c = chunk(i);
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          v[e] = col_lt3(g, i, e, D) ? X[8 * i + e] : (8 * c + e == D ? 1.0f : 0.0f);
+        return make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
+      };
+      // X̃_n -> the TMEM operand of G1 (bf16 pairs, 4 columns per chunk)
+      auto put_x = [&]() {
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+          if (chunk_lt3(g, i, NCD)) tmem_st4(xT + 4u * chunk(i), xchunk(i));
+        tmem_wait_st();
+        tc_before();
+      };
+      // Y_{n+1} (and P_{n+1}) from the E3 partial sums of step n
+      auto finish_y = [&](int n) {
+        float cz = 0.f, z2 = 0.f;
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+          cz += part[(0 * G + k) * 128 + row];
+          z2 += part[(1 * G + k) * 128 + row];
+        }
+        if (store && per_step_abar(a.problem)) {
+          P *= 1.0f - a.dt * driver_dfdy(a.problem, Y);
+          if (valid) a.Pstore[(int64_t)n * a.B_local + mloc] = P;
+        }
+        Y = Y - driver_f(a.problem, Y, z2, z2, a.lam) * a.dt + cz;
+      };
+      put_x();
+      named_arrive(kBarX, kFwdThreads);
+      // this row's 16-byte chunks in the global images of step n (advanced per step)
+      uint8_t* ximg = xst + (size_t)tile * Dm::XB + roff;
+      uint8_t* dimg = dst + (size_t)tile * Dm::XB + roff;
+      const size_t istep = (size_t)ntiles * Dm::XB;
+      for (int n = 0; n < N; ++n, ++s, ximg += istep, dimg += istep) {
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 0);
+        uint32_t dwh[2 * NB];   // ΔW_n of this worker's columns, binary16 pairs (R17), until
+                                // the chunk is complete and parked in shared memory
+        // blocks [b0, b1) of ΔW_n: a2 X_{n+1} = X_n + √2 ΔW_n (Black-Scholes:
+        // X_n + σ X_n ⊙ ΔW_n) at once, ΔW_n kept as fp16 pairs.  The global
+        // images for the adjoint are spread over the slices: X̃_n of a chunk
+        // before the slice that starts to advance it, ΔW_n of a chunk once complete.
+        auto slice = [&](auto b0c, auto b1c) {
+          constexpr int b0 = decltype(b0c)::value, nb = decltype(b1c)::value - b0;
+          if constexpr (nb > 0) {
+            if (store) {
+#pragma unroll
+              for (int i = (b0 + 1) / 2; 2 * i < b0 + nb; ++i)
+                if (chunk_lt3(g, i, NCD))
+                  *reinterpret_cast<uint4*>(ximg + chunk(i) * 128) = xchunk(i);
+            }
+            // a2 and ΔW_n bookkeeping of block b from its four increments
+            auto put_block = [&](int b, const float* z) {
+              const int i = b / 2, h = b % 2;
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (col_lt3(g, i, 4 * h + e, D)) {
+                  float& x = X[8 * i + 4 * h + e];
+                  x = mult ? fmaf(kBSSigma * z[e], x, x) : fmaf(kSqrt2, z[e], x);
+                }
+              dwh[2 * b] = pack_h2(z[0], z[1]);
+              dwh[2 * b + 1] = pack_h2(z[2], z[3]);
+              if (h == 1 && chunk_lt3(g, i, NCD)) {   // chunk complete: smem copy for E3, image
+                const uint4 u = make_uint4(dwh[4 * i], dwh[4 * i + 1], dwh[4 * i + 2], dwh[4 * i + 3]);
+                dws[i * kFwdWorkers] = u;
+                if (store) *reinterpret_cast<uint4*>(dimg + chunk(i) * 128) = u;
+              }
+            };
+            auto gen = [&](auto bc, auto& z) {   // z: float[4k], blocks bb .. bb+k-1
+              constexpr int bb = decltype(bc)::value, k = sizeof(z) / sizeof(float) / 4;
+              gen_blocks<D, bb, k, CPL>(g, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt_f, z, a.cpl);
+            };
+            // blocks valid for every column group: one interleaved group
+            constexpr int bv = blk_prefix(b0, b0 + nb, D);
+            if constexpr (bv > b0) {
+              float z[4 * (bv - b0)];
+              gen(Int<b0>{}, z);
+#pragma unroll
+              for (int j = 0; j < bv - b0; ++j) put_block(b0 + j, z + 4 * j);
+            }
+            // the rest one at a time behind a warp-uniform branch (0 where past D)
+            auto tail = [&](auto bc) {
+              constexpr int bb = decltype(bc)::value;
+              if constexpr (bb < b0 + nb) {
+                float z[4] = {0.f, 0.f, 0.f, 0.f};
+                if constexpr (!blk_none(bb, D)) {
+                  if (col_lt3(g, bb / 2, 4 * (bb % 2), D)) gen(Int<bb>{}, z);
+                }
+                put_block(bb, z);
+              }
+            };
+            tail(Int<bv>{});
+            tail(Int<bv + 1>{});
+            tail(Int<bv + 2>{});
+            tail(Int<bv + 3>{});
+            static_assert(bv + 4 >= b0 + nb, "slice tail longer than four blocks");
+          }
+        };
+        // ---- slice 1 (behind G1); E1: H1 = ReLU(A1) -> TMEM operand
+        slice(Int<0>{}, Int<S1>{});
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 1);
+        mbar_wait(bg, gph);
+        gph ^= 1;
+        tc_after();
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 2);
+#pragma unroll
+        for (int i0 = 0; i0 < NS; i0 += NS) {   // all chunks' loads in flight, one wait
+          uint32_t r[NS][8];
+#pragma unroll
+          for (int k = 0; k < NS; ++k)
+            if (i0 + k < NS && chunk_lt3(g, i0 + k, NCW)) tmem_ld8_nowait(acc + 8u * chunk(i0 + k), r[k]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < NS; ++k) {
+            if (i0 + k >= NS || !chunk_lt3(g, i0 + k, NCW)) continue;
+            reg_fence8(r[k]);
+            const float* v = reinterpret_cast<const float*>(r[k]);
+            tmem_st4(hT + 4u * chunk(i0 + k),
+                     make_uint4(relu_pack2(v[0], v[1]), relu_pack2(v[2], v[3]),
+                                relu_pack2(v[4], v[5]), relu_pack2(v[6], v[7])));
+          }
+        }
+        tmem_wait_st();
+        tc_before();
+        named_arrive(kBarE1, kFwdThreads);
+        if (g == 0 && n > 0) finish_y(n - 1);   // E3 partials of step n-1 are complete
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 3);
+        // ---- slice 2 (behind G2); E2: H2 = H1 + ReLU(A2) in bf16x2 arithmetic (R17)
+        slice(Int<S1>{}, Int<S2>{});
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 4);
+        mbar_wait(bg, gph);
+        gph ^= 1;
+        tc_after();
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 5);
+#pragma unroll
+        for (int i0 = 0; i0 < NS; i0 += 3) {   // E2 holds two registers sets: rounds of 3
+          uint32_t r[3][8], h[3][4];
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            if (i0 + k < NS && chunk_lt3(g, i0 + k, NCW)) {
+              tmem_ld8_nowait(acc + 8u * chunk(i0 + k), r[k]);
+              tmem_ld4_nowait(hT + 4u * chunk(i0 + k), h[k]);
+            }
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            if (i0 + k >= NS || !chunk_lt3(g, i0 + k, NCW)) continue;
+            reg_fence8(r[k]);
+            reg_fence4(h[k]);
+            const float* v = reinterpret_cast<const float*>(r[k]);
+            tmem_st4(hT + 4u * chunk(i0 + k),
+                     make_uint4(bf2_add(h[k][0], relu_pack2(v[0], v[1])),
+                                bf2_add(h[k][1], relu_pack2(v[2], v[3])),
+                                bf2_add(h[k][2], relu_pack2(v[4], v[5])),
+                                bf2_add(h[k][3], relu_pack2(v[6], v[7]))));
+          }
+        }
+        tmem_wait_st();
+        tc_before();
+        named_arrive(kBarE2, kFwdThreads);
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 6);
+        // ---- slice 3 (behind G3)
+        slice(Int<S2>{}, Int<NB>{});
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 7);
+        // ---- E3: partial sums of Z·ΔW (|Z|² for HJB, Σ Z for Black-Scholes) over
+        // this worker's columns, with the binary16 ΔW_n (R17)
+        mbar_wait(bg, gph);
+        gph ^= 1;
+        tc_after();
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 8);
+        {
+          float cz[2] = {0.f, 0.f}, z2[2] = {0.f, 0.f};
+#pragma unroll
+          for (int i0 = 0; i0 < NS; i0 += 3) {
+            uint32_t r[3][8];
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              if (i0 + k < NS && col_lt3(g, i0 + k, 0, D)) tmem_ld8_nowait(acc + 8u * chunk(i0 + k), r[k]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              const int i = i0 + k;
+              if (i >= NS || !col_lt3(g, i, 0, D)) continue;
+              reg_fence8(r[k]);
+              const float* zv = reinterpret_cast<const float*>(r[k]);
+              float dwv[8];
+              unpack_dw(dws[i * kFwdWorkers], dwv);
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                if (col_lt3(g, i, e, D)) {
+                  cz[e & 1] = fmaf(zv[e], dwv[e], cz[e & 1]);
+                  if (hjb) z2[e & 1] = fmaf(zv[e], zv[e], z2[e & 1]);
+                  else if (mult) z2[e & 1] += zv[e];
+                }
+            }
+          }
+          part[(0 * G + g) * 128 + row] = cz[0] + cz[1];
+          part[(1 * G + g) * 128 + row] = z2[0] + z2[1];
+        }
+        tc_before();
+        if (n + 1 < N) {
+          put_x();   // X̃_{n+1}: G1 of step n has completed, its operand columns are free
+          named_arrive(kBarX, kFwdThreads);
+        }
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 9);
+      }
+      // ---- a5 (tile tail): Y_N, R = Y_N - g(X_N), loss, ā_N (times P_N), dY0 = ā_0
+      {
+        float sx = 0.0f;   // |X_N|² partial of this worker's columns
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (col_lt3(g, i, e, D)) sx = fmaf(X[8 * i + e], X[8 * i + e], sx);
+        part[(2 * G + g) * 128 + row] = sx;
+      }
+      named_sync(kBarTail, kFwdWorkers);
+      if (g == 0) {
+        finish_y(N - 1);
+        if (valid) {
+          float xn2 = 0.0f;
+#pragma unroll
+          for (int k = 0; k < G; ++k) xn2 += part[(2 * G + k) * 128 + row];
+          const float R = Y - terminal_g(a.problem, xn2);
+          lsum += (double)R * R;
+          if (store) {
+            a.Rstore[mloc] = R;
+            float ab = 2.0f * R * a.inv_B;
+            if (per_step_abar(a.problem)) ab *= P;
+            a.abar[mloc] = ab;
+            dy0 += ab;
+          }
+        }
+      }
+      named_sync(kBarTail, kFwdWorkers);   // partials read before they are rewritten
     }
   }
-  else fwd_consumer<D, W>(a, ntiles, sm, tm, warp & 3, lane, lsum, dy0);
   double lw = lsum;
   float gw = dy0;
 #pragma unroll
@@ -539,23 +533,24 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
     lw += __shfl_xor_sync(0xffffffffu, lw, o);
     gw += __shfl_xor_sync(0xffffffffu, gw, o);
   }
-  if (warp >= kFwdProdWarps && lane == 0) { lred[warp - kFwdProdWarps] = lw; gred[warp - kFwdProdWarps] = gw; }
+  if (warp < kFwdWorkerWarps && lane == 0) { lred[warp] = lw; gred[warp] = gw; }
   tc_before();
   __syncthreads();
   if (t == 0) {
-    const double L = lred[0] + lred[1] + lred[2] + lred[3];
-    const float g0 = gred[0] + gred[1] + gred[2] + gred[3];
+    double Ls = 0.0;
+    float g0 = 0.0f;
+    for (int w = 0; w < kFwdWorkerWarps; ++w) { Ls += lred[w]; g0 += gred[w]; }
     if (a.lpart) {   // deterministic mode: per-CTA partials, summed in order by k_det_reduce
-      a.lpart[blockIdx.x] = L;
+      a.lpart[blockIdx.x] = Ls;
       a.y0part[blockIdx.x] = a.eval ? 0.0f : g0;
     } else {
-      if (L != 0.0) atomicAdd(a.loss_acc, L);
+      if (Ls != 0.0) atomicAdd(a.loss_acc, Ls);
       if (!a.eval && g0 != 0.0f) atomicAdd(a.grad, g0);
     }
   }
   if (warp == 0) {
     tc_after();
-    tmem_dealloc(tm, 512);
+    tmem_dealloc(tm, L::TCOLS);
   }
 }
 
