@@ -369,9 +369,10 @@ def main():
         if family in ("tc", "shared-tc") and wl.precision == "bf16":
             bound, peak, pk_name = "tensor", pk["bf16_tflops"], "bf16 burst (measured)"
             peak_sus = pk["bf16_tflops_sustained"]
-        elif family == "tc":
+        elif family == "tc32":
             bound, peak = "tensor", pk["bf16_tflops"] / 3.0
-            pk_name = "bf16 burst / 3 (bf16x3 fp32-accurate split: three bf16 products per product)"
+            pk_name = ("bf16 burst / 3 (bf16x3 fp32-accurate split: three bf16 MMAs per product, "
+                       "DESIGN R18b)")
             peak_sus = pk["bf16_tflops_sustained"] / 3.0
         else:
             bound, peak = "alu", 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
@@ -395,6 +396,11 @@ def main():
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16" if (family in ("tc", "shared-tc") and wl.precision == "bf16") else "f32",
+            "dtype_note": ("fp32-accurate: bf16x3 split operands (hi·hi + hi·lo + lo·hi), fp32 "
+                           "accumulation" if family == "tc32" else
+                           "bf16 GEMM operands (biases folded; H1, H2 = bf16(H1 + bf16(ReLU(A2))); "
+                           "binary16 dW copy), fp32 accumulation, X/Y/reductions/Adam fp32"
+                           if family == "tc" else "fp32"),
             "data": "synthetic (Philox4x32-10 Brownian increments generated on device, R8)",
             "config": config_dict(wl, world, family),
             "roofline": {"bound": bound, "kernel": "bsde_" + dom, "achieved": achieved,

@@ -92,6 +92,7 @@ struct bsde_ctx {
   int nais = 0;                 // per-step nets with the NAIS-Net block (NEXT-2, R25)
   int L = 0;                    // shared: number of tanh layers
   void* shbuf = nullptr;        // shared: row buffers (carved into ShArgs)
+  void* rowsbuf = nullptr;      // fp32-accurate tcgen05 family: row buffers (RowsArgs)
   bool external_ws = false;     // buffers carved from cfg.workspace (caller-owned)
   int sms = 148;                // SM count (grid sizes of the deterministic partials)
   float* dpart = nullptr;       // deterministic mode: adjoint partials
@@ -200,6 +201,39 @@ ShArgs sh_args(bsde_ctx* c) {
   return a;
 }
 
+// internal kernel family: the per-step nets at BSDE_FP32 on tcgen05 (bf16x3 row GEMMs,
+// rows_tc.cu); the public kernel enum asks for it as BSDE_KERNEL_TC with BSDE_FP32
+constexpr int kFamilyRows = 3;
+
+RowsArgs rows_args(bsde_ctx* c, int64_t B, int64_t m0) {
+  RowsArgs a{};
+  a.problem = c->problem;
+  a.d = c->d;
+  a.w = c->w;
+  a.N = c->N;
+  a.dt = (float)(c->T / c->N);
+  a.cpl = c->cfg.coupled_paths ? c->N_max / c->N : 1;
+  a.sqrt_dt_f = (float)std::sqrt(c->T / ((double)c->N * a.cpl));
+  a.lam = (float)c->cfg.lambda;
+  a.x0 = (float)c->cfg.x0;
+  a.inv_B = (float)(1.0 / (double)c->cfg.batch_global);
+  a.B = B;
+  a.m0 = m0;
+  a.k0 = (uint32_t)(c->cfg.seed & 0xffffffffu);
+  a.k1 = (uint32_t)(c->cfg.seed >> 32);
+  a.state = c->state;
+  a.loss_acc = &c->state->loss_sum;
+  a.params = c->params;
+  a.grad = c->grad;
+  a.wimg = static_cast<const uint8_t*>(c->wpack);
+  a.wimg_w = static_cast<uint8_t*>(c->wpack);
+  a.abar = c->abar;
+  a.Pstore = c->Pstore;
+  a.Rstore = c->Rstore;
+  rows_carve(a, c->rowsbuf, c->N_max);
+  return a;
+}
+
 PassArgs pass_args(bsde_ctx* c) {
   PassArgs a{};
   a.problem = c->problem;
@@ -270,6 +304,11 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
     int nl = 0;
     CK(launch_shared_step(sh_args(ctx), ctx->stream, ev ? ev[2] : nullptr, &nl));
     launches += nl;
+  } else if (ctx->family == kFamilyRows) {
+    const RowsArgs ra = rows_args(ctx, ctx->B_local, ctx->m0);
+    CK(launch_rows_forward(ra, ctx->stream, &launches));
+    mark(2);
+    CK(launch_rows_backward(ra, ctx->stream, &launches));
   } else if (ctx->family == BSDE_KERNEL_TC) {
     CK(launch_fwd_tc(a, ctx->stream));
     mark(2);
@@ -343,7 +382,8 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
     }
     // weight images for the next step (bf16 UMMA images / fp32 transposed images)
     if (!ctx->shared) {
-      if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(a, ctx->stream));
+      if (ctx->family == kFamilyRows) CK(launch_rows_pack(rows_args(ctx, ctx->B_local, ctx->m0), ctx->stream));
+      else if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(a, ctx->stream));
       else CK(launch_pack_simt(a, ctx->stream));
       launches += 1;
     }
@@ -361,7 +401,8 @@ int read_state(bsde_ctx* ctx, DeviceState* hs) {
 
 int repack(bsde_ctx* ctx) {
   if (ctx->shared) return BSDE_OK;   // the shared kernels read the fp32 master directly
-  if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(pass_args(ctx), ctx->stream));
+  if (ctx->family == kFamilyRows) CK(launch_rows_pack(rows_args(ctx, ctx->B_local, ctx->m0), ctx->stream));
+  else if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(pass_args(ctx), ctx->stream));
   else CK(launch_pack_simt(pass_args(ctx), ctx->stream));
   return BSDE_OK;
 }
@@ -375,7 +416,7 @@ void free_all(bsde_ctx* c) {
   }
   void* bufs[] = {c->params, c->grad, c->adam_m, c->adam_v, c->scratch, c->Xstore, c->Pstore,
                   c->abar, c->Rstore, c->wpack, c->xpack, c->gpart, c->state,
-                  c->eval_loss, c->shbuf, c->dpart, c->lpart, c->y0part};
+                  c->eval_loss, c->shbuf, c->dpart, c->lpart, c->y0part, c->rowsbuf};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
@@ -475,22 +516,30 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     return fail(none, BSDE_EINVAL, "the NAIS-Net block runs on the fp32 SIMT kernels only (R25)");
   int family = cfg.kernel;
   if (shared || nais) family = BSDE_KERNEL_SIMT;
+  // fp32-accurate precision on tcgen05: bf16x3 row GEMMs (R18b); the fixed-order
+  // reductions of deterministic mode exist on the SIMT kernels only
+  const bool rows_ok = !shared && !nais && rows_supported(d, w) && !cfg.deterministic;
   if (family == BSDE_KERNEL_AUTO)
-    family = (cfg.precision == BSDE_BF16 && tc_supported(d, w)) ? BSDE_KERNEL_TC : BSDE_KERNEL_SIMT;
+    family = (cfg.precision == BSDE_BF16 && tc_supported(d, w)) ? BSDE_KERNEL_TC
+             : (cfg.precision == BSDE_FP32 && rows_ok)          ? kFamilyRows
+                                                                : BSDE_KERNEL_SIMT;
+  if (family == BSDE_KERNEL_TC && cfg.precision == BSDE_FP32) {
+    if (!rows_ok)
+      return fail(none, BSDE_EINVAL,
+                  "fp32 on tcgen05 needs d+1, w+1 <= 128, the residual block and deterministic=0 "
+                  "(got d=%d w=%d); use kernel=SIMT", d, w);
+    family = kFamilyRows;
+  }
   if (family == BSDE_KERNEL_TC && !tc_supported(d, w))
     return fail(none, BSDE_EINVAL,
                 "no tcgen05 instantiation for d=%d w=%d (built: 100/110, 10/20, 37/45; d+1, w+1 <= 128)",
                 d, w);
-  if (family == BSDE_KERNEL_TC && cfg.precision != BSDE_BF16)
-    return fail(none, BSDE_EINVAL,
-                "the tcgen05 kernels compute with bf16 operands; fp32-accurate precision runs on "
-                "kernel=SIMT");
   if (family == BSDE_KERNEL_SIMT && cfg.precision == BSDE_BF16 && !shared)
     return fail(none, BSDE_EINVAL, "bf16 operands need the tcgen05 kernels (kernel=SIMT given)");
   if (family == BSDE_KERNEL_SIMT && !shared && !simt_supported(d, w))
     return fail(none, BSDE_EINVAL, "d=%d w=%d too large for the SIMT kernels (d, w <= 127 and shared "
                 "memory)", d, w);
-  if (family != BSDE_KERNEL_SIMT && family != BSDE_KERNEL_TC)
+  if (family != BSDE_KERNEL_SIMT && family != BSDE_KERNEL_TC && family != kFamilyRows)
     return fail(none, BSDE_EINVAL, "kernel=%d", cfg.kernel);
   if (cfg.nccl_id && !nccl().ok)
     return fail(none, BSDE_ENCCL, "nccl_id given (world=%d) but libnccl.so.2 could not be loaded",
@@ -538,7 +587,7 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
   const int64_t npalloc = std::max<int64_t>(npmax, shard_of(ctx, npmax) * cfg.world);   // NEXT-4 padding
   struct Alloc { void** p; size_t bytes; };
   // X_n store for the adjoint: fp32 rows (SIMT) or bf16 operand images (tcgen05)
-  const size_t xs = shared ? 16
+  const size_t xs = (shared || family == kFamilyRows) ? 16
                    : family == BSDE_KERNEL_TC ? tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)
                                               : simt_xstore_bytes(d, ctx->N_max, ctx->B_local);
   std::vector<Alloc> allocs = {
@@ -565,6 +614,9 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     allocs.push_back({(void**)&ctx->Pstore, (size_t)ctx->N_max * ctx->B_local * sizeof(float)});
   }
   if (shared) {
+  } else if (family == kFamilyRows) {
+    allocs.push_back({&ctx->wpack, rows_pack_bytes(d, w, ctx->N_max)});
+    allocs.push_back({&ctx->rowsbuf, rows_buffer_bytes(d, w, ctx->N_max, ctx->B_local)});
   } else if (family == BSDE_KERNEL_TC) {
     allocs.push_back({&ctx->wpack, tc_pack_bytes(d, w, ctx->N_max, cfg.precision)});
     allocs.push_back({&ctx->xpack, tc_xstore_bytes(d, w, ctx->N_max, ctx->B_local)});
@@ -859,6 +911,19 @@ int bsde_eval_loss(bsde_ctx* ctx, uint32_t eval_id, int64_t batch, double* loss_
       CK(launch_shared_step(sa, ctx->stream, nullptr, nullptr));
     }
   }
+  if (ctx->family == kFamilyRows) {   // the rank's eval paths in chunks of <= B_local rows per step
+    const int64_t per_rank = batch / ctx->cfg.world, first = (int64_t)ctx->cfg.rank * per_rank;
+    CK(cudaMemsetAsync(ctx->eval_loss, 0, sizeof(double), ctx->stream));
+    for (int64_t c0 = 0; c0 < per_rank; c0 += ctx->B_local) {
+      RowsArgs ra = rows_args(ctx, per_rank - c0 < ctx->B_local ? per_rank - c0 : ctx->B_local,
+                              first + c0);
+      ra.eval = 1;
+      ra.eval_it = kEvalBit | (eval_id & 0x7fffffffu);
+      ra.inv_B = (float)(1.0 / (double)batch);
+      ra.loss_acc = ctx->eval_loss;
+      CK(launch_rows_forward(ra, ctx->stream, nullptr));
+    }
+  }
   PassArgs a = pass_args(ctx);
   a.eval = 1;
   a.eval_it = kEvalBit | (eval_id & 0x7fffffffu);
@@ -866,7 +931,7 @@ int bsde_eval_loss(bsde_ctx* ctx, uint32_t eval_id, int64_t batch, double* loss_
   a.m0 = (int64_t)ctx->cfg.rank * a.B_local;
   a.inv_B = (float)(1.0 / (double)batch);
   a.loss_acc = ctx->eval_loss;
-  if (ctx->shared) {
+  if (ctx->shared || ctx->family == kFamilyRows) {
   } else if (ctx->family == BSDE_KERNEL_TC) {
     CK(cudaMemsetAsync(ctx->eval_loss, 0, sizeof(double), ctx->stream));
     CK(launch_fwd_tc(a, ctx->stream));   // an evaluation pass stores no path images
@@ -999,7 +1064,7 @@ int bsde_launches_per_step(const bsde_ctx* ctx, int* n) {
 const char* bsde_kernel_family(const bsde_ctx* ctx) {
   if (!ctx) return "none";
   if (ctx->shared) return ctx->cfg.precision == BSDE_BF16 ? "shared-tc" : "shared-simt";
-  return ctx->family == BSDE_KERNEL_TC ? "tc" : "simt";
+  return ctx->family == BSDE_KERNEL_TC ? "tc" : ctx->family == kFamilyRows ? "tc32" : "simt";
 }
 
 const char* bsde_last_error(const bsde_ctx* ctx) {

@@ -45,6 +45,34 @@ struct PassArgs {
   float sqrt_dt_f;                     // √(Δt/cpl)
 };
 
+// fp32-accurate per-step nets on tcgen05 (rows_tc.cu; DESIGN R18b): one iteration's
+// row buffers over R = N·B rows (row (n, m) = n·B + m), bf16x3 GEMM operands
+struct RowsArgs {
+  int problem, d, w, N, Dp, Wp;        // Dp = pad16(d+1), Wp = pad16(w+1)
+  float dt, sqrt_dt_f, lam, x0, inv_B;
+  int cpl;                             // coupled paths: fine steps per step
+  int64_t B, m0;                       // local paths (rows per step), first global path
+  uint32_t k0, k1;
+  int eval;
+  uint32_t eval_it;
+  DeviceState* state;
+  double* loss_acc;
+  const float* params;
+  float* grad;
+  const uint8_t* wimg;                 // per step: W̃1, W̃2, W̃3 bf16 hi images, then lo images
+  uint8_t* wimg_w;                     // the same, for the pack kernel
+  float *XT, *GW, *H1, *H2, *DH, *DA;  // X̃ [R×Dp]; ΔW then G = ΔW - Δt∂_z f [R×Dp]; H1, H2, dH2, dA1 [R×Wp]
+  float *S, *xn2;                      // per row (Z·ΔW, |Z|² | Σ Z); |X_N|² per path
+  float *abar, *Pstore, *Rstore;       // as PassArgs
+};
+bool rows_supported(int d, int w);
+size_t rows_buffer_bytes(int d, int w, int N, int64_t B);
+size_t rows_pack_bytes(int d, int w, int N);
+void rows_carve(RowsArgs& a, void* base, int N_max);
+cudaError_t launch_rows_pack(const RowsArgs& a, cudaStream_t s);
+cudaError_t launch_rows_forward(const RowsArgs& a, cudaStream_t s, int* launches);
+cudaError_t launch_rows_backward(const RowsArgs& a, cudaStream_t s, int* launches);
+
 // Shared-network formulation (shared.cu): one
 // iteration's device state.  Rows r = n·M + m, n = 0..N, row-major buffers.
 constexpr int kMaxSharedLayers = 8;

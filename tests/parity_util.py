@@ -49,7 +49,14 @@ def tensor_slices(d, w, N, nais=False):
 # fp32: accumulation order of fp32 sums; bf16: bf16 operand rounding (used only
 # against the exact oracle; against the tc emulation the operands are the same
 # and the fp32 band applies).
-KINK_BAND = {"fp32": 2e-6, "bf16": 8e-3}
+# fp32x3: the fp32-accurate tcgen05 family ("tc32", bf16x3 operands, DESIGN R18b),
+# whose products carry ~2^-16 relative error: a band ten times the fp32 one.
+KINK_BAND = {"fp32": 2e-6, "bf16": 8e-3, "fp32x3": 2e-5}
+
+
+def band_of(s, precision="fp32"):
+    """The kink band R19 for a context's kernel family."""
+    return KINK_BAND["fp32x3"] if s.family == "tc32" else KINK_BAND[precision]
 
 
 def oracle_iteration(problem, d, w, N, T, params, seed, it, paths, batch, x0=0.0, lam=1.0,
@@ -102,7 +109,7 @@ def _limit_threads():
 
 
 def compare_grads(g_gpu, g_orc, d, w, N, tol, slack=None, nais=False, max_slack_share=0.1,
-                  elem_tol=None):
+                  elem_tol=None, step0_shared_x0=False):
     """R19: per tensor ‖Δ‖₂/‖g‖₂ ≤ tol and max|Δ| ≤ tol·max|g|, where Δ is the
     GPU-oracle difference beyond the kink slack (both ReLU masks are valid for a
     pre-activation inside the rounding band).  max_slack_share bounds
@@ -110,6 +117,9 @@ def compare_grads(g_gpu, g_orc, d, w, N, tol, slack=None, nais=False, max_slack_
     only for the secondary bf16-vs-exact checks, whose bf16-wide band is
     larger than some tensors: the binding bf16 check is the tc emulation).
     elem_tol (default tol) is the elementwise bound relative to max|g|.
+    step0_shared_x0: X_0 = x0·1 with x0 != 0, so at n = 0 every path evaluates the
+    same pre-activation and a unit inside the band flips for the whole batch; the
+    slack-share cap then does not apply to the step-0 tensors (the slack still does).
     Returns the worst relative L2 error; raises AssertionError naming the tensor."""
     worst = 0.0
     elem_tol = tol if elem_tol is None else elem_tol
@@ -122,7 +132,8 @@ def compare_grads(g_gpu, g_orc, d, w, N, tol, slack=None, nais=False, max_slack_
         if nb == 0.0:
             assert np.all(diff <= 1e-30), (name, "oracle gradient is exactly 0")
             continue
-        if max_slack_share is not None and slack is not None:
+        if max_slack_share is not None and slack is not None and not (
+                step0_shared_x0 and name.endswith("_0")):
             share = np.linalg.norm(s) / nb
             assert share < max_slack_share, (name, "slack share", share)
         rel = np.linalg.norm(diff) / nb

@@ -7,7 +7,8 @@ import numpy as np
 import pytest
 
 from oracle import bsde as ob, closed_forms as cf, philox
-from parity_util import KINK_BAND, TOL, check_tc_against_emulation, compare_grads, oracle_iteration
+from parity_util import (KINK_BAND, TOL, band_of, check_tc_against_emulation, compare_grads,
+                         oracle_iteration)
 from workloads import CONFIGS
 
 pytestmark = pytest.mark.gpu
@@ -116,7 +117,7 @@ def test_full_size_cfg2_gradient_and_sampled_residuals():
     p = s.get_params()
     loss = s.compute_grad()
     ref = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, p, 0, 0, np.arange(wl.batch),
-                           wl.batch, kink_band=KINK_BAND["fp32"])
+                           wl.batch, kink_band=band_of(s))
     assert abs(loss - ref["loss"]) <= 1e-4 * ref["loss"]
     compare_grads(s.get_grads(), ref["grad"], wl.d, wl.w, wl.N, 1e-4, ref["slack"])
     idx = np.random.default_rng(3).choice(wl.batch, 64, replace=False)
@@ -150,7 +151,7 @@ def test_cfg1_trajectory():
             pk = s.get_params()
             lk = s.compute_grad()
             ref = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, pk, 0, k,
-                                   np.arange(wl.batch), wl.batch, kink_band=KINK_BAND["fp32"])
+                                   np.arange(wl.batch), wl.batch, kink_band=band_of(s))
             assert abs(lk - ref["loss"]) <= 1e-4 * ref["loss"]
             compare_grads(s.get_grads(), ref["grad"], wl.d, wl.w, wl.N, 1e-4, ref["slack"])
         losses.append(s.train_step())
