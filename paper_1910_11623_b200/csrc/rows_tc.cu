@@ -17,8 +17,9 @@
 //          G = ΔW - Δt ∂_z f (the factor of ā in dZ) in place of ΔW
 //   Y      per path: Y_{n+1} = Y_n - f Δt + Z·ΔW (Eq. 5, R2), R = Y_N - g(X_N), the loss
 //          (Eq. 6 terminal term), ā_N (times P_N), dY0
-//   B1     dH2 = dZ W̃3 with dZ = ā_{n+1} G formed while staging the operand
-//   B2     dH1 = dH2 + dA2 W̃2, dA2 = dH2 ⊙ 1[A2 > 0] staged; dA1 = dH1 ⊙ 1[A1 > 0]
+//   B1     dH2 = dZ W̃3 with dZ = ā_{n+1} G formed while staging the operand;
+//          dA2 = dH2 ⊙ 1[A2 > 0] (A2 > 0 <=> H2 > H1)
+//   B2     dH1 = dH2 + dA2 W̃2, dA1 = dH1 ⊙ 1[A1 > 0]
 //   TN     dW̃1 = Σ_m dA1ᵀ X̃, dW̃2 = Σ_m dA2ᵀ H1, dW̃3 = Σ_m dZᵀ H2 (the constant-1
 //          columns give the bias gradients), split over row ranges, fp32 atomics
 // The biases are folded into the weight images (column d of W̃1, column w of W̃2, W̃3;
@@ -50,6 +51,19 @@ __device__ __forceinline__ void split4(float4 v, uint2& hi, uint2& lo) {
 // byte offset of (r, c) (c % 4 == 0: 8 bytes) in an [R × C] operand image (tc_common.cuh)
 __device__ __forceinline__ uint32_t ioff(int r, int c, int C) {
   return (uint32_t)((r >> 3) * (C * 16) + (c >> 3) * 128 + (r & 7) * 16 + (c & 7) * 2);
+}
+
+// float4 slot e of a row-major [R × C] fp32 tile -> (row r, column c): each warp's
+// 32 slots cover 8 consecutive rows × 16 columns, so the 8-byte stores of its bf16
+// halves fill two whole 128-byte core-matrix blocks of the operand image (no bank
+// conflicts; a row-major walk puts 16 lanes on the same banks)
+template <int C>
+__device__ __forceinline__ void slot_rc(int e, int& r, int& c) {
+  constexpr int NCG = C / 16;
+  const int wi = e >> 5, l = e & 31;
+  const int rg = wi / NCG, cg = wi - rg * NCG;
+  r = 8 * rg + (l & 7);
+  c = 16 * cg + 4 * (l >> 3);
 }
 
 // ------------------------------------------------------------------ weight images
@@ -155,34 +169,51 @@ __device__ __forceinline__ float abar_of(const RowsArgs& a, int n, int64_t m) {
   return per_step_abar(a.problem) ? __fdividef(ab, a.Pstore[(int64_t)n * a.B + m]) : ab;
 }
 
-// One CTA per (row-tile group, step n): step n's weight images are loaded once, then
-// the CTA walks its 128-row tiles (tile = blockIdx.x, + gridDim.x, ...): stage the A
-// tile as bf16 hi / lo images, three MMA passes, fused epilogue out of TMEM.  Two
-// CTAs fit an SM (smem sized to the operands), so one stages while the other multiplies.
+// One CTA per SM-share of step n's row tiles (tile = blockIdx.x, + gridDim.x, ...):
+// step n's weight images are loaded once; the fp32 source tile (128 consecutive rows
+// of a [N][B][K] buffer: one contiguous block) arrives by bulk copy, is converted to
+// bf16 hi / lo images, and the next tile's copy is issued at once, so it lands while
+// this tile is multiplied (three MMA passes) and written out.  The epilogue runs in
+// two phases through shared memory: TMEM -> a padded [128 × Nc] tile (lane = row),
+// then each warp walks whole rows, four columns per lane, so every global access of
+// the fused elementwise work is a coalesced row segment.
+// Sources: F1 X̃, F2 H1, F3 H2, B1 G (scaled by ā_{n+1} while converting), B2 dA2.
 template <int OP>
-__global__ void __launch_bounds__(RT, 2) k_rows_gemm(RowsArgs a) {
+__global__ void __launch_bounds__(RT, 1) k_rows_gemm(RowsArgs a) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[3];   // weights, MMA, raw tile
   __shared__ uint32_t tslot;
-  __shared__ float sred[2][2][128];
+  __shared__ float srow[128];
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int n = blockIdx.y;
   const int Dp = a.Dp, Wp = a.Wp, d = a.d;
-  // K (A columns) and Nc (output columns); the weight image and its use
-  const int K = (OP == F1 || OP == B1) ? Dp : Wp;
+  const int K = (OP == F1 || OP == B1) ? Dp : Wp;    // A columns = source row stride
   const int Nc = (OP == F3) ? Dp : Wp;
+  const int ldt = Nc + 4;                            // padded tile row (conflict-free phase 1)
   const int mat = (OP == F1) ? 0 : (OP == F2 || OP == B2) ? 1 : 2;   // W̃1, W̃2, W̃3
   constexpr bool NN = OP == B1 || OP == B2;                           // A·W̃ (else A·W̃ᵀ)
+  const float* src = OP == F1 ? a.XT : OP == F2 ? a.H1 : OP == F3 ? a.H2 : OP == B1 ? a.GW : a.DH;
   const uint32_t WB = img_bytes(Wp, Dp) + img_bytes(Wp, Wp) + img_bytes(Dp, Wp);
   const uint32_t moff = mat == 0 ? 0u : mat == 1 ? img_bytes(Wp, Dp) : img_bytes(Wp, Dp) + img_bytes(Wp, Wp);
-  const uint32_t mbytes = img_bytes(Nc, K);
+  const uint32_t mbytes = img_bytes(Nc, K), abytes = img_bytes(128, K);
   uint8_t* whi = sm;
   uint8_t* wlo = sm + mbytes;
   uint8_t* ahi = sm + 2 * mbytes;
-  uint8_t* alo = ahi + img_bytes(128, K);
+  uint8_t* alo = ahi + abytes;
+  float* rawt = reinterpret_cast<float*>(alo + abytes);   // [128 × K]
+  float* stile = rawt + 128 * K;                           // [128 × ldt]
+  const int ntiles = (int)((a.B + 127) / 128);
+  auto prefetch = [&](int tile) {   // thread 0: rows of `tile` -> rawt
+    const int64_t i0 = (int64_t)tile * 128;
+    const uint32_t rows = (uint32_t)(a.B - i0 < 128 ? a.B - i0 : 128);
+    const uint32_t bytes = rows * K * 4u;
+    const uint8_t* g = reinterpret_cast<const uint8_t*>(src + ((size_t)n * a.B + i0) * K);
+    uint8_t* dst = reinterpret_cast<uint8_t*>(rawt);
+    mbar_expect_tx(&bars[2], bytes);
+    for (uint32_t o = 0; o < bytes; o += 16384u) bulk_g2s(dst + o, g + o, min(16384u, bytes - o), &bars[2]);
+  };
   if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(&tslot, 128);
@@ -190,72 +221,52 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm(RowsArgs a) {
   __syncthreads();
   tc_after();
   const uint32_t tm = tslot;
-  if (t == 0) {   // step n's weight images, hi and lo
-    const uint8_t* src = a.wimg + (size_t)n * 2 * WB + moff;
+  if (t == 0) {   // step n's weight images (hi, lo) and the first source tile
+    const uint8_t* wsrc = a.wimg + (size_t)n * 2 * WB + moff;
     mbar_expect_tx(&bars[0], 2 * mbytes);
     for (uint32_t o = 0; o < mbytes; o += 16384u) {
-      bulk_g2s(whi + o, src + o, min(16384u, mbytes - o), &bars[0]);
-      bulk_g2s(wlo + o, src + WB + o, min(16384u, mbytes - o), &bars[0]);
+      bulk_g2s(whi + o, wsrc + o, min(16384u, mbytes - o), &bars[0]);
+      bulk_g2s(wlo + o, wsrc + WB + o, min(16384u, mbytes - o), &bars[0]);
     }
+    if ((int)blockIdx.x < ntiles) prefetch(blockIdx.x);
   }
   const uint32_t idesc = idesc_bf16(128, Nc, false, NN);
-  const int ntiles = (int)((a.B + 127) / 128);
   const int q = warp & 3, h = warp >> 2, rr = 32 * q + lane;
   const uint32_t lb = tm + ((uint32_t)(32 * q) << 16);
-  const int cb = h * (Nc / 2), nch8 = Nc / 16;   // this warp's 8-column chunks: cb + 8j, j < nch8
+  const int cb = h * (Nc / 2), nch8 = Nc / 16;   // phase-1 columns: cb + 8j, j < nch8
   const float dt = a.dt;
-  uint32_t ph = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ph ^= 1) {
+  const float zc = -dt * driver_dfdz_coef(a.problem, a.lam), zc0 = -dt * driver_dfdz_const(a.problem);
+  int j = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++j) {
     const int64_t i0 = (int64_t)tile * 128;
-    // stage A (fp32 -> bf16 hi / lo images [128 × K]): float4 groups, coalesced per row,
-    // SU groups per thread with all their loads in flight before any conversion
+    // per-row operand scale (B1: ā_{n+1}); rows past B are zero (not copied)
+    if (t < 128) {
+      const int64_t m = i0 + t;
+      srow[t] = m < a.B ? (OP == B1 ? abar_of(a, n, m) : 1.0f) : 0.0f;
+    }
+    mbar_wait(&bars[2], (uint32_t)(j & 1));
+    __syncthreads();
     const int g4 = K / 4;
-    constexpr int SU = (OP == B2) ? 2 : 4;
-    for (int e0 = t; e0 < 128 * g4; e0 += RT * SU) {
-      float4 vv[SU];
-#pragma unroll
-      for (int u = 0; u < SU; ++u) {
-      const int e = e0 + u * RT;
+    for (int e = t; e < 128 * g4; e += RT) {
       const int r = e / g4, c = 4 * (e - r * g4);
-      const int64_t m = i0 + r;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (e < 128 * g4 && m < a.B) {
-        const size_t row = (size_t)n * a.B + m;
-        if (OP == F1) v = __ldg(reinterpret_cast<const float4*>(a.XT + row * Dp + c));
-        if (OP == F2) v = __ldg(reinterpret_cast<const float4*>(a.H1 + row * Wp + c));
-        if (OP == F3) v = __ldg(reinterpret_cast<const float4*>(a.H2 + row * Wp + c));
-        if (OP == B1) {   // dZ = ā_{n+1} G (columns >= d of G are 0)
-          const float ab = abar_of(a, n, m);
-          const float4 gv = __ldg(reinterpret_cast<const float4*>(a.GW + row * Dp + c));
-          v = make_float4(ab * gv.x, ab * gv.y, ab * gv.z, ab * gv.w);
-        }
-        if (OP == B2) {   // dA2 = dH2 ⊙ 1[A2 > 0], A2 > 0 <=> H2 > H1 (R15)
-          const float4 g = __ldg(reinterpret_cast<const float4*>(a.DH + row * Wp + c));
-          const float4 h1 = __ldg(reinterpret_cast<const float4*>(a.H1 + row * Wp + c));
-          const float4 h2 = __ldg(reinterpret_cast<const float4*>(a.H2 + row * Wp + c));
-          v = make_float4(h2.x > h1.x ? g.x : 0.f, h2.y > h1.y ? g.y : 0.f, h2.z > h1.z ? g.z : 0.f,
-                          h2.w > h1.w ? g.w : 0.f);
-        }
+      const float sc = srow[r];
+      if (sc != 0.0f) {
+        v = *reinterpret_cast<const float4*>(rawt + r * K + c);
+        v = make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w);
       }
-      vv[u] = v;
-      }
-#pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        const int e = e0 + u * RT;
-        if (e >= 128 * g4) break;
-        const int r = e / g4, c = 4 * (e - r * g4);
-        uint2 hi, lo;
-        split4(vv[u], hi, lo);
-        *reinterpret_cast<uint2*>(ahi + ioff(r, c, K)) = hi;
-        *reinterpret_cast<uint2*>(alo + ioff(r, c, K)) = lo;
-      }
+      uint2 hi, lo;
+      split4(v, hi, lo);
+      *reinterpret_cast<uint2*>(ahi + ioff(r, c, K)) = hi;
+      *reinterpret_cast<uint2*>(alo + ioff(r, c, K)) = lo;
     }
     fence_async_smem();
     tc_before();
-    __syncthreads();
+    __syncthreads();   // images complete; the source tile is consumed
     if (t == 0) {
       tc_after();
-      if (tile == (int)blockIdx.x) mbar_wait(&bars[0], 0);
+      if (tile + (int)gridDim.x < ntiles) prefetch(tile + gridDim.x);
+      if (j == 0) mbar_wait(&bars[0], 0);
       const Opnd Ah = kmaj(ahi, K), Al = kmaj(alo, K);
       const Opnd Wh = NN ? mnmaj(whi, Nc) : kmaj(whi, K), Wl = NN ? mnmaj(wlo, Nc) : kmaj(wlo, K);
       gemm(tm, Ah, Wh, K / 16, idesc, false);
@@ -263,88 +274,270 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm(RowsArgs a) {
       gemm(tm, Al, Wh, K / 16, idesc, true);
       mma_commit(&bars[1]);
     }
-    mbar_wait(&bars[1], ph);
+    mbar_wait(&bars[1], (uint32_t)(j & 1));
     tc_after();
-    // epilogue: warp (q, h) = lanes 32q.., columns [h·Nc/2, (h+1)·Nc/2), all loads in flight
-    const int64_t m = i0 + rr;
-    const bool ok = m < a.B;
-    const size_t row = (size_t)n * a.B + (ok ? m : 0);
-    float s1 = 0.f, s2 = 0.f;
-    uint32_t r8[8][8];
+    {   // phase 1: TMEM -> tile (lane = row), all loads in flight
+      uint32_t r8[8][8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < nch8) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * j), r8[j]);
-    tmem_ld_wait();
+      for (int jj = 0; jj < 8; ++jj)
+        if (jj < nch8) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
+      tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j >= nch8) break;
-      reg_fence8(r8[j]);
-      if (!ok) continue;
-      const int c0 = cb + 8 * j;
-      float v[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r8[j][e]);
-      if (OP == F1) {
-        float* dst = a.H1 + row * Wp + c0;
-        *reinterpret_cast<float4*>(dst) = make_float4(fmaxf(v[0], 0.f), fmaxf(v[1], 0.f), fmaxf(v[2], 0.f), fmaxf(v[3], 0.f));
-        *reinterpret_cast<float4*>(dst + 4) = make_float4(fmaxf(v[4], 0.f), fmaxf(v[5], 0.f), fmaxf(v[6], 0.f), fmaxf(v[7], 0.f));
+      for (int jj = 0; jj < 8; ++jj) {
+        if (jj >= nch8) break;
+        reg_fence8(r8[jj]);
+        float* dst = stile + rr * ldt + cb + 8 * jj;
+        *reinterpret_cast<uint4*>(dst) = make_uint4(r8[jj][0], r8[jj][1], r8[jj][2], r8[jj][3]);
+        *reinterpret_cast<uint4*>(dst + 4) = make_uint4(r8[jj][4], r8[jj][5], r8[jj][6], r8[jj][7]);
       }
-      if (OP == F2) {
-        const float4 p0 = *reinterpret_cast<const float4*>(a.H1 + row * Wp + c0);
-        const float4 p1 = *reinterpret_cast<const float4*>(a.H1 + row * Wp + c0 + 4);
-        float* dst = a.H2 + row * Wp + c0;
-        *reinterpret_cast<float4*>(dst) = make_float4(p0.x + fmaxf(v[0], 0.f), p0.y + fmaxf(v[1], 0.f),
-                                                      p0.z + fmaxf(v[2], 0.f), p0.w + fmaxf(v[3], 0.f));
-        *reinterpret_cast<float4*>(dst + 4) = make_float4(p1.x + fmaxf(v[4], 0.f), p1.y + fmaxf(v[5], 0.f),
-                                                          p1.z + fmaxf(v[6], 0.f), p1.w + fmaxf(v[7], 0.f));
-      }
-      if (OP == F3) {   // Z·ΔW, |Z|² | Σ Z; G = ΔW - Δt ∂_z f in place (R2)
-        float* gp = a.GW + row * Dp + c0;
-        float g[8];
-        *reinterpret_cast<float4*>(g) = *reinterpret_cast<const float4*>(gp);
-        *reinterpret_cast<float4*>(g + 4) = *reinterpret_cast<const float4*>(gp + 4);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          if (c0 + e >= d) { g[e] = 0.f; continue; }
-          s1 = fmaf(v[e], g[e], s1);
-          if (a.problem == kHJB) s2 = fmaf(v[e], v[e], s2);
-          else if (a.problem == kBlackScholes) s2 += v[e];
-          // ∂_z f = -λ z (HJB), r/σ (Black-Scholes), 0 (heat, Allen-Cahn)
-          g[e] = fmaf(-dt, driver_dfdz_coef(a.problem, a.lam) * v[e] + driver_dfdz_const(a.problem), g[e]);
-        }
-        if (!a.eval) {
-          *reinterpret_cast<float4*>(gp) = *reinterpret_cast<const float4*>(g);
-          *reinterpret_cast<float4*>(gp + 4) = *reinterpret_cast<const float4*>(g + 4);
-        }
-      }
-      if (OP == B1) {
-        float* dst = a.DH + row * Wp + c0;
-        *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-        *reinterpret_cast<float4*>(dst + 4) = make_float4(v[4], v[5], v[6], v[7]);
-      }
-      if (OP == B2) {   // dH1 = dH2 + dA2 W̃2; dA1 = dH1 ⊙ 1[A1 > 0] = 1[H1 > 0]
-        float dh[8], h1[8];
-        *reinterpret_cast<float4*>(dh) = *reinterpret_cast<const float4*>(a.DH + row * Wp + c0);
-        *reinterpret_cast<float4*>(dh + 4) = *reinterpret_cast<const float4*>(a.DH + row * Wp + c0 + 4);
-        *reinterpret_cast<float4*>(h1) = *reinterpret_cast<const float4*>(a.H1 + row * Wp + c0);
-        *reinterpret_cast<float4*>(h1 + 4) = *reinterpret_cast<const float4*>(a.H1 + row * Wp + c0 + 4);
-        float o[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = h1[e] > 0.f ? dh[e] + v[e] : 0.f;
-        *reinterpret_cast<float4*>(a.DA + row * Wp + c0) = *reinterpret_cast<const float4*>(o);
-        *reinterpret_cast<float4*>(a.DA + row * Wp + c0 + 4) = *reinterpret_cast<const float4*>(o + 4);
-      }
-    }
-    if (OP == F3) {   // the two column halves of a row
-      sred[0][h][rr] = s1;
-      sred[1][h][rr] = s2;
     }
     tc_before();
-    __syncthreads();   // TMEM read and the A images consumed: the next tile may overwrite them
-    if (OP == F3 && h == 0 && ok)
-      *reinterpret_cast<float2*>(a.S + row * 2) = make_float2(sred[0][0][rr] + sred[0][1][rr],
-                                                             sred[1][0][rr] + sred[1][1][rr]);
-    if (OP == F3) __syncthreads();   // sred read before the next tile writes it
+    __syncthreads();   // the tile is complete; the accumulator may be overwritten
+    // phase 2: warp w, rows w, w+8, ...; lane = columns 4·lane .. +3
+    const int c4 = 4 * lane;
+    const bool lane_on = c4 < Nc;
+    for (int r = warp; r < 128; r += RT / 32) {
+      const int64_t m = i0 + r;
+      if (m >= a.B) break;
+      const size_t row = (size_t)n * a.B + m;
+      float4 v = lane_on ? *reinterpret_cast<const float4*>(stile + r * ldt + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (OP == F1 && lane_on)
+        *reinterpret_cast<float4*>(a.H1 + row * Wp + c4) =
+            make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+      if (OP == F2 && lane_on) {   // H2 = H1 + ReLU(A2)
+        const float4 p = __ldg(reinterpret_cast<const float4*>(a.H1 + row * Wp + c4));
+        *reinterpret_cast<float4*>(a.H2 + row * Wp + c4) =
+            make_float4(p.x + fmaxf(v.x, 0.f), p.y + fmaxf(v.y, 0.f), p.z + fmaxf(v.z, 0.f),
+                        p.w + fmaxf(v.w, 0.f));
+      }
+      if (OP == F3) {   // Z·ΔW, |Z|² | Σ Z; G = ΔW - Δt ∂_z f in place (R2)
+        float s1 = 0.f, s2 = 0.f;
+        if (lane_on) {
+          float* gp = a.GW + row * Dp + c4;
+          const float4 gv = *reinterpret_cast<const float4*>(gp);
+          const float z[4] = {v.x, v.y, v.z, v.w};
+          float g[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (c4 + e >= d) { g[e] = 0.f; continue; }
+            s1 = fmaf(z[e], g[e], s1);
+            if (a.problem == kHJB) s2 = fmaf(z[e], z[e], s2);
+            else if (a.problem == kBlackScholes) s2 += z[e];
+            // ∂_z f = -λ z (HJB), r/σ (Black-Scholes), 0 (heat, Allen-Cahn)
+            g[e] = fmaf(zc, z[e], g[e] + zc0);
+          }
+          if (!a.eval) *reinterpret_cast<float4*>(gp) = make_float4(g[0], g[1], g[2], g[3]);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        if (lane == 0) *reinterpret_cast<float2*>(a.S + row * 2) = make_float2(s1, s2);
+      }
+      if (OP == B1 && lane_on) {   // dH2 -> DA; dA2 = dH2 ⊙ 1[A2 > 0] (A2 > 0 <=> H2 > H1, R15) -> DH
+        const float4 h1 = __ldg(reinterpret_cast<const float4*>(a.H1 + row * Wp + c4));
+        const float4 h2 = __ldg(reinterpret_cast<const float4*>(a.H2 + row * Wp + c4));
+        *reinterpret_cast<float4*>(a.DA + row * Wp + c4) = v;
+        *reinterpret_cast<float4*>(a.DH + row * Wp + c4) =
+            make_float4(h2.x > h1.x ? v.x : 0.f, h2.y > h1.y ? v.y : 0.f, h2.z > h1.z ? v.z : 0.f,
+                        h2.w > h1.w ? v.w : 0.f);
+      }
+      if (OP == B2 && lane_on) {   // dH1 = dH2 + dA2 W̃2; dA1 = dH1 ⊙ 1[H1 > 0] -> DA (over dH2)
+        const float4 dh = *reinterpret_cast<const float4*>(a.DA + row * Wp + c4);
+        const float4 h1 = __ldg(reinterpret_cast<const float4*>(a.H1 + row * Wp + c4));
+        *reinterpret_cast<float4*>(a.DA + row * Wp + c4) =
+            make_float4(h1.x > 0.f ? dh.x + v.x : 0.f, h1.y > 0.f ? dh.y + v.y : 0.f,
+                        h1.z > 0.f ? dh.z + v.z : 0.f, h1.w > 0.f ? dh.w + v.w : 0.f);
+      }
+    }
+    __syncthreads();   // the tile is read: the next tile's phase 1 may overwrite it
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_after();
+    tmem_dealloc(tm, 128);
+  }
+}
+
+// The same row GEMMs with compile-time operand shapes (the built dims): one CTA per
+// (128-row tile, step n), two CTAs per SM, so one CTA's loads overlap the other's MMAs
+// and epilogue.  A is loaded from global with all of a thread's float4 loads in
+// flight, converted to bf16 hi / lo in shared memory; the epilogue goes through a
+// padded half tile that reuses the A images (free once the MMAs completed), then whole
+// rows per warp (coalesced).
+template <int OP, int DP, int WP>
+__global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
+  constexpr int K = (OP == F1 || OP == B1) ? DP : WP, NC = (OP == F3) ? DP : WP;
+  constexpr int G4 = K / 4, U = (128 * G4 + RT - 1) / RT, LDT = NC + 4, NCH8 = NC / 16;
+  constexpr uint32_t MB = (uint32_t)NC * K * 2, AB = 128u * K * 2;
+  // the half tile reuses the A images when it fits them (the built large shapes), else
+  // it has its own region after them (small shapes)
+  constexpr bool ALIAS = 64 * LDT * 4 <= 2 * AB;
+  constexpr int mat = (OP == F1) ? 0 : (OP == F2 || OP == B2) ? 1 : 2;
+  constexpr bool NN = OP == B1 || OP == B2;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ uint32_t tslot;
+  __shared__ float srow[128];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int n = blockIdx.y;
+  const int64_t i0 = (int64_t)blockIdx.x * 128;
+  const int d = a.d;
+  const float* src = OP == F1 ? a.XT : OP == F2 ? a.H1 : OP == F3 ? a.H2 : OP == B1 ? a.GW : a.DH;
+  constexpr uint32_t WB = 2u * (WP * DP + WP * WP + DP * WP);
+  constexpr uint32_t moff = mat == 0 ? 0u : mat == 1 ? 2u * WP * DP : 2u * (WP * DP + WP * WP);
+  uint8_t* whi = sm;
+  uint8_t* wlo = sm + MB;
+  uint8_t* ahi = sm + 2 * MB;
+  uint8_t* alo = ahi + AB;
+  float* stile = reinterpret_cast<float*>(ALIAS ? ahi : alo + AB);
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tslot, 128);
+  if (t < 128) {
+    const int64_t m = i0 + t;
+    srow[t] = m < a.B ? (OP == B1 ? abar_of(a, n, m) : 1.0f) : 0.0f;
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tm = tslot;
+  if (t == 0) {
+    const uint8_t* wsrc = a.wimg + (size_t)n * 2 * WB + moff;
+    mbar_expect_tx(&bars[0], 2 * MB);
+    for (uint32_t o = 0; o < MB; o += 16384u) {
+      bulk_g2s(whi + o, wsrc + o, min(16384u, MB - o), &bars[0]);
+      bulk_g2s(wlo + o, wsrc + WB + o, min(16384u, MB - o), &bars[0]);
+    }
+  }
+  // stage A: all U float4 loads in flight, then split / store
+  {
+    const float* base = src + ((size_t)n * a.B + i0) * K;
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = t + u * RT;
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      int r, c;
+      slot_rc<K>(e, r, c);
+      if (e < 128 * G4 && srow[r] != 0.0f) v[u] = __ldg(reinterpret_cast<const float4*>(base + r * K + c));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = t + u * RT;
+      if (e >= 128 * G4) break;
+      int r, c;
+      slot_rc<K>(e, r, c);
+      const float sc = srow[r];
+      uint2 hi, lo;
+      split4(make_float4(sc * v[u].x, sc * v[u].y, sc * v[u].z, sc * v[u].w), hi, lo);
+      *reinterpret_cast<uint2*>(ahi + ioff(r, c, K)) = hi;
+      *reinterpret_cast<uint2*>(alo + ioff(r, c, K)) = lo;
+    }
+  }
+  fence_async_smem();
+  tc_before();
+  __syncthreads();
+  if (t == 0) {
+    tc_after();
+    mbar_wait(&bars[0], 0);
+    constexpr uint32_t idesc = idesc_bf16(128, NC, false, NN);
+    const Opnd Ah = kmaj(ahi, K), Al = kmaj(alo, K);
+    const Opnd Wh = NN ? mnmaj(whi, NC) : kmaj(whi, K), Wl = NN ? mnmaj(wlo, NC) : kmaj(wlo, K);
+    gemm(tm, Ah, Wh, K / 16, idesc, false);
+    gemm(tm, Ah, Wl, K / 16, idesc, true);
+    gemm(tm, Al, Wh, K / 16, idesc, true);
+    mma_commit(&bars[1]);
+  }
+  mbar_wait(&bars[1], 0);
+  tc_after();
+  const int q = warp & 3, h = warp >> 2;
+  const uint32_t lb = tm + ((uint32_t)(32 * q) << 16);
+  const int cb = h * (NC / 2);
+  const float dt = a.dt;
+  const float zc = -dt * driver_dfdz_coef(a.problem, a.lam), zc0 = -dt * driver_dfdz_const(a.problem);
+  const int c4 = 4 * lane;
+  const bool lane_on = c4 < NC;
+#pragma unroll 1
+  for (int hf = 0; hf < 2; ++hf) {
+    if ((q >> 1) == hf) {   // phase 1: this half's lane quadrants -> tile rows 0..63
+      uint32_t r8[NCH8][8];
+#pragma unroll
+      for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
+      tmem_ld_wait();
+      const int rl = 32 * (q & 1) + lane;
+#pragma unroll
+      for (int jj = 0; jj < NCH8; ++jj) {
+        reg_fence8(r8[jj]);
+        float* dstp = stile + rl * LDT + cb + 8 * jj;
+        *reinterpret_cast<uint4*>(dstp) = make_uint4(r8[jj][0], r8[jj][1], r8[jj][2], r8[jj][3]);
+        *reinterpret_cast<uint4*>(dstp + 4) = make_uint4(r8[jj][4], r8[jj][5], r8[jj][6], r8[jj][7]);
+      }
+    }
+    __syncthreads();
+    // phase 2: warp w, half-tile rows w, w+8, ...; lane = columns 4·lane .. +3
+#pragma unroll 1
+    for (int r = warp; r < 64; r += RT / 32) {
+      const int64_t m = i0 + 64 * hf + r;
+      if (m >= a.B) break;
+      const size_t row = (size_t)n * a.B + m;
+      const float4 v = lane_on ? *reinterpret_cast<const float4*>(stile + r * LDT + c4)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (OP == F1 && lane_on)
+        *reinterpret_cast<float4*>(a.H1 + row * WP + c4) =
+            make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+      if (OP == F2 && lane_on) {   // H2 = H1 + ReLU(A2)
+        const float4 p = __ldg(reinterpret_cast<const float4*>(a.H1 + row * WP + c4));
+        *reinterpret_cast<float4*>(a.H2 + row * WP + c4) =
+            make_float4(p.x + fmaxf(v.x, 0.f), p.y + fmaxf(v.y, 0.f), p.z + fmaxf(v.z, 0.f),
+                        p.w + fmaxf(v.w, 0.f));
+      }
+      if (OP == F3) {   // Z·ΔW, |Z|² | Σ Z; G = ΔW - Δt ∂_z f in place (R2)
+        float s1 = 0.f, s2 = 0.f;
+        if (lane_on) {
+          float* gp = a.GW + row * DP + c4;
+          const float4 gv = *reinterpret_cast<const float4*>(gp);
+          const float z[4] = {v.x, v.y, v.z, v.w};
+          float g[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (c4 + e >= d) { g[e] = 0.f; continue; }
+            s1 = fmaf(z[e], g[e], s1);
+            if (a.problem == kHJB) s2 = fmaf(z[e], z[e], s2);
+            else if (a.problem == kBlackScholes) s2 += z[e];
+            g[e] = fmaf(zc, z[e], g[e] + zc0);   // ∂_z f = -λ z (HJB), r/σ (Black-Scholes)
+          }
+          if (!a.eval) *reinterpret_cast<float4*>(gp) = make_float4(g[0], g[1], g[2], g[3]);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        if (lane == 0) *reinterpret_cast<float2*>(a.S + row * 2) = make_float2(s1, s2);
+      }
+      if (OP == B1 && lane_on) {   // dH2 -> DA; dA2 = dH2 ⊙ 1[A2 > 0] (H2 > H1, R15) -> DH
+        const float4 h1 = __ldg(reinterpret_cast<const float4*>(a.H1 + row * WP + c4));
+        const float4 h2 = __ldg(reinterpret_cast<const float4*>(a.H2 + row * WP + c4));
+        *reinterpret_cast<float4*>(a.DA + row * WP + c4) = v;
+        *reinterpret_cast<float4*>(a.DH + row * WP + c4) =
+            make_float4(h2.x > h1.x ? v.x : 0.f, h2.y > h1.y ? v.y : 0.f, h2.z > h1.z ? v.z : 0.f,
+                        h2.w > h1.w ? v.w : 0.f);
+      }
+      if (OP == B2 && lane_on) {   // dH1 = dH2 + dA2 W̃2; dA1 = dH1 ⊙ 1[H1 > 0] -> DA
+        const float4 dh = *reinterpret_cast<const float4*>(a.DA + row * WP + c4);
+        const float4 h1 = __ldg(reinterpret_cast<const float4*>(a.H1 + row * WP + c4));
+        *reinterpret_cast<float4*>(a.DA + row * WP + c4) =
+            make_float4(h1.x > 0.f ? dh.x + v.x : 0.f, h1.y > 0.f ? dh.y + v.y : 0.f,
+                        h1.z > 0.f ? dh.z + v.z : 0.f, h1.w > 0.f ? dh.w + v.w : 0.f);
+      }
+    }
+    __syncthreads();
   }
   tc_before();
   __syncthreads();
@@ -400,129 +593,110 @@ __global__ void __launch_bounds__(256) k_rows_y(RowsArgs a) {
 
 // ------------------------------------------------------------------ weight gradients
 // blockIdx.y = which: 0 dW̃1 = Σ dA1ᵀ X̃, 1 dW̃2 = Σ dA2ᵀ H1, 2 dW̃3 = Σ dZᵀ H2 over the rows
-// [r0, r1) of step n = blockIdx.z; M = 128 (output rows p < P), N = Q, K = 32 rows a chunk
-constexpr int TK = 32;
-__global__ void __launch_bounds__(RT) k_rows_tn(RowsArgs a, int rows_per_cta) {
+// [r0, r1) of step n = blockIdx.z; M = 128 (output rows p < P), N = Q, K = TK rows a
+// chunk.  Both fp32 sources are contiguous per chunk ([N][B][cols] buffers): bulk copies
+// two chunks ahead, converted to MN-major bf16 hi / lo images, three MMA passes.
+constexpr int TK = 64;
+__global__ void __launch_bounds__(RT, 1) k_rows_tn(RowsArgs a, int rows_per_cta) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[3];   // MMA, raw[0], raw[1]
   __shared__ uint32_t tslot;
+  __shared__ float srow[TK];
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int which = blockIdx.y, n = blockIdx.z;
   const int Dp = a.Dp, Wp = a.Wp, d = a.d, w = a.w;
-  const int P = which == 2 ? Dp : Wp, Q = which == 0 ? Dp : Wp;
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta, r1 = (a.B < r0 + rows_per_cta ? a.B : r0 + rows_per_cta);
-  // per buffer: A hi, A lo [TK × 128], B hi, B lo [TK × Q]
-  const uint32_t AB = img_bytes(TK, 128), BB = img_bytes(TK, Q), BUF = 2 * AB + 2 * BB;
+  const int P = which == 2 ? Dp : Wp, Q = which == 0 ? Dp : Wp;   // source row strides
+  const float* srcA = which == 0 ? a.DA : which == 1 ? a.DH : a.GW;
+  const float* srcB = which == 0 ? a.XT : which == 1 ? a.H1 : a.H2;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = (a.B < r0 + rows_per_cta ? a.B : r0 + rows_per_cta);
+  const uint32_t AB = img_bytes(TK, 128), BB = img_bytes(TK, Q);
+  uint8_t* aimg = sm;                          // A hi, A lo [TK × 128]
+  uint8_t* bimg = sm + 2 * AB;                 // B hi, B lo [TK × Q]
+  float* rawA0 = reinterpret_cast<float*>(bimg + 2 * img_bytes(TK, 128));
+  float* rawB0 = rawA0 + 2 * TK * 128;
+  auto rawA = [&](int b) { return rawA0 + (size_t)b * TK * 128; };
+  auto rawB = [&](int b) { return rawB0 + (size_t)b * TK * 128; };
+  const int nch = r0 < r1 ? (int)((r1 - r0 + TK - 1) / TK) : 0;
+  auto prefetch = [&](int c, int b) {
+    const int64_t rb = r0 + (int64_t)c * TK;
+    const uint32_t rows = (uint32_t)(r1 - rb < TK ? r1 - rb : TK);
+    const uint32_t ba = rows * P * 4u, bb = rows * Q * 4u;
+    const uint8_t* ga = reinterpret_cast<const uint8_t*>(srcA + ((size_t)n * a.B + rb) * P);
+    const uint8_t* gb = reinterpret_cast<const uint8_t*>(srcB + ((size_t)n * a.B + rb) * Q);
+    uint8_t* da = reinterpret_cast<uint8_t*>(rawA(b));
+    uint8_t* db = reinterpret_cast<uint8_t*>(rawB(b));
+    mbar_expect_tx(&bars[1 + b], ba + bb);
+    for (uint32_t o = 0; o < ba; o += 16384u) bulk_g2s(da + o, ga + o, min(16384u, ba - o), &bars[1 + b]);
+    for (uint32_t o = 0; o < bb; o += 16384u) bulk_g2s(db + o, gb + o, min(16384u, bb - o), &bars[1 + b]);
+  };
   if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
+  // A image columns >= P stay 0 (M = 128 rows of the MMA)
+  for (int e = t; e < (int)(2 * AB / 16); e += RT) reinterpret_cast<uint4*>(aimg)[e] = make_uint4(0, 0, 0, 0);
   if (warp == 0) tmem_alloc(&tslot, 128);
   tc_before();
   __syncthreads();
   tc_after();
   const uint32_t tm = tslot;
-  const int nch = r0 < r1 ? (int)((r1 - r0 + TK - 1) / TK) : 0;
-  auto convert = [&](int c, int b) {
-    uint8_t* base = sm + b * BUF;
-    const int64_t rb = r0 + (int64_t)c * TK;
-    // A: [TK rows × 128 cols] (columns >= P zero); all of a thread's loads in flight first
-    constexpr int UA = TK * 32 / RT;
-    float4 va[UA];
-#pragma unroll
-    for (int u = 0; u < UA; ++u) {
-      const int e = t + u * RT;
-      const int rl = e >> 5, c4 = 4 * (e & 31);
-      const int64_t m = rb + rl;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (m < r1 && c4 < P) {
-        const size_t row = (size_t)n * a.B + m;
-        if (which == 0) v = __ldg(reinterpret_cast<const float4*>(a.DA + row * Wp + c4));
-        if (which == 1) {
-          const float4 g = __ldg(reinterpret_cast<const float4*>(a.DH + row * Wp + c4));
-          const float4 h1 = __ldg(reinterpret_cast<const float4*>(a.H1 + row * Wp + c4));
-          const float4 h2 = __ldg(reinterpret_cast<const float4*>(a.H2 + row * Wp + c4));
-          v = make_float4(h2.x > h1.x ? g.x : 0.f, h2.y > h1.y ? g.y : 0.f, h2.z > h1.z ? g.z : 0.f,
-                          h2.w > h1.w ? g.w : 0.f);
-        }
-        if (which == 2) {
-          const float ab = abar_of(a, n, m);
-          const float4 gv = __ldg(reinterpret_cast<const float4*>(a.GW + row * Dp + c4));
-          v = make_float4(ab * gv.x, ab * gv.y, ab * gv.z, ab * gv.w);
-        }
-      }
-      va[u] = v;
-    }
-    // B loads of the chunk, then all conversions
-    const int q4 = Q / 4;
-    constexpr int UB = (TK * 32 + RT - 1) / RT;   // Q <= 128: at most TK·32 groups
-    float4 vb[UB];
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int e = t + u * RT;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (e < TK * q4) {
-        const int rl = e / q4, c4 = 4 * (e - rl * q4);
-        const int64_t m = rb + rl;
-        if (m < r1) {
-          const size_t row = (size_t)n * a.B + m;
-          if (which == 0) v = __ldg(reinterpret_cast<const float4*>(a.XT + row * Dp + c4));
-          if (which == 1) v = __ldg(reinterpret_cast<const float4*>(a.H1 + row * Wp + c4));
-          if (which == 2) v = __ldg(reinterpret_cast<const float4*>(a.H2 + row * Wp + c4));
-        }
-      }
-      vb[u] = v;
-    }
-#pragma unroll
-    for (int u = 0; u < UA; ++u) {
-      const int e = t + u * RT;
-      const int rl = e >> 5, c4 = 4 * (e & 31);
-      uint2 hi, lo;
-      split4(va[u], hi, lo);
-      *reinterpret_cast<uint2*>(base + ioff(rl, c4, 128)) = hi;
-      *reinterpret_cast<uint2*>(base + AB + ioff(rl, c4, 128)) = lo;
-    }
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int e = t + u * RT;
-      if (e >= TK * q4) break;
-      const int rl = e / q4, c4 = 4 * (e - rl * q4);
-      uint2 hi, lo;
-      split4(vb[u], hi, lo);
-      *reinterpret_cast<uint2*>(base + 2 * AB + ioff(rl, c4, Q)) = hi;
-      *reinterpret_cast<uint2*>(base + 2 * AB + BB + ioff(rl, c4, Q)) = lo;
-    }
-  };
-  const uint32_t idesc = idesc_bf16(128, Q, true, true);
-  if (nch > 0) {
-    convert(0, 0);
-    fence_async_smem();
+  if (t == 0) {
+    if (nch > 0) prefetch(0, 0);
+    if (nch > 1) prefetch(1, 1);
   }
-  tc_before();
-  __syncthreads();
+  const uint32_t idesc = idesc_bf16(128, Q, true, true);
   for (int c = 0; c < nch; ++c) {
     const int b = c & 1;
+    const int64_t rb = r0 + (int64_t)c * TK;
+    if (t < TK) {   // per-row scale of A: ā_{n+1} for dZ (which 2), 0 past the range
+      const int64_t m = rb + t;
+      srow[t] = m < r1 ? (which == 2 ? abar_of(a, n, m) : 1.0f) : 0.0f;
+    }
+    mbar_wait(&bars[1 + b], (uint32_t)((c >> 1) & 1));
+    if (c > 0) mbar_wait(&bars[0], (uint32_t)((c - 1) & 1));   // MMA c-1 has read the images
+    __syncthreads();
+    const float* ra = rawA(b);
+    const float* rbuf = rawB(b);
+    const int pa = P / 4, qb = Q / 4;
+    for (int e = t; e < TK * pa; e += RT) {
+      const int rl = e / pa, c4 = 4 * (e - rl * pa);
+      const float sc = srow[rl];
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (sc != 0.0f) {
+        v = *reinterpret_cast<const float4*>(ra + rl * P + c4);
+        v = make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w);
+      }
+      uint2 hi, lo;
+      split4(v, hi, lo);
+      *reinterpret_cast<uint2*>(aimg + ioff(rl, c4, 128)) = hi;
+      *reinterpret_cast<uint2*>(aimg + AB + ioff(rl, c4, 128)) = lo;
+    }
+    for (int e = t; e < TK * qb; e += RT) {
+      const int rl = e / qb, c4 = 4 * (e - rl * qb);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (rb + rl < r1) v = *reinterpret_cast<const float4*>(rbuf + rl * Q + c4);
+      uint2 hi, lo;
+      split4(v, hi, lo);
+      *reinterpret_cast<uint2*>(bimg + ioff(rl, c4, Q)) = hi;
+      *reinterpret_cast<uint2*>(bimg + BB + ioff(rl, c4, Q)) = lo;
+    }
+    fence_async_smem();
+    tc_before();
+    __syncthreads();
     if (t == 0) {
       tc_after();
-      uint8_t* base = sm + b * BUF;
-      const Opnd Ah = mnmaj(base, 128), Al = mnmaj(base + AB, 128);
-      const Opnd Bh = mnmaj(base + 2 * AB, Q), Bl = mnmaj(base + 2 * AB + BB, Q);
+      if (c + 2 < nch) prefetch(c + 2, b);   // raw[b] consumed
+      const Opnd Ah = mnmaj(aimg, 128), Al = mnmaj(aimg + AB, 128);
+      const Opnd Bh = mnmaj(bimg, Q), Bl = mnmaj(bimg + BB, Q);
       gemm(tm, Ah, Bh, TK / 16, idesc, c > 0);
       gemm(tm, Ah, Bl, TK / 16, idesc, true);
       gemm(tm, Al, Bh, TK / 16, idesc, true);
-      mma_commit(&bars[b]);
+      mma_commit(&bars[0]);
     }
-    if (c + 1 < nch) {
-      if (c >= 1) mbar_wait(&bars[b ^ 1], (uint32_t)(((c - 1) >> 1) & 1));   // chunk c-1 read it
-      convert(c + 1, b ^ 1);
-      fence_async_smem();
-    }
-    tc_before();
-    __syncthreads();
   }
   if (nch > 0) {
-    mbar_wait(&bars[(nch - 1) & 1], (uint32_t)(((nch - 1) >> 1) & 1));
+    mbar_wait(&bars[0], (uint32_t)((nch - 1) & 1));
     tc_after();
     // accumulator lane p = output row, columns q: the flat gradient of step n
     const NetDims nd{d, w};
@@ -555,6 +729,159 @@ __global__ void __launch_bounds__(RT) k_rows_tn(RowsArgs a, int rows_per_cta) {
   }
 }
 
+// Weight gradients with compile-time shapes: blockIdx.y = which (as k_rows_tn), two
+// or three CTAs per SM; a chunk's fp32 rows are loaded with all of a thread's loads in
+// flight while the previous chunk's MMAs run, then converted into the (single) image
+// buffer once those MMAs have read it.
+template <int WHICH, int DP, int WP>
+__device__ __forceinline__ void rows_tn_body(const RowsArgs& a, int n, int64_t r0, int64_t r1,
+                                             uint8_t* sm, uint64_t* bar, uint32_t tm, float* srow) {
+  constexpr int P = WHICH == 2 ? DP : WP, Q = WHICH == 0 ? DP : WP;
+  constexpr int PA = P / 4, QB = Q / 4;
+  constexpr int UA = (TK * PA + RT - 1) / RT, UB = (TK * QB + RT - 1) / RT;
+  constexpr uint32_t AB = (uint32_t)TK * 128 * 2, BB = (uint32_t)TK * Q * 2;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const float* srcA = WHICH == 0 ? a.DA : WHICH == 1 ? a.DH : a.GW;
+  const float* srcB = WHICH == 0 ? a.XT : WHICH == 1 ? a.H1 : a.H2;
+  uint8_t* aimg = sm;
+  uint8_t* bimg = sm + 2 * AB;
+  // image columns P..127 of A stay 0 (MMA M = 128)
+  for (int e = t; e < (int)(2 * AB / 16); e += RT) reinterpret_cast<uint4*>(aimg)[e] = make_uint4(0, 0, 0, 0);
+  const int nch = r0 < r1 ? (int)((r1 - r0 + TK - 1) / TK) : 0;
+  constexpr uint32_t idesc = idesc_bf16(128, Q, true, true);
+  float4 va[UA], vb[UB];
+  auto load = [&](int c) {
+    const int64_t rb = r0 + (int64_t)c * TK;
+    const float* ga = srcA + ((size_t)n * a.B + rb) * P;
+    const float* gb = srcB + ((size_t)n * a.B + rb) * Q;
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const int e = t + u * RT;
+      int rl, c4;
+      slot_rc<P>(e, rl, c4);
+      va[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < TK * PA && rb + rl < r1) va[u] = __ldg(reinterpret_cast<const float4*>(ga + rl * P + c4));
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int e = t + u * RT;
+      int rl, c4;
+      slot_rc<Q>(e, rl, c4);
+      vb[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < TK * QB && rb + rl < r1) vb[u] = __ldg(reinterpret_cast<const float4*>(gb + rl * Q + c4));
+    }
+  };
+  if (nch > 0) load(0);
+  for (int c = 0; c < nch; ++c) {
+    const int64_t rb = r0 + (int64_t)c * TK;
+    if (WHICH == 2 && t < TK) {   // ā_{n+1} of the chunk's rows (dZ = ā G)
+      const int64_t m = rb + t;
+      srow[t] = m < r1 ? abar_of(a, n, m) : 0.0f;
+    }
+    if (c > 0) mbar_wait(bar, (uint32_t)((c - 1) & 1));   // chunk c-1's MMAs have read the images
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const int e = t + u * RT;
+      if (e >= TK * PA) break;
+      int rl, c4;
+      slot_rc<P>(e, rl, c4);
+      float4 v = va[u];
+      if (WHICH == 2) {
+        const float sc = srow[rl];
+        v = make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w);
+      }
+      uint2 hi, lo;
+      split4(v, hi, lo);
+      *reinterpret_cast<uint2*>(aimg + ioff(rl, c4, 128)) = hi;
+      *reinterpret_cast<uint2*>(aimg + AB + ioff(rl, c4, 128)) = lo;
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int e = t + u * RT;
+      if (e >= TK * QB) break;
+      int rl, c4;
+      slot_rc<Q>(e, rl, c4);
+      uint2 hi, lo;
+      split4(vb[u], hi, lo);
+      *reinterpret_cast<uint2*>(bimg + ioff(rl, c4, Q)) = hi;
+      *reinterpret_cast<uint2*>(bimg + BB + ioff(rl, c4, Q)) = lo;
+    }
+    fence_async_smem();
+    tc_before();
+    __syncthreads();
+    if (t == 0) {
+      tc_after();
+      const Opnd Ah = mnmaj(aimg, 128), Al = mnmaj(aimg + AB, 128);
+      const Opnd Bh = mnmaj(bimg, Q), Bl = mnmaj(bimg + BB, Q);
+      gemm(tm, Ah, Bh, TK / 16, idesc, c > 0);
+      gemm(tm, Ah, Bl, TK / 16, idesc, true);
+      gemm(tm, Al, Bh, TK / 16, idesc, true);
+      mma_commit(bar);
+    }
+    if (c + 1 < nch) load(c + 1);   // in flight while the MMAs run
+  }
+  if (nch > 0) {
+    mbar_wait(bar, (uint32_t)((nch - 1) & 1));
+    tc_after();
+    const int d = a.d, w = a.w;
+    const NetDims nd{d, w};
+    float* G = a.grad + nd.step_base(n);
+    const int qd = warp & 3, hh = warp >> 2, p = 32 * qd + lane;
+    const uint32_t lb = tm + ((uint32_t)(32 * qd) << 16);
+    constexpr int NCH8 = Q / 16;
+    uint32_t r8[NCH8][8];
+#pragma unroll
+    for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(hh * (Q / 2) + 8 * jj), r8[jj]);
+    tmem_ld_wait();
+#pragma unroll
+    for (int jj = 0; jj < NCH8; ++jj) {
+      reg_fence8(r8[jj]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int k = hh * (Q / 2) + 8 * jj + e;
+        const float v = __uint_as_float(r8[jj][e]);
+        if (v == 0.0f) continue;
+        int64_t off = -1;
+        if (WHICH == 0 && p < w) off = k < d ? nd.off_W1() + p * d + k : (k == d ? nd.off_b1() + p : -1);
+        if (WHICH == 1 && p < w) off = k < w ? nd.off_W2() + p * w + k : (k == w ? nd.off_b2() + p : -1);
+        if (WHICH == 2 && p < d) off = k < w ? nd.off_W3() + p * w + k : (k == w ? nd.off_b3() + p : -1);
+        if (off >= 0) atomicAdd(G + off, v);
+      }
+    }
+  }
+}
+
+template <int DP, int WP>
+__global__ void __launch_bounds__(RT, 2) k_rows_tn_t(RowsArgs a, int rows_per_cta) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tslot;
+  __shared__ float srow[TK];
+  const int t = threadIdx.x, warp = t >> 5;
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tslot, 128);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tm = tslot;
+  const int n = blockIdx.z;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = (a.B < r0 + rows_per_cta ? a.B : r0 + rows_per_cta);
+  if (blockIdx.y == 0) rows_tn_body<0, DP, WP>(a, n, r0, r1, sm, &bar, tm, srow);
+  else if (blockIdx.y == 1) rows_tn_body<1, DP, WP>(a, n, r0, r1, sm, &bar, tm, srow);
+  else rows_tn_body<2, DP, WP>(a, n, r0, r1, sm, &bar, tm, srow);
+  tc_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_after();
+    tmem_dealloc(tm, 128);
+  }
+}
+
 inline int pad16(int x) { return (x + 15) / 16 * 16; }
 inline int sm_count() {
   int dev = 0, sms = 148;
@@ -562,16 +889,35 @@ inline int sm_count() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return sms;
 }
+template <int OP, int DP, int WP>
+cudaError_t gemm_launch_t(const RowsArgs& a, cudaStream_t s) {
+  constexpr int K = (OP == F1 || OP == B1) ? DP : WP, NC = (OP == F3) ? DP : WP;
+  constexpr size_t half = 64 * (size_t)(NC + 4) * 4, ab2 = 2 * 128 * (size_t)K * 2;
+  constexpr size_t smem = 2 * (size_t)NC * K * 2 + (half <= ab2 ? ab2 : ab2 + half);
+  cudaError_t e = cudaFuncSetAttribute(k_rows_gemm_t<OP, DP, WP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_rows_gemm_t<OP, DP, WP><<<dim3((unsigned)((a.B + 127) / 128), (unsigned)a.N), RT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// compile-time shapes for the built (Dp, Wp) pairs, else the runtime-shaped kernel
+#define BSDE_ROWS_SHAPES(X) X(112, 112) X(16, 32) X(48, 48) X(16, 16)
+
 template <int OP>
 cudaError_t gemm_launch(const RowsArgs& a, cudaStream_t s) {
+#define X(DP_, WP_) if (a.Dp == DP_ && a.Wp == WP_) return gemm_launch_t<OP, DP_, WP_>(a, s);
+  BSDE_ROWS_SHAPES(X)
+#undef X
   const int K = (OP == F1 || OP == B1) ? a.Dp : a.Wp, Nc = (OP == F3) ? a.Dp : a.Wp;
-  const size_t smem = 2 * (size_t)img_bytes(Nc, K) + 2 * (size_t)img_bytes(128, K);
+  const size_t smem = 2 * (size_t)img_bytes(Nc, K) + 2 * (size_t)img_bytes(128, K) + 128 * (size_t)K * 4 +
+                      128 * (size_t)(Nc + 4) * 4;
   cudaError_t e = cudaFuncSetAttribute(k_rows_gemm<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  // two CTAs per SM over the N steps; each walks the row tiles of its step
+  // one CTA per SM over the N steps; each walks the row tiles of its step
   const int ntiles = (int)((a.B + 127) / 128), sms = sm_count();
-  int g = (2 * sms + a.N - 1) / a.N;
+  int g = (sms + a.N - 1) / a.N;
   if (g > ntiles) g = ntiles;
   if (g < 1) g = 1;
   k_rows_gemm<OP><<<dim3((unsigned)g, (unsigned)a.N), RT, smem, s>>>(a);
@@ -640,15 +986,33 @@ cudaError_t launch_rows_forward(const RowsArgs& a, cudaStream_t s, int* launches
 cudaError_t launch_rows_backward(const RowsArgs& a, cudaStream_t s, int* launches) {
   RCK(rows::gemm_launch<rows::B1>(a, s));
   RCK(rows::gemm_launch<rows::B2>(a, s));
-  // about four CTAs per SM over the 3·N weight-gradient problems, >= 256 rows each
   const int sms = rows::sm_count();
-  int split = (int)((4LL * sms + 3LL * a.N - 1) / (3LL * a.N));
+#define X(DP_, WP_)                                                                               \
+  if (a.Dp == DP_ && a.Wp == WP_) {   /* compile-time shapes: ~2 CTAs per SM */                   \
+    int sp = (int)((2LL * sms + 3LL * a.N - 1) / (3LL * a.N));                                    \
+    const int64_t mx = (a.B + 255) / 256;                                                          \
+    if (sp > mx) sp = (int)mx;                                                                     \
+    if (sp < 1) sp = 1;                                                                            \
+    const int rp = (int)((a.B + sp - 1) / sp);                                                     \
+    const size_t sm2 = 2 * (size_t)rows::TK * 128 * 2 + 2 * (size_t)rows::TK * 128 * 2;           \
+    RCK(cudaFuncSetAttribute(rows::k_rows_tn_t<DP_, WP_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)sm2));                                                           \
+    rows::k_rows_tn_t<DP_, WP_><<<dim3((unsigned)((a.B + rp - 1) / rp), 3, (unsigned)a.N),         \
+                                  rows::RT, sm2, s>>>(a, rp);                                      \
+    RCK(cudaGetLastError());                                                                       \
+    if (launches) *launches += 3;                                                                  \
+    return cudaSuccess;                                                                            \
+  }
+  BSDE_ROWS_SHAPES(X)
+#undef X
+  // one CTA per SM over the 3·N weight-gradient problems, >= 256 rows each
+  int split = (int)((sms + 3LL * a.N - 1) / (3LL * a.N));
   const int64_t maxsplit = (a.B + 255) / 256;
   if (split > maxsplit) split = (int)maxsplit;
   if (split < 1) split = 1;
   const int rpc = (int)((a.B + split - 1) / split);
-  const int Qmax = a.Dp > a.Wp ? a.Dp : a.Wp;
-  const size_t smem = 2 * (2 * (size_t)rows::img_bytes(rows::TK, 128) + 2 * (size_t)rows::img_bytes(rows::TK, Qmax));
+  const size_t smem = 2 * (size_t)rows::img_bytes(rows::TK, 128) + 2 * (size_t)rows::img_bytes(rows::TK, 128) +
+                      4 * (size_t)rows::TK * 128 * 4;
   RCK(cudaFuncSetAttribute(rows::k_rows_tn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   rows::k_rows_tn<<<dim3((unsigned)((a.B + rpc - 1) / rpc), 3, (unsigned)a.N), rows::RT, smem, s>>>(a, rpc);
   RCK(cudaGetLastError());
