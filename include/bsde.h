@@ -51,7 +51,10 @@ enum {
 
 /* GEMM operand precision; accumulation is always fp32 (R17, R18). */
 enum {
-  BSDE_FP32 = 0,       /* fp32-accurate: bf16x3 split operands on tcgen05, or SIMT FFMA */
+  BSDE_FP32 = 0,       /* fp32-accurate: on tcgen05 ("tc32", kernel AUTO | TC) every GEMM
+                          operand split into bf16 hi + lo and three MMAs per product
+                          (hi·hi + hi·lo + lo·hi, ~2^-16 relative, DESIGN R18b); SIMT
+                          FFMA with kernel SIMT, NAIS-Net or deterministic mode        */
   BSDE_BF16 = 1        /* bf16 operands, fp32 accumulate.  Per-step nets on tcgen05
                           (DESIGN R17): the biases are folded into the bf16 weight images,
                           H1 = bf16(ReLU(A1)), H2 = bf16(H1 + bf16(ReLU(A2))) (one bf16x2
@@ -262,8 +265,26 @@ int bsde_debug_phase_clocks(bsde_ctx* ctx, int which, uint64_t* out, int n);
  * n_out must be >= 6.  Synchronises. */
 int bsde_profile_steps(bsde_ctx* ctx, int steps, float* ms_out, int n_out);
 
+/* NEXT-4 (BASELINE north_star (e)): the gradient
+ * reduce-scatter, Adam on this rank's 1/world shard of the parameters and the
+ * all-gather of the updated parameters as ONE kernel over peer memory (NVLink loads /
+ * stores through CUDA IPC mappings, fused_opt.cu), chained after the adjoint in the
+ * step graph in place of the NCCL allreduce + check + Adam.  Shards are reduced in
+ * rank order (deterministic); the divergence guard is decided over all ranks.
+ *   bsde_ipc_export writes 4 cudaIpcMemHandle_t (256 bytes: gradient, parameters,
+ *     barrier flags, device state) to out[bytes >= 256].  Not with cfg.workspace.
+ *   bsde_fused_opt_enable takes every rank's 256 bytes in rank order (world × 256;
+ *     NULL allowed at world = 1), opens the peers' buffers and switches
+ *     bsde_train_step to the fused kernel.  Every rank must enable it; all ranks
+ *     then run the same number of steps (the kernel's barriers span the ranks).
+ * One block per SM must be co-resident (nothing else on the GPU while it runs).
+ * Collective over the ranks; EINVAL on a world mismatch, ESTATE if already enabled. */
+int bsde_ipc_export(const bsde_ctx* ctx, void* out, int64_t bytes);
+int bsde_fused_opt_enable(bsde_ctx* ctx, const void* handles, int world);
+
 /* Number of kernels the last bsde_train_step enqueued (for the bench's
- * gpu_launches), and the name of the kernel family in use ("simt" | "tc"). */
+ * gpu_launches), and the name of the kernel family in use ("simt" | "tc" bf16 |
+ * "tc32" fp32-accurate bf16x3 row GEMMs | "shared-simt" | "shared-tc"). */
 int bsde_launches_per_step(const bsde_ctx* ctx, int* n);
 const char* bsde_kernel_family(const bsde_ctx* ctx);
 

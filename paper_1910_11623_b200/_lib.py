@@ -27,7 +27,7 @@ SYMBOLS = [
     "bsde_debug_dw", "bsde_debug_dw_fast", "bsde_debug_residuals", "bsde_debug_umma",
     "bsde_debug_phase_clocks", "bsde_profile_steps",
     "bsde_launches_per_step", "bsde_kernel_family", "bsde_nccl_unique_id", "bsde_last_error",
-    "bsde_destroy",
+    "bsde_ipc_export", "bsde_fused_opt_enable", "bsde_destroy",
 ]
 
 
@@ -108,6 +108,8 @@ def lib():
             "bsde_kernel_family": (ctypes.c_char_p, [P]),
             "bsde_nccl_unique_id": (I32, [P]),
             "bsde_last_error": (ctypes.c_char_p, [P]),
+            "bsde_ipc_export": (I32, [P, P, I64]),
+            "bsde_fused_opt_enable": (I32, [P, P, I32]),
             "bsde_destroy": (None, [P]),
         }
         for name, (res, args) in sig.items():

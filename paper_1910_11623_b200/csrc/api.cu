@@ -93,6 +93,10 @@ struct bsde_ctx {
   int L = 0;                    // shared: number of tanh layers
   void* shbuf = nullptr;        // shared: row buffers (carved into ShArgs)
   void* rowsbuf = nullptr;      // fp32-accurate tcgen05 family: row buffers (RowsArgs)
+  unsigned* flags = nullptr;    // NEXT-4 fused optimizer: barrier counters / divergence flags
+  bool fused = false;           // bsde_fused_opt_enable done: the peer-memory optimizer runs
+  FusedOptArgs fo{};            // its peer pointers (np / shard filled per step)
+  std::vector<void*> ipc_open;  // peer mappings to close
   bool external_ws = false;     // buffers carved from cfg.workspace (caller-owned)
   int sms = 148;                // SM count (grid sizes of the deterministic partials)
   float* dpart = nullptr;       // deterministic mode: adjoint partials
@@ -297,7 +301,7 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
   mark(0);
   const bool sharded = ctx->comm && ctx->cfg.sharded_adam && with_update;
   const int64_t shard = shard_of(ctx, np), npad = shard * ctx->cfg.world;
-  CK(launch_begin_step(ctx->state, ctx->grad, sharded ? npad : np, ctx->stream));
+  CK(launch_begin_step(ctx->state, ctx->grad, (sharded || ctx->fused) ? npad : np, ctx->stream));
   launches += 1;   // k_begin_step (the memset is not a kernel)
   mark(1);
   if (ctx->shared) {
@@ -339,6 +343,30 @@ int enqueue_step(bsde_ctx* ctx, bool with_update, cudaEvent_t* ev = nullptr) {
     }
   }
   mark(3);
+  if (ctx->fused && with_update) {   // NEXT-4: one peer-memory kernel replaces a7 + check + a8
+    FusedOptArgs fo = ctx->fo;
+    fo.np = np;
+    fo.shard = shard;
+    fo.inv_B = 1.0 / (double)ctx->cfg.batch_global;
+    CK(launch_fused_opt(fo, ctx->sms, ctx->stream));
+    mark(4);
+    mark(5);
+    CK(launch_end_step(ctx->state, 1, ctx->stream));
+    launches += 2;
+    if (ctx->nais) {
+      CK(launch_nais_project(ctx->params, ctx->d, ctx->w, ctx->N, ctx->stream));
+      launches += 1;
+    }
+    if (!ctx->shared) {
+      if (ctx->family == kFamilyRows) CK(launch_rows_pack(rows_args(ctx, ctx->B_local, ctx->m0), ctx->stream));
+      else if (ctx->family == BSDE_KERNEL_TC) CK(launch_pack_weights(a, ctx->stream));
+      else CK(launch_pack_simt(a, ctx->stream));
+      launches += 1;
+    }
+    mark(6);
+    ctx->launches = launches;
+    return BSDE_OK;
+  }
   const int64_t off = sharded ? shard * ctx->cfg.rank : 0;
   const int64_t nloc = sharded ? std::max<int64_t>(0, std::min(shard, np - off)) : np;
   if (sharded) {   // reduce-scatter: this rank's shard of the summed gradient, in place
@@ -409,6 +437,8 @@ int repack(bsde_ctx* ctx) {
 
 void free_all(bsde_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
+  c->ipc_open.clear();
   if (c->external_ws) {   // nothing of ours to free but the communicator and the stream
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -416,7 +446,7 @@ void free_all(bsde_ctx* c) {
   }
   void* bufs[] = {c->params, c->grad, c->adam_m, c->adam_v, c->scratch, c->Xstore, c->Pstore,
                   c->abar, c->Rstore, c->wpack, c->xpack, c->gpart, c->state,
-                  c->eval_loss, c->shbuf, c->dpart, c->lpart, c->y0part, c->rowsbuf};
+                  c->eval_loss, c->shbuf, c->dpart, c->lpart, c->y0part, c->rowsbuf, c->flags};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
@@ -488,6 +518,8 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
       return fail(none, BSDE_EINVAL, "the shared NAIS-Net network runs on the fp32 kernels only");
     if (cfg.deterministic)
       return fail(none, BSDE_EINVAL, "deterministic mode covers the per-step formulation only");
+    if (widths[0] % 4)   // the activation rows (stride w) are read as float4 by the GEMMs
+      return fail(none, BSDE_EINVAL, "shared net: width w=%d must be a multiple of 4", widths[0]);
   } else if (!widths || n_widths != 2 || widths[0] != widths[1] || widths[0] < 1) {
     return fail(none, BSDE_EINVAL,
                 "widths must be {w, w} with w >= 1 (d->w->w->d residual net, R4); got n_widths=%d",
@@ -601,6 +633,7 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
       {(void**)&ctx->Rstore, (size_t)ctx->B_local * sizeof(float)},
       {(void**)&ctx->state, sizeof(DeviceState)},
       {(void**)&ctx->eval_loss, sizeof(double) * 2},
+      {(void**)&ctx->flags, 32 * sizeof(unsigned)},
   };
   if (det_floats) {
     allocs.push_back({(void**)&ctx->dpart, det_floats * sizeof(float)});
@@ -671,6 +704,7 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
   cudaMemsetAsync(ctx->adam_v, 0, npalloc * sizeof(float), ctx->stream);
   cudaMemsetAsync(ctx->params, 0, npalloc * sizeof(float), ctx->stream);
   cudaMemsetAsync(ctx->state, 0, sizeof(DeviceState), ctx->stream);
+  cudaMemsetAsync(ctx->flags, 0, 32 * sizeof(unsigned), ctx->stream);
   const cudaError_t ie =
       shared ? launch_shared_init(ctx->params, sh_args(ctx), (uint32_t)(cfg.seed & 0xffffffffu),
                                   (uint32_t)(cfg.seed >> 32), ctx->stream)
@@ -1052,6 +1086,60 @@ int bsde_debug_phase_clocks(bsde_ctx* ctx, int which, uint64_t* out, int n) {
   CK(cudaMemcpyAsync(out, buf, (size_t)n * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   cudaFree(buf);
+  return BSDE_OK;
+}
+
+int bsde_ipc_export(const bsde_ctx* c, void* out, int64_t bytes) {
+  bsde_ctx* ctx = const_cast<bsde_ctx*>(c);
+  if (!ctx || !out || bytes < 4 * (int64_t)sizeof(cudaIpcMemHandle_t))
+    return fail(ctx, BSDE_EINVAL, "ipc_export: need %d bytes", (int)(4 * sizeof(cudaIpcMemHandle_t)));
+  if (ctx->external_ws)
+    return fail(ctx, BSDE_EINVAL, "ipc_export: not available with a caller-owned workspace");
+  void* bufs[4] = {ctx->grad, ctx->params, ctx->flags, ctx->state};
+  cudaIpcMemHandle_t* h = static_cast<cudaIpcMemHandle_t*>(out);
+  for (int i = 0; i < 4; ++i) CK(cudaIpcGetMemHandle(&h[i], bufs[i]));
+  return BSDE_OK;
+}
+
+int bsde_fused_opt_enable(bsde_ctx* ctx, const void* handles, int world) {
+  if (!ctx) return fail(ctx, BSDE_EINVAL, "ctx is NULL");
+  if (world != ctx->cfg.world || world < 1 || world > kMaxPeers)
+    return fail(ctx, BSDE_EINVAL, "fused_opt_enable: world=%d (context world %d, at most %d)", world,
+                ctx->cfg.world, kMaxPeers);
+  if (world > 1 && !handles) return fail(ctx, BSDE_EINVAL, "fused_opt_enable: handles is NULL");
+  if (ctx->fused) return fail(ctx, BSDE_ESTATE, "fused optimizer already enabled");
+  FusedOptArgs fo{};
+  fo.world = world;
+  fo.rank = ctx->cfg.rank;
+  fo.m = ctx->adam_m;
+  fo.v = ctx->adam_v;
+  fo.state = ctx->state;
+  fo.lr = (float)ctx->cfg.lr;
+  fo.beta1 = (float)ctx->cfg.beta1;
+  fo.beta2 = (float)ctx->cfg.beta2;
+  fo.eps = (float)ctx->cfg.eps;
+  const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int q = 0; q < world; ++q) {
+    if (q == ctx->cfg.rank) {
+      fo.peer_grad[q] = ctx->grad;
+      fo.peer_params[q] = ctx->params;
+      fo.peer_flags[q] = ctx->flags;
+      fo.peer_state[q] = ctx->state;
+      continue;
+    }
+    void* p[4];
+    for (int i = 0; i < 4; ++i) {
+      CK(cudaIpcOpenMemHandle(&p[i], h[4 * q + i], cudaIpcMemLazyEnablePeerAccess));
+      ctx->ipc_open.push_back(p[i]);
+    }
+    fo.peer_grad[q] = static_cast<float*>(p[0]);
+    fo.peer_params[q] = static_cast<float*>(p[1]);
+    fo.peer_flags[q] = static_cast<unsigned*>(p[2]);
+    fo.peer_state[q] = static_cast<DeviceState*>(p[3]);
+  }
+  ctx->fo = fo;
+  ctx->fused = true;
+  if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
   return BSDE_OK;
 }
 

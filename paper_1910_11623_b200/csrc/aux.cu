@@ -296,6 +296,11 @@ cudaError_t launch_adam(float* params, const float* grad, float* m, float* v, in
   return cudaGetLastError();
 }
 
+cudaError_t launch_end_step(DeviceState* st, int advance_it, cudaStream_t s) {
+  k_end_step<<<1, 1, 0, s>>>(st, advance_it);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_prolong(const float* src, float* dst, int64_t P, int N, int mode,
                            cudaStream_t s) {
   k_prolong<<<grid_for(2LL * N * P), NT, 0, s>>>(src, dst, P, N, mode);

@@ -170,7 +170,7 @@ struct DeviceState {
   double loss_sum;    // Σ_m R² of the current step (local, then all-reduced)
   double loss_last;   // loss of the last step (mean over the global batch)
   float c1, c2;       // Adam bias corrections 1/(1-β1^(t+1)), 1/(1-β2^(t+1)) of this step
-  int32_t pad;
+  uint32_t opt_epoch; // launches of the fused peer-memory optimizer (fused_opt.cu)
 };
 
 }  // namespace bsde

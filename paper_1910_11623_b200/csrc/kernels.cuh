@@ -45,6 +45,22 @@ struct PassArgs {
   float sqrt_dt_f;                     // √(Δt/cpl)
 };
 
+// NEXT-4 (fused_opt.cu): reduce-scatter + sharded Adam + all-gather over peer memory
+constexpr int kMaxPeers = 8;
+struct FusedOptArgs {
+  int world, rank;
+  int64_t np, shard;                       // parameters (unpadded), shard (multiple of 4)
+  float* peer_grad[kMaxPeers];             // every rank's gradient buffer (IPC-mapped; [rank] = own)
+  float* peer_params[kMaxPeers];
+  unsigned* peer_flags[kMaxPeers];         // [0] arrivals, [1+q] divergence of rank q, [16] grid barrier
+  DeviceState* peer_state[kMaxPeers];
+  float *m, *v;                            // this rank's Adam moments (shard entries used)
+  DeviceState* state;
+  double inv_B;
+  float lr, beta1, beta2, eps;
+};
+cudaError_t launch_fused_opt(const FusedOptArgs& a, int sms, cudaStream_t s);
+
 // fp32-accurate per-step nets on tcgen05 (rows_tc.cu; DESIGN R18b): one iteration's
 // row buffers over R = N·B rows (row (n, m) = n·B + m), bf16x3 GEMM operands
 struct RowsArgs {
@@ -140,6 +156,7 @@ cudaError_t launch_check(const float* grad, int64_t n, DeviceState* st, double i
 cudaError_t launch_adam(float* params, const float* grad, float* m, float* v, int64_t n,
                         DeviceState* st, float lr, float beta1, float beta2, float eps,
                         int advance_it, cudaStream_t s);
+cudaError_t launch_end_step(DeviceState* st, int advance_it, cudaStream_t s);
 cudaError_t launch_prolong(const float* src, float* dst, int64_t P, int N, int mode,
                            cudaStream_t s);
 cudaError_t launch_debug_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, int64_t count,

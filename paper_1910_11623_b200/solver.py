@@ -118,6 +118,7 @@ class BSDE:
         cfg.coupled_paths = int(bool(coupled_paths))
         cfg.formulation = FORMULATIONS[formulation]
         cfg.sharded_adam = int(bool(sharded_adam))
+        self._sharded, self._fused = bool(sharded_adam), False
         cfg.deterministic = int(bool(deterministic))
         cfg.shared_zN = int(bool(zN))
         if workspace is not None:   # caller-owned device memory (a torch tensor), kept alive
@@ -224,7 +225,13 @@ class BSDE:
     def save_checkpoint(self, path):
         """Flat named arrays: parameters, Adam m, v, t and the
         Philox iteration (the paths of every later iteration follow from it, R8/R9).
-        np.savez; bit-exact round trip through load_checkpoint."""
+        np.savez; bit-exact round trip through load_checkpoint.  A rank of a sharded
+        optimizer (sharded_adam or the fused NEXT-4 kernel, world > 1) holds the Adam
+        moments of its own shard only, so its checkpoint would not restore the others:
+        refused."""
+        if self.world > 1 and (self._sharded or self._fused):
+            raise BSDEError(-5, "save_checkpoint: Adam state is sharded over the ranks "
+                                "(sharded_adam / fused optimizer), a single rank cannot save it")
         m, v, t = self.get_adam_state()
         np.savez(path, params=self.get_params(), adam_m=m, adam_v=v, adam_t=np.int64(t),
                  iteration=np.int64(self.iteration), N=np.int64(self.N),
@@ -254,6 +261,24 @@ class BSDE:
     @iteration.setter
     def iteration(self, it):
         self._ck(self._L.bsde_set_iteration(self._h, int(it)))
+
+    def enable_fused_optimizer(self):
+        """NEXT-4: switch the optimizer to the single peer-memory kernel (reduce-scatter,
+        sharded Adam, all-gather; fused_opt.cu).  Collective: with world > 1 every rank
+        calls it after torch.distributed is initialised (the 256-byte CUDA IPC handles
+        are exchanged with all_gather_object); at world = 1 the peer is the context."""
+        world = self.world
+        if world > 1:
+            import torch.distributed as dist
+            buf = ctypes.create_string_buffer(256)
+            self._ck(self._L.bsde_ipc_export(self._h, ctypes.cast(buf, ctypes.c_void_p), 256))
+            parts = [None] * world
+            dist.all_gather_object(parts, buf.raw)
+            allh = ctypes.create_string_buffer(b"".join(parts), 256 * world)
+            self._ck(self._L.bsde_fused_opt_enable(self._h, ctypes.cast(allh, ctypes.c_void_p), world))
+        else:
+            self._ck(self._L.bsde_fused_opt_enable(self._h, None, 1))
+        self._fused = True
 
     def launches_per_step(self):
         n = ctypes.c_int()

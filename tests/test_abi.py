@@ -81,3 +81,7 @@ def test_workspace_bytes_without_gpu(libpath):
     assert s > 0
     with pytest.raises(BSDEError):
         workspace_bytes("heat", 0, 2, 8, 16)
+    # the shared net's activation rows are read as float4: a width not divisible by 4 is
+    # refused at create time instead of misaligning the GEMM loads
+    with pytest.raises(BSDEError, match="multiple of 4"):
+        workspace_bytes("black_scholes", 100, 50, 30, 100, formulation="shared", layers=4)

@@ -274,7 +274,7 @@ def test_torch_workspace_context_matches_own_allocations():
     import torch
     from paper_1910_11623_b200.solver import workspace_bytes
     d, w, N, B = 12, 16, 3, 128
-    nbytes = workspace_bytes("hjb", d, N, w, B)
+    nbytes = workspace_bytes("hjb", d, N, w, B, kernel="simt")
     ws = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
     off = (-ws.data_ptr()) % 256
     view = ws[off:off + nbytes]

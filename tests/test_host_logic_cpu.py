@@ -145,3 +145,16 @@ def test_multilevel_loss_csv(tmp_path):
     cols = [r.split(",") for r in rows[1:]]
     assert [int(c[1]) for c in cols] == [0, 0, 1, 1] and [int(c[2]) for c in cols] == [2, 2, 4, 4]
     assert np.allclose([float(c[3]) for c in cols], [r.train_loss for r in res.records])
+
+
+def test_checkpoint_refused_for_sharded_optimizer_state(tmp_path):
+    """a rank of a sharded optimizer (sharded_adam / fused NEXT-4 kernel,
+    world > 1) holds 1/world of the Adam moments; save_checkpoint refuses instead of
+    writing a file that load_checkpoint would restore wrongly."""
+    from paper_1910_11623_b200 import BSDE, BSDEError
+    for sharded, fused in ((True, False), (False, True)):
+        s = BSDE.__new__(BSDE)
+        s.world, s._sharded, s._fused = 2, sharded, fused
+        with pytest.raises(BSDEError, match="sharded"):
+            s.save_checkpoint(tmp_path / "ck.npz")
+        assert not (tmp_path / "ck.npz").exists()
