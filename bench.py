@@ -259,6 +259,8 @@ def main():
     ap.add_argument("--ml-precision", default="bf16")
     ap.add_argument("--sharded-adam", action="store_true",
                     help="reduce-scatter + sharded Adam + all-gather (NEXT-4) for N > 1")
+    ap.add_argument("--fused-opt", action="store_true",
+                    help="NEXT-4 as one peer-memory kernel (fused_opt.cu) instead of NCCL + Adam")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = 10 if args.impl == "reference" else 40
@@ -299,6 +301,8 @@ def main():
         s = BSDE.distributed(wl.problem, wl.d, wl.N, wl.T, wl.w, wl.batch, **kw)
     else:
         s = BSDE(wl.problem, wl.d, wl.N, wl.T, wl.w, wl.batch, **kw)
+    if args.fused_opt:
+        s.enable_fused_optimizer()
     family = s.family
     stream = s.stream          # the stream libbsde enqueues on
 
@@ -402,7 +406,11 @@ def main():
                            "binary16 dW copy), fp32 accumulation, X/Y/reductions/Adam fp32"
                            if family == "tc" else "fp32"),
             "data": "synthetic (Philox4x32-10 Brownian increments generated on device, R8)",
-            "config": config_dict(wl, world, family),
+            "config": dict(config_dict(wl, world, family),
+                           optimizer=("fused peer-memory kernel" if args.fused_opt else
+                                      "NCCL reduce-scatter + sharded Adam + all-gather"
+                                      if args.sharded_adam else "NCCL allreduce + Adam"
+                                      if world > 1 else "Adam")),
             "roofline": {"bound": bound, "kernel": "bsde_" + dom, "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "peak_sustained": peak_sus, "frac_sustained": achieved / peak_sus,

@@ -10,6 +10,9 @@
 #pragma once
 #include <cuda_bf16.h>
 #include <stdint.h>
+#ifdef BSDE_WATCHDOG
+#include <cstdio>
+#endif
 
 namespace bsde {
 namespace tc {
@@ -43,6 +46,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity), "r"(1000000u)
       : "memory");
 }
+#ifdef BSDE_WATCHDOG
+// debug builds: a phase wait that reports (barrier offset, parity, block, thread) and
+// traps after ~2 s instead of hanging
+static __device__ __noinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int tag) {
+  for (long long i = 0;; ++i) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity), "r"(1000u) : "memory");
+    if (ok) return;
+    if (i == 2000000 && (threadIdx.x & 31) == 0) {
+      printf("WATCHDOG tag %d bar %p parity %u block %d thread %d\n", tag, bar, parity, blockIdx.x, threadIdx.x);
+      asm volatile("trap;");
+    }
+  }
+}
+#define mbar_wait(b, p) mbar_wait_wd((b), (p), __LINE__)
+#endif
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
