@@ -988,8 +988,8 @@ cudaError_t launch_rows_backward(const RowsArgs& a, cudaStream_t s, int* launche
   RCK(rows::gemm_launch<rows::B2>(a, s));
   const int sms = rows::sm_count();
 #define X(DP_, WP_)                                                                               \
-  if (a.Dp == DP_ && a.Wp == WP_) {   /* compile-time shapes: ~2 CTAs per SM */                   \
-    int sp = (int)((2LL * sms + 3LL * a.N - 1) / (3LL * a.N));                                    \
+  if (a.Dp == DP_ && a.Wp == WP_) {   /* compile-time shapes: 2 CTAs per SM, one wave */          \
+    int sp = (int)((2LL * sms) / (3LL * a.N));                                                     \
     const int64_t mx = (a.B + 255) / 256;                                                          \
     if (sp > mx) sp = (int)mx;                                                                     \
     if (sp < 1) sp = 1;                                                                            \
