@@ -79,6 +79,9 @@ struct RowsArgs {
   uint8_t* wimg_w;                     // the same, for the pack kernel
   float *XT, *GW, *H1, *H2, *DH, *DA;  // X̃ [R×Dp]; ΔW then G = ΔW - Δt∂_z f [R×Dp]; H1, H2, dH2, dA1 [R×Wp]
   float *S, *xn2;                      // per row (Z·ΔW, |Z|² | Σ Z); |X_N|² per path
+  // ReLU masks per row (compile-time shapes): 1[A1 > 0], 1[A2 > 0] as 4 words, bit l of
+  // word e = column 4l + e (written by F1 / F2, read by the fused adjoint B12)
+  uint32_t *M1, *M2;
   float *abar, *Pstore, *Rstore;       // as PassArgs
 };
 bool rows_supported(int d, int w);

@@ -488,6 +488,14 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
       const size_t row = (size_t)n * a.B + m;
       const float4 v = lane_on ? *reinterpret_cast<const float4*>(stile + r * LDT + c4)
                                : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (OP == F1 || OP == F2) {   // ReLU masks 1[A > 0] of the row for the fused adjoint
+        const uint32_t b0 = __ballot_sync(0xffffffffu, lane_on && v.x > 0.f);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, lane_on && v.y > 0.f);
+        const uint32_t b2 = __ballot_sync(0xffffffffu, lane_on && v.z > 0.f);
+        const uint32_t b3 = __ballot_sync(0xffffffffu, lane_on && v.w > 0.f);
+        if (lane == 0 && !a.eval)
+          *reinterpret_cast<uint4*>((OP == F1 ? a.M1 : a.M2) + row * 4) = make_uint4(b0, b1, b2, b3);
+      }
       if (OP == F1 && lane_on)
         *reinterpret_cast<float4*>(a.H1 + row * WP + c4) =
             make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
@@ -538,6 +546,195 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
       }
     }
     __syncthreads();
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_after();
+    tmem_dealloc(tm, 128);
+  }
+}
+
+// ------------------------------------------------------------------ fused adjoint B1 + B2
+// Compile-time shapes: one CTA per SM walks the 128-row tiles of step n = blockIdx.y
+// with the step's W̃3 and W̃2 images (hi / lo) resident, the next tile's G rows in
+// flight while the current one computes:
+//   G4  dH2 = dZ W̃3, dZ = ā_{n+1} G (staged as bf16 hi / lo; three MMA passes)
+//   E4  dA2 = dH2 ⊙ 1[A2 > 0] (mask words from F2) -> DH (fp32, for dW̃2) and, as
+//       bf16 hi / lo, the A operand of G6 (over the dZ images, which G4 has read)
+//   G6  dH1 = dH2 + dA2 W̃2 (accumulated onto dH2 in TMEM)
+//   E6  dA1 = dH1 ⊙ 1[A1 > 0] (mask words from F1) -> DA (fp32, for dW̃1)
+// dH2 never leaves the chip, and the masks replace the H1 / H2 reads of B1 / B2.
+template <int DP, int WP>
+__global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
+  constexpr int G4N = DP / 4, U = (128 * G4N + RT - 1) / RT, LDT = WP + 4, NCH8 = WP / 16;
+  constexpr int KM = DP > WP ? DP : WP;
+  constexpr uint32_t MB3 = (uint32_t)DP * WP * 2, MB2 = (uint32_t)WP * WP * 2, AB = 128u * KM * 2;
+  constexpr uint32_t WB = 2u * (WP * DP + WP * WP + DP * WP);
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bars[2];   // 0 weights, 1 MMA
+  __shared__ uint32_t tslot;
+  __shared__ float srow[128];
+  uint8_t* w3h = sm;
+  uint8_t* w3l = sm + MB3;
+  uint8_t* w2h = sm + 2 * MB3;
+  uint8_t* w2l = w2h + MB2;
+  uint8_t* ahi = w2l + MB2;
+  uint8_t* alo = ahi + AB;
+  float* stile = reinterpret_cast<float*>(alo + AB);   // [64 × LDT] half tile
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int n = blockIdx.y;
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tslot, 128);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tm = tslot;
+  if (t == 0) {   // step n's W̃3 and W̃2 (hi, lo)
+    const uint8_t* wsrc = a.wimg + (size_t)n * 2 * WB;
+    const uint32_t o3 = 2u * (WP * DP + WP * WP), o2 = 2u * WP * DP;
+    mbar_expect_tx(&bars[0], 2 * (MB3 + MB2));
+    for (uint32_t o = 0; o < MB3; o += 16384u) {
+      bulk_g2s(w3h + o, wsrc + o3 + o, min(16384u, MB3 - o), &bars[0]);
+      bulk_g2s(w3l + o, wsrc + WB + o3 + o, min(16384u, MB3 - o), &bars[0]);
+    }
+    for (uint32_t o = 0; o < MB2; o += 16384u) {
+      bulk_g2s(w2h + o, wsrc + o2 + o, min(16384u, MB2 - o), &bars[0]);
+      bulk_g2s(w2l + o, wsrc + WB + o2 + o, min(16384u, MB2 - o), &bars[0]);
+    }
+  }
+  const int ntiles = (int)((a.B + 127) / 128);
+  const int q = warp & 3, h = warp >> 2, rr = 32 * q + lane;
+  const uint32_t lb = tm + ((uint32_t)(32 * q) << 16);
+  const int cb = h * (WP / 2);
+  constexpr uint32_t idesc = idesc_bf16(128, WP, false, true);
+  float4 v[U];
+  auto load = [&](int tile) {   // G rows of `tile`, all loads in flight
+    const int64_t i0 = (int64_t)tile * 128;
+    const float* base = a.GW + ((size_t)n * a.B + i0) * DP;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = t + u * RT;
+      int r, c;
+      slot_rc<DP>(e, r, c);
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < 128 * G4N && i0 + r < a.B) v[u] = __ldg(reinterpret_cast<const float4*>(base + r * DP + c));
+    }
+  };
+  // E4 / E6 on the accumulator: mask, then fp32 rows -> dst (coalesced through the
+  // half tile); E4 also writes the bf16 hi / lo operand image of G6
+  auto epilogue = [&](int64_t i0, const uint4& mk, float* dst, bool img) {
+    const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
+#pragma unroll 1
+    for (int hf = 0; hf < 2; ++hf) {
+      if ((q >> 1) == hf) {
+        uint32_t r8[NCH8][8];
+#pragma unroll
+        for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
+        tmem_ld_wait();
+        const int rl = 32 * (q & 1) + lane;
+#pragma unroll
+        for (int jj = 0; jj < NCH8; ++jj) {
+          reg_fence8(r8[jj]);
+          const int c0 = cb + 8 * jj;
+          float f[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int col = c0 + j;
+            f[j] = ((mw[col & 3] >> (col >> 2)) & 1u) ? __uint_as_float(r8[jj][j]) : 0.0f;
+          }
+          float* sp = stile + rl * LDT + c0;
+          *reinterpret_cast<float4*>(sp) = make_float4(f[0], f[1], f[2], f[3]);
+          *reinterpret_cast<float4*>(sp + 4) = make_float4(f[4], f[5], f[6], f[7]);
+          if (img) {
+            uint2 h0, l0, h1, l1;
+            split4(make_float4(f[0], f[1], f[2], f[3]), h0, l0);
+            split4(make_float4(f[4], f[5], f[6], f[7]), h1, l1);
+            const uint32_t o = ioff(rr, c0, WP);
+            *reinterpret_cast<uint4*>(ahi + o) = make_uint4(h0.x, h0.y, h1.x, h1.y);
+            *reinterpret_cast<uint4*>(alo + o) = make_uint4(l0.x, l0.y, l1.x, l1.y);
+          }
+        }
+      }
+      __syncthreads();
+      const int c4 = 4 * lane;
+#pragma unroll 1
+      for (int r = warp; r < 64; r += RT / 32) {
+        const int64_t m = i0 + 64 * hf + r;
+        if (m >= a.B) break;
+        if (c4 < WP)
+          *reinterpret_cast<float4*>(dst + ((size_t)n * a.B + m) * WP + c4) =
+              *reinterpret_cast<const float4*>(stile + r * LDT + c4);
+      }
+      __syncthreads();
+    }
+  };
+  uint32_t mph = 0;
+  bool first = true;
+  if ((int)blockIdx.x < ntiles) load(blockIdx.x);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i0 = (int64_t)tile * 128;
+    if (t < 128) {
+      const int64_t m = i0 + t;
+      srow[t] = m < a.B ? abar_of(a, n, m) : 0.0f;
+    }
+    __syncthreads();
+    // dZ = ā_{n+1} G -> bf16 hi / lo A image (K = DP)
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = t + u * RT;
+      if (e >= 128 * G4N) break;
+      int r, c;
+      slot_rc<DP>(e, r, c);
+      const float sc = srow[r];
+      uint2 hi, lo;
+      split4(make_float4(sc * v[u].x, sc * v[u].y, sc * v[u].z, sc * v[u].w), hi, lo);
+      *reinterpret_cast<uint2*>(ahi + ioff(r, c, DP)) = hi;
+      *reinterpret_cast<uint2*>(alo + ioff(r, c, DP)) = lo;
+    }
+    // this thread's row masks (TMEM lane layout: row rr)
+    const int64_t mrow = i0 + rr;
+    const size_t ro = ((size_t)n * a.B + (size_t)mrow) * 4;
+    const uint4 mk2 = mrow < a.B ? __ldg(reinterpret_cast<const uint4*>(a.M2 + ro)) : make_uint4(0, 0, 0, 0);
+    const uint4 mk1 = mrow < a.B ? __ldg(reinterpret_cast<const uint4*>(a.M1 + ro)) : make_uint4(0, 0, 0, 0);
+    if (tile + (int)gridDim.x < ntiles) load(tile + gridDim.x);   // in flight until the next tile
+    fence_async_smem();
+    tc_before();
+    __syncthreads();
+    if (t == 0) {   // G4: dH2 = dZ W̃3
+      tc_after();
+      if (first) mbar_wait(&bars[0], 0);
+      const Opnd Ah = kmaj(ahi, DP), Al = kmaj(alo, DP), Wh = mnmaj(w3h, WP), Wl = mnmaj(w3l, WP);
+      gemm(tm, Ah, Wh, DP / 16, idesc, false);
+      gemm(tm, Ah, Wl, DP / 16, idesc, true);
+      gemm(tm, Al, Wh, DP / 16, idesc, true);
+      mma_commit(&bars[1]);
+    }
+    first = false;
+    mbar_wait(&bars[1], mph);
+    mph ^= 1;
+    tc_after();
+    epilogue(i0, mk2, a.DH, true);   // E4: dA2 -> DH and the G6 operand
+    fence_async_smem();
+    tc_before();
+    __syncthreads();
+    if (t == 0) {   // G6: dH1 = dH2 + dA2 W̃2
+      tc_after();
+      const Opnd Ah = kmaj(ahi, WP), Al = kmaj(alo, WP), Wh = mnmaj(w2h, WP), Wl = mnmaj(w2l, WP);
+      gemm(tm, Ah, Wh, WP / 16, idesc, true);
+      gemm(tm, Ah, Wl, WP / 16, idesc, true);
+      gemm(tm, Al, Wh, WP / 16, idesc, true);
+      mma_commit(&bars[1]);
+    }
+    mbar_wait(&bars[1], mph);
+    mph ^= 1;
+    tc_after();
+    epilogue(i0, mk1, a.DA, false);   // E6: dA1 -> DA
+    tc_before();
   }
   tc_before();
   __syncthreads();
@@ -930,7 +1127,7 @@ bool rows_supported(int d, int w) { return d + 1 <= 128 && w + 1 <= 128; }
 
 size_t rows_buffer_bytes(int d, int w, int N, int64_t B) {
   const size_t Dp = rows::pad16(d + 1), Wp = rows::pad16(w + 1), R = (size_t)N * B;
-  return 4 * (2 * R * Dp + 4 * R * Wp + 2 * R + B) + 6 * 256;
+  return 4 * (2 * R * Dp + 4 * R * Wp + 2 * R + B) + 2 * 16 * R + 8 * 256;
 }
 size_t rows_pack_bytes(int d, int w, int N) {
   const int Dp = rows::pad16(d + 1), Wp = rows::pad16(w + 1);
@@ -956,6 +1153,8 @@ void rows_carve(RowsArgs& a, void* base, int N_max) {
   a.DA = take(R * a.Wp);
   a.S = take(R * 2);
   a.xn2 = take(a.B);
+  a.M1 = reinterpret_cast<uint32_t*>(take(R * 4));
+  a.M2 = reinterpret_cast<uint32_t*>(take(R * 4));
 }
 
 cudaError_t launch_rows_pack(const RowsArgs& a, cudaStream_t s) {
@@ -984,9 +1183,29 @@ cudaError_t launch_rows_forward(const RowsArgs& a, cudaStream_t s, int* launches
 
 // adjoint: B1, B2 and the three weight-gradient GEMMs (one launch)
 cudaError_t launch_rows_backward(const RowsArgs& a, cudaStream_t s, int* launches) {
-  RCK(rows::gemm_launch<rows::B1>(a, s));
-  RCK(rows::gemm_launch<rows::B2>(a, s));
   const int sms = rows::sm_count();
+  bool fused = false;
+#define X(DP_, WP_)                                                                               \
+  if (a.Dp == DP_ && a.Wp == WP_) {   /* B1 + B2 fused: one CTA per SM over the steps */          \
+    constexpr int KM_ = DP_ > WP_ ? DP_ : WP_;                                                     \
+    const size_t smb = 2 * (size_t)DP_ * WP_ * 2 + 2 * (size_t)WP_ * WP_ * 2 + 2 * 128 * (size_t)KM_ * 2 + \
+                       64 * (size_t)(WP_ + 4) * 4;                                                 \
+    RCK(cudaFuncSetAttribute(rows::k_rows_b12_t<DP_, WP_>,                                         \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));              \
+    int g = sms / a.N;                                                                             \
+    const int nt = (int)((a.B + 127) / 128);                                                       \
+    if (g > nt) g = nt;                                                                            \
+    if (g < 1) g = 1;                                                                              \
+    rows::k_rows_b12_t<DP_, WP_><<<dim3((unsigned)g, (unsigned)a.N), rows::RT, smb, s>>>(a);       \
+    RCK(cudaGetLastError());                                                                       \
+    fused = true;                                                                                  \
+  }
+  BSDE_ROWS_SHAPES(X)
+#undef X
+  if (!fused) {
+    RCK(rows::gemm_launch<rows::B1>(a, s));
+    RCK(rows::gemm_launch<rows::B2>(a, s));
+  }
 #define X(DP_, WP_)                                                                               \
   if (a.Dp == DP_ && a.Wp == WP_) {   /* compile-time shapes: 2 CTAs per SM, one wave */          \
     int sp = (int)((2LL * sms) / (3LL * a.N));                                                     \
@@ -1000,7 +1219,7 @@ cudaError_t launch_rows_backward(const RowsArgs& a, cudaStream_t s, int* launche
     rows::k_rows_tn_t<DP_, WP_><<<dim3((unsigned)((a.B + rp - 1) / rp), 3, (unsigned)a.N),         \
                                   rows::RT, sm2, s>>>(a, rp);                                      \
     RCK(cudaGetLastError());                                                                       \
-    if (launches) *launches += 3;                                                                  \
+    if (launches) *launches += fused ? 2 : 3;                                                      \
     return cudaSuccess;                                                                            \
   }
   BSDE_ROWS_SHAPES(X)
