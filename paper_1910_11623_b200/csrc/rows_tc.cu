@@ -555,6 +555,217 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ fused forward F1 + F2
+// Compile-time shapes: one CTA per SM walks the 128-row tiles of step n = blockIdx.y
+// with W̃1 and W̃2 (hi / lo) resident, the next tile's X̃ rows in flight:
+//   G1  A1 = X̃ W̃1ᵀ          E1  H1 = ReLU(A1) -> H1 (fp32, for dW̃2 and F3), the G2
+//                                 operand (bf16 hi / lo), mask 1[A1 > 0]; H1 stays in
+//                                 the registers of its TMEM lane for E2
+//   G2  A2 = H1 W̃2ᵀ          E2  H2 = H1 + ReLU(A2) -> H2, mask 1[A2 > 0]
+// H1 is not read back from memory (F2 read it twice).
+template <int DP, int WP>
+__global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
+  constexpr int G4N = DP / 4, U = (128 * G4N + RT - 1) / RT, LDT = WP + 4, NCH8 = WP / 16;
+  constexpr int KM = DP > WP ? DP : WP;
+  constexpr uint32_t MB1 = (uint32_t)WP * DP * 2, MB2 = (uint32_t)WP * WP * 2, AB = 128u * KM * 2;
+  constexpr uint32_t WB = 2u * (WP * DP + WP * WP + DP * WP);
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bars[2];   // 0 weights, 1 MMA
+  __shared__ uint32_t tslot;
+  __shared__ uint32_t mk[2][128][4];          // mask words per column half (disjoint bits)
+  uint8_t* w1h = sm;
+  uint8_t* w1l = sm + MB1;
+  uint8_t* w2h = sm + 2 * MB1;
+  uint8_t* w2l = w2h + MB2;
+  uint8_t* ahi = w2l + MB2;
+  uint8_t* alo = ahi + AB;
+  float* stile = reinterpret_cast<float*>(alo + AB);   // [64 × LDT] half tile
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int n = blockIdx.y;
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tslot, 128);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tm = tslot;
+  if (t == 0) {   // step n's W̃1 and W̃2 (hi, lo)
+    const uint8_t* wsrc = a.wimg + (size_t)n * 2 * WB;
+    const uint32_t o2 = MB1;
+    mbar_expect_tx(&bars[0], 2 * (MB1 + MB2));
+    for (uint32_t o = 0; o < MB1; o += 16384u) {
+      bulk_g2s(w1h + o, wsrc + o, min(16384u, MB1 - o), &bars[0]);
+      bulk_g2s(w1l + o, wsrc + WB + o, min(16384u, MB1 - o), &bars[0]);
+    }
+    for (uint32_t o = 0; o < MB2; o += 16384u) {
+      bulk_g2s(w2h + o, wsrc + o2 + o, min(16384u, MB2 - o), &bars[0]);
+      bulk_g2s(w2l + o, wsrc + WB + o2 + o, min(16384u, MB2 - o), &bars[0]);
+    }
+  }
+  const int ntiles = (int)((a.B + 127) / 128);
+  const int q = warp & 3, h = warp >> 2, rr = 32 * q + lane;
+  const uint32_t lb = tm + ((uint32_t)(32 * q) << 16);
+  const int cb = h * (WP / 2);
+  constexpr uint32_t idesc = idesc_bf16(128, WP, false, false);
+  const bool store = !a.eval;
+  float4 v[U];
+  auto load = [&](int tile) {   // X̃ rows of `tile`, all loads in flight
+    const int64_t i0 = (int64_t)tile * 128;
+    const float* base = a.XT + ((size_t)n * a.B + i0) * DP;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = t + u * RT;
+      int r, c;
+      slot_rc<DP>(e, r, c);
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < 128 * G4N && i0 + r < a.B) v[u] = __ldg(reinterpret_cast<const float4*>(base + r * DP + c));
+    }
+  };
+  // half-tile rows -> dst (coalesced), and the mask words of the rows
+  auto out_rows = [&](int64_t i0, int hf, float* dst, uint32_t* mdst) {
+    const int c4 = 4 * lane;
+#pragma unroll 1
+    for (int r = warp; r < 64; r += RT / 32) {
+      const int64_t m = i0 + 64 * hf + r;
+      if (m >= a.B) break;
+      const size_t row = (size_t)n * a.B + m;
+      if (c4 < WP)
+        *reinterpret_cast<float4*>(dst + row * WP + c4) = *reinterpret_cast<const float4*>(stile + r * LDT + c4);
+      if (store && lane < 4) mdst[row * 4 + lane] = mk[0][64 * hf + r][lane] | mk[1][64 * hf + r][lane];
+    }
+  };
+  float h1[NCH8 * 8];   // H1 of this thread's row and column half (E1 -> E2)
+  uint32_t mph = 0;
+  bool first = true;
+  if ((int)blockIdx.x < ntiles) load(blockIdx.x);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i0 = (int64_t)tile * 128;
+    // X̃ -> bf16 hi / lo A image (K = DP)
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = t + u * RT;
+      if (e >= 128 * G4N) break;
+      int r, c;
+      slot_rc<DP>(e, r, c);
+      uint2 hi, lo;
+      split4(v[u], hi, lo);
+      *reinterpret_cast<uint2*>(ahi + ioff(r, c, DP)) = hi;
+      *reinterpret_cast<uint2*>(alo + ioff(r, c, DP)) = lo;
+    }
+    if (tile + (int)gridDim.x < ntiles) load(tile + gridDim.x);   // in flight until the next tile
+    fence_async_smem();
+    tc_before();
+    __syncthreads();
+    if (t == 0) {   // G1: A1 = X̃ W̃1ᵀ
+      tc_after();
+      if (first) mbar_wait(&bars[0], 0);
+      const Opnd Ah = kmaj(ahi, DP), Al = kmaj(alo, DP), Wh = kmaj(w1h, DP), Wl = kmaj(w1l, DP);
+      gemm(tm, Ah, Wh, DP / 16, idesc, false);
+      gemm(tm, Ah, Wl, DP / 16, idesc, true);
+      gemm(tm, Al, Wh, DP / 16, idesc, true);
+      mma_commit(&bars[1]);
+    }
+    first = false;
+    mbar_wait(&bars[1], mph);
+    mph ^= 1;
+    tc_after();
+    // ---- E1
+#pragma unroll 1
+    for (int hf = 0; hf < 2; ++hf) {
+      if ((q >> 1) == hf) {
+        uint32_t r8[NCH8][8];
+#pragma unroll
+        for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
+        tmem_ld_wait();
+        const int rl = 32 * (q & 1) + lane;
+        uint32_t bits[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int jj = 0; jj < NCH8; ++jj) {
+          reg_fence8(r8[jj]);
+          const int c0 = cb + 8 * jj;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float x = __uint_as_float(r8[jj][j]);
+            h1[8 * jj + j] = fmaxf(x, 0.0f);
+            bits[j & 3] |= (x > 0.0f ? 1u : 0u) << ((c0 + j) >> 2);
+          }
+          const float* f = h1 + 8 * jj;
+          float* sp = stile + rl * LDT + c0;
+          *reinterpret_cast<float4*>(sp) = make_float4(f[0], f[1], f[2], f[3]);
+          *reinterpret_cast<float4*>(sp + 4) = make_float4(f[4], f[5], f[6], f[7]);
+          uint2 h0, l0, hh1, l1;
+          split4(make_float4(f[0], f[1], f[2], f[3]), h0, l0);
+          split4(make_float4(f[4], f[5], f[6], f[7]), hh1, l1);
+          const uint32_t o = ioff(rr, c0, WP);
+          *reinterpret_cast<uint4*>(ahi + o) = make_uint4(h0.x, h0.y, hh1.x, hh1.y);
+          *reinterpret_cast<uint4*>(alo + o) = make_uint4(l0.x, l0.y, l1.x, l1.y);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mk[h][rr][e] = bits[e];
+      }
+      __syncthreads();
+      out_rows(i0, hf, a.H1, a.M1);
+      __syncthreads();
+    }
+    fence_async_smem();
+    tc_before();
+    __syncthreads();
+    if (t == 0) {   // G2: A2 = H1 W̃2ᵀ
+      tc_after();
+      const Opnd Ah = kmaj(ahi, WP), Al = kmaj(alo, WP), Wh = kmaj(w2h, WP), Wl = kmaj(w2l, WP);
+      gemm(tm, Ah, Wh, WP / 16, idesc, false);
+      gemm(tm, Ah, Wl, WP / 16, idesc, true);
+      gemm(tm, Al, Wh, WP / 16, idesc, true);
+      mma_commit(&bars[1]);
+    }
+    mbar_wait(&bars[1], mph);
+    mph ^= 1;
+    tc_after();
+    // ---- E2
+#pragma unroll 1
+    for (int hf = 0; hf < 2; ++hf) {
+      if ((q >> 1) == hf) {
+        uint32_t r8[NCH8][8];
+#pragma unroll
+        for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
+        tmem_ld_wait();
+        const int rl = 32 * (q & 1) + lane;
+        uint32_t bits[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int jj = 0; jj < NCH8; ++jj) {
+          reg_fence8(r8[jj]);
+          const int c0 = cb + 8 * jj;
+          float f[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float x = __uint_as_float(r8[jj][j]);
+            f[j] = h1[8 * jj + j] + fmaxf(x, 0.0f);
+            bits[j & 3] |= (x > 0.0f ? 1u : 0u) << ((c0 + j) >> 2);
+          }
+          float* sp = stile + rl * LDT + c0;
+          *reinterpret_cast<float4*>(sp) = make_float4(f[0], f[1], f[2], f[3]);
+          *reinterpret_cast<float4*>(sp + 4) = make_float4(f[4], f[5], f[6], f[7]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mk[h][rr][e] = bits[e];
+      }
+      __syncthreads();
+      out_rows(i0, hf, a.H2, a.M2);
+      __syncthreads();
+    }
+    tc_before();
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_after();
+    tmem_dealloc(tm, 128);
+  }
+}
+
 // ------------------------------------------------------------------ fused adjoint B1 + B2
 // Compile-time shapes: one CTA per SM walks the 128-row tiles of step n = blockIdx.y
 // with the step's W̃3 and W̃2 images (hi / lo) resident, the next tile's G rows in
@@ -1172,12 +1383,32 @@ cudaError_t launch_rows_pack(const RowsArgs& a, cudaStream_t s) {
 cudaError_t launch_rows_forward(const RowsArgs& a, cudaStream_t s, int* launches) {
   rows::k_rows_paths<<<(unsigned)((a.B * 32 + 255) / 256), 256, 0, s>>>(a);
   RCK(cudaGetLastError());
-  RCK(rows::gemm_launch<rows::F1>(a, s));
-  RCK(rows::gemm_launch<rows::F2>(a, s));
+  bool fused = false;
+#define X(DP_, WP_)                                                                               \
+  if (a.Dp == DP_ && a.Wp == WP_) {   /* F1 + F2 fused: one CTA per SM over the steps */          \
+    constexpr int KM_ = DP_ > WP_ ? DP_ : WP_;                                                     \
+    const size_t smf = 2 * (size_t)WP_ * DP_ * 2 + 2 * (size_t)WP_ * WP_ * 2 + 2 * 128 * (size_t)KM_ * 2 + \
+                       64 * (size_t)(WP_ + 4) * 4;                                                 \
+    RCK(cudaFuncSetAttribute(rows::k_rows_f12_t<DP_, WP_>,                                         \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf));              \
+    int g = rows::sm_count() / a.N;                                                                \
+    const int nt = (int)((a.B + 127) / 128);                                                       \
+    if (g > nt) g = nt;                                                                            \
+    if (g < 1) g = 1;                                                                              \
+    rows::k_rows_f12_t<DP_, WP_><<<dim3((unsigned)g, (unsigned)a.N), rows::RT, smf, s>>>(a);       \
+    RCK(cudaGetLastError());                                                                       \
+    fused = true;                                                                                  \
+  }
+  BSDE_ROWS_SHAPES(X)
+#undef X
+  if (!fused) {
+    RCK(rows::gemm_launch<rows::F1>(a, s));
+    RCK(rows::gemm_launch<rows::F2>(a, s));
+  }
   RCK(rows::gemm_launch<rows::F3>(a, s));
   rows::k_rows_y<<<(unsigned)((a.B + 255) / 256), 256, 0, s>>>(a);
   RCK(cudaGetLastError());
-  if (launches) *launches += 5;
+  if (launches) *launches += fused ? 4 : 5;
   return cudaSuccess;
 }
 

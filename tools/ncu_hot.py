@@ -7,9 +7,10 @@ import sys
 from collections import Counter
 
 rows = list(csv.reader(open(sys.argv[1])))
-hdr = rows[1]
+h0 = next(i for i, r in enumerate(rows) if "Source" in r and "Address" in r)
+hdr = rows[h0]
 ix = {h: i for i, h in enumerate(hdr)}
-data = [r for r in rows[2:] if len(r) == len(hdr)]
+data = [r for r in rows[h0 + 1:] if len(r) == len(hdr) and r[0] != "Address"]
 tot = sum(int(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in data)
 stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 byop = Counter()
