@@ -18,8 +18,12 @@
 //   Y      per path: Y_{n+1} = Y_n - f Δt + Z·ΔW (Eq. 5, R2), R = Y_N - g(X_N), the loss
 //          (Eq. 6 terminal term), ā_N (times P_N), dY0
 //   B1     dH2 = dZ W̃3 with dZ = ā_{n+1} G formed while staging the operand;
-//          dA2 = dH2 ⊙ 1[A2 > 0] (A2 > 0 <=> H2 > H1)
+//          dA2 = dH2 ⊙ 1[A2 > 0]
 //   B2     dH1 = dH2 + dA2 W̃2, dA1 = dH1 ⊙ 1[A1 > 0]
+// For the built shapes F1 + F2 and B1 + B2 are fused kernels (k_rows_f12_t,
+// k_rows_b12_t): the masks 1[A1 > 0], 1[A2 > 0] are taken from the accumulators and
+// stored as bit words; the unfused B1 / B2 (runtime shapes) test H2 > H1 and H1 > 0,
+// which equal them except where ReLU(A2) is below half an ulp of H1.
 //   TN     dW̃1 = Σ_m dA1ᵀ X̃, dW̃2 = Σ_m dA2ᵀ H1, dW̃3 = Σ_m dZᵀ H2 (the constant-1
 //          columns give the bias gradients), split over row ranges, fp32 atomics
 // The biases are folded into the weight images (column d of W̃1, column w of W̃2, W̃3;
