@@ -1,7 +1,10 @@
 """DRAM traffic per launch of each kernel in an `ncu --set full` report, written
 to profiles/traffic.json for bench.py's roofline "traffic" field.
 
-    python tools/ncu_traffic.py gpurun_out/prof.ncu-rep cfg5_allen_cahn_scaleout [profiles/traffic.json]
+    python tools/ncu_traffic.py gpurun_out/prof.ncu-rep cfg5_allen_cahn_scaleout [source-label] [profiles/traffic.json]
+
+Entries of other kernels already in the file for the workload are kept; `source-label`
+(default: the report's file name) names the committed summary of the capture.
 """
 import csv
 import io
@@ -12,7 +15,7 @@ import subprocess
 import sys
 
 
-def main(rep, workload, out="profiles/traffic.json"):
+def main(rep, workload, label=None, out="profiles/traffic.json"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -30,8 +33,9 @@ def main(rep, workload, out="profiles/traffic.json"):
             tot += float(d[i].replace(",", "")) * scale.get(units[i], 1)
         res.setdefault(key, []).append(tot)
     db = json.load(open(out)) if os.path.exists(out) else {}
-    db[workload] = {k: {"bytes_per_launch": sum(v) / len(v), "source": os.path.basename(rep)}
-                    for k, v in res.items()}
+    entry = db.setdefault(workload, {})
+    for k, v in res.items():
+        entry[k] = {"bytes_per_launch": sum(v) / len(v), "source": label or os.path.basename(rep)}
     json.dump(db, open(out, "w"), indent=1)
     print(json.dumps(db[workload], indent=1))
 
