@@ -303,6 +303,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
         tmem_wait_st();
         tc_before();
       };
+      // chunks [I0, I1) of X̃ -> the G1 operand without waiting for the stores: a chunk
+      // of X_{n+1} is final once its two Philox blocks are in (chunk i: blocks 2i, 2i+1),
+      // and the operand columns are free once G1 of step n has completed (before E1), so
+      // the stores are spread over the step and one tcgen05.wait::st in E3 covers them
+      auto put_chunks = [&](auto i0c, auto i1c) {
+        constexpr int I0 = decltype(i0c)::value, I1 = decltype(i1c)::value;
+#pragma unroll
+        for (int i = I0; i < I1; ++i)
+          if (chunk_lt3(g, i, NCD)) tmem_st4(xT + 4u * chunk(i), xchunk(i));
+      };
+      constexpr int C1 = S1 / 2, C2 = S2 / 2;   // chunks final after slice 1 / slice 2
       // Y_{n+1} (and P_{n+1}) from the E3 partial sums of step n
       auto finish_y = [&](int n) {
         float cz = 0.f, z2 = 0.f;
@@ -401,6 +412,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
           for (int k = 0; k < NS; ++k)
             if (i0 + k < NS && chunk_lt3(g, i0 + k, NCW)) tmem_ld8_nowait(acc + 8u * chunk(i0 + k), r[k]);
           tmem_ld_wait();
+          if (s < 64) BSDE_STAMP(clk, s * 16 + 15);
 #pragma unroll
           for (int k = 0; k < NS; ++k) {
             if (i0 + k >= NS || !chunk_lt3(g, i0 + k, NCW)) continue;
@@ -415,9 +427,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
         tc_before();
         named_arrive(kBarE1, kFwdThreads);
         if (g == 0 && n > 0) finish_y(n - 1);   // E3 partials of step n-1 are complete
+        if (n + 1 < N) put_chunks(Int<0>{}, Int<C1>{});
         if (s < 64) BSDE_STAMP(clk, s * 16 + 3);
         // ---- slice 2 (behind G2); E2: H2 = H1 + ReLU(A2) in bf16x2 arithmetic (R17)
         slice(Int<S1>{}, Int<S2>{});
+        if (n + 1 < N) put_chunks(Int<C1>{}, Int<C2>{});
         if (s < 64) BSDE_STAMP(clk, s * 16 + 4);
         mbar_wait(bg, gph);
         gph ^= 1;
@@ -461,15 +475,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
         if (s < 64) BSDE_STAMP(clk, s * 16 + 8);
         {
           float cz[2] = {0.f, 0.f}, z2[2] = {0.f, 0.f};
+          constexpr int RZ = NS;   // every chunk's load in flight, one wait
 #pragma unroll
-          for (int i0 = 0; i0 < NS; i0 += 3) {
-            uint32_t r[3][8];
+          for (int i0 = 0; i0 < NS; i0 += RZ) {
+            uint32_t r[RZ][8];
 #pragma unroll
-            for (int k = 0; k < 3; ++k)
+            for (int k = 0; k < RZ; ++k)
               if (i0 + k < NS && col_lt3(g, i0 + k, 0, D)) tmem_ld8_nowait(acc + 8u * chunk(i0 + k), r[k]);
             tmem_ld_wait();
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
+            for (int k = 0; k < RZ; ++k) {
               const int i = i0 + k;
               if (i >= NS || !col_lt3(g, i, 0, D)) continue;
               reg_fence8(r[k]);
@@ -485,12 +500,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
                 }
             }
           }
+          if (s < 64) BSDE_STAMP(clk, s * 16 + 10);
           part[(0 * G + g) * 128 + row] = cz[0] + cz[1];
           part[(1 * G + g) * 128 + row] = z2[0] + z2[1];
         }
         tc_before();
-        if (n + 1 < N) {
-          put_x();   // X̃_{n+1}: G1 of step n has completed, its operand columns are free
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 11);
+        if (n + 1 < N) {   // the rest of X̃_{n+1}; G1 of step n+1 may start
+          put_chunks(Int<C2>{}, Int<NS>{});
+          tmem_wait_st();
+          tc_before();
           named_arrive(kBarX, kFwdThreads);
         }
         if (s < 64) BSDE_STAMP(clk, s * 16 + 9);

@@ -37,6 +37,10 @@ for which, name in ((0, "fwd (per step)"), (1, "bwd (per item)")):
         print("  worker: S1 %d  waitG1 %d  E1 %d  S2 %d  waitG2 %d  E2 %d  S3 %d  waitG3 %d  E3 %d" % tuple(d))
         print("  control (from worker step start): B_X %.0f  B_E1 %.0f  B_E2 %.0f"
               % tuple((p[:, j] - p[:, 0]).mean() for j in (12, 13, 14)))
+        if p[:, 10].any():
+            print("  E1 loads %.0f | E3: loads+sums %.0f  part %.0f  X~ put %.0f"
+                  % ((p[:, 15] - p[:, 2]).mean(), (p[:, 10] - p[:, 8]).mean(), (p[:, 11] - p[:, 10]).mean(),
+                     (p[:, 9] - p[:, 11]).mean()))
         continue
     lim = 12
     npts = max(int(np.max(np.nonzero(r[:lim])[0])) + 1 for r in rows)
