@@ -87,6 +87,41 @@ def test_tc32_full_size_cfg2():
     compare_grads(s.get_grads(), ref["grad"], wl.d, wl.w, wl.N, TOL, ref["slack"])
 
 
+def test_tc32_full_size_cfg4():
+    """Config 4's finest level at full size (65 536 paths, N = 80: 5.2 M rows) on tc32:
+    (a) in bench_multilevel's launch configuration, residuals of sampled paths against
+    the oracle path by path and the loss as the mean of all device residuals; (b) the
+    gradient of one 1/64 shard of the same global batch (fake world: paths
+    [17·1024, 18·1024), 1/B_global normalisation) against the oracle on those paths."""
+    wl = CONFIGS["cfg4_hjb_multilevel"].with_(N=80)
+    s = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr, kernel="auto")
+    assert s.family == "tc32"
+    p = s.get_params()
+    p[1:] += (0.02 * np.random.default_rng(9).standard_normal(p.size - 1)).astype(np.float32)
+    s.set_params(p)
+    s.iteration = 5
+    loss = s.compute_grad()
+    assert np.isfinite(loss) and np.all(np.isfinite(s.get_grads()))
+    idx = np.sort(np.random.default_rng(4).choice(wl.batch, 48, replace=False))
+    ref = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, p, 0, 5, idx, wl.batch,
+                           want_grad=False)
+    R = np.array([s.debug_residuals(int(i), 1)[0] for i in idx])
+    assert np.max(np.abs(R - ref["R"])) <= TOL * np.max(np.abs(ref["R"]))
+    Rall = s.debug_residuals(0, wl.batch).astype(np.float64)
+    assert abs(np.mean(Rall ** 2) - loss) <= 1e-5 * loss
+    s.close()
+    world, rank = 64, 17
+    sh = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr, world=world, rank=rank)
+    sh.set_params(p)
+    sh.iteration = 5
+    ls = sh.compute_grad()
+    m0 = rank * (wl.batch // world)
+    ref = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, p, 0, 5,
+                           np.arange(m0, m0 + wl.batch // world), wl.batch, kink_band=BAND)
+    assert abs(ls - ref["loss"]) <= TOL * ref["loss"], (ls, ref["loss"])
+    compare_grads(sh.get_grads(), ref["grad"], wl.d, wl.w, wl.N, TOL, ref["slack"])
+
+
 def test_tc32_matches_simt_kernels():
     """Same parameters and paths on the FFMA kernels and the bf16x3 tensor-core rows:
     losses to 1e-5, gradients within the parity bound of each other."""

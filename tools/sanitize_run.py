@@ -19,12 +19,22 @@ if which in ("all", "simt"):
 if which in ("all", "tc"):
     runs += [("allen_cahn", 100, 110, 2, 300, dict(precision="bf16")),
              ("allen_cahn", 100, 110, 2, 300, dict(precision="bf16", deterministic=True))]
+if which in ("all", "tc32"):
+    runs += [("hjb", 100, 110, 2, 300, dict(kernel="tc")), ("hjb", 37, 45, 3, 200, dict(kernel="tc")),
+             ("black_scholes", 100, 110, 2, 130, dict(kernel="tc", x0=1.0))]
+if which in ("all", "fused"):
+    runs += [("allen_cahn", 100, 110, 2, 300, dict(precision="bf16", fused_opt=True))]
 if which in ("all", "shared"):
     runs += [("black_scholes", 16, 32, 3, 64, dict(formulation="shared", layers=3, x0=0.5)),
              ("hjb", 16, 32, 3, 64, dict(formulation="shared", layers=3, arch="nais"))]
 for prob, d, w, N, B, kw in runs:
-    kern = "simt" if kw.get("precision", "fp32") == "fp32" and kw.get("formulation") != "shared" else "auto"
+    kw = dict(kw)
+    fused = kw.pop("fused_opt", False)
+    kern = kw.pop("kernel", None) or ("simt" if kw.get("precision", "fp32") == "fp32"
+                                      and kw.get("formulation") != "shared" else "auto")
     s = BSDE(prob, d, N, 1.0, w, B, kernel=kern, use_graph=False, **kw)
+    if fused:
+        s.enable_fused_optimizer()
     for _ in range(2):
         s.train_step()
     s.eval_loss(1, B)
