@@ -430,6 +430,22 @@ def main():
                             "synchronised every step; the step's inputs are Philox counters "
                             "held on the device (no host input data exists, R8)"},
         }
+        if family in ("tc", "tc32") and wl.formulation == "per_step":
+            # the forward's other bound: the Philox4x32-10 + Box-Muller increments, 1 Philox
+            # block per 4 normals, ceil(d/4) per path and (fine) step, against the
+            # standalone generator's measured rate (profiles/r01_microbench.md: 0.96
+            # lane-Philox per cycle per SM with the MUFU Box-Muller) at this run's clock
+            blocks = B_local * wl.N * ((wl.d + 3) // 4)
+            rng_ach = blocks / (phase["fwd"] * 1e-3)
+            mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
+            rng_peak = 0.96 * 148 * mhz * 1e6
+            line["rng_roofline"] = {
+                "kernel": "bsde_fwd", "bound": "alu", "unit": "Philox4x32-10 blocks/s",
+                "achieved": rng_ach, "peak": rng_peak, "frac": rng_ach / rng_peak,
+                "peak_source": "0.96 blocks/cycle/SM (Philox + MUFU Box-Muller, standalone, "
+                               "profiles/r01_microbench.md) x 148 SM x median SM clock of the run",
+                "note": "the forward kernel also runs the three chain epilogues between its "
+                        "random-number slices (DESIGN §6)"}
         if wl.name in PAPER_MINUTES:
             # the paper's own timing of this workload: context only
             line["paper_context"] = {
