@@ -68,6 +68,8 @@ struct RowsArgs {
   float dt, sqrt_dt_f, lam, x0, inv_B;
   int cpl;                             // coupled paths: fine steps per step
   int64_t B, m0;                       // local paths (rows per step), first global path
+  int64_t Bs;                          // row stride per step of the [N][Bs][·] row buffers: B, or
+                                       // B rounded up to 128-row tiles for the tile-image formats
   uint32_t k0, k1;
   int eval;
   uint32_t eval_it;

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(256) k_rows_paths(RowsArgs a) {
         xv[e] = c < d ? X[e] : (c == d ? 1.0f : 0.0f);
         gv[e] = c < d ? dw[e] : 0.0f;
       }
-      const size_t o = ((size_t)n * a.B + m) * Dp + 4 * q;
+      const size_t o = ((size_t)n * a.Bs + m) * Dp + 4 * q;
       *reinterpret_cast<float4*>(a.XT + o) = make_float4(xv[0], xv[1], xv[2], xv[3]);
       *reinterpret_cast<float4*>(a.GW + o) = make_float4(gv[0], gv[1], gv[2], gv[3]);
     }
@@ -162,6 +162,18 @@ __global__ void __launch_bounds__(256) k_rows_paths(RowsArgs a) {
     if (4 * q + e < d) s = fmaf(X[e], X[e], s);
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) a.xn2[m] = s;
+}
+
+// ------------------------------------------------------------------ tile images
+// Compile-time shapes keep the row buffers that only feed GEMM operands as bf16 hi / lo
+// operand images, per (step n, 128-row tile): [hi 128×C | lo 128×C] in the core-matrix
+// layout ioff(r, c, C) (tc_common.cuh), the bytes of the fp32 rows they replace.  The
+// same bytes are a K-major A operand of a 128-row tile (F3 reads H2 so) and, half a
+// tile at a time, an MN-major operand over 64 rows (the weight-gradient kernel), so no
+// consumer converts anything.  X̃, H1, H2, dA1, dA2 and dZ = ā G are images; ΔW / G
+// stays fp32 rows (F3 rewrites it, B12 scales it).  Rows past B are zero in every image.
+__device__ __forceinline__ uint8_t* tile_img(const float* buf, const RowsArgs& a, int n, int64_t i0, int C) {
+  return reinterpret_cast<uint8_t*>(const_cast<float*>(buf) + ((size_t)n * a.Bs + (size_t)i0) * C);
 }
 
 // ------------------------------------------------------------------ row GEMMs
@@ -211,7 +223,7 @@ __global__ void __launch_bounds__(RT, 1) k_rows_gemm(RowsArgs a) {
     const int64_t i0 = (int64_t)tile * 128;
     const uint32_t rows = (uint32_t)(a.B - i0 < 128 ? a.B - i0 : 128);
     const uint32_t bytes = rows * K * 4u;
-    const uint8_t* g = reinterpret_cast<const uint8_t*>(src + ((size_t)n * a.B + i0) * K);
+    const uint8_t* g = reinterpret_cast<const uint8_t*>(src + ((size_t)n * a.Bs + i0) * K);
     uint8_t* dst = reinterpret_cast<uint8_t*>(rawt);
     mbar_expect_tx(&bars[2], bytes);
     for (uint32_t o = 0; o < bytes; o += 16384u) bulk_g2s(dst + o, g + o, min(16384u, bytes - o), &bars[2]);
@@ -303,7 +315,7 @@ __global__ void __launch_bounds__(RT, 1) k_rows_gemm(RowsArgs a) {
     for (int r = warp; r < 128; r += RT / 32) {
       const int64_t m = i0 + r;
       if (m >= a.B) break;
-      const size_t row = (size_t)n * a.B + m;
+      const size_t row = (size_t)n * a.Bs + m;
       float4 v = lane_on ? *reinterpret_cast<const float4*>(stile + r * ldt + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
       if (OP == F1 && lane_on)
         *reinterpret_cast<float4*>(a.H1 + row * Wp + c4) =
@@ -382,7 +394,9 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
   constexpr int mat = (OP == F1) ? 0 : (OP == F2 || OP == B2) ? 1 : 2;
   constexpr bool NN = OP == B1 || OP == B2;
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[3];   // 0 weights, 1 MMA, 2 A image (F3)
+  // F3 reads H2 as the tile image F12 wrote (no conversion)
+  constexpr bool IMGA = OP == F3;
   __shared__ uint32_t tslot;
   __shared__ float srow[128];
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -400,6 +414,7 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
   if (t == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(&tslot, 128);
@@ -418,10 +433,19 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
       bulk_g2s(whi + o, wsrc + o, min(16384u, MB - o), &bars[0]);
       bulk_g2s(wlo + o, wsrc + WB + o, min(16384u, MB - o), &bars[0]);
     }
+    if (IMGA) {   // the tile's hi / lo image straight into the A operand
+      constexpr uint32_t IB = 128u * K * 2;
+      const uint8_t* g = tile_img(src, a, n, i0, K);
+      mbar_expect_tx(&bars[2], 2 * IB);
+      for (uint32_t o = 0; o < IB; o += 16384u) {
+        bulk_g2s(ahi + o, g + o, min(16384u, IB - o), &bars[2]);
+        bulk_g2s(alo + o, g + IB + o, min(16384u, IB - o), &bars[2]);
+      }
+    }
   }
   // stage A: all U float4 loads in flight, then split / store
-  {
-    const float* base = src + ((size_t)n * a.B + i0) * K;
+  if constexpr (!IMGA) {
+    const float* base = src + ((size_t)n * a.Bs + i0) * K;
     float4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -450,6 +474,7 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
   if (t == 0) {
     tc_after();
     mbar_wait(&bars[0], 0);
+    if (IMGA) mbar_wait(&bars[2], 0);
     constexpr uint32_t idesc = idesc_bf16(128, NC, false, NN);
     const Opnd Ah = kmaj(ahi, K), Al = kmaj(alo, K);
     const Opnd Wh = NN ? mnmaj(whi, NC) : kmaj(whi, K), Wl = NN ? mnmaj(wlo, NC) : kmaj(wlo, K);
@@ -484,12 +509,34 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
       }
     }
     __syncthreads();
-    // phase 2: warp w, half-tile rows w, w+8, ...; lane = columns 4·lane .. +3
+    // phase 2: warp w, half-tile rows w, w+8, ...; lane = columns 4·lane .. +3.  Rows
+    // go in batches of RB whose global inputs (H1, H2, G, dH2) are loaded together, so
+    // a warp waits one memory round trip per batch, not per row
+    constexpr int RB = 4;
 #pragma unroll 1
-    for (int r = warp; r < 64; r += RT / 32) {
-      const int64_t m = i0 + 64 * hf + r;
-      if (m >= a.B) break;
-      const size_t row = (size_t)n * a.B + m;
+    for (int r0 = warp; r0 < 64; r0 += RB * (RT / 32)) {
+      float4 pa[RB], pb[RB];
+      size_t rws[RB];
+      bool ok[RB];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const int r = r0 + k * (RT / 32);
+        const int64_t m = i0 + 64 * hf + r;
+        ok[k] = r < 64 && m < a.B;
+        rws[k] = (size_t)n * a.Bs + (size_t)(ok[k] ? m : 0);
+        pa[k] = pb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok[k] && lane_on) {
+          if (OP == F2 || OP == B1 || OP == B2) pa[k] = __ldg(reinterpret_cast<const float4*>(a.H1 + rws[k] * WP + c4));
+          if (OP == F3) pa[k] = *reinterpret_cast<const float4*>(a.GW + rws[k] * DP + c4);
+          if (OP == B1) pb[k] = __ldg(reinterpret_cast<const float4*>(a.H2 + rws[k] * WP + c4));
+          if (OP == B2) pb[k] = *reinterpret_cast<const float4*>(a.DA + rws[k] * WP + c4);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+      if (!ok[k]) continue;   // warp-uniform
+      const int r = r0 + k * (RT / 32);
+      const size_t row = rws[k];
       const float4 v = lane_on ? *reinterpret_cast<const float4*>(stile + r * LDT + c4)
                                : make_float4(0.f, 0.f, 0.f, 0.f);
       if (OP == F1 || OP == F2) {   // ReLU masks 1[A > 0] of the row for the fused adjoint
@@ -504,7 +551,7 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
         *reinterpret_cast<float4*>(a.H1 + row * WP + c4) =
             make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
       if (OP == F2 && lane_on) {   // H2 = H1 + ReLU(A2)
-        const float4 p = __ldg(reinterpret_cast<const float4*>(a.H1 + row * WP + c4));
+        const float4 p = pa[k];
         *reinterpret_cast<float4*>(a.H2 + row * WP + c4) =
             make_float4(p.x + fmaxf(v.x, 0.f), p.y + fmaxf(v.y, 0.f), p.z + fmaxf(v.z, 0.f),
                         p.w + fmaxf(v.w, 0.f));
@@ -513,7 +560,7 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
         float s1 = 0.f, s2 = 0.f;
         if (lane_on) {
           float* gp = a.GW + row * DP + c4;
-          const float4 gv = *reinterpret_cast<const float4*>(gp);
+          const float4 gv = pa[k];
           const float z[4] = {v.x, v.y, v.z, v.w};
           float g[4] = {gv.x, gv.y, gv.z, gv.w};
 #pragma unroll
@@ -534,21 +581,20 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
         if (lane == 0) *reinterpret_cast<float2*>(a.S + row * 2) = make_float2(s1, s2);
       }
       if (OP == B1 && lane_on) {   // dH2 -> DA; dA2 = dH2 ⊙ 1[A2 > 0] (H2 > H1, R15) -> DH
-        const float4 h1 = __ldg(reinterpret_cast<const float4*>(a.H1 + row * WP + c4));
-        const float4 h2 = __ldg(reinterpret_cast<const float4*>(a.H2 + row * WP + c4));
+        const float4 h1 = pa[k], h2 = pb[k];
         *reinterpret_cast<float4*>(a.DA + row * WP + c4) = v;
         *reinterpret_cast<float4*>(a.DH + row * WP + c4) =
             make_float4(h2.x > h1.x ? v.x : 0.f, h2.y > h1.y ? v.y : 0.f, h2.z > h1.z ? v.z : 0.f,
                         h2.w > h1.w ? v.w : 0.f);
       }
       if (OP == B2 && lane_on) {   // dH1 = dH2 + dA2 W̃2; dA1 = dH1 ⊙ 1[H1 > 0] -> DA
-        const float4 dh = *reinterpret_cast<const float4*>(a.DA + row * WP + c4);
-        const float4 h1 = __ldg(reinterpret_cast<const float4*>(a.H1 + row * WP + c4));
+        const float4 dh = pb[k], h1 = pa[k];
         *reinterpret_cast<float4*>(a.DA + row * WP + c4) =
             make_float4(h1.x > 0.f ? dh.x + v.x : 0.f, h1.y > 0.f ? dh.y + v.y : 0.f,
                         h1.z > 0.f ? dh.z + v.z : 0.f, h1.w > 0.f ? dh.w + v.w : 0.f);
       }
     }
+      }
     __syncthreads();
   }
   tc_before();
@@ -562,17 +608,21 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
 // ------------------------------------------------------------------ fused forward F1 + F2
 // Compile-time shapes: one CTA per SM walks the 128-row tiles of step n = blockIdx.y
 // with W̃1 and W̃2 (hi / lo) resident, the next tile's X̃ rows in flight:
-//   G1  A1 = X̃ W̃1ᵀ          E1  H1 = ReLU(A1) -> H1 (fp32, for dW̃2 and F3), the G2
-//                                 operand (bf16 hi / lo), mask 1[A1 > 0]; H1 stays in
-//                                 the registers of its TMEM lane for E2
-//   G2  A2 = H1 W̃2ᵀ          E2  H2 = H1 + ReLU(A2) -> H2, mask 1[A2 > 0]
-// H1 is not read back from memory (F2 read it twice).
+//   G1  A1 = X̃ W̃1ᵀ   (X̃ converted from the fp32 rows the path kernel wrote; its image
+//                     replaces them in place, for dW̃1)
+//   E1  H1 = ReLU(A1): the G2 operand (shared memory) and the H1 image (for dW̃2), mask
+//       1[A1 > 0]; H1 stays in the registers of its TMEM lane for E2
+//   G2  A2 = H1 W̃2ᵀ
+//   E2  H2 = H1 + ReLU(A2): the H2 image (F3's A operand, dW̃3), mask 1[A2 > 0]
+// Thread (lane quadrant q, column half h) owns row 32q + lane and writes its half row of
+// each image as 16-byte chunks straight to memory (8 consecutive rows per 128 bytes).
 template <int DP, int WP>
 __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
-  constexpr int G4N = DP / 4, U = (128 * G4N + RT - 1) / RT, LDT = WP + 4, NCH8 = WP / 16;
+  constexpr int G4N = DP / 4, U = (128 * G4N + RT - 1) / RT, NCH8 = WP / 16;
   constexpr int KM = DP > WP ? DP : WP;
   constexpr uint32_t MB1 = (uint32_t)WP * DP * 2, MB2 = (uint32_t)WP * WP * 2, AB = 128u * KM * 2;
   constexpr uint32_t WB = 2u * (WP * DP + WP * WP + DP * WP);
+  constexpr uint32_t XIMG = 128u * DP * 2, HIMG = 128u * WP * 2;   // bytes of one hi (or lo) image
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ __align__(8) uint64_t bars[2];   // 0 weights, 1 MMA
   __shared__ uint32_t tslot;
@@ -583,7 +633,6 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
   uint8_t* w2l = w2h + MB2;
   uint8_t* ahi = w2l + MB2;
   uint8_t* alo = ahi + AB;
-  float* stile = reinterpret_cast<float*>(alo + AB);   // [64 × LDT] half tile
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int n = blockIdx.y;
   if (t == 0) {
@@ -616,9 +665,9 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
   constexpr uint32_t idesc = idesc_bf16(128, WP, false, false);
   const bool store = !a.eval;
   float4 v[U];
-  auto load = [&](int tile) {   // X̃ rows of `tile`, all loads in flight
+  auto load = [&](int tile) {   // X̃ rows of `tile` (fp32, from the path kernel), all loads in flight
     const int64_t i0 = (int64_t)tile * 128;
-    const float* base = a.XT + ((size_t)n * a.B + i0) * DP;
+    const float* base = a.XT + ((size_t)n * a.Bs + i0) * DP;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = t + u * RT;
@@ -628,17 +677,12 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
       if (e < 128 * G4N && i0 + r < a.B) v[u] = __ldg(reinterpret_cast<const float4*>(base + r * DP + c));
     }
   };
-  // half-tile rows -> dst (coalesced), and the mask words of the rows
-  auto out_rows = [&](int64_t i0, int hf, float* dst, uint32_t* mdst) {
-    const int c4 = 4 * lane;
+  auto out_masks = [&](int64_t i0, uint32_t* mdst) {   // 4 words per row
+    if (!store) return;
 #pragma unroll 1
-    for (int r = warp; r < 64; r += RT / 32) {
-      const int64_t m = i0 + 64 * hf + r;
-      if (m >= a.B) break;
-      const size_t row = (size_t)n * a.B + m;
-      if (c4 < WP)
-        *reinterpret_cast<float4*>(dst + row * WP + c4) = *reinterpret_cast<const float4*>(stile + r * LDT + c4);
-      if (store && lane < 4) mdst[row * 4 + lane] = mk[0][64 * hf + r][lane] | mk[1][64 * hf + r][lane];
+    for (int r = warp; r < 128; r += RT / 32) {
+      if (i0 + r >= a.B) break;
+      if (lane < 4) mdst[((size_t)n * a.Bs + i0 + r) * 4 + lane] = mk[0][r][lane] | mk[1][r][lane];
     }
   };
   float h1[NCH8 * 8];   // H1 of this thread's row and column half (E1 -> E2)
@@ -663,7 +707,7 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
     fence_async_smem();
     tc_before();
     __syncthreads();
-    if (t == 0) {   // G1: A1 = X̃ W̃1ᵀ
+    if (t == 0) {   // G1: A1 = X̃ W̃1ᵀ; the X̃ image over this tile's fp32 rows (for dW̃1)
       tc_after();
       if (first) mbar_wait(&bars[0], 0);
       const Opnd Ah = kmaj(ahi, DP), Al = kmaj(alo, DP), Wh = kmaj(w1h, DP), Wl = kmaj(w1l, DP);
@@ -671,48 +715,54 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
       gemm(tm, Ah, Wl, DP / 16, idesc, true);
       gemm(tm, Al, Wh, DP / 16, idesc, true);
       mma_commit(&bars[1]);
+      if (store) {
+        uint8_t* xd = tile_img(a.XT, a, n, i0, DP);
+        for (uint32_t o = 0; o < XIMG; o += 16384u) {
+          bulk_s2g(xd + o, ahi + o, min(16384u, XIMG - o));
+          bulk_s2g(xd + XIMG + o, alo + o, min(16384u, XIMG - o));
+        }
+        bulk_commit();
+        bulk_wait_read0();   // the images are read before E1 overwrites them
+      }
     }
     first = false;
     mbar_wait(&bars[1], mph);
     mph ^= 1;
     tc_after();
-    // ---- E1
-#pragma unroll 1
-    for (int hf = 0; hf < 2; ++hf) {
-      if ((q >> 1) == hf) {
-        uint32_t r8[NCH8][8];
+    __syncthreads();
+    // ---- E1 (every thread: its half row)
+    {
+      uint8_t* hd = tile_img(a.H1, a, n, i0, WP);
+      uint32_t r8[NCH8][8];
 #pragma unroll
-        for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
-        tmem_ld_wait();
-        const int rl = 32 * (q & 1) + lane;
-        uint32_t bits[4] = {0u, 0u, 0u, 0u};
+      for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
+      tmem_ld_wait();
+      uint32_t bits[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int jj = 0; jj < NCH8; ++jj) {
-          reg_fence8(r8[jj]);
-          const int c0 = cb + 8 * jj;
+      for (int jj = 0; jj < NCH8; ++jj) {
+        reg_fence8(r8[jj]);
+        const int c0 = cb + 8 * jj;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float x = __uint_as_float(r8[jj][j]);
-            h1[8 * jj + j] = fmaxf(x, 0.0f);
-            bits[j & 3] |= (x > 0.0f ? 1u : 0u) << ((c0 + j) >> 2);
-          }
-          const float* f = h1 + 8 * jj;
-          float* sp = stile + rl * LDT + c0;
-          *reinterpret_cast<float4*>(sp) = make_float4(f[0], f[1], f[2], f[3]);
-          *reinterpret_cast<float4*>(sp + 4) = make_float4(f[4], f[5], f[6], f[7]);
-          uint2 h0, l0, hh1, l1;
-          split4(make_float4(f[0], f[1], f[2], f[3]), h0, l0);
-          split4(make_float4(f[4], f[5], f[6], f[7]), hh1, l1);
-          const uint32_t o = ioff(rr, c0, WP);
-          *reinterpret_cast<uint4*>(ahi + o) = make_uint4(h0.x, h0.y, hh1.x, hh1.y);
-          *reinterpret_cast<uint4*>(alo + o) = make_uint4(l0.x, l0.y, l1.x, l1.y);
+        for (int j = 0; j < 8; ++j) {
+          const float x = __uint_as_float(r8[jj][j]);
+          h1[8 * jj + j] = fmaxf(x, 0.0f);
+          bits[j & 3] |= (x > 0.0f ? 1u : 0u) << ((c0 + j) >> 2);
         }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) mk[h][rr][e] = bits[e];
+        const float* f = h1 + 8 * jj;
+        uint2 h0, l0, hh1, l1;
+        split4(make_float4(f[0], f[1], f[2], f[3]), h0, l0);
+        split4(make_float4(f[4], f[5], f[6], f[7]), hh1, l1);
+        const uint32_t o = ioff(rr, c0, WP);
+        const uint4 hv = make_uint4(h0.x, h0.y, hh1.x, hh1.y), lv = make_uint4(l0.x, l0.y, l1.x, l1.y);
+        *reinterpret_cast<uint4*>(ahi + o) = hv;
+        *reinterpret_cast<uint4*>(alo + o) = lv;
+        if (store) {
+          *reinterpret_cast<uint4*>(hd + o) = hv;
+          *reinterpret_cast<uint4*>(hd + HIMG + o) = lv;
+        }
       }
-      __syncthreads();
-      out_rows(i0, hf, a.H1, a.M1);
-      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < 4; ++e) mk[h][rr][e] = bits[e];
     }
     fence_async_smem();
     tc_before();
@@ -725,43 +775,46 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
       gemm(tm, Al, Wh, WP / 16, idesc, true);
       mma_commit(&bars[1]);
     }
+    out_masks(i0, a.M1);
     mbar_wait(&bars[1], mph);
     mph ^= 1;
     tc_after();
+    __syncthreads();   // mask words read before E2 rewrites them
     // ---- E2
-#pragma unroll 1
-    for (int hf = 0; hf < 2; ++hf) {
-      if ((q >> 1) == hf) {
-        uint32_t r8[NCH8][8];
+    {
+      uint8_t* hd = tile_img(a.H2, a, n, i0, WP);
+      uint32_t r8[NCH8][8];
 #pragma unroll
-        for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
-        tmem_ld_wait();
-        const int rl = 32 * (q & 1) + lane;
-        uint32_t bits[4] = {0u, 0u, 0u, 0u};
+      for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
+      tmem_ld_wait();
+      uint32_t bits[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int jj = 0; jj < NCH8; ++jj) {
-          reg_fence8(r8[jj]);
-          const int c0 = cb + 8 * jj;
-          float f[8];
+      for (int jj = 0; jj < NCH8; ++jj) {
+        reg_fence8(r8[jj]);
+        const int c0 = cb + 8 * jj;
+        float f[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float x = __uint_as_float(r8[jj][j]);
-            f[j] = h1[8 * jj + j] + fmaxf(x, 0.0f);
-            bits[j & 3] |= (x > 0.0f ? 1u : 0u) << ((c0 + j) >> 2);
-          }
-          float* sp = stile + rl * LDT + c0;
-          *reinterpret_cast<float4*>(sp) = make_float4(f[0], f[1], f[2], f[3]);
-          *reinterpret_cast<float4*>(sp + 4) = make_float4(f[4], f[5], f[6], f[7]);
+        for (int j = 0; j < 8; ++j) {
+          const float x = __uint_as_float(r8[jj][j]);
+          f[j] = h1[8 * jj + j] + fmaxf(x, 0.0f);
+          bits[j & 3] |= (x > 0.0f ? 1u : 0u) << ((c0 + j) >> 2);
         }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) mk[h][rr][e] = bits[e];
+        uint2 h0, l0, hh1, l1;
+        split4(make_float4(f[0], f[1], f[2], f[3]), h0, l0);
+        split4(make_float4(f[4], f[5], f[6], f[7]), hh1, l1);
+        const uint32_t o = ioff(rr, c0, WP);
+        *reinterpret_cast<uint4*>(hd + o) = make_uint4(h0.x, h0.y, hh1.x, hh1.y);
+        *reinterpret_cast<uint4*>(hd + HIMG + o) = make_uint4(l0.x, l0.y, l1.x, l1.y);
       }
-      __syncthreads();
-      out_rows(i0, hf, a.H2, a.M2);
-      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < 4; ++e) mk[h][rr][e] = bits[e];
     }
     tc_before();
+    __syncthreads();
+    out_masks(i0, a.M2);
+    __syncthreads();   // mask words read before the next tile's E1
   }
+  if (t == 0) bulk_wait0();   // this CTA's image stores are complete before it retires
   tc_before();
   __syncthreads();
   if (warp == 0) {
@@ -774,18 +827,20 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
 // Compile-time shapes: one CTA per SM walks the 128-row tiles of step n = blockIdx.y
 // with the step's W̃3 and W̃2 images (hi / lo) resident, the next tile's G rows in
 // flight while the current one computes:
-//   G4  dH2 = dZ W̃3, dZ = ā_{n+1} G (staged as bf16 hi / lo; three MMA passes)
-//   E4  dA2 = dH2 ⊙ 1[A2 > 0] (mask words from F2) -> DH (fp32, for dW̃2) and, as
-//       bf16 hi / lo, the A operand of G6 (over the dZ images, which G4 has read)
+//   G4  dH2 = dZ W̃3, dZ = ā_{n+1} G (staged as bf16 hi / lo; its image replaces the
+//       tile's G rows in place, the A operand of dW̃3)
+//   E4  dA2 = dH2 ⊙ 1[A2 > 0] (mask words from F2): the dA2 image (dW̃2) and, in shared
+//       memory, the A operand of G6 (over the dZ images, which G4 has read)
 //   G6  dH1 = dH2 + dA2 W̃2 (accumulated onto dH2 in TMEM)
-//   E6  dA1 = dH1 ⊙ 1[A1 > 0] (mask words from F1) -> DA (fp32, for dW̃1)
-// dH2 never leaves the chip, and the masks replace the H1 / H2 reads of B1 / B2.
+//   E6  dA1 = dH1 ⊙ 1[A1 > 0] (mask words from F1): the dA1 image (dW̃1)
+// dH2 never leaves the chip; every thread writes its half row of the images directly.
 template <int DP, int WP>
 __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
-  constexpr int G4N = DP / 4, U = (128 * G4N + RT - 1) / RT, LDT = WP + 4, NCH8 = WP / 16;
+  constexpr int G4N = DP / 4, U = (128 * G4N + RT - 1) / RT, NCH8 = WP / 16;
   constexpr int KM = DP > WP ? DP : WP;
   constexpr uint32_t MB3 = (uint32_t)DP * WP * 2, MB2 = (uint32_t)WP * WP * 2, AB = 128u * KM * 2;
   constexpr uint32_t WB = 2u * (WP * DP + WP * WP + DP * WP);
+  constexpr uint32_t ZIMG = 128u * DP * 2, HIMG = 128u * WP * 2;
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ __align__(8) uint64_t bars[2];   // 0 weights, 1 MMA
   __shared__ uint32_t tslot;
@@ -796,7 +851,6 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
   uint8_t* w2l = w2h + MB2;
   uint8_t* ahi = w2l + MB2;
   uint8_t* alo = ahi + AB;
-  float* stile = reinterpret_cast<float*>(alo + AB);   // [64 × LDT] half tile
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int n = blockIdx.y;
   if (t == 0) {
@@ -830,7 +884,7 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
   float4 v[U];
   auto load = [&](int tile) {   // G rows of `tile`, all loads in flight
     const int64_t i0 = (int64_t)tile * 128;
-    const float* base = a.GW + ((size_t)n * a.B + i0) * DP;
+    const float* base = a.GW + ((size_t)n * a.Bs + i0) * DP;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = t + u * RT;
@@ -840,52 +894,35 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
       if (e < 128 * G4N && i0 + r < a.B) v[u] = __ldg(reinterpret_cast<const float4*>(base + r * DP + c));
     }
   };
-  // E4 / E6 on the accumulator: mask, then fp32 rows -> dst (coalesced through the
-  // half tile); E4 also writes the bf16 hi / lo operand image of G6
-  auto epilogue = [&](int64_t i0, const uint4& mk, float* dst, bool img) {
+  // E4 / E6 on the accumulator: mask, then the half row's bf16 hi / lo chunks -> the
+  // image at dst (and, for E4, the G6 operand in shared memory)
+  auto epilogue = [&](const uint4& mk, uint8_t* dst, bool smem_img) {
     const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
-#pragma unroll 1
-    for (int hf = 0; hf < 2; ++hf) {
-      if ((q >> 1) == hf) {
-        uint32_t r8[NCH8][8];
+    uint32_t r8[NCH8][8];
 #pragma unroll
-        for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
-        tmem_ld_wait();
-        const int rl = 32 * (q & 1) + lane;
+    for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
+    tmem_ld_wait();
 #pragma unroll
-        for (int jj = 0; jj < NCH8; ++jj) {
-          reg_fence8(r8[jj]);
-          const int c0 = cb + 8 * jj;
-          float f[8];
+    for (int jj = 0; jj < NCH8; ++jj) {
+      reg_fence8(r8[jj]);
+      const int c0 = cb + 8 * jj;
+      float f[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int col = c0 + j;
-            f[j] = ((mw[col & 3] >> (col >> 2)) & 1u) ? __uint_as_float(r8[jj][j]) : 0.0f;
-          }
-          float* sp = stile + rl * LDT + c0;
-          *reinterpret_cast<float4*>(sp) = make_float4(f[0], f[1], f[2], f[3]);
-          *reinterpret_cast<float4*>(sp + 4) = make_float4(f[4], f[5], f[6], f[7]);
-          if (img) {
-            uint2 h0, l0, h1, l1;
-            split4(make_float4(f[0], f[1], f[2], f[3]), h0, l0);
-            split4(make_float4(f[4], f[5], f[6], f[7]), h1, l1);
-            const uint32_t o = ioff(rr, c0, WP);
-            *reinterpret_cast<uint4*>(ahi + o) = make_uint4(h0.x, h0.y, h1.x, h1.y);
-            *reinterpret_cast<uint4*>(alo + o) = make_uint4(l0.x, l0.y, l1.x, l1.y);
-          }
-        }
+      for (int j = 0; j < 8; ++j) {
+        const int col = c0 + j;
+        f[j] = ((mw[col & 3] >> (col >> 2)) & 1u) ? __uint_as_float(r8[jj][j]) : 0.0f;
       }
-      __syncthreads();
-      const int c4 = 4 * lane;
-#pragma unroll 1
-      for (int r = warp; r < 64; r += RT / 32) {
-        const int64_t m = i0 + 64 * hf + r;
-        if (m >= a.B) break;
-        if (c4 < WP)
-          *reinterpret_cast<float4*>(dst + ((size_t)n * a.B + m) * WP + c4) =
-              *reinterpret_cast<const float4*>(stile + r * LDT + c4);
+      uint2 h0, l0, h1, l1;
+      split4(make_float4(f[0], f[1], f[2], f[3]), h0, l0);
+      split4(make_float4(f[4], f[5], f[6], f[7]), h1, l1);
+      const uint32_t o = ioff(rr, c0, WP);
+      const uint4 hv = make_uint4(h0.x, h0.y, h1.x, h1.y), lv = make_uint4(l0.x, l0.y, l1.x, l1.y);
+      if (smem_img) {
+        *reinterpret_cast<uint4*>(ahi + o) = hv;
+        *reinterpret_cast<uint4*>(alo + o) = lv;
       }
-      __syncthreads();
+      *reinterpret_cast<uint4*>(dst + o) = hv;
+      *reinterpret_cast<uint4*>(dst + HIMG + o) = lv;
     }
   };
   uint32_t mph = 0;
@@ -913,14 +950,14 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
     }
     // this thread's row masks (TMEM lane layout: row rr)
     const int64_t mrow = i0 + rr;
-    const size_t ro = ((size_t)n * a.B + (size_t)mrow) * 4;
+    const size_t ro = ((size_t)n * a.Bs + (size_t)mrow) * 4;
     const uint4 mk2 = mrow < a.B ? __ldg(reinterpret_cast<const uint4*>(a.M2 + ro)) : make_uint4(0, 0, 0, 0);
     const uint4 mk1 = mrow < a.B ? __ldg(reinterpret_cast<const uint4*>(a.M1 + ro)) : make_uint4(0, 0, 0, 0);
     if (tile + (int)gridDim.x < ntiles) load(tile + gridDim.x);   // in flight until the next tile
     fence_async_smem();
     tc_before();
     __syncthreads();
-    if (t == 0) {   // G4: dH2 = dZ W̃3
+    if (t == 0) {   // G4: dH2 = dZ W̃3; the dZ image over this tile's G rows (for dW̃3)
       tc_after();
       if (first) mbar_wait(&bars[0], 0);
       const Opnd Ah = kmaj(ahi, DP), Al = kmaj(alo, DP), Wh = mnmaj(w3h, WP), Wl = mnmaj(w3l, WP);
@@ -928,12 +965,20 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
       gemm(tm, Ah, Wl, DP / 16, idesc, true);
       gemm(tm, Al, Wh, DP / 16, idesc, true);
       mma_commit(&bars[1]);
+      uint8_t* zd = tile_img(a.GW, a, n, i0, DP);
+      for (uint32_t o = 0; o < ZIMG; o += 16384u) {
+        bulk_s2g(zd + o, ahi + o, min(16384u, ZIMG - o));
+        bulk_s2g(zd + ZIMG + o, alo + o, min(16384u, ZIMG - o));
+      }
+      bulk_commit();
+      bulk_wait_read0();   // the images are read before E4 overwrites them
     }
     first = false;
     mbar_wait(&bars[1], mph);
     mph ^= 1;
     tc_after();
-    epilogue(i0, mk2, a.DH, true);   // E4: dA2 -> DH and the G6 operand
+    __syncthreads();
+    epilogue(mk2, tile_img(a.DH, a, n, i0, WP), true);   // E4: dA2
     fence_async_smem();
     tc_before();
     __syncthreads();
@@ -948,9 +993,11 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
     mbar_wait(&bars[1], mph);
     mph ^= 1;
     tc_after();
-    epilogue(i0, mk1, a.DA, false);   // E6: dA1 -> DA
+    epilogue(mk1, tile_img(a.DA, a, n, i0, WP), false);   // E6: dA1
     tc_before();
+    __syncthreads();   // accumulator and A images read before the next tile
   }
+  if (t == 0) bulk_wait0();   // this CTA's image stores are complete before it retires
   tc_before();
   __syncthreads();
   if (warp == 0) {
@@ -970,7 +1017,7 @@ __global__ void __launch_bounds__(256) k_rows_y(RowsArgs a) {
     float Y = a.params[0], P = 1.0f;
     const bool pa = per_step_abar(a.problem) && !a.eval;
     for (int n = 0; n < a.N; ++n) {
-      const float2 s = *reinterpret_cast<const float2*>(a.S + ((size_t)n * a.B + m) * 2);
+      const float2 s = *reinterpret_cast<const float2*>(a.S + ((size_t)n * a.Bs + m) * 2);
       if (pa) {
         P *= 1.0f - a.dt * driver_dfdy(a.problem, Y);
         a.Pstore[(int64_t)n * a.B + m] = P;
@@ -1034,8 +1081,8 @@ __global__ void __launch_bounds__(RT, 1) k_rows_tn(RowsArgs a, int rows_per_cta)
     const int64_t rb = r0 + (int64_t)c * TK;
     const uint32_t rows = (uint32_t)(r1 - rb < TK ? r1 - rb : TK);
     const uint32_t ba = rows * P * 4u, bb = rows * Q * 4u;
-    const uint8_t* ga = reinterpret_cast<const uint8_t*>(srcA + ((size_t)n * a.B + rb) * P);
-    const uint8_t* gb = reinterpret_cast<const uint8_t*>(srcB + ((size_t)n * a.B + rb) * Q);
+    const uint8_t* ga = reinterpret_cast<const uint8_t*>(srcA + ((size_t)n * a.Bs + rb) * P);
+    const uint8_t* gb = reinterpret_cast<const uint8_t*>(srcB + ((size_t)n * a.Bs + rb) * Q);
     uint8_t* da = reinterpret_cast<uint8_t*>(rawA(b));
     uint8_t* db = reinterpret_cast<uint8_t*>(rawB(b));
     mbar_expect_tx(&bars[1 + b], ba + bb);
@@ -1164,8 +1211,8 @@ __device__ __forceinline__ void rows_tn_body(const RowsArgs& a, int n, int64_t r
   float4 va[UA], vb[UB];
   auto load = [&](int c) {
     const int64_t rb = r0 + (int64_t)c * TK;
-    const float* ga = srcA + ((size_t)n * a.B + rb) * P;
-    const float* gb = srcB + ((size_t)n * a.B + rb) * Q;
+    const float* ga = srcA + ((size_t)n * a.Bs + rb) * P;
+    const float* gb = srcB + ((size_t)n * a.Bs + rb) * Q;
 #pragma unroll
     for (int u = 0; u < UA; ++u) {
       const int e = t + u * RT;
@@ -1294,6 +1341,149 @@ __global__ void __launch_bounds__(RT, 2) k_rows_tn_t(RowsArgs a, int rows_per_ct
   }
 }
 
+// Weight gradients from the tile images (compile-time shapes): one CTA per SM takes an
+// equal share of the 3·N·2·tiles (which, step, 64-row half tile) units in order.  Thread
+// 0 streams the four images of a unit (A hi / lo, B hi / lo: MN-major over the 64 rows,
+// no conversion) by bulk copy into a ring of NSI stages, NSI - 1 units ahead, and issues
+// the three MMA passes of each unit straight from its stage into the TMEM accumulator of
+// the current (which, step) segment; all threads flush the segment with fp32 atomics.
+// A rows past P (M = 128) read the neighbouring bytes of the stage: their products land
+// in accumulator rows >= P, which the flush never reads.
+constexpr int NSI = 3;
+template <int WHICH>
+__device__ __forceinline__ void tn_flush_img(const RowsArgs& a, int n, uint32_t tm) {
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int d = a.d, w = a.w;
+  const int Q = WHICH == 0 ? a.Dp : a.Wp;
+  const NetDims nd{d, w};
+  float* G = a.grad + nd.step_base(n);
+  const int qd = warp & 3, hh = warp >> 2, p = 32 * qd + lane;
+  const uint32_t lb = tm + ((uint32_t)(32 * qd) << 16);
+#pragma unroll 1
+  for (int c0 = hh * (Q / 2); c0 < (hh + 1) * (Q / 2); c0 += 8) {
+    uint32_t r8[8];
+    tmem_ld8_nowait(lb + (uint32_t)c0, r8);
+    tmem_ld_wait();
+    reg_fence8(r8);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = c0 + e;
+      const float v = __uint_as_float(r8[e]);
+      if (v == 0.0f) continue;
+      int64_t off = -1;
+      if (WHICH == 0 && p < w) off = k < d ? nd.off_W1() + p * d + k : (k == d ? nd.off_b1() + p : -1);
+      if (WHICH == 1 && p < w) off = k < w ? nd.off_W2() + p * w + k : (k == w ? nd.off_b2() + p : -1);
+      if (WHICH == 2 && p < d) off = k < w ? nd.off_W3() + p * w + k : (k == w ? nd.off_b3() + p : -1);
+      if (off >= 0) atomicAdd(G + off, v);
+    }
+  }
+}
+template <int DP, int WP>
+__global__ void __launch_bounds__(RT, 1) k_rows_tn_img(RowsArgs a) {
+  constexpr int KM = DP > WP ? DP : WP;
+  constexpr uint32_t HB = 64u * KM * 2;              // one 64-row hi (or lo) image, max width
+  constexpr uint32_t STB = 4 * HB;                   // stage: A hi, A lo, B hi, B lo
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t full[NSI], mmab[NSI];
+  __shared__ uint32_t tslot;
+  const int t = threadIdx.x, warp = t >> 5;
+  const int N = a.N;
+  const int64_t nt2 = 2 * ((a.B + 127) / 128);        // 64-row units per (which, step)
+  const int64_t U = 3LL * N * nt2;
+  const int64_t u0 = blockIdx.x * U / gridDim.x, u1 = (blockIdx.x + 1) * U / gridDim.x;
+  if (t == 0) {
+    for (int i = 0; i < NSI; ++i) { mbar_init(&full[i], 1); mbar_init(&mmab[i], 1); }
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tslot, 128);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tm = tslot;
+  struct Cur { int which, n; int64_t k; };
+  auto decode = [&](int64_t u) {
+    const int64_t sgi = u / nt2;
+    Cur c;
+    c.k = u - sgi * nt2;
+    c.which = (int)(sgi / N);
+    c.n = (int)(sgi - (int64_t)c.which * N);
+    return c;
+  };
+  auto advance = [&](Cur& c) {
+    if (++c.k == nt2) { c.k = 0; if (++c.n == N) { c.n = 0; ++c.which; } }
+  };
+  auto issue_load = [&](const Cur& c, int stg) {   // thread 0
+    const int P = c.which == 2 ? DP : WP, Q = c.which == 0 ? DP : WP;
+    const float* srcA = c.which == 0 ? a.DA : c.which == 1 ? a.DH : a.GW;
+    const float* srcB = c.which == 0 ? a.XT : c.which == 1 ? a.H1 : a.H2;
+    const int64_t i0 = (c.k >> 1) * 128;
+    const uint32_t half = (uint32_t)(c.k & 1);
+    const uint8_t* ga = tile_img(srcA, a, c.n, i0, P) + half * 64u * P * 2;
+    const uint8_t* gb = tile_img(srcB, a, c.n, i0, Q) + half * 64u * Q * 2;
+    const uint32_t ba = 64u * P * 2, bb = 64u * Q * 2;   // <= 16 KB each
+    uint8_t* st = sm + stg * STB;
+    mbar_expect_tx(&full[stg], 2 * (ba + bb));
+    bulk_g2s(st, ga, ba, &full[stg]);
+    bulk_g2s(st + HB, ga + 128u * P * 2, ba, &full[stg]);
+    bulk_g2s(st + 2 * HB, gb, bb, &full[stg]);
+    bulk_g2s(st + 3 * HB, gb + 128u * Q * 2, bb, &full[stg]);
+  };
+  Cur cu = decode(u0 < U ? u0 : 0), cl = cu;
+  if (t == 0)
+    for (int i = 0; i < NSI && u0 + i < u1; ++i) { issue_load(cl, i); advance(cl); }
+  bool seg_first = true;
+  int stg = 0;
+  uint32_t sph = 0;   // ring pass parity of stage stg
+  for (int64_t u = u0, j = 0; u < u1; ++u, ++j) {
+    const int which = cu.which, n = cu.n;
+    const bool seg_end = u + 1 == u1 || cu.k + 1 == nt2;
+    if (t == 0) {
+      mbar_wait(&full[stg], sph);
+      tc_after();
+      const int P = which == 2 ? DP : WP, Q = which == 0 ? DP : WP;
+      const uint32_t idesc = idesc_bf16(128, Q, true, true);
+      uint8_t* st = sm + stg * STB;
+      const Opnd Ah = mnmaj(st, P), Al = mnmaj(st + HB, P);
+      const Opnd Bh = mnmaj(st + 2 * HB, Q), Bl = mnmaj(st + 3 * HB, Q);
+      gemm(tm, Ah, Bh, 64 / 16, idesc, !seg_first);
+      gemm(tm, Ah, Bl, 64 / 16, idesc, true);
+      gemm(tm, Al, Bh, 64 / 16, idesc, true);
+      mma_commit(&mmab[stg]);
+      // refill the stage of the previous unit once its MMAs are done (NSI - 1 ahead)
+      if (j > 0 && u - 1 + NSI < u1) {
+        const int ps = stg == 0 ? NSI - 1 : stg - 1;
+        const uint32_t pph = (stg == 0) ? (sph ^ 1u) : sph;
+        mbar_wait(&mmab[ps], pph);
+        issue_load(cl, ps);
+        advance(cl);
+      }
+    }
+    seg_first = false;
+    if (seg_end) {   // flush the (which, step) accumulator
+      // the other threads run ahead of thread 0 between flushes: they wait for this
+      // unit's commit only once it is issued, so that the parity wait cannot alias an
+      // earlier, still incomplete pass of the stage's barrier
+      __syncthreads();
+      mbar_wait(&mmab[stg], sph);
+      tc_after();
+      if (which == 0) tn_flush_img<0>(a, n, tm);
+      else if (which == 1) tn_flush_img<1>(a, n, tm);
+      else tn_flush_img<2>(a, n, tm);
+      tc_before();
+      __syncthreads();   // accumulator read before the next segment's first MMA
+      seg_first = true;
+    }
+    advance(cu);
+    if (++stg == NSI) { stg = 0; sph ^= 1u; }
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_after();
+    tmem_dealloc(tm, 128);
+  }
+}
+
 inline int pad16(int x) { return (x + 15) / 16 * 16; }
 inline int sm_count() {
   int dev = 0, sms = 148;
@@ -1340,8 +1530,19 @@ cudaError_t gemm_launch(const RowsArgs& a, cudaStream_t s) {
 
 bool rows_supported(int d, int w) { return d + 1 <= 128 && w + 1 <= 128; }
 
+// compile-time shapes use the tile-image formats (row stride per step: whole tiles)
+static bool rows_img_shape(int Dp, int Wp) {
+#define X(DP_, WP_) if (Dp == DP_ && Wp == WP_) return true;
+  BSDE_ROWS_SHAPES(X)
+#undef X
+  return false;
+}
+static int64_t rows_stride(int Dp, int Wp, int64_t B) {
+  return rows_img_shape(Dp, Wp) ? (B + 127) / 128 * 128 : B;
+}
 size_t rows_buffer_bytes(int d, int w, int N, int64_t B) {
-  const size_t Dp = rows::pad16(d + 1), Wp = rows::pad16(w + 1), R = (size_t)N * B;
+  const size_t Dp = rows::pad16(d + 1), Wp = rows::pad16(w + 1);
+  const size_t R = (size_t)N * rows_stride((int)Dp, (int)Wp, B);
   return 4 * (2 * R * Dp + 4 * R * Wp + 2 * R + B) + 2 * 16 * R + 8 * 256;
 }
 size_t rows_pack_bytes(int d, int w, int N) {
@@ -1353,8 +1554,9 @@ size_t rows_pack_bytes(int d, int w, int N) {
 void rows_carve(RowsArgs& a, void* base, int N_max) {
   a.Dp = rows::pad16(a.d + 1);
   a.Wp = rows::pad16(a.w + 1);
+  a.Bs = rows_stride(a.Dp, a.Wp, a.B);
   uint8_t* p = static_cast<uint8_t*>(base);
-  const size_t R = (size_t)N_max * a.B;
+  const size_t R = (size_t)N_max * a.Bs;
   auto take = [&](size_t floats) {
     float* f = reinterpret_cast<float*>(p);
     p += (floats * 4 + 255) / 256 * 256;
@@ -1391,8 +1593,7 @@ cudaError_t launch_rows_forward(const RowsArgs& a, cudaStream_t s, int* launches
 #define X(DP_, WP_)                                                                               \
   if (a.Dp == DP_ && a.Wp == WP_) {   /* F1 + F2 fused: one CTA per SM over the steps */          \
     constexpr int KM_ = DP_ > WP_ ? DP_ : WP_;                                                     \
-    const size_t smf = 2 * (size_t)WP_ * DP_ * 2 + 2 * (size_t)WP_ * WP_ * 2 + 2 * 128 * (size_t)KM_ * 2 + \
-                       64 * (size_t)(WP_ + 4) * 4;                                                 \
+    const size_t smf = 2 * (size_t)WP_ * DP_ * 2 + 2 * (size_t)WP_ * WP_ * 2 + 2 * 128 * (size_t)KM_ * 2; \
     RCK(cudaFuncSetAttribute(rows::k_rows_f12_t<DP_, WP_>,                                         \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf));              \
     int g = rows::sm_count() / a.N;                                                                \
@@ -1423,8 +1624,7 @@ cudaError_t launch_rows_backward(const RowsArgs& a, cudaStream_t s, int* launche
 #define X(DP_, WP_)                                                                               \
   if (a.Dp == DP_ && a.Wp == WP_) {   /* B1 + B2 fused: one CTA per SM over the steps */          \
     constexpr int KM_ = DP_ > WP_ ? DP_ : WP_;                                                     \
-    const size_t smb = 2 * (size_t)DP_ * WP_ * 2 + 2 * (size_t)WP_ * WP_ * 2 + 2 * 128 * (size_t)KM_ * 2 + \
-                       64 * (size_t)(WP_ + 4) * 4;                                                 \
+    const size_t smb = 2 * (size_t)DP_ * WP_ * 2 + 2 * (size_t)WP_ * WP_ * 2 + 2 * 128 * (size_t)KM_ * 2; \
     RCK(cudaFuncSetAttribute(rows::k_rows_b12_t<DP_, WP_>,                                         \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));              \
     int g = sms / a.N;                                                                             \
@@ -1442,17 +1642,12 @@ cudaError_t launch_rows_backward(const RowsArgs& a, cudaStream_t s, int* launche
     RCK(rows::gemm_launch<rows::B2>(a, s));
   }
 #define X(DP_, WP_)                                                                               \
-  if (a.Dp == DP_ && a.Wp == WP_) {   /* compile-time shapes: 2 CTAs per SM, one wave */          \
-    int sp = (int)((2LL * sms) / (3LL * a.N));                                                     \
-    const int64_t mx = (a.B + 255) / 256;                                                          \
-    if (sp > mx) sp = (int)mx;                                                                     \
-    if (sp < 1) sp = 1;                                                                            \
-    const int rp = (int)((a.B + sp - 1) / sp);                                                     \
-    const size_t sm2 = 2 * (size_t)rows::TK * 128 * 2 + 2 * (size_t)rows::TK * 128 * 2;           \
-    RCK(cudaFuncSetAttribute(rows::k_rows_tn_t<DP_, WP_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             (int)sm2));                                                           \
-    rows::k_rows_tn_t<DP_, WP_><<<dim3((unsigned)((a.B + rp - 1) / rp), 3, (unsigned)a.N),         \
-                                  rows::RT, sm2, s>>>(a, rp);                                      \
+  if (a.Dp == DP_ && a.Wp == WP_) {   /* compile-time shapes: tile images, one CTA per SM */      \
+    constexpr int KM_ = DP_ > WP_ ? DP_ : WP_;                                                     \
+    const size_t smt = rows::NSI * 4 * 64 * (size_t)KM_ * 2;                                      \
+    RCK(cudaFuncSetAttribute(rows::k_rows_tn_img<DP_, WP_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)smt));                                                           \
+    rows::k_rows_tn_img<DP_, WP_><<<sms, rows::RT, smt, s>>>(a);                                   \
     RCK(cudaGetLastError());                                                                       \
     if (launches) *launches += fused ? 2 : 3;                                                      \
     return cudaSuccess;                                                                            \
