@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ __align__(8) uint64_t bars[2];   // 0 weights, 1 MMA
   __shared__ uint32_t tslot;
-  __shared__ uint32_t mk[2][128][4];          // mask words per column half (disjoint bits)
+  __shared__ __align__(16) uint32_t mk[2][128][4];   // mask words per column half (disjoint bits)
   uint8_t* w1h = sm;
   uint8_t* w1l = sm + MB1;
   uint8_t* w2h = sm + 2 * MB1;
@@ -677,13 +677,13 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
       if (e < 128 * G4N && i0 + r < a.B) v[u] = __ldg(reinterpret_cast<const float4*>(base + r * DP + c));
     }
   };
-  auto out_masks = [&](int64_t i0, uint32_t* mdst) {   // 4 words per row
-    if (!store) return;
-#pragma unroll 1
-    for (int r = warp; r < 128; r += RT / 32) {
-      if (i0 + r >= a.B) break;
-      if (lane < 4) mdst[((size_t)n * a.Bs + i0 + r) * 4 + lane] = mk[0][r][lane] | mk[1][r][lane];
-    }
+  auto out_masks = [&](int64_t i0, uint32_t* mdst) {   // 4 words per row, one row per lane
+    if (!store || lane >= 16) return;
+    const int r = 16 * warp + lane;
+    if (i0 + r >= a.B) return;
+    const uint4 m0 = *reinterpret_cast<const uint4*>(mk[0][r]), m1 = *reinterpret_cast<const uint4*>(mk[1][r]);
+    *reinterpret_cast<uint4*>(mdst + ((size_t)n * a.Bs + i0 + r) * 4) =
+        make_uint4(m0.x | m1.x, m0.y | m1.y, m0.z | m1.z, m0.w | m1.w);
   };
   float h1[NCH8 * 8];   // H1 of this thread's row and column half (E1 -> E2)
   uint32_t mph = 0;
@@ -925,15 +925,24 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
       *reinterpret_cast<uint4*>(dst + HIMG + o) = lv;
     }
   };
+  // ā_{n+1} of a tile's rows (threads t < 128), loaded one tile ahead like G
+  float pab = 0.0f, ppn = 1.0f;
+  auto load_ab = [&](int tile) {
+    const int64_t m = (int64_t)tile * 128 + t;
+    if (t < 128 && m < a.B) {
+      pab = __ldg(a.abar + m);
+      ppn = per_step_abar(a.problem) ? __ldg(a.Pstore + (int64_t)n * a.B + m) : 1.0f;
+    } else {
+      pab = 0.0f;
+      ppn = 1.0f;
+    }
+  };
   uint32_t mph = 0;
   bool first = true;
-  if ((int)blockIdx.x < ntiles) load(blockIdx.x);
+  if ((int)blockIdx.x < ntiles) { load(blockIdx.x); load_ab(blockIdx.x); }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i0 = (int64_t)tile * 128;
-    if (t < 128) {
-      const int64_t m = i0 + t;
-      srow[t] = m < a.B ? abar_of(a, n, m) : 0.0f;
-    }
+    if (t < 128) srow[t] = __fdividef(pab, ppn);   // 0 past B (pab = 0)
     __syncthreads();
     // dZ = ā_{n+1} G -> bf16 hi / lo A image (K = DP)
 #pragma unroll
@@ -953,7 +962,10 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
     const size_t ro = ((size_t)n * a.Bs + (size_t)mrow) * 4;
     const uint4 mk2 = mrow < a.B ? __ldg(reinterpret_cast<const uint4*>(a.M2 + ro)) : make_uint4(0, 0, 0, 0);
     const uint4 mk1 = mrow < a.B ? __ldg(reinterpret_cast<const uint4*>(a.M1 + ro)) : make_uint4(0, 0, 0, 0);
-    if (tile + (int)gridDim.x < ntiles) load(tile + gridDim.x);   // in flight until the next tile
+    if (tile + (int)gridDim.x < ntiles) {   // in flight until the next tile
+      load(tile + gridDim.x);
+      load_ab(tile + gridDim.x);
+    }
     fence_async_smem();
     tc_before();
     __syncthreads();
