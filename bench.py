@@ -92,8 +92,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, interval_ms=100):
         self.index = index
+        self.interval_ms = interval_ms
         self.proc = None
         self.lines = []
 
@@ -101,7 +102,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -350,8 +351,15 @@ def main():
     path_steps = wl.batch * wl.N
     value = path_steps / (ms * 1e-3)
 
-    # per-phase CUDA-event timing of the same step (eager replay of the step)
+    # per-phase CUDA-event timing of the same step (eager replay of the step), with the
+    # SM clock sampled over it: the replay is short, so it usually runs above the
+    # power-capped clock of the long timed region, which is most of the gap between
+    # ms_per_step and the sum of the phases
+    pclocks = ClockSampler(local_rank if "CUDA_VISIBLE_DEVICES" not in os.environ else
+                           os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local_rank], 20)
+    pclocks.start()
     phase = s.profile_steps(max(2, min(args.steps, 5)))
+    pclk = pclocks.stop()
 
     # e2e: the public API call per step with the loss read back to the host
     barrier()
@@ -422,6 +430,9 @@ def main():
                               "frac_sustained": step_flops / (ms * 1e-3) / 1e12 / peak_sus,
                               "flop_per_path_step": ffw + fbw},
             "phase_ms": phase,
+            "phase_clocks": {"sm_mhz": pclk.get("sm_mhz"), "samples": pclk.get("samples"),
+                             "note": "SM clock during the eager per-phase replay; ms_per_step's "
+                                     "region is in 'clocks'"},
             "gpu_launches": launches * args.steps,
             "clocks": clk,
             "e2e": {"value": path_steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 0,
