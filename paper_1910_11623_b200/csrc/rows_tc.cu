@@ -937,9 +937,18 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
       ppn = 1.0f;
     }
   };
+  // this thread's row masks (TMEM lane layout: row rr), also one tile ahead
+  uint4 mk1n = make_uint4(0, 0, 0, 0), mk2n = make_uint4(0, 0, 0, 0);
+  auto load_mk = [&](int tile) {
+    const int64_t mrow = (int64_t)tile * 128 + rr;
+    const size_t ro = ((size_t)n * a.Bs + (size_t)mrow) * 4;
+    const bool ok = mrow < a.B;
+    mk2n = ok ? __ldg(reinterpret_cast<const uint4*>(a.M2 + ro)) : make_uint4(0, 0, 0, 0);
+    mk1n = ok ? __ldg(reinterpret_cast<const uint4*>(a.M1 + ro)) : make_uint4(0, 0, 0, 0);
+  };
   uint32_t mph = 0;
   bool first = true;
-  if ((int)blockIdx.x < ntiles) { load(blockIdx.x); load_ab(blockIdx.x); }
+  if ((int)blockIdx.x < ntiles) { load(blockIdx.x); load_ab(blockIdx.x); load_mk(blockIdx.x); }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i0 = (int64_t)tile * 128;
     if (t < 128) srow[t] = __fdividef(pab, ppn);   // 0 past B (pab = 0)
@@ -957,14 +966,11 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
       *reinterpret_cast<uint2*>(ahi + ioff(r, c, DP)) = hi;
       *reinterpret_cast<uint2*>(alo + ioff(r, c, DP)) = lo;
     }
-    // this thread's row masks (TMEM lane layout: row rr)
-    const int64_t mrow = i0 + rr;
-    const size_t ro = ((size_t)n * a.Bs + (size_t)mrow) * 4;
-    const uint4 mk2 = mrow < a.B ? __ldg(reinterpret_cast<const uint4*>(a.M2 + ro)) : make_uint4(0, 0, 0, 0);
-    const uint4 mk1 = mrow < a.B ? __ldg(reinterpret_cast<const uint4*>(a.M1 + ro)) : make_uint4(0, 0, 0, 0);
+    const uint4 mk1 = mk1n, mk2 = mk2n;
     if (tile + (int)gridDim.x < ntiles) {   // in flight until the next tile
       load(tile + gridDim.x);
       load_ab(tile + gridDim.x);
+      load_mk(tile + gridDim.x);
     }
     fence_async_smem();
     tc_before();
