@@ -691,7 +691,9 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
   if ((int)blockIdx.x < ntiles) load(blockIdx.x);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i0 = (int64_t)tile * 128;
-    // X̃ -> bf16 hi / lo A image (K = DP)
+    // X̃ -> bf16 hi / lo A image (K = DP), and the same bytes over the tile's fp32 rows
+    // in memory (the X̃ image of dW̃1; a warp writes two whole 128-byte core matrices)
+    uint8_t* xd = tile_img(a.XT, a, n, i0, DP);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = t + u * RT;
@@ -700,8 +702,13 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
       slot_rc<DP>(e, r, c);
       uint2 hi, lo;
       split4(v[u], hi, lo);
-      *reinterpret_cast<uint2*>(ahi + ioff(r, c, DP)) = hi;
-      *reinterpret_cast<uint2*>(alo + ioff(r, c, DP)) = lo;
+      const uint32_t o = ioff(r, c, DP);
+      *reinterpret_cast<uint2*>(ahi + o) = hi;
+      *reinterpret_cast<uint2*>(alo + o) = lo;
+      if (store) {
+        *reinterpret_cast<uint2*>(xd + o) = hi;
+        *reinterpret_cast<uint2*>(xd + XIMG + o) = lo;
+      }
     }
     if (tile + (int)gridDim.x < ntiles) load(tile + gridDim.x);   // in flight until the next tile
     fence_async_smem();
@@ -715,21 +722,11 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
       gemm(tm, Ah, Wl, DP / 16, idesc, true);
       gemm(tm, Al, Wh, DP / 16, idesc, true);
       mma_commit(&bars[1]);
-      if (store) {
-        uint8_t* xd = tile_img(a.XT, a, n, i0, DP);
-        for (uint32_t o = 0; o < XIMG; o += 16384u) {
-          bulk_s2g(xd + o, ahi + o, min(16384u, XIMG - o));
-          bulk_s2g(xd + XIMG + o, alo + o, min(16384u, XIMG - o));
-        }
-        bulk_commit();
-        bulk_wait_read0();   // the images are read before E1 overwrites them
-      }
     }
     first = false;
     mbar_wait(&bars[1], mph);
     mph ^= 1;
     tc_after();
-    __syncthreads();
     // ---- E1 (every thread: its half row)
     {
       uint8_t* hd = tile_img(a.H1, a, n, i0, WP);
@@ -814,7 +811,6 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
     out_masks(i0, a.M2);
     __syncthreads();   // mask words read before the next tile's E1
   }
-  if (t == 0) bulk_wait0();   // this CTA's image stores are complete before it retires
   tc_before();
   __syncthreads();
   if (warp == 0) {
@@ -953,7 +949,9 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
     const int64_t i0 = (int64_t)tile * 128;
     if (t < 128) srow[t] = __fdividef(pab, ppn);   // 0 past B (pab = 0)
     __syncthreads();
-    // dZ = ā_{n+1} G -> bf16 hi / lo A image (K = DP)
+    // dZ = ā_{n+1} G -> bf16 hi / lo A image (K = DP), and the same bytes over the
+    // tile's G rows in memory (the dZ image of dW̃3)
+    uint8_t* zd = tile_img(a.GW, a, n, i0, DP);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = t + u * RT;
@@ -963,8 +961,11 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
       const float sc = srow[r];
       uint2 hi, lo;
       split4(make_float4(sc * v[u].x, sc * v[u].y, sc * v[u].z, sc * v[u].w), hi, lo);
-      *reinterpret_cast<uint2*>(ahi + ioff(r, c, DP)) = hi;
-      *reinterpret_cast<uint2*>(alo + ioff(r, c, DP)) = lo;
+      const uint32_t o = ioff(r, c, DP);
+      *reinterpret_cast<uint2*>(ahi + o) = hi;
+      *reinterpret_cast<uint2*>(alo + o) = lo;
+      *reinterpret_cast<uint2*>(zd + o) = hi;
+      *reinterpret_cast<uint2*>(zd + ZIMG + o) = lo;
     }
     const uint4 mk1 = mk1n, mk2 = mk2n;
     if (tile + (int)gridDim.x < ntiles) {   // in flight until the next tile
@@ -983,19 +984,11 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
       gemm(tm, Ah, Wl, DP / 16, idesc, true);
       gemm(tm, Al, Wh, DP / 16, idesc, true);
       mma_commit(&bars[1]);
-      uint8_t* zd = tile_img(a.GW, a, n, i0, DP);
-      for (uint32_t o = 0; o < ZIMG; o += 16384u) {
-        bulk_s2g(zd + o, ahi + o, min(16384u, ZIMG - o));
-        bulk_s2g(zd + ZIMG + o, alo + o, min(16384u, ZIMG - o));
-      }
-      bulk_commit();
-      bulk_wait_read0();   // the images are read before E4 overwrites them
     }
     first = false;
     mbar_wait(&bars[1], mph);
     mph ^= 1;
     tc_after();
-    __syncthreads();
     epilogue(mk2, tile_img(a.DH, a, n, i0, WP), true);   // E4: dA2
     fence_async_smem();
     tc_before();
@@ -1015,7 +1008,6 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
     tc_before();
     __syncthreads();   // accumulator and A images read before the next tile
   }
-  if (t == 0) bulk_wait0();   // this CTA's image stores are complete before it retires
   tc_before();
   __syncthreads();
   if (warp == 0) {
