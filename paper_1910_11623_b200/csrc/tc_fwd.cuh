@@ -261,7 +261,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
   if (warp == kFwdWorkerWarps) {
     fwd_control<D, W>(a, (int64_t)my_tiles * N, sm, tm, lane);
   } else {
-    const int q = warp & 3, g = warp >> 2;
+    // warp group gw = warp / 4 (group 0 also finishes the Y recursion of its rows) and
+    // column group g = (gw + 2) mod 3: at d = 100 the 25 Philox blocks of a path-step
+    // split 9 / 8 / 8 over the column groups, and the rotation gives the 9-block share to
+    // a warp group without the Y work, so that no worker carries both
+    const int q = warp & 3, gw = warp >> 2, g = (gw + kFwdGroups - 1) % kFwdGroups;
     const int row = 32 * q + lane;
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     const uint32_t acc = tm + lane_off, hT = tm + L::T_H + lane_off, xT = tm + L::T_X + lane_off;
@@ -426,7 +430,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
         tmem_wait_st();
         tc_before();
         named_arrive(kBarE1, kFwdThreads);
-        if (g == 0 && n > 0) finish_y(n - 1);   // E3 partials of step n-1 are complete
+        if (gw == 0 && n > 0) finish_y(n - 1);   // E3 partials of step n-1 are complete
         if (n + 1 < N) put_chunks(Int<0>{}, Int<C1>{});
         if (s < 64) BSDE_STAMP(clk, s * 16 + 3);
         // ---- slice 2 (behind G2); E2: H2 = H1 + ReLU(A2) in bf16x2 arithmetic (R17)
@@ -525,7 +529,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
         part[(2 * G + g) * 128 + row] = sx;
       }
       named_sync(kBarTail, kFwdWorkers);
-      if (g == 0) {
+      if (gw == 0) {
         finish_y(N - 1);
         if (valid) {
           float xn2 = 0.0f;
