@@ -250,6 +250,42 @@ def test_tc_full_size_cfg5_sampled_residuals():
     assert abs(np.mean(Rall ** 2) - loss) <= 1e-4 * loss
 
 
+def test_tc_full_size_cfg4_finest_level_bf16():
+    """Config 4's finest level (HJB, 65 536 paths, N = 80) on the bf16 kernels that the
+    bench's multilevel experiment runs: sampled residuals against the oracle path by
+    path, the loss as the mean of all device residuals, and the gradient of a 1/64
+    fake-world shard of the same global batch against the R17 emulation."""
+    wl = CONFIGS["cfg4_hjb_multilevel"].with_(N=80, precision="bf16")
+    s = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr, precision="bf16")
+    assert s.family == "tc"
+    p = s.get_params()
+    p[1:] += (0.02 * np.random.default_rng(8).standard_normal(p.size - 1)).astype(np.float32)
+    s.set_params(p)
+    s.iteration = 3
+    loss = s.compute_grad()
+    assert np.isfinite(loss) and np.all(np.isfinite(s.get_grads()))
+    idx = np.sort(np.random.default_rng(6).choice(wl.batch, 48, replace=False))
+    ref = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, p, 0, 3, idx, wl.batch,
+                           want_grad=False)
+    R = np.array([s.debug_residuals(int(i), 1)[0] for i in idx])
+    assert np.max(np.abs(R - ref["R"])) <= 2e-2 * np.max(np.abs(ref["R"]))
+    Rall = s.debug_residuals(0, wl.batch).astype(np.float64)
+    assert abs(np.mean(Rall ** 2) - loss) <= 1e-4 * loss
+    s.close()
+    world, rank = 64, 33
+    sh = make(wl.problem, wl.d, wl.w, wl.N, wl.T, wl.batch, lr=wl.lr, precision="bf16",
+              world=world, rank=rank)
+    sh.set_params(p)
+    sh.iteration = 3
+    ls = sh.compute_grad()
+    m0 = rank * (wl.batch // world)
+    emu = oracle_iteration(wl.problem, wl.d, wl.w, wl.N, wl.T, p, 0, 3,
+                           np.arange(m0, m0 + wl.batch // world), wl.batch,
+                           kink_band=KINK_BAND["fp32"], tc=True)
+    check_tc_against_emulation(ls, sh.get_grads(), sh.debug_residuals(0, wl.batch // world),
+                               emu, wl.d, wl.w, wl.N)
+
+
 def test_tc_full_size_cfg2_shape_gradient():
     """Config-2 shape (HJB, 16384 paths, N = 20) with bf16 operands: full gradient."""
     wl = CONFIGS["cfg2_hjb"].with_(precision="bf16")
