@@ -1198,159 +1198,6 @@ __global__ void __launch_bounds__(RT, 1) k_rows_tn(RowsArgs a, int rows_per_cta)
   }
 }
 
-// Weight gradients with compile-time shapes: blockIdx.y = which (as k_rows_tn), two
-// or three CTAs per SM; a chunk's fp32 rows are loaded with all of a thread's loads in
-// flight while the previous chunk's MMAs run, then converted into the (single) image
-// buffer once those MMAs have read it.
-template <int WHICH, int DP, int WP>
-__device__ __forceinline__ void rows_tn_body(const RowsArgs& a, int n, int64_t r0, int64_t r1,
-                                             uint8_t* sm, uint64_t* bar, uint32_t tm, float* srow) {
-  constexpr int P = WHICH == 2 ? DP : WP, Q = WHICH == 0 ? DP : WP;
-  constexpr int PA = P / 4, QB = Q / 4;
-  constexpr int UA = (TK * PA + RT - 1) / RT, UB = (TK * QB + RT - 1) / RT;
-  constexpr uint32_t AB = (uint32_t)TK * 128 * 2, BB = (uint32_t)TK * Q * 2;
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const float* srcA = WHICH == 0 ? a.DA : WHICH == 1 ? a.DH : a.GW;
-  const float* srcB = WHICH == 0 ? a.XT : WHICH == 1 ? a.H1 : a.H2;
-  uint8_t* aimg = sm;
-  uint8_t* bimg = sm + 2 * AB;
-  // image columns P..127 of A stay 0 (MMA M = 128)
-  for (int e = t; e < (int)(2 * AB / 16); e += RT) reinterpret_cast<uint4*>(aimg)[e] = make_uint4(0, 0, 0, 0);
-  const int nch = r0 < r1 ? (int)((r1 - r0 + TK - 1) / TK) : 0;
-  constexpr uint32_t idesc = idesc_bf16(128, Q, true, true);
-  float4 va[UA], vb[UB];
-  auto load = [&](int c) {
-    const int64_t rb = r0 + (int64_t)c * TK;
-    const float* ga = srcA + ((size_t)n * a.Bs + rb) * P;
-    const float* gb = srcB + ((size_t)n * a.Bs + rb) * Q;
-#pragma unroll
-    for (int u = 0; u < UA; ++u) {
-      const int e = t + u * RT;
-      int rl, c4;
-      slot_rc<P>(e, rl, c4);
-      va[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (e < TK * PA && rb + rl < r1) va[u] = __ldg(reinterpret_cast<const float4*>(ga + rl * P + c4));
-    }
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int e = t + u * RT;
-      int rl, c4;
-      slot_rc<Q>(e, rl, c4);
-      vb[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (e < TK * QB && rb + rl < r1) vb[u] = __ldg(reinterpret_cast<const float4*>(gb + rl * Q + c4));
-    }
-  };
-  if (nch > 0) load(0);
-  for (int c = 0; c < nch; ++c) {
-    const int64_t rb = r0 + (int64_t)c * TK;
-    if (WHICH == 2 && t < TK) {   // ā_{n+1} of the chunk's rows (dZ = ā G)
-      const int64_t m = rb + t;
-      srow[t] = m < r1 ? abar_of(a, n, m) : 0.0f;
-    }
-    if (c > 0) mbar_wait(bar, (uint32_t)((c - 1) & 1));   // chunk c-1's MMAs have read the images
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < UA; ++u) {
-      const int e = t + u * RT;
-      if (e >= TK * PA) break;
-      int rl, c4;
-      slot_rc<P>(e, rl, c4);
-      float4 v = va[u];
-      if (WHICH == 2) {
-        const float sc = srow[rl];
-        v = make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w);
-      }
-      uint2 hi, lo;
-      split4(v, hi, lo);
-      *reinterpret_cast<uint2*>(aimg + ioff(rl, c4, 128)) = hi;
-      *reinterpret_cast<uint2*>(aimg + AB + ioff(rl, c4, 128)) = lo;
-    }
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int e = t + u * RT;
-      if (e >= TK * QB) break;
-      int rl, c4;
-      slot_rc<Q>(e, rl, c4);
-      uint2 hi, lo;
-      split4(vb[u], hi, lo);
-      *reinterpret_cast<uint2*>(bimg + ioff(rl, c4, Q)) = hi;
-      *reinterpret_cast<uint2*>(bimg + BB + ioff(rl, c4, Q)) = lo;
-    }
-    fence_async_smem();
-    tc_before();
-    __syncthreads();
-    if (t == 0) {
-      tc_after();
-      const Opnd Ah = mnmaj(aimg, 128), Al = mnmaj(aimg + AB, 128);
-      const Opnd Bh = mnmaj(bimg, Q), Bl = mnmaj(bimg + BB, Q);
-      gemm(tm, Ah, Bh, TK / 16, idesc, c > 0);
-      gemm(tm, Ah, Bl, TK / 16, idesc, true);
-      gemm(tm, Al, Bh, TK / 16, idesc, true);
-      mma_commit(bar);
-    }
-    if (c + 1 < nch) load(c + 1);   // in flight while the MMAs run
-  }
-  if (nch > 0) {
-    mbar_wait(bar, (uint32_t)((nch - 1) & 1));
-    tc_after();
-    const int d = a.d, w = a.w;
-    const NetDims nd{d, w};
-    float* G = a.grad + nd.step_base(n);
-    const int qd = warp & 3, hh = warp >> 2, p = 32 * qd + lane;
-    const uint32_t lb = tm + ((uint32_t)(32 * qd) << 16);
-    constexpr int NCH8 = Q / 16;
-    uint32_t r8[NCH8][8];
-#pragma unroll
-    for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(hh * (Q / 2) + 8 * jj), r8[jj]);
-    tmem_ld_wait();
-#pragma unroll
-    for (int jj = 0; jj < NCH8; ++jj) {
-      reg_fence8(r8[jj]);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int k = hh * (Q / 2) + 8 * jj + e;
-        const float v = __uint_as_float(r8[jj][e]);
-        if (v == 0.0f) continue;
-        int64_t off = -1;
-        if (WHICH == 0 && p < w) off = k < d ? nd.off_W1() + p * d + k : (k == d ? nd.off_b1() + p : -1);
-        if (WHICH == 1 && p < w) off = k < w ? nd.off_W2() + p * w + k : (k == w ? nd.off_b2() + p : -1);
-        if (WHICH == 2 && p < d) off = k < w ? nd.off_W3() + p * w + k : (k == w ? nd.off_b3() + p : -1);
-        if (off >= 0) atomicAdd(G + off, v);
-      }
-    }
-  }
-}
-
-template <int DP, int WP>
-__global__ void __launch_bounds__(RT, 2) k_rows_tn_t(RowsArgs a, int rows_per_cta) {
-  extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ uint32_t tslot;
-  __shared__ float srow[TK];
-  const int t = threadIdx.x, warp = t >> 5;
-  if (t == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-  }
-  if (warp == 0) tmem_alloc(&tslot, 128);
-  tc_before();
-  __syncthreads();
-  tc_after();
-  const uint32_t tm = tslot;
-  const int n = blockIdx.z;
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
-  const int64_t r1 = (a.B < r0 + rows_per_cta ? a.B : r0 + rows_per_cta);
-  if (blockIdx.y == 0) rows_tn_body<0, DP, WP>(a, n, r0, r1, sm, &bar, tm, srow);
-  else if (blockIdx.y == 1) rows_tn_body<1, DP, WP>(a, n, r0, r1, sm, &bar, tm, srow);
-  else rows_tn_body<2, DP, WP>(a, n, r0, r1, sm, &bar, tm, srow);
-  tc_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_after();
-    tmem_dealloc(tm, 128);
-  }
-}
-
 // Weight gradients from the tile images (compile-time shapes): one CTA per SM takes an
 // equal share of the 3·N·2·tiles (which, step, 64-row half tile) units in order.  Thread
 // 0 streams the four images of a unit (A hi / lo, B hi / lo: MN-major over the 64 rows,
@@ -1518,7 +1365,12 @@ cudaError_t gemm_launch_t(const RowsArgs& a, cudaStream_t s) {
 
 template <int OP>
 cudaError_t gemm_launch(const RowsArgs& a, cudaStream_t s) {
-#define X(DP_, WP_) if (a.Dp == DP_ && a.Wp == WP_) return gemm_launch_t<OP, DP_, WP_>(a, s);
+  // compile-time shapes: F3 reads the H2 tile image; F1, F2, B1, B2 run inside the
+  // fused kernels there (their buffers are tile images, which the unfused kernels
+  // would misread)
+#define X(DP_, WP_)                                                                       \
+  if (a.Dp == DP_ && a.Wp == WP_)                                                        \
+    return OP == F3 ? gemm_launch_t<F3, DP_, WP_>(a, s) : cudaErrorNotSupported;
   BSDE_ROWS_SHAPES(X)
 #undef X
   const int K = (OP == F1 || OP == B1) ? a.Dp : a.Wp, Nc = (OP == F3) ? a.Dp : a.Wp;
