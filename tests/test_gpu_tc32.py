@@ -122,6 +122,26 @@ def test_tc32_full_size_cfg4():
     compare_grads(sh.get_grads(), ref["grad"], wl.d, wl.w, wl.N, TOL, ref["slack"])
 
 
+def test_tc32_fake_world_shards_sum():
+    """Two ragged shards (300 paths each: two 128-row tiles and a 44-row tail, global
+    path offsets m0 = 0, 300) of a 600-path batch add up to the full context's loss and
+    gradient (§8(e)), through the tile-image buffers."""
+    d, w, N, T, B = 100, 110, 4, 1.0, 600
+    full = make("hjb", d, w, N, T, B)
+    p = full.get_params()
+    p[1:] += (0.02 * np.random.default_rng(12).standard_normal(p.size - 1)).astype(np.float32)
+    full.set_params(p)
+    lf = full.compute_grad()
+    gf = full.get_grads().astype(np.float64)
+    parts = [make("hjb", d, w, N, T, B, rank=r, world=2) for r in range(2)]
+    for pt in parts:
+        pt.set_params(p)
+    ls = sum(pt.compute_grad() for pt in parts)
+    gs = sum(pt.get_grads().astype(np.float64) for pt in parts)
+    assert abs(ls - lf) <= 1e-6 * lf
+    assert np.linalg.norm(gs - gf) <= 1e-5 * np.linalg.norm(gf)
+
+
 def test_tc32_matches_simt_kernels():
     """Same parameters and paths on the FFMA kernels and the bf16x3 tensor-core rows:
     losses to 1e-5, gradients within the parity bound of each other."""
