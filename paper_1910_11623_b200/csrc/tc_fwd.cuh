@@ -261,11 +261,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
   if (warp == kFwdWorkerWarps) {
     fwd_control<D, W>(a, (int64_t)my_tiles * N, sm, tm, lane);
   } else {
-    // warp group gw = warp / 4 (group 0 also finishes the Y recursion of its rows) and
-    // column group g = (gw + 2) mod 3: at d = 100 the 25 Philox blocks of a path-step
-    // split 9 / 8 / 8 over the column groups, and the rotation gives the 9-block share to
-    // a warp group without the Y work, so that no worker carries both
+    // warp group gw = warp / 4 and column group g = (gw + 2) mod 3.  The last warp group
+    // (the highest warp ids, which the schedulers issue first) also finishes the Y
+    // recursion of its rows; at d = 100 the 25 Philox blocks of a path-step split 9 / 8 /
+    // 8 over the column groups, and the rotation gives the 9-block share to a warp group
+    // without the Y work, so that no worker carries both
     const int q = warp & 3, gw = warp >> 2, g = (gw + kFwdGroups - 1) % kFwdGroups;
+    const bool ywork = gw == kFwdGroups - 1;
     const int row = 32 * q + lane;
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     const uint32_t acc = tm + lane_off, hT = tm + L::T_H + lane_off, xT = tm + L::T_X + lane_off;
@@ -288,7 +290,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
       float X[8 * NS];
 #pragma unroll
       for (int i = 0; i < 8 * NS; ++i) X[i] = a.x0;
-      float Y = a.params[0];   // Y and P are carried by the group-0 worker of each path
+      float Y = a.params[0];   // Y and P are carried by the Y-work warp group (ywork)
       float P = 1.0f;          // prefix product P_{n+1} of the ā factors (per_step_abar problems)
       // X̃_n chunk i from X (bf16, constant 1 in column D)
       auto xchunk = [&](int i) {
@@ -427,10 +429,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
                                 relu_pack2(v[4], v[5]), relu_pack2(v[6], v[7])));
           }
         }
+#ifdef BSDE_E1DETAIL
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 10);
+#endif
         tmem_wait_st();
         tc_before();
         named_arrive(kBarE1, kFwdThreads);
-        if (gw == 0 && n > 0) finish_y(n - 1);   // E3 partials of step n-1 are complete
+#ifdef BSDE_E1DETAIL
+        if (s < 64) BSDE_STAMP(clk, s * 16 + 11);
+#endif
+        if (ywork && n > 0) finish_y(n - 1);   // E3 partials of step n-1 are complete
         if (n + 1 < N) put_chunks(Int<0>{}, Int<C1>{});
         if (s < 64) BSDE_STAMP(clk, s * 16 + 3);
         // ---- slice 2 (behind G2); E2: H2 = H1 + ReLU(A2) in bf16x2 arithmetic (R17)
@@ -504,12 +512,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
                 }
             }
           }
+#ifndef BSDE_E1DETAIL
           if (s < 64) BSDE_STAMP(clk, s * 16 + 10);
+#endif
           part[(0 * G + g) * 128 + row] = cz[0] + cz[1];
           part[(1 * G + g) * 128 + row] = z2[0] + z2[1];
         }
         tc_before();
+#ifndef BSDE_E1DETAIL
         if (s < 64) BSDE_STAMP(clk, s * 16 + 11);
+#endif
         if (n + 1 < N) {   // the rest of X̃_{n+1}; G1 of step n+1 may start
           put_chunks(Int<C2>{}, Int<NS>{});
           tmem_wait_st();
@@ -529,7 +541,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
         part[(2 * G + g) * 128 + row] = sx;
       }
       named_sync(kBarTail, kFwdWorkers);
-      if (gw == 0) {
+      if (ywork) {
         finish_y(N - 1);
         if (valid) {
           float xn2 = 0.0f;
