@@ -261,13 +261,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
   if (warp == kFwdWorkerWarps) {
     fwd_control<D, W>(a, (int64_t)my_tiles * N, sm, tm, lane);
   } else {
-    // warp group gw = warp / 4 and column group g = (gw + 2) mod 3.  The last warp group
-    // (the highest warp ids, which the schedulers issue first) also finishes the Y
-    // recursion of its rows; at d = 100 the 25 Philox blocks of a path-step split 9 / 8 /
-    // 8 over the column groups, and the rotation gives the 9-block share to a warp group
-    // without the Y work, so that no worker carries both
-    const int q = warp & 3, gw = warp >> 2, g = (gw + kFwdGroups - 1) % kFwdGroups;
-    const bool ywork = gw == kFwdGroups - 1;
+    // warp group gw = warp / 4 and column group g = (gw + 1) mod 3.  At d = 100 the 25
+    // Philox blocks of a path-step split 9 / 8 / 8 over the column groups: the 9-block
+    // share goes to the highest warp ids (gw = 2, which the schedulers issue first), the
+    // Y recursion to gw = 1, and the lowest-priority group carries neither
+    const int q = warp & 3, gw = warp >> 2, g = (gw + 1) % kFwdGroups;
+    const bool ywork = gw == 1;
     const int row = 32 * q + lane;
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     const uint32_t acc = tm + lane_off, hT = tm + L::T_H + lane_off, xT = tm + L::T_X + lane_off;
