@@ -120,30 +120,36 @@ __global__ void k_rows_pack(RowsArgs a, int N) {
 }
 
 // ------------------------------------------------------------------ paths
-// one warp per path, lane q = columns 4q..4q+3 (Dp <= 128)
-__global__ void __launch_bounds__(256) k_rows_paths(RowsArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t m = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (m >= a.B) return;
-  const int d = a.d, Dp = a.Dp, q = lane;
-  const bool live = 4 * q < Dp, gen = 4 * q < d;
+// Thread (path m, column quad q < Dp/4): paths packed back to back, Dp/4 threads each
+// (blocks of PPB whole paths), so every lane of a warp draws or stores and a warp's
+// 16-byte row stores are one contiguous run; |X_N|² summed over a path's threads in
+// shared memory, in column order (deterministic).
+constexpr int PPB = 8;   // paths per block
+__global__ void __launch_bounds__(PPB * 32) k_rows_paths(RowsArgs a) {
+  __shared__ float sq[PPB][32];
+  const int Q4 = a.Dp / 4;
+  const int lp = threadIdx.x / Q4, q = threadIdx.x - lp * Q4;
+  const int64_t m = (int64_t)blockIdx.x * PPB + lp;
+  const bool act = lp < PPB && m < a.B;
+  const int d = a.d, Dp = a.Dp;
+  const bool gen = act && 4 * q < d;
   const uint32_t it = a.eval ? a.eval_it : a.state->it;
   const uint32_t mg = (uint32_t)(a.m0 + m);
   const bool mult = a.problem == kBlackScholes;
   float X[4];
   for (int e = 0; e < 4; ++e) X[e] = a.x0;
-  for (int n = 0; n < a.N; ++n) {
-    float dw[4] = {0.f, 0.f, 0.f, 0.f};
-    if (gen) {
-      for (int j = 0; j < a.cpl; ++j) {   // coupled paths: the sum of the fine increments
-        // the MUFU Box-Muller of the tensor-core kernels (R8; ~1e-6 relative, pinned by
-        // test_fast_normals_match_oracle), four times the rate of the libm map
-        const float4 z = dw4_fast((uint32_t)q, mg, (uint32_t)(n * a.cpl + j), it, a.k0, a.k1,
-                                  a.sqrt_dt_f);
-        dw[0] += z.x; dw[1] += z.y; dw[2] += z.z; dw[3] += z.w;
+  if (act) {
+    for (int n = 0; n < a.N; ++n) {
+      float dw[4] = {0.f, 0.f, 0.f, 0.f};
+      if (gen) {
+        for (int j = 0; j < a.cpl; ++j) {   // coupled paths: the sum of the fine increments
+          // the MUFU Box-Muller of the tensor-core kernels (R8; ~1e-6 relative, pinned by
+          // test_fast_normals_match_oracle), four times the rate of the libm map
+          const float4 z = dw4_fast((uint32_t)q, mg, (uint32_t)(n * a.cpl + j), it, a.k0, a.k1,
+                                    a.sqrt_dt_f);
+          dw[0] += z.x; dw[1] += z.y; dw[2] += z.z; dw[3] += z.w;
+        }
       }
-    }
-    if (live) {
       float xv[4], gv[4];
       for (int e = 0; e < 4; ++e) {
         const int c = 4 * q + e;
@@ -153,15 +159,23 @@ __global__ void __launch_bounds__(256) k_rows_paths(RowsArgs a) {
       const size_t o = ((size_t)n * a.Bs + m) * Dp + 4 * q;
       *reinterpret_cast<float4*>(a.XT + o) = make_float4(xv[0], xv[1], xv[2], xv[3]);
       *reinterpret_cast<float4*>(a.GW + o) = make_float4(gv[0], gv[1], gv[2], gv[3]);
+      for (int e = 0; e < 4; ++e)
+        if (4 * q + e < d) X[e] = mult ? fmaf(kBSSigma * dw[e], X[e], X[e]) : fmaf(1.41421356237309515f, dw[e], X[e]);
     }
+    float s2 = 0.0f;
     for (int e = 0; e < 4; ++e)
-      if (4 * q + e < d) X[e] = mult ? fmaf(kBSSigma * dw[e], X[e], X[e]) : fmaf(1.41421356237309515f, dw[e], X[e]);
+      if (4 * q + e < d) s2 = fmaf(X[e], X[e], s2);
+    sq[lp][q] = s2;
   }
-  float s = 0.0f;
-  for (int e = 0; e < 4; ++e)
-    if (4 * q + e < d) s = fmaf(X[e], X[e], s);
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) a.xn2[m] = s;
+  __syncthreads();
+  if (threadIdx.x < PPB) {
+    const int64_t mm = (int64_t)blockIdx.x * PPB + threadIdx.x;
+    if (mm < a.B) {
+      float s = 0.0f;
+      for (int k = 0; k < Q4; ++k) s += sq[threadIdx.x][k];
+      a.xn2[mm] = s;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ tile images
@@ -1449,7 +1463,7 @@ cudaError_t launch_rows_pack(const RowsArgs& a, cudaStream_t s) {
 
 // forward: paths, F1-F3, Y (a.eval: forward only, nothing for the adjoint is kept)
 cudaError_t launch_rows_forward(const RowsArgs& a, cudaStream_t s, int* launches) {
-  rows::k_rows_paths<<<(unsigned)((a.B * 32 + 255) / 256), 256, 0, s>>>(a);
+  rows::k_rows_paths<<<(unsigned)((a.B + rows::PPB - 1) / rows::PPB), rows::PPB * (a.Dp / 4), 0, s>>>(a);
   RCK(cudaGetLastError());
   bool fused = false;
 #define X(DP_, WP_)                                                                               \
