@@ -424,7 +424,13 @@ def main():
                          "peak_sustained": peak_sus, "frac_sustained": achieved / peak_sus,
                          "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": pk_name + "; " + pk["source"],
-                         "algorithmic_flop_per_path_step": fbw if dom == "bwd" else ffw},
+                         "algorithmic_flop_per_path_step": fbw if dom == "bwd" else ffw,
+                         # the other roofline axis: the kernel's DRAM bytes (ncu) over its
+                         # live duration against the measured copy bandwidth
+                         "hbm": ({"achieved_gbs": traffic / (phase[dom] * 1e-3) / 1e9,
+                                  "peak_gbs": pk["hbm_gbs"],
+                                  "frac": traffic / (phase[dom] * 1e-3) / 1e9 / pk["hbm_gbs"]}
+                                 if traffic else None)},
             "step_roofline": {"achieved_tflops": step_flops / (ms * 1e-3) / 1e12,
                               "frac": step_flops / (ms * 1e-3) / 1e12 / peak,
                               "frac_sustained": step_flops / (ms * 1e-3) / 1e12 / peak_sus,
