@@ -477,6 +477,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
         if (s < 64) BSDE_STAMP(clk, s * 16 + 6);
         // ---- slice 3 (behind G3)
         slice(Int<S2>{}, Int<NB>{});
+        if (n + 1 < N) put_chunks(Int<C2>{}, Int<NS>{});   // the rest of X̃_{n+1}, behind G3
         if (s < 64) BSDE_STAMP(clk, s * 16 + 7);
         // ---- E3: partial sums of Z·ΔW (|Z|² for HJB, Σ Z for Black-Scholes) over
         // this worker's columns, with the binary16 ΔW_n (R17)
@@ -521,8 +522,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
 #ifndef BSDE_E1DETAIL
         if (s < 64) BSDE_STAMP(clk, s * 16 + 11);
 #endif
-        if (n + 1 < N) {   // the rest of X̃_{n+1}; G1 of step n+1 may start
-          put_chunks(Int<C2>{}, Int<NS>{});
+        if (n + 1 < N) {   // X̃_{n+1} complete: G1 of step n+1 may start
           tmem_wait_st();
           tc_before();
           named_arrive(kBarX, kFwdThreads);
