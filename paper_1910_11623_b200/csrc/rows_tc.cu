@@ -25,10 +25,15 @@
 // stored as bit words; the unfused B1 / B2 (runtime shapes) test H2 > H1 and H1 > 0,
 // which equal them except where ReLU(A2) is below half an ulp of H1.
 //   TN     dW̃1 = Σ_m dA1ᵀ X̃, dW̃2 = Σ_m dA2ᵀ H1, dW̃3 = Σ_m dZᵀ H2 (the constant-1
-//          columns give the bias gradients), split over row ranges, fp32 atomics
+//          columns give the bias gradients), fp32 atomics per (which, step) segment
 // The biases are folded into the weight images (column d of W̃1, column w of W̃2, W̃3;
 // W̃1 row w = e_d makes H1[w] = H2[w] = 1), as in the bf16 kernels (tc.cu).
-// Row buffers are fp32 [N][B][Dp | Wp] (Dp = pad16(d+1), Wp = pad16(w+1)).
+// Row buffers are [N][Bs][Dp | Wp] (Dp = pad16(d+1), Wp = pad16(w+1)).  Runtime shapes
+// keep fp32 rows (Bs = B).  The built shapes (BSDE_ROWS_SHAPES) keep the buffers that
+// only feed GEMM operands — X̃, H1, H2, dA2, dA1 and dZ = ā G — as bf16 hi / lo tile
+// images (Bs = B rounded up to 128-row tiles; see "tile images" below), so that the
+// weight gradients (k_rows_tn_img) and F3 stream them into the MMAs without
+// converting; the launch sequence there is paths, F12, F3, Y | B12, TN.
 #include <cuda_fp16.h>
 
 #include "kernels.cuh"
