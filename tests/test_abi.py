@@ -85,3 +85,18 @@ def test_workspace_bytes_without_gpu(libpath):
     # refused at create time instead of misaligning the GEMM loads
     with pytest.raises(BSDEError, match="multiple of 4"):
         workspace_bytes("black_scholes", 100, 50, 30, 100, formulation="shared", layers=4)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without libbsde.so the binding refuses to construct a solver."""
+    import subprocess
+    import sys
+    code = ("from paper_1910_11623_b200 import BSDE\n"
+            "try:\n"
+            "    BSDE('heat', 10, 5, 1.0, 20, 256)\n"
+            "except ImportError as e:\n"
+            "    print('raised:', e)\n")
+    env = dict(os.environ, BSDE_LIB=str(tmp_path / "nope" / "libbsde.so"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=120)
+    assert "raised:" in r.stdout and "no CPU fallback" in r.stdout, (r.stdout, r.stderr)
