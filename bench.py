@@ -391,15 +391,27 @@ def main():
             pk_name = "fp32 FFMA: 148 SM x 128 lanes x 2 flop x sm_max_mhz (derived)"
             peak_sus = peak
         dom = "bwd" if phase["bwd"] >= phase["fwd"] else "fwd"
-        traffic, traffic_src = None, None
-        try:   # dram bytes per launch from one `ncu --set full` capture (tools/ncu_traffic.py)
-            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                tr = json.load(f).get(wl.name, {}).get("bsde_" + dom)
-            if tr and world == 1:
-                traffic, traffic_src = tr["bytes_per_launch"], "profiles/" + tr["source"]
-        except Exception:
-            pass
+
+        def kernel_traffic(k):   # dram bytes per launch from one `ncu --set full` capture
+            try:                 # (tools/ncu_traffic.py)
+                with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                    tr = json.load(f).get(wl.name, {}).get("bsde_" + k)
+                if tr and world == 1:
+                    return tr["bytes_per_launch"], "profiles/" + tr["source"]
+            except Exception:
+                pass
+            return None, None
+
+        traffic, traffic_src = kernel_traffic(dom)
         ffw, fbw = flops_per_path_step(wl)
+
+        def kernel_roof(k):   # the same figures for each of the two pass kernels
+            fl = B_local * wl.N * (fbw if k == "bwd" else ffw)
+            ach = fl / (phase[k] * 1e-3) / 1e12
+            tb, _ = kernel_traffic(k)
+            return {"ms": phase[k], "achieved": ach, "frac": ach / peak, "frac_sustained": ach / peak_sus,
+                    "algorithmic_flop_per_path_step": fbw if k == "bwd" else ffw, "traffic": tb,
+                    "hbm_frac": (tb / (phase[k] * 1e-3) / 1e9 / pk["hbm_gbs"]) if tb else None}
         flops = B_local * wl.N * (fbw if dom == "bwd" else ffw)
         achieved = flops / (phase[dom] * 1e-3) / 1e12
         step_flops = wl.batch * wl.N * (ffw + fbw) / world
@@ -430,7 +442,10 @@ def main():
                          "hbm": ({"achieved_gbs": traffic / (phase[dom] * 1e-3) / 1e9,
                                   "peak_gbs": pk["hbm_gbs"],
                                   "frac": traffic / (phase[dom] * 1e-3) / 1e9 / pk["hbm_gbs"]}
-                                 if traffic else None)},
+                                 if traffic else None),
+                         # the dominant kernel is whichever pass took longer in this run; the
+                         # two are within a few percent of each other at config 5
+                         "per_kernel": {"bsde_fwd": kernel_roof("fwd"), "bsde_bwd": kernel_roof("bwd")}},
             "step_roofline": {"achieved_tflops": step_flops / (ms * 1e-3) / 1e12,
                               "frac": step_flops / (ms * 1e-3) / 1e12 / peak,
                               "frac_sustained": step_flops / (ms * 1e-3) / 1e12 / peak_sus,
