@@ -2,7 +2,7 @@
 each variant runs in its own process (BSDE_LIB=build_variants/NAME.so), the order
 alternating over the repeats; prints the best forward / adjoint / step ms of each.
 
-    python tools/ab_variants.py base new [--reps 3]
+    python tools/ab_variants.py base new [--reps 3] [--workload cfg2_hjb --precision fp32]
 """
 import argparse
 import os
@@ -14,8 +14,8 @@ import sys
 sys.path.insert(0, %r)
 from paper_1910_11623_b200 import BSDE
 from workloads import CONFIGS
-wl = CONFIGS["cfg5_allen_cahn_scaleout"]
-s = BSDE(wl.problem, wl.d, wl.N, wl.T, wl.w, wl.batch, lr=wl.lr, precision="bf16")
+wl = CONFIGS[%r]
+s = BSDE(wl.problem, wl.d, wl.N, wl.T, wl.w, wl.batch, lr=wl.lr, precision=%r, kernel=%r)
 for _ in range(3):
     try: s.train_step()
     except Exception: pass
@@ -26,13 +26,16 @@ print("%%.4f %%.4f %%.4f" %% (min(x["fwd"] for x in r), min(x["bwd"] for x in r)
 ap = argparse.ArgumentParser()
 ap.add_argument("variants", nargs="+")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--workload", default="cfg5_allen_cahn_scaleout")
+ap.add_argument("--precision", default="bf16")
+ap.add_argument("--kernel", default="auto")
 args = ap.parse_args()
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 res = {v: [] for v in args.variants}
 for rep in range(args.reps):
     for v in (args.variants if rep % 2 == 0 else args.variants[::-1]):
         env = dict(os.environ, BSDE_LIB=os.path.join(root, "build_variants", v + ".so"))
-        r = subprocess.run([sys.executable, "-c", CODE % root], env=env, capture_output=True, text=True)
+        r = subprocess.run([sys.executable, "-c", CODE % (root, args.workload, args.precision, args.kernel)], env=env, capture_output=True, text=True)
         try:
             res[v].append([float(x) for x in r.stdout.split()])
         except ValueError:
