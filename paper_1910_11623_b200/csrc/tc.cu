@@ -197,12 +197,16 @@ struct Impl {
   }
   template <bool CPL, bool MULT>
   static cudaError_t fwd_v(const PassArgs& a, cudaStream_t s) {
-    const size_t smem = fwd_smem();
-    cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<D, W, CPL, MULT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the Philox round 0-2 table when it fits beside the kernel's own 111 KB (N <= ~200)
+    using L = FwdSmem<D, W>;
+    const size_t with_tab = (size_t)L::TAB + L::tab_bytes(a.N);
+    const bool use_tab = !CPL && with_tab <= 227u * 1024u;
+    const size_t smem = use_tab ? with_tab : fwd_smem();
+    const auto kern = use_tab ? k_fwd_tc<D, W, CPL, MULT, !CPL> : k_fwd_tc<D, W, CPL, MULT, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int nt = ntiles(a), sms = sm_count();
-    k_fwd_tc<D, W, CPL, MULT><<<nt < sms ? nt : sms, kFwdThreads, smem, s>>>(a, nt);
+    kern<<<nt < sms ? nt : sms, kFwdThreads, smem, s>>>(a, nt);
     return cudaGetLastError();
   }
   static cudaError_t fwd(const PassArgs& a, cudaStream_t s) {

@@ -89,6 +89,32 @@ __host__ __device__ constexpr int blk_prefix(int b0, int b1, int D) {   // first
   return b0 >= b1 ? b1 : (blk_all(b0, D) ? blk_prefix(b0 + 1, b1, D) : b0);
 }
 
+// Rounds 0-2 of Philox4x32-10 on the counter (q, m, n, it) (R8): every product except
+// the two that involve the path index m depends on (q, n, it, key) only, so they are
+// computed once per launch for every (step n, block q) into shared memory, and a lane
+// starts each block at round 1's m-dependent multiply (16 IMAD.WIDE instead of 20).
+// Row entry (A, B, C, D) and E, with (round 0) lo0 = M0 q, hi0 = hi(M0 q), lo1 = M1 n,
+// hi1 = hi(M1 n), z1 = hi0 ^ it ^ k1; (round 1) x2 = hi(M1 z1) ^ lo1 ^ (k0 + W0),
+// y2 = M1 z1:
+//   A = hi1 ^ k0              x1 = A ^ m
+//   B = lo0 ^ (k1 + W1)       z2 = hi(M0 x1) ^ B,   w2 = M0 x1
+//   C = y2 ^ (k0 + 2 W0)      x3 = hi(M1 z2) ^ C,   y3 = M1 z2
+//   D = hi(M0 x2) ^ (k1 + 2 W1)   z3 = D ^ w2
+//   E = M0 x2                 w3 = E
+__device__ __forceinline__ void fwd_philox_table(uint4* tab4, uint32_t* tabE, int nq, int nsteps, uint32_t it,
+                                                 uint32_t k0, uint32_t k1) {
+  for (int i = threadIdx.x; i < nq * nsteps; i += blockDim.x) {
+    const uint32_t q = (uint32_t)(i % nq), n = (uint32_t)(i / nq);
+    const uint32_t lo0 = kPhiloxM0 * q, hi0 = __umulhi(kPhiloxM0, q);
+    const uint32_t lo1 = kPhiloxM1 * n, hi1 = __umulhi(kPhiloxM1, n);
+    const uint32_t z1 = hi0 ^ it ^ k1;
+    const uint32_t x2 = __umulhi(kPhiloxM1, z1) ^ lo1 ^ (k0 + kPhiloxW0), y2 = kPhiloxM1 * z1;
+    tab4[i] = make_uint4(hi1 ^ k0, lo0 ^ (k1 + kPhiloxW1), y2 ^ (k0 + 2u * kPhiloxW0),
+                         __umulhi(kPhiloxM0, x2) ^ (k1 + 2u * kPhiloxW1));
+    tabE[i] = kPhiloxM0 * x2;
+  }
+}
+
 // Increments of the worker's Philox blocks b = B0 .. B0+NB-1 of step n: block b
 // holds columns 8c + 4(b%2) .. +3 of chunk c = g + 3(b/2), i.e. counter word 0
 // q = 2c + b%2 (R8).  Interleaved for ILP; blocks whose columns are all >= D
@@ -96,22 +122,37 @@ __host__ __device__ constexpr int blk_prefix(int b0, int b1, int D) {   // first
 // as 0.  Coupled paths (cpl > 1, NEXT-3): the sum over the cpl fine steps
 // n·cpl + j of √(Δt/cpl)·z (sdt = √(Δt/cpl)); the uncoupled instance (CPL false)
 // keeps the loop out of the hot code.
-template <int D, int B0, int NB, bool CPL>
+template <int D, int B0, int NB, bool CPL, bool TAB>
 __device__ __forceinline__ void gen_blocks(int g, uint32_t m, uint32_t n, uint32_t it, uint32_t k0,
-                                           uint32_t k1, float sdt, float (&z)[4 * NB], int cpl) {
+                                           uint32_t k1, float sdt, float (&z)[4 * NB], int cpl,
+                                           const uint4* tab4, const uint32_t* tabE) {
   auto one = [&](uint32_t nf, bool add) {   // the normals of (fine) step nf
     uint4 c[NB];
     bool ok[NB];
+    constexpr int NQ = Dims<D, 8>::Dp / 4;   // Philox blocks per path-step (table row)
+    constexpr bool tab = !CPL && TAB;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       const int b = B0 + j, q = 2 * (g + kFwdGroups * (b / 2)) + b % 2;
-      c[j] = make_uint4((uint32_t)q, m, nf, it);
       ok[j] = col_lt3(g, b / 2, 4 * (b % 2), D);   // 4q < D
+      if (tab) {   // rounds 0-2 from the step's table row (fwd_philox_table); only the
+                   // two multiplies that involve the path index m remain per lane
+        const uint4 u = tab4[nf * NQ + q];
+        const uint32_t x1 = u.x ^ m;
+        const uint32_t l0 = kPhiloxM0 * x1, h0 = __umulhi(kPhiloxM0, x1);
+        const uint32_t z2 = h0 ^ u.y;
+        const uint32_t m1 = kPhiloxM1 * z2, g1 = __umulhi(kPhiloxM1, z2);
+        c[j] = make_uint4(g1 ^ u.z, m1, u.w ^ l0, tabE[nf * NQ + q]);
+      } else {
+        c[j] = make_uint4((uint32_t)q, m, nf, it);
+      }
     }
-    uint32_t a0 = k0, a1 = k1;
+    constexpr int r0 = tab ? 3 : 0;
+    uint32_t a0 = k0 + (uint32_t)r0 * kPhiloxW0, a1 = k1 + (uint32_t)r0 * kPhiloxW1;
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
-      if (r) { a0 += kPhiloxW0; a1 += kPhiloxW1; }
+      if (r < r0) continue;
+      if (r > r0) { a0 += kPhiloxW0; a1 += kPhiloxW1; }
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         if (!ok[j]) continue;
@@ -155,6 +196,10 @@ struct FwdSmem {
   static constexpr int NBARS = 4;
   static constexpr uint32_t TSLOT = BARS + NBARS * 8;
   static constexpr uint32_t BYTES = TSLOT + 16;
+  // the Philox round 0-2 table (fwd_philox_table): NQ x N uint4 rows, then NQ x N words
+  static constexpr int NQ = Dm::Dp / 4;
+  static constexpr uint32_t TAB = (BYTES + 15u) & ~15u;
+  static constexpr uint32_t tab_bytes(int n_steps) { return (uint32_t)NQ * (uint32_t)n_steps * 20u; }
   // tensor memory: the fp32 accumulator, the bf16 A operand of G2/G3 (H1, H2)
   // and that of G1 (X̃_n; no shared-memory operand, so no proxy fence on the
   // workers' path)
@@ -226,8 +271,9 @@ __device__ __forceinline__ void fwd_control(const PassArgs& a, int64_t total, ui
 
 // CPL: coupled multilevel paths (a.cpl > 1); MULT: Black-Scholes multiplicative
 // noise.  Both are compile-time so that the hot instance carries neither.
-template <int D, int W, bool CPL, bool MULT>
+template <int D, int W, bool CPL, bool MULT, bool TAB>
 __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntiles) {
+  constexpr bool use_tab = TAB && !CPL;
   using Dm = Dims<D, W>;
   using L = FwdSmem<D, W>;
   constexpr int Dp = Dm::Dp, Wp = Dm::Wp, NCD = Dp / 8, NCW = Wp / 8;
@@ -248,6 +294,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tslot, L::TCOLS);
+  uint4* const tab4 = use_tab ? reinterpret_cast<uint4*>(sm + L::TAB) : nullptr;
+  uint32_t* const tabE = use_tab ? reinterpret_cast<uint32_t*>(sm + L::TAB + (uint32_t)L::NQ * a.N * 16u) : nullptr;
+  if (use_tab) fwd_philox_table(tab4, tabE, L::NQ, a.N, a.eval ? a.eval_it : a.state->it, a.k0, a.k1);
   tc_before();
   __syncthreads();
   tc_after();
@@ -375,7 +424,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
             };
             auto gen = [&](auto bc, auto& z) {   // z: float[4k], blocks bb .. bb+k-1
               constexpr int bb = decltype(bc)::value, k = sizeof(z) / sizeof(float) / 4;
-              gen_blocks<D, bb, k, CPL>(g, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt_f, z, a.cpl);
+              gen_blocks<D, bb, k, CPL, use_tab>(g, mg, (uint32_t)n, it, a.k0, a.k1, a.sqrt_dt_f, z, a.cpl, tab4, tabE);
             };
             // blocks valid for every column group: one interleaved group
             constexpr int bv = blk_prefix(b0, b0 + nb, D);
