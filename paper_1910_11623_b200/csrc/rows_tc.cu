@@ -462,6 +462,22 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
       }
     }
   }
+  // F3: this warp's G rows of half tile 0 (rows warp + 8j) in flight during the bulk
+  // copies and the MMAs; half 1's are issued once half 0's rows are done
+  constexpr int NRH = 64 / (RT / 32);   // rows per warp and half tile
+  const int c4 = 4 * lane;
+  const bool lane_on = c4 < NC;
+  float4 gq0[OP == F3 ? NRH : 1];
+  auto load_g = [&](int hf, float4 (&gq)[OP == F3 ? NRH : 1]) {
+#pragma unroll
+    for (int j = 0; j < (OP == F3 ? NRH : 0); ++j) {
+      const int64_t m = i0 + 64 * hf + warp + 8 * j;
+      gq[j] = (m < a.B && lane_on)
+                  ? __ldcs(reinterpret_cast<const float4*>(a.GW + ((size_t)n * a.Bs + (size_t)m) * DP + c4))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  if constexpr (OP == F3) load_g(0, gq0);
   // stage A: all U float4 loads in flight, then split / store
   if constexpr (!IMGA) {
     const float* base = src + ((size_t)n * a.Bs + i0) * K;
@@ -509,8 +525,59 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
   const int cb = h * (NC / 2);
   const float dt = a.dt;
   const float zc = -dt * driver_dfdz_coef(a.problem, a.lam), zc0 = -dt * driver_dfdz_const(a.problem);
-  const int c4 = 4 * lane;
-  const bool lane_on = c4 < NC;
+  if constexpr (OP == F3) {
+    // the epilogue from the prefetched G rows: no memory round trip per row batch
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      if ((q >> 1) == hf) {   // phase 1: this half's lane quadrants -> tile rows 0..63
+        uint32_t r8[NCH8][8];
+#pragma unroll
+        for (int jj = 0; jj < NCH8; ++jj) tmem_ld8_nowait(lb + (uint32_t)(cb + 8 * jj), r8[jj]);
+        tmem_ld_wait();
+        const int rl = 32 * (q & 1) + lane;
+#pragma unroll
+        for (int jj = 0; jj < NCH8; ++jj) {
+          reg_fence8(r8[jj]);
+          float* dstp = stile + rl * LDT + cb + 8 * jj;
+          *reinterpret_cast<uint4*>(dstp) = make_uint4(r8[jj][0], r8[jj][1], r8[jj][2], r8[jj][3]);
+          *reinterpret_cast<uint4*>(dstp + 4) = make_uint4(r8[jj][4], r8[jj][5], r8[jj][6], r8[jj][7]);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < NRH; ++j) {
+        const int r = warp + 8 * j;
+        const int64_t m = i0 + 64 * hf + r;
+        if (m >= a.B) continue;   // warp-uniform
+        const size_t row = (size_t)n * a.Bs + (size_t)m;
+        const float4 v = lane_on ? *reinterpret_cast<const float4*>(stile + r * LDT + c4)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        float s1 = 0.f, s2 = 0.f;
+        if (lane_on) {   // Z·ΔW, |Z|² | Σ Z; G = ΔW - Δt ∂_z f in place (R2)
+          const float4 gv = gq0[j];
+          const float z[4] = {v.x, v.y, v.z, v.w};
+          float g[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (c4 + e >= d) { g[e] = 0.f; continue; }
+            s1 = fmaf(z[e], g[e], s1);
+            if (a.problem == kHJB) s2 = fmaf(z[e], z[e], s2);
+            else if (a.problem == kBlackScholes) s2 += z[e];
+            g[e] = fmaf(zc, z[e], g[e] + zc0);   // ∂_z f = -λ z (HJB), r/σ (Black-Scholes)
+          }
+          if (!a.eval) *reinterpret_cast<float4*>(a.GW + row * DP + c4) = make_float4(g[0], g[1], g[2], g[3]);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        if (lane == 0) *reinterpret_cast<float2*>(a.S + row * 2) = make_float2(s1, s2);
+      }
+      if (hf == 0) load_g(1, gq0);   // half 1's rows, in flight over its phase 1
+      __syncthreads();
+    }
+  } else {
 #pragma unroll 1
   for (int hf = 0; hf < 2; ++hf) {
     if ((q >> 1) == hf) {   // phase 1: this half's lane quadrants -> tile rows 0..63
@@ -615,6 +682,7 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
     }
       }
     __syncthreads();
+  }
   }
   tc_before();
   __syncthreads();
