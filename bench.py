@@ -465,19 +465,24 @@ def main():
         if family in ("tc", "tc32") and wl.formulation == "per_step":
             # the forward's other bound: the Philox4x32-10 + Box-Muller increments, 1 Philox
             # block per 4 normals, ceil(d/4) per path and (fine) step, against the
-            # standalone generator's measured rate (profiles/r01_microbench.md: 0.96
-            # lane-Philox per cycle per SM with the MUFU Box-Muller) at this run's clock
+            # standalone generator's best measured rate (profiles/r02_ubench_philox.txt, lane
+            # blocks per cycle per SM with the MUFU Box-Muller): 1.162 for the forward's
+            # generator (rounds 0-2 from the per-launch table: eight rounds' multiplies per
+            # lane), 1.039 for the full ten rounds of the tc32 path kernel, at the SM clock
+            # of the phase replay the forward's time comes from
             blocks = B_local * wl.N * ((wl.d + 3) // 4)
             rng_ach = blocks / (phase["fwd"] * 1e-3)
-            mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
-            rng_peak = 0.96 * 148 * mhz * 1e6
+            mhz = pclk.get("sm_mhz") or clk.get("sm_mhz") or pk["sm_max_mhz"]
+            rate = 1.162 if family == "tc" else 1.039
+            rng_peak = rate * 148 * mhz * 1e6
             line["rng_roofline"] = {
                 "kernel": "bsde_fwd", "bound": "alu", "unit": "Philox4x32-10 blocks/s",
                 "achieved": rng_ach, "peak": rng_peak, "frac": rng_ach / rng_peak,
-                "peak_source": "0.96 blocks/cycle/SM (Philox + MUFU Box-Muller, standalone, "
-                               "profiles/r01_microbench.md) x 148 SM x median SM clock of the run",
+                "peak_source": "%.3f blocks/cycle/SM (Philox + MUFU Box-Muller, standalone, best "
+                               "measured, profiles/r02_ubench_philox.txt) x 148 SM x SM clock of "
+                               "the phase replay (%s MHz)" % (rate, mhz),
                 "note": "the forward kernel also runs the three chain epilogues between its "
-                        "random-number slices (DESIGN §6)"}
+                        "random-number slices (DESIGN §6, §8 step floor)"}
         if wl.name in PAPER_MINUTES:
             # the paper's own timing of this workload: context only
             line["paper_context"] = {

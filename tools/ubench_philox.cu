@@ -28,8 +28,10 @@ __global__ void __launch_bounds__(512, 1) k_philox(int iters, uint32_t k0, uint3
 #pragma unroll
     for (int j = 0; j < K; ++j) x[j] = make_uint4(c[j].x + i, c[j].y, c[j].z, c[j].w);
     uint32_t a0 = k0, a1 = k1;
+    // MODE 3: the forward's per-lane share with the round 0-2 table (fwd_philox_table):
+    // 16 IMAD.WIDE per block, i.e. eight full rounds, + Box-Muller
 #pragma unroll
-    for (int r = 0; r < 10; ++r) {
+    for (int r = (MODE == 3 ? 2 : 0); r < 10; ++r) {
       if (r) { a0 += kPhiloxW0; a1 += kPhiloxW1; }
 #pragma unroll
       for (int j = 0; j < K; ++j) {
@@ -44,7 +46,7 @@ __global__ void __launch_bounds__(512, 1) k_philox(int iters, uint32_t k0, uint3
         x[j] = make_uint4(hi1 ^ x[j].y ^ a0, lo1, hi0 ^ x[j].w ^ a1, lo0);
       }
     }
-    if (MODE == 2) {   // + the fast Box-Muller map of the tcgen05 kernels
+    if (MODE == 2 || MODE == 3) {   // + the fast Box-Muller map of the tcgen05 kernels
 #pragma unroll
       for (int j = 0; j < K; ++j) {
         float z0, z1, z2, z3;
@@ -102,6 +104,10 @@ int main() {
   run<2, 4>("philox + box-muller fast", 384);
   run<2, 6>("philox + box-muller fast", 384);
   run<2, 8>("philox + box-muller fast", 512);
+  run<3, 4>("philox(8 rounds) + box-muller", 512);
+  run<3, 3>("philox(8 rounds) + box-muller", 384);
+  run<3, 3>("philox(8 rounds) + box-muller", 416);
+  run<2, 3>("philox + box-muller fast", 416);
   // (a polynomial sin/cos instead of MUFU measured 0.76 Philox/cyc/SM at 384
   //  and 512 threads: the map is issue-bound, not MUFU-bound)
   printf("status: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
