@@ -503,7 +503,7 @@ def main():
             s.close()
             s = None
             from bench_multilevel import run_cfg4
-            ml = run_cfg4(args.ml_precision, args.ml_iters)
+            ml = run_cfg4(args.ml_precision, args.ml_iters, alt=[(1000, False)])
             ml["note"] = ("config 4 (HJB d=100, N 5->80, B=65536) with %s operands on the %s "
                           "kernels; time-to-target = training wall clock (evaluations excluded) "
                           "until the eval loss <= target" % (args.ml_precision, ml["kernel"]))

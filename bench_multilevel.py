@@ -1,14 +1,19 @@
 """Multilevel time-to-target-loss experiment (BASELINE.json config 4).
 
-    python bench_multilevel.py [--precision fp32|bf16] [--iters 10000] [--per-level 400]
+    python bench_multilevel.py [--precision fp32|bf16] [--iters 10000] [--per-level 1000] [--reset-adam]
 
 Single-level baseline: HJB d = 100, w = 110, N = 80, B = 65 536 paths, Adam lr
 1e-2, `--iters` iterations (10 000: enough for Y0 to settle within 0.5% of the
 Cole-Hopf value, which 2 000 are not); the target loss L* is 1.01 × its final loss, the
 mean of its last 5 evaluations on the fixed evaluation stream (eval_id 0,
 65 536 paths, the current grid).  Multilevel: N = 5 -> 10 -> 20 -> 40 -> 80 with
-`--per-level` iterations per level (copy prolongation, Adam reset, R14); the
+`--per-level` iterations per level (copy prolongation; the Adam moments prolonged
+with the parameters and t kept, R14b, or reset with `--reset-adam`, R14); the
 N = 80 level may run up to `--iters` extra iterations until L* is reached.
+The per-level budget and the Adam rule were chosen by `tools/ml_sweep.py`
+(profiles/r02_ml_sweep.txt): with the R14 reset the coarse levels barely help
+(1.3-2.5x, the restarted Adam kicks every weight by ~lr), with R14b and >= 1 000
+iterations per level the fine grid starts close to the target (3.7-4.0x).
 Wall clock counts training steps only (evaluations excluded) and is reported
 for both runs with their ratio; Y0 per level is compared with the Cole-Hopf
 value u(0,0) = 4.590161724605 (pin H4).  Prints one JSON line.
@@ -27,9 +32,13 @@ from workloads import CONFIGS  # noqa: E402
 COLE_HOPF = 4.590161724605
 
 
-def run_cfg4(precision="bf16", iters=10000, per_level=400, eval_every=50, batch=0, kernel="auto"):
+def run_cfg4(precision="bf16", iters=10000, per_level=1000, eval_every=50, batch=0, kernel="auto",
+             keep_adam=True, alt=None):
     """BASELINE config 4 on the device: single-level N = 80 for `iters` iterations,
-    then the multilevel schedule; returns the result dict (see the module doc)."""
+    then the multilevel schedule (`per_level` iterations per level, the Adam state kept
+    across level changes, R14b, or reset, R14); returns the result dict (see the module
+    doc).  `alt` = [(per_level, keep_adam), ...]: further schedules timed to the same
+    target in the same run (reported under "other_schedules")."""
     import numpy as np
     import torch
     from paper_1910_11623_b200 import BSDE
@@ -56,13 +65,29 @@ def run_cfg4(precision="bf16", iters=10000, per_level=400, eval_every=50, batch=
     single.close()
     torch.cuda.synchronize()
 
-    multi = BSDE(wl.problem, wl.d, levels[0], wl.T, wl.w, B, max_levels=len(levels) - 1, **kw)
-    res_m = run_schedule(multi, [per_level] * len(levels), eval_every=eval_every,
-                         eval_batch=B, target_loss=target, final_N=Nf, extend_last=iters)
+    def schedule(per, keep):
+        m = BSDE(wl.problem, wl.d, levels[0], wl.T, wl.w, B, max_levels=len(levels) - 1,
+                 keep_adam=keep, **kw)
+        r = run_schedule(m, [per] * len(levels), eval_every=eval_every, eval_batch=B,
+                         target_loss=target, final_N=Nf, extend_last=iters)
+        m.close()
+        torch.cuda.synchronize()
+        return r
+
+    res_m = schedule(per_level, keep_adam)
+    others = []
+    for per, keep in (alt or []):
+        r = schedule(per, keep)
+        others.append({"per_level_iters": per, "adam_at_level_change": "kept (R14b)" if keep else "reset (R14)",
+                       "time_to_target_s": r.time_to_target, "iteration_at_target": r.iteration_at_target,
+                       "speedup_to_target": (t_single_target / r.time_to_target
+                                             if r.time_to_target and t_single_target else None)})
     out = {
         "experiment": "multilevel time-to-target (config 4)",
         "precision": precision, "kernel": family, "batch": B, "levels": levels,
         "per_level_iters": per_level, "single_level_iters": iters, "eval_every": eval_every,
+        "adam_at_level_change": "kept: m, v prolonged like the parameters, t kept (R14b)" if keep_adam
+                                else "reset (R14)",
         "target_rule": "1.01 x the single-level run's final evaluation loss (mean of its last 5 "
                        "evaluations, eval_id 0, %d paths, N = %d)" % (B, Nf),
         "single_final_loss": final, "target_loss": target,
@@ -79,7 +104,8 @@ def run_cfg4(precision="bf16", iters=10000, per_level=400, eval_every=50, batch=
         "paper_context": "PAPER.md Table (P:481-493): multilevel 6-11 min vs single-level 59-123 min "
                          "on a Tesla T4 (Black-Scholes, shared net) - context only",
     }
-    multi.close()
+    if others:
+        out["other_schedules"] = others
     return out
 
 
@@ -87,7 +113,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--precision", default="bf16")
     ap.add_argument("--iters", type=int, default=10000)
-    ap.add_argument("--per-level", type=int, default=400)
+    ap.add_argument("--per-level", type=int, default=1000)
+    ap.add_argument("--reset-adam", action="store_true", help="R14: reset Adam at each level change")
     ap.add_argument("--eval-every", type=int, default=50)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--workload", default="cfg4", choices=["cfg4", "shared_bs_paper"])
@@ -96,7 +123,7 @@ def main():
     if args.workload == "shared_bs_paper":
         return shared_paper(args)
     print(json.dumps(run_cfg4(args.precision, args.iters, args.per_level, args.eval_every,
-                              args.batch)), flush=True)
+                              args.batch, keep_adam=not args.reset_adam)), flush=True)
 
 
 def shared_paper(args):

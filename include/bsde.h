@@ -69,7 +69,10 @@ enum {
   BSDE_KERNEL_TC = 2     /* tcgen05 tensor-core kernels (sm_100a)                       */
 };
 
-enum { BSDE_PROLONG_COPY = 0, BSDE_PROLONG_INTERP = 1 };   /* a9, R14 */
+/* a9: BSDE_PROLONG_COPY or BSDE_PROLONG_INTERP, optionally | BSDE_PROLONG_KEEP_ADAM
+ * (R14b: the Adam moments m, v are prolonged by the same rule as the parameters and t
+ * is kept, instead of the R14 reset; not with a sharded optimizer at world > 1) */
+enum { BSDE_PROLONG_COPY = 0, BSDE_PROLONG_INTERP = 1, BSDE_PROLONG_KEEP_ADAM = 16 };
 
 enum {
   BSDE_OK = 0,
@@ -92,7 +95,7 @@ typedef struct {
   uint64_t seed;          /* Philox key = (seed mod 2^32, seed >> 32) (R8)                  */
   int precision;          /* BSDE_FP32 | BSDE_BF16                                          */
   int kernel;             /* BSDE_KERNEL_*                                                  */
-  int prolong_mode;       /* BSDE_PROLONG_COPY | BSDE_PROLONG_INTERP                        */
+  int prolong_mode;       /* BSDE_PROLONG_COPY | BSDE_PROLONG_INTERP, | BSDE_PROLONG_KEEP_ADAM */
   int max_levels;         /* buffers sized for N * 2^max_levels time steps                  */
   int device;             /* CUDA ordinal                                                   */
   void* stream;           /* cudaStream_t to enqueue on (NULL = legacy default stream)      */
@@ -190,9 +193,11 @@ int bsde_train_step(bsde_ctx* ctx, double* loss_out);
 
 /* Multilevel level change (§3.2):
  * N <- 2N, Δt <- T/(2N); step k of the fine grid takes the coarse net k/2 (COPY)
- * or the midpoint rule (INTERP); Y0 is kept; Adam m, v, t are reset; the
- * iteration counter continues.  `level` must equal the current level + 1 and be
- * <= cfg.max_levels.  Errors: ESTATE. */
+ * or the midpoint rule (INTERP); Y0 is kept; Adam m, v, t are reset (R14), or with
+ * BSDE_PROLONG_KEEP_ADAM m and v are prolonged by the same rule and t is kept (R14b);
+ * the iteration counter continues.  `level` must equal the current level + 1 and be
+ * <= cfg.max_levels.  Errors: ESTATE (also KEEP_ADAM with sharded_adam or the fused
+ * optimizer at world > 1: each rank holds one shard of m, v). */
 int bsde_prolongate(bsde_ctx* ctx, int level);
 
 /* The trainable Y0 ≈ u(0, X0) (BASELINE.json north_star). Synchronises. */

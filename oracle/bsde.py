@@ -360,17 +360,30 @@ def train(problem, d, w, N, T, params, seed, batch, iters, lr, it0=0, state=None
     return params, state, losses
 
 
+def prolongate_adam(state, d, w, N, mode=COPY):
+    """R14b: the moments m, v follow the parameters' prolongation rule
+    (the same function, `prolongate`), t is kept; the alternative to the R14 reset."""
+    out = AdamState(1 + 2 * N * step_size(d, w))
+    out.m = prolongate(state.m, d, w, N, mode)
+    out.v = prolongate(state.v, d, w, N, mode)
+    out.t = state.t
+    return out
+
+
 def train_multilevel(problem, d, w, levels, T, params, seed, batch, iters_per_level, lr,
-                     mode=COPY, lam=1.0):
-    """Levels N_0 < N_1 = 2N_0 < ...; Adam state reset at each change (R14);
-    the Philox iteration counter continues across levels (R9)."""
+                     mode=COPY, lam=1.0, keep_adam=False):
+    """Levels N_0 < N_1 = 2N_0 < ...; Adam state reset at each change (R14), or
+    prolonged with the parameters (keep_adam, R14b); the Philox iteration counter
+    continues across levels (R9)."""
     it = 0
     history = []
+    state = None
     for li, N in enumerate(levels):
         if li:
             params = prolongate(params, d, w, levels[li - 1], mode)
-        params, _, losses = train(problem, d, w, N, T, params, seed, batch,
-                                  iters_per_level[li], lr, it0=it, lam=lam)
+            state = prolongate_adam(state, d, w, levels[li - 1], mode) if keep_adam else None
+        params, state, losses = train(problem, d, w, N, T, params, seed, batch,
+                                      iters_per_level[li], lr, it0=it, state=state, lam=lam)
         history += [(li, N, l) for l in losses]
         it += iters_per_level[li]
     return params, history

@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("BSDE_LIB") or os.path.join(_HERE, "libbsde.so")
 HEAT, HJB, ALLEN_CAHN, BLACK_SCHOLES = 0, 1, 2, 3
 FP32, BF16 = 0, 1
 KERNEL_AUTO, KERNEL_SIMT, KERNEL_TC = 0, 1, 2
-PROLONG_COPY, PROLONG_INTERP = 0, 1
+PROLONG_COPY, PROLONG_INTERP, PROLONG_KEEP_ADAM = 0, 1, 16
 OK, EINVAL, ECUDA, ENCCL, EDIVERGED, ESTATE, ENOMEM = 0, -1, -2, -3, -4, -5, -6
 ERROR_NAMES = {EINVAL: "EINVAL", ECUDA: "ECUDA", ENCCL: "ENCCL", EDIVERGED: "EDIVERGED",
                ESTATE: "ESTATE", ENOMEM: "ENOMEM"}

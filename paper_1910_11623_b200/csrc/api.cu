@@ -538,7 +538,8 @@ int bsde_create(int problem, int d, int N, double T, const int* widths, int n_wi
     return fail(none, BSDE_EINVAL, "precision=%d", cfg.precision);
   if (cfg.max_levels < 0 || cfg.max_levels > 12)
     return fail(none, BSDE_EINVAL, "max_levels=%d", cfg.max_levels);
-  if (cfg.prolong_mode != BSDE_PROLONG_COPY && cfg.prolong_mode != BSDE_PROLONG_INTERP)
+  if ((cfg.prolong_mode & ~BSDE_PROLONG_KEEP_ADAM) != BSDE_PROLONG_COPY &&
+      (cfg.prolong_mode & ~BSDE_PROLONG_KEEP_ADAM) != BSDE_PROLONG_INTERP)
     return fail(none, BSDE_EINVAL, "prolong_mode=%d", cfg.prolong_mode);
   if (!(cfg.lr > 0) || !(cfg.beta1 >= 0 && cfg.beta1 < 1) || !(cfg.beta2 >= 0 && cfg.beta2 < 1) ||
       !(cfg.eps > 0))
@@ -793,23 +794,34 @@ int bsde_prolongate(bsde_ctx* ctx, int level) {
   if (level != ctx->level + 1 || level > ctx->cfg.max_levels)
     return fail(ctx, BSDE_ESTATE, "prolongate(level=%d): current level %d, max_levels %d", level,
                 ctx->level, ctx->cfg.max_levels);
+  const int pmode = ctx->cfg.prolong_mode & ~BSDE_PROLONG_KEEP_ADAM;
+  const bool keep = (ctx->cfg.prolong_mode & BSDE_PROLONG_KEEP_ADAM) != 0;   // R14b
+  if (keep && ctx->cfg.world > 1 && (ctx->cfg.sharded_adam || ctx->fused))
+    return fail(ctx, BSDE_ESTATE, "prolongate: KEEP_ADAM with a sharded optimizer (each rank "
+                                  "holds one shard of the Adam moments)");
   if (!ctx->shared) {   // the shared network is the same function on every grid
     const int64_t P = NetDims{ctx->d, ctx->w, ctx->nais}.step_size();
     const int64_t np = num_params_at(ctx, ctx->N);
-    CK(cudaMemcpyAsync(ctx->scratch, ctx->params, np * sizeof(float), cudaMemcpyDeviceToDevice,
-                       ctx->stream));
-    CK(launch_prolong(ctx->scratch, ctx->params, P, ctx->N, ctx->cfg.prolong_mode, ctx->stream));
+    float* bufs[3] = {ctx->params, ctx->adam_m, ctx->adam_v};
+    for (int b = 0; b < (keep ? 3 : 1); ++b) {   // parameters, then (R14b) m and v by the same rule
+      CK(cudaMemcpyAsync(ctx->scratch, bufs[b], np * sizeof(float), cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+      CK(launch_prolong(ctx->scratch, bufs[b], P, ctx->N, pmode, ctx->stream));
+    }
   }
   ctx->N *= 2;
   ctx->level = level;
   const int64_t np2 = num_params_at(ctx, ctx->N);
-  CK(cudaMemsetAsync(ctx->adam_m, 0, np2 * sizeof(float), ctx->stream));
-  CK(cudaMemsetAsync(ctx->adam_v, 0, np2 * sizeof(float), ctx->stream));
-  DeviceState hs;
-  int rc = read_state(ctx, &hs);
-  if (rc != BSDE_OK) return rc;
-  hs.t = 0;
-  CK(cudaMemcpyAsync(ctx->state, &hs, sizeof hs, cudaMemcpyHostToDevice, ctx->stream));
+  int rc;
+  if (!keep) {   // R14: the optimizer restarts on the fine grid
+    CK(cudaMemsetAsync(ctx->adam_m, 0, np2 * sizeof(float), ctx->stream));
+    CK(cudaMemsetAsync(ctx->adam_v, 0, np2 * sizeof(float), ctx->stream));
+    DeviceState hs;
+    rc = read_state(ctx, &hs);
+    if (rc != BSDE_OK) return rc;
+    hs.t = 0;
+    CK(cudaMemcpyAsync(ctx->state, &hs, sizeof hs, cudaMemcpyHostToDevice, ctx->stream));
+  }
   rc = repack(ctx);
   if (rc != BSDE_OK) return rc;
   CK(cudaStreamSynchronize(ctx->stream));

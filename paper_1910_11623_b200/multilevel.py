@@ -8,7 +8,8 @@ sizes h_l = h_0 M^{-l}; the experiments use 2, 4, 8, 16 and 32 steps
 
 This is host-side control only: each level runs `bsde_train_step` on the
 device, and a level change is one `bsde_prolongate` call (copy or midpoint
-prolongation of the per-step nets, Adam state reset, R14).  Evaluation uses a
+prolongation of the per-step nets; the Adam state reset, R14, or prolonged with the
+parameters when the context was created with keep_adam, R14b).  Evaluation uses a
 fixed evaluation stream (`bsde_eval_loss`) so that losses at different
 iterations are comparable; evaluation time is excluded from the training clock.
 """

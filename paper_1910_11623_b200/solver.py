@@ -77,11 +77,13 @@ class BSDE:
                  stream=None, rank=0, world=1, nccl_id=None, use_graph=True, beta1=0.9,
                  beta2=0.999, eps=1e-8, zero_head=None, coupled_paths=False,
                  formulation="per_step", arch="fc", layers=4, sharded_adam=False,
-                 workspace=None, deterministic=False, zN=False):
+                 workspace=None, deterministic=False, zN=False, keep_adam=False):
         """stream: a torch.cuda.Stream, a raw cudaStream_t (int), or None (a new
         torch stream on `device`, kept in self.stream).  zero_head: R7b, defaults
         to True for Allen-Cahn.  coupled_paths: every level draws the finest grid's
         (N·2^max_levels) Brownian path, summed per coarse step (NEXT-3).
+        keep_adam: at a level change prolong the Adam moments like the parameters and
+        keep t (R14b) instead of resetting them (R14).
         formulation="shared": the paper's own method (one tanh network u(t, x) of
         `layers` layers of `width`, arch "fc" | "resnet", Eq. 6 loss; NEXT-1)."""
         L = _lib.lib()
@@ -95,6 +97,8 @@ class BSDE:
         cfg.precision = PRECISIONS[precision] if isinstance(precision, str) else int(precision)
         cfg.kernel = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
         cfg.prolong_mode = PROLONG[prolong] if isinstance(prolong, str) else int(prolong)
+        if keep_adam:
+            cfg.prolong_mode |= _lib.PROLONG_KEEP_ADAM
         cfg.max_levels = int(max_levels)
         cfg.device = int(device)
         self.stream = None

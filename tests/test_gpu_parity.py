@@ -187,6 +187,41 @@ def test_prolongate_matches_oracle(mode):
         s.prolongate(3)
 
 
+@pytest.mark.parametrize("mode,kernel", [("copy", "simt"), ("interp", "simt"), ("copy", "tc")])
+def test_prolongate_keep_adam_matches_oracle(mode, kernel):
+    """R14b (BSDE_PROLONG_KEEP_ADAM): the Adam moments follow the parameters'
+    prolongation on the device (oracle.prolongate_adam of the pre-change state), t is
+    kept, and the next update is Adam from that state (teacher-forced on the
+    context's own gradient)."""
+    d, w, N, B = (10, 20, 5, 64) if kernel == "tc" else (6, 9, 5, 64)   # tc: a built shape
+    prec = "bf16" if kernel == "tc" else "fp32"
+    s = make("hjb", d, w, N, 1.0, B, kernel=kernel, precision=prec, max_levels=2, prolong=mode,
+             keep_adam=True)
+    for _ in range(3):
+        s.train_step()
+    m, v, t = s.get_adam_state()
+    s.prolongate(1)
+    om = ob.COPY if mode == "copy" else ob.INTERP
+    st = ob.AdamState(m.size)
+    st.m, st.v, st.t = m.astype(np.float64), v.astype(np.float64), t
+    ref = ob.prolongate_adam(st, d, w, N, om)
+    m2, v2, t2 = s.get_adam_state()
+    assert t2 == t == 3 and m2.size == ref.m.size
+    if mode == "copy":
+        assert np.array_equal(m2, ref.m.astype(np.float32)) and np.array_equal(v2, ref.v.astype(np.float32))
+    else:
+        assert np.allclose(m2, ref.m, rtol=1e-6, atol=1e-12) and np.allclose(v2, ref.v, rtol=1e-6, atol=1e-15)
+    q = s.get_params().astype(np.float64)
+    s.train_step()
+    g = s.get_grads().astype(np.float64)
+    st2 = ob.AdamState(q.size)
+    st2.m, st2.v, st2.t = m2.astype(np.float64), v2.astype(np.float64), t2
+    assert ob.adam_step(q, g, st2, 1e-2)
+    got = s.get_params()
+    assert np.allclose(got, q, rtol=0, atol=2e-6), np.abs(got - q).max()
+    assert s.get_adam_state()[2] == t2 + 1
+
+
 @pytest.mark.parametrize("problem,x0", [("hjb", 0.0), ("black_scholes", 0.7)])
 def test_coupled_paths_match_oracle(problem, x0):
     """Coupled multilevel paths (NEXT-3): at every level of N = 5 -> 10 -> 20 the

@@ -281,6 +281,52 @@ def test_prolongate_copy_and_interp():
     assert np.array_equal(i[-1], src[-1])
 
 
+def test_keep_adam_prolongation_commutes_with_adam():
+    """R14b (keep the Adam state across a level change): Adam is elementwise, so with
+    copy prolongation of the parameters *and* the moments (t kept) one Adam step on
+    the fine grid, restricted to the even steps 2c, is the coarse Adam step with
+    that restricted gradient.  A reset moment, a reset t (bias correction), or
+    moments shifted against their parameters break it; an odd fine step 2c+1 with
+    gradient g equals the coarse update with g as well."""
+    d, w, N = 3, 4, 3
+    P = bsde.step_size(d, w)
+    rng = np.random.default_rng(5)
+    p = bsde.init_params(1, d, w, N)
+    st = bsde.AdamState(p.size)
+    for _ in range(3):   # a non-trivial coarse state (t = 3, m, v != 0)
+        assert bsde.adam_step(p, rng.normal(size=p.size), st, 1e-2)
+    q = bsde.prolongate(p, d, w, N, bsde.COPY)
+    sf = bsde.prolongate_adam(st, d, w, N, bsde.COPY)
+    assert sf.t == st.t and sf.m.size == q.size
+    g = rng.normal(size=q.size)
+    assert bsde.adam_step(q, g, sf, 1e-2)
+    for par in (0, 1):
+        sel = np.concatenate([[0], (np.arange(2 * N * P).reshape(2 * N, P)[par::2] + 1).reshape(-1)])
+        pc, sc = p.copy(), bsde.AdamState(p.size)
+        sc.m, sc.v, sc.t = st.m.copy(), st.v.copy(), st.t
+        assert bsde.adam_step(pc, g[sel], sc, 1e-2)
+        assert np.allclose(q[sel], pc, rtol=0, atol=1e-15)
+        assert np.allclose(sf.m[sel], sc.m, rtol=0, atol=1e-15)
+    # against the R14 reset: the first fine step then moves every entry by ~lr
+    q2, s2 = bsde.prolongate(p, d, w, N, bsde.COPY), bsde.AdamState(q.size)
+    bsde.adam_step(q2, g, s2, 1e-2)
+    assert not np.allclose(q2, q)
+    # the interp rule moves the moments with their parameters (midpoints of both)
+    si = bsde.prolongate_adam(st, d, w, N, bsde.INTERP)
+    mi = si.m[1:].reshape(2 * N, P)
+    src = st.m[1:].reshape(N, P)
+    assert np.allclose(mi[1], 0.5 * (src[0] + src[1])) and np.array_equal(mi[-1], src[-1])
+
+
+def test_keep_adam_schedule_one_level_is_single_level():
+    """With one level the keep-Adam schedule is plain training (no level change)."""
+    d, w, N, T, B = 3, 4, 2, 1.0, 16
+    p0 = bsde.init_params(0, d, w, N)
+    a, _ = bsde.train_multilevel(bsde.HJB, d, w, [N], T, p0.copy(), 0, B, [3], 1e-2, keep_adam=True)
+    b, _, _ = bsde.train(bsde.HJB, d, w, N, T, p0.copy(), 0, B, 3, 1e-2)
+    assert np.array_equal(a, b)
+
+
 def test_prolongated_heat_optimum_stays_optimal():
     """The heat optimum is time-independent, so its prolongation is the optimum
     on the 2N grid: the path-wise identity holds there too (floor 8dT²/(2N))."""
