@@ -222,6 +222,27 @@ def test_prolongate_keep_adam_matches_oracle(mode, kernel):
     assert s.get_adam_state()[2] == t2 + 1
 
 
+@pytest.mark.parametrize("keep", [False, True])
+def test_multilevel_schedule_matches_oracle(keep):
+    """The multilevel schedule end to end through the C-ABI (run_schedule: train
+    steps, bsde_prolongate between levels N = 2 -> 4 -> 8) against the oracle's
+    train_multilevel with the same Adam rule at the level changes (R14 reset or
+    R14b kept): the per-iteration losses and the final parameters."""
+    from paper_1910_11623_b200.multilevel import run_schedule
+    d, w, B, T, iters = 6, 9, 64, 1.0, [6, 6, 4]
+    s = make("hjb", d, w, 2, T, B, kernel="simt", max_levels=2, keep_adam=keep)
+    p0 = s.get_params().astype(np.float64)
+    res = run_schedule(s, iters, eval_every=0)
+    pr, hist = ob.train_multilevel(ob.HJB, d, w, [2, 4, 8], T, p0.copy(), 0, B, iters, 1e-2,
+                                   keep_adam=keep)
+    got = np.array([r.train_loss for r in res.records])
+    ref = np.array([h[2] for h in hist])
+    assert np.allclose(got, ref, rtol=1e-4), np.abs(got / ref - 1).max()
+    q = s.get_params().astype(np.float64)
+    assert np.linalg.norm(q - pr) <= 1e-4 * np.linalg.norm(pr)
+    assert s.get_adam_state()[2] == (sum(iters) if keep else iters[-1])
+
+
 @pytest.mark.parametrize("problem,x0", [("hjb", 0.0), ("black_scholes", 0.7)])
 def test_coupled_paths_match_oracle(problem, x0):
     """Coupled multilevel paths (NEXT-3): at every level of N = 5 -> 10 -> 20 the
