@@ -257,7 +257,9 @@ def main():
                     help="skip the config-4 multilevel time-to-target sub-object (rank 0, N = 1)")
     ap.add_argument("--ml-iters", type=int, default=10000,
                     help="single-level iterations of the multilevel experiment")
-    ap.add_argument("--ml-precision", default="bf16")
+    ap.add_argument("--ml-precision", default="fp32",
+                    help="config 4 is fp32 in BASELINE.json (as config 2): the fp32-accurate "
+                         "tc32 kernels by default; bf16 for a quick run")
     ap.add_argument("--sharded-adam", action="store_true",
                     help="reduce-scatter + sharded Adam + all-gather (NEXT-4) for N > 1")
     ap.add_argument("--fused-opt", action="store_true",
@@ -504,9 +506,10 @@ def main():
             s = None
             from bench_multilevel import run_cfg4
             ml = run_cfg4(args.ml_precision, args.ml_iters, alt=[(1000, False)])
-            ml["note"] = ("config 4 (HJB d=100, N 5->80, B=65536) with %s operands on the %s "
-                          "kernels; time-to-target = training wall clock (evaluations excluded) "
-                          "until the eval loss <= target" % (args.ml_precision, ml["kernel"]))
+            ml["note"] = ("config 4 (HJB d=100, N 5->80, B=65536), precision %s on the %s kernels "
+                          "(tc32 = fp32-accurate bf16x3 split operands, R18b); time-to-target = "
+                          "training wall clock (evaluations excluded) until the eval loss <= target"
+                          % (args.ml_precision, ml["kernel"]))
             line["multilevel"] = ml
         print(json.dumps(line), flush=True)
     if s is not None:
