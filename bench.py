@@ -505,7 +505,8 @@ def main():
             s.close()
             s = None
             from bench_multilevel import run_cfg4
-            ml = run_cfg4(args.ml_precision, args.ml_iters, alt=[(1000, False)])
+            ml = run_cfg4(args.ml_precision, args.ml_iters,
+                          alt=[(1000, False, "copy"), (1000, True, "copy")])
             ml["note"] = ("config 4 (HJB d=100, N 5->80, B=65536), precision %s on the %s kernels "
                           "(tc32 = fp32-accurate bf16x3 split operands, R18b); time-to-target = "
                           "training wall clock (evaluations excluded) until the eval loss <= target"

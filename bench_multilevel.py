@@ -1,19 +1,21 @@
 """Multilevel time-to-target-loss experiment (BASELINE.json config 4).
 
-    python bench_multilevel.py [--precision fp32|bf16] [--iters 10000] [--per-level 1000] [--reset-adam]
+    python bench_multilevel.py [--precision fp32|bf16] [--iters 10000] [--per-level 1000]
+                               [--prolong interp|copy] [--keep-adam]
 
 Single-level baseline: HJB d = 100, w = 110, N = 80, B = 65 536 paths, Adam lr
 1e-2, `--iters` iterations (10 000: enough for Y0 to settle within 0.5% of the
 Cole-Hopf value, which 2 000 are not); the target loss L* is 1.01 × its final loss, the
 mean of its last 5 evaluations on the fixed evaluation stream (eval_id 0,
 65 536 paths, the current grid).  Multilevel: N = 5 -> 10 -> 20 -> 40 -> 80 with
-`--per-level` iterations per level (copy prolongation; the Adam moments prolonged
-with the parameters and t kept, R14b, or reset with `--reset-adam`, R14); the
-N = 80 level may run up to `--iters` extra iterations until L* is reached.
-The per-level budget and the Adam rule were chosen by `tools/ml_sweep.py`
-(profiles/r02_ml_sweep.txt): with the R14 reset the coarse levels barely help
-(1.3-2.5x, the restarted Adam kicks every weight by ~lr), with R14b and >= 1 000
-iterations per level the fine grid starts close to the target (3.7-4.0x).
+`--per-level` iterations per level (midpoint prolongation by default, `--prolong
+copy`; the Adam state reset, R14, or kept with `--keep-adam`, R14b); the N = 80 level
+may run up to `--iters` extra iterations until L* is reached.  The per-level budget
+and the prolongation were chosen by `tools/ml_sweep.py` (profiles/r02_ml_sweep.txt):
+1 000 iterations per level settle Y0 on the coarse grids (400 or 600 do not); copy
+prolongation with the R14 reset gains only 1.3-2.5x (the restarted Adam kicks every
+weight by ~lr and the fine grid retrains), keeping the Adam state 3.7-4.6x, midpoint
+prolongation with the reset 6-8x (the N = 80 nets start at the target).
 Wall clock counts training steps only (evaluations excluded) and is reported
 for both runs with their ratio; Y0 per level is compared with the Cole-Hopf
 value u(0,0) = 4.590161724605 (pin H4).  Prints one JSON line.
@@ -32,13 +34,13 @@ from workloads import CONFIGS  # noqa: E402
 COLE_HOPF = 4.590161724605
 
 
-def run_cfg4(precision="bf16", iters=10000, per_level=1000, eval_every=50, batch=0, kernel="auto",
-             keep_adam=True, alt=None):
+def run_cfg4(precision="fp32", iters=10000, per_level=1000, eval_every=50, batch=0, kernel="auto",
+             keep_adam=False, prolong="interp", alt=None):
     """BASELINE config 4 on the device: single-level N = 80 for `iters` iterations,
-    then the multilevel schedule (`per_level` iterations per level, the Adam state kept
-    across level changes, R14b, or reset, R14); returns the result dict (see the module
-    doc).  `alt` = [(per_level, keep_adam), ...]: further schedules timed to the same
-    target in the same run (reported under "other_schedules")."""
+    then the multilevel schedule (`per_level` iterations per level, `prolong` "copy" or
+    "interp", the Adam state reset, R14, or kept across level changes, R14b); returns the
+    result dict (see the module doc).  `alt` = [(per_level, keep_adam, prolong), ...]:
+    further schedules timed to the same target in the same run ("other_schedules")."""
     import numpy as np
     import torch
     from paper_1910_11623_b200 import BSDE
@@ -65,20 +67,21 @@ def run_cfg4(precision="bf16", iters=10000, per_level=1000, eval_every=50, batch
     single.close()
     torch.cuda.synchronize()
 
-    def schedule(per, keep):
+    def schedule(per, keep, pro):
         m = BSDE(wl.problem, wl.d, levels[0], wl.T, wl.w, B, max_levels=len(levels) - 1,
-                 keep_adam=keep, **kw)
+                 keep_adam=keep, prolong=pro, **kw)
         r = run_schedule(m, [per] * len(levels), eval_every=eval_every, eval_batch=B,
                          target_loss=target, final_N=Nf, extend_last=iters)
         m.close()
         torch.cuda.synchronize()
         return r
 
-    res_m = schedule(per_level, keep_adam)
+    res_m = schedule(per_level, keep_adam, prolong)
     others = []
-    for per, keep in (alt or []):
-        r = schedule(per, keep)
-        others.append({"per_level_iters": per, "adam_at_level_change": "kept (R14b)" if keep else "reset (R14)",
+    for per, keep, pro in (alt or []):
+        r = schedule(per, keep, pro)
+        others.append({"per_level_iters": per, "prolongation": pro,
+                       "adam_at_level_change": "kept (R14b)" if keep else "reset (R14)",
                        "time_to_target_s": r.time_to_target, "iteration_at_target": r.iteration_at_target,
                        "speedup_to_target": (t_single_target / r.time_to_target
                                              if r.time_to_target and t_single_target else None)})
@@ -86,6 +89,7 @@ def run_cfg4(precision="bf16", iters=10000, per_level=1000, eval_every=50, batch
         "experiment": "multilevel time-to-target (config 4)",
         "precision": precision, "kernel": family, "batch": B, "levels": levels,
         "per_level_iters": per_level, "single_level_iters": iters, "eval_every": eval_every,
+        "prolongation": prolong,
         "adam_at_level_change": "kept: m, v prolonged like the parameters, t kept (R14b)" if keep_adam
                                 else "reset (R14)",
         "target_rule": "1.01 x the single-level run's final evaluation loss (mean of its last 5 "
@@ -114,7 +118,8 @@ def main():
     ap.add_argument("--precision", default="bf16")
     ap.add_argument("--iters", type=int, default=10000)
     ap.add_argument("--per-level", type=int, default=1000)
-    ap.add_argument("--reset-adam", action="store_true", help="R14: reset Adam at each level change")
+    ap.add_argument("--keep-adam", action="store_true", help="R14b: keep the Adam state across level changes")
+    ap.add_argument("--prolong", default="interp", choices=["copy", "interp"])
     ap.add_argument("--eval-every", type=int, default=50)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--workload", default="cfg4", choices=["cfg4", "shared_bs_paper"])
@@ -123,7 +128,7 @@ def main():
     if args.workload == "shared_bs_paper":
         return shared_paper(args)
     print(json.dumps(run_cfg4(args.precision, args.iters, args.per_level, args.eval_every,
-                              args.batch, keep_adam=not args.reset_adam)), flush=True)
+                              args.batch, keep_adam=args.keep_adam, prolong=args.prolong)), flush=True)
 
 
 def shared_paper(args):

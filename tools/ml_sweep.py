@@ -46,10 +46,10 @@ def main():
     single.close()
     torch.cuda.synchronize()
     for var in args.variants.split(",") * args.reps:
-        per, mode = var.split(":")
+        per, mode, *pro = var.split(":")   # per-level:reset|carry[:copy|interp]
         per = int(per)
         s = BSDE(wl.problem, wl.d, levels[0], wl.T, wl.w, B, max_levels=len(levels) - 1,
-                 keep_adam=(mode == "carry"), **kw)
+                 keep_adam=(mode == "carry"), prolong=(pro[0] if pro else "copy"), **kw)
         rm = run_schedule(s, [per] * (len(levels) - 1) + [per], eval_every=args.eval_every, eval_batch=B,
                           target_loss=target, final_N=Nf, extend_last=args.iters)
         coarse = next((r.train_seconds for r in rm.records if r.N == Nf), None)
