@@ -102,6 +102,10 @@ def run_cfg4(precision="fp32", iters=10000, per_level=1000, eval_every=50, batch
         "speedup_to_target": (t_single_target / res_m.time_to_target
                               if res_m.time_to_target and t_single_target else None),
         "multilevel_final_eval_loss": res_m.final_eval_loss,
+        # the multilevel run's own converged level on the finest grid, by the rule that set
+        # the target (mean of its last 5 evaluations): not a first-crossing dip
+        "multilevel_final_eval_mean5": float(np.mean([r.eval_loss for r in res_m.records
+                                                      if r.eval_loss is not None][-5:])),
         "y0_single": y0_single, "y0_per_level": res_m.y0_per_level,
         "cole_hopf_u0": COLE_HOPF,
         "single_converged": abs(y0_single / COLE_HOPF - 1.0) < 5e-3,
