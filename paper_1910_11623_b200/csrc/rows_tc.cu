@@ -693,8 +693,10 @@ __global__ void __launch_bounds__(RT, 2) k_rows_gemm_t(RowsArgs a) {
 }
 
 // ------------------------------------------------------------------ fused forward F1 + F2
-// Compile-time shapes: one CTA per SM walks the 128-row tiles of step n = blockIdx.y
-// with W̃1 and W̃2 (hi / lo) resident, the next tile's X̃ rows in flight:
+// Compile-time shapes: one CTA per SM walks a contiguous range of the (step n, 128-row
+// tile) items in step-major order (one wave at any N; a grid of ⌊#SM/N⌋ × N CTAs left
+// 68 SMs idle at N = 80) with the step's W̃1 and W̃2 (hi / lo) resident, reloaded when
+// the range crosses a step, the next item's X̃ rows in flight:
 //   G1  A1 = X̃ W̃1ᵀ   (X̃ converted from the fp32 rows the path kernel wrote; its image
 //                     replaces them in place, for dW̃1)
 //   E1  H1 = ReLU(A1): the G2 operand (shared memory) and the H1 image (for dW̃2), mask
@@ -721,7 +723,12 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
   uint8_t* ahi = w2l + MB2;
   uint8_t* alo = ahi + AB;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int n = blockIdx.y;
+  // (step, tile) items in step-major order, a contiguous range per CTA (one wave of one
+  // CTA per SM at any N; the weights are reloaded when the range crosses a step)
+  const int ntiles = (int)((a.B + 127) / 128);
+  const int64_t items = (int64_t)a.N * ntiles;
+  const int64_t it0 = blockIdx.x * items / gridDim.x, it1 = (blockIdx.x + 1) * items / gridDim.x;
+  int n = (int)(it0 / ntiles);
   if (t == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -732,8 +739,8 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
   __syncthreads();
   tc_after();
   const uint32_t tm = tslot;
-  if (t == 0) {   // step n's W̃1 and W̃2 (hi, lo)
-    const uint8_t* wsrc = a.wimg + (size_t)n * 2 * WB;
+  auto load_w = [&](int nn) {   // step nn's W̃1 and W̃2 (hi, lo); thread 0
+    const uint8_t* wsrc = a.wimg + (size_t)nn * 2 * WB;
     const uint32_t o2 = MB1;
     mbar_expect_tx(&bars[0], 2 * (MB1 + MB2));
     for (uint32_t o = 0; o < MB1; o += 16384u) {
@@ -744,17 +751,17 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
       bulk_g2s(w2h + o, wsrc + o2 + o, min(16384u, MB2 - o), &bars[0]);
       bulk_g2s(w2l + o, wsrc + WB + o2 + o, min(16384u, MB2 - o), &bars[0]);
     }
-  }
-  const int ntiles = (int)((a.B + 127) / 128);
+  };
+  if (t == 0 && it0 < it1) load_w(n);
   const int q = warp & 3, h = warp >> 2, rr = 32 * q + lane;
   const uint32_t lb = tm + ((uint32_t)(32 * q) << 16);
   const int cb = h * (WP / 2);
   constexpr uint32_t idesc = idesc_bf16(128, WP, false, false);
   const bool store = !a.eval;
   float4 v[U];
-  auto load = [&](int tile) {   // X̃ rows of `tile` (fp32, from the path kernel), all loads in flight
+  auto load = [&](int nn, int tile) {   // X̃ rows of item (nn, tile) (fp32, from the path kernel)
     const int64_t i0 = (int64_t)tile * 128;
-    const float* base = a.XT + ((size_t)n * a.Bs + i0) * DP;
+    const float* base = a.XT + ((size_t)nn * a.Bs + i0) * DP;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = t + u * RT;
@@ -773,10 +780,12 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
         make_uint4(m0.x | m1.x, m0.y | m1.y, m0.z | m1.z, m0.w | m1.w);
   };
   float h1[NCH8 * 8];   // H1 of this thread's row and column half (E1 -> E2)
-  uint32_t mph = 0;
-  bool first = true;
-  if ((int)blockIdx.x < ntiles) load(blockIdx.x);
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  uint32_t mph = 0, wph = 0;
+  bool wait_w = true;   // the weights of step n are being loaded
+  int tile = (int)(it0 - (int64_t)n * ntiles);
+  if (it0 < it1) load(n, tile);
+  for (int64_t item = it0; item < it1; ++item) {
+    const int nn = tile + 1 == ntiles ? n + 1 : n, ntile = tile + 1 == ntiles ? 0 : tile + 1;
     const int64_t i0 = (int64_t)tile * 128;
     // X̃ -> bf16 hi / lo A image (K = DP), and the same bytes over the tile's fp32 rows
     // in memory (the X̃ image of dW̃1; a warp writes two whole 128-byte core matrices)
@@ -797,20 +806,20 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
         *reinterpret_cast<uint2*>(xd + XIMG + o) = lo;
       }
     }
-    if (tile + (int)gridDim.x < ntiles) load(tile + gridDim.x);   // in flight until the next tile
+    if (item + 1 < it1) load(nn, ntile);   // in flight until the next item
     fence_async_smem();
     tc_before();
     __syncthreads();
     if (t == 0) {   // G1: A1 = X̃ W̃1ᵀ; the X̃ image over this tile's fp32 rows (for dW̃1)
       tc_after();
-      if (first) mbar_wait(&bars[0], 0);
+      if (wait_w) { mbar_wait(&bars[0], wph); wph ^= 1; }
       const Opnd Ah = kmaj(ahi, DP), Al = kmaj(alo, DP), Wh = kmaj(w1h, DP), Wl = kmaj(w1l, DP);
       gemm(tm, Ah, Wh, DP / 16, idesc, false);
       gemm(tm, Ah, Wl, DP / 16, idesc, true);
       gemm(tm, Al, Wh, DP / 16, idesc, true);
       mma_commit(&bars[1]);
     }
-    first = false;
+    wait_w = false;
     mbar_wait(&bars[1], mph);
     mph ^= 1;
     tc_after();
@@ -897,6 +906,12 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
     __syncthreads();
     out_masks(i0, a.M2);
     __syncthreads();   // mask words read before the next tile's E1
+    if (item + 1 < it1 && nn != n) {   // G1 and G2 of step n have completed: its weights are free
+      if (t == 0) load_w(nn);
+      wait_w = true;
+    }
+    n = nn;
+    tile = ntile;
   }
   tc_before();
   __syncthreads();
@@ -907,9 +922,10 @@ __global__ void __launch_bounds__(RT, 1) k_rows_f12_t(RowsArgs a) {
 }
 
 // ------------------------------------------------------------------ fused adjoint B1 + B2
-// Compile-time shapes: one CTA per SM walks the 128-row tiles of step n = blockIdx.y
-// with the step's W̃3 and W̃2 images (hi / lo) resident, the next tile's G rows in
-// flight while the current one computes:
+// Compile-time shapes: one CTA per SM walks a contiguous range of the (step n, 128-row
+// tile) items in step-major order with the step's W̃3 and W̃2 images (hi / lo) resident
+// (reloaded when the range crosses a step), the next item's G rows in flight while the
+// current one computes:
 //   G4  dH2 = dZ W̃3, dZ = ā_{n+1} G (staged as bf16 hi / lo; its image replaces the
 //       tile's G rows in place, the A operand of dW̃3)
 //   E4  dA2 = dH2 ⊙ 1[A2 > 0] (mask words from F2): the dA2 image (dW̃2) and, in shared
@@ -935,7 +951,12 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
   uint8_t* ahi = w2l + MB2;
   uint8_t* alo = ahi + AB;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int n = blockIdx.y;
+  // (step, tile) items in step-major order, a contiguous range per CTA (one wave of one
+  // CTA per SM at any N; the weights are reloaded when the range crosses a step)
+  const int ntiles = (int)((a.B + 127) / 128);
+  const int64_t items = (int64_t)a.N * ntiles;
+  const int64_t it0 = blockIdx.x * items / gridDim.x, it1 = (blockIdx.x + 1) * items / gridDim.x;
+  int n = (int)(it0 / ntiles);
   if (t == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -946,8 +967,8 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
   __syncthreads();
   tc_after();
   const uint32_t tm = tslot;
-  if (t == 0) {   // step n's W̃3 and W̃2 (hi, lo)
-    const uint8_t* wsrc = a.wimg + (size_t)n * 2 * WB;
+  auto load_w = [&](int nn) {   // step nn's W̃3 and W̃2 (hi, lo); thread 0
+    const uint8_t* wsrc = a.wimg + (size_t)nn * 2 * WB;
     const uint32_t o3 = 2u * (WP * DP + WP * WP), o2 = 2u * WP * DP;
     mbar_expect_tx(&bars[0], 2 * (MB3 + MB2));
     for (uint32_t o = 0; o < MB3; o += 16384u) {
@@ -958,16 +979,16 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
       bulk_g2s(w2h + o, wsrc + o2 + o, min(16384u, MB2 - o), &bars[0]);
       bulk_g2s(w2l + o, wsrc + WB + o2 + o, min(16384u, MB2 - o), &bars[0]);
     }
-  }
-  const int ntiles = (int)((a.B + 127) / 128);
+  };
+  if (t == 0 && it0 < it1) load_w(n);
   const int q = warp & 3, h = warp >> 2, rr = 32 * q + lane;
   const uint32_t lb = tm + ((uint32_t)(32 * q) << 16);
   const int cb = h * (WP / 2);
   constexpr uint32_t idesc = idesc_bf16(128, WP, false, true);
   float4 v[U];
-  auto load = [&](int tile) {   // G rows of `tile`, all loads in flight
+  auto load = [&](int nn, int tile) {   // G rows of item (nn, tile), all loads in flight
     const int64_t i0 = (int64_t)tile * 128;
-    const float* base = a.GW + ((size_t)n * a.Bs + i0) * DP;
+    const float* base = a.GW + ((size_t)nn * a.Bs + i0) * DP;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = t + u * RT;
@@ -1010,11 +1031,11 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
   };
   // ā_{n+1} of a tile's rows (threads t < 128), loaded one tile ahead like G
   float pab = 0.0f, ppn = 1.0f;
-  auto load_ab = [&](int tile) {
+  auto load_ab = [&](int nn, int tile) {
     const int64_t m = (int64_t)tile * 128 + t;
     if (t < 128 && m < a.B) {
       pab = __ldg(a.abar + m);
-      ppn = per_step_abar(a.problem) ? __ldg(a.Pstore + (int64_t)n * a.B + m) : 1.0f;
+      ppn = per_step_abar(a.problem) ? __ldg(a.Pstore + (int64_t)nn * a.B + m) : 1.0f;
     } else {
       pab = 0.0f;
       ppn = 1.0f;
@@ -1022,17 +1043,19 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
   };
   // this thread's row masks (TMEM lane layout: row rr), also one tile ahead
   uint4 mk1n = make_uint4(0, 0, 0, 0), mk2n = make_uint4(0, 0, 0, 0);
-  auto load_mk = [&](int tile) {
+  auto load_mk = [&](int nn, int tile) {
     const int64_t mrow = (int64_t)tile * 128 + rr;
-    const size_t ro = ((size_t)n * a.Bs + (size_t)mrow) * 4;
+    const size_t ro = ((size_t)nn * a.Bs + (size_t)mrow) * 4;
     const bool ok = mrow < a.B;
     mk2n = ok ? __ldg(reinterpret_cast<const uint4*>(a.M2 + ro)) : make_uint4(0, 0, 0, 0);
     mk1n = ok ? __ldg(reinterpret_cast<const uint4*>(a.M1 + ro)) : make_uint4(0, 0, 0, 0);
   };
-  uint32_t mph = 0;
-  bool first = true;
-  if ((int)blockIdx.x < ntiles) { load(blockIdx.x); load_ab(blockIdx.x); load_mk(blockIdx.x); }
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  uint32_t mph = 0, wph = 0;
+  bool wait_w = true;   // the weights of step n are being loaded
+  int tile = (int)(it0 - (int64_t)n * ntiles);
+  if (it0 < it1) { load(n, tile); load_ab(n, tile); load_mk(n, tile); }
+  for (int64_t item = it0; item < it1; ++item) {
+    const int nn = tile + 1 == ntiles ? n + 1 : n, ntile = tile + 1 == ntiles ? 0 : tile + 1;
     const int64_t i0 = (int64_t)tile * 128;
     if (t < 128) srow[t] = __fdividef(pab, ppn);   // 0 past B (pab = 0)
     __syncthreads();
@@ -1055,24 +1078,24 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
       *reinterpret_cast<uint2*>(zd + ZIMG + o) = lo;
     }
     const uint4 mk1 = mk1n, mk2 = mk2n;
-    if (tile + (int)gridDim.x < ntiles) {   // in flight until the next tile
-      load(tile + gridDim.x);
-      load_ab(tile + gridDim.x);
-      load_mk(tile + gridDim.x);
+    if (item + 1 < it1) {   // in flight until the next item
+      load(nn, ntile);
+      load_ab(nn, ntile);
+      load_mk(nn, ntile);
     }
     fence_async_smem();
     tc_before();
     __syncthreads();
     if (t == 0) {   // G4: dH2 = dZ W̃3; the dZ image over this tile's G rows (for dW̃3)
       tc_after();
-      if (first) mbar_wait(&bars[0], 0);
+      if (wait_w) { mbar_wait(&bars[0], wph); wph ^= 1; }
       const Opnd Ah = kmaj(ahi, DP), Al = kmaj(alo, DP), Wh = mnmaj(w3h, WP), Wl = mnmaj(w3l, WP);
       gemm(tm, Ah, Wh, DP / 16, idesc, false);
       gemm(tm, Ah, Wl, DP / 16, idesc, true);
       gemm(tm, Al, Wh, DP / 16, idesc, true);
       mma_commit(&bars[1]);
     }
-    first = false;
+    wait_w = false;
     mbar_wait(&bars[1], mph);
     mph ^= 1;
     tc_after();
@@ -1094,6 +1117,12 @@ __global__ void __launch_bounds__(RT, 1) k_rows_b12_t(RowsArgs a) {
     epilogue(mk1, tile_img(a.DA, a, n, i0, WP), false);   // E6: dA1
     tc_before();
     __syncthreads();   // accumulator and A images read before the next tile
+    if (item + 1 < it1 && nn != n) {   // G4 and G6 of step n have completed: its weights are free
+      if (t == 0) load_w(nn);
+      wait_w = true;
+    }
+    n = nn;
+    tile = ntile;
   }
   tc_before();
   __syncthreads();
@@ -1545,11 +1574,10 @@ cudaError_t launch_rows_forward(const RowsArgs& a, cudaStream_t s, int* launches
     const size_t smf = 2 * (size_t)WP_ * DP_ * 2 + 2 * (size_t)WP_ * WP_ * 2 + 2 * 128 * (size_t)KM_ * 2; \
     RCK(cudaFuncSetAttribute(rows::k_rows_f12_t<DP_, WP_>,                                         \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf));              \
-    int g = rows::sm_count() / a.N;                                                                \
-    const int nt = (int)((a.B + 127) / 128);                                                       \
-    if (g > nt) g = nt;                                                                            \
-    if (g < 1) g = 1;                                                                              \
-    rows::k_rows_f12_t<DP_, WP_><<<dim3((unsigned)g, (unsigned)a.N), rows::RT, smf, s>>>(a);       \
+    const int64_t nit = (int64_t)a.N * ((a.B + 127) / 128);   /* (step, tile) items */         \
+    const int64_t sm_ = rows::sm_count();                                                                \
+    const unsigned g = (unsigned)(nit < 1 ? 1 : (nit < sm_ ? nit : sm_));                       \
+    rows::k_rows_f12_t<DP_, WP_><<<g, rows::RT, smf, s>>>(a);                                     \
     RCK(cudaGetLastError());                                                                       \
     fused = true;                                                                                  \
   }
@@ -1576,11 +1604,10 @@ cudaError_t launch_rows_backward(const RowsArgs& a, cudaStream_t s, int* launche
     const size_t smb = 2 * (size_t)DP_ * WP_ * 2 + 2 * (size_t)WP_ * WP_ * 2 + 2 * 128 * (size_t)KM_ * 2; \
     RCK(cudaFuncSetAttribute(rows::k_rows_b12_t<DP_, WP_>,                                         \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));              \
-    int g = sms / a.N;                                                                             \
-    const int nt = (int)((a.B + 127) / 128);                                                       \
-    if (g > nt) g = nt;                                                                            \
-    if (g < 1) g = 1;                                                                              \
-    rows::k_rows_b12_t<DP_, WP_><<<dim3((unsigned)g, (unsigned)a.N), rows::RT, smb, s>>>(a);       \
+    const int64_t nit = (int64_t)a.N * ((a.B + 127) / 128);   /* (step, tile) items */         \
+    const int64_t sm_ = sms;                                                                \
+    const unsigned g = (unsigned)(nit < 1 ? 1 : (nit < sm_ ? nit : sm_));                       \
+    rows::k_rows_b12_t<DP_, WP_><<<g, rows::RT, smb, s>>>(a);                                     \
     RCK(cudaGetLastError());                                                                       \
     fused = true;                                                                                  \
   }

@@ -15,6 +15,7 @@ sys.path.insert(0, %r)
 from paper_1910_11623_b200 import BSDE
 from workloads import CONFIGS
 wl = CONFIGS[%r]
+if %r: wl = wl.with_(N=%r)
 s = BSDE(wl.problem, wl.d, wl.N, wl.T, wl.w, wl.batch, lr=wl.lr, precision=%r, kernel=%r)
 for _ in range(3):
     try: s.train_step()
@@ -29,13 +30,14 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--workload", default="cfg5_allen_cahn_scaleout")
 ap.add_argument("--precision", default="bf16")
 ap.add_argument("--kernel", default="auto")
+ap.add_argument("--N", type=int, default=0, help="override the workload's number of steps")
 args = ap.parse_args()
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 res = {v: [] for v in args.variants}
 for rep in range(args.reps):
     for v in (args.variants if rep % 2 == 0 else args.variants[::-1]):
         env = dict(os.environ, BSDE_LIB=os.path.join(root, "build_variants", v + ".so"))
-        r = subprocess.run([sys.executable, "-c", CODE % (root, args.workload, args.precision, args.kernel)], env=env, capture_output=True, text=True)
+        r = subprocess.run([sys.executable, "-c", CODE % (root, args.workload, args.N, args.N, args.precision, args.kernel)], env=env, capture_output=True, text=True)
         try:
             res[v].append([float(x) for x in r.stdout.split()])
         except ValueError:
