@@ -280,7 +280,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
   constexpr int G = kFwdGroups;
   constexpr int NS = ((NCD > NCW ? NCD : NCW) + G - 1) / G;   // chunk slots per worker
   constexpr int NB = 2 * NS;                                   // Philox blocks per worker
-  constexpr int S1 = NB / 3, S2 = 2 * NB / 3;                  // slices [0,S1) [S1,S2) [S2,NB)
+#if defined(BSDE_FWD_S1) && defined(BSDE_FWD_S2)   // experiment builds: other slice splits
+  constexpr int S1 = BSDE_FWD_S1, S2 = BSDE_FWD_S2;
+#else
+  // slices [0,S1) [S1,S2) [S2,NB): 4 / 3 / 3 blocks at d = 100 (NB = 10; the front-loaded
+  // split covers G1, whose wait was the longest, and measured 1.6% faster than 3 / 3 / 4,
+  // profiles/r02_experiments.md), thirds for the small test shapes
+  constexpr int S1 = NB >= 9 ? (2 * NB + 2) / 5 : NB / 3, S2 = NB >= 9 ? (7 * NB + 5) / 10 : 2 * NB / 3;
+#endif
   extern __shared__ __align__(1024) uint8_t sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::BARS);
   uint64_t* bg = bars;          // chain GEMM commits (3 per step, in order)

@@ -43,7 +43,8 @@ for rep in range(args.reps):
         except ValueError:
             print(v, "failed:", r.stderr[-400:])
 for v, xs in res.items():
+    xs = [x for x in xs if len(x) == 3]
     if xs:
-        print("%-12s fwd %.3f  bwd %.3f  step %.3f   (best of %d; bwd runs %s)"
+        print("%-12s fwd %.3f  bwd %.3f  step %.3f   (best of %d; fwd runs %s; bwd runs %s)"
               % (v, min(x[0] for x in xs), min(x[1] for x in xs), min(x[2] for x in xs), len(xs),
-                 " ".join("%.3f" % x[1] for x in xs)))
+                 " ".join("%.3f" % x[0] for x in xs), " ".join("%.3f" % x[1] for x in xs)))
