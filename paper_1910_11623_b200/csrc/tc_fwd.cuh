@@ -280,8 +280,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
   constexpr int G = kFwdGroups;
   constexpr int NS = ((NCD > NCW ? NCD : NCW) + G - 1) / G;   // chunk slots per worker
   constexpr int NB = 2 * NS;                                   // Philox blocks per worker
-#if defined(BSDE_FWD_S1) && defined(BSDE_FWD_S2)   // experiment builds: other slice splits
-  constexpr int S1 = BSDE_FWD_S1, S2 = BSDE_FWD_S2;
+#if defined(BSDE_FWD_S1) && defined(BSDE_FWD_S2)   // experiment builds: other splits at d = 100
+  constexpr int S1 = NB >= 9 ? BSDE_FWD_S1 : NB / 3, S2 = NB >= 9 ? BSDE_FWD_S2 : 2 * NB / 3;
 #else
   // slices [0,S1) [S1,S2) [S2,NB): 4 / 3 / 3 blocks at d = 100 (NB = 10; the front-loaded
   // split covers G1, whose wait was the longest, and measured 1.6% faster than 3 / 3 / 4,
