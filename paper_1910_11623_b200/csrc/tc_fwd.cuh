@@ -321,8 +321,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd_tc(PassArgs a, int ntile
     // Philox blocks of a path-step split 9 / 8 / 8 over the column groups: the 9-block
     // share goes to the highest warp ids (gw = 2, which the schedulers issue first), the
     // Y recursion to gw = 1, and the lowest-priority group carries neither
-    const int q = warp & 3, gw = warp >> 2, g = (gw + 1) % kFwdGroups;
-    const bool ywork = gw == 1;
+#ifndef BSDE_FWD_GROT   // experiment builds: other group rotations / Y-work placements
+#define BSDE_FWD_GROT 1
+#endif
+#ifndef BSDE_FWD_YGW
+#define BSDE_FWD_YGW 1
+#endif
+    const int q = warp & 3, gw = warp >> 2, g = (gw + BSDE_FWD_GROT) % kFwdGroups;
+    const bool ywork = gw == BSDE_FWD_YGW;
     const int row = 32 * q + lane;
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     const uint32_t acc = tm + lane_off, hT = tm + L::T_H + lane_off, xT = tm + L::T_X + lane_off;
